@@ -1,0 +1,229 @@
+"""Device-resident primitives over the C-ABI (torch is plumbing only:
+device memory, the current CUDA stream and pinned host buffers).
+
+Every function here launches sm_100a kernels from libsdb200.so; nothing
+computes on the host.
+"""
+
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import SDB_F32, SDB_F64
+
+PRECISIONS = ("fp64", "fp32")
+# Singular-support guard on the Cholesky pivot (_kernels.py:18). FP64 keeps the
+# reference's 1e-12; in FP32 that threshold is below the arithmetic's
+# resolution (unit-norm atoms give pivots accurate to ~1e-7), so the FP32 mode
+# uses 1e-6 ("FP32 divergences").
+GUARD = {"fp64": 1e-12, "fp32": 1e-6}
+MAX_K = 1024
+
+_precision = os.environ.get("SPARSEDICT_B200_PRECISION", "fp64")
+
+
+def set_precision(p: str) -> None:
+    """Select the arithmetic of the GPU path: "fp64" (default; OMP bitwise
+    identical to the reference) or "fp32" (fast mode, tcgen05 3xTF32
+    correlation GEMM, tolerance-based parity)."""
+    global _precision
+    if p not in PRECISIONS:
+        raise ValueError(f"precision must be one of {PRECISIONS}")
+    _precision = p
+
+
+def get_precision(override: str | None = None) -> str:
+    p = override or _precision
+    if p not in PRECISIONS:
+        raise ValueError(f"precision must be one of {PRECISIONS}")
+    return p
+
+
+def sdb_dtype(p: str) -> int:
+    return SDB_F64 if p == "fp64" else SDB_F32
+
+
+def torch_dtype(p: str):
+    return torch.float64 if p == "fp64" else torch.float32
+
+
+_dev_checked = False
+
+
+def device() -> torch.device:
+    """The CUDA device; raises NativeUnavailable without an sm_100 GPU."""
+    global _dev_checked
+    if not _dev_checked:
+        if not torch.cuda.is_available():
+            raise _lib.NativeUnavailable("no CUDA device: the sparsedict-B200 path has no CPU fallback")
+        _lib.load()
+        torch.cuda.init()
+        cc = _lib.load().sdb_device_cc()
+        if cc < 100:
+            raise _lib.NativeUnavailable(f"compute capability {cc / 10:.1f} < 10.0 (sm_100a build)")
+        _dev_checked = True
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def empty(shape, dtype) -> torch.Tensor:
+    return torch.empty(shape, dtype=dtype, device=device())
+
+
+def zeros(shape, dtype) -> torch.Tensor:
+    return torch.zeros(shape, dtype=dtype, device=device())
+
+
+# ---------------------------------------------------------------- ingest
+def h2d_f64(a: np.ndarray) -> torch.Tensor:
+    """Copy a host float64 array (any layout) to the device unchanged."""
+    t = torch.from_numpy(np.ascontiguousarray(a) if not (a.flags.c_contiguous or a.flags.f_contiguous)
+                         else a)
+    return t.to(device(), non_blocking=False)
+
+
+def ingest_signals(Y, prec: str) -> tuple[torch.Tensor, int]:
+    """m x N host (numpy f64, any order) or device tensor -> device N x m
+    signal-major in the working precision. Returns (Ydev, nonfinite_flag)."""
+    dt = sdb_dtype(prec)
+    if isinstance(Y, torch.Tensor) and Y.is_cuda:
+        src = Y.to(torch.float64) if Y.dtype != torch.float64 else Y
+        m, N = src.shape
+        s_row, s_col = src.stride()
+    else:
+        Yh = np.asarray(Y, dtype=np.float64)
+        m, N = Yh.shape
+        if not (Yh.flags.c_contiguous or Yh.flags.f_contiguous):
+            Yh = np.asfortranarray(Yh)
+        src = torch.from_numpy(Yh).to(device())
+        s_row, s_col = (Yh.strides[0] // 8, Yh.strides[1] // 8)
+    out = empty((N, m), torch_dtype(prec))
+    bad = zeros((1,), torch.int32)
+    _lib.call("sdb_ingest", dt, m, N, ptr(src), s_row, s_col, ptr(out), m, ptr(bad), stream())
+    return out, bad
+
+
+def dict_to_device(D: np.ndarray) -> torch.Tensor:
+    """Host m x K f64 dictionary -> device (1, K, m) f64 atom-major."""
+    D = np.asarray(D, dtype=np.float64)
+    return torch.from_numpy(np.ascontiguousarray(D.T)).to(device()).unsqueeze(0)
+
+
+def working_dict(D64: torch.Tensor, prec: str) -> torch.Tensor:
+    if prec == "fp64":
+        return D64
+    out = empty(D64.shape, torch.float32)
+    _lib.call("sdb_cast", SDB_F32, D64.numel(), ptr(D64), ptr(out), stream())
+    return out
+
+
+def gram(D64: torch.Tensor, prec: str) -> torch.Tensor:
+    P, K, m = D64.shape
+    G = empty((P, K, K), torch_dtype(prec))
+    _lib.call("sdb_gram", sdb_dtype(prec), P, m, K, ptr(D64), ptr(G), stream())
+    return G
+
+
+# ---------------------------------------------------------------- coding
+@dataclass
+class DeviceCodes:
+    """OMP results on the device (selection order)."""
+
+    K: int
+    cap: int
+    idx: torch.Tensor      # (N, cap) int32
+    val: torch.Tensor      # (N, cap) working precision
+    counts: torch.Tensor   # (N,) int32
+    status: torch.Tensor   # (N,) int8
+    rnorm: torch.Tensor    # (N,) working precision
+
+    @property
+    def N(self) -> int:
+        return self.counts.shape[0]
+
+
+def shard_offsets(sizes) -> tuple[torch.Tensor, int]:
+    off = np.concatenate([[0], np.cumsum(np.asarray(sizes, dtype=np.int64))]).astype(np.int64)
+    return torch.from_numpy(off).to(device()), int(max(sizes) if len(sizes) else 0)
+
+
+def alpha_chunk_rows(K: int, prec: str) -> int:
+    """Signals per coding chunk so that alpha0 stays <= 4 GiB."""
+    return max(1, (4 << 30) // (K * (8 if prec == "fp64" else 4)))
+
+
+def code(Ydev: torch.Tensor, off: torch.Tensor, max_rows: int, DT: torch.Tensor, G: torch.Tensor,
+         cap: int, eps: float, prec: str, use_tc: bool = True, out: DeviceCodes | None = None
+         ) -> DeviceCodes:
+    """OMP over every row of Ydev; row i uses the dictionary of its shard."""
+    N, m = Ydev.shape
+    P, K, _ = DT.shape
+    dt = sdb_dtype(prec)
+    tdt = torch_dtype(prec)
+    if out is None:
+        out = DeviceCodes(K, cap, empty((N, cap), torch.int32), empty((N, cap), tdt),
+                          empty((N,), torch.int32), empty((N,), torch.int8), empty((N,), tdt))
+    if N == 0:
+        return out
+    alpha = empty((N, K), tdt)
+    _lib.call("sdb_correlate", dt, N, m, K, P, ptr(off), max_rows, ptr(Ydev), m, ptr(DT),
+              ptr(alpha), K, int(use_tc), stream())
+    sb = _lib.load().sdb_omp_scratch_bytes(dt, N, m, cap)
+    scratch = empty((max(sb, 1),), torch.uint8) if sb > 0 else None
+    _lib.call("sdb_omp", dt, N, m, K, P, ptr(off), ptr(alpha), K, ptr(Ydev), m, ptr(DT), ptr(G),
+              cap, float(eps), GUARD[prec], ptr(out.idx), ptr(out.val), ptr(out.counts),
+              ptr(out.status), ptr(out.rnorm), ptr(scratch), int(sb), stream())
+    return out
+
+
+def code_single_dict(Ydev, D64, cap, eps, prec, use_tc=True) -> DeviceCodes:
+    """Code all rows of Ydev against one dictionary (P = 1), chunked."""
+    N = Ydev.shape[0]
+    DT = working_dict(D64, prec)
+    G = gram(D64, prec)
+    K = D64.shape[1]
+    rows = alpha_chunk_rows(K, prec)
+    if N <= rows:
+        off, mx = shard_offsets([N])
+        return code(Ydev, off, mx, DT, G, cap, eps, prec, use_tc)
+    tdt = torch_dtype(prec)
+    res = DeviceCodes(K, cap, empty((N, cap), torch.int32), empty((N, cap), tdt),
+                      empty((N,), torch.int32), empty((N,), torch.int8), empty((N,), tdt))
+    for lo in range(0, N, rows):
+        hi = min(N, lo + rows)
+        off, mx = shard_offsets([hi - lo])
+        view = DeviceCodes(K, cap, res.idx[lo:hi], res.val[lo:hi], res.counts[lo:hi],
+                           res.status[lo:hi], res.rnorm[lo:hi])
+        code(Ydev[lo:hi], off, mx, DT, G, cap, eps, prec, use_tc, out=view)
+    return res
+
+
+def csc(codes: DeviceCodes, prec: str):
+    """Device CSC packing -> (indptr, indices int64, data f64) device tensors."""
+    N = codes.N
+    indptr = empty((N + 1,), torch.int64)
+    ws = empty((max(_lib.load().sdb_csc_workspace_bytes(N), 8),), torch.uint8)
+    _lib.call("sdb_csc_indptr", N, ptr(codes.counts), ptr(indptr), ptr(ws), stream())
+    nnz = int(indptr[N].item()) if N else 0
+    indices = empty((max(nnz, 1),), torch.int64)
+    data = empty((max(nnz, 1),), torch.float64)
+    if N:
+        _lib.call("sdb_csc_fill", sdb_dtype(prec), N, codes.cap, ptr(codes.idx), ptr(codes.val),
+                  ptr(codes.counts), ptr(indptr), ptr(indices), ptr(data), stream())
+    return indptr, indices[:nnz], data[:nnz]
+
+
+def d2h(t: torch.Tensor) -> np.ndarray:
+    return t.detach().to("cpu").numpy()

@@ -1,0 +1,83 @@
+"""ctypes binding of the C-ABI library (include/sparsedict_b200.h).
+
+The CUDA library is the ONLY compute path: there is no CPU fallback. If the
+library is missing or no sm_100 device is present, every compute entry point
+raises ``NativeUnavailable`` loudly.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = PKG / "libsdb200.so"
+
+SDB_F32, SDB_F64 = 0, 1
+
+c_i64 = ctypes.c_int64
+c_int = ctypes.c_int
+c_dbl = ctypes.c_double
+c_vp = ctypes.c_void_p
+
+# name -> (restype, argtypes); mirrors include/sparsedict_b200.h
+SIGNATURES = {
+    "sdb_abi_version": (c_int, []),
+    "sdb_last_error": (ctypes.c_char_p, []),
+    "sdb_device_cc": (c_int, []),
+    "sdb_ingest": (c_int, [c_int, c_i64, c_i64, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp]),
+    "sdb_cast": (c_int, [c_int, c_i64, c_vp, c_vp, c_vp]),
+    "sdb_gram": (c_int, [c_int, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
+    "sdb_correlate": (c_int, [c_int, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp,
+                              c_vp, c_i64, c_int, c_vp]),
+    "sdb_omp_scratch_bytes": (c_i64, [c_int, c_i64, c_i64, c_i64]),
+    "sdb_omp": (c_int, [c_int, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp,
+                        c_vp, c_i64, c_dbl, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64,
+                        c_vp]),
+    "sdb_csc_workspace_bytes": (c_i64, [c_i64]),
+    "sdb_csc_indptr": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "sdb_csc_fill": (c_int, [c_int, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+}
+
+
+class NativeUnavailable(RuntimeError):
+    """The sm_100a CUDA library or device is not available (no fallback)."""
+
+
+class NativeError(RuntimeError):
+    """A C-ABI call returned an error code."""
+
+
+_lib = None
+
+
+def load():
+    """Load (building first if needed) and bind the library."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        if os.environ.get("SDB_NO_BUILD"):
+            raise NativeUnavailable(f"{LIB_PATH} is missing (run python -m paper_1403_4781_b200.build)")
+        from . import build as _build
+        _build.build()
+    lib = ctypes.CDLL(str(LIB_PATH))
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = load().sdb_last_error().decode(errors="replace")
+        raise NativeError(f"{what} failed ({rc}): {msg}")
+
+
+def call(name: str, *args) -> int:
+    rc = getattr(load(), name)(*args)
+    check(rc, name)
+    return rc

@@ -1,0 +1,59 @@
+// Internal (C++) launch interface shared by the .cu translation units.
+// The public C-ABI lives in include/sparsedict_b200.h / sdb_capi.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+namespace sdb {
+
+template <typename T>
+struct OmpArgs {
+    int64_t N;
+    int m, K, cap, P;
+    T eps, guard;
+    const int64_t* shard_off;  // P+1 signal offsets
+    const T* alpha0;           // N x lda
+    int64_t lda;
+    const T* Y;                // N x ldy
+    int64_t ldy;
+    const T* D;                // P x K x m (atom-major)
+    const T* G;                // P x K x K
+    int32_t* idx;              // N x cap
+    T* val;                    // N x cap
+    int32_t* counts;
+    int8_t* status;
+    T* rnorm;
+    unsigned char* gscratch;   // optional per-warp scratch in global memory
+    int64_t gscratch_warps;
+    int64_t warp_bytes;
+};
+
+int gram_f64(const double* D, int P, int64_t m, int64_t K, double* G, cudaStream_t st);
+int gram_f32(const double* D, int P, int64_t m, int64_t K, float* G, cudaStream_t st);
+int correlate_simt_f64(const double* Y, int64_t ldy, const int64_t* off, int64_t max_rows, int P,
+                       const double* D, int64_t m, int64_t K, double* alpha, int64_t lda,
+                       cudaStream_t st);
+int correlate_simt_f32(const float* Y, int64_t ldy, const int64_t* off, int64_t max_rows, int P,
+                       const float* D, int64_t m, int64_t K, float* alpha, int64_t lda,
+                       cudaStream_t st);
+// tcgen05 3xTF32 correlation GEMM (sdb_tc_gemm.cu); returns cudaErrorNotSupported
+// when the shape is outside the kernel's tiling.
+int correlate_tc_f32(const float* Y, int64_t ldy, const int64_t* off, int64_t max_rows, int P,
+                     const float* D, int64_t m, int64_t K, float* alpha, int64_t lda,
+                     cudaStream_t st);
+
+template <typename T>
+int launch_omp(OmpArgs<T> a, cudaStream_t st);
+int64_t omp_warp_bytes_f32(int cap, int m);
+int64_t omp_warp_bytes_f64(int cap, int m);
+
+int64_t scan_workspace_bytes(int64_t N);
+int exclusive_scan_counts(const int32_t* counts, int64_t N, int64_t* indptr, int64_t* ws,
+                          cudaStream_t st);
+template <typename T>
+int pack_csc(int64_t N, int cap, const int32_t* idx, const T* val, const int32_t* counts,
+             const int64_t* indptr, int64_t* out_idx, double* out_val, cudaStream_t st);
+
+}  // namespace sdb

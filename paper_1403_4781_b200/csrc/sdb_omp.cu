@@ -1,0 +1,539 @@
+// Batch-OMP on B200: correlation / Gram products, the warp-per-signal greedy
+// kernel and CSC packing.
+//
+// Reference: /root/reference/pkg/src/sparsedict/_kernels.py:23-173 (Numba
+// kernels) and sparse_coding.py:266-303 (Gram per call, batch loop, packing).
+//
+// Device layouts:
+//   Y      : N x ldy, signal-major (row i = signal i, m contiguous)  [= F-order m x N]
+//   D      : P x K x m, atom-major per shard                          [= F-order m x K]
+//   G      : P x K x K
+//   alpha0 : N x lda   (alpha0[i, j] = <d_j, y_i>, shard of i)
+//   codes  : idx N x cap (int32, selection order), val N x cap, counts, status, rnorm
+#include "sdb_common.cuh"
+#include "sdb_internal.h"
+
+namespace sdb {
+
+// ----------------------------------------------------------------------------
+// Row-dot tile kernel:  C[a, b] = sum_t A[a, t] * B_p[b, t]  (t ascending).
+// Used for the exact FP64 correlation alpha0 = Y D (per shard) and for every
+// Gram matrix G = D^T D (A = B = D_p). In exact mode each output is a
+// sequential sum over t with separately rounded products, matching
+// _kernels.py:23-35 / :54-59 bit for bit.
+// ----------------------------------------------------------------------------
+constexpr int RD_BM = 64, RD_BN = 64, RD_BK = 16;
+
+template <typename TIn, typename TOut>
+__global__ void __launch_bounds__(256)
+k_rowdot(const TIn* __restrict__ A, int64_t lda, const int64_t* __restrict__ a_off,
+         int64_t a_rows_per_shard, const TIn* __restrict__ B, int64_t ldb, int64_t b_stride,
+         int64_t nb, int64_t kdim, TOut* __restrict__ C, int64_t ldc) {
+    using R = Ar<TIn>;
+    __shared__ TIn As[RD_BK][RD_BM + 1];
+    __shared__ TIn Bs[RD_BK][RD_BN + 1];
+    const int p = blockIdx.z;
+    const int64_t a_lo = a_off ? a_off[p] : (int64_t)p * a_rows_per_shard;
+    const int64_t a_hi = a_off ? a_off[p + 1] : a_lo + a_rows_per_shard;
+    const int64_t a0 = a_lo + (int64_t)blockIdx.x * RD_BM;
+    if (a0 >= a_hi) return;
+    const int64_t b0 = (int64_t)blockIdx.y * RD_BN;
+    if (b0 >= nb) return;
+    const TIn* Bp = B + (int64_t)p * b_stride;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    TIn acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = TIn(0);
+
+    for (int64_t k0 = 0; k0 < kdim; k0 += RD_BK) {
+        // cooperative loads: 64 rows x 16 k for each operand (4 per thread)
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+            const int e = threadIdx.x + l * 256;
+            const int row = e >> 4, kk = e & 15;
+            const int64_t ga = a0 + row, gb = b0 + row, gk = k0 + kk;
+            As[kk][row] = (ga < a_hi && gk < kdim) ? A[ga * lda + gk] : TIn(0);
+            Bs[kk][row] = (gb < nb && gk < kdim) ? Bp[gb * ldb + gk] : TIn(0);
+        }
+        __syncthreads();
+        const int kend = (int)((kdim - k0) < RD_BK ? (kdim - k0) : RD_BK);
+        for (int kk = 0; kk < kend; ++kk) {
+            TIn av[4], bv[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) av[i] = As[kk][ty + 16 * i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = R::mac(acc[i][j], av[i], bv[j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int64_t ga = a0 + ty + 16 * i;
+        if (ga >= a_hi) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t gb = b0 + tx + 16 * j;
+            if (gb < nb) C[ga * ldc + gb] = (TOut)acc[i][j];
+        }
+    }
+}
+
+template <typename TIn, typename TOut>
+static int launch_rowdot(const TIn* A, int64_t lda, const int64_t* a_off, int64_t a_rows_max,
+                         int64_t a_rows_per_shard, const TIn* B, int64_t ldb, int64_t b_stride,
+                         int64_t nb, int64_t kdim, TOut* C, int64_t ldc, int P,
+                         cudaStream_t st) {
+    if (a_rows_max <= 0 || nb <= 0 || P <= 0) return 0;
+    dim3 grid((unsigned)((a_rows_max + RD_BM - 1) / RD_BM), (unsigned)((nb + RD_BN - 1) / RD_BN),
+              (unsigned)P);
+    k_rowdot<TIn, TOut><<<grid, 256, 0, st>>>(A, lda, a_off, a_rows_per_shard, B, ldb, b_stride,
+                                              nb, kdim, C, ldc);
+    return (int)cudaGetLastError();
+}
+
+int gram_f64(const double* D, int P, int64_t m, int64_t K, double* G, cudaStream_t st) {
+    return launch_rowdot<double, double>(D, m, nullptr, K, K, D, m, K * m, K, m, G, K, P, st);
+}
+int gram_f32(const double* D, int P, int64_t m, int64_t K, float* G, cudaStream_t st) {
+    return launch_rowdot<double, float>(D, m, nullptr, K, K, D, m, K * m, K, m, G, K, P, st);
+}
+int correlate_simt_f64(const double* Y, int64_t ldy, const int64_t* off, int64_t max_rows, int P,
+                       const double* D, int64_t m, int64_t K, double* alpha, int64_t lda,
+                       cudaStream_t st) {
+    return launch_rowdot<double, double>(Y, ldy, off, max_rows, 0, D, m, K * m, K, m, alpha, lda,
+                                         P, st);
+}
+int correlate_simt_f32(const float* Y, int64_t ldy, const int64_t* off, int64_t max_rows, int P,
+                       const float* D, int64_t m, int64_t K, float* alpha, int64_t lda,
+                       cudaStream_t st) {
+    return launch_rowdot<float, float>(Y, ldy, off, max_rows, 0, D, m, K * m, K, m, alpha, lda, P,
+                                       st);
+}
+
+// ----------------------------------------------------------------------------
+// Greedy OMP, one warp per signal.
+//
+// Lane l owns atoms j = l + 32k (k < KPL): c0 and corr live in registers.
+// Per step (reference _kernels.py:78-154):
+//   corr = c0 - sum_t G[idx_t, :] x_t  (G rows streamed through L2, coalesced)
+//   |.|, support exclusion, warp max, stall test, lowest index in tie window
+//   Cholesky append with the diagonal guard, forward/back substitution,
+//   explicit residual r = y - D_S x and its norm.
+// Exact mode (double) runs the O(n^2) recurrences in the reference's order on
+// every lane (identical values, no divergence); fast mode (float) uses
+// lane-parallel column sweeps when the support fits one warp (cap <= 32).
+// ----------------------------------------------------------------------------
+template <typename T>
+struct WarpScratch {
+    T* L;      // packed lower-triangular Cholesky factor, row t at t(t+1)/2
+    T* tmp;    // forward-substitution vector
+    T* x;      // coefficients (support order)
+    T* y;      // signal
+    T* r;      // residual
+    int* ids;  // support (selection order)
+};
+
+__host__ __device__ inline int64_t align16(int64_t b) { return (b + 15) & ~int64_t(15); }
+
+template <typename T>
+__host__ __device__ inline int64_t omp_warp_bytes(int cap, int m) {
+    int64_t b = align16(sizeof(T) * ((int64_t)cap * (cap + 1) / 2));
+    b += align16(sizeof(T) * cap) * 2;
+    b += align16(sizeof(T) * m) * 2;
+    b += align16(sizeof(int) * cap);
+    return b;
+}
+
+template <typename T>
+__device__ inline WarpScratch<T> carve(unsigned char* base, int cap, int m) {
+    WarpScratch<T> w;
+    unsigned char* p = base;
+    w.L = (T*)p;   p += align16(sizeof(T) * ((int64_t)cap * (cap + 1) / 2));
+    w.tmp = (T*)p; p += align16(sizeof(T) * cap);
+    w.x = (T*)p;   p += align16(sizeof(T) * cap);
+    w.y = (T*)p;   p += align16(sizeof(T) * m);
+    w.r = (T*)p;   p += align16(sizeof(T) * m);
+    w.ids = (int*)p;
+    return w;
+}
+
+template <typename T>
+__device__ __forceinline__ const T* tri_row(const T* L, int t) { return L + (int64_t)t * (t + 1) / 2; }
+template <typename T>
+__device__ __forceinline__ T* tri_row(T* L, int t) { return L + (int64_t)t * (t + 1) / 2; }
+
+template <typename T, int KPL>
+__global__ void __launch_bounds__(256)
+k_omp(OmpArgs<T> a) {
+    using R = Ar<T>;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    const int wpb = blockDim.x >> 5;
+    const int64_t gw = (int64_t)blockIdx.x * wpb + wib;
+    const int64_t nw = (int64_t)gridDim.x * wpb;
+    unsigned char* base = a.gscratch ? a.gscratch + gw * a.warp_bytes : smem + wib * a.warp_bytes;
+    WarpScratch<T> w = carve<T>(base, a.cap, a.m);
+    const int m = a.m, K = a.K, cap = a.cap;
+    const T eps = a.eps;
+
+    for (int64_t i = gw; i < a.N; i += nw) {
+        const int p = shard_of(a.shard_off, a.P, i);
+        const T* __restrict__ Gp = a.G + (int64_t)p * K * K;
+        const T* __restrict__ Dp = a.D + (int64_t)p * K * m;
+        T c0[KPL];
+#pragma unroll
+        for (int k = 0; k < KPL; ++k) {
+            const int j = lane + 32 * k;
+            c0[k] = (j < K) ? a.alpha0[i * a.lda + j] : T(0);
+        }
+        for (int t = lane; t < m; t += 32) w.y[t] = a.Y[i * a.ldy + t];
+        __syncwarp();
+        T ysq;
+        if constexpr (R::kExact) {
+            ysq = T(0);
+            for (int t = 0; t < m; ++t) ysq = R::mac(ysq, w.y[t], w.y[t]);
+        } else {
+            T part = T(0);
+            for (int t = lane; t < m; t += 32) part = fmaf(w.y[t], w.y[t], part);
+            ysq = warp_sum(part);
+        }
+        T rnorm = R::sqrt_(ysq);
+        int n = 0;
+        int status = 0;
+        if (!(rnorm <= eps || rnorm == T(0))) {
+            uint32_t selbits = 0;  // bit k: atom lane+32k is in the support
+            for (int step = 0; step < cap; ++step) {
+                // ---- correlations of the current residual (_kernels.py:81-96)
+                T corr[KPL];
+#pragma unroll
+                for (int k = 0; k < KPL; ++k) corr[k] = c0[k];
+                for (int t = 0; t < n; ++t) {
+                    const T coef = w.x[t];
+                    const T* __restrict__ g = Gp + (int64_t)w.ids[t] * K;
+#pragma unroll
+                    for (int k = 0; k < KPL; ++k) {
+                        const int j = lane + 32 * k;
+                        if (j < K) corr[k] = R::msub(corr[k], __ldg(g + j), coef);
+                    }
+                }
+                T lmax = T(-1);
+#pragma unroll
+                for (int k = 0; k < KPL; ++k) {
+                    const int j = lane + 32 * k;
+                    const bool ok = (j < K) && !((selbits >> k) & 1u);
+                    const T av = ok ? fabs(corr[k]) : T(-1);
+                    corr[k] = av;
+                    lmax = fmax(lmax, av);
+                }
+                const T cmax = warp_max(lmax);
+                if (cmax <= R::mul(T(1e-13), rnorm)) {  // _kernels.py:97-100
+                    status = 3;
+                    break;
+                }
+                const T thresh = R::sub(cmax, R::mul(T(1e-12), cmax));
+                int cand = 0x7fffffff;
+#pragma unroll
+                for (int k = KPL - 1; k >= 0; --k)
+                    if (corr[k] >= thresh) cand = lane + 32 * k;  // lowest k wins
+                const int best = warp_min_int(cand);
+
+                // ---- Cholesky append (_kernels.py:109-127)
+                T* Lrow = tri_row(w.L, n);
+                T dsq = __ldg(Gp + (int64_t)best * K + best);
+                if (R::kExact || n > 32) {
+                    for (int t = 0; t < n; ++t) {
+                        T acc = __ldg(Gp + (int64_t)w.ids[t] * K + best);
+                        const T* Lt = tri_row(w.L, t);
+                        for (int u = 0; u < t; ++u) acc = R::msub(acc, Lt[u], Lrow[u]);
+                        const T wv = R::div(acc, Lt[t]);
+                        Lrow[t] = wv;  // every lane writes the same value
+                        dsq = R::msub(dsq, wv, wv);
+                    }
+                } else {
+                    // lane-parallel column sweep: lane t solves for w_t
+                    T acc = (lane < n) ? __ldg(Gp + (int64_t)w.ids[lane] * K + best) : T(0);
+                    T mine = T(0);
+                    for (int u = 0; u < n; ++u) {
+                        const T wu = R::div(__shfl_sync(SDB_FULL, acc, u), tri_row(w.L, u)[u]);
+                        if (lane == u) mine = wu;
+                        if (lane > u && lane < n) acc = R::msub(acc, tri_row(w.L, lane)[u], wu);
+                    }
+                    if (lane < n) Lrow[lane] = mine;
+                    dsq = R::sub(dsq, warp_sum(lane < n ? mine * mine : T(0)));
+                }
+                if (dsq <= a.guard) {  // numerically singular support Gram
+                    status = 2;
+                    break;
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    Lrow[n] = R::sqrt_(dsq);
+                    w.ids[n] = best;
+                }
+                if (lane == (best & 31)) selbits |= 1u << (best >> 5);
+                // c0[best] from its owner lane (static register selection)
+                T cb = T(0);
+#pragma unroll
+                for (int k = 0; k < KPL; ++k)
+                    if (k == (best >> 5)) cb = c0[k];
+                cb = __shfl_sync(SDB_FULL, cb, best & 31);
+                n += 1;
+                __syncwarp();
+
+                // ---- L L^T x = c0[S] (_kernels.py:129-139); tmp[0..n-2]
+                // are unchanged from the previous step, only tmp[n-1] is new.
+                {
+                    const T* Ln = tri_row(w.L, n - 1);
+                    T acc = cb;
+                    if (R::kExact || n > 33) {
+                        for (int u = 0; u < n - 1; ++u) acc = R::msub(acc, Ln[u], w.tmp[u]);
+                    } else {
+                        acc -= warp_sum(lane < n - 1 ? Ln[lane] * w.tmp[lane] : T(0));
+                    }
+                    const T tv = R::div(acc, Ln[n - 1]);
+                    __syncwarp();
+                    if (lane == 0) w.tmp[n - 1] = tv;
+                }
+                __syncwarp();
+                if (R::kExact || n > 32) {
+                    for (int t = n - 1; t >= 0; --t) {
+                        T acc = w.tmp[t];
+                        for (int u = t + 1; u < n; ++u) acc = R::msub(acc, tri_row(w.L, u)[t], w.x[u]);
+                        const T xv = R::div(acc, tri_row(w.L, t)[t]);
+                        __syncwarp();
+                        if (lane == 0) w.x[t] = xv;
+                        __syncwarp();
+                    }
+                } else {
+                    T acc = (lane < n) ? w.tmp[lane] : T(0);
+                    T mine = T(0);
+                    for (int u = n - 1; u >= 0; --u) {
+                        const T xu = R::div(__shfl_sync(SDB_FULL, acc, u), tri_row(w.L, u)[u]);
+                        if (lane == u) mine = xu;
+                        if (lane < u) acc = R::msub(acc, tri_row(w.L, u)[lane], xu);
+                    }
+                    __syncwarp();
+                    if (lane < n) w.x[lane] = mine;
+                    __syncwarp();
+                }
+
+                // ---- explicit residual (_kernels.py:141-154)
+                T part = T(0);
+                for (int r = lane; r < m; r += 32) {
+                    T rv = w.y[r];
+                    for (int t = 0; t < n; ++t)
+                        rv = R::msub(rv, __ldg(Dp + (int64_t)w.ids[t] * m + r), w.x[t]);
+                    if constexpr (R::kExact) w.r[r] = rv;
+                    else part = fmaf(rv, rv, part);
+                }
+                T rsq;
+                if constexpr (R::kExact) {
+                    __syncwarp();
+                    rsq = T(0);
+                    for (int r = 0; r < m; ++r) rsq = R::mac(rsq, w.r[r], w.r[r]);
+                } else {
+                    rsq = warp_sum(part);
+                }
+                rnorm = R::sqrt_(rsq);
+                __syncwarp();
+                if (rnorm <= eps) break;
+            }
+        }
+        // ---- outputs (selection order; entries >= n zeroed like the reference)
+        __syncwarp();
+        for (int t = lane; t < cap; t += 32) {
+            a.idx[i * cap + t] = (t < n) ? w.ids[t] : 0;
+            a.val[i * cap + t] = (t < n) ? w.x[t] : T(0);
+        }
+        if (lane == 0) {
+            a.counts[i] = n;
+            a.status[i] = (int8_t)status;
+            a.rnorm[i] = rnorm;
+        }
+        __syncwarp();
+    }
+}
+
+template <typename T>
+int64_t omp_scratch_bytes(int64_t N, int cap, int m, int* use_global) {
+    const int64_t wb = omp_warp_bytes<T>(cap, m);
+    *use_global = (wb * 8 > 200 * 1024) ? 1 : 0;
+    if (!*use_global) return 0;
+    const int64_t warps = std::min<int64_t>((N + 0), (int64_t)148 * 32);
+    return wb * std::max<int64_t>(warps, 1);
+}
+
+template <typename T, int KPL>
+static int launch_omp_k(const OmpArgs<T>& a, int blocks, int smem, cudaStream_t st) {
+    auto fn = k_omp<T, KPL>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return (int)e;
+    }
+    fn<<<blocks, 256, smem, st>>>(a);
+    return (int)cudaGetLastError();
+}
+
+template <typename T>
+int launch_omp(OmpArgs<T> a, cudaStream_t st) {
+    if (a.N <= 0) return 0;
+    const int64_t wb = omp_warp_bytes<T>(a.cap, a.m);
+    a.warp_bytes = wb;
+    int smem = 0;
+    int64_t warps_needed = a.N;
+    int64_t blocks;
+    if (a.gscratch) {
+        // global scratch holds a.gscratch_warps warps
+        blocks = std::max<int64_t>(1, std::min<int64_t>(a.gscratch_warps / 8, (warps_needed + 7) / 8));
+    } else {
+        smem = (int)(wb * 8);
+        blocks = std::min<int64_t>((warps_needed + 7) / 8, (int64_t)148 * 64);
+    }
+    const int kpl = (a.K + 31) / 32;
+    if (kpl <= 1) return launch_omp_k<T, 1>(a, (int)blocks, smem, st);
+    if (kpl <= 2) return launch_omp_k<T, 2>(a, (int)blocks, smem, st);
+    if (kpl <= 4) return launch_omp_k<T, 4>(a, (int)blocks, smem, st);
+    if (kpl <= 8) return launch_omp_k<T, 8>(a, (int)blocks, smem, st);
+    if (kpl <= 16) return launch_omp_k<T, 16>(a, (int)blocks, smem, st);
+    if (kpl <= 32) return launch_omp_k<T, 32>(a, (int)blocks, smem, st);
+    return (int)cudaErrorInvalidValue;  // K > 1024: rejected at the API boundary
+}
+
+template int launch_omp<float>(OmpArgs<float>, cudaStream_t);
+template int launch_omp<double>(OmpArgs<double>, cudaStream_t);
+int64_t omp_warp_bytes_f32(int cap, int m) { return omp_warp_bytes<float>(cap, m); }
+int64_t omp_warp_bytes_f64(int cap, int m) { return omp_warp_bytes<double>(cap, m); }
+
+// ----------------------------------------------------------------------------
+// CSC packing (sparse_coding.py:294-303): indptr = exclusive scan of counts,
+// then each column's entries in ascending atom index.
+// ----------------------------------------------------------------------------
+constexpr int SCAN_TPB = 256, SCAN_IPT = 8, SCAN_TILE = SCAN_TPB * SCAN_IPT;
+
+__device__ __forceinline__ int64_t block_exclusive_scan(int64_t v, int64_t* sh, int64_t* total) {
+    // warp inclusive scan
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int64_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int64_t y = __shfl_up_sync(SDB_FULL, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) sh[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        int64_t s = (lane < (int)(blockDim.x >> 5)) ? sh[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int64_t y = __shfl_up_sync(SDB_FULL, s, o);
+            if (lane >= o) s += y;
+        }
+        sh[lane] = s;  // inclusive warp totals
+    }
+    __syncthreads();
+    const int64_t wpre = wid ? sh[wid - 1] : 0;
+    *total = sh[(blockDim.x >> 5) - 1];
+    __syncthreads();
+    return wpre + x - v;
+}
+
+__global__ void __launch_bounds__(SCAN_TPB)
+k_scan_tiles(const int32_t* __restrict__ counts, int64_t N, int64_t* __restrict__ out,
+             int64_t* __restrict__ tile_sums) {
+    __shared__ int64_t sh[32];
+    const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_IPT;
+    int64_t loc[SCAN_IPT];
+    int64_t s = 0;
+#pragma unroll
+    for (int q = 0; q < SCAN_IPT; ++q) {
+        const int64_t i = base + q;
+        loc[q] = s;
+        s += (i < N) ? counts[i] : 0;
+    }
+    int64_t total;
+    const int64_t pre = block_exclusive_scan(s, sh, &total);
+#pragma unroll
+    for (int q = 0; q < SCAN_IPT; ++q) {
+        const int64_t i = base + q;
+        if (i < N) out[i] = pre + loc[q];
+    }
+    if (threadIdx.x == 0) tile_sums[blockIdx.x] = total;
+}
+
+// one block: exclusive scan of the tile sums in chunks with a running carry
+__global__ void __launch_bounds__(SCAN_TPB)
+k_scan_sums(int64_t* __restrict__ tile_sums, int64_t ntiles, int64_t* __restrict__ grand) {
+    __shared__ int64_t sh[32];
+    int64_t carry = 0;
+    for (int64_t c0 = 0; c0 < ntiles; c0 += SCAN_TPB) {
+        const int64_t i = c0 + threadIdx.x;
+        const int64_t v = (i < ntiles) ? tile_sums[i] : 0;
+        int64_t total;
+        const int64_t pre = block_exclusive_scan(v, sh, &total);
+        if (i < ntiles) tile_sums[i] = carry + pre;
+        carry += total;
+    }
+    if (threadIdx.x == 0) *grand = carry;
+}
+
+__global__ void k_scan_add(int64_t* __restrict__ out, int64_t N, const int64_t* __restrict__ tile_sums) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < N) out[i] += tile_sums[i / SCAN_TILE];
+}
+
+int64_t scan_workspace_bytes(int64_t N) { return sizeof(int64_t) * ((N + SCAN_TILE - 1) / SCAN_TILE + 1); }
+
+// indptr[0..N] (N+1 entries): indptr[0] = 0, indptr[i+1] = sum_{u<=i} counts[u]
+int exclusive_scan_counts(const int32_t* counts, int64_t N, int64_t* indptr, int64_t* ws,
+                          cudaStream_t st) {
+    if (N <= 0) {
+        cudaMemsetAsync(indptr, 0, sizeof(int64_t), st);
+        return (int)cudaGetLastError();
+    }
+    const int64_t ntiles = (N + SCAN_TILE - 1) / SCAN_TILE;
+    k_scan_tiles<<<(unsigned)ntiles, SCAN_TPB, 0, st>>>(counts, N, indptr, ws);
+    k_scan_sums<<<1, SCAN_TPB, 0, st>>>(ws, ntiles, indptr + N);
+    k_scan_add<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(indptr, N, ws);
+    return (int)cudaGetLastError();
+}
+
+template <typename T>
+__global__ void k_pack(int64_t N, int cap, const int32_t* __restrict__ idx, const T* __restrict__ val,
+                       const int32_t* __restrict__ counts, const int64_t* __restrict__ indptr,
+                       int64_t* __restrict__ out_idx, double* __restrict__ out_val) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const int n = counts[i];
+    const int32_t* ii = idx + i * cap;
+    const T* vv = val + i * cap;
+    const int64_t b = indptr[i];
+    for (int t = 0; t < n; ++t) {
+        const int32_t me = ii[t];
+        int rank = 0;
+        for (int u = 0; u < n; ++u) rank += (ii[u] < me);
+        out_idx[b + rank] = me;
+        out_val[b + rank] = (double)vv[t];
+    }
+}
+
+template <typename T>
+int pack_csc(int64_t N, int cap, const int32_t* idx, const T* val, const int32_t* counts,
+             const int64_t* indptr, int64_t* out_idx, double* out_val, cudaStream_t st) {
+    if (N <= 0) return 0;
+    k_pack<T><<<(unsigned)((N + 255) / 256), 256, 0, st>>>(N, cap, idx, val, counts, indptr, out_idx,
+                                                           out_val);
+    return (int)cudaGetLastError();
+}
+template int pack_csc<float>(int64_t, int, const int32_t*, const float*, const int32_t*,
+                             const int64_t*, int64_t*, double*, cudaStream_t);
+template int pack_csc<double>(int64_t, int, const int32_t*, const double*, const int32_t*,
+                              const int64_t*, int64_t*, double*, cudaStream_t);
+
+}  // namespace sdb

@@ -1,0 +1,84 @@
+"""GPU parity of the OMP path (C-ABI via the Python boundary) against the
+reference's golden vectors and the oracle.
+
+FP64 ("exact") mode: bitwise identical selection order, coefficients,
+statuses and residual norms. FP32 ("fast") mode: north-star tolerances —
+identical supports on >= 99.9% of signals, codes relative Frobenius error
+<= 1e-4.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import case, golden_cases, load_golden
+
+pytestmark = pytest.mark.gpu
+
+OMP = load_golden("omp_golden.npz")
+
+
+def _run(c, prec):
+    import paper_1403_4781_b200 as sdb
+    from paper_1403_4781_b200 import _engine as E
+    cap, eps = int(c["cap"]), float(c["eps"])
+    Ydev, bad = E.ingest_signals(c["Y"], prec)
+    D64 = E.dict_to_device(c["D"])
+    codes = E.code_single_dict(Ydev, D64, cap, eps, prec)
+    return codes
+
+
+@pytest.mark.parametrize("name", golden_cases(OMP))
+def test_omp_fp64_bitwise(name):
+    from paper_1403_4781_b200 import _engine as E
+    c = case(OMP, name)
+    if c["Y"].shape[1] == 0:
+        pytest.skip("empty batch handled at the API boundary")
+    codes = _run(c, "fp64")
+    counts = E.d2h(codes.counts).astype(np.int64)
+    assert np.array_equal(counts, c["counts"])
+    assert np.array_equal(E.d2h(codes.status).astype(np.int64), c["status"])
+    assert np.array_equal(E.d2h(codes.idx).astype(np.int64), c["idx"])
+    assert np.array_equal(E.d2h(codes.val), c["val"])
+    assert np.array_equal(E.d2h(codes.rnorm), c["rnorm"])
+
+
+@pytest.mark.parametrize("name", golden_cases(OMP))
+def test_omp_batch_api_fp64_matches_reference_csc(name):
+    import paper_1403_4781_b200 as sdb
+    c = case(OMP, name)
+    cap, eps = int(c["cap"]), float(c["eps"])
+    if eps == 0.0:
+        X = sdb.omp_batch(c["Y"], c["D"], s=cap, precision="fp64")
+    else:
+        X = sdb.omp_batch(c["Y"], c["D"], eps=eps, s_max=cap, precision="fp64")
+    assert np.array_equal(X.indptr, c["indptr"])
+    assert np.array_equal(X.indices, c["indices"])
+    assert np.array_equal(X.data, c["data"])
+
+
+def _fp32_inputs(c):
+    # both sides see the same FP32-representable values
+    Y = c["Y"].astype(np.float32).astype(np.float64)
+    D = c["D"].astype(np.float32).astype(np.float64)
+    D = D / np.linalg.norm(D, axis=0)
+    return Y, D
+
+
+@pytest.mark.parametrize("name", [n for n in golden_cases(OMP)
+                                  if n.startswith(("fixed", "eps"))])
+def test_omp_fp32_tolerance(name):
+    import paper_1403_4781_b200 as sdb
+    from oracle import oracle as O
+    c = case(OMP, name)
+    Y, D = _fp32_inputs(c)
+    cap, eps = int(c["cap"]), float(c["eps"])
+    kw = dict(s=cap) if eps == 0.0 else dict(eps=eps, s_max=cap)
+    X = sdb.omp_batch(Y, D, precision="fp32", **kw)
+    Xr, _ = O.omp_codes(Y, D, **kw)
+    ref = O.csc_matrix(Xr).toarray()
+    got = X.to_dense()
+    same = np.mean([np.array_equal(np.flatnonzero(ref[:, i]), np.flatnonzero(got[:, i]))
+                    for i in range(ref.shape[1])])
+    assert same >= 0.999
+    rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    assert rel <= 1e-4
