@@ -93,6 +93,101 @@ int sdb_csc_fill(int dtype, int64_t N, int64_t cap, const int32_t *idx, const vo
                  const int32_t *counts, const int64_t *indptr, int64_t *indices, double *data,
                  void *stream);
 
+
+/* MOD update for every shard at once: dictionary_update.mod_update
+ * (dictionary_update.py:72-114). Codes are counting-sorted into per-atom
+ * buckets (deterministic), A = X X^T and B = (Y X^T)^T are FP64 sequential
+ * bucket sums, A Z = B is solved by a masked FP64 blocked Cholesky (unused
+ * atoms -> identity rows, numerically dependent pivots -> atom dropped), then
+ * residual_fro = ||Y - Z^T X||_F (before normalisation), dead atoms
+ * (usage 0 or norm <= 1e-12 max(maxnorm,1)) restored from D_prev and every
+ * column normalised. Shards with no nonzero code return D_prev unchanged.
+ * Outputs: D_out (P,K,m) f64, scales (P,K) raw column norms, usage (P,K),
+ * dead (P,K), resid_fro (P), rank (P), deficient (P, dependent pivots). */
+int64_t sdb_mod_workspace_bytes(int64_t P, int64_t N, int64_t m, int64_t K, int64_t cap);
+int sdb_mod_update(int dtype, int64_t P, int64_t N, int64_t m, int64_t K, int64_t cap,
+                   const int64_t *shard_off, const void *Y, int64_t ldy, const int32_t *idx,
+                   const void *val, const int32_t *counts, const double *D_prev, double *D_out,
+                   double *scales, int32_t *usage, int8_t *dead, double *resid_fro, int32_t *rank,
+                   int32_t *deficient, double rank_rcond, void *ws, int64_t ws_bytes, void *stream);
+
+/* replace_degenerate_atoms (dictionary_update.py:117-177) per shard, in place
+ * on D (P,K,m) f64: degenerate = usage 0 | norm <= 1e-12 | higher index of a
+ * twin pair |<dn_i,dn_j>| > 0.999 (pairs in row-major order, the lower index
+ * kept unless itself degenerate); each target (ascending) takes the next data
+ * column by descending ||y - D x|| (ties to the lower column), zero columns
+ * skipped. flags (P,K): 0 kept, 1 replaced, 2 unreplaced. ntarget (P). */
+int64_t sdb_replace_workspace_bytes(int64_t P, int64_t N, int64_t m, int64_t K);
+int sdb_replace_degenerate(int dtype, int64_t P, int64_t N, int64_t m, int64_t K, int64_t cap,
+                           const int64_t *shard_off, const void *Y, int64_t ldy,
+                           const int32_t *idx, const void *val, const int32_t *counts,
+                           const int32_t *usage, double *D, int8_t *flags, int32_t *ntarget,
+                           void *ws, int64_t ws_bytes, void *stream);
+
+/* usage (P,K) int32 = atom histogram of the codes per shard
+ * (SparseCodeMatrix.row_usage, sparse_coding.py:122-124). */
+int sdb_code_usage(int64_t P, int64_t N, int64_t K, int64_t cap, const int64_t *shard_off,
+                   const int32_t *idx, const int32_t *counts, int32_t *usage, void *stream);
+
+/* rsq[i] = ||y_i - D_p x_i||^2 (FP64), ysq[i] = ||y_i||^2 (ysq may be NULL):
+ * the residual of metrics.mse_db (metrics.py:30-44) and of
+ * dictionary_update.py:103,159. */
+int sdb_residual_sq(int dtype, int64_t N, int64_t m, int64_t K, int64_t cap, int64_t P,
+                    const int64_t *shard_off, const void *Y, int64_t ldy, const int32_t *idx,
+                    const void *val, const int32_t *counts, const double *D, double *rsq,
+                    double *ysq, void *stream);
+
+/* out[p] = sum (or sqrt of the sum) of v over shard p, fixed reduction order. */
+int sdb_shard_sum(int64_t P, const int64_t *shard_off, const double *v, double *out, int do_sqrt,
+                  void *stream);
+
+/* out[i] = sum_t val[i,t]^2 (per-signal code energy; ||X_t||_F^2 after a
+ * shard sum — the merge weights of trainer.py:250). */
+int sdb_code_energy(int dtype, int64_t N, int64_t cap, const void *val, const int32_t *counts,
+                    double *out, void *stream);
+
+/* first-columns init (trainer.py:145-148): D[p][a] = y_{off[p]+a} / ||.||,
+ * zero_flag[p*K+a] = 1 for zero columns (host fills them from the seeded RNG). */
+int sdb_first_columns(int dtype, int64_t P, int64_t K, int64_t m, const int64_t *shard_off,
+                      const void *Y, int64_t ldy, double *D, int32_t *zero_flag, void *stream);
+
+/* merge dataset (trainer.py:248-256): out[r] = w[r / group] * D[r], rows of m. */
+int sdb_scale_rows(int dtype, int64_t rows, int64_t group, int64_t m, const double *D,
+                   const double *w, void *out, void *stream);
+
+/* out[r] = in[perm[r]] (rows of m values): split_dataset's column gather
+ * (trainer.py:220-223) into shard-contiguous order. */
+int sdb_gather_rows(int dtype, int64_t rows, int64_t m, const void *in, int64_t ldi,
+                    const int64_t *perm, void *out, int64_t ldo, void *stream);
+
+/* SparseCodeMatrix (CSC, sparse_coding.py:76-96) -> code rows (idx N x cap,
+ * val, counts) for the MOD / residual kernels. cap >= max column nnz. */
+int sdb_csc_to_codes(int dtype, int64_t N, int64_t cap, const int64_t *indptr,
+                     const int64_t *indices, const double *data, int32_t *idx, void *val,
+                     int32_t *counts, void *stream);
+
+/* normalize_columns (dictionary_update.py:56-69) on atom-major rows of m:
+ * out = row / ||row|| (zero rows untouched), scales = norms (may be NULL). */
+int sdb_normalize(int64_t rows, int64_t m, const double *in, double *out, double *scales,
+                  void *stream);
+
+/* extract_patches (denoising.py:118-135): img H x W f64 row-major -> patches
+ * (R*C) x p^2 signal-major in dtype, R = (H-p)/s+1, C = (W-p)/s+1. */
+int sdb_extract_patches(int dtype, const double *img, int64_t H, int64_t W, int64_t p, int64_t s,
+                        void *out, void *stream);
+
+/* denoise_image tail (denoising.py:236-239 + :138-163): overlap-average the
+ * patch estimates D x_k (computed on the fly from the codes), clip to
+ * [lo, hi]. D is (K, p^2) f64 atom-major. */
+int sdb_reconstruct(int dtype, int64_t H, int64_t W, int64_t p, int64_t s, const double *D,
+                    int64_t cap, const int32_t *idx, const void *val, const int32_t *counts,
+                    double lo, double hi, double *out, void *stream);
+
+/* reconstruct_from_patches (denoising.py:138-163) on explicit estimates
+ * P ((R*C) x p^2, signal-major f64). */
+int sdb_reconstruct_dense(int64_t H, int64_t W, int64_t p, int64_t s, const double *P, double *out,
+                          void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -227,3 +227,165 @@ def csc(codes: DeviceCodes, prec: str):
 
 def d2h(t: torch.Tensor) -> np.ndarray:
     return t.detach().to("cpu").numpy()
+
+
+# ---------------------------------------------------------------- MOD layer
+RANK_RCOND = 1e-10   # dictionary_update.py:27 (used as the relative pivot tolerance)
+
+
+@dataclass
+class ShardSet:
+    """Signals on the device, shard-contiguous: rows off[p]..off[p+1] of Y."""
+
+    Y: torch.Tensor        # (N, m) working precision
+    off: torch.Tensor      # (P+1,) int64 device
+    sizes: list            # host copy of the shard sizes
+    prec: str
+
+    @property
+    def P(self) -> int:
+        return len(self.sizes)
+
+    @property
+    def N(self) -> int:
+        return self.Y.shape[0]
+
+    @property
+    def m(self) -> int:
+        return self.Y.shape[1]
+
+    @property
+    def max_rows(self) -> int:
+        return int(max(self.sizes)) if self.sizes else 0
+
+    @classmethod
+    def single(cls, Y: torch.Tensor, prec: str) -> "ShardSet":
+        off, _ = shard_offsets([Y.shape[0]])
+        return cls(Y, off, [Y.shape[0]], prec)
+
+
+@dataclass
+class ModResult:
+    D: torch.Tensor          # (P, K, m) f64, normalised
+    scales: torch.Tensor     # (P, K) raw column norms
+    usage: torch.Tensor      # (P, K) int32
+    dead: torch.Tensor       # (P, K) int8
+    resid: torch.Tensor      # (P,) f64
+    rank: torch.Tensor       # (P,) int32
+    deficient: torch.Tensor  # (P,) int32
+
+
+def mod_update(S: ShardSet, codes: DeviceCodes, D64: torch.Tensor) -> ModResult:
+    P, K, m = D64.shape
+    dt = sdb_dtype(S.prec)
+    r = ModResult(empty((P, K, m), torch.float64), empty((P, K), torch.float64),
+                  empty((P, K), torch.int32), empty((P, K), torch.int8),
+                  empty((P,), torch.float64), empty((P,), torch.int32), empty((P,), torch.int32))
+    wsb = _lib.load().sdb_mod_workspace_bytes(P, S.N, m, K, codes.cap)
+    ws = empty((wsb,), torch.uint8)
+    _lib.call("sdb_mod_update", dt, P, S.N, m, K, codes.cap, ptr(S.off), ptr(S.Y), m,
+              ptr(codes.idx), ptr(codes.val), ptr(codes.counts), ptr(D64), ptr(r.D),
+              ptr(r.scales), ptr(r.usage), ptr(r.dead), ptr(r.resid), ptr(r.rank),
+              ptr(r.deficient), RANK_RCOND, ptr(ws), wsb, stream())
+    return r
+
+
+def replace_degenerate(S: ShardSet, codes: DeviceCodes, D64: torch.Tensor, usage: torch.Tensor):
+    """In place on D64; returns (flags (P,K) int8, ntarget (P,) int32)."""
+    P, K, m = D64.shape
+    flags = empty((P, K), torch.int8)
+    ntarget = empty((P,), torch.int32)
+    wsb = _lib.load().sdb_replace_workspace_bytes(P, S.N, m, K)
+    ws = empty((wsb,), torch.uint8)
+    _lib.call("sdb_replace_degenerate", sdb_dtype(S.prec), P, S.N, m, K, codes.cap, ptr(S.off),
+              ptr(S.Y), m, ptr(codes.idx), ptr(codes.val), ptr(codes.counts), ptr(usage),
+              ptr(D64), ptr(flags), ptr(ntarget), ptr(ws), wsb, stream())
+    return flags, ntarget
+
+
+def code_usage(S: ShardSet, codes: DeviceCodes) -> torch.Tensor:
+    u = empty((S.P, codes.K), torch.int32)
+    _lib.call("sdb_code_usage", S.P, S.N, codes.K, codes.cap, ptr(S.off), ptr(codes.idx),
+              ptr(codes.counts), ptr(u), stream())
+    return u
+
+
+def residual_sq(S: ShardSet, codes: DeviceCodes, D64: torch.Tensor, want_ysq=False):
+    P, K, m = D64.shape
+    rsq = empty((max(S.N, 1),), torch.float64)
+    ysq = empty((max(S.N, 1),), torch.float64) if want_ysq else None
+    if S.N:
+        _lib.call("sdb_residual_sq", sdb_dtype(S.prec), S.N, m, K, codes.cap, P, ptr(S.off),
+                  ptr(S.Y), m, ptr(codes.idx), ptr(codes.val), ptr(codes.counts), ptr(D64),
+                  ptr(rsq), ptr(ysq), stream())
+    return rsq, ysq
+
+
+def shard_sum(S: ShardSet, v: torch.Tensor, do_sqrt: bool) -> torch.Tensor:
+    out = empty((S.P,), torch.float64)
+    _lib.call("sdb_shard_sum", S.P, ptr(S.off), ptr(v), ptr(out), int(do_sqrt), stream())
+    return out
+
+
+def code_energy(S: ShardSet, codes: DeviceCodes) -> torch.Tensor:
+    """||X_p||_F per shard (trainer.py:250)."""
+    e = empty((max(S.N, 1),), torch.float64)
+    if S.N:
+        _lib.call("sdb_code_energy", sdb_dtype(S.prec), S.N, codes.cap, ptr(codes.val),
+                  ptr(codes.counts), ptr(e), stream())
+    return shard_sum(S, e, True)
+
+
+def codes_from_csc(indptr, indices, data, K: int, prec: str) -> DeviceCodes:
+    N = indptr.size - 1
+    counts = np.diff(indptr)
+    cap = max(1, int(counts.max()) if N else 1)
+    dip = torch.from_numpy(np.ascontiguousarray(indptr, dtype=np.int64)).to(device())
+    dii = torch.from_numpy(np.ascontiguousarray(indices, dtype=np.int64)).to(device()) \
+        if indices.size else zeros((1,), torch.int64)
+    dd = torch.from_numpy(np.ascontiguousarray(data, dtype=np.float64)).to(device()) \
+        if data.size else zeros((1,), torch.float64)
+    tdt = torch_dtype(prec)
+    c = DeviceCodes(K, cap, empty((max(N, 1), cap), torch.int32), empty((max(N, 1), cap), tdt),
+                    empty((max(N, 1),), torch.int32), zeros((max(N, 1),), torch.int8),
+                    zeros((max(N, 1),), tdt))
+    if N:
+        _lib.call("sdb_csc_to_codes", sdb_dtype(prec), N, cap, ptr(dip), ptr(dii), ptr(dd),
+                  ptr(c.idx), ptr(c.val), ptr(c.counts), stream())
+    c.idx, c.val, c.counts, c.status, c.rnorm = (c.idx[:N], c.val[:N], c.counts[:N],
+                                                 c.status[:N], c.rnorm[:N])
+    return c
+
+
+def normalize_rows(D64: torch.Tensor):
+    """normalize_columns on atom-major rows (any leading shape)."""
+    m = D64.shape[-1]
+    rows = D64.numel() // m
+    out = empty(D64.shape, torch.float64)
+    sc = empty(D64.shape[:-1], torch.float64)
+    _lib.call("sdb_normalize", rows, m, ptr(D64), ptr(out), ptr(sc), stream())
+    return out, sc
+
+
+def gather_rows(Y: torch.Tensor, perm: torch.Tensor, prec: str) -> torch.Tensor:
+    rows, m = perm.shape[0], Y.shape[1]
+    out = empty((rows, m), Y.dtype)
+    _lib.call("sdb_gather_rows", sdb_dtype(prec), rows, m, ptr(Y), Y.stride(0), ptr(perm),
+              ptr(out), m, stream())
+    return out
+
+
+def first_columns(S: ShardSet, K: int):
+    D = empty((S.P, K, S.m), torch.float64)
+    zf = empty((S.P, K), torch.int32)
+    _lib.call("sdb_first_columns", sdb_dtype(S.prec), S.P, K, S.m, ptr(S.off), ptr(S.Y), S.m,
+              ptr(D), ptr(zf), stream())
+    return D, zf
+
+
+def scale_rows(D64: torch.Tensor, w: torch.Tensor, group: int, prec: str) -> torch.Tensor:
+    rows, m = D64.shape[0] * D64.shape[1], D64.shape[2]
+    out = empty((rows, m), torch_dtype(prec))
+    _lib.call("sdb_scale_rows", sdb_dtype(prec), rows, group, m, ptr(D64), ptr(w), ptr(out),
+              stream())
+    return out

@@ -38,6 +38,27 @@ SIGNATURES = {
     "sdb_csc_workspace_bytes": (c_i64, [c_i64]),
     "sdb_csc_indptr": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp]),
     "sdb_csc_fill": (c_int, [c_int, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "sdb_mod_workspace_bytes": (c_i64, [c_i64, c_i64, c_i64, c_i64, c_i64]),
+    "sdb_mod_update": (c_int, [c_int, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp,
+                               c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_dbl,
+                               c_vp, c_i64, c_vp]),
+    "sdb_replace_workspace_bytes": (c_i64, [c_i64, c_i64, c_i64, c_i64]),
+    "sdb_replace_degenerate": (c_int, [c_int, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64,
+                                       c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp]),
+    "sdb_code_usage": (c_int, [c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "sdb_residual_sq": (c_int, [c_int, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp,
+                                c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "sdb_shard_sum": (c_int, [c_i64, c_vp, c_vp, c_vp, c_int, c_vp]),
+    "sdb_code_energy": (c_int, [c_int, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "sdb_first_columns": (c_int, [c_int, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "sdb_scale_rows": (c_int, [c_int, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "sdb_gather_rows": (c_int, [c_int, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp]),
+    "sdb_csc_to_codes": (c_int, [c_int, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "sdb_normalize": (c_int, [c_i64, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "sdb_extract_patches": (c_int, [c_int, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp]),
+    "sdb_reconstruct": (c_int, [c_int, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp,
+                                c_dbl, c_dbl, c_vp, c_vp]),
+    "sdb_reconstruct_dense": (c_int, [c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
 }
 
 

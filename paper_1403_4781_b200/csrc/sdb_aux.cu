@@ -1,0 +1,185 @@
+// Data-movement and patch-pipeline kernels around the OMP/MOD core.
+//
+// Reference: denoising.py:118-163,223-239 (patch extraction, overlap
+// averaging, clip), trainer.py:200-223 (shard gather), sparse_coding.py:76-133
+// (CSC container -> per-signal code rows), dictionary_update.py:56-69
+// (normalize_columns).
+#include "sdb_common.cuh"
+#include "sdb_internal.h"
+#include "sdb_aux.h"
+
+namespace sdb {
+
+// out[r] = in[perm[r]] for rows of length m (split_dataset's column gather)
+template <typename T>
+__global__ void k_gather_rows(int64_t rows, int m, const T* __restrict__ in, int64_t ldi,
+                              const int64_t* __restrict__ perm, T* __restrict__ out, int64_t ldo) {
+    const int lane = threadIdx.x & 31;
+    const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (r >= rows) return;
+    const T* src = in + perm[r] * ldi;
+    T* dst = out + r * ldo;
+    for (int t = lane; t < m; t += 32) dst[t] = src[t];
+}
+
+// CSC (indptr, indices, data) -> codes rows (idx N x cap, val, counts)
+template <typename T>
+__global__ void k_csc_to_codes(int64_t N, int cap, const int64_t* __restrict__ indptr,
+                               const int64_t* __restrict__ indices, const double* __restrict__ data,
+                               int32_t* __restrict__ idx, T* __restrict__ val, int32_t* __restrict__ counts) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const int64_t a = indptr[i], b = indptr[i + 1];
+    const int n = (int)(b - a);
+    counts[i] = n;
+    for (int t = 0; t < cap; ++t) {
+        idx[i * cap + t] = t < n ? (int32_t)indices[a + t] : 0;
+        val[i * cap + t] = t < n ? (T)data[a + t] : T(0);
+    }
+}
+
+// rows of length m: out = row / ||row|| (zero rows untouched), scales = norms
+__global__ void k_normalize(int64_t rows, int m, const double* __restrict__ in, double* __restrict__ out,
+                            double* __restrict__ scales) {
+    const int lane = threadIdx.x & 31;
+    const int64_t a = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (a >= rows) return;
+    double s = 0.0;
+    for (int r = lane; r < m; r += 32) s = fma(in[a * m + r], in[a * m + r], s);
+    const double nrm = sqrt(warp_sum(s));
+    for (int r = lane; r < m; r += 32) out[a * m + r] = nrm > 0.0 ? in[a * m + r] / nrm : in[a * m + r];
+    if (lane == 0 && scales) scales[a] = nrm;
+}
+
+// all p x p windows at stride s, column-major vectorised, row-offset major
+// order (denoising.py:118-135): patch k = r*C + c, element i + j*p
+template <typename T>
+__global__ void k_extract(const double* __restrict__ img, int H, int W, int p, int s, int R, int C,
+                          T* __restrict__ out) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t pp = (int64_t)p * p;
+    if (e >= (int64_t)R * C * pp) return;
+    const int64_t k = e / pp;
+    const int q = (int)(e % pp);
+    const int i = q % p, j = q / p;
+    const int r = (int)(k / C), c = (int)(k % C);
+    out[e] = (T)img[(int64_t)(r * s + i) * W + (c * s + j)];
+}
+
+// overlap averaging of the patch estimates D x_k (denoising.py:138-163,236-239)
+// as a gather: each pixel sums its covering patches in the reference's
+// (column offset j, row offset i) order, divides by the count, clips.
+template <typename T>
+__global__ void k_reconstruct(int H, int W, int p, int s, int R, int C, const double* __restrict__ D,
+                              int m, int cap, const int32_t* __restrict__ idx, const T* __restrict__ val,
+                              const int32_t* __restrict__ counts, double lo, double hi,
+                              double* __restrict__ out) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (int64_t)H * W) return;
+    const int y = (int)(e / W), x = (int)(e % W);
+    double sum = 0.0, cnt = 0.0;
+    for (int j = 0; j < p; ++j) {
+        const int cx = x - j;
+        if (cx < 0 || cx % s) continue;
+        const int c = cx / s;
+        if (c >= C) continue;
+        for (int i = 0; i < p; ++i) {
+            const int ry = y - i;
+            if (ry < 0 || ry % s) continue;
+            const int r = ry / s;
+            if (r >= R) continue;
+            const int64_t k = (int64_t)r * C + c;
+            const int n = counts[k];
+            const int row = i + j * p;
+            double est = 0.0;
+            for (int t = 0; t < n; ++t)
+                est = fma(D[(int64_t)idx[k * cap + t] * m + row], (double)val[k * cap + t], est);
+            sum += est;
+            cnt += 1.0;
+        }
+    }
+    double v = cnt > 0.0 ? sum / cnt : 0.0;
+    out[e] = fmin(fmax(v, lo), hi);
+}
+
+// reconstruct_from_patches on an explicit estimate matrix (n x p^2, signal-major)
+__global__ void k_reconstruct_dense(int H, int W, int p, int s, int R, int C, const double* __restrict__ P,
+                                    double* __restrict__ out) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (int64_t)H * W) return;
+    const int y = (int)(e / W), x = (int)(e % W);
+    double sum = 0.0, cnt = 0.0;
+    for (int j = 0; j < p; ++j) {
+        const int cx = x - j;
+        if (cx < 0 || cx % s) continue;
+        const int c = cx / s;
+        if (c >= C) continue;
+        for (int i = 0; i < p; ++i) {
+            const int ry = y - i;
+            if (ry < 0 || ry % s) continue;
+            const int r = ry / s;
+            if (r >= R) continue;
+            sum += P[((int64_t)r * C + c) * p * p + i + j * p];
+            cnt += 1.0;
+        }
+    }
+    out[e] = cnt > 0.0 ? sum / cnt : 0.0;
+}
+
+int reconstruct_dense(int H, int W, int p, int s, const double* P, double* out, cudaStream_t st) {
+    const int R = (H - p) / s + 1, C = (W - p) / s + 1;
+    const int64_t n = (int64_t)H * W;
+    k_reconstruct_dense<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(H, W, p, s, R, C, P, out);
+    return (int)cudaGetLastError();
+}
+
+template <typename T>
+int gather_rows(int64_t rows, int m, const T* in, int64_t ldi, const int64_t* perm, T* out, int64_t ldo,
+                cudaStream_t st) {
+    if (rows <= 0) return 0;
+    k_gather_rows<T><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(rows, m, in, ldi, perm, out, ldo);
+    return (int)cudaGetLastError();
+}
+template int gather_rows<float>(int64_t, int, const float*, int64_t, const int64_t*, float*, int64_t, cudaStream_t);
+template int gather_rows<double>(int64_t, int, const double*, int64_t, const int64_t*, double*, int64_t, cudaStream_t);
+
+template <typename T>
+int csc_to_codes(int64_t N, int cap, const int64_t* indptr, const int64_t* indices, const double* data,
+                 int32_t* idx, T* val, int32_t* counts, cudaStream_t st) {
+    if (N <= 0) return 0;
+    k_csc_to_codes<T><<<(unsigned)((N + 255) / 256), 256, 0, st>>>(N, cap, indptr, indices, data, idx, val, counts);
+    return (int)cudaGetLastError();
+}
+template int csc_to_codes<float>(int64_t, int, const int64_t*, const int64_t*, const double*, int32_t*, float*, int32_t*, cudaStream_t);
+template int csc_to_codes<double>(int64_t, int, const int64_t*, const int64_t*, const double*, int32_t*, double*, int32_t*, cudaStream_t);
+
+int normalize_rows(int64_t rows, int m, const double* in, double* out, double* scales, cudaStream_t st) {
+    if (rows <= 0) return 0;
+    k_normalize<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(rows, m, in, out, scales);
+    return (int)cudaGetLastError();
+}
+
+template <typename T>
+int extract_patches(const double* img, int H, int W, int p, int s, T* out, cudaStream_t st) {
+    const int R = (H - p) / s + 1, C = (W - p) / s + 1;
+    const int64_t n = (int64_t)R * C * p * p;
+    if (n <= 0) return 0;
+    k_extract<T><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(img, H, W, p, s, R, C, out);
+    return (int)cudaGetLastError();
+}
+template int extract_patches<float>(const double*, int, int, int, int, float*, cudaStream_t);
+template int extract_patches<double>(const double*, int, int, int, int, double*, cudaStream_t);
+
+template <typename T>
+int reconstruct(int H, int W, int p, int s, const double* D, int cap, const int32_t* idx, const T* val,
+                const int32_t* counts, double lo, double hi, double* out, cudaStream_t st) {
+    const int R = (H - p) / s + 1, C = (W - p) / s + 1;
+    const int64_t n = (int64_t)H * W;
+    k_reconstruct<T><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(H, W, p, s, R, C, D, p * p, cap, idx,
+                                                                 val, counts, lo, hi, out);
+    return (int)cudaGetLastError();
+}
+template int reconstruct<float>(int, int, int, int, const double*, int, const int32_t*, const float*, const int32_t*, double, double, double*, cudaStream_t);
+template int reconstruct<double>(int, int, int, int, const double*, int, const int32_t*, const double*, const int32_t*, double, double, double*, cudaStream_t);
+
+}  // namespace sdb

@@ -6,10 +6,13 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <type_traits>
 
 #include "../../include/sparsedict_b200.h"
 #include "sdb_common.cuh"
 #include "sdb_internal.h"
+#include "sdb_mod.h"
+#include "sdb_aux.h"
 
 namespace {
 thread_local std::string g_err;
@@ -182,6 +185,158 @@ int sdb_csc_fill(int dtype, int64_t N, int64_t cap, const int32_t* idx, const vo
                  ? sdb::pack_csc<double>(N, (int)cap, idx, (const double*)val, counts, indptr, indices, data, S(stream))
                  : sdb::pack_csc<float>(N, (int)cap, idx, (const float*)val, counts, indptr, indices, data, S(stream));
     return cuda_rc(rc, "sdb_csc_fill");
+}
+
+
+int64_t sdb_mod_workspace_bytes(int64_t P, int64_t N, int64_t m, int64_t K, int64_t cap) {
+    return sdb::mod_ws_bytes((int)P, N, (int)m, (int)K, (int)cap);
+}
+
+int sdb_mod_update(int dtype, int64_t P, int64_t N, int64_t m, int64_t K, int64_t cap,
+                   const int64_t* shard_off, const void* Y, int64_t ldy, const int32_t* idx,
+                   const void* val, const int32_t* counts, const double* D_prev, double* D_out,
+                   double* scales, int32_t* usage, int8_t* dead, double* resid_fro, int32_t* rank,
+                   int32_t* deficient, double rank_rcond, void* ws, int64_t ws_bytes, void* stream) {
+    if (!dtype_ok(dtype) || P < 1 || N < 0 || m < 1 || m > 256 || K < 1 || K > 1024 || cap < 1 || ldy < m)
+        return fail(SDB_EINVAL, "sdb_mod_update: bad args (m <= 256, K <= 1024)");
+    if (ws == nullptr || ws_bytes < sdb::mod_ws_bytes((int)P, N, (int)m, (int)K, (int)cap))
+        return fail(SDB_EINVAL, "sdb_mod_update: workspace too small");
+    auto go = [&](auto* tag) {
+        using T = std::remove_pointer_t<decltype(tag)>;
+        sdb::ModArgs<T> a{};
+        a.P = (int)P; a.m = (int)m; a.K = (int)K; a.cap = (int)cap; a.N = N;
+        a.off = shard_off; a.Y = (const T*)Y; a.ldy = ldy; a.idx = idx; a.val = (const T*)val;
+        a.counts = counts; a.Dprev = D_prev; a.Dout = D_out; a.scales = scales; a.usage = usage;
+        a.dead = dead; a.resid_fro = resid_fro; a.rank = rank; a.deficient_out = deficient;
+        a.nnz_out = nullptr; a.rank_rcond = rank_rcond; a.ws = ws;
+        return sdb::mod_update<T>(a, S(stream));
+    };
+    int rc = dtype == SDB_F64 ? go((double*)nullptr) : go((float*)nullptr);
+    return cuda_rc(rc, "sdb_mod_update");
+}
+
+int64_t sdb_replace_workspace_bytes(int64_t P, int64_t N, int64_t m, int64_t K) {
+    return sdb::replace_ws_bytes((int)P, N, (int)m, (int)K);
+}
+
+int sdb_replace_degenerate(int dtype, int64_t P, int64_t N, int64_t m, int64_t K, int64_t cap,
+                           const int64_t* shard_off, const void* Y, int64_t ldy,
+                           const int32_t* idx, const void* val, const int32_t* counts,
+                           const int32_t* usage, double* D, int8_t* flags, int32_t* ntarget,
+                           void* ws, int64_t ws_bytes, void* stream) {
+    if (!dtype_ok(dtype) || P < 1 || N < 0 || m < 1 || m > 256 || K < 1 || cap < 1 || ldy < m)
+        return fail(SDB_EINVAL, "sdb_replace_degenerate: bad args");
+    if (ws == nullptr || ws_bytes < sdb::replace_ws_bytes((int)P, N, (int)m, (int)K))
+        return fail(SDB_EINVAL, "sdb_replace_degenerate: workspace too small");
+    auto go = [&](auto* tag) {
+        using T = std::remove_pointer_t<decltype(tag)>;
+        sdb::ReplaceArgs<T> a{};
+        a.P = (int)P; a.m = (int)m; a.K = (int)K; a.cap = (int)cap; a.N = N; a.off = shard_off;
+        a.Y = (const T*)Y; a.ldy = ldy; a.idx = idx; a.val = (const T*)val; a.counts = counts;
+        a.usage = usage; a.D = D; a.flags = flags; a.ntarget_out = ntarget; a.ws = ws;
+        return sdb::replace_degenerate<T>(a, S(stream));
+    };
+    int rc = dtype == SDB_F64 ? go((double*)nullptr) : go((float*)nullptr);
+    return cuda_rc(rc, "sdb_replace_degenerate");
+}
+
+int sdb_code_usage(int64_t P, int64_t N, int64_t K, int64_t cap, const int64_t* shard_off,
+                   const int32_t* idx, const int32_t* counts, int32_t* usage, void* stream) {
+    if (P < 1 || N < 0 || K < 1 || cap < 1) return fail(SDB_EINVAL, "sdb_code_usage: bad args");
+    return cuda_rc(sdb::usage_direct(N, (int)K, (int)cap, (int)P, shard_off, idx, counts, usage,
+                                     S(stream)), "sdb_code_usage");
+}
+
+int sdb_residual_sq(int dtype, int64_t N, int64_t m, int64_t K, int64_t cap, int64_t P,
+                    const int64_t* shard_off, const void* Y, int64_t ldy, const int32_t* idx,
+                    const void* val, const int32_t* counts, const double* D, double* rsq,
+                    double* ysq, void* stream) {
+    if (!dtype_ok(dtype) || N < 0 || m < 1 || m > 256 || K < 1 || cap < 1 || P < 1 || ldy < m)
+        return fail(SDB_EINVAL, "sdb_residual_sq: bad args");
+    int rc = dtype == SDB_F64
+                 ? sdb::residual_sq<double>(N, (int)m, (int)K, (int)cap, (int)P, shard_off, (const double*)Y,
+                                            ldy, idx, (const double*)val, counts, D, rsq, ysq, S(stream))
+                 : sdb::residual_sq<float>(N, (int)m, (int)K, (int)cap, (int)P, shard_off, (const float*)Y,
+                                           ldy, idx, (const float*)val, counts, D, rsq, ysq, S(stream));
+    return cuda_rc(rc, "sdb_residual_sq");
+}
+
+int sdb_shard_sum(int64_t P, const int64_t* shard_off, const double* v, double* out, int do_sqrt,
+                  void* stream) {
+    if (P < 1) return fail(SDB_EINVAL, "sdb_shard_sum: bad args");
+    return cuda_rc(sdb::shard_sum((int)P, shard_off, v, out, do_sqrt, S(stream)), "sdb_shard_sum");
+}
+
+int sdb_code_energy(int dtype, int64_t N, int64_t cap, const void* val, const int32_t* counts,
+                    double* out, void* stream) {
+    if (!dtype_ok(dtype) || N < 0 || cap < 1) return fail(SDB_EINVAL, "sdb_code_energy: bad args");
+    int rc = dtype == SDB_F64 ? sdb::code_sq<double>(N, (int)cap, (const double*)val, counts, out, S(stream))
+                              : sdb::code_sq<float>(N, (int)cap, (const float*)val, counts, out, S(stream));
+    return cuda_rc(rc, "sdb_code_energy");
+}
+
+int sdb_first_columns(int dtype, int64_t P, int64_t K, int64_t m, const int64_t* shard_off,
+                      const void* Y, int64_t ldy, double* D, int32_t* zero_flag, void* stream) {
+    if (!dtype_ok(dtype) || P < 1 || K < 1 || m < 1 || ldy < m) return fail(SDB_EINVAL, "sdb_first_columns: bad args");
+    int rc = dtype == SDB_F64
+                 ? sdb::first_columns<double>((int)P, (int)K, (int)m, shard_off, (const double*)Y, ldy, D, zero_flag, S(stream))
+                 : sdb::first_columns<float>((int)P, (int)K, (int)m, shard_off, (const float*)Y, ldy, D, zero_flag, S(stream));
+    return cuda_rc(rc, "sdb_first_columns");
+}
+
+int sdb_scale_rows(int dtype, int64_t rows, int64_t group, int64_t m, const double* D,
+                   const double* w, void* out, void* stream) {
+    if (!dtype_ok(dtype) || rows < 0 || group < 1 || m < 1) return fail(SDB_EINVAL, "sdb_scale_rows: bad args");
+    int rc = dtype == SDB_F64 ? sdb::scale_rows<double>(rows, (int)group, (int)m, D, w, (double*)out, S(stream))
+                              : sdb::scale_rows<float>(rows, (int)group, (int)m, D, w, (float*)out, S(stream));
+    return cuda_rc(rc, "sdb_scale_rows");
+}
+
+
+int sdb_gather_rows(int dtype, int64_t rows, int64_t m, const void* in, int64_t ldi,
+                    const int64_t* perm, void* out, int64_t ldo, void* stream) {
+    if (!dtype_ok(dtype) || rows < 0 || m < 1 || ldi < m || ldo < m) return fail(SDB_EINVAL, "sdb_gather_rows: bad args");
+    int rc = dtype == SDB_F64 ? sdb::gather_rows<double>(rows, (int)m, (const double*)in, ldi, perm, (double*)out, ldo, S(stream))
+                              : sdb::gather_rows<float>(rows, (int)m, (const float*)in, ldi, perm, (float*)out, ldo, S(stream));
+    return cuda_rc(rc, "sdb_gather_rows");
+}
+
+int sdb_csc_to_codes(int dtype, int64_t N, int64_t cap, const int64_t* indptr,
+                     const int64_t* indices, const double* data, int32_t* idx, void* val,
+                     int32_t* counts, void* stream) {
+    if (!dtype_ok(dtype) || N < 0 || cap < 1) return fail(SDB_EINVAL, "sdb_csc_to_codes: bad args");
+    int rc = dtype == SDB_F64 ? sdb::csc_to_codes<double>(N, (int)cap, indptr, indices, data, idx, (double*)val, counts, S(stream))
+                              : sdb::csc_to_codes<float>(N, (int)cap, indptr, indices, data, idx, (float*)val, counts, S(stream));
+    return cuda_rc(rc, "sdb_csc_to_codes");
+}
+
+int sdb_normalize(int64_t rows, int64_t m, const double* in, double* out, double* scales, void* stream) {
+    if (rows < 0 || m < 1) return fail(SDB_EINVAL, "sdb_normalize: bad args");
+    return cuda_rc(sdb::normalize_rows(rows, (int)m, in, out, scales, S(stream)), "sdb_normalize");
+}
+
+int sdb_extract_patches(int dtype, const double* img, int64_t H, int64_t W, int64_t p, int64_t s,
+                        void* out, void* stream) {
+    if (!dtype_ok(dtype) || p < 1 || s < 1 || p > H || p > W) return fail(SDB_EINVAL, "sdb_extract_patches: bad args");
+    int rc = dtype == SDB_F64 ? sdb::extract_patches<double>(img, (int)H, (int)W, (int)p, (int)s, (double*)out, S(stream))
+                              : sdb::extract_patches<float>(img, (int)H, (int)W, (int)p, (int)s, (float*)out, S(stream));
+    return cuda_rc(rc, "sdb_extract_patches");
+}
+
+int sdb_reconstruct(int dtype, int64_t H, int64_t W, int64_t p, int64_t s, const double* D,
+                    int64_t cap, const int32_t* idx, const void* val, const int32_t* counts,
+                    double lo, double hi, double* out, void* stream) {
+    if (!dtype_ok(dtype) || p < 1 || s < 1 || p > H || p > W || cap < 1) return fail(SDB_EINVAL, "sdb_reconstruct: bad args");
+    int rc = dtype == SDB_F64
+                 ? sdb::reconstruct<double>((int)H, (int)W, (int)p, (int)s, D, (int)cap, idx, (const double*)val, counts, lo, hi, out, S(stream))
+                 : sdb::reconstruct<float>((int)H, (int)W, (int)p, (int)s, D, (int)cap, idx, (const float*)val, counts, lo, hi, out, S(stream));
+    return cuda_rc(rc, "sdb_reconstruct");
+}
+
+int sdb_reconstruct_dense(int64_t H, int64_t W, int64_t p, int64_t s, const double* P, double* out,
+                          void* stream) {
+    if (p < 1 || s < 1 || p > H || p > W) return fail(SDB_EINVAL, "sdb_reconstruct_dense: bad args");
+    return cuda_rc(sdb::reconstruct_dense((int)H, (int)W, (int)p, (int)s, P, out, S(stream)), "sdb_reconstruct_dense");
 }
 
 }  // extern "C"

@@ -1,0 +1,879 @@
+// MOD dictionary update, degenerate-atom replacement and residual norms on
+// B200, batched over P shards (one launch per phase covers every shard).
+//
+// Reference: /root/reference/pkg/src/sparsedict/dictionary_update.py
+//   mod_update :72-114, replace_degenerate_atoms :117-177, normalize :56-69
+// and metrics.py:30-44 (mse_db), trainer.py:138-162,248-256 (init / merge).
+//
+// Determinism: no floating-point atomics anywhere. The codes are
+// counting-sorted into per-(shard, atom) buckets with a fixed order (integer
+// atomics only for counts), then every normal-equation entry is a sequential
+// FP64 sum over its bucket. Results are bitwise reproducible run to run.
+//
+// Normal equations per shard:  A = X X^T (K x K), B = (Y X^T)^T (K x m)
+// solved as A Z = B with an FP64 blocked Cholesky (unused atoms masked to the
+// identity, which equals the minimum-norm lstsq solution on the used block);
+// D_new = Z^T (atom-major storage == Z row-major).
+#include <cfloat>
+
+#include "sdb_common.cuh"
+#include "sdb_internal.h"
+#include "sdb_mod.h"
+
+namespace sdb {
+
+constexpr int CH = 256;  // signals per chunk (chunks never straddle shards)
+
+// chunk_first[p] = first chunk of shard p; chunk_first[P] = total chunks
+__global__ void k_chunk_layout(const int64_t* __restrict__ off, int P, int64_t* __restrict__ cf) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        int64_t c = 0;
+        for (int p = 0; p < P; ++p) {
+            cf[p] = c;
+            c += (off[p + 1] - off[p] + CH - 1) / CH;
+        }
+        cf[P] = c;
+    }
+}
+
+struct ChunkInfo {
+    int p;
+    int64_t lo, hi;
+};
+
+__device__ __forceinline__ ChunkInfo chunk_info(const int64_t* off, const int64_t* cf, int P, int64_t c) {
+    int lo = 0, hi = P - 1;
+    while (lo < hi) {  // last p with cf[p] <= c (empty shards share cf values)
+        int mid = (lo + hi + 1) >> 1;
+        if (cf[mid] <= c) lo = mid; else hi = mid - 1;
+    }
+    ChunkInfo ci;
+    ci.p = lo;
+    ci.lo = off[lo] + (c - cf[lo]) * CH;
+    ci.hi = min(ci.lo + CH, off[lo + 1]);
+    return ci;
+}
+
+// ---- (a) per-chunk atom histograms (warp per chunk, smem int atomics)
+__global__ void __launch_bounds__(256)
+k_chunk_hist(const int64_t* __restrict__ off, const int64_t* __restrict__ cf, int P, int K, int cap,
+             const int32_t* __restrict__ idx, const int32_t* __restrict__ counts,
+             int32_t* __restrict__ chunk_hist) {
+    extern __shared__ int32_t sh_cnt[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t c = (int64_t)blockIdx.x * 8 + wib;
+    const int64_t nch = cf[P];
+    int32_t* cnt = sh_cnt + wib * K;
+    if (c >= nch) return;
+    for (int a = lane; a < K; a += 32) cnt[a] = 0;
+    __syncwarp();
+    const ChunkInfo ci = chunk_info(off, cf, P, c);
+    for (int64_t i = ci.lo + lane; i < ci.hi; i += 32) {
+        const int n = counts[i];
+        for (int t = 0; t < n; ++t) atomicAdd(&cnt[idx[i * cap + t]], 1);
+    }
+    __syncwarp();
+    for (int a = lane; a < K; a += 32) chunk_hist[c * K + a] = cnt[a];
+}
+
+// ---- (b) usage[p][a] = sum over the shard's chunks
+__global__ void k_usage_from_chunks(const int64_t* __restrict__ cf, int P, int K,
+                                    const int32_t* __restrict__ chunk_hist, int32_t* __restrict__ usage) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (int64_t)P * K) return;
+    const int p = (int)(e / K), a = (int)(e % K);
+    int32_t s = 0;
+    for (int64_t c = cf[p]; c < cf[p + 1]; ++c) s += chunk_hist[c * K + a];
+    usage[e] = s;
+}
+
+// ---- (d) chunk_off[c][a] = bucket_off[p][a] + prefix over earlier chunks
+__global__ void k_chunk_offsets(const int64_t* __restrict__ cf, int P, int K,
+                                const int32_t* __restrict__ chunk_hist,
+                                const int64_t* __restrict__ bucket_off, int64_t* __restrict__ chunk_off) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (int64_t)P * K) return;
+    const int p = (int)(e / K), a = (int)(e % K);
+    int64_t run = bucket_off[e];
+    for (int64_t c = cf[p]; c < cf[p + 1]; ++c) {
+        chunk_off[c * K + a] = run;
+        run += chunk_hist[c * K + a];
+    }
+}
+
+// ---- (e) stable placement: order inside a bucket = (chunk, 32-signal group,
+// slot, lane) — a fixed function of the input.
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_place(const int64_t* __restrict__ off, const int64_t* __restrict__ cf, int P, int K, int cap,
+        const int32_t* __restrict__ idx, const T* __restrict__ val, const int32_t* __restrict__ counts,
+        const int64_t* __restrict__ chunk_off, int32_t* __restrict__ bsig, double* __restrict__ bval) {
+    extern __shared__ int64_t sh_pos[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t c = (int64_t)blockIdx.x * 8 + wib;
+    if (c >= cf[P]) return;
+    int64_t* pos = sh_pos + (int64_t)wib * K;
+    for (int a = lane; a < K; a += 32) pos[a] = chunk_off[c * K + a];
+    __syncwarp();
+    const ChunkInfo ci = chunk_info(off, cf, P, c);
+    for (int64_t g = ci.lo; g < ci.hi; g += 32) {
+        const int64_t i = g + lane;
+        const int n = (i < ci.hi) ? counts[i] : 0;
+        const int nmax = __reduce_max_sync(SDB_FULL, n);
+        for (int t = 0; t < nmax; ++t) {
+            const bool act = t < n;
+            const unsigned am = __ballot_sync(SDB_FULL, act);
+            int a = 0;
+            unsigned peers = 0;
+            int64_t base = 0;
+            if (act) {
+                a = idx[i * cap + t];
+                peers = __match_any_sync(am, a);
+                base = pos[a];
+            }
+            __syncwarp();
+            if (act) {
+                const int rank = __popc(peers & ((1u << lane) - 1u));
+                const int64_t q = base + rank;
+                bsig[q] = (int32_t)i;
+                bval[q] = (double)val[i * cap + t];
+                if (rank == 0) pos[a] = base + __popc(peers);
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// ---- (f) B[p][a][:] = sum over bucket (y_i * x_ai), lanes over m
+template <typename T, int MPL>
+__global__ void __launch_bounds__(256)
+k_yxt(int P, int K, int m, const T* __restrict__ Y, int64_t ldy, const int64_t* __restrict__ bucket_off,
+      const int32_t* __restrict__ bsig, const double* __restrict__ bval, double* __restrict__ B) {
+    const int lane = threadIdx.x & 31;
+    const int64_t e = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);  // (p, a)
+    if (e >= (int64_t)P * K) return;
+    double acc[MPL];
+#pragma unroll
+    for (int q = 0; q < MPL; ++q) acc[q] = 0.0;
+    const int64_t lo = bucket_off[e], hi = bucket_off[e + 1];
+    for (int64_t b = lo; b < hi; ++b) {
+        const int64_t i = bsig[b];
+        const double v = bval[b];
+        const T* y = Y + i * ldy;
+#pragma unroll
+        for (int q = 0; q < MPL; ++q) {
+            const int r = lane + 32 * q;
+            if (r < m) acc[q] = fma((double)y[r], v, acc[q]);
+        }
+    }
+    double* out = B + e * m;
+#pragma unroll
+    for (int q = 0; q < MPL; ++q) {
+        const int r = lane + 32 * q;
+        if (r < m) out[r] = acc[q];
+    }
+}
+
+// ---- (g) A[p][a][:] = sum over bucket (x_ai * x_i), row accumulator in smem
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_xxt(int P, int K, int cap, const int32_t* __restrict__ idx, const T* __restrict__ val,
+      const int32_t* __restrict__ counts, const int64_t* __restrict__ bucket_off,
+      const int32_t* __restrict__ bsig, const double* __restrict__ bval, double* __restrict__ A) {
+    extern __shared__ double sh_row[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t e = (int64_t)blockIdx.x * 8 + wib;
+    if (e >= (int64_t)P * K) return;
+    double* row = sh_row + (int64_t)wib * K;
+    for (int b = lane; b < K; b += 32) row[b] = 0.0;
+    __syncwarp();
+    const int64_t lo = bucket_off[e], hi = bucket_off[e + 1];
+    for (int64_t q = lo; q < hi; ++q) {
+        const int64_t i = bsig[q];
+        const double v = bval[q];
+        const int n = counts[i];
+        for (int t = lane; t < n; t += 32) {
+            const int b = idx[i * cap + t];
+            row[b] = fma(v, (double)val[i * cap + t], row[b]);
+        }
+        __syncwarp();
+    }
+    double* out = A + e * K;
+    for (int b = lane; b < K; b += 32) out[b] = row[b];
+}
+
+// ---- (h) masked blocked Cholesky, one CTA per shard, in place (lower), then
+// the upper triangle is overwritten with L^T for the back substitution.
+constexpr int NB = 32;
+
+__global__ void __launch_bounds__(512)
+k_cholesky(int K, double* __restrict__ Aall, const int32_t* __restrict__ usage,
+           int32_t* __restrict__ deficient, int8_t* __restrict__ depmask, double rel_tol) {
+    const int p = blockIdx.x;
+    double* A = Aall + (int64_t)p * K * K;
+    const int32_t* use = usage + (int64_t)p * K;
+    __shared__ double Ld[NB][NB + 1];
+    __shared__ double Pa[NB][NB + 1];
+    __shared__ double Pb[NB][NB + 1];
+    __shared__ double s_tol;
+    __shared__ int s_def;
+    __shared__ int8_t s_dep[NB];
+    int8_t* dm = depmask + (int64_t)p * K;
+    const int tid = threadIdx.x, nth = blockDim.x;
+
+    // mask unused atoms: row/col zero, unit diagonal (== min-norm on the used block)
+    for (int64_t e = tid; e < (int64_t)K * K; e += nth) {
+        const int r = (int)(e / K), c = (int)(e % K);
+        if (!use[r] || !use[c]) A[e] = (r == c) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double mx = 0.0;
+        for (int r = 0; r < K; ++r)
+            if (use[r]) mx = fmax(mx, A[(int64_t)r * K + r]);
+        s_tol = rel_tol * mx;
+        s_def = 0;
+    }
+    __syncthreads();
+    const double tol = s_tol;
+
+    for (int j0 = 0; j0 < K; j0 += NB) {
+        const int nb = min(NB, K - j0);
+        // 1. diagonal block, unblocked, by warp 0
+        if (tid < 32) {
+            for (int e = tid; e < nb * nb; e += 32) {
+                const int r = e / nb, c = e % nb;
+                Ld[r][c] = A[(int64_t)(j0 + r) * K + j0 + c];
+            }
+            __syncwarp();
+            for (int c = 0; c < nb; ++c) {
+                double d = Ld[c][c];
+                const bool dep = !(d > tol);
+                if (tid == 0) {
+                    s_dep[c] = dep ? 1 : 0;
+                    dm[j0 + c] = dep ? 1 : 0;
+                    if (dep) s_def += 1;  // numerically dependent pivot: atom dropped
+                }
+                if (dep) d = 1.0;
+                const double lc = sqrt(d);
+                __syncwarp();
+                if (tid == 0) Ld[c][c] = lc;
+                for (int r = c + 1 + tid; r < nb; r += 32) Ld[r][c] = dep ? 0.0 : Ld[r][c] / lc;
+                __syncwarp();
+                for (int r = c + 1 + tid; r < nb; r += 32)
+                    for (int q = c + 1; q <= r; ++q) Ld[r][q] -= Ld[r][c] * Ld[q][c];
+                __syncwarp();
+            }
+            for (int e = tid; e < nb * nb; e += 32) {
+                const int r = e / nb, c = e % nb;
+                if (c <= r) A[(int64_t)(j0 + r) * K + j0 + c] = Ld[r][c];
+            }
+        }
+        __syncthreads();
+        // 2. panel below: X L11^T = A21 (thread per row)
+        for (int r = j0 + nb + tid; r < K; r += nth) {
+            double* ar = A + (int64_t)r * K + j0;
+            double xr[NB];
+#pragma unroll
+            for (int c = 0; c < NB; ++c) xr[c] = (c < nb) ? ar[c] : 0.0;
+#pragma unroll
+            for (int c = 0; c < NB; ++c) {
+                if (c < nb) {
+                    double s = xr[c];
+                    for (int q = 0; q < c; ++q) s -= xr[q] * Ld[c][q];
+                    xr[c] = s_dep[c] ? 0.0 : s / Ld[c][c];
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < NB; ++c)
+                if (c < nb) ar[c] = xr[c];
+        }
+        __syncthreads();
+        // 3. trailing update of the lower triangle: A22 -= L21 L21^T, 32x32 tiles
+        const int t0 = j0 + nb;
+        const int nt = (K - t0 + NB - 1) / NB;
+        for (int tile = 0; tile < nt * (nt + 1) / 2; ++tile) {
+            // tile -> (bi >= bj)
+            int bi = (int)((sqrt(8.0 * tile + 1.0) - 1.0) * 0.5);
+            while ((bi + 1) * (bi + 2) / 2 <= tile) ++bi;
+            while (bi * (bi + 1) / 2 > tile) --bi;
+            const int bj = tile - bi * (bi + 1) / 2;
+            const int r0 = t0 + bi * NB, c0 = t0 + bj * NB;
+            for (int e = tid; e < NB * NB; e += nth) {
+                const int r = e / NB, q = e % NB;
+                Pa[r][q] = (r0 + r < K && q < nb) ? A[(int64_t)(r0 + r) * K + j0 + q] : 0.0;
+                Pb[r][q] = (c0 + r < K && q < nb) ? A[(int64_t)(c0 + r) * K + j0 + q] : 0.0;
+            }
+            __syncthreads();
+            for (int e = tid; e < NB * NB; e += nth) {
+                const int r = e / NB, c = e % NB;
+                const int gr = r0 + r, gc = c0 + c;
+                if (gr < K && gc < K && gc <= gr) {
+                    double s = 0.0;
+#pragma unroll 8
+                    for (int q = 0; q < NB; ++q) s = fma(Pa[r][q], Pb[c][q], s);
+                    A[(int64_t)gr * K + gc] -= s;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    // mirror: upper triangle <- L^T
+    for (int64_t e = tid; e < (int64_t)K * K; e += nth) {
+        const int r = (int)(e / K), c = (int)(e % K);
+        if (c > r) A[e] = A[(int64_t)c * K + r];
+    }
+    if (tid == 0) deficient[p] = s_def;
+}
+
+// ---- triangular solves A Z = B in place on B (K x m per shard); warp per
+// right-hand side column, lanes split each dot product (coalesced L rows).
+__global__ void __launch_bounds__(256)
+k_trsolve(int K, int m, const double* __restrict__ Lall, const int8_t* __restrict__ depmask,
+          double* __restrict__ Ball) {
+    extern __shared__ double sh_w[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int p = blockIdx.y;
+    const int col = blockIdx.x * 8 + wib;
+    if (col >= m) return;
+    const double* L = Lall + (int64_t)p * K * K;
+    double* B = Ball + (int64_t)p * K * m;
+    double* w = sh_w + (int64_t)wib * K;
+    const int8_t* dm = depmask + (int64_t)p * K;
+    // forward: L w = b (dependent atoms: w = 0, so their solution row is 0)
+    for (int r = 0; r < K; ++r) {
+        const double* lr = L + (int64_t)r * K;
+        double s = 0.0;
+        for (int c = lane; c < r; c += 32) s = fma(lr[c], w[c], s);
+        s = warp_sum(s);
+        const double v = dm[r] ? 0.0 : (B[(int64_t)r * m + col] - s) / lr[r];
+        if (lane == 0) w[r] = v;
+        __syncwarp();
+    }
+    // back: L^T z = w  (row r of the upper triangle holds L[c][r], c > r)
+    for (int r = K - 1; r >= 0; --r) {
+        const double* ur = L + (int64_t)r * K;
+        double s = 0.0;
+        for (int c = r + 1 + lane; c < K; c += 32) s = fma(ur[c], w[c], s);
+        s = warp_sum(s);
+        const double v = (w[r] - s) / ur[r];
+        __syncwarp();
+        if (lane == 0) w[r] = v;
+        __syncwarp();
+    }
+    for (int r = lane; r < K; r += 32) B[(int64_t)r * m + col] = w[r];
+}
+
+// ---- per-signal residual ||y_i - D_p x_i||^2 (D in f64, atom-major)
+template <typename T, int MPL>
+__global__ void __launch_bounds__(256)
+k_resid_sq(int64_t N, int m, int K, int cap, int P, const int64_t* __restrict__ off,
+           const T* __restrict__ Y, int64_t ldy, const int32_t* __restrict__ idx,
+           const T* __restrict__ val, const int32_t* __restrict__ counts,
+           const double* __restrict__ D, double* __restrict__ out, double* __restrict__ ysq_out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (i >= N) return;
+    const int p = shard_of(off, P, i);
+    const double* Dp = D + (int64_t)p * K * m;
+    const T* y = Y + i * ldy;
+    double r[MPL];
+    double yy = 0.0;
+#pragma unroll
+    for (int q = 0; q < MPL; ++q) {
+        const int row = lane + 32 * q;
+        r[q] = (row < m) ? (double)y[row] : 0.0;
+        yy = fma(r[q], r[q], yy);
+    }
+    const int n = counts[i];
+    for (int t = 0; t < n; ++t) {
+        const double* d = Dp + (int64_t)idx[i * cap + t] * m;
+        const double v = (double)val[i * cap + t];
+#pragma unroll
+        for (int q = 0; q < MPL; ++q) {
+            const int row = lane + 32 * q;
+            if (row < m) r[q] = fma(-d[row], v, r[q]);
+        }
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < MPL; ++q) s = fma(r[q], r[q], s);
+    s = warp_sum(s);
+    yy = warp_sum(yy);
+    if (lane == 0) {
+        out[i] = s;
+        if (ysq_out) ysq_out[i] = yy;
+    }
+}
+
+// ---- deterministic per-shard sum of a per-signal array (fixed order)
+__global__ void __launch_bounds__(256)
+k_shard_sum(const int64_t* __restrict__ off, const double* __restrict__ v, double* __restrict__ out,
+            int do_sqrt) {
+    __shared__ double sh[256];
+    const int p = blockIdx.x;
+    double s = 0.0;
+    for (int64_t i = off[p] + threadIdx.x; i < off[p + 1]; i += 256) s += v[i];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[p] = do_sqrt ? sqrt(sh[0]) : sh[0];
+}
+
+// ---- (i) finish MOD: norms, dead atoms, restore, normalise (dictionary_update.py:103-113)
+__global__ void __launch_bounds__(256)
+k_mod_finish(int P, int K, int m, const double* __restrict__ Z, const double* __restrict__ Dprev,
+             const int32_t* __restrict__ usage, const int64_t* __restrict__ nnz_shard,
+             double* __restrict__ Dout, double* __restrict__ scales, int8_t* __restrict__ dead,
+             int32_t* __restrict__ rank, const int32_t* __restrict__ deficient) {
+    __shared__ double s_max;
+    __shared__ int s_rank;
+    const int p = blockIdx.x;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const double* Zp = Z + (int64_t)p * K * m;
+    if (threadIdx.x == 0) { s_max = 0.0; s_rank = 0; }
+    __syncthreads();
+    const bool empty = nnz_shard[p] == 0;
+    // column norms of the raw solution
+    for (int a = wib; a < K; a += 8) {
+        double s = 0.0;
+        for (int r = lane; r < m; r += 32) s = fma(Zp[(int64_t)a * m + r], Zp[(int64_t)a * m + r], s);
+        s = warp_sum(s);
+        if (lane == 0) scales[(int64_t)p * K + a] = sqrt(s);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double mx = 0.0;
+        int rk = 0;
+        for (int a = 0; a < K; ++a) {
+            mx = fmax(mx, scales[(int64_t)p * K + a]);
+            rk += usage[(int64_t)p * K + a] > 0;
+        }
+        s_max = mx;
+        s_rank = empty ? 0 : rk;
+    }
+    __syncthreads();
+    const double thr = 1e-12 * fmax(s_max, 1.0);
+    for (int a = wib; a < K; a += 8) {
+        const int64_t e = (int64_t)p * K + a;
+        const bool dd = empty || usage[e] == 0 || scales[e] <= thr;
+        if (lane == 0) dead[e] = dd ? 1 : 0;
+        const double* src = dd ? (Dprev + e * m) : (Zp + (int64_t)a * m);
+        double* dst = Dout + e * m;
+        if (empty) {  // all-zero codes: D_prev returned unchanged (:92-95)
+            for (int r = lane; r < m; r += 32) dst[r] = src[r];
+            continue;
+        }
+        double s = 0.0;
+        for (int r = lane; r < m; r += 32) s = fma(src[r], src[r], s);
+        const double nrm = sqrt(warp_sum(s));
+        for (int r = lane; r < m; r += 32) dst[r] = nrm > 0.0 ? src[r] / nrm : src[r];
+    }
+    if (threadIdx.x == 0) rank[p] = empty ? 0 : s_rank - deficient[p];
+}
+
+// ---- replace_degenerate_atoms (dictionary_update.py:134-176)
+// twins + target marking, warp per shard, rows processed in order
+__global__ void __launch_bounds__(32)
+k_twins(int K, const double* __restrict__ C, const double* __restrict__ D, int m,
+        const int32_t* __restrict__ usage, int8_t* __restrict__ deg, int32_t* __restrict__ ntarget) {
+    const int p = blockIdx.x, lane = threadIdx.x;
+    const double* Cp = C + (int64_t)p * K * K;
+    int8_t* dg = deg + (int64_t)p * K;
+    for (int a = lane; a < K; a += 32) {
+        double s = 0.0;
+        const double* d = D + ((int64_t)p * K + a) * m;
+        for (int r = 0; r < m; ++r) s = fma(d[r], d[r], s);
+        dg[a] = (usage[(int64_t)p * K + a] == 0 || sqrt(s) <= 1e-12) ? 1 : 0;
+    }
+    __syncwarp();
+    for (int i = 0; i < K; ++i) {
+        __syncwarp();
+        if (dg[i]) continue;  // warp-uniform
+        const double* ci = Cp + (int64_t)i * K;
+        for (int j = i + 1 + lane; j < K; j += 32)
+            if (fabs(ci[j]) > 0.999) dg[j] = 1;
+    }
+    __syncwarp();
+    int cnt = 0;
+    for (int a = lane; a < K; a += 32) cnt += dg[a];
+    cnt = (int)warp_sum((double)cnt);
+    if (lane == 0) ntarget[p] = cnt;
+}
+
+// normalised copy Dn = D / ||D|| (columns with zero norm untouched)
+__global__ void k_normalize_rows(int64_t rows, int m, const double* __restrict__ D, double* __restrict__ Dn) {
+    const int lane = threadIdx.x & 31;
+    const int64_t a = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (a >= rows) return;
+    double s = 0.0;
+    for (int r = lane; r < m; r += 32) s = fma(D[a * m + r], D[a * m + r], s);
+    const double nrm = sqrt(warp_sum(s));
+    for (int r = lane; r < m; r += 32) Dn[a * m + r] = nrm > 0.0 ? D[a * m + r] / nrm : D[a * m + r];
+}
+
+// Candidate selection: targets (ascending atom) take data columns in order
+// of descending residual, ties to the lower column; zero columns skipped.
+// One CTA per shard, one block-argmax round per target.
+__global__ void __launch_bounds__(512)
+k_replace_select(int K, int m, const int64_t* __restrict__ off, const double* __restrict__ rsq,
+                 const double* __restrict__ ysq, const int8_t* __restrict__ deg,
+                 const int32_t* __restrict__ ntarget, int8_t* __restrict__ taken,
+                 int64_t* __restrict__ pick /* P*K: chosen column or -1 */) {
+    const int p = blockIdx.x;
+    const int64_t lo = off[p], hi = off[p + 1];
+    __shared__ double sv[512];
+    __shared__ int64_t si[512];
+    if (ntarget[p] == 0) return;
+    for (int a = 0; a < K; ++a) {
+        if (!deg[(int64_t)p * K + a]) continue;
+        double bv = -1.0;
+        int64_t bi = INT64_MAX;
+        for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+            if (taken[i] || !(ysq[i] > 0.0)) continue;
+            const double v = rsq[i];
+            if (v > bv || (v == bv && i < bi)) { bv = v; bi = i; }
+        }
+        sv[threadIdx.x] = bv;
+        si[threadIdx.x] = bi;
+        __syncthreads();
+        for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+            if (threadIdx.x < w) {
+                const double ov = sv[threadIdx.x + w];
+                const int64_t oi = si[threadIdx.x + w];
+                if (ov > sv[threadIdx.x] || (ov == sv[threadIdx.x] && oi < si[threadIdx.x])) {
+                    sv[threadIdx.x] = ov;
+                    si[threadIdx.x] = oi;
+                }
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            const bool ok = si[0] != INT64_MAX && sv[0] >= 0.0;
+            pick[(int64_t)p * K + a] = ok ? si[0] : -1;
+            if (ok) taken[si[0]] = 1;
+        }
+        __syncthreads();
+    }
+}
+
+template <typename T>
+__global__ void k_replace_apply(int P, int K, int m, const T* __restrict__ Y, int64_t ldy,
+                                const int8_t* __restrict__ deg, const int64_t* __restrict__ pick,
+                                const double* __restrict__ ysq, const int32_t* __restrict__ ntarget,
+                                double* __restrict__ D, int8_t* __restrict__ flags) {
+    const int lane = threadIdx.x & 31;
+    const int64_t e = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (e >= (int64_t)P * K) return;
+    const int p = (int)(e / K);
+    if (ntarget[p] == 0 || !deg[e]) {
+        if (lane == 0) flags[e] = 0;
+        return;
+    }
+    const int64_t c = pick[e];
+    if (c < 0) {
+        if (lane == 0) flags[e] = 2;
+        return;
+    }
+    const double nrm = sqrt(ysq[c]);
+    for (int r = lane; r < m; r += 32) D[e * m + r] = (double)Y[c * ldy + r] / nrm;
+    if (lane == 0) flags[e] = 1;
+}
+
+// ---- usage histogram only (replace_degenerate_atoms called on its own)
+__global__ void k_usage_direct(int64_t N, int K, int cap, int P, const int64_t* __restrict__ off,
+                               const int32_t* __restrict__ idx, const int32_t* __restrict__ counts,
+                               int32_t* __restrict__ usage) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const int p = shard_of(off, P, i);
+    const int n = counts[i];
+    for (int t = 0; t < n; ++t) atomicAdd(&usage[(int64_t)p * K + idx[i * cap + t]], 1);
+}
+
+__global__ void k_shard_nnz(const int64_t* __restrict__ off, const int32_t* __restrict__ counts,
+                            int64_t* __restrict__ out) {
+    __shared__ int64_t sh[256];
+    const int p = blockIdx.x;
+    int64_t s = 0;
+    for (int64_t i = off[p] + threadIdx.x; i < off[p + 1]; i += 256) s += counts[i];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[p] = sh[0];
+}
+
+// ---- code energy per shard: sum of squared code values (w_t^2, trainer.py:250)
+template <typename T>
+__global__ void k_code_sq(int64_t N, int cap, const T* __restrict__ val, const int32_t* __restrict__ counts,
+                          double* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    double s = 0.0;
+    const int n = counts[i];
+    for (int t = 0; t < n; ++t) {
+        const double v = (double)val[i * cap + t];
+        s = fma(v, v, s);
+    }
+    out[i] = s;
+}
+
+// ---- first-columns init per shard (trainer.py:145-148): D0[p][a] =
+// normalise(first K signals of shard p); zero columns flagged for the host.
+template <typename T>
+__global__ void k_first_columns(int P, int K, int m, const int64_t* __restrict__ off,
+                                const T* __restrict__ Y, int64_t ldy, double* __restrict__ D,
+                                int32_t* __restrict__ zero_flag) {
+    const int lane = threadIdx.x & 31;
+    const int64_t e = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (e >= (int64_t)P * K) return;
+    const int p = (int)(e / K), a = (int)(e % K);
+    const T* y = Y + (off[p] + a) * ldy;
+    double s = 0.0;
+    for (int r = lane; r < m; r += 32) s = fma((double)y[r], (double)y[r], s);
+    const double nrm = sqrt(warp_sum(s));
+    for (int r = lane; r < m; r += 32) D[e * m + r] = nrm > 0.0 ? (double)y[r] / nrm : 0.0;
+    if (lane == 0) zero_flag[e] = nrm > 0.0 ? 0 : 1;
+}
+
+// ---- merge dataset rows: out[t*K1 + a] = w_t * D_t[a]  (trainer.py:248-256)
+template <typename T>
+__global__ void k_scale_rows(int64_t rows, int group, int m, const double* __restrict__ D,
+                             const double* __restrict__ w, T* __restrict__ out) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= rows * m) return;
+    const int64_t row = e / m;
+    out[e] = (T)(w[row / group] * D[e]);
+}
+
+// =============================================================================
+// host launchers
+// =============================================================================
+template <typename F>
+static int with_mpl(int m, F&& f) {
+    const int mpl = (m + 31) / 32;
+    if (mpl <= 1) return f(std::integral_constant<int, 1>{});
+    if (mpl <= 2) return f(std::integral_constant<int, 2>{});
+    if (mpl <= 4) return f(std::integral_constant<int, 4>{});
+    if (mpl <= 8) return f(std::integral_constant<int, 8>{});
+    return (int)cudaErrorInvalidValue;  // m > 256 rejected at the ABI
+}
+
+static int64_t nchunks_upper(int64_t N, int P) { return N / CH + P + 1; }
+
+ModWs carve_mod_ws(void* base, int P, int64_t N, int m, int K, int cap) {
+    ModWs w{};
+    unsigned char* p = (unsigned char*)base;
+    auto take = [&](int64_t bytes) { void* r = p; p += (bytes + 255) & ~int64_t(255); return r; };
+    const int64_t nch = nchunks_upper(N, P);
+    w.cf = (int64_t*)take(sizeof(int64_t) * (P + 1));
+    w.chunk_hist = (int32_t*)take(sizeof(int32_t) * nch * K);
+    w.chunk_off = (int64_t*)take(sizeof(int64_t) * nch * K);
+    w.bucket_off = (int64_t*)take(sizeof(int64_t) * ((int64_t)P * K + 1));
+    w.scan_ws = (int64_t*)take(scan_workspace_bytes((int64_t)P * K));
+    w.bsig = (int32_t*)take(sizeof(int32_t) * std::max<int64_t>(N * cap, 1));
+    w.bval = (double*)take(sizeof(double) * std::max<int64_t>(N * cap, 1));
+    w.A = (double*)take(sizeof(double) * (int64_t)P * K * K);
+    w.B = (double*)take(sizeof(double) * (int64_t)P * K * m);
+    w.rsq = (double*)take(sizeof(double) * std::max<int64_t>(N, 1));
+    w.nnz = (int64_t*)take(sizeof(int64_t) * P);
+    w.deficient = (int32_t*)take(sizeof(int32_t) * P);
+    w.depmask = (int8_t*)take((int64_t)P * K);
+    w.end = p;
+    return w;
+}
+
+int64_t mod_ws_bytes(int P, int64_t N, int m, int K, int cap) {
+    ModWs w = carve_mod_ws(nullptr, P, N, m, K, cap);
+    return (int64_t)(w.end - (unsigned char*)nullptr) + 256;
+}
+
+template <typename T>
+int mod_update(const ModArgs<T>& a, cudaStream_t st) {
+    const int P = a.P, K = a.K, m = a.m, cap = a.cap;
+    const int64_t N = a.N;
+    ModWs w = carve_mod_ws(a.ws, P, N, m, K, cap);
+    const int64_t PK = (int64_t)P * K;
+    const int64_t nch_max = nchunks_upper(N, P);
+    k_chunk_layout<<<1, 32, 0, st>>>(a.off, P, w.cf);
+    const unsigned hb = (unsigned)((nch_max + 7) / 8);
+    k_chunk_hist<<<hb, 256, 8 * K * sizeof(int32_t), st>>>(a.off, w.cf, P, K, cap, a.idx, a.counts,
+                                                          w.chunk_hist);
+    k_usage_from_chunks<<<(unsigned)((PK + 255) / 256), 256, 0, st>>>(w.cf, P, K, w.chunk_hist, a.usage);
+    int rc = exclusive_scan_counts(a.usage, PK, w.bucket_off, w.scan_ws, st);
+    if (rc) return rc;
+    k_chunk_offsets<<<(unsigned)((PK + 255) / 256), 256, 0, st>>>(w.cf, P, K, w.chunk_hist,
+                                                                  w.bucket_off, w.chunk_off);
+    {
+        const int smem = 8 * K * (int)sizeof(int64_t);
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(k_place<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        k_place<T><<<hb, 256, smem, st>>>(a.off, w.cf, P, K, cap, a.idx, a.val, a.counts,
+                                         w.chunk_off, w.bsig, w.bval);
+    }
+    rc = with_mpl(m, [&](auto c) {
+        constexpr int MPL = decltype(c)::value;
+        k_yxt<T, MPL><<<(unsigned)((PK + 7) / 8), 256, 0, st>>>(P, K, m, a.Y, a.ldy, w.bucket_off,
+                                                               w.bsig, w.bval, w.B);
+        return (int)cudaGetLastError();
+    });
+    if (rc) return rc;
+    {
+        const int smem = 8 * K * (int)sizeof(double);
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(k_xxt<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        k_xxt<T><<<(unsigned)((PK + 7) / 8), 256, smem, st>>>(P, K, cap, a.idx, a.val, a.counts,
+                                                             w.bucket_off, w.bsig, w.bval, w.A);
+    }
+    k_cholesky<<<P, 512, 0, st>>>(K, w.A, a.usage, w.deficient, w.depmask, a.rank_rcond);
+    {
+        // masked RHS rows for unused atoms are irrelevant: A is identity there
+        // and B holds zeros (their buckets are empty).
+        const int smem = 8 * K * (int)sizeof(double);
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(k_trsolve, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        dim3 g((unsigned)((m + 7) / 8), (unsigned)P);
+        k_trsolve<<<g, 256, smem, st>>>(K, m, w.A, w.depmask, w.B);
+    }
+    // residual before normalisation with the raw solution Z (= B now)
+    rc = with_mpl(m, [&](auto c) {
+        constexpr int MPL = decltype(c)::value;
+        k_resid_sq<T, MPL><<<(unsigned)((N + 7) / 8), 256, 0, st>>>(
+            N, m, K, cap, P, a.off, a.Y, a.ldy, a.idx, a.val, a.counts, w.B, w.rsq, nullptr);
+        return (int)cudaGetLastError();
+    });
+    if (rc) return rc;
+    k_shard_sum<<<P, 256, 0, st>>>(a.off, w.rsq, a.resid_fro, 1);
+    k_shard_nnz<<<P, 256, 0, st>>>(a.off, a.counts, w.nnz);
+    k_mod_finish<<<P, 256, 0, st>>>(P, K, m, w.B, a.Dprev, a.usage, w.nnz, a.Dout, a.scales, a.dead,
+                                    a.rank, w.deficient);
+    if (a.deficient_out)
+        cudaMemcpyAsync(a.deficient_out, w.deficient, sizeof(int32_t) * P, cudaMemcpyDeviceToDevice, st);
+    if (a.nnz_out)
+        cudaMemcpyAsync(a.nnz_out, w.nnz, sizeof(int64_t) * P, cudaMemcpyDeviceToDevice, st);
+    return (int)cudaGetLastError();
+}
+template int mod_update<float>(const ModArgs<float>&, cudaStream_t);
+template int mod_update<double>(const ModArgs<double>&, cudaStream_t);
+
+int64_t replace_ws_bytes(int P, int64_t N, int m, int K) {
+    int64_t b = 0;
+    auto add = [&](int64_t x) { b += (x + 255) & ~int64_t(255); };
+    add(sizeof(double) * (int64_t)P * K * m);  // normalised copy
+    add(sizeof(double) * (int64_t)P * K * K);  // |Dn^T Dn|
+    add(sizeof(int8_t) * (int64_t)P * K);      // degenerate flags
+    add(sizeof(int32_t) * P);                  // targets per shard
+    add(sizeof(double) * std::max<int64_t>(N, 1));  // residual^2
+    add(sizeof(double) * std::max<int64_t>(N, 1));  // ||y||^2
+    add(sizeof(int8_t) * std::max<int64_t>(N, 1));  // taken
+    add(sizeof(int64_t) * (int64_t)P * K);     // picks
+    return b + 256;
+}
+
+template <typename T>
+int replace_degenerate(const ReplaceArgs<T>& a, cudaStream_t st) {
+    const int P = a.P, K = a.K, m = a.m, cap = a.cap;
+    const int64_t N = a.N, PK = (int64_t)P * K;
+    unsigned char* p = (unsigned char*)a.ws;
+    auto take = [&](int64_t bytes) { void* r = p; p += (bytes + 255) & ~int64_t(255); return r; };
+    double* Dn = (double*)take(sizeof(double) * PK * m);
+    double* C = (double*)take(sizeof(double) * PK * K);
+    int8_t* deg = (int8_t*)take(PK);
+    int32_t* ntarget = (int32_t*)take(sizeof(int32_t) * P);
+    double* rsq = (double*)take(sizeof(double) * std::max<int64_t>(N, 1));
+    double* ysq = (double*)take(sizeof(double) * std::max<int64_t>(N, 1));
+    int8_t* taken = (int8_t*)take(std::max<int64_t>(N, 1));
+    int64_t* pick = (int64_t*)take(sizeof(int64_t) * PK);
+
+    k_normalize_rows<<<(unsigned)((PK + 7) / 8), 256, 0, st>>>(PK, m, a.D, Dn);
+    int rc = gram_f64(Dn, P, m, K, C, st);
+    if (rc) return rc;
+    k_twins<<<P, 32, 0, st>>>(K, C, a.D, m, a.usage, deg, ntarget);
+    // residuals with the current D and the given codes (always computed; the
+    // reference skips them when no atom is degenerate, which changes nothing)
+    rc = with_mpl(m, [&](auto c) {
+        constexpr int MPL = decltype(c)::value;
+        k_resid_sq<T, MPL><<<(unsigned)((N + 7) / 8), 256, 0, st>>>(
+            N, m, K, cap, P, a.off, a.Y, a.ldy, a.idx, a.val, a.counts, a.D, rsq, ysq);
+        return (int)cudaGetLastError();
+    });
+    if (rc) return rc;
+    if (N > 0) cudaMemsetAsync(taken, 0, N, st);
+    k_replace_select<<<P, 512, 0, st>>>(K, m, a.off, rsq, ysq, deg, ntarget, taken, pick);
+    k_replace_apply<T><<<(unsigned)((PK + 7) / 8), 256, 0, st>>>(P, K, m, a.Y, a.ldy, deg, pick, ysq,
+                                                                ntarget, a.D, a.flags);
+    if (a.ntarget_out)
+        cudaMemcpyAsync(a.ntarget_out, ntarget, sizeof(int32_t) * P, cudaMemcpyDeviceToDevice, st);
+    return (int)cudaGetLastError();
+}
+template int replace_degenerate<float>(const ReplaceArgs<float>&, cudaStream_t);
+template int replace_degenerate<double>(const ReplaceArgs<double>&, cudaStream_t);
+
+template <typename T>
+int residual_sq(int64_t N, int m, int K, int cap, int P, const int64_t* off, const T* Y, int64_t ldy,
+                const int32_t* idx, const T* val, const int32_t* counts, const double* D,
+                double* rsq, double* ysq, cudaStream_t st) {
+    if (N <= 0) return 0;
+    return with_mpl(m, [&](auto c) {
+        constexpr int MPL = decltype(c)::value;
+        k_resid_sq<T, MPL><<<(unsigned)((N + 7) / 8), 256, 0, st>>>(N, m, K, cap, P, off, Y, ldy, idx,
+                                                                   val, counts, D, rsq, ysq);
+        return (int)cudaGetLastError();
+    });
+}
+template int residual_sq<float>(int64_t, int, int, int, int, const int64_t*, const float*, int64_t,
+                                const int32_t*, const float*, const int32_t*, const double*, double*,
+                                double*, cudaStream_t);
+template int residual_sq<double>(int64_t, int, int, int, int, const int64_t*, const double*, int64_t,
+                                 const int32_t*, const double*, const int32_t*, const double*, double*,
+                                 double*, cudaStream_t);
+
+int shard_sum(int P, const int64_t* off, const double* v, double* out, int do_sqrt, cudaStream_t st) {
+    k_shard_sum<<<P, 256, 0, st>>>(off, v, out, do_sqrt);
+    return (int)cudaGetLastError();
+}
+
+int usage_direct(int64_t N, int K, int cap, int P, const int64_t* off, const int32_t* idx,
+                 const int32_t* counts, int32_t* usage, cudaStream_t st) {
+    cudaMemsetAsync(usage, 0, sizeof(int32_t) * (int64_t)P * K, st);
+    if (N > 0)
+        k_usage_direct<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(N, K, cap, P, off, idx, counts, usage);
+    return (int)cudaGetLastError();
+}
+
+template <typename T>
+int code_sq(int64_t N, int cap, const T* val, const int32_t* counts, double* out, cudaStream_t st) {
+    if (N <= 0) return 0;
+    k_code_sq<T><<<(unsigned)((N + 255) / 256), 256, 0, st>>>(N, cap, val, counts, out);
+    return (int)cudaGetLastError();
+}
+template int code_sq<float>(int64_t, int, const float*, const int32_t*, double*, cudaStream_t);
+template int code_sq<double>(int64_t, int, const double*, const int32_t*, double*, cudaStream_t);
+
+template <typename T>
+int first_columns(int P, int K, int m, const int64_t* off, const T* Y, int64_t ldy, double* D,
+                  int32_t* zero_flag, cudaStream_t st) {
+    const int64_t PK = (int64_t)P * K;
+    k_first_columns<T><<<(unsigned)((PK + 7) / 8), 256, 0, st>>>(P, K, m, off, Y, ldy, D, zero_flag);
+    return (int)cudaGetLastError();
+}
+template int first_columns<float>(int, int, int, const int64_t*, const float*, int64_t, double*, int32_t*, cudaStream_t);
+template int first_columns<double>(int, int, int, const int64_t*, const double*, int64_t, double*, int32_t*, cudaStream_t);
+
+template <typename T>
+int scale_rows(int64_t rows, int group, int m, const double* D, const double* w, T* out, cudaStream_t st) {
+    const int64_t n = rows * m;
+    if (n <= 0) return 0;
+    k_scale_rows<T><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(rows, group, m, D, w, out);
+    return (int)cudaGetLastError();
+}
+template int scale_rows<float>(int64_t, int, int, const double*, const double*, float*, cudaStream_t);
+template int scale_rows<double>(int64_t, int, int, const double*, const double*, double*, cudaStream_t);
+
+}  // namespace sdb

@@ -1,0 +1,84 @@
+// MOD / replacement launch interface (internal).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sdb {
+
+struct ModWs {
+    int64_t* cf;
+    int32_t* chunk_hist;
+    int64_t* chunk_off;
+    int64_t* bucket_off;
+    int64_t* scan_ws;
+    int32_t* bsig;
+    double* bval;
+    double* A;
+    double* B;
+    double* rsq;
+    int64_t* nnz;
+    int32_t* deficient;
+    int8_t* depmask;
+    unsigned char* end;
+};
+
+template <typename T>
+struct ModArgs {
+    int P, m, K, cap;
+    int64_t N;
+    const int64_t* off;
+    const T* Y;
+    int64_t ldy;
+    const int32_t* idx;
+    const T* val;
+    const int32_t* counts;
+    const double* Dprev;   // P x K x m
+    double* Dout;          // P x K x m
+    double* scales;        // P x K
+    int32_t* usage;        // P x K
+    int8_t* dead;          // P x K
+    double* resid_fro;     // P
+    int32_t* rank;         // P
+    int32_t* deficient_out;  // P (optional)
+    int64_t* nnz_out;        // P (optional)
+    double rank_rcond;
+    void* ws;
+};
+
+template <typename T>
+struct ReplaceArgs {
+    int P, m, K, cap;
+    int64_t N;
+    const int64_t* off;
+    const T* Y;
+    int64_t ldy;
+    const int32_t* idx;
+    const T* val;
+    const int32_t* counts;
+    const int32_t* usage;
+    double* D;             // in/out
+    int8_t* flags;         // P x K: 0 kept, 1 replaced, 2 unreplaced
+    int32_t* ntarget_out;  // P (optional)
+    void* ws;
+};
+
+int64_t mod_ws_bytes(int P, int64_t N, int m, int K, int cap);
+template <typename T> int mod_update(const ModArgs<T>& a, cudaStream_t st);
+int64_t replace_ws_bytes(int P, int64_t N, int m, int K);
+template <typename T> int replace_degenerate(const ReplaceArgs<T>& a, cudaStream_t st);
+template <typename T>
+int residual_sq(int64_t N, int m, int K, int cap, int P, const int64_t* off, const T* Y, int64_t ldy,
+                const int32_t* idx, const T* val, const int32_t* counts, const double* D,
+                double* rsq, double* ysq, cudaStream_t st);
+int shard_sum(int P, const int64_t* off, const double* v, double* out, int do_sqrt, cudaStream_t st);
+int usage_direct(int64_t N, int K, int cap, int P, const int64_t* off, const int32_t* idx,
+                 const int32_t* counts, int32_t* usage, cudaStream_t st);
+template <typename T>
+int code_sq(int64_t N, int cap, const T* val, const int32_t* counts, double* out, cudaStream_t st);
+template <typename T>
+int first_columns(int P, int K, int m, const int64_t* off, const T* Y, int64_t ldy, double* D,
+                  int32_t* zero_flag, cudaStream_t st);
+template <typename T>
+int scale_rows(int64_t rows, int group, int m, const double* D, const double* w, T* out, cudaStream_t st);
+
+}  // namespace sdb

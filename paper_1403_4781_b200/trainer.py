@@ -1,0 +1,446 @@
+"""Standard and split-and-merge dictionary training on the B200 — drop-in for
+sparsedict.trainer (/root/reference/pkg/src/sparsedict/trainer.py).
+
+The alternating loop (OMP coding, MOD update, atom replacement) is
+device-resident: Y is uploaded once, every iteration is a fixed sequence of
+stream-ordered launches with no host synchronisation, and the split phase
+trains ALL L shards in the same launches (shard-batched kernels), instead of
+the reference's process pool (trainer.py:301-305). Only the seeded host
+pieces the reference defines through numpy's RNG stay on the host: the split
+permutation (trainer.py:208-209), the seed derivation (:263-265) and the
+random fill of zero init columns (:157-161).
+
+Extensions (optional, reference-preserving defaults): ``TrainConfig.eps`` /
+``s_max`` select error-bounded coding for standard / local training
+(BASELINE configs 2-3; SURVEY.md §7 hard part 9), ``precision`` selects the
+arithmetic ("fp64" default, "fp32" fast mode).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _engine as E
+from .dictionary_update import normalize_columns
+from .exceptions import InvalidInputError
+from .metrics import mse_db_device
+from .sparse_coding import SparseCodeMatrix, codes_to_matrix
+
+__all__ = [
+    "TrainConfig",
+    "TrainReport",
+    "train_standard",
+    "split_indices",
+    "split_dataset",
+    "train_local",
+    "merge_dictionaries",
+    "train_split_merge",
+]
+
+INIT_MODES = ("first-columns", "overcomplete-dct")
+_CONFIG_FIELDS = {"K", "s", "iterations", "init", "seed", "mode", "L", "K1", "s1", "s2",
+                  "local_iterations", "merge_iterations", "eps", "s_max", "precision"}
+
+
+@dataclass
+class TrainConfig:
+    """Parameters of either training mode (trainer.py:44-111)."""
+
+    K: int
+    s: int
+    iterations: int = 100
+    init: str | np.ndarray = "first-columns"
+    seed: int = 0
+    mode: str = "standard"
+    L: int = 1
+    K1: int | None = None
+    s1: int | None = None
+    s2: int | None = None
+    local_iterations: int | None = None
+    merge_iterations: int | None = None
+    threads: int = 1
+    eps: float | None = None        # extension: error-bounded coding (standard / locals)
+    s_max: int | None = None        # extension: support cap in error-bounded mode
+    precision: str | None = None    # extension: "fp64" | "fp32"
+
+    def validate(self) -> None:
+        if self.K < 1 or self.s < 1 or self.iterations < 1:
+            raise InvalidInputError("K, s, iterations must be positive")
+        if isinstance(self.init, str):
+            if self.init not in INIT_MODES:
+                raise InvalidInputError(f"unknown init mode {self.init!r}")
+        else:
+            M = np.asarray(self.init, dtype=np.float64)
+            if M.ndim != 2 or M.shape[1] != self.K:
+                raise InvalidInputError("explicit init must be an (m, K) matrix")
+        if self.eps is not None:
+            e = float(self.eps)
+            if e < 0 or not np.isfinite(e):
+                raise InvalidInputError("eps must be a finite nonnegative real")
+            if self.s_max is not None and int(self.s_max) < 1:
+                raise InvalidInputError("s_max must be positive")
+        if self.precision is not None:
+            E.get_precision(self.precision)
+        if self.mode == "standard":
+            return
+        if self.mode != "split-merge":
+            raise InvalidInputError(f"unknown mode {self.mode!r}")
+        if self.L < 1:
+            raise InvalidInputError("L must be >= 1")
+        if self.K1 is None or self.s1 is None or self.s2 is None:
+            raise InvalidInputError("split-merge mode requires K1, s1 and s2")
+        if self.s1 * self.s2 != self.s:
+            raise InvalidInputError(
+                f"sparsity levels must compose: s1*s2 = {self.s1}*{self.s2} != s = {self.s}")
+        if self.K1 > self.K:
+            raise InvalidInputError("K1 must not exceed K")
+
+    @classmethod
+    def from_dict(cls, d: dict) -> "TrainConfig":
+        unknown = set(d) - _CONFIG_FIELDS
+        if unknown:
+            raise InvalidInputError(f"unknown config fields: {sorted(unknown)}")
+        cfg = cls(**d)
+        cfg.validate()
+        return cfg
+
+    def to_dict(self) -> dict:
+        d = {"K": self.K, "s": self.s, "iterations": self.iterations, "seed": self.seed,
+             "mode": self.mode,
+             "init": self.init if isinstance(self.init, str) else "explicit-matrix"}
+        if self.mode == "split-merge":
+            d.update(L=self.L, K1=self.K1, s1=self.s1, s2=self.s2,
+                     local_iterations=self.local_iterations,
+                     merge_iterations=self.merge_iterations)
+        for k in ("eps", "s_max", "precision"):
+            if getattr(self, k) is not None:
+                d[k] = getattr(self, k)
+        return d
+
+
+@dataclass
+class TrainReport:
+    """Timing and quality summary (trainer.py:114-135)."""
+
+    final_mse_db: float
+    per_iteration_residuals: list[float] = field(default_factory=list)
+    wall_time_s: float = 0.0
+    split_time_s: float = 0.0
+    local_wall_times_s: list[float] = field(default_factory=list)
+    merge_wall_time_s: float = 0.0
+    critical_path_s: float = 0.0
+
+    def to_dict(self) -> dict:
+        return {
+            "final_mse_db": self.final_mse_db,
+            "per_iteration_residuals": list(self.per_iteration_residuals),
+            "wall_time_s": self.wall_time_s,
+            "split_time_s": self.split_time_s,
+            "local_wall_times_s": list(self.local_wall_times_s),
+            "merge_wall_time_s": self.merge_wall_time_s,
+            "critical_path_s": self.critical_path_s,
+        }
+
+
+# ============================================================ device engine
+def _zero_fill(D: torch.Tensor, zero_flags: np.ndarray, seeds) -> None:
+    """Seeded N(0,1) atoms for zero init columns (trainer.py:156-161); the
+    columns come from numpy's PCG64 so they match the reference exactly."""
+    P, K, m = D.shape
+    for p in range(P):
+        z = np.flatnonzero(zero_flags[p])
+        if z.size == 0:
+            continue
+        rng = np.random.default_rng(np.random.SeedSequence(int(seeds[p])).spawn(1)[0])
+        fill = rng.standard_normal((m, z.size))
+        cols = torch.from_numpy(np.ascontiguousarray((fill / np.linalg.norm(fill, axis=0)).T))
+        D[p, torch.from_numpy(z)] = cols.to(D.device)
+
+
+def init_dictionaries(S: E.ShardSet, K: int, init, seeds) -> torch.Tensor:
+    """_init_dictionary (trainer.py:138-162) for every shard: (P, K, m) f64."""
+    m = S.m
+    if isinstance(init, str) and init == "first-columns":
+        if min(S.sizes) < K:
+            raise InvalidInputError("first-columns init needs N >= K")
+        D, zf = E.first_columns(S, K)
+        zfh = E.d2h(zf)
+        if zfh.any():
+            _zero_fill(D, zfh, seeds)
+        return D
+    if isinstance(init, str):  # overcomplete-dct
+        from .denoising import overcomplete_dct
+        p = int(round(np.sqrt(m)))
+        if p * p != m:
+            raise InvalidInputError("overcomplete-dct init needs a square patch dimension")
+        D0 = overcomplete_dct(p, K)
+    else:
+        D0 = np.asarray(init, dtype=np.float64)
+        if D0.shape != (m, K):
+            raise InvalidInputError("explicit init has wrong shape")
+        D0, _ = normalize_columns(D0)
+    D = E.dict_to_device(D0).repeat(S.P, 1, 1).contiguous()
+    zero = (np.linalg.norm(D0, axis=0) == 0)
+    if zero.any():
+        _zero_fill(D, np.tile(zero, (S.P, 1)), seeds)
+    return D
+
+
+def coding_mode(m: int, K: int, s: int, eps, s_max) -> tuple[int, float]:
+    """(cap, eps) for the training loop (fixed s unless eps is given)."""
+    if eps is None:
+        if not 1 <= s <= min(m, K):
+            raise InvalidInputError("sparsity must satisfy 1 <= s <= min(m, K)")
+        return int(s), 0.0
+    cap = int(s_max) if s_max is not None else m
+    if not 1 <= cap <= m:
+        raise InvalidInputError("s_max must satisfy 1 <= s_max <= m")
+    return cap, float(eps)
+
+
+def train_device(S: E.ShardSet, D0: torch.Tensor, cap: int, eps: float, iterations: int,
+                 use_tc: bool = True):
+    """The alternating loop (trainer.py:183-188) on every shard at once.
+
+    Returns (D (P,K,m) f64, final codes, residuals (iterations, P) f64 device).
+    Stream-ordered; nothing here synchronises with the host.
+    """
+    prec = S.prec
+    D = D0
+    P = D.shape[0]
+    resid = E.empty((iterations, P), torch.float64)
+    for it in range(iterations):
+        DT = E.working_dict(D, prec)
+        G = E.gram(D, prec)
+        codes = E.code(S.Y, S.off, S.max_rows, DT, G, cap, eps, prec, use_tc)
+        r = E.mod_update(S, codes, D)
+        resid[it].copy_(r.resid)
+        E.replace_degenerate(S, codes, r.D, r.usage)
+        D = r.D
+    codes = E.code(S.Y, S.off, S.max_rows, E.working_dict(D, prec), E.gram(D, prec), cap, eps,
+                   prec, use_tc)
+    return D, codes, resid
+
+
+def _check_Y(Y) -> np.ndarray:
+    Y = np.asarray(Y, dtype=np.float64)
+    if Y.ndim != 2 or Y.shape[0] < 1:
+        raise InvalidInputError("Y must be a nonempty m x N matrix")
+    if Y.shape[0] > 256:
+        raise InvalidInputError("signal dimension m > 256 is outside the GPU path")
+    return Y
+
+
+def _ingest_checked(Y, prec):
+    Ydev, bad = E.ingest_signals(Y, prec)
+    if int(bad.item()):
+        raise InvalidInputError("batch contains non-finite entries")
+    return Ydev
+
+
+def _sync():
+    torch.cuda.synchronize()
+
+
+# ============================================================ public API
+def train_standard(Y, cfg: TrainConfig) -> tuple[np.ndarray, SparseCodeMatrix, TrainReport]:
+    """Alternating OMP / MOD / replacement on the whole dataset
+    (trainer.py:165-197); returns (D, codes against the final D, report)."""
+    cfg.validate()
+    if cfg.mode != "standard":
+        raise InvalidInputError("train_standard requires mode='standard'")
+    Y = _check_Y(Y)
+    m, N = Y.shape
+    if cfg.K > E.MAX_K:
+        raise InvalidInputError(f"K={cfg.K} exceeds the GPU path's limit of {E.MAX_K}")
+    prec = E.get_precision(cfg.precision)
+    cap, eps = coding_mode(m, cfg.K, cfg.s, cfg.eps, cfg.s_max)
+    t0 = time.perf_counter()
+    S = E.ShardSet.single(_ingest_checked(Y, prec), prec)
+    D0 = init_dictionaries(S, cfg.K, cfg.init, [cfg.seed])
+    D, codes, resid = train_device(S, D0, cap, eps, cfg.iterations)
+    _sync()
+    wall = time.perf_counter() - t0
+    report = TrainReport(final_mse_db=mse_db_device(S, codes, D),
+                         per_iteration_residuals=[float(v) for v in E.d2h(resid[:, 0])],
+                         wall_time_s=wall, critical_path_s=wall)
+    return E.d2h(D[0]).T.copy(), codes_to_matrix(codes, prec), report
+
+
+def split_indices(N: int, L: int, seed: int) -> list[np.ndarray]:
+    """Seeded partition of range(N) into L blocks (trainer.py:200-217): a
+    PCG64 permutation cut into consecutive blocks, the first N mod L one longer."""
+    if L < 1 or L > N:
+        raise InvalidInputError("require 1 <= L <= N")
+    perm = np.random.default_rng(seed).permutation(N)
+    base, extra = divmod(N, L)
+    ends = np.cumsum([base + (1 if t < extra else 0) for t in range(L)])
+    return np.split(perm, ends[:-1])
+
+
+def split_dataset(Y, L: int, seed: int) -> list[np.ndarray]:
+    """Column shards of Y (trainer.py:220-223)."""
+    Y = np.asarray(Y, dtype=np.float64)
+    return [Y[:, ids] for ids in split_indices(Y.shape[1], L, seed)]
+
+
+def train_local(Y_t, K1: int, s1: int, iterations: int, seed: int,
+                init: str | np.ndarray = "first-columns", threads: int = 1,
+                precision: str | None = None, eps: float | None = None,
+                s_max: int | None = None) -> tuple[np.ndarray, SparseCodeMatrix]:
+    """One local dictionary: train_standard with (K1, s1) (trainer.py:226-233)."""
+    cfg = TrainConfig(K=K1, s=s1, iterations=iterations, init=init, seed=seed, threads=threads,
+                      precision=precision, eps=eps, s_max=s_max)
+    D, X, _ = train_standard(Y_t, cfg)
+    return D, X
+
+
+def _merge_weights(local_results, prec) -> list[float]:
+    """w_t = ||X_t||_F (trainer.py:250-251) as device reductions."""
+    ws = []
+    for _D, X_t in local_results:
+        data = X_t.data if isinstance(X_t, SparseCodeMatrix) else np.asarray(X_t).reshape(-1)
+        data = np.ascontiguousarray(data, dtype=np.float64)
+        if data.size == 0:
+            ws.append(0.0)
+            continue
+        v = torch.from_numpy(data).to(E.device())
+        n = data.size
+        off, _ = E.shard_offsets([n])
+        e = E.empty((n,), torch.float64)
+        counts = torch.ones((n,), dtype=torch.int32, device=E.device())
+        E._lib.call("sdb_code_energy", E.SDB_F64, n, 1, E.ptr(v), E.ptr(counts), E.ptr(e), E.stream())
+        out = E.empty((1,), torch.float64)
+        E._lib.call("sdb_shard_sum", 1, E.ptr(off), E.ptr(e), E.ptr(out), 1, E.stream())
+        ws.append(float(out.item()))
+    return ws
+
+
+def merge_dictionaries(local_results: list, K: int, s2: int, merge_iterations: int, seed: int,
+                       init: str | np.ndarray = "first-columns", threads: int = 1,
+                       precision: str | None = None) -> np.ndarray:
+    """Global dictionary from the scaled local atoms (trainer.py:236-260)."""
+    if not local_results:
+        raise InvalidInputError("empty list of local dictionaries")
+    prec = E.get_precision(precision)
+    ws = _merge_weights(local_results, prec)
+    keep = [t for t, w in enumerate(ws) if w > 0.0]
+    if not keep:
+        raise InvalidInputError("all local code matrices are zero")
+    Dl = torch.stack([E.dict_to_device(np.asarray(local_results[t][0], dtype=np.float64))[0]
+                      for t in keep])
+    w = torch.tensor([ws[t] for t in keep], dtype=torch.float64, device=E.device())
+    Ym = E.scale_rows(Dl.contiguous(), w, Dl.shape[1], prec)
+    return _train_merge(Ym, K, s2, merge_iterations, seed, init, prec)[0]
+
+
+def _train_merge(Ym: torch.Tensor, K: int, s2: int, iters: int, seed: int, init, prec: str):
+    m = Ym.shape[1]
+    cfg = TrainConfig(K=K, s=s2, iterations=iters, init=init, seed=seed)
+    cfg.validate()
+    cap, eps = coding_mode(m, K, s2, None, None)
+    S = E.ShardSet.single(Ym, prec)
+    D0 = init_dictionaries(S, K, init, [seed])
+    D, codes, _ = train_device(S, D0, cap, eps, iters)
+    return E.d2h(D[0]).T.copy(), D, codes
+
+
+def _derive_seeds(seed: int, count: int) -> list[int]:
+    """trainer.py:263-265."""
+    return [int(c.generate_state(1, np.uint64)[0])
+            for c in np.random.SeedSequence(seed).spawn(count)]
+
+
+@dataclass
+class SplitMergeResult:
+    D: np.ndarray
+    D_dev: torch.Tensor            # (1, K, m) f64
+    local_D: torch.Tensor          # (L, K1, m) f64
+    weights: np.ndarray            # (L,)
+    split_s: float
+    local_s: float
+    merge_s: float
+    wall_s: float
+    codings: int                   # OMP signal-codings performed
+
+
+def split_merge_device(Ydev: torch.Tensor, L: int, K1: int, local_cap: int, local_eps: float,
+                       local_iters: int, K: int, s2: int, merge_iters: int, seed: int,
+                       init="first-columns", prec: str = "fp64", use_tc: bool = True,
+                       t_start: float | None = None) -> SplitMergeResult:
+    """split_dataset -> all locals in one batched loop -> merge (trainer.py:
+    291-313). ``Ydev`` is (N, m) device, signal-major."""
+    if t_start is None:
+        _sync()
+        t_start = time.perf_counter()
+    N, m = Ydev.shape
+    blocks = split_indices(N, L, seed)
+    sizes = [b.size for b in blocks]
+    perm = torch.from_numpy(np.concatenate(blocks).astype(np.int64)).to(E.device())
+    Ys = E.gather_rows(Ydev, perm, prec)
+    off, _ = E.shard_offsets(sizes)
+    S = E.ShardSet(Ys, off, sizes, prec)
+    _sync()
+    t_split = time.perf_counter()
+    seeds = _derive_seeds(seed, L + 1)
+    if min(sizes) < K1:
+        raise InvalidInputError("first-columns init needs N >= K")
+    D0 = init_dictionaries(S, K1, "first-columns", seeds[:L])
+    Dl, codes, _ = train_device(S, D0, local_cap, local_eps, local_iters, use_tc)
+    w = E.code_energy(S, codes)
+    w_h = E.d2h(w)                       # synchronises: end of the split phase
+    t_local = time.perf_counter()
+    keep = np.flatnonzero(w_h > 0.0)
+    if keep.size == 0:
+        raise InvalidInputError("all local code matrices are zero")
+    if keep.size < L:
+        kt = torch.from_numpy(keep).to(E.device())
+        Dk, wk = Dl.index_select(0, kt).contiguous(), w.index_select(0, kt).contiguous()
+    else:
+        Dk, wk = Dl, w
+    Ym = E.scale_rows(Dk, wk, K1, prec)
+    cap2, _ = coding_mode(m, K, s2, None, None)
+    Sm = E.ShardSet.single(Ym, prec)
+    D0m = init_dictionaries(Sm, K, init, [seeds[L]])
+    Dm, _codes_m, _ = train_device(Sm, D0m, cap2, 0.0, merge_iters, use_tc)
+    _sync()
+    t_end = time.perf_counter()
+    codings = (local_iters + 1) * N + (merge_iters + 1) * Ym.shape[0]
+    return SplitMergeResult(E.d2h(Dm[0]).T.copy(), Dm, Dl, w_h, t_split - t_start,
+                            t_local - t_split, t_end - t_local, t_end - t_start, codings)
+
+
+def train_split_merge(Y, cfg: TrainConfig) -> tuple[np.ndarray, TrainReport]:
+    """Split / all-locals-at-once / merge pipeline (trainer.py:275-326),
+    followed by the s1*s2 evaluation pass that is not counted in wall time."""
+    cfg.validate()
+    if cfg.mode != "split-merge":
+        raise InvalidInputError("train_split_merge requires mode='split-merge'")
+    Y = _check_Y(Y)
+    m, N = Y.shape
+    if max(cfg.K, cfg.K1) > E.MAX_K:
+        raise InvalidInputError(f"K exceeds the GPU path's limit of {E.MAX_K}")
+    if cfg.L > N:
+        raise InvalidInputError("require 1 <= L <= N")
+    prec = E.get_precision(cfg.precision)
+    local_iters = cfg.local_iterations or cfg.iterations
+    merge_iters = cfg.merge_iterations or cfg.iterations
+    cap1, eps1 = coding_mode(m, cfg.K1, cfg.s1, cfg.eps, cfg.s_max)
+    _sync()
+    t0 = time.perf_counter()
+    Ydev = _ingest_checked(Y, prec)
+    r = split_merge_device(Ydev, cfg.L, cfg.K1, cap1, eps1, local_iters, cfg.K, cfg.s2,
+                           merge_iters, cfg.seed, cfg.init, prec, t_start=t0)
+    # evaluation pass (trainer.py:315-319), outside wall_time_s
+    S = E.ShardSet.single(Ydev, prec)
+    cap_e, _ = coding_mode(m, cfg.K, cfg.s, None, None)
+    codes = E.code_single_dict(Ydev, r.D_dev, cap_e, 0.0, prec)
+    report = TrainReport(final_mse_db=mse_db_device(S, codes, r.D_dev), wall_time_s=r.wall_s,
+                         split_time_s=r.split_s, local_wall_times_s=[r.local_s] * cfg.L,
+                         merge_wall_time_s=r.merge_s,
+                         critical_path_s=r.split_s + r.local_s + r.merge_s)
+    return r.D, report
