@@ -54,6 +54,22 @@ def torch_dtype(p: str):
 
 _dev_checked = False
 
+# Optional per-call CUDA-event timers (bench.py roofline): name -> list of
+# (start_event, end_event, algorithmic_bytes, flops). None = disabled.
+KTIMER: dict | None = None
+
+
+def timed_call(name: str, nbytes: float, flops: float, fn, *args):
+    if KTIMER is None:
+        return _lib.call(fn, *args)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    rc = _lib.call(fn, *args)
+    e1.record()
+    KTIMER.setdefault(name, []).append((e0, e1, float(nbytes), float(flops)))
+    return rc
+
 
 def device() -> torch.device:
     """The CUDA device; raises NativeUnavailable without an sm_100 GPU."""
@@ -178,13 +194,17 @@ def code(Ydev: torch.Tensor, off: torch.Tensor, max_rows: int, DT: torch.Tensor,
     if N == 0:
         return out
     alpha = empty((N, K), tdt)
-    _lib.call("sdb_correlate", dt, N, m, K, P, ptr(off), max_rows, ptr(Ydev), m, ptr(DT),
-              ptr(alpha), K, int(use_tc), stream())
+    es = 8 if prec == "fp64" else 4
+    timed_call("correlate", N * (m + K) * es, 2.0 * N * m * K,
+               "sdb_correlate", dt, N, m, K, P, ptr(off), max_rows, ptr(Ydev), m, ptr(DT),
+               ptr(alpha), K, int(use_tc), stream())
     sb = _lib.load().sdb_omp_scratch_bytes(dt, N, m, cap)
     scratch = empty((max(sb, 1),), torch.uint8) if sb > 0 else None
-    _lib.call("sdb_omp", dt, N, m, K, P, ptr(off), ptr(alpha), K, ptr(Ydev), m, ptr(DT), ptr(G),
-              cap, float(eps), GUARD[prec], ptr(out.idx), ptr(out.val), ptr(out.counts),
-              ptr(out.status), ptr(out.rnorm), ptr(scratch), int(sb), stream())
+    # algorithmic HBM bytes per signal: alpha0 row + y + code row (idx+val) + count/status/rnorm
+    timed_call("omp", N * (K * es + m * es + cap * (4 + es) + 5 + es), 0.0,
+               "sdb_omp", dt, N, m, K, P, ptr(off), ptr(alpha), K, ptr(Ydev), m, ptr(DT), ptr(G),
+               cap, float(eps), GUARD[prec], ptr(out.idx), ptr(out.val), ptr(out.counts),
+               ptr(out.status), ptr(out.rnorm), ptr(scratch), int(sb), stream())
     return out
 
 
@@ -283,7 +303,8 @@ def mod_update(S: ShardSet, codes: DeviceCodes, D64: torch.Tensor) -> ModResult:
                   empty((P,), torch.float64), empty((P,), torch.int32), empty((P,), torch.int32))
     wsb = _lib.load().sdb_mod_workspace_bytes(P, S.N, m, K, codes.cap)
     ws = empty((wsb,), torch.uint8)
-    _lib.call("sdb_mod_update", dt, P, S.N, m, K, codes.cap, ptr(S.off), ptr(S.Y), m,
+    es = 8 if S.prec == "fp64" else 4
+    timed_call("mod_update", S.N * (2 * m * es + codes.cap * (4 + es) + 4), 0.0, "sdb_mod_update", dt, P, S.N, m, K, codes.cap, ptr(S.off), ptr(S.Y), m,
               ptr(codes.idx), ptr(codes.val), ptr(codes.counts), ptr(D64), ptr(r.D),
               ptr(r.scales), ptr(r.usage), ptr(r.dead), ptr(r.resid), ptr(r.rank),
               ptr(r.deficient), RANK_RCOND, ptr(ws), wsb, stream())
@@ -297,7 +318,8 @@ def replace_degenerate(S: ShardSet, codes: DeviceCodes, D64: torch.Tensor, usage
     ntarget = empty((P,), torch.int32)
     wsb = _lib.load().sdb_replace_workspace_bytes(P, S.N, m, K)
     ws = empty((wsb,), torch.uint8)
-    _lib.call("sdb_replace_degenerate", sdb_dtype(S.prec), P, S.N, m, K, codes.cap, ptr(S.off),
+    es = 8 if S.prec == "fp64" else 4
+    timed_call("replace", S.N * (m * es + codes.cap * (4 + es) + 4), 0.0, "sdb_replace_degenerate", sdb_dtype(S.prec), P, S.N, m, K, codes.cap, ptr(S.off),
               ptr(S.Y), m, ptr(codes.idx), ptr(codes.val), ptr(codes.counts), ptr(usage),
               ptr(D64), ptr(flags), ptr(ntarget), ptr(ws), wsb, stream())
     return flags, ntarget

@@ -414,9 +414,10 @@ def split_merge_device(Ydev: torch.Tensor, L: int, K1: int, local_cap: int, loca
                             t_local - t_split, t_end - t_local, t_end - t_start, codings)
 
 
-def train_split_merge(Y, cfg: TrainConfig) -> tuple[np.ndarray, TrainReport]:
+def train_split_merge(Y, cfg: TrainConfig, evaluate: bool = True) -> tuple[np.ndarray, TrainReport]:
     """Split / all-locals-at-once / merge pipeline (trainer.py:275-326),
-    followed by the s1*s2 evaluation pass that is not counted in wall time."""
+    followed by the s1*s2 evaluation pass that is not counted in wall time
+    (``evaluate=False``, an extension, skips it: final_mse_db is then nan)."""
     cfg.validate()
     if cfg.mode != "split-merge":
         raise InvalidInputError("train_split_merge requires mode='split-merge'")
@@ -436,10 +437,13 @@ def train_split_merge(Y, cfg: TrainConfig) -> tuple[np.ndarray, TrainReport]:
     r = split_merge_device(Ydev, cfg.L, cfg.K1, cap1, eps1, local_iters, cfg.K, cfg.s2,
                            merge_iters, cfg.seed, cfg.init, prec, t_start=t0)
     # evaluation pass (trainer.py:315-319), outside wall_time_s
-    S = E.ShardSet.single(Ydev, prec)
-    cap_e, _ = coding_mode(m, cfg.K, cfg.s, None, None)
-    codes = E.code_single_dict(Ydev, r.D_dev, cap_e, 0.0, prec)
-    report = TrainReport(final_mse_db=mse_db_device(S, codes, r.D_dev), wall_time_s=r.wall_s,
+    mse = float("nan")
+    if evaluate:
+        S = E.ShardSet.single(Ydev, prec)
+        cap_e, _ = coding_mode(m, cfg.K, cfg.s, None, None)
+        codes = E.code_single_dict(Ydev, r.D_dev, cap_e, 0.0, prec)
+        mse = mse_db_device(S, codes, r.D_dev)
+    report = TrainReport(final_mse_db=mse, wall_time_s=r.wall_s,
                          split_time_s=r.split_s, local_wall_times_s=[r.local_s] * cfg.L,
                          merge_wall_time_s=r.merge_s,
                          critical_path_s=r.split_s + r.local_s + r.merge_s)
