@@ -1,0 +1,369 @@
+// Shard-batched FP64 blocked Cholesky solve of the MOD normal equations
+// A Z = B (A = X X^T, K x K; B = (Y X^T)^T, K x m), replacing
+// numpy.linalg.lstsq in dictionary_update.py:100.
+//
+// Right-looking, 64-wide panels; every launch covers all P shards:
+//   prep        mask unused atoms (identity rows/cols), pivot tolerance
+//   per panel j: diag   factor A_jj = L_jj L_jj^T (one CTA), T_j = L_jj^-1
+//                panel  L_ij = A_ij T_j^T (i > j), W_j = T_j B_j
+//                update A_ik -= L_ij L_kj^T (lower tiles), B_i -= L_ij W_j
+//   per panel j (descending): Z_j = T_j^T W_j ; W_i -= L_ji^T Z_j (i < j)
+// Numerically dependent pivots (<= rcond * max used diagonal) drop their atom
+// (zero row/column of T_j), which the caller then treats as dead.
+#include "sdb_common.cuh"
+#include "sdb_internal.h"
+#include "sdb_chol.h"
+
+namespace sdb {
+
+constexpr int CB = 64;       // panel / tile width
+constexpr int CBP = CB + 1;  // padded smem row
+
+__global__ void __launch_bounds__(256)
+k_chol_prep(int K, double* __restrict__ Aall, const int32_t* __restrict__ usage,
+            double rel_tol, double* __restrict__ tol_out, int32_t* __restrict__ ndep) {
+    const int p = blockIdx.y;
+    double* A = Aall + (int64_t)p * K * K;
+    const int32_t* use = usage + (int64_t)p * K;
+    const int64_t KK = (int64_t)K * K;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < KK;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(e / K), c = (int)(e % K);
+        if (!use[r] || !use[c]) A[e] = (r == c) ? 1.0 : 0.0;
+    }
+    if (blockIdx.x == 0) {
+        __shared__ double sh[256];
+        double mx = 0.0;
+        for (int r = threadIdx.x; r < K; r += 256)
+            if (use[r]) mx = fmax(mx, A[(int64_t)r * K + r]);
+        sh[threadIdx.x] = mx;
+        __syncthreads();
+        for (int w = 128; w > 0; w >>= 1) {
+            if (threadIdx.x < w) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + w]);
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            tol_out[p] = rel_tol * sh[0];
+            ndep[p] = 0;
+        }
+    }
+}
+
+// factor the diagonal block of panel j0 and invert it (T = L^-1)
+__global__ void __launch_bounds__(256)
+k_chol_diag(int K, int j0, double* __restrict__ Aall, double* __restrict__ Tall,
+            const double* __restrict__ tol, int8_t* __restrict__ depmask, int32_t* __restrict__ ndep) {
+    extern __shared__ double csm[];
+    double (*Ls)[CBP] = reinterpret_cast<double (*)[CBP]>(csm);
+    double (*Ts)[CBP] = reinterpret_cast<double (*)[CBP]>(csm + CB * CBP);
+    __shared__ int8_t sdep[CB];
+    const int p = blockIdx.x;
+    double* A = Aall + (int64_t)p * K * K;
+    const int nb = min(CB, K - j0);
+    const int tid = threadIdx.x;
+    for (int e = tid; e < CB * CB; e += 256) {
+        const int r = e / CB, c = e % CB;
+        Ls[r][c] = (r < nb && c <= r) ? A[(int64_t)(j0 + r) * K + j0 + c] : 0.0;
+    }
+    __syncthreads();
+    const double tl = tol[p];
+    for (int c = 0; c < nb; ++c) {
+        if (tid == 0) {
+            const double d = Ls[c][c];
+            const bool dep = !(d > tl);
+            sdep[c] = dep ? 1 : 0;
+            Ls[c][c] = dep ? 1.0 : sqrt(d);
+            if (dep) ndep[p] += 1;
+        }
+        __syncthreads();
+        const bool dep = sdep[c];
+        const double lc = Ls[c][c];
+        for (int r = c + 1 + tid; r < nb; r += 256) Ls[r][c] = dep ? 0.0 : Ls[r][c] / lc;
+        __syncthreads();
+        // rank-1 update of the remaining lower triangle of the block
+        const int rem = nb - c - 1;
+        for (int e = tid; e < rem * rem; e += 256) {
+            const int r = c + 1 + e / rem, q = c + 1 + e % rem;
+            if (q <= r) Ls[r][q] -= Ls[r][c] * Ls[q][c];
+        }
+        __syncthreads();
+    }
+    // T = L^-1 (lower), one thread per column
+    if (tid < nb) {
+        const int c = tid;
+        for (int r = 0; r < nb; ++r) Ts[r][c] = 0.0;
+        if (!sdep[c]) {
+            Ts[c][c] = 1.0 / Ls[c][c];
+            for (int r = c + 1; r < nb; ++r) {
+                double s = 0.0;
+                for (int q = c; q < r; ++q) s = fma(Ls[r][q], Ts[q][c], s);
+                Ts[r][c] = sdep[r] ? 0.0 : -s / Ls[r][r];
+            }
+        }
+    }
+    __syncthreads();
+    double* T = Tall + ((int64_t)p * ((K + CB - 1) / CB) + j0 / CB) * CB * CB;
+    for (int e = tid; e < CB * CB; e += 256) {
+        const int r = e / CB, c = e % CB;
+        T[e] = Ts[r][c];
+        if (r < nb && c <= r) A[(int64_t)(j0 + r) * K + j0 + c] = Ls[r][c];
+    }
+    if (tid < nb) depmask[(int64_t)p * K + j0 + tid] = sdep[tid];
+}
+
+// blockIdx.x == 0: W_j = T_j B_j (RHS rows of the panel, all m columns)
+// blockIdx.x >= 1: rows block i: L_ij = A_ij T_j^T
+__global__ void __launch_bounds__(256)
+k_chol_panel(int K, int m, int j0, double* __restrict__ Aall, double* __restrict__ Ball,
+             const double* __restrict__ Tall) {
+    extern __shared__ double csm[];
+    double (*Ts)[CBP] = reinterpret_cast<double (*)[CBP]>(csm);
+    double (*Xs)[CBP] = reinterpret_cast<double (*)[CBP]>(csm + CB * CBP);
+    const int p = blockIdx.y;
+    const int nb = min(CB, K - j0);
+    const int tid = threadIdx.x;
+    const double* T = Tall + ((int64_t)p * ((K + CB - 1) / CB) + j0 / CB) * CB * CB;
+    for (int e = tid; e < CB * CB; e += 256) Ts[e / CB][e % CB] = T[e];
+    if (blockIdx.x == 0) {
+        double* B = Ball + (int64_t)p * K * m + (int64_t)j0 * m;
+        for (int c0 = 0; c0 < m; c0 += CB) {
+            const int nc = min(CB, m - c0);
+            __syncthreads();
+            for (int e = tid; e < CB * CB; e += 256) {
+                const int r = e / CB, c = e % CB;
+                Xs[r][c] = (r < nb && c < nc) ? B[(int64_t)r * m + c0 + c] : 0.0;
+            }
+            __syncthreads();
+            for (int e = tid; e < nb * nc; e += 256) {
+                const int r = e / nc, c = e % nc;
+                double s = 0.0;
+                for (int q = 0; q <= r; ++q) s = fma(Ts[r][q], Xs[q][c], s);
+                B[(int64_t)r * m + c0 + c] = s;
+            }
+        }
+        return;
+    }
+    const int i0 = j0 + nb + (blockIdx.x - 1) * CB;
+    if (i0 >= K) return;
+    const int ni = min(CB, K - i0);
+    double* A = Aall + (int64_t)p * K * K;
+    for (int e = tid; e < CB * CB; e += 256) {
+        const int r = e / CB, c = e % CB;
+        Xs[r][c] = (r < ni && c < nb) ? A[(int64_t)(i0 + r) * K + j0 + c] : 0.0;
+    }
+    __syncthreads();
+    for (int e = tid; e < ni * nb; e += 256) {
+        const int r = e / nb, c = e % nb;
+        double s = 0.0;
+        for (int q = 0; q <= c; ++q) s = fma(Xs[r][q], Ts[c][q], s);
+        A[(int64_t)(i0 + r) * K + j0 + c] = s;
+    }
+}
+
+// 64x64 tile update  C -= X Y^T  with X (64 x nb), Y (64 x nb) from smem;
+// each thread owns a 4x4 micro-tile (rows ty+16a, cols tx+16b).
+__device__ __forceinline__ void tile_update(double (*Xs)[CBP], double (*Ys)[CBP], int nb,
+                                            double acc[4][4]) {
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    for (int q = 0; q < nb; ++q) {
+        double xv[4], yv[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) xv[a] = Xs[ty + 16 * a][q];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) yv[b] = Ys[tx + 16 * b][q];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b] = fma(xv[a], yv[b], acc[a][b]);
+    }
+}
+
+// trailing update: blockIdx.x enumerates lower tiles (I >= J) of the trailing
+// matrix, then RHS tiles (I, column chunk).
+__global__ void __launch_bounds__(256)
+k_chol_update(int K, int m, int j0, double* __restrict__ Aall, double* __restrict__ Ball) {
+    extern __shared__ double csm[];
+    double (*Xs)[CBP] = reinterpret_cast<double (*)[CBP]>(csm);
+    double (*Ys)[CBP] = reinterpret_cast<double (*)[CBP]>(csm + CB * CBP);
+    const int p = blockIdx.y;
+    const int nb = min(CB, K - j0);
+    const int t0 = j0 + nb;
+    const int nt = (K - t0 + CB - 1) / CB;
+    const int ntri = nt * (nt + 1) / 2;
+    const int nmc = (m + CB - 1) / CB;
+    int tile = blockIdx.x;
+    if (tile >= ntri + nt * nmc) return;
+    double* A = Aall + (int64_t)p * K * K;
+    double* B = Ball + (int64_t)p * K * m;
+    const int tid = threadIdx.x;
+    const int tx = tid & 15, ty = tid >> 4;
+    if (tile < ntri) {
+        int bi = 0;
+        while ((bi + 1) * (bi + 2) / 2 <= tile) ++bi;
+        const int bj = tile - bi * (bi + 1) / 2;
+        const int r0 = t0 + bi * CB, c0 = t0 + bj * CB;
+        for (int e = tid; e < CB * CB; e += 256) {
+            const int r = e / CB, q = e % CB;
+            Xs[r][q] = (r0 + r < K && q < nb) ? A[(int64_t)(r0 + r) * K + j0 + q] : 0.0;
+            Ys[r][q] = (c0 + r < K && q < nb) ? A[(int64_t)(c0 + r) * K + j0 + q] : 0.0;
+        }
+        __syncthreads();
+        double acc[4][4];
+        tile_update(Xs, Ys, nb, acc);
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            const int gr = r0 + ty + 16 * a;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int gc = c0 + tx + 16 * b;
+                if (gr < K && gc <= gr) A[(int64_t)gr * K + gc] -= acc[a][b];
+            }
+        }
+        return;
+    }
+    tile -= ntri;
+    const int bi = tile / nmc, mc = tile % nmc;
+    const int r0 = t0 + bi * CB, c0 = mc * CB;
+    // C[r][c] (B rows r0.., cols c0..) -= sum_q L[r0+r][j0+q] * W[j0+q][c0+c]
+    for (int e = tid; e < CB * CB; e += 256) {
+        const int r = e / CB, q = e % CB;
+        Xs[r][q] = (r0 + r < K && q < nb) ? A[(int64_t)(r0 + r) * K + j0 + q] : 0.0;
+        const int qq = e / CB, c = e % CB;  // coalesced over c
+        Ys[c][qq] = (qq < nb && c0 + c < m) ? B[(int64_t)(j0 + qq) * m + c0 + c] : 0.0;
+    }
+    __syncthreads();
+    double acc[4][4];
+    tile_update(Xs, Ys, nb, acc);
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const int gr = r0 + ty + 16 * a;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int gc = c0 + tx + 16 * b;
+            if (gr < K && gc < m) B[(int64_t)gr * m + gc] -= acc[a][b];
+        }
+    }
+}
+
+// back substitution, panel j0: Z_j = T_j^T W_j (in place on B rows of panel j)
+__global__ void __launch_bounds__(256)
+k_back_diag(int K, int m, int j0, double* __restrict__ Ball, const double* __restrict__ Tall) {
+    extern __shared__ double csm[];
+    double (*Ts)[CBP] = reinterpret_cast<double (*)[CBP]>(csm);
+    double (*Ws)[CBP] = reinterpret_cast<double (*)[CBP]>(csm + CB * CBP);
+    const int p = blockIdx.x;
+    const int nb = min(CB, K - j0);
+    const int tid = threadIdx.x;
+    const double* T = Tall + ((int64_t)p * ((K + CB - 1) / CB) + j0 / CB) * CB * CB;
+    double* B = Ball + (int64_t)p * K * m + (int64_t)j0 * m;
+    for (int e = tid; e < CB * CB; e += 256) Ts[e / CB][e % CB] = T[e];
+    for (int c0 = 0; c0 < m; c0 += CB) {
+        const int nc = min(CB, m - c0);
+        __syncthreads();
+        for (int e = tid; e < CB * CB; e += 256) {
+            const int r = e / CB, c = e % CB;
+            Ws[r][c] = (r < nb && c < nc) ? B[(int64_t)r * m + c0 + c] : 0.0;
+        }
+        __syncthreads();
+        for (int e = tid; e < nb * nc; e += 256) {
+            const int r = e / nc, c = e % nc;
+            double s = 0.0;
+            for (int q = r; q < nb; ++q) s = fma(Ts[q][r], Ws[q][c], s);
+            B[(int64_t)r * m + c0 + c] = s;
+        }
+    }
+}
+
+// back substitution update: W_i -= L_ji^T Z_j for row blocks i < j
+// grid (i blocks * column chunks, P)
+__global__ void __launch_bounds__(256)
+k_back_update(int K, int m, int j0, const double* __restrict__ Aall, double* __restrict__ Ball) {
+    extern __shared__ double csm[];
+    double (*Xs)[CBP] = reinterpret_cast<double (*)[CBP]>(csm);  // Xs[r][q] = L[j0+q][i0+r]
+    double (*Ys)[CBP] = reinterpret_cast<double (*)[CBP]>(csm + CB * CBP);  // Ys[c][q] = Z[j0+q][c0+c]
+    const int p = blockIdx.y;
+    const int nb = min(CB, K - j0);
+    const int nmc = (m + CB - 1) / CB;
+    const int bi = blockIdx.x / nmc, mc = blockIdx.x % nmc;
+    const int i0 = bi * CB, c0 = mc * CB;
+    if (i0 >= j0) return;
+    const int ni = min(CB, j0 - i0);
+    const double* A = Aall + (int64_t)p * K * K;
+    double* B = Ball + (int64_t)p * K * m;
+    const int tid = threadIdx.x;
+    const int tx = tid & 15, ty = tid >> 4;
+    for (int e = tid; e < CB * CB; e += 256) {
+        const int q = e / CB, r = e % CB;  // coalesced over r (row j0+q of L)
+        Xs[r][q] = (q < nb && r < ni) ? A[(int64_t)(j0 + q) * K + i0 + r] : 0.0;
+        Ys[r][q] = (q < nb && c0 + r < m) ? B[(int64_t)(j0 + q) * m + c0 + r] : 0.0;
+    }
+    __syncthreads();
+    double acc[4][4];
+    tile_update(Xs, Ys, nb, acc);
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const int gr = i0 + ty + 16 * a;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int gc = c0 + tx + 16 * b;
+            if (gr < i0 + ni && gc < m) B[(int64_t)gr * m + gc] -= acc[a][b];
+        }
+    }
+}
+
+int64_t chol_ws_bytes(int P, int K) {
+    const int64_t nblk = (K + CB - 1) / CB;
+    return (int64_t)P * nblk * CB * CB * sizeof(double) + (int64_t)P * sizeof(double) + 512;
+}
+
+int chol_solve(int P, int K, int m, double* A, double* B, const int32_t* usage, double rel_tol,
+               int8_t* depmask, int32_t* ndep, void* ws, cudaStream_t st) {
+    double* T = (double*)ws;
+    const int64_t nblk = (K + CB - 1) / CB;
+    double* tol = T + (int64_t)P * nblk * CB * CB;
+    const int smem2 = 2 * CB * CBP * (int)sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_chol_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+        cudaFuncSetAttribute(k_chol_update, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+        cudaFuncSetAttribute(k_back_update, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+        cudaFuncSetAttribute(k_chol_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+        cudaFuncSetAttribute(k_back_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+        attr = true;
+    }
+    {
+        const int64_t KK = (int64_t)K * K;
+        dim3 g((unsigned)std::min<int64_t>(64, (KK + 255) / 256), (unsigned)P);
+        k_chol_prep<<<g, 256, 0, st>>>(K, A, usage, rel_tol, tol, ndep);
+    }
+    const int nmc = (m + CB - 1) / CB;
+    for (int j0 = 0; j0 < K; j0 += CB) {
+        const int nb = std::min(CB, K - j0);
+        k_chol_diag<<<P, 256, smem2, st>>>(K, j0, A, T, tol, depmask, ndep);
+        const int rows_below = K - j0 - nb;
+        dim3 gp((unsigned)(1 + (rows_below + CB - 1) / CB), (unsigned)P);
+        k_chol_panel<<<gp, 256, smem2, st>>>(K, m, j0, A, B, T);
+        const int nt = (rows_below + CB - 1) / CB;
+        const int tiles = nt * (nt + 1) / 2 + nt * nmc;
+        if (tiles > 0) {
+            dim3 gu((unsigned)tiles, (unsigned)P);
+            k_chol_update<<<gu, 256, smem2, st>>>(K, m, j0, A, B);
+        }
+    }
+    const int last = (int)((nblk - 1) * CB);
+    for (int j0 = last; j0 >= 0; j0 -= CB) {
+        k_back_diag<<<P, 256, smem2, st>>>(K, m, j0, B, T);
+        if (j0 > 0) {
+            const int ib = (j0 + CB - 1) / CB;
+            dim3 gb((unsigned)(ib * nmc), (unsigned)P);
+            k_back_update<<<gb, 256, smem2, st>>>(K, m, j0, A, B);
+        }
+    }
+    return (int)cudaGetLastError();
+}
+
+}  // namespace sdb

@@ -19,6 +19,7 @@
 #include "sdb_common.cuh"
 #include "sdb_internal.h"
 #include "sdb_mod.h"
+#include "sdb_chol.h"
 
 namespace sdb {
 
@@ -144,7 +145,9 @@ k_place(const int64_t* __restrict__ off, const int64_t* __restrict__ cf, int P, 
     }
 }
 
-// ---- (f) B[p][a][:] = sum over bucket (y_i * x_ai), lanes over m
+// ---- (f) B[p][a][:] = sum over bucket (y_i * x_ai), lanes over m. Bucket
+// entries are fetched 32 at a time (one per lane) and broadcast, and four
+// signal rows are loaded before they are accumulated (in bucket order).
 template <typename T, int MPL>
 __global__ void __launch_bounds__(256)
 k_yxt(int P, int K, int m, const T* __restrict__ Y, int64_t ldy, const int64_t* __restrict__ bucket_off,
@@ -156,14 +159,28 @@ k_yxt(int P, int K, int m, const T* __restrict__ Y, int64_t ldy, const int64_t* 
 #pragma unroll
     for (int q = 0; q < MPL; ++q) acc[q] = 0.0;
     const int64_t lo = bucket_off[e], hi = bucket_off[e + 1];
-    for (int64_t b = lo; b < hi; ++b) {
-        const int64_t i = bsig[b];
-        const double v = bval[b];
-        const T* y = Y + i * ldy;
+    for (int64_t b0 = lo; b0 < hi; b0 += 32) {
+        const int nbat = (int)min((int64_t)32, hi - b0);
+        const int my_sig = lane < nbat ? bsig[b0 + lane] : 0;
+        const double my_val = lane < nbat ? bval[b0 + lane] : 0.0;
+        for (int j = 0; j < nbat; j += 4) {
+            double yv[4][MPL];
+            double vv[4];
 #pragma unroll
-        for (int q = 0; q < MPL; ++q) {
-            const int r = lane + 32 * q;
-            if (r < m) acc[q] = fma((double)y[r], v, acc[q]);
+            for (int u = 0; u < 4; ++u) {
+                const int i = __shfl_sync(SDB_FULL, my_sig, j + u);
+                vv[u] = __shfl_sync(SDB_FULL, my_val, j + u);
+                const T* y = Y + (int64_t)i * ldy;
+#pragma unroll
+                for (int q = 0; q < MPL; ++q) {
+                    const int r = lane + 32 * q;
+                    yv[u][q] = (j + u < nbat && r < m) ? (double)y[r] : 0.0;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int q = 0; q < MPL; ++q) acc[q] = fma(yv[u][q], vv[u], acc[q]);
         }
     }
     double* out = B + e * m;
@@ -174,7 +191,11 @@ k_yxt(int P, int K, int m, const T* __restrict__ Y, int64_t ldy, const int64_t* 
     }
 }
 
-// ---- (g) A[p][a][:] = sum over bucket (x_ai * x_i), row accumulator in smem
+// ---- (g) A[p][a][:] = sum over bucket (x_ai * x_i), row accumulator in smem.
+// Batches of 32 bucket entries: their code rows are staged in smem with all
+// loads in flight, then applied in bucket order (deterministic).
+constexpr int XXT_CAP = 32;
+
 template <typename T>
 __global__ void __launch_bounds__(256)
 k_xxt(int P, int K, int cap, const int32_t* __restrict__ idx, const T* __restrict__ val,
@@ -183,185 +204,42 @@ k_xxt(int P, int K, int cap, const int32_t* __restrict__ idx, const T* __restric
     extern __shared__ double sh_row[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t e = (int64_t)blockIdx.x * 8 + wib;
-    if (e >= (int64_t)P * K) return;
     double* row = sh_row + (int64_t)wib * K;
+    // staging area after the 8 row accumulators: per warp 32 x XXT_CAP (idx, val)
+    int32_t* sidx = (int32_t*)(sh_row + 8 * (int64_t)K) + wib * 32 * XXT_CAP;
+    double* sval = (double*)(sh_row + 8 * (int64_t)K + 4 * 32 * XXT_CAP) + wib * 32 * XXT_CAP;
+    if (e >= (int64_t)P * K) return;
     for (int b = lane; b < K; b += 32) row[b] = 0.0;
     __syncwarp();
     const int64_t lo = bucket_off[e], hi = bucket_off[e + 1];
-    for (int64_t q = lo; q < hi; ++q) {
-        const int64_t i = bsig[q];
-        const double v = bval[q];
-        const int n = counts[i];
-        for (int t = lane; t < n; t += 32) {
-            const int b = idx[i * cap + t];
-            row[b] = fma(v, (double)val[i * cap + t], row[b]);
+    const bool staged = cap <= XXT_CAP;
+    for (int64_t q0 = lo; q0 < hi; q0 += 32) {
+        const int nbat = (int)min((int64_t)32, hi - q0);
+        const int my_sig = lane < nbat ? bsig[q0 + lane] : 0;
+        const double my_v = lane < nbat ? bval[q0 + lane] : 0.0;
+        const int my_n = lane < nbat ? counts[my_sig] : 0;
+        if (staged) {
+            // lane u stages entry u's code row (<= cap values)
+            for (int t = 0; t < my_n; ++t) {
+                sidx[lane * XXT_CAP + t] = idx[(int64_t)my_sig * cap + t];
+                sval[lane * XXT_CAP + t] = (double)val[(int64_t)my_sig * cap + t];
+            }
+            __syncwarp();
         }
-        __syncwarp();
+        for (int j = 0; j < nbat; ++j) {
+            const double v = __shfl_sync(SDB_FULL, my_v, j);
+            const int n = __shfl_sync(SDB_FULL, my_n, j);
+            const int i = __shfl_sync(SDB_FULL, my_sig, j);
+            for (int t = lane; t < n; t += 32) {
+                const int b = staged ? sidx[j * XXT_CAP + t] : idx[(int64_t)i * cap + t];
+                const double w = staged ? sval[j * XXT_CAP + t] : (double)val[(int64_t)i * cap + t];
+                row[b] = fma(v, w, row[b]);
+            }
+            __syncwarp();
+        }
     }
     double* out = A + e * K;
     for (int b = lane; b < K; b += 32) out[b] = row[b];
-}
-
-// ---- (h) masked blocked Cholesky, one CTA per shard, in place (lower), then
-// the upper triangle is overwritten with L^T for the back substitution.
-constexpr int NB = 32;
-
-__global__ void __launch_bounds__(512)
-k_cholesky(int K, double* __restrict__ Aall, const int32_t* __restrict__ usage,
-           int32_t* __restrict__ deficient, int8_t* __restrict__ depmask, double rel_tol) {
-    const int p = blockIdx.x;
-    double* A = Aall + (int64_t)p * K * K;
-    const int32_t* use = usage + (int64_t)p * K;
-    __shared__ double Ld[NB][NB + 1];
-    __shared__ double Pa[NB][NB + 1];
-    __shared__ double Pb[NB][NB + 1];
-    __shared__ double s_tol;
-    __shared__ int s_def;
-    __shared__ int8_t s_dep[NB];
-    int8_t* dm = depmask + (int64_t)p * K;
-    const int tid = threadIdx.x, nth = blockDim.x;
-
-    // mask unused atoms: row/col zero, unit diagonal (== min-norm on the used block)
-    for (int64_t e = tid; e < (int64_t)K * K; e += nth) {
-        const int r = (int)(e / K), c = (int)(e % K);
-        if (!use[r] || !use[c]) A[e] = (r == c) ? 1.0 : 0.0;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        double mx = 0.0;
-        for (int r = 0; r < K; ++r)
-            if (use[r]) mx = fmax(mx, A[(int64_t)r * K + r]);
-        s_tol = rel_tol * mx;
-        s_def = 0;
-    }
-    __syncthreads();
-    const double tol = s_tol;
-
-    for (int j0 = 0; j0 < K; j0 += NB) {
-        const int nb = min(NB, K - j0);
-        // 1. diagonal block, unblocked, by warp 0
-        if (tid < 32) {
-            for (int e = tid; e < nb * nb; e += 32) {
-                const int r = e / nb, c = e % nb;
-                Ld[r][c] = A[(int64_t)(j0 + r) * K + j0 + c];
-            }
-            __syncwarp();
-            for (int c = 0; c < nb; ++c) {
-                double d = Ld[c][c];
-                const bool dep = !(d > tol);
-                if (tid == 0) {
-                    s_dep[c] = dep ? 1 : 0;
-                    dm[j0 + c] = dep ? 1 : 0;
-                    if (dep) s_def += 1;  // numerically dependent pivot: atom dropped
-                }
-                if (dep) d = 1.0;
-                const double lc = sqrt(d);
-                __syncwarp();
-                if (tid == 0) Ld[c][c] = lc;
-                for (int r = c + 1 + tid; r < nb; r += 32) Ld[r][c] = dep ? 0.0 : Ld[r][c] / lc;
-                __syncwarp();
-                for (int r = c + 1 + tid; r < nb; r += 32)
-                    for (int q = c + 1; q <= r; ++q) Ld[r][q] -= Ld[r][c] * Ld[q][c];
-                __syncwarp();
-            }
-            for (int e = tid; e < nb * nb; e += 32) {
-                const int r = e / nb, c = e % nb;
-                if (c <= r) A[(int64_t)(j0 + r) * K + j0 + c] = Ld[r][c];
-            }
-        }
-        __syncthreads();
-        // 2. panel below: X L11^T = A21 (thread per row)
-        for (int r = j0 + nb + tid; r < K; r += nth) {
-            double* ar = A + (int64_t)r * K + j0;
-            double xr[NB];
-#pragma unroll
-            for (int c = 0; c < NB; ++c) xr[c] = (c < nb) ? ar[c] : 0.0;
-#pragma unroll
-            for (int c = 0; c < NB; ++c) {
-                if (c < nb) {
-                    double s = xr[c];
-                    for (int q = 0; q < c; ++q) s -= xr[q] * Ld[c][q];
-                    xr[c] = s_dep[c] ? 0.0 : s / Ld[c][c];
-                }
-            }
-#pragma unroll
-            for (int c = 0; c < NB; ++c)
-                if (c < nb) ar[c] = xr[c];
-        }
-        __syncthreads();
-        // 3. trailing update of the lower triangle: A22 -= L21 L21^T, 32x32 tiles
-        const int t0 = j0 + nb;
-        const int nt = (K - t0 + NB - 1) / NB;
-        for (int tile = 0; tile < nt * (nt + 1) / 2; ++tile) {
-            // tile -> (bi >= bj)
-            int bi = (int)((sqrt(8.0 * tile + 1.0) - 1.0) * 0.5);
-            while ((bi + 1) * (bi + 2) / 2 <= tile) ++bi;
-            while (bi * (bi + 1) / 2 > tile) --bi;
-            const int bj = tile - bi * (bi + 1) / 2;
-            const int r0 = t0 + bi * NB, c0 = t0 + bj * NB;
-            for (int e = tid; e < NB * NB; e += nth) {
-                const int r = e / NB, q = e % NB;
-                Pa[r][q] = (r0 + r < K && q < nb) ? A[(int64_t)(r0 + r) * K + j0 + q] : 0.0;
-                Pb[r][q] = (c0 + r < K && q < nb) ? A[(int64_t)(c0 + r) * K + j0 + q] : 0.0;
-            }
-            __syncthreads();
-            for (int e = tid; e < NB * NB; e += nth) {
-                const int r = e / NB, c = e % NB;
-                const int gr = r0 + r, gc = c0 + c;
-                if (gr < K && gc < K && gc <= gr) {
-                    double s = 0.0;
-#pragma unroll 8
-                    for (int q = 0; q < NB; ++q) s = fma(Pa[r][q], Pb[c][q], s);
-                    A[(int64_t)gr * K + gc] -= s;
-                }
-            }
-            __syncthreads();
-        }
-    }
-    // mirror: upper triangle <- L^T
-    for (int64_t e = tid; e < (int64_t)K * K; e += nth) {
-        const int r = (int)(e / K), c = (int)(e % K);
-        if (c > r) A[e] = A[(int64_t)c * K + r];
-    }
-    if (tid == 0) deficient[p] = s_def;
-}
-
-// ---- triangular solves A Z = B in place on B (K x m per shard); warp per
-// right-hand side column, lanes split each dot product (coalesced L rows).
-__global__ void __launch_bounds__(256)
-k_trsolve(int K, int m, const double* __restrict__ Lall, const int8_t* __restrict__ depmask,
-          double* __restrict__ Ball) {
-    extern __shared__ double sh_w[];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int p = blockIdx.y;
-    const int col = blockIdx.x * 8 + wib;
-    if (col >= m) return;
-    const double* L = Lall + (int64_t)p * K * K;
-    double* B = Ball + (int64_t)p * K * m;
-    double* w = sh_w + (int64_t)wib * K;
-    const int8_t* dm = depmask + (int64_t)p * K;
-    // forward: L w = b (dependent atoms: w = 0, so their solution row is 0)
-    for (int r = 0; r < K; ++r) {
-        const double* lr = L + (int64_t)r * K;
-        double s = 0.0;
-        for (int c = lane; c < r; c += 32) s = fma(lr[c], w[c], s);
-        s = warp_sum(s);
-        const double v = dm[r] ? 0.0 : (B[(int64_t)r * m + col] - s) / lr[r];
-        if (lane == 0) w[r] = v;
-        __syncwarp();
-    }
-    // back: L^T z = w  (row r of the upper triangle holds L[c][r], c > r)
-    for (int r = K - 1; r >= 0; --r) {
-        const double* ur = L + (int64_t)r * K;
-        double s = 0.0;
-        for (int c = r + 1 + lane; c < K; c += 32) s = fma(ur[c], w[c], s);
-        s = warp_sum(s);
-        const double v = (w[r] - s) / ur[r];
-        __syncwarp();
-        if (lane == 0) w[r] = v;
-        __syncwarp();
-    }
-    for (int r = lane; r < K; r += 32) B[(int64_t)r * m + col] = w[r];
 }
 
 // ---- per-signal residual ||y_i - D_p x_i||^2 (D in f64, atom-major)
@@ -370,11 +248,13 @@ __global__ void __launch_bounds__(256)
 k_resid_sq(int64_t N, int m, int K, int cap, int P, const int64_t* __restrict__ off,
            const T* __restrict__ Y, int64_t ldy, const int32_t* __restrict__ idx,
            const T* __restrict__ val, const int32_t* __restrict__ counts,
-           const double* __restrict__ D, double* __restrict__ out, double* __restrict__ ysq_out) {
+           const double* __restrict__ D, double* __restrict__ out, double* __restrict__ ysq_out,
+           const int32_t* __restrict__ only_if) {
     const int lane = threadIdx.x & 31;
     const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     if (i >= N) return;
     const int p = shard_of(off, P, i);
+    if (only_if && only_if[p] == 0) return;  // replacement: shard has no target
     const double* Dp = D + (int64_t)p * K * m;
     const T* y = Y + i * ldy;
     double r[MPL];
@@ -476,32 +356,52 @@ k_mod_finish(int P, int K, int m, const double* __restrict__ Z, const double* __
 }
 
 // ---- replace_degenerate_atoms (dictionary_update.py:134-176)
-// twins + target marking, warp per shard, rows processed in order
-__global__ void __launch_bounds__(32)
+// degenerate flags + twins, one CTA per shard: norms and "row has a twin"
+// flags in parallel, then the order-dependent rule (the lower index of a pair
+// is kept unless itself degenerate) sequentially over the rows with twins only.
+__global__ void __launch_bounds__(256)
 k_twins(int K, const double* __restrict__ C, const double* __restrict__ D, int m,
         const int32_t* __restrict__ usage, int8_t* __restrict__ deg, int32_t* __restrict__ ntarget) {
-    const int p = blockIdx.x, lane = threadIdx.x;
+    extern __shared__ int8_t sh_flags[];
+    int8_t* dg = sh_flags;          // K
+    int8_t* tw = sh_flags + K;      // K
+    __shared__ int s_cnt;
+    const int p = blockIdx.x;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const double* Cp = C + (int64_t)p * K * K;
-    int8_t* dg = deg + (int64_t)p * K;
-    for (int a = lane; a < K; a += 32) {
-        double s = 0.0;
+    for (int a = wib; a < K; a += 8) {
         const double* d = D + ((int64_t)p * K + a) * m;
-        for (int r = 0; r < m; ++r) s = fma(d[r], d[r], s);
-        dg[a] = (usage[(int64_t)p * K + a] == 0 || sqrt(s) <= 1e-12) ? 1 : 0;
+        double s = 0.0;
+        for (int r = lane; r < m; r += 32) s = fma(d[r], d[r], s);
+        s = warp_sum(s);
+        const double* ci = Cp + (int64_t)a * K;
+        bool any = false;
+        for (int j = a + 1 + lane; j < K; j += 32) any |= fabs(ci[j]) > 0.999;
+        any = __any_sync(SDB_FULL, any);
+        if (lane == 0) {
+            dg[a] = (usage[(int64_t)p * K + a] == 0 || sqrt(s) <= 1e-12) ? 1 : 0;
+            tw[a] = any ? 1 : 0;
+        }
     }
-    __syncwarp();
-    for (int i = 0; i < K; ++i) {
-        __syncwarp();
-        if (dg[i]) continue;  // warp-uniform
-        const double* ci = Cp + (int64_t)i * K;
-        for (int j = i + 1 + lane; j < K; j += 32)
-            if (fabs(ci[j]) > 0.999) dg[j] = 1;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < K; ++i) {
+            if (!tw[i] || dg[i]) continue;
+            const double* ci = Cp + (int64_t)i * K;
+            for (int j = i + 1; j < K; ++j)
+                if (fabs(ci[j]) > 0.999) dg[j] = 1;
+        }
+        s_cnt = 0;
     }
-    __syncwarp();
+    __syncthreads();
     int cnt = 0;
-    for (int a = lane; a < K; a += 32) cnt += dg[a];
-    cnt = (int)warp_sum((double)cnt);
-    if (lane == 0) ntarget[p] = cnt;
+    for (int a = threadIdx.x; a < K; a += 256) {
+        deg[(int64_t)p * K + a] = dg[a];
+        cnt += dg[a];
+    }
+    atomicAdd(&s_cnt, cnt);
+    __syncthreads();
+    if (threadIdx.x == 0) ntarget[p] = s_cnt;
 }
 
 // normalised copy Dn = D / ||D|| (columns with zero norm untouched)
@@ -685,6 +585,7 @@ ModWs carve_mod_ws(void* base, int P, int64_t N, int m, int K, int cap) {
     w.nnz = (int64_t*)take(sizeof(int64_t) * P);
     w.deficient = (int32_t*)take(sizeof(int32_t) * P);
     w.depmask = (int8_t*)take((int64_t)P * K);
+    w.chol = take(chol_ws_bytes(P, K));
     w.end = p;
     return w;
 }
@@ -725,27 +626,21 @@ int mod_update(const ModArgs<T>& a, cudaStream_t st) {
     });
     if (rc) return rc;
     {
-        const int smem = 8 * K * (int)sizeof(double);
+        const int smem = 8 * K * (int)sizeof(double) + 8 * 32 * XXT_CAP * (4 + 8);
         if (smem > 48 * 1024)
             cudaFuncSetAttribute(k_xxt<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         k_xxt<T><<<(unsigned)((PK + 7) / 8), 256, smem, st>>>(P, K, cap, a.idx, a.val, a.counts,
                                                              w.bucket_off, w.bsig, w.bval, w.A);
     }
-    k_cholesky<<<P, 512, 0, st>>>(K, w.A, a.usage, w.deficient, w.depmask, a.rank_rcond);
-    {
-        // masked RHS rows for unused atoms are irrelevant: A is identity there
-        // and B holds zeros (their buckets are empty).
-        const int smem = 8 * K * (int)sizeof(double);
-        if (smem > 48 * 1024)
-            cudaFuncSetAttribute(k_trsolve, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        dim3 g((unsigned)((m + 7) / 8), (unsigned)P);
-        k_trsolve<<<g, 256, smem, st>>>(K, m, w.A, w.depmask, w.B);
-    }
+    // masked RHS rows of unused atoms are irrelevant: A is the identity there
+    // and B holds zeros (their buckets are empty).
+    rc = chol_solve(P, K, m, w.A, w.B, a.usage, a.rank_rcond, w.depmask, w.deficient, w.chol, st);
+    if (rc) return rc;
     // residual before normalisation with the raw solution Z (= B now)
     rc = with_mpl(m, [&](auto c) {
         constexpr int MPL = decltype(c)::value;
         k_resid_sq<T, MPL><<<(unsigned)((N + 7) / 8), 256, 0, st>>>(
-            N, m, K, cap, P, a.off, a.Y, a.ldy, a.idx, a.val, a.counts, w.B, w.rsq, nullptr);
+            N, m, K, cap, P, a.off, a.Y, a.ldy, a.idx, a.val, a.counts, w.B, w.rsq, nullptr, nullptr);
         return (int)cudaGetLastError();
     });
     if (rc) return rc;
@@ -794,13 +689,13 @@ int replace_degenerate(const ReplaceArgs<T>& a, cudaStream_t st) {
     k_normalize_rows<<<(unsigned)((PK + 7) / 8), 256, 0, st>>>(PK, m, a.D, Dn);
     int rc = gram_f64(Dn, P, m, K, C, st);
     if (rc) return rc;
-    k_twins<<<P, 32, 0, st>>>(K, C, a.D, m, a.usage, deg, ntarget);
+    k_twins<<<P, 256, 2 * K, st>>>(K, C, a.D, m, a.usage, deg, ntarget);
     // residuals with the current D and the given codes (always computed; the
     // reference skips them when no atom is degenerate, which changes nothing)
     rc = with_mpl(m, [&](auto c) {
         constexpr int MPL = decltype(c)::value;
         k_resid_sq<T, MPL><<<(unsigned)((N + 7) / 8), 256, 0, st>>>(
-            N, m, K, cap, P, a.off, a.Y, a.ldy, a.idx, a.val, a.counts, a.D, rsq, ysq);
+            N, m, K, cap, P, a.off, a.Y, a.ldy, a.idx, a.val, a.counts, a.D, rsq, ysq, ntarget);
         return (int)cudaGetLastError();
     });
     if (rc) return rc;
@@ -823,7 +718,7 @@ int residual_sq(int64_t N, int m, int K, int cap, int P, const int64_t* off, con
     return with_mpl(m, [&](auto c) {
         constexpr int MPL = decltype(c)::value;
         k_resid_sq<T, MPL><<<(unsigned)((N + 7) / 8), 256, 0, st>>>(N, m, K, cap, P, off, Y, ldy, idx,
-                                                                   val, counts, D, rsq, ysq);
+                                                                   val, counts, D, rsq, ysq, nullptr);
         return (int)cudaGetLastError();
     });
 }

@@ -19,6 +19,7 @@ struct ModWs {
     int64_t* nnz;
     int32_t* deficient;
     int8_t* depmask;
+    void* chol;
     unsigned char* end;
 };
 
