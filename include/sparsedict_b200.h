@@ -66,10 +66,12 @@ int sdb_gram(int dtype, int64_t P, int64_t m, int64_t K, const double *D64, void
 /* alpha0[i, j] = <d_j, y_i> with d from the shard of i: the c0 = D^T y loop of
  * omp_single (_kernels.py:54-59) for every signal at once. F64: bitwise
  * identical sequential sums. F32: tcgen05 3xTF32 GEMM when use_tc != 0 and the
- * shape is supported, FP32 SIMT otherwise. max_shard_rows = max shard size. */
+ * shape is supported, FP32 SIMT otherwise. max_shard_rows = max shard size.
+ * ws: sdb_correlate_workspace_bytes() (pre-split D_hi/D_lo for 3xTF32). */
+int64_t sdb_correlate_workspace_bytes(int dtype, int64_t P, int64_t m, int64_t K);
 int sdb_correlate(int dtype, int64_t N, int64_t m, int64_t K, int64_t P, const int64_t *shard_off,
                   int64_t max_shard_rows, const void *Y, int64_t ldy, const void *D, void *alpha0,
-                  int64_t lda, int use_tc, void *stream);
+                  int64_t lda, int use_tc, void *ws, int64_t ws_bytes, void *stream);
 
 /* Batch OMP: _kernels.omp_batch_range (_kernels.py:161-173) over all N
  * signals, i.e. omp_single (:38-158) per signal: greedy selection with the

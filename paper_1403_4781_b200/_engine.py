@@ -195,9 +195,11 @@ def code(Ydev: torch.Tensor, off: torch.Tensor, max_rows: int, DT: torch.Tensor,
         return out
     alpha = empty((N, K), tdt)
     es = 8 if prec == "fp64" else 4
+    cwb = _lib.load().sdb_correlate_workspace_bytes(dt, P, m, K) if use_tc else 0
+    cws = empty((cwb,), torch.uint8) if cwb > 0 else None
     timed_call("correlate", N * (m + K) * es, 2.0 * N * m * K,
                "sdb_correlate", dt, N, m, K, P, ptr(off), max_rows, ptr(Ydev), m, ptr(DT),
-               ptr(alpha), K, int(use_tc), stream())
+               ptr(alpha), K, int(use_tc), ptr(cws), int(cwb), stream())
     sb = _lib.load().sdb_omp_scratch_bytes(dt, N, m, cap)
     scratch = empty((max(sb, 1),), torch.uint8) if sb > 0 else None
     # algorithmic HBM bytes per signal: alpha0 row + y + code row (idx+val) + count/status/rnorm

@@ -29,8 +29,9 @@ SIGNATURES = {
     "sdb_ingest": (c_int, [c_int, c_i64, c_i64, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp]),
     "sdb_cast": (c_int, [c_int, c_i64, c_vp, c_vp, c_vp]),
     "sdb_gram": (c_int, [c_int, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
+    "sdb_correlate_workspace_bytes": (c_i64, [c_int, c_i64, c_i64, c_i64]),
     "sdb_correlate": (c_int, [c_int, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp,
-                              c_vp, c_i64, c_int, c_vp]),
+                              c_vp, c_i64, c_int, c_vp, c_i64, c_vp]),
     "sdb_omp_scratch_bytes": (c_i64, [c_int, c_i64, c_i64, c_i64]),
     "sdb_omp": (c_int, [c_int, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp,
                         c_vp, c_i64, c_dbl, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64,

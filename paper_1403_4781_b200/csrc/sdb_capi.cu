@@ -97,9 +97,13 @@ int sdb_gram(int dtype, int64_t P, int64_t m, int64_t K, const double* D64, void
     return cuda_rc(rc, "sdb_gram");
 }
 
+int64_t sdb_correlate_workspace_bytes(int dtype, int64_t P, int64_t m, int64_t K) {
+    return dtype == SDB_F32 ? sdb::corr_tc_ws_bytes((int)P, m, K) : 0;
+}
+
 int sdb_correlate(int dtype, int64_t N, int64_t m, int64_t K, int64_t P, const int64_t* shard_off,
                   int64_t max_shard_rows, const void* Y, int64_t ldy, const void* D, void* alpha0,
-                  int64_t lda, int use_tc, void* stream) {
+                  int64_t lda, int use_tc, void* ws, int64_t ws_bytes, void* stream) {
     if (!dtype_ok(dtype) || N < 0 || m < 1 || K < 1 || P < 1 || ldy < m || lda < K)
         return fail(SDB_EINVAL, "sdb_correlate: bad args");
     if (N == 0) return SDB_OK;
@@ -110,8 +114,9 @@ int sdb_correlate(int dtype, int64_t N, int64_t m, int64_t K, int64_t P, const i
     } else {
         rc = cudaErrorNotSupported;
         if (use_tc)
-            rc = sdb::correlate_tc_f32((const float*)Y, ldy, shard_off, max_shard_rows, (int)P,
-                                       (const float*)D, m, K, (float*)alpha0, lda, S(stream));
+            rc = sdb::correlate_tc_f32(N, (const float*)Y, ldy, shard_off, max_shard_rows, (int)P,
+                                       (const float*)D, m, K, (float*)alpha0, lda, ws, ws_bytes,
+                                       S(stream));
         if (rc == cudaErrorNotSupported)
             rc = sdb::correlate_simt_f32((const float*)Y, ldy, shard_off, max_shard_rows, (int)P,
                                          (const float*)D, m, K, (float*)alpha0, lda, S(stream));

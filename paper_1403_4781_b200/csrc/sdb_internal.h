@@ -40,9 +40,10 @@ int correlate_simt_f32(const float* Y, int64_t ldy, const int64_t* off, int64_t 
                        cudaStream_t st);
 // tcgen05 3xTF32 correlation GEMM (sdb_tc_gemm.cu); returns cudaErrorNotSupported
 // when the shape is outside the kernel's tiling.
-int correlate_tc_f32(const float* Y, int64_t ldy, const int64_t* off, int64_t max_rows, int P,
-                     const float* D, int64_t m, int64_t K, float* alpha, int64_t lda,
-                     cudaStream_t st);
+int correlate_tc_f32(int64_t N, const float* Y, int64_t ldy, const int64_t* off, int64_t max_rows,
+                     int P, const float* D, int64_t m, int64_t K, float* alpha, int64_t lda, void* ws,
+                     int64_t ws_bytes, cudaStream_t st);
+int64_t corr_tc_ws_bytes(int P, int64_t m, int64_t K);
 
 template <typename T>
 int launch_omp(OmpArgs<T> a, cudaStream_t st);

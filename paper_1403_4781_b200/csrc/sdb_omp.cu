@@ -361,6 +361,227 @@ k_omp(OmpArgs<T> a) {
     }
 }
 
+// ----------------------------------------------------------------------------
+// FP32 fast path (cap <= 32): same algorithm and stopping rules as k_omp, but
+//  * each warp owns a contiguous range of signals and prefetches the next
+//    signal's alpha0 row and y while the current one is coded;
+//  * y and the residual live in registers (lane owns rows lane + 32q);
+//  * argmax is two redux.sync ops: |corr| >= 0 so its IEEE bits order like
+//    the values, and in FP32 the reference's 1e-12 tie window collapses to
+//    exact equality (cmax - 1e-12*cmax == cmax), i.e. lowest index among the
+//    maxima;
+//  * Cholesky / substitutions are lane-parallel column sweeps;
+//  * the selected atoms' columns are cached in shared memory for the residual.
+// ----------------------------------------------------------------------------
+constexpr int FAST_CAP = 32;
+constexpr int FAST_TRI = FAST_CAP * (FAST_CAP + 1) / 2;
+
+__host__ __device__ inline int fast_warp_floats(int cap, int m) {
+    return FAST_TRI + 3 * FAST_CAP + cap * m;  // L, tmp, x, ids(as int), Dsel
+}
+
+template <int KPL, int MPL>
+__global__ void __launch_bounds__(256, (KPL >= 16) ? 1 : 2)
+k_omp_fast(OmpArgs<float> a) {
+    extern __shared__ __align__(16) float fsm[];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    const int wpb = blockDim.x >> 5;
+    const int m = a.m, K = a.K, cap = a.cap;
+    float* Ls = fsm + (int64_t)wib * fast_warp_floats(cap, m);
+    float* tmp = Ls + FAST_TRI;
+    float* xs = tmp + FAST_CAP;
+    int* ids = (int*)(xs + FAST_CAP);
+    float* Dsel = (float*)(ids + FAST_CAP);
+    const float eps = a.eps;
+
+    const int64_t gw = (int64_t)blockIdx.x * wpb + wib;
+    const int64_t nw = (int64_t)gridDim.x * wpb;
+    const int64_t per = (a.N + nw - 1) / nw;
+    const int64_t i_begin = gw * per;
+    const int64_t i_end = min(a.N, i_begin + per);
+    if (i_begin >= i_end) return;
+
+    int p = shard_of(a.shard_off, a.P, i_begin);
+    int64_t p_end = a.shard_off[p + 1];
+
+    float c0n[KPL], yn[MPL];
+    auto fetch = [&](int64_t i) {
+#pragma unroll
+        for (int k = 0; k < KPL; ++k) {
+            const int j = lane + 32 * k;
+            c0n[k] = (j < K) ? __ldg(a.alpha0 + i * a.lda + j) : 0.0f;
+        }
+#pragma unroll
+        for (int q = 0; q < MPL; ++q) {
+            const int r = lane + 32 * q;
+            yn[q] = (r < m) ? __ldg(a.Y + i * a.ldy + r) : 0.0f;
+        }
+    };
+    fetch(i_begin);
+    for (int64_t i = i_begin; i < i_end; ++i) {
+        while (i >= p_end) { ++p; p_end = a.shard_off[p + 1]; }
+        float c0[KPL], y[MPL];
+#pragma unroll
+        for (int k = 0; k < KPL; ++k) c0[k] = c0n[k];
+#pragma unroll
+        for (int q = 0; q < MPL; ++q) y[q] = yn[q];
+        if (i + 1 < i_end) fetch(i + 1);
+        const float* __restrict__ Gp = a.G + (int64_t)p * K * K;
+        const float* __restrict__ Dp = a.D + (int64_t)p * K * m;
+
+        float ysq = 0.0f;
+#pragma unroll
+        for (int q = 0; q < MPL; ++q) ysq = fmaf(y[q], y[q], ysq);
+        ysq = warp_sum(ysq);
+        float rnorm = __fsqrt_rn(ysq);
+        int n = 0, status = 0;
+        if (!(rnorm <= eps || rnorm == 0.0f)) {
+            uint32_t selbits = 0;
+            for (int step = 0; step < cap; ++step) {
+                float corr[KPL];
+#pragma unroll
+                for (int k = 0; k < KPL; ++k) corr[k] = c0[k];
+                for (int t = 0; t < n; ++t) {
+                    const float coef = xs[t];
+                    const float* __restrict__ g = Gp + (int64_t)ids[t] * K;
+#pragma unroll
+                    for (int k = 0; k < KPL; ++k) {
+                        const int j = lane + 32 * k;
+                        if (j < K) corr[k] = fmaf(-__ldg(g + j), coef, corr[k]);
+                    }
+                }
+                uint32_t bits[KPL];
+                uint32_t lmax = 0;
+#pragma unroll
+                for (int k = 0; k < KPL; ++k) {
+                    const int j = lane + 32 * k;
+                    const bool ok = (j < K) && !((selbits >> k) & 1u);
+                    bits[k] = ok ? __float_as_uint(fabsf(corr[k])) : 0u;
+                    lmax = max(lmax, bits[k]);
+                }
+                const uint32_t cbits = __reduce_max_sync(SDB_FULL, lmax);
+                const float cmax = __uint_as_float(cbits);
+                if (cmax <= 1e-13f * rnorm) { status = 3; break; }
+                int cand = 0x7fffffff;
+#pragma unroll
+                for (int k = KPL - 1; k >= 0; --k)
+                    if (bits[k] == cbits) cand = lane + 32 * k;
+                const int best = (int)__reduce_min_sync(SDB_FULL, (unsigned)cand);
+
+                // Cholesky row of the new atom (column sweep, lane t -> w_t)
+                float* Lrow = Ls + n * (n + 1) / 2;
+                float gacc = (lane < n) ? __ldg(Gp + (int64_t)ids[lane] * K + best) : 0.0f;
+                float wme = 0.0f;
+                for (int u = 0; u < n; ++u) {
+                    const float wu = __fdiv_rn(__shfl_sync(SDB_FULL, gacc, u), Ls[u * (u + 1) / 2 + u]);
+                    if (lane == u) wme = wu;
+                    if (lane > u && lane < n) gacc = fmaf(-Ls[lane * (lane + 1) / 2 + u], wu, gacc);
+                }
+                const float dsq = __ldg(Gp + (int64_t)best * K + best) -
+                                  warp_sum(lane < n ? wme * wme : 0.0f);
+                if (dsq <= a.guard) { status = 2; break; }
+                float cb = 0.0f;
+#pragma unroll
+                for (int k = 0; k < KPL; ++k)
+                    if (k == (best >> 5)) cb = c0[k];
+                cb = __shfl_sync(SDB_FULL, cb, best & 31);
+                const float ldiag = __fsqrt_rn(dsq);
+                if (lane < n) Lrow[lane] = wme;
+                if (lane == 0) { Lrow[n] = ldiag; ids[n] = best; }
+                // cache the atom's column for the residual
+                const float* dcol = Dp + (int64_t)best * m;
+                for (int r = lane; r < m; r += 32) Dsel[n * m + r] = __ldg(dcol + r);
+                if (lane == (best & 31)) selbits |= 1u << (best >> 5);
+                // forward: only tmp[n] is new
+                const float part = (lane < n) ? wme * tmp[lane] : 0.0f;
+                const float tn = __fdiv_rn(cb - warp_sum(part), ldiag);
+                n += 1;
+                __syncwarp();
+                if (lane == 0) tmp[n - 1] = tn;
+                __syncwarp();
+                // back substitution, column sweep from the bottom
+                float bacc = (lane < n) ? tmp[lane] : 0.0f;
+                float xme = 0.0f;
+                for (int u = n - 1; u >= 0; --u) {
+                    const float* Lu = Ls + u * (u + 1) / 2;
+                    const float xu = __fdiv_rn(__shfl_sync(SDB_FULL, bacc, u), Lu[u]);
+                    if (lane == u) xme = xu;
+                    if (lane < u) bacc = fmaf(-Lu[lane], xu, bacc);
+                }
+                if (lane < n) xs[lane] = xme;
+                __syncwarp();
+                // explicit residual from the cached columns
+                float rr[MPL];
+#pragma unroll
+                for (int q = 0; q < MPL; ++q) rr[q] = y[q];
+                for (int t = 0; t < n; ++t) {
+                    const float xt = xs[t];
+#pragma unroll
+                    for (int q = 0; q < MPL; ++q) {
+                        const int r = lane + 32 * q;
+                        if (r < m) rr[q] = fmaf(-Dsel[t * m + r], xt, rr[q]);
+                    }
+                }
+                float rs = 0.0f;
+#pragma unroll
+                for (int q = 0; q < MPL; ++q) rs = fmaf(rr[q], rr[q], rs);
+                rnorm = __fsqrt_rn(warp_sum(rs));
+                if (rnorm <= eps) break;
+            }
+        }
+        __syncwarp();
+        for (int t = lane; t < cap; t += 32) {
+            a.idx[i * cap + t] = (t < n) ? ids[t] : 0;
+            a.val[i * cap + t] = (t < n) ? xs[t] : 0.0f;
+        }
+        if (lane == 0) {
+            a.counts[i] = n;
+            a.status[i] = (int8_t)status;
+            a.rnorm[i] = rnorm;
+        }
+        __syncwarp();
+    }
+}
+
+template <int KPL, int MPL>
+static int launch_fast_k(const OmpArgs<float>& a, cudaStream_t st) {
+    const int wf = fast_warp_floats(a.cap, a.m);
+    int wpb = 8;
+    while (wpb > 1 && wpb * wf * 4 > 200 * 1024) wpb >>= 1;
+    const int smem = wpb * wf * 4;
+    auto fn = k_omp_fast<KPL, MPL>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return (int)e;
+    }
+    // enough warps to fill every SM several times, a contiguous range each
+    const int64_t warps = std::min<int64_t>(a.N, (int64_t)148 * 64);
+    const int64_t blocks = (warps + wpb - 1) / wpb;
+    fn<<<(unsigned)blocks, wpb * 32, smem, st>>>(a);
+    return (int)cudaGetLastError();
+}
+
+template <int KPL>
+static int launch_fast_m(const OmpArgs<float>& a, cudaStream_t st) {
+    const int mpl = (a.m + 31) / 32;
+    if (mpl <= 1) return launch_fast_k<KPL, 1>(a, st);
+    if (mpl <= 2) return launch_fast_k<KPL, 2>(a, st);
+    if (mpl <= 5) return launch_fast_k<KPL, 5>(a, st);
+    return launch_fast_k<KPL, 8>(a, st);
+}
+
+static int launch_omp_fast(const OmpArgs<float>& a, cudaStream_t st) {
+    const int kpl = (a.K + 31) / 32;
+    if (kpl <= 1) return launch_fast_m<1>(a, st);
+    if (kpl <= 2) return launch_fast_m<2>(a, st);
+    if (kpl <= 4) return launch_fast_m<4>(a, st);
+    if (kpl <= 8) return launch_fast_m<8>(a, st);
+    if (kpl <= 16) return launch_fast_m<16>(a, st);
+    if (kpl <= 18) return launch_fast_m<18>(a, st);
+    return launch_fast_m<32>(a, st);
+}
+
 template <typename T>
 int64_t omp_scratch_bytes(int64_t N, int cap, int m, int* use_global) {
     const int64_t wb = omp_warp_bytes<T>(cap, m);
@@ -384,6 +605,10 @@ static int launch_omp_k(const OmpArgs<T>& a, int blocks, int smem, cudaStream_t 
 template <typename T>
 int launch_omp(OmpArgs<T> a, cudaStream_t st) {
     if (a.N <= 0) return 0;
+    if constexpr (!Ar<T>::kExact) {
+        if (a.cap <= FAST_CAP && a.m <= 256 && a.gscratch == nullptr)
+            return launch_omp_fast(a, st);
+    }
     const int64_t wb = omp_warp_bytes<T>(a.cap, a.m);
     a.warp_bytes = wb;
     int smem = 0;
