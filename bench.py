@@ -301,6 +301,7 @@ def main():
                        "local_iters": cfg["local_iters"], "merge_iters": cfg["merge_iters"],
                        "eps": cfg["eps"], "s_max": cfg["s_max"], "s1": cfg["s1"], "s2": cfg["s2"],
                        "codings_per_step": codings, "train_time_s": ms / 1000.0,
+                       "phase_s": {"split": r.split_s, "locals": r.local_s, "merge": r.merge_s},
                        "precision": prec, "parallelism": f"shards over {world} GPU(s)",
                        "l2": "inputs larger than L2 (Y is %.0f MB)" % (N * m * 4 / 1e6)},
             "roofline": roof, "kernels": breakdown, "cpu_baseline": cpu, "e2e": e2e,

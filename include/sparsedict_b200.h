@@ -105,13 +105,21 @@ int sdb_csc_fill(int dtype, int64_t N, int64_t cap, const int32_t *idx, const vo
  * (usage 0 or norm <= 1e-12 max(maxnorm,1)) restored from D_prev and every
  * column normalised. Shards with no nonzero code return D_prev unchanged.
  * Outputs: D_out (P,K,m) f64, scales (P,K) raw column norms, usage (P,K),
- * dead (P,K), resid_fro (P), rank (P), deficient (P, dependent pivots). */
+ * dead (P,K), resid_fro (P), rank (P), deficient (P, dependent pivots).
+ * residual_fro uses the least-squares identity ||Y - Z^T X||^2 = ||Y||^2 -
+ * ||L^-1 B||^2; ysq_shard (P, optional) supplies ||Y_p||^2 (constant across
+ * training iterations, see sdb_shard_energy), NULL computes it. */
 int64_t sdb_mod_workspace_bytes(int64_t P, int64_t N, int64_t m, int64_t K, int64_t cap);
 int sdb_mod_update(int dtype, int64_t P, int64_t N, int64_t m, int64_t K, int64_t cap,
                    const int64_t *shard_off, const void *Y, int64_t ldy, const int32_t *idx,
                    const void *val, const int32_t *counts, const double *D_prev, double *D_out,
                    double *scales, int32_t *usage, int8_t *dead, double *resid_fro, int32_t *rank,
-                   int32_t *deficient, double rank_rcond, void *ws, int64_t ws_bytes, void *stream);
+                   int32_t *deficient, double rank_rcond, const double *ysq_shard, void *ws,
+                   int64_t ws_bytes, void *stream);
+
+/* out[p] = ||Y_p||_F^2 per shard (FP64, fixed reduction order); tmp holds N doubles. */
+int sdb_shard_energy(int dtype, int64_t P, int64_t N, int64_t m, const int64_t *shard_off,
+                     const void *Y, int64_t ldy, double *tmp, double *out, void *stream);
 
 /* replace_degenerate_atoms (dictionary_update.py:117-177) per shard, in place
  * on D (P,K,m) f64: degenerate = usage 0 | norm <= 1e-12 | higher index of a

@@ -280,6 +280,18 @@ class ShardSet:
     def max_rows(self) -> int:
         return int(max(self.sizes)) if self.sizes else 0
 
+    _ysq: torch.Tensor | None = None
+
+    def energy(self) -> torch.Tensor:
+        """||Y_p||_F^2 per shard (computed once, reused by every MOD step)."""
+        if self._ysq is None:
+            tmp = empty((max(self.N, 1),), torch.float64)
+            out = empty((self.P,), torch.float64)
+            _lib.call("sdb_shard_energy", sdb_dtype(self.prec), self.P, self.N, self.m,
+                      ptr(self.off), ptr(self.Y), self.m, ptr(tmp), ptr(out), stream())
+            self._ysq = out
+        return self._ysq
+
     @classmethod
     def single(cls, Y: torch.Tensor, prec: str) -> "ShardSet":
         off, _ = shard_offsets([Y.shape[0]])
@@ -309,7 +321,7 @@ def mod_update(S: ShardSet, codes: DeviceCodes, D64: torch.Tensor) -> ModResult:
     timed_call("mod_update", S.N * (2 * m * es + codes.cap * (4 + es) + 4), 0.0, "sdb_mod_update", dt, P, S.N, m, K, codes.cap, ptr(S.off), ptr(S.Y), m,
               ptr(codes.idx), ptr(codes.val), ptr(codes.counts), ptr(D64), ptr(r.D),
               ptr(r.scales), ptr(r.usage), ptr(r.dead), ptr(r.resid), ptr(r.rank),
-              ptr(r.deficient), RANK_RCOND, ptr(ws), wsb, stream())
+              ptr(r.deficient), RANK_RCOND, ptr(S.energy()), ptr(ws), wsb, stream())
     return r
 
 

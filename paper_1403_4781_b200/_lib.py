@@ -42,7 +42,8 @@ SIGNATURES = {
     "sdb_mod_workspace_bytes": (c_i64, [c_i64, c_i64, c_i64, c_i64, c_i64]),
     "sdb_mod_update": (c_int, [c_int, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp,
                                c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_dbl,
-                               c_vp, c_i64, c_vp]),
+                               c_vp, c_vp, c_i64, c_vp]),
+    "sdb_shard_energy": (c_int, [c_int, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "sdb_replace_workspace_bytes": (c_i64, [c_i64, c_i64, c_i64, c_i64]),
     "sdb_replace_degenerate": (c_int, [c_int, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64,
                                        c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp]),

@@ -201,7 +201,8 @@ int sdb_mod_update(int dtype, int64_t P, int64_t N, int64_t m, int64_t K, int64_
                    const int64_t* shard_off, const void* Y, int64_t ldy, const int32_t* idx,
                    const void* val, const int32_t* counts, const double* D_prev, double* D_out,
                    double* scales, int32_t* usage, int8_t* dead, double* resid_fro, int32_t* rank,
-                   int32_t* deficient, double rank_rcond, void* ws, int64_t ws_bytes, void* stream) {
+                   int32_t* deficient, double rank_rcond, const double* ysq_shard, void* ws,
+                   int64_t ws_bytes, void* stream) {
     if (!dtype_ok(dtype) || P < 1 || N < 0 || m < 1 || m > 256 || K < 1 || K > 1024 || cap < 1 || ldy < m)
         return fail(SDB_EINVAL, "sdb_mod_update: bad args (m <= 256, K <= 1024)");
     if (ws == nullptr || ws_bytes < sdb::mod_ws_bytes((int)P, N, (int)m, (int)K, (int)cap))
@@ -213,11 +214,19 @@ int sdb_mod_update(int dtype, int64_t P, int64_t N, int64_t m, int64_t K, int64_
         a.off = shard_off; a.Y = (const T*)Y; a.ldy = ldy; a.idx = idx; a.val = (const T*)val;
         a.counts = counts; a.Dprev = D_prev; a.Dout = D_out; a.scales = scales; a.usage = usage;
         a.dead = dead; a.resid_fro = resid_fro; a.rank = rank; a.deficient_out = deficient;
-        a.nnz_out = nullptr; a.rank_rcond = rank_rcond; a.ws = ws;
+        a.nnz_out = nullptr; a.rank_rcond = rank_rcond; a.ysq_shard = ysq_shard; a.ws = ws;
         return sdb::mod_update<T>(a, S(stream));
     };
     int rc = dtype == SDB_F64 ? go((double*)nullptr) : go((float*)nullptr);
     return cuda_rc(rc, "sdb_mod_update");
+}
+
+int sdb_shard_energy(int dtype, int64_t P, int64_t N, int64_t m, const int64_t* shard_off,
+                     const void* Y, int64_t ldy, double* tmp, double* out, void* stream) {
+    if (!dtype_ok(dtype) || P < 1 || N < 0 || m < 1 || m > 256 || ldy < m)
+        return fail(SDB_EINVAL, "sdb_shard_energy: bad args");
+    return cuda_rc(sdb::shard_ysq((int)P, N, (int)m, Y, ldy, dtype == SDB_F64, shard_off, tmp, out,
+                                  S(stream)), "sdb_shard_energy");
 }
 
 int64_t sdb_replace_workspace_bytes(int64_t P, int64_t N, int64_t m, int64_t K) {

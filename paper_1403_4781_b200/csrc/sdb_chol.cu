@@ -88,20 +88,28 @@ k_chol_diag(int K, int j0, double* __restrict__ Aall, double* __restrict__ Tall,
         }
         __syncthreads();
     }
-    // T = L^-1 (lower), one thread per column
-    if (tid < nb) {
-        const int c = tid;
-        for (int r = 0; r < nb; ++r) Ts[r][c] = 0.0;
-        if (!sdep[c]) {
-            Ts[c][c] = 1.0 / Ls[c][c];
-            for (int r = c + 1; r < nb; ++r) {
-                double s = 0.0;
-                for (int q = c; q < r; ++q) s = fma(Ls[r][q], Ts[q][c], s);
-                Ts[r][c] = sdep[r] ? 0.0 : -s / Ls[r][r];
+    // T = L^-1 (lower): rows in sequence, all columns in parallel, each
+    // partial dot split over 4 threads (fixed order -> deterministic)
+    {
+        __shared__ double part[4][CB];
+        const int c = tid & (CB - 1), h = tid >> 6;  // 64 columns x 4 quarters
+        for (int e = tid; e < CB * CB; e += 256) Ts[e / CB][e % CB] = 0.0;
+        __syncthreads();
+        if (tid < nb && !sdep[tid]) Ts[tid][tid] = 1.0 / Ls[tid][tid];
+        __syncthreads();
+        for (int r = 1; r < nb; ++r) {
+            double s = 0.0;
+            if (c < r) {
+                const int len = r - c, q0 = c + (len * h) / 4, q1 = c + (len * (h + 1)) / 4;
+                for (int q = q0; q < q1; ++q) s = fma(Ls[r][q], Ts[q][c], s);
             }
+            part[h][c] = s;
+            __syncthreads();
+            if (tid < r && !sdep[tid] && !sdep[r])
+                Ts[r][tid] = -(((part[0][tid] + part[1][tid]) + part[2][tid]) + part[3][tid]) / Ls[r][r];
+            __syncthreads();
         }
     }
-    __syncthreads();
     double* T = Tall + ((int64_t)p * ((K + CB - 1) / CB) + j0 / CB) * CB * CB;
     for (int e = tid; e < CB * CB; e += 256) {
         const int r = e / CB, c = e % CB;
@@ -315,13 +323,28 @@ k_back_update(int K, int m, int j0, const double* __restrict__ Aall, double* __r
     }
 }
 
+// out[p] = sum of squares of the (K*m) block of shard p (fixed order)
+__global__ void __launch_bounds__(256) k_sumsq(int64_t n, const double* __restrict__ X, double* __restrict__ out) {
+    __shared__ double sh[256];
+    const double* x = X + (int64_t)blockIdx.x * n;
+    double s = 0.0;
+    for (int64_t e = threadIdx.x; e < n; e += 256) s = fma(x[e], x[e], s);
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[blockIdx.x] = sh[0];
+}
+
 int64_t chol_ws_bytes(int P, int K) {
     const int64_t nblk = (K + CB - 1) / CB;
     return (int64_t)P * nblk * CB * CB * sizeof(double) + (int64_t)P * sizeof(double) + 512;
 }
 
 int chol_solve(int P, int K, int m, double* A, double* B, const int32_t* usage, double rel_tol,
-               int8_t* depmask, int32_t* ndep, void* ws, cudaStream_t st) {
+               int8_t* depmask, int32_t* ndep, double* wsq, void* ws, cudaStream_t st) {
     double* T = (double*)ws;
     const int64_t nblk = (K + CB - 1) / CB;
     double* tol = T + (int64_t)P * nblk * CB * CB;
@@ -354,6 +377,7 @@ int chol_solve(int P, int K, int m, double* A, double* B, const int32_t* usage, 
             k_chol_update<<<gu, 256, smem2, st>>>(K, m, j0, A, B);
         }
     }
+    if (wsq) k_sumsq<<<P, 256, 0, st>>>((int64_t)K * m, B, wsq);
     const int last = (int)((nblk - 1) * CB);
     for (int j0 = last; j0 >= 0; j0 -= CB) {
         k_back_diag<<<P, 256, smem2, st>>>(K, m, j0, B, T);

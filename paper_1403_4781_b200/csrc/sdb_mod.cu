@@ -145,21 +145,22 @@ k_place(const int64_t* __restrict__ off, const int64_t* __restrict__ cf, int P, 
     }
 }
 
-// ---- (f) B[p][a][:] = sum over bucket (y_i * x_ai), lanes over m. Bucket
-// entries are fetched 32 at a time (one per lane) and broadcast, and four
-// signal rows are loaded before they are accumulated (in bucket order).
+// ---- (f) B[p][a][:] = sum over bucket (y_i * x_ai). One CTA per (p, a):
+// warp w takes the bucket's 32-entry batches w, w+8, ... (entries fetched one
+// per lane, broadcast, four signal rows in flight); the 8 partial sums are
+// combined in warp order, so the result is a fixed function of the input.
 template <typename T, int MPL>
 __global__ void __launch_bounds__(256)
 k_yxt(int P, int K, int m, const T* __restrict__ Y, int64_t ldy, const int64_t* __restrict__ bucket_off,
       const int32_t* __restrict__ bsig, const double* __restrict__ bval, double* __restrict__ B) {
-    const int lane = threadIdx.x & 31;
-    const int64_t e = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);  // (p, a)
-    if (e >= (int64_t)P * K) return;
+    __shared__ double part[8][MPL * 32];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t e = blockIdx.x;  // (p, a)
     double acc[MPL];
 #pragma unroll
     for (int q = 0; q < MPL; ++q) acc[q] = 0.0;
     const int64_t lo = bucket_off[e], hi = bucket_off[e + 1];
-    for (int64_t b0 = lo; b0 < hi; b0 += 32) {
+    for (int64_t b0 = lo + 32 * wib; b0 < hi; b0 += 32 * 8) {
         const int nbat = (int)min((int64_t)32, hi - b0);
         const int my_sig = lane < nbat ? bsig[b0 + lane] : 0;
         const double my_val = lane < nbat ? bval[b0 + lane] : 0.0;
@@ -168,8 +169,8 @@ k_yxt(int P, int K, int m, const T* __restrict__ Y, int64_t ldy, const int64_t* 
             double vv[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const int i = __shfl_sync(SDB_FULL, my_sig, j + u);
-                vv[u] = __shfl_sync(SDB_FULL, my_val, j + u);
+                const int i = __shfl_sync(SDB_FULL, my_sig, (j + u) & 31);
+                vv[u] = __shfl_sync(SDB_FULL, my_val, (j + u) & 31);
                 const T* y = Y + (int64_t)i * ldy;
 #pragma unroll
                 for (int q = 0; q < MPL; ++q) {
@@ -183,17 +184,22 @@ k_yxt(int P, int K, int m, const T* __restrict__ Y, int64_t ldy, const int64_t* 
                 for (int q = 0; q < MPL; ++q) acc[q] = fma(yv[u][q], vv[u], acc[q]);
         }
     }
-    double* out = B + e * m;
 #pragma unroll
-    for (int q = 0; q < MPL; ++q) {
-        const int r = lane + 32 * q;
-        if (r < m) out[r] = acc[q];
+    for (int q = 0; q < MPL; ++q) part[wib][lane + 32 * q] = acc[q];
+    __syncthreads();
+    double* out = B + e * m;
+    for (int r = threadIdx.x; r < m; r += 256) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) t += part[w][r];
+        out[r] = t;
     }
 }
 
-// ---- (g) A[p][a][:] = sum over bucket (x_ai * x_i), row accumulator in smem.
-// Batches of 32 bucket entries: their code rows are staged in smem with all
-// loads in flight, then applied in bucket order (deterministic).
+// ---- (g) A[p][a][:] = sum over bucket (x_ai * x_i). One CTA per (p, a):
+// warp w accumulates batches w, w+8, ... into its own smem row (code rows of
+// a batch staged in smem first, all loads in flight), rows combined in warp
+// order (deterministic).
 constexpr int XXT_CAP = 32;
 
 template <typename T>
@@ -203,23 +209,20 @@ k_xxt(int P, int K, int cap, const int32_t* __restrict__ idx, const T* __restric
       const int32_t* __restrict__ bsig, const double* __restrict__ bval, double* __restrict__ A) {
     extern __shared__ double sh_row[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int64_t e = (int64_t)blockIdx.x * 8 + wib;
+    const int64_t e = blockIdx.x;
     double* row = sh_row + (int64_t)wib * K;
-    // staging area after the 8 row accumulators: per warp 32 x XXT_CAP (idx, val)
     int32_t* sidx = (int32_t*)(sh_row + 8 * (int64_t)K) + wib * 32 * XXT_CAP;
     double* sval = (double*)(sh_row + 8 * (int64_t)K + 4 * 32 * XXT_CAP) + wib * 32 * XXT_CAP;
-    if (e >= (int64_t)P * K) return;
     for (int b = lane; b < K; b += 32) row[b] = 0.0;
     __syncwarp();
     const int64_t lo = bucket_off[e], hi = bucket_off[e + 1];
     const bool staged = cap <= XXT_CAP;
-    for (int64_t q0 = lo; q0 < hi; q0 += 32) {
+    for (int64_t q0 = lo + 32 * wib; q0 < hi; q0 += 32 * 8) {
         const int nbat = (int)min((int64_t)32, hi - q0);
         const int my_sig = lane < nbat ? bsig[q0 + lane] : 0;
         const double my_v = lane < nbat ? bval[q0 + lane] : 0.0;
         const int my_n = lane < nbat ? counts[my_sig] : 0;
         if (staged) {
-            // lane u stages entry u's code row (<= cap values)
             for (int t = 0; t < my_n; ++t) {
                 sidx[lane * XXT_CAP + t] = idx[(int64_t)my_sig * cap + t];
                 sval[lane * XXT_CAP + t] = (double)val[(int64_t)my_sig * cap + t];
@@ -238,8 +241,14 @@ k_xxt(int P, int K, int cap, const int32_t* __restrict__ idx, const T* __restric
             __syncwarp();
         }
     }
+    __syncthreads();
     double* out = A + e * K;
-    for (int b = lane; b < K; b += 32) out[b] = row[b];
+    for (int b = threadIdx.x; b < K; b += 256) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) t += sh_row[(int64_t)w * K + b];
+        out[b] = t;
+    }
 }
 
 // ---- per-signal residual ||y_i - D_p x_i||^2 (D in f64, atom-major)
@@ -284,6 +293,55 @@ k_resid_sq(int64_t N, int m, int K, int cap, int P, const int64_t* __restrict__ 
         out[i] = s;
         if (ysq_out) ysq_out[i] = yy;
     }
+}
+
+// ---- ||y_i||^2 per signal
+template <typename T, int MPL>
+__global__ void __launch_bounds__(256)
+k_row_sq(int64_t N, int m, const T* __restrict__ Y, int64_t ldy, double* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (i >= N) return;
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < MPL; ++q) {
+        const int r = lane + 32 * q;
+        if (r < m) {
+            const double v = (double)Y[i * ldy + r];
+            s = fma(v, v, s);
+        }
+    }
+    s = warp_sum(s);
+    if (lane == 0) out[i] = s;
+}
+
+// least-squares residual from the identity; shards whose relative residual^2
+// is below 1e-4 (near-exact fits, where the subtraction cancels) are flagged
+// for the explicit pass
+__global__ void k_ls_resid(int P, const double* __restrict__ ysq, const double* __restrict__ wsq,
+                           double* __restrict__ resid, int32_t* __restrict__ need) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+    const double r2 = ysq[p] - wsq[p];
+    resid[p] = sqrt(fmax(r2, 0.0));
+    need[p] = (r2 <= 1e-4 * ysq[p]) ? 1 : 0;
+}
+
+__global__ void __launch_bounds__(256)
+k_shard_sum_masked(const int64_t* __restrict__ off, const double* __restrict__ v,
+                   const int32_t* __restrict__ mask, double* __restrict__ out) {
+    __shared__ double sh[256];
+    const int p = blockIdx.x;
+    if (!mask[p]) return;
+    double s = 0.0;
+    for (int64_t i = off[p] + threadIdx.x; i < off[p + 1]; i += 256) s += v[i];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[p] = sqrt(sh[0]);
 }
 
 // ---- deterministic per-shard sum of a per-signal array (fixed order)
@@ -586,6 +644,9 @@ ModWs carve_mod_ws(void* base, int P, int64_t N, int m, int K, int cap) {
     w.deficient = (int32_t*)take(sizeof(int32_t) * P);
     w.depmask = (int8_t*)take((int64_t)P * K);
     w.chol = take(chol_ws_bytes(P, K));
+    w.wsq = (double*)take(sizeof(double) * P);
+    w.ysqp = (double*)take(sizeof(double) * P);
+    w.need = (int32_t*)take(sizeof(int32_t) * P);
     w.end = p;
     return w;
 }
@@ -620,7 +681,7 @@ int mod_update(const ModArgs<T>& a, cudaStream_t st) {
     }
     rc = with_mpl(m, [&](auto c) {
         constexpr int MPL = decltype(c)::value;
-        k_yxt<T, MPL><<<(unsigned)((PK + 7) / 8), 256, 0, st>>>(P, K, m, a.Y, a.ldy, w.bucket_off,
+        k_yxt<T, MPL><<<(unsigned)PK, 256, 0, st>>>(P, K, m, a.Y, a.ldy, w.bucket_off,
                                                                w.bsig, w.bval, w.B);
         return (int)cudaGetLastError();
     });
@@ -629,22 +690,35 @@ int mod_update(const ModArgs<T>& a, cudaStream_t st) {
         const int smem = 8 * K * (int)sizeof(double) + 8 * 32 * XXT_CAP * (4 + 8);
         if (smem > 48 * 1024)
             cudaFuncSetAttribute(k_xxt<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        k_xxt<T><<<(unsigned)((PK + 7) / 8), 256, smem, st>>>(P, K, cap, a.idx, a.val, a.counts,
+        k_xxt<T><<<(unsigned)PK, 256, smem, st>>>(P, K, cap, a.idx, a.val, a.counts,
                                                              w.bucket_off, w.bsig, w.bval, w.A);
     }
     // masked RHS rows of unused atoms are irrelevant: A is the identity there
     // and B holds zeros (their buckets are empty).
-    rc = chol_solve(P, K, m, w.A, w.B, a.usage, a.rank_rcond, w.depmask, w.deficient, w.chol, st);
+    rc = chol_solve(P, K, m, w.A, w.B, a.usage, a.rank_rcond, w.depmask, w.deficient, w.wsq, w.chol, st);
     if (rc) return rc;
-    // residual before normalisation with the raw solution Z (= B now)
+    // residual before normalisation: ||Y - Z^T X||^2 = ||Y||^2 - <Z, B> and
+    // <Z, B> = ||L^-1 B||^2 (captured between the forward and back phases)
+    const double* ysq = a.ysq_shard;
+    if (ysq == nullptr) {
+        rc = with_mpl(m, [&](auto c) {
+            constexpr int MPL = decltype(c)::value;
+            k_row_sq<T, MPL><<<(unsigned)((N + 7) / 8), 256, 0, st>>>(N, m, a.Y, a.ldy, w.rsq);
+            return (int)cudaGetLastError();
+        });
+        if (rc) return rc;
+        k_shard_sum<<<P, 256, 0, st>>>(a.off, w.rsq, w.ysqp, 0);
+        ysq = w.ysqp;
+    }
+    k_ls_resid<<<(P + 127) / 128, 128, 0, st>>>(P, ysq, w.wsq, a.resid_fro, w.need);
     rc = with_mpl(m, [&](auto c) {
         constexpr int MPL = decltype(c)::value;
         k_resid_sq<T, MPL><<<(unsigned)((N + 7) / 8), 256, 0, st>>>(
-            N, m, K, cap, P, a.off, a.Y, a.ldy, a.idx, a.val, a.counts, w.B, w.rsq, nullptr, nullptr);
+            N, m, K, cap, P, a.off, a.Y, a.ldy, a.idx, a.val, a.counts, w.B, w.rsq, nullptr, w.need);
         return (int)cudaGetLastError();
     });
     if (rc) return rc;
-    k_shard_sum<<<P, 256, 0, st>>>(a.off, w.rsq, a.resid_fro, 1);
+    k_shard_sum_masked<<<P, 256, 0, st>>>(a.off, w.rsq, w.need, a.resid_fro);
     k_shard_nnz<<<P, 256, 0, st>>>(a.off, a.counts, w.nnz);
     k_mod_finish<<<P, 256, 0, st>>>(P, K, m, w.B, a.Dprev, a.usage, w.nnz, a.Dout, a.scales, a.dead,
                                     a.rank, w.deficient);
@@ -728,6 +802,23 @@ template int residual_sq<float>(int64_t, int, int, int, int, const int64_t*, con
 template int residual_sq<double>(int64_t, int, int, int, int, const int64_t*, const double*, int64_t,
                                  const int32_t*, const double*, const int32_t*, const double*, double*,
                                  double*, cudaStream_t);
+
+int shard_ysq(int P, int64_t N, int m, const void* Y, int64_t ldy, bool f64, const int64_t* off,
+              double* tmp, double* out, cudaStream_t st) {
+    if (N > 0) {
+        int rc = with_mpl(m, [&](auto c) {
+            constexpr int MPL = decltype(c)::value;
+            if (f64)
+                k_row_sq<double, MPL><<<(unsigned)((N + 7) / 8), 256, 0, st>>>(N, m, (const double*)Y, ldy, tmp);
+            else
+                k_row_sq<float, MPL><<<(unsigned)((N + 7) / 8), 256, 0, st>>>(N, m, (const float*)Y, ldy, tmp);
+            return (int)cudaGetLastError();
+        });
+        if (rc) return rc;
+    }
+    k_shard_sum<<<P, 256, 0, st>>>(off, tmp, out, 0);
+    return (int)cudaGetLastError();
+}
 
 int shard_sum(int P, const int64_t* off, const double* v, double* out, int do_sqrt, cudaStream_t st) {
     k_shard_sum<<<P, 256, 0, st>>>(off, v, out, do_sqrt);

@@ -20,6 +20,9 @@ struct ModWs {
     int32_t* deficient;
     int8_t* depmask;
     void* chol;
+    double* wsq;
+    double* ysqp;
+    int32_t* need;
     unsigned char* end;
 };
 
@@ -43,6 +46,7 @@ struct ModArgs {
     int32_t* deficient_out;  // P (optional)
     int64_t* nnz_out;        // P (optional)
     double rank_rcond;
+    const double* ysq_shard;  // optional (P): ||Y_p||_F^2, else computed
     void* ws;
 };
 
@@ -71,6 +75,8 @@ template <typename T>
 int residual_sq(int64_t N, int m, int K, int cap, int P, const int64_t* off, const T* Y, int64_t ldy,
                 const int32_t* idx, const T* val, const int32_t* counts, const double* D,
                 double* rsq, double* ysq, cudaStream_t st);
+int shard_ysq(int P, int64_t N, int m, const void* Y, int64_t ldy, bool f64, const int64_t* off,
+              double* tmp, double* out, cudaStream_t st);
 int shard_sum(int P, const int64_t* off, const double* v, double* out, int do_sqrt, cudaStream_t st);
 int usage_direct(int64_t N, int K, int cap, int P, const int64_t* off, const int32_t* idx,
                  const int32_t* counts, int32_t* usage, cudaStream_t st);

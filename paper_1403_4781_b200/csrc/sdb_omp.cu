@@ -377,7 +377,36 @@ constexpr int FAST_CAP = 32;
 constexpr int FAST_TRI = FAST_CAP * (FAST_CAP + 1) / 2;
 
 __host__ __device__ inline int fast_warp_floats(int cap, int m) {
-    return FAST_TRI + 3 * FAST_CAP + cap * m;  // L, tmp, x, ids(as int), Dsel
+    return FAST_TRI + 4 * FAST_CAP + cap * m;  // L, 1/diag, tmp, x, ids(as int), Dsel
+}
+
+// lane owns the KPL consecutive atoms [lane*KPL, lane*KPL + KPL): rows of
+// alpha0 and G are read with vector loads when the shape allows it.
+template <int KPL>
+__device__ __forceinline__ void load_row(float (&v)[KPL], const float* __restrict__ row, int lane,
+                                         int K, bool vec) {
+    const int j0 = lane * KPL;
+    if constexpr (KPL % 4 == 0) {
+        if (vec) {
+#pragma unroll
+            for (int k = 0; k < KPL; k += 4) {
+                const float4 q = __ldg(reinterpret_cast<const float4*>(row + j0 + k));
+                v[k] = q.x; v[k + 1] = q.y; v[k + 2] = q.z; v[k + 3] = q.w;
+            }
+            return;
+        }
+    } else if constexpr (KPL % 2 == 0) {
+        if (vec) {
+#pragma unroll
+            for (int k = 0; k < KPL; k += 2) {
+                const float2 q = __ldg(reinterpret_cast<const float2*>(row + j0 + k));
+                v[k] = q.x; v[k + 1] = q.y;
+            }
+            return;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < KPL; ++k) v[k] = (j0 + k < K) ? __ldg(row + j0 + k) : 0.0f;
 }
 
 template <int KPL, int MPL>
@@ -389,11 +418,13 @@ k_omp_fast(OmpArgs<float> a) {
     const int wpb = blockDim.x >> 5;
     const int m = a.m, K = a.K, cap = a.cap;
     float* Ls = fsm + (int64_t)wib * fast_warp_floats(cap, m);
-    float* tmp = Ls + FAST_TRI;
+    float* invd = Ls + FAST_TRI;
+    float* tmp = invd + FAST_CAP;
     float* xs = tmp + FAST_CAP;
     int* ids = (int*)(xs + FAST_CAP);
     float* Dsel = (float*)(ids + FAST_CAP);
     const float eps = a.eps;
+    const int j0 = lane * KPL;
 
     const int64_t gw = (int64_t)blockIdx.x * wpb + wib;
     const int64_t nw = (int64_t)gridDim.x * wpb;
@@ -401,21 +432,20 @@ k_omp_fast(OmpArgs<float> a) {
     const int64_t i_begin = gw * per;
     const int64_t i_end = min(a.N, i_begin + per);
     if (i_begin >= i_end) return;
+    const bool vec_a = (K == 32 * KPL) && ((a.lda * 4) % 16 == 0) && (((uintptr_t)a.alpha0 & 15) == 0);
+    const bool vec_g = (K == 32 * KPL) && ((K * 4) % 16 == 0) && (((uintptr_t)a.G & 15) == 0);
 
     int p = shard_of(a.shard_off, a.P, i_begin);
     int64_t p_end = a.shard_off[p + 1];
 
     float c0n[KPL], yn[MPL];
     auto fetch = [&](int64_t i) {
-#pragma unroll
-        for (int k = 0; k < KPL; ++k) {
-            const int j = lane + 32 * k;
-            c0n[k] = (j < K) ? __ldg(a.alpha0 + i * a.lda + j) : 0.0f;
-        }
+        load_row<KPL>(c0n, a.alpha0 + i * a.lda, lane, K, vec_a);
+        const float* yr = a.Y + i * a.ldy;
 #pragma unroll
         for (int q = 0; q < MPL; ++q) {
             const int r = lane + 32 * q;
-            yn[q] = (r < m) ? __ldg(a.Y + i * a.ldy + r) : 0.0f;
+            yn[q] = (r < m) ? __ldg(yr + r) : 0.0f;
         }
     };
     fetch(i_begin);
@@ -429,6 +459,7 @@ k_omp_fast(OmpArgs<float> a) {
         if (i + 1 < i_end) fetch(i + 1);
         const float* __restrict__ Gp = a.G + (int64_t)p * K * K;
         const float* __restrict__ Dp = a.D + (int64_t)p * K * m;
+        const float* __restrict__ arow = a.alpha0 + i * a.lda;
 
         float ysq = 0.0f;
 #pragma unroll
@@ -437,28 +468,25 @@ k_omp_fast(OmpArgs<float> a) {
         float rnorm = __fsqrt_rn(ysq);
         int n = 0, status = 0;
         if (!(rnorm <= eps || rnorm == 0.0f)) {
-            uint32_t selbits = 0;
+            uint32_t selbits = 0;  // bit k: atom j0 + k is in the support
             for (int step = 0; step < cap; ++step) {
                 float corr[KPL];
 #pragma unroll
                 for (int k = 0; k < KPL; ++k) corr[k] = c0[k];
                 for (int t = 0; t < n; ++t) {
+                    float g[KPL];
+                    load_row<KPL>(g, Gp + (int64_t)ids[t] * K, lane, K, vec_g);
                     const float coef = xs[t];
-                    const float* __restrict__ g = Gp + (int64_t)ids[t] * K;
 #pragma unroll
-                    for (int k = 0; k < KPL; ++k) {
-                        const int j = lane + 32 * k;
-                        if (j < K) corr[k] = fmaf(-__ldg(g + j), coef, corr[k]);
-                    }
+                    for (int k = 0; k < KPL; ++k) corr[k] = fmaf(-g[k], coef, corr[k]);
                 }
-                uint32_t bits[KPL];
                 uint32_t lmax = 0;
 #pragma unroll
                 for (int k = 0; k < KPL; ++k) {
-                    const int j = lane + 32 * k;
-                    const bool ok = (j < K) && !((selbits >> k) & 1u);
-                    bits[k] = ok ? __float_as_uint(fabsf(corr[k])) : 0u;
-                    lmax = max(lmax, bits[k]);
+                    const uint32_t bk = ((selbits >> k) & 1u) || (j0 + k >= K)
+                                            ? 0u : (__float_as_uint(corr[k]) & 0x7fffffffu);
+                    corr[k] = __uint_as_float(bk);
+                    lmax = max(lmax, bk);
                 }
                 const uint32_t cbits = __reduce_max_sync(SDB_FULL, lmax);
                 const float cmax = __uint_as_float(cbits);
@@ -466,36 +494,38 @@ k_omp_fast(OmpArgs<float> a) {
                 int cand = 0x7fffffff;
 #pragma unroll
                 for (int k = KPL - 1; k >= 0; --k)
-                    if (bits[k] == cbits) cand = lane + 32 * k;
+                    if (__float_as_uint(corr[k]) == cbits) cand = j0 + k;
                 const int best = (int)__reduce_min_sync(SDB_FULL, (unsigned)cand);
 
-                // Cholesky row of the new atom (column sweep, lane t -> w_t)
+                // Cholesky row of the new atom (column sweep: lane t -> w_t)
                 float* Lrow = Ls + n * (n + 1) / 2;
                 float gacc = (lane < n) ? __ldg(Gp + (int64_t)ids[lane] * K + best) : 0.0f;
                 float wme = 0.0f;
                 for (int u = 0; u < n; ++u) {
-                    const float wu = __fdiv_rn(__shfl_sync(SDB_FULL, gacc, u), Ls[u * (u + 1) / 2 + u]);
+                    const float wu = __shfl_sync(SDB_FULL, gacc, u) * invd[u];
                     if (lane == u) wme = wu;
-                    if (lane > u && lane < n) gacc = fmaf(-Ls[lane * (lane + 1) / 2 + u], wu, gacc);
+                    else if (lane > u && lane < n) gacc = fmaf(-Ls[lane * (lane + 1) / 2 + u], wu, gacc);
                 }
                 const float dsq = __ldg(Gp + (int64_t)best * K + best) -
                                   warp_sum(lane < n ? wme * wme : 0.0f);
                 if (dsq <= a.guard) { status = 2; break; }
-                float cb = 0.0f;
-#pragma unroll
-                for (int k = 0; k < KPL; ++k)
-                    if (k == (best >> 5)) cb = c0[k];
-                cb = __shfl_sync(SDB_FULL, cb, best & 31);
+                const float cb = __ldg(arow + best);   // c0[best] (L1 hit)
                 const float ldiag = __fsqrt_rn(dsq);
+                const float inv = 1.0f / ldiag;
                 if (lane < n) Lrow[lane] = wme;
-                if (lane == 0) { Lrow[n] = ldiag; ids[n] = best; }
-                // cache the atom's column for the residual
-                const float* dcol = Dp + (int64_t)best * m;
-                for (int r = lane; r < m; r += 32) Dsel[n * m + r] = __ldg(dcol + r);
-                if (lane == (best & 31)) selbits |= 1u << (best >> 5);
-                // forward: only tmp[n] is new
-                const float part = (lane < n) ? wme * tmp[lane] : 0.0f;
-                const float tn = __fdiv_rn(cb - warp_sum(part), ldiag);
+                if (lane == 0) { Lrow[n] = ldiag; invd[n] = inv; ids[n] = best; }
+                {   // cache the atom's column for the residual
+                    const float* dcol = Dp + (int64_t)best * m;
+                    float* dst = Dsel + n * m;
+#pragma unroll
+                    for (int q = 0; q < MPL; ++q) {
+                        const int r = lane + 32 * q;
+                        if (r < m) dst[r] = __ldg(dcol + r);
+                    }
+                }
+                if (lane == best / KPL) selbits |= 1u << (best - j0);
+                // forward substitution: only tmp[n] is new
+                const float tn = (cb - warp_sum(lane < n ? wme * tmp[lane] : 0.0f)) * inv;
                 n += 1;
                 __syncwarp();
                 if (lane == 0) tmp[n - 1] = tn;
@@ -504,10 +534,9 @@ k_omp_fast(OmpArgs<float> a) {
                 float bacc = (lane < n) ? tmp[lane] : 0.0f;
                 float xme = 0.0f;
                 for (int u = n - 1; u >= 0; --u) {
-                    const float* Lu = Ls + u * (u + 1) / 2;
-                    const float xu = __fdiv_rn(__shfl_sync(SDB_FULL, bacc, u), Lu[u]);
+                    const float xu = __shfl_sync(SDB_FULL, bacc, u) * invd[u];
                     if (lane == u) xme = xu;
-                    if (lane < u) bacc = fmaf(-Lu[lane], xu, bacc);
+                    else if (lane < u) bacc = fmaf(-Ls[u * (u + 1) / 2 + lane], xu, bacc);
                 }
                 if (lane < n) xs[lane] = xme;
                 __syncwarp();
@@ -517,10 +546,11 @@ k_omp_fast(OmpArgs<float> a) {
                 for (int q = 0; q < MPL; ++q) rr[q] = y[q];
                 for (int t = 0; t < n; ++t) {
                     const float xt = xs[t];
+                    const float* dc = Dsel + t * m;
 #pragma unroll
                     for (int q = 0; q < MPL; ++q) {
                         const int r = lane + 32 * q;
-                        if (r < m) rr[q] = fmaf(-Dsel[t * m + r], xt, rr[q]);
+                        if (r < m) rr[q] = fmaf(-dc[r], xt, rr[q]);
                     }
                 }
                 float rs = 0.0f;
@@ -531,9 +561,9 @@ k_omp_fast(OmpArgs<float> a) {
             }
         }
         __syncwarp();
-        for (int t = lane; t < cap; t += 32) {
-            a.idx[i * cap + t] = (t < n) ? ids[t] : 0;
-            a.val[i * cap + t] = (t < n) ? xs[t] : 0.0f;
+        if (lane < cap) {
+            a.idx[i * cap + lane] = (lane < n) ? ids[lane] : 0;
+            a.val[i * cap + lane] = (lane < n) ? xs[lane] : 0.0f;
         }
         if (lane == 0) {
             a.counts[i] = n;
