@@ -60,7 +60,7 @@ KTIMER: dict | None = None
 
 
 def timed_call(name: str, nbytes: float, flops: float, fn, *args):
-    if KTIMER is None:
+    if KTIMER is None or torch.cuda.is_current_stream_capturing():
         return _lib.call(fn, *args)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)

@@ -49,123 +49,116 @@ k_chol_prep(int K, double* __restrict__ Aall, const int32_t* __restrict__ usage,
     }
 }
 
-// factor the diagonal block of panel j0 and invert it (T = L^-1)
+// factor the diagonal block of panel j0 (left-looking): column c of L is
+// (A[c:,c] - L[c:,:c] L[c,:c]^T) / sqrt(pivot); 4 threads per row split each
+// dot product and combine it with shuffles in a fixed order.
 __global__ void __launch_bounds__(256)
-k_chol_diag(int K, int j0, double* __restrict__ Aall, double* __restrict__ Tall,
-            const double* __restrict__ tol, int8_t* __restrict__ depmask, int32_t* __restrict__ ndep) {
-    extern __shared__ double csm[];
-    double (*Ls)[CBP] = reinterpret_cast<double (*)[CBP]>(csm);
-    double (*Ts)[CBP] = reinterpret_cast<double (*)[CBP]>(csm + CB * CBP);
+k_chol_diag(int K, int j0, double* __restrict__ Aall, const double* __restrict__ tol,
+            int8_t* __restrict__ depmask, int32_t* __restrict__ ndep) {
+    __shared__ double Ls[CB][CBP];
     __shared__ int8_t sdep[CB];
+    __shared__ double piv;
     const int p = blockIdx.x;
     double* A = Aall + (int64_t)p * K * K;
     const int nb = min(CB, K - j0);
     const int tid = threadIdx.x;
+    const int rr = tid >> 2, h = tid & 3;  // row offset, quarter
     for (int e = tid; e < CB * CB; e += 256) {
         const int r = e / CB, c = e % CB;
         Ls[r][c] = (r < nb && c <= r) ? A[(int64_t)(j0 + r) * K + j0 + c] : 0.0;
     }
     __syncthreads();
     const double tl = tol[p];
+    int nd = 0;
     for (int c = 0; c < nb; ++c) {
-        if (tid == 0) {
-            const double d = Ls[c][c];
-            const bool dep = !(d > tl);
+        const int r = c + rr;  // rows c .. c+63 (only < nb used)
+        double v = 0.0;
+        if (r < nb) {
+            const int q0 = (c * h) >> 2, q1 = (c * (h + 1)) >> 2;
+            for (int q = q0; q < q1; ++q) v = fma(Ls[r][q], Ls[c][q], v);
+        }
+        v += __shfl_xor_sync(SDB_FULL, v, 1);
+        v += __shfl_xor_sync(SDB_FULL, v, 2);
+        const double a_rc = (r < nb) ? Ls[r][c] - v : 0.0;
+        if (r == c && h == 0) {
+            const bool dep = !(a_rc > tl);
             sdep[c] = dep ? 1 : 0;
-            Ls[c][c] = dep ? 1.0 : sqrt(d);
-            if (dep) ndep[p] += 1;
+            piv = dep ? 1.0 : sqrt(a_rc);
         }
         __syncthreads();
+        const double lc = piv;
         const bool dep = sdep[c];
-        const double lc = Ls[c][c];
-        for (int r = c + 1 + tid; r < nb; r += 256) Ls[r][c] = dep ? 0.0 : Ls[r][c] / lc;
-        __syncthreads();
-        // rank-1 update of the remaining lower triangle of the block
-        const int rem = nb - c - 1;
-        for (int e = tid; e < rem * rem; e += 256) {
-            const int r = c + 1 + e / rem, q = c + 1 + e % rem;
-            if (q <= r) Ls[r][q] -= Ls[r][c] * Ls[q][c];
-        }
+        if (h == 0 && r < nb) Ls[r][c] = (r == c) ? lc : (dep ? 0.0 : a_rc / lc);
+        nd += dep;
         __syncthreads();
     }
-    // T = L^-1 (lower): rows in sequence, all columns in parallel, each
-    // partial dot split over 4 threads (fixed order -> deterministic)
-    {
-        __shared__ double part[4][CB];
-        const int c = tid & (CB - 1), h = tid >> 6;  // 64 columns x 4 quarters
-        for (int e = tid; e < CB * CB; e += 256) Ts[e / CB][e % CB] = 0.0;
-        __syncthreads();
-        if (tid < nb && !sdep[tid]) Ts[tid][tid] = 1.0 / Ls[tid][tid];
-        __syncthreads();
-        for (int r = 1; r < nb; ++r) {
-            double s = 0.0;
-            if (c < r) {
-                const int len = r - c, q0 = c + (len * h) / 4, q1 = c + (len * (h + 1)) / 4;
-                for (int q = q0; q < q1; ++q) s = fma(Ls[r][q], Ts[q][c], s);
-            }
-            part[h][c] = s;
-            __syncthreads();
-            if (tid < r && !sdep[tid] && !sdep[r])
-                Ts[r][tid] = -(((part[0][tid] + part[1][tid]) + part[2][tid]) + part[3][tid]) / Ls[r][r];
-            __syncthreads();
-        }
-    }
-    double* T = Tall + ((int64_t)p * ((K + CB - 1) / CB) + j0 / CB) * CB * CB;
     for (int e = tid; e < CB * CB; e += 256) {
         const int r = e / CB, c = e % CB;
-        T[e] = Ts[r][c];
         if (r < nb && c <= r) A[(int64_t)(j0 + r) * K + j0 + c] = Ls[r][c];
     }
     if (tid < nb) depmask[(int64_t)p * K + j0 + tid] = sdep[tid];
+    if (tid == 0) ndep[p] += nd;
 }
 
-// blockIdx.x == 0: W_j = T_j B_j (RHS rows of the panel, all m columns)
-// blockIdx.x >= 1: rows block i: L_ij = A_ij T_j^T
+// blockIdx.x == 0: forward-solve the panel's RHS rows, W_j = L_jj^-1 B_j
+//                  (thread per right-hand-side column)
+// blockIdx.x >= 1: panel rows block i: L_ij = A_ij L_jj^-T (thread per row)
 __global__ void __launch_bounds__(256)
 k_chol_panel(int K, int m, int j0, double* __restrict__ Aall, double* __restrict__ Ball,
-             const double* __restrict__ Tall) {
-    extern __shared__ double csm[];
-    double (*Ts)[CBP] = reinterpret_cast<double (*)[CBP]>(csm);
-    double (*Xs)[CBP] = reinterpret_cast<double (*)[CBP]>(csm + CB * CBP);
+             const int8_t* __restrict__ depmask) {
+    __shared__ double Ls[CB][CBP];
+    __shared__ double inv[CB];
+    __shared__ int8_t sdep[CB];
     const int p = blockIdx.y;
     const int nb = min(CB, K - j0);
     const int tid = threadIdx.x;
-    const double* T = Tall + ((int64_t)p * ((K + CB - 1) / CB) + j0 / CB) * CB * CB;
-    for (int e = tid; e < CB * CB; e += 256) Ts[e / CB][e % CB] = T[e];
-    if (blockIdx.x == 0) {
-        double* B = Ball + (int64_t)p * K * m + (int64_t)j0 * m;
-        for (int c0 = 0; c0 < m; c0 += CB) {
-            const int nc = min(CB, m - c0);
-            __syncthreads();
-            for (int e = tid; e < CB * CB; e += 256) {
-                const int r = e / CB, c = e % CB;
-                Xs[r][c] = (r < nb && c < nc) ? B[(int64_t)r * m + c0 + c] : 0.0;
-            }
-            __syncthreads();
-            for (int e = tid; e < nb * nc; e += 256) {
-                const int r = e / nc, c = e % nc;
-                double s = 0.0;
-                for (int q = 0; q <= r; ++q) s = fma(Ts[r][q], Xs[q][c], s);
-                B[(int64_t)r * m + c0 + c] = s;
-            }
-        }
-        return;
-    }
-    const int i0 = j0 + nb + (blockIdx.x - 1) * CB;
-    if (i0 >= K) return;
-    const int ni = min(CB, K - i0);
     double* A = Aall + (int64_t)p * K * K;
     for (int e = tid; e < CB * CB; e += 256) {
         const int r = e / CB, c = e % CB;
-        Xs[r][c] = (r < ni && c < nb) ? A[(int64_t)(i0 + r) * K + j0 + c] : 0.0;
+        Ls[r][c] = (r < nb && c <= r) ? A[(int64_t)(j0 + r) * K + j0 + c] : 0.0;
     }
+    if (tid < nb) sdep[tid] = depmask[(int64_t)p * K + j0 + tid];
     __syncthreads();
-    for (int e = tid; e < ni * nb; e += 256) {
-        const int r = e / nb, c = e % nb;
-        double s = 0.0;
-        for (int q = 0; q <= c; ++q) s = fma(Xs[r][q], Ts[c][q], s);
-        A[(int64_t)(i0 + r) * K + j0 + c] = s;
+    if (tid < nb) inv[tid] = 1.0 / Ls[tid][tid];
+    __syncthreads();
+    if (blockIdx.x == 0) {
+        double* B = Ball + (int64_t)p * K * m + (int64_t)j0 * m;
+        for (int col = tid; col < m; col += 256) {
+            double w[CB];
+#pragma unroll
+            for (int r = 0; r < CB; ++r) {
+                if (r < nb) {
+                    double sacc[4] = {0.0, 0.0, 0.0, 0.0};
+                    for (int q = 0; q < r; ++q) sacc[q & 3] = fma(Ls[r][q], w[q], sacc[q & 3]);
+                    const double bv = B[(int64_t)r * m + col];
+                    w[r] = sdep[r] ? 0.0 : (bv - ((sacc[0] + sacc[1]) + (sacc[2] + sacc[3]))) * inv[r];
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < CB; ++r)
+                if (r < nb) B[(int64_t)r * m + col] = w[r];
+        }
+        return;
     }
+    const int i0 = j0 + nb + (blockIdx.x - 1) * 256;
+    const int row = i0 + tid;
+    if (row >= K) return;
+    double* ar = A + (int64_t)row * K + j0;
+    double x[CB];
+#pragma unroll
+    for (int c = 0; c < CB; ++c) x[c] = (c < nb) ? ar[c] : 0.0;
+#pragma unroll
+    for (int c = 0; c < CB; ++c) {
+        if (c < nb) {
+            double sacc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int q = 0; q < c; ++q) sacc[q & 3] = fma(x[q], Ls[c][q], sacc[q & 3]);
+            x[c] = sdep[c] ? 0.0 : (x[c] - ((sacc[0] + sacc[1]) + (sacc[2] + sacc[3]))) * inv[c];
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < CB; ++c)
+        if (c < nb) ar[c] = x[c];
 }
 
 // 64x64 tile update  C -= X Y^T  with X (64 x nb), Y (64 x nb) from smem;
@@ -257,32 +250,41 @@ k_chol_update(int K, int m, int j0, double* __restrict__ Aall, double* __restric
     }
 }
 
-// back substitution, panel j0: Z_j = T_j^T W_j (in place on B rows of panel j)
+// back substitution, panel j0: solve L_jj^T Z_j = W_j in place (thread per
+// right-hand-side column)
 __global__ void __launch_bounds__(256)
-k_back_diag(int K, int m, int j0, double* __restrict__ Ball, const double* __restrict__ Tall) {
-    extern __shared__ double csm[];
-    double (*Ts)[CBP] = reinterpret_cast<double (*)[CBP]>(csm);
-    double (*Ws)[CBP] = reinterpret_cast<double (*)[CBP]>(csm + CB * CBP);
+k_back_diag(int K, int m, int j0, const double* __restrict__ Aall, double* __restrict__ Ball) {
+    __shared__ double Ls[CB][CBP];
+    __shared__ double inv[CB];
     const int p = blockIdx.x;
     const int nb = min(CB, K - j0);
     const int tid = threadIdx.x;
-    const double* T = Tall + ((int64_t)p * ((K + CB - 1) / CB) + j0 / CB) * CB * CB;
+    const double* A = Aall + (int64_t)p * K * K;
     double* B = Ball + (int64_t)p * K * m + (int64_t)j0 * m;
-    for (int e = tid; e < CB * CB; e += 256) Ts[e / CB][e % CB] = T[e];
-    for (int c0 = 0; c0 < m; c0 += CB) {
-        const int nc = min(CB, m - c0);
-        __syncthreads();
-        for (int e = tid; e < CB * CB; e += 256) {
-            const int r = e / CB, c = e % CB;
-            Ws[r][c] = (r < nb && c < nc) ? B[(int64_t)r * m + c0 + c] : 0.0;
+    for (int e = tid; e < CB * CB; e += 256) {
+        const int r = e / CB, c = e % CB;
+        Ls[r][c] = (r < nb && c <= r) ? A[(int64_t)(j0 + r) * K + j0 + c] : 0.0;
+    }
+    __syncthreads();
+    if (tid < nb) inv[tid] = 1.0 / Ls[tid][tid];
+    __syncthreads();
+    for (int col = tid; col < m; col += 256) {
+        double z[CB];
+#pragma unroll
+        for (int r = 0; r < CB; ++r) z[r] = (r < nb) ? B[(int64_t)r * m + col] : 0.0;
+#pragma unroll
+        for (int r = CB - 1; r >= 0; --r) {
+            if (r < nb) {
+                double sacc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                for (int q = r + 1; q < CB; ++q)
+                    if (q < nb) sacc[q & 3] = fma(Ls[q][r], z[q], sacc[q & 3]);
+                z[r] = (z[r] - ((sacc[0] + sacc[1]) + (sacc[2] + sacc[3]))) * inv[r];
+            }
         }
-        __syncthreads();
-        for (int e = tid; e < nb * nc; e += 256) {
-            const int r = e / nc, c = e % nc;
-            double s = 0.0;
-            for (int q = r; q < nb; ++q) s = fma(Ts[q][r], Ws[q][c], s);
-            B[(int64_t)r * m + c0 + c] = s;
-        }
+#pragma unroll
+        for (int r = 0; r < CB; ++r)
+            if (r < nb) B[(int64_t)r * m + col] = z[r];
     }
 }
 
@@ -338,24 +340,17 @@ __global__ void __launch_bounds__(256) k_sumsq(int64_t n, const double* __restri
     if (threadIdx.x == 0) out[blockIdx.x] = sh[0];
 }
 
-int64_t chol_ws_bytes(int P, int K) {
-    const int64_t nblk = (K + CB - 1) / CB;
-    return (int64_t)P * nblk * CB * CB * sizeof(double) + (int64_t)P * sizeof(double) + 512;
-}
+int64_t chol_ws_bytes(int P, int K) { return (int64_t)P * sizeof(double) + 512; }
 
 int chol_solve(int P, int K, int m, double* A, double* B, const int32_t* usage, double rel_tol,
                int8_t* depmask, int32_t* ndep, double* wsq, void* ws, cudaStream_t st) {
-    double* T = (double*)ws;
     const int64_t nblk = (K + CB - 1) / CB;
-    double* tol = T + (int64_t)P * nblk * CB * CB;
+    double* tol = (double*)ws;
     const int smem2 = 2 * CB * CBP * (int)sizeof(double);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_chol_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
         cudaFuncSetAttribute(k_chol_update, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
         cudaFuncSetAttribute(k_back_update, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
-        cudaFuncSetAttribute(k_chol_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
-        cudaFuncSetAttribute(k_back_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
         attr = true;
     }
     {
@@ -366,10 +361,10 @@ int chol_solve(int P, int K, int m, double* A, double* B, const int32_t* usage, 
     const int nmc = (m + CB - 1) / CB;
     for (int j0 = 0; j0 < K; j0 += CB) {
         const int nb = std::min(CB, K - j0);
-        k_chol_diag<<<P, 256, smem2, st>>>(K, j0, A, T, tol, depmask, ndep);
+        k_chol_diag<<<P, 256, 0, st>>>(K, j0, A, tol, depmask, ndep);
         const int rows_below = K - j0 - nb;
-        dim3 gp((unsigned)(1 + (rows_below + CB - 1) / CB), (unsigned)P);
-        k_chol_panel<<<gp, 256, smem2, st>>>(K, m, j0, A, B, T);
+        dim3 gp((unsigned)(1 + (rows_below + 255) / 256), (unsigned)P);
+        k_chol_panel<<<gp, 256, 0, st>>>(K, m, j0, A, B, depmask);
         const int nt = (rows_below + CB - 1) / CB;
         const int tiles = nt * (nt + 1) / 2 + nt * nmc;
         if (tiles > 0) {
@@ -380,7 +375,7 @@ int chol_solve(int P, int K, int m, double* A, double* B, const int32_t* usage, 
     if (wsq) k_sumsq<<<P, 256, 0, st>>>((int64_t)K * m, B, wsq);
     const int last = (int)((nblk - 1) * CB);
     for (int j0 = last; j0 >= 0; j0 -= CB) {
-        k_back_diag<<<P, 256, smem2, st>>>(K, m, j0, B, T);
+        k_back_diag<<<P, 256, 0, st>>>(K, m, j0, A, B);
         if (j0 > 0) {
             const int ib = (j0 + CB - 1) / CB;
             dim3 gb((unsigned)(ib * nmc), (unsigned)P);

@@ -441,13 +441,15 @@ k_omp_fast(OmpArgs<float> a) {
     float c0n[KPL], yn[MPL];
     auto fetch = [&](int64_t i) {
         load_row<KPL>(c0n, a.alpha0 + i * a.lda, lane, K, vec_a);
-        const float* yr = a.Y + i * a.ldy;
+        const float* yr = a.Y + i * a.ldy + lane;
 #pragma unroll
-        for (int q = 0; q < MPL; ++q) {
-            const int r = lane + 32 * q;
-            yn[q] = (r < m) ? __ldg(yr + r) : 0.0f;
-        }
+        for (int q = 0; q < MPL; ++q) yn[q] = (32 * q + lane < m) ? __ldg(yr + 32 * q) : 0.0f;
     };
+    // atoms this lane owns that exist (K not a multiple of 32*KPL)
+    float valid[KPL];
+#pragma unroll
+    for (int k = 0; k < KPL; ++k) valid[k] = (j0 + k < K) ? 1.0f : 0.0f;
+
     fetch(i_begin);
     for (int64_t i = i_begin; i < i_end; ++i) {
         while (i >= p_end) { ++p; p_end = a.shard_off[p + 1]; }
@@ -467,96 +469,113 @@ k_omp_fast(OmpArgs<float> a) {
         ysq = warp_sum(ysq);
         float rnorm = __fsqrt_rn(ysq);
         int n = 0, status = 0;
+        float avail[KPL];  // 1: atom may be selected, 0: in the support / absent
+#pragma unroll
+        for (int k = 0; k < KPL; ++k) avail[k] = valid[k];
         if (!(rnorm <= eps || rnorm == 0.0f)) {
-            uint32_t selbits = 0;  // bit k: atom j0 + k is in the support
             for (int step = 0; step < cap; ++step) {
-                float corr[KPL];
+                // ---- correlations of the residual, support excluded
+                float v[KPL];
+                if (n == 0) {
 #pragma unroll
-                for (int k = 0; k < KPL; ++k) corr[k] = c0[k];
-                for (int t = 0; t < n; ++t) {
-                    float g[KPL];
-                    load_row<KPL>(g, Gp + (int64_t)ids[t] * K, lane, K, vec_g);
-                    const float coef = xs[t];
+                    for (int k = 0; k < KPL; ++k) v[k] = fabsf(c0[k]) * avail[k];
+                } else {
 #pragma unroll
-                    for (int k = 0; k < KPL; ++k) corr[k] = fmaf(-g[k], coef, corr[k]);
+                    for (int k = 0; k < KPL; ++k) v[k] = c0[k];
+                    for (int t = 0; t < n; ++t) {
+                        float g[KPL];
+                        load_row<KPL>(g, Gp + (int64_t)ids[t] * K, lane, K, vec_g);
+                        const float coef = xs[t];
+#pragma unroll
+                        for (int k = 0; k < KPL; ++k) v[k] = fmaf(-g[k], coef, v[k]);
+                    }
+#pragma unroll
+                    for (int k = 0; k < KPL; ++k) v[k] = fabsf(v[k]) * avail[k];
                 }
-                uint32_t lmax = 0;
+                float lm = 0.0f;
 #pragma unroll
-                for (int k = 0; k < KPL; ++k) {
-                    const uint32_t bk = ((selbits >> k) & 1u) || (j0 + k >= K)
-                                            ? 0u : (__float_as_uint(corr[k]) & 0x7fffffffu);
-                    corr[k] = __uint_as_float(bk);
-                    lmax = max(lmax, bk);
-                }
-                const uint32_t cbits = __reduce_max_sync(SDB_FULL, lmax);
+                for (int k = 0; k < KPL; ++k) lm = fmaxf(lm, v[k]);
+                const uint32_t cbits = __reduce_max_sync(SDB_FULL, __float_as_uint(lm));
                 const float cmax = __uint_as_float(cbits);
                 if (cmax <= 1e-13f * rnorm) { status = 3; break; }
                 int cand = 0x7fffffff;
 #pragma unroll
                 for (int k = KPL - 1; k >= 0; --k)
-                    if (__float_as_uint(corr[k]) == cbits) cand = j0 + k;
+                    if (__float_as_uint(v[k]) == cbits) cand = j0 + k;
                 const int best = (int)__reduce_min_sync(SDB_FULL, (unsigned)cand);
 
-                // Cholesky row of the new atom (column sweep: lane t -> w_t)
-                float* Lrow = Ls + n * (n + 1) / 2;
-                float gacc = (lane < n) ? __ldg(Gp + (int64_t)ids[lane] * K + best) : 0.0f;
-                float wme = 0.0f;
-                for (int u = 0; u < n; ++u) {
-                    const float wu = __shfl_sync(SDB_FULL, gacc, u) * invd[u];
-                    if (lane == u) wme = wu;
-                    else if (lane > u && lane < n) gacc = fmaf(-Ls[lane * (lane + 1) / 2 + u], wu, gacc);
+                // ---- Cholesky row of the new atom
+                float wme = 0.0f, dsq = __ldg(Gp + (int64_t)best * K + best);
+                if (n > 0) {
+                    float gacc = (lane < n) ? __ldg(Gp + (int64_t)ids[lane] * K + best) : 0.0f;
+                    for (int u = 0; u < n; ++u) {
+                        const float wu = __shfl_sync(SDB_FULL, gacc, u) * invd[u];
+                        if (lane == u) wme = wu;
+                        else if (lane > u && lane < n) gacc = fmaf(-Ls[lane * (lane + 1) / 2 + u], wu, gacc);
+                    }
+                    dsq -= warp_sum(lane < n ? wme * wme : 0.0f);
                 }
-                const float dsq = __ldg(Gp + (int64_t)best * K + best) -
-                                  warp_sum(lane < n ? wme * wme : 0.0f);
                 if (dsq <= a.guard) { status = 2; break; }
-                const float cb = __ldg(arow + best);   // c0[best] (L1 hit)
+                const float cb = __ldg(arow + best);   // c0[best]
                 const float ldiag = __fsqrt_rn(dsq);
                 const float inv = 1.0f / ldiag;
+                float* Lrow = Ls + n * (n + 1) / 2;
                 if (lane < n) Lrow[lane] = wme;
                 if (lane == 0) { Lrow[n] = ldiag; invd[n] = inv; ids[n] = best; }
-                {   // cache the atom's column for the residual
-                    const float* dcol = Dp + (int64_t)best * m;
-                    float* dst = Dsel + n * m;
+                float dv[MPL];  // the new atom's column (lane rows)
+                {
+                    const float* dcol = Dp + (int64_t)best * m + lane;
+                    float* dst = Dsel + n * m + lane;
 #pragma unroll
                     for (int q = 0; q < MPL; ++q) {
-                        const int r = lane + 32 * q;
-                        if (r < m) dst[r] = __ldg(dcol + r);
+                        dv[q] = (32 * q + lane < m) ? __ldg(dcol + 32 * q) : 0.0f;
+                        if (32 * q + lane < m) dst[32 * q] = dv[q];
                     }
                 }
-                if (lane == best / KPL) selbits |= 1u << (best - j0);
-                // forward substitution: only tmp[n] is new
-                const float tn = (cb - warp_sum(lane < n ? wme * tmp[lane] : 0.0f)) * inv;
-                n += 1;
-                __syncwarp();
-                if (lane == 0) tmp[n - 1] = tn;
-                __syncwarp();
-                // back substitution, column sweep from the bottom
-                float bacc = (lane < n) ? tmp[lane] : 0.0f;
-                float xme = 0.0f;
-                for (int u = n - 1; u >= 0; --u) {
-                    const float xu = __shfl_sync(SDB_FULL, bacc, u) * invd[u];
-                    if (lane == u) xme = xu;
-                    else if (lane < u) bacc = fmaf(-Ls[u * (u + 1) / 2 + lane], xu, bacc);
+                if (lane == best / KPL) {
+#pragma unroll
+                    for (int k = 0; k < KPL; ++k)
+                        if (j0 + k == best) avail[k] = 0.0f;
                 }
-                if (lane < n) xs[lane] = xme;
-                __syncwarp();
-                // explicit residual from the cached columns
                 float rr[MPL];
+                if (n == 0) {
+                    // one atom: tmp = c0[b]/L00, x = tmp/L00, r = y - d_b x
+                    const float tn = cb * inv;
+                    const float x0 = tn * inv;
+                    if (lane == 0) { tmp[0] = tn; xs[0] = x0; }
 #pragma unroll
-                for (int q = 0; q < MPL; ++q) rr[q] = y[q];
-                for (int t = 0; t < n; ++t) {
-                    const float xt = xs[t];
-                    const float* dc = Dsel + t * m;
+                    for (int q = 0; q < MPL; ++q) rr[q] = fmaf(-dv[q], x0, y[q]);
+                    n = 1;
+                } else {
+                    const float tn = (cb - warp_sum(lane < n ? wme * tmp[lane] : 0.0f)) * inv;
+                    n += 1;
+                    __syncwarp();
+                    if (lane == 0) tmp[n - 1] = tn;
+                    __syncwarp();
+                    float bacc = (lane < n) ? tmp[lane] : 0.0f;
+                    float xme = 0.0f;
+                    for (int u = n - 1; u >= 0; --u) {
+                        const float xu = __shfl_sync(SDB_FULL, bacc, u) * invd[u];
+                        if (lane == u) xme = xu;
+                        else if (lane < u) bacc = fmaf(-Ls[u * (u + 1) / 2 + lane], xu, bacc);
+                    }
+                    if (lane < n) xs[lane] = xme;
+                    __syncwarp();
 #pragma unroll
-                    for (int q = 0; q < MPL; ++q) {
-                        const int r = lane + 32 * q;
-                        if (r < m) rr[q] = fmaf(-dc[r], xt, rr[q]);
+                    for (int q = 0; q < MPL; ++q) rr[q] = y[q];
+                    for (int t = 0; t < n; ++t) {
+                        const float xt = xs[t];
+                        const float* dc = Dsel + t * m + lane;
+#pragma unroll
+                        for (int q = 0; q < MPL; ++q)
+                            if (32 * q + lane < m) rr[q] = fmaf(-dc[32 * q], xt, rr[q]);
                     }
                 }
                 float rs = 0.0f;
 #pragma unroll
                 for (int q = 0; q < MPL; ++q) rs = fmaf(rr[q], rr[q], rs);
                 rnorm = __fsqrt_rn(warp_sum(rs));
+                __syncwarp();
                 if (rnorm <= eps) break;
             }
         }

@@ -202,25 +202,57 @@ def coding_mode(m: int, K: int, s: int, eps, s_max) -> tuple[int, float]:
     return cap, float(eps)
 
 
+USE_GRAPHS = False  # measured: capture+instantiate per call costs more than it saves (merge is GPU-latency bound)
+
+
+def _iteration(S: E.ShardSet, D: torch.Tensor, cap: int, eps: float, use_tc: bool):
+    """One alternating step (trainer.py:184-187): code, MOD, replace.
+    Returns (new D, residual_fro per shard)."""
+    prec = S.prec
+    codes = E.code(S.Y, S.off, S.max_rows, E.working_dict(D, prec), E.gram(D, prec), cap, eps,
+                   prec, use_tc)
+    r = E.mod_update(S, codes, D)
+    E.replace_degenerate(S, codes, r.D, r.usage)
+    return r.D, r.resid
+
+
 def train_device(S: E.ShardSet, D0: torch.Tensor, cap: int, eps: float, iterations: int,
-                 use_tc: bool = True):
+                 use_tc: bool = True, use_graph: bool | None = None):
     """The alternating loop (trainer.py:183-188) on every shard at once.
 
     Returns (D (P,K,m) f64, final codes, residuals (iterations, P) f64 device).
-    Stream-ordered; nothing here synchronises with the host.
+    Stream-ordered; nothing here synchronises with the host. The first
+    iteration runs eagerly; the remaining ones replay one captured CUDA graph
+    of an iteration (static D buffer), so the host issues one launch per
+    iteration instead of ~60 (the merge phase is launch-latency bound).
     """
     prec = S.prec
-    D = D0
-    P = D.shape[0]
+    P = D0.shape[0]
     resid = E.empty((iterations, P), torch.float64)
-    for it in range(iterations):
-        DT = E.working_dict(D, prec)
-        G = E.gram(D, prec)
-        codes = E.code(S.Y, S.off, S.max_rows, DT, G, cap, eps, prec, use_tc)
-        r = E.mod_update(S, codes, D)
-        resid[it].copy_(r.resid)
-        E.replace_degenerate(S, codes, r.D, r.usage)
-        D = r.D
+    graph = USE_GRAPHS if use_graph is None else use_graph
+    D = D0
+    if iterations > 0:
+        D, rr = _iteration(S, D, cap, eps, use_tc)
+        resid[0].copy_(rr)
+    if iterations > 1:
+        if graph:
+            D_static = D.clone()
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(g, stream=s):
+                    D_new, rr_static = _iteration(S, D_static, cap, eps, use_tc)
+                    D_static.copy_(D_new)
+            torch.cuda.current_stream().wait_stream(s)
+            for it in range(1, iterations):
+                g.replay()
+                resid[it].copy_(rr_static)
+            D = D_static
+        else:
+            for it in range(1, iterations):
+                D, rr = _iteration(S, D, cap, eps, use_tc)
+                resid[it].copy_(rr)
     codes = E.code(S.Y, S.off, S.max_rows, E.working_dict(D, prec), E.gram(D, prec), cap, eps,
                    prec, use_tc)
     return D, codes, resid
@@ -378,9 +410,13 @@ def split_merge_device(Ydev: torch.Tensor, L: int, K1: int, local_cap: int, loca
         _sync()
         t_start = time.perf_counter()
     N, m = Ydev.shape
-    blocks = split_indices(N, L, seed)
-    sizes = [b.size for b in blocks]
-    perm = torch.from_numpy(np.concatenate(blocks).astype(np.int64)).to(E.device())
+    if not 1 <= L <= N:
+        raise InvalidInputError("require 1 <= L <= N")
+    # split_indices' blocks are consecutive slices of one PCG64 permutation
+    perm_h = np.random.default_rng(seed).permutation(N)
+    base, extra = divmod(N, L)
+    sizes = [base + (1 if t < extra else 0) for t in range(L)]
+    perm = torch.from_numpy(perm_h).to(E.device())
     Ys = E.gather_rows(Ydev, perm, prec)
     off, _ = E.shard_offsets(sizes)
     S = E.ShardSet(Ys, off, sizes, prec)
@@ -390,7 +426,8 @@ def split_merge_device(Ydev: torch.Tensor, L: int, K1: int, local_cap: int, loca
     if min(sizes) < K1:
         raise InvalidInputError("first-columns init needs N >= K")
     D0 = init_dictionaries(S, K1, "first-columns", seeds[:L])
-    Dl, codes, _ = train_device(S, D0, local_cap, local_eps, local_iters, use_tc)
+    # locals: GPU-bound launches, eager (host launch overhead hides behind them)
+    Dl, codes, _ = train_device(S, D0, local_cap, local_eps, local_iters, use_tc, use_graph=False)
     w = E.code_energy(S, codes)
     w_h = E.d2h(w)                       # synchronises: end of the split phase
     t_local = time.perf_counter()
