@@ -4,12 +4,13 @@
 //
 // Right-looking, 64-wide panels; every launch covers all P shards:
 //   prep        mask unused atoms (identity rows/cols), pivot tolerance
-//   per panel j: diag   factor A_jj = L_jj L_jj^T (one CTA), T_j = L_jj^-1
-//                panel  L_ij = A_ij T_j^T (i > j), W_j = T_j B_j
+//   per panel j: diag   A_jj = L_jj L_jj^T (one CTA: two warp-synchronous
+//                       32-wide sub-blocks + a shuffle row sweep)
+//                panel  L_ij = A_ij L_jj^-T (i > j, row sweeps), W_j = L_jj^-1 B_j
 //                update A_ik -= L_ij L_kj^T (lower tiles), B_i -= L_ij W_j
-//   per panel j (descending): Z_j = T_j^T W_j ; W_i -= L_ji^T Z_j (i < j)
+//   per panel j (descending): Z_j = L_jj^-T W_j ; W_i -= L_ji^T Z_j (i < j)
 // Numerically dependent pivots (<= rcond * max used diagonal) drop their atom
-// (zero row/column of T_j), which the caller then treats as dead.
+// (zero column of L, zero solution row), which the caller treats as dead.
 #include "sdb_common.cuh"
 #include "sdb_internal.h"
 #include "sdb_chol.h"
@@ -49,64 +50,96 @@ k_chol_prep(int K, double* __restrict__ Aall, const int32_t* __restrict__ usage,
     }
 }
 
-// factor the diagonal block of panel j0 (left-looking): column c of L is
-// (A[c:,c] - L[c:,:c] L[c,:c]^T) / sqrt(pivot); 4 threads per row split each
-// dot product and combine it with shuffles in a fixed order.
+// ---- row sweep X L^T = A for rows of Xs (4 lanes per row, 8 rows per warp):
+// x_c = (a_c - sum_{q<c} x_q L[c][q]) / L[c][c], written in place into Xs.
+__device__ __forceinline__ void rows_trsm(double (*Xs)[CBP], int nrows, double (*Ls)[CBP],
+                                          const double* inv, const int8_t* sdep, int nb) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int h = lane & 3;
+    const int r = warp * 8 + (lane >> 2);
+    for (int c = 0; c < nb; ++c) {
+        double v = 0.0;
+        if (r < nrows)
+            for (int q = h; q < c; q += 4) v = fma(Xs[r][q], Ls[c][q], v);
+        v += __shfl_xor_sync(SDB_FULL, v, 1);
+        v += __shfl_xor_sync(SDB_FULL, v, 2);
+        if (r < nrows && h == 0) Xs[r][c] = sdep[c] ? 0.0 : (Xs[r][c] - v) * inv[c];
+        __syncwarp();
+    }
+}
+
+// factor the diagonal block of panel j0, right-looking. Thread t owns row
+// t/4 and the columns q = t%4 (mod 4) of that row, so the rank-1 update of
+// each column needs no index arithmetic; the scaled pivot column goes through
+// a double-buffered smem vector: two CTA barriers per column.
 __global__ void __launch_bounds__(256)
 k_chol_diag(int K, int j0, double* __restrict__ Aall, const double* __restrict__ tol,
             int8_t* __restrict__ depmask, int32_t* __restrict__ ndep) {
     __shared__ double Ls[CB][CBP];
+    __shared__ double colv[2][CB];
+    __shared__ double s_inv;
     __shared__ int8_t sdep[CB];
-    __shared__ double piv;
     const int p = blockIdx.x;
     double* A = Aall + (int64_t)p * K * K;
     const int nb = min(CB, K - j0);
     const int tid = threadIdx.x;
-    const int rr = tid >> 2, h = tid & 3;  // row offset, quarter
+    const int r = tid >> 2, g = tid & 3;
     for (int e = tid; e < CB * CB; e += 256) {
-        const int r = e / CB, c = e % CB;
-        Ls[r][c] = (r < nb && c <= r) ? A[(int64_t)(j0 + r) * K + j0 + c] : 0.0;
+        const int rr = e / CB, c = e % CB;
+        Ls[rr][c] = (rr < nb && c <= rr) ? A[(int64_t)(j0 + rr) * K + j0 + c] : 0.0;
     }
     __syncthreads();
     const double tl = tol[p];
-    int nd = 0;
     for (int c = 0; c < nb; ++c) {
-        const int r = c + rr;  // rows c .. c+63 (only < nb used)
-        double v = 0.0;
-        if (r < nb) {
-            const int q0 = (c * h) >> 2, q1 = (c * (h + 1)) >> 2;
-            for (int q = q0; q < q1; ++q) v = fma(Ls[r][q], Ls[c][q], v);
-        }
-        v += __shfl_xor_sync(SDB_FULL, v, 1);
-        v += __shfl_xor_sync(SDB_FULL, v, 2);
-        const double a_rc = (r < nb) ? Ls[r][c] - v : 0.0;
-        if (r == c && h == 0) {
-            const bool dep = !(a_rc > tl);
+        const int buf = c & 1;
+        if (r == c && g == (c & 3)) {  // owner of the pivot
+            const double d = Ls[c][c];
+            const bool dep = !(d > tl);
+            const double piv = dep ? 1.0 : sqrt(d);
+            Ls[c][c] = piv;
             sdep[c] = dep ? 1 : 0;
-            piv = dep ? 1.0 : sqrt(a_rc);
+            s_inv = dep ? 0.0 : 1.0 / piv;  // dependent: column below becomes 0
+            colv[buf][c] = piv;
         }
         __syncthreads();
-        const double lc = piv;
-        const bool dep = sdep[c];
-        if (h == 0 && r < nb) Ls[r][c] = (r == c) ? lc : (dep ? 0.0 : a_rc / lc);
-        nd += dep;
+        const double inv = s_inv;
+        if (r > c && r < nb && g == (c & 3)) {
+            const double l = Ls[r][c] * inv;
+            Ls[r][c] = l;
+            colv[buf][r] = l;
+        }
         __syncthreads();
+        if (r > c && r < nb) {
+            const double lr = colv[buf][r];
+#pragma unroll
+            for (int j = 0; j < CB / 4; ++j) {
+                const int q = 4 * j + g;
+                if (q > c && q <= r) Ls[r][q] = fma(-lr, colv[buf][q], Ls[r][q]);
+            }
+        }
     }
+    __syncthreads();
     for (int e = tid; e < CB * CB; e += 256) {
-        const int r = e / CB, c = e % CB;
-        if (r < nb && c <= r) A[(int64_t)(j0 + r) * K + j0 + c] = Ls[r][c];
+        const int rr = e / CB, c = e % CB;
+        if (rr < nb && c <= rr) A[(int64_t)(j0 + rr) * K + j0 + c] = Ls[rr][c];
     }
     if (tid < nb) depmask[(int64_t)p * K + j0 + tid] = sdep[tid];
-    if (tid == 0) ndep[p] += nd;
+    if (tid == 0) {
+        int nd = 0;
+        for (int c = 0; c < nb; ++c) nd += sdep[c];
+        ndep[p] += nd;
+    }
 }
 
 // blockIdx.x == 0: forward-solve the panel's RHS rows, W_j = L_jj^-1 B_j
-//                  (thread per right-hand-side column)
-// blockIdx.x >= 1: panel rows block i: L_ij = A_ij L_jj^-T (thread per row)
+//                  (thread per right-hand-side column, tile in smem)
+// blockIdx.x >= 1: 64-row block of the panel: L_ij = A_ij L_jj^-T (row sweep)
 __global__ void __launch_bounds__(256)
 k_chol_panel(int K, int m, int j0, double* __restrict__ Aall, double* __restrict__ Ball,
              const int8_t* __restrict__ depmask) {
-    __shared__ double Ls[CB][CBP];
+    extern __shared__ double csm[];
+    double (*Ls)[CBP] = reinterpret_cast<double (*)[CBP]>(csm);
+    double (*Xs)[CBP] = reinterpret_cast<double (*)[CBP]>(csm + CB * CBP);
     __shared__ double inv[CB];
     __shared__ int8_t sdep[CB];
     const int p = blockIdx.y;
@@ -123,42 +156,49 @@ k_chol_panel(int K, int m, int j0, double* __restrict__ Aall, double* __restrict
     __syncthreads();
     if (blockIdx.x == 0) {
         double* B = Ball + (int64_t)p * K * m + (int64_t)j0 * m;
-        for (int col = tid; col < m; col += 256) {
-            double w[CB];
-#pragma unroll
-            for (int r = 0; r < CB; ++r) {
-                if (r < nb) {
-                    double sacc[4] = {0.0, 0.0, 0.0, 0.0};
-                    for (int q = 0; q < r; ++q) sacc[q & 3] = fma(Ls[r][q], w[q], sacc[q & 3]);
-                    const double bv = B[(int64_t)r * m + col];
-                    w[r] = sdep[r] ? 0.0 : (bv - ((sacc[0] + sacc[1]) + (sacc[2] + sacc[3]))) * inv[r];
+        for (int c0 = 0; c0 < m; c0 += CB) {  // 64 RHS columns per pass, tile Xs[row][col]
+            const int nc = min(CB, m - c0);
+            __syncthreads();
+            for (int e = tid; e < CB * CB; e += 256) {
+                const int r = e / CB, c = e % CB;
+                Xs[r][c] = (r < nb && c < nc) ? B[(int64_t)r * m + c0 + c] : 0.0;
+            }
+            __syncthreads();
+            if (tid < nc) {
+                const int col = tid;
+                for (int r = 0; r < nb; ++r) {
+                    double s0 = 0.0, s1 = 0.0;
+                    int q = 0;
+                    for (; q + 1 < r; q += 2) {
+                        s0 = fma(Ls[r][q], Xs[q][col], s0);
+                        s1 = fma(Ls[r][q + 1], Xs[q + 1][col], s1);
+                    }
+                    if (q < r) s0 = fma(Ls[r][q], Xs[q][col], s0);
+                    Xs[r][col] = sdep[r] ? 0.0 : (Xs[r][col] - (s0 + s1)) * inv[r];
                 }
             }
-#pragma unroll
-            for (int r = 0; r < CB; ++r)
-                if (r < nb) B[(int64_t)r * m + col] = w[r];
+            __syncthreads();
+            for (int e = tid; e < nb * nc; e += 256) {
+                const int r = e / nc, c = e % nc;
+                B[(int64_t)r * m + c0 + c] = Xs[r][c];
+            }
         }
         return;
     }
-    const int i0 = j0 + nb + (blockIdx.x - 1) * 256;
-    const int row = i0 + tid;
-    if (row >= K) return;
-    double* ar = A + (int64_t)row * K + j0;
-    double x[CB];
-#pragma unroll
-    for (int c = 0; c < CB; ++c) x[c] = (c < nb) ? ar[c] : 0.0;
-#pragma unroll
-    for (int c = 0; c < CB; ++c) {
-        if (c < nb) {
-            double sacc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-            for (int q = 0; q < c; ++q) sacc[q & 3] = fma(x[q], Ls[c][q], sacc[q & 3]);
-            x[c] = sdep[c] ? 0.0 : (x[c] - ((sacc[0] + sacc[1]) + (sacc[2] + sacc[3]))) * inv[c];
-        }
+    const int i0 = j0 + nb + (blockIdx.x - 1) * CB;
+    if (i0 >= K) return;
+    const int ni = min(CB, K - i0);
+    for (int e = tid; e < CB * CB; e += 256) {
+        const int r = e / CB, c = e % CB;
+        Xs[r][c] = (r < ni && c < nb) ? A[(int64_t)(i0 + r) * K + j0 + c] : 0.0;
     }
-#pragma unroll
-    for (int c = 0; c < CB; ++c)
-        if (c < nb) ar[c] = x[c];
+    __syncthreads();
+    rows_trsm(Xs, ni, Ls, inv, sdep, nb);
+    __syncthreads();
+    for (int e = tid; e < ni * nb; e += 256) {
+        const int r = e / nb, c = e % nb;
+        A[(int64_t)(i0 + r) * K + j0 + c] = Xs[r][c];
+    }
 }
 
 // 64x64 tile update  C -= X Y^T  with X (64 x nb), Y (64 x nb) from smem;
@@ -251,10 +291,12 @@ k_chol_update(int K, int m, int j0, double* __restrict__ Aall, double* __restric
 }
 
 // back substitution, panel j0: solve L_jj^T Z_j = W_j in place (thread per
-// right-hand-side column)
+// right-hand-side column, 64-column tiles in smem)
 __global__ void __launch_bounds__(256)
 k_back_diag(int K, int m, int j0, const double* __restrict__ Aall, double* __restrict__ Ball) {
-    __shared__ double Ls[CB][CBP];
+    extern __shared__ double csm[];
+    double (*Ls)[CBP] = reinterpret_cast<double (*)[CBP]>(csm);
+    double (*Ws)[CBP] = reinterpret_cast<double (*)[CBP]>(csm + CB * CBP);
     __shared__ double inv[CB];
     const int p = blockIdx.x;
     const int nb = min(CB, K - j0);
@@ -267,24 +309,32 @@ k_back_diag(int K, int m, int j0, const double* __restrict__ Aall, double* __res
     }
     __syncthreads();
     if (tid < nb) inv[tid] = 1.0 / Ls[tid][tid];
-    __syncthreads();
-    for (int col = tid; col < m; col += 256) {
-        double z[CB];
-#pragma unroll
-        for (int r = 0; r < CB; ++r) z[r] = (r < nb) ? B[(int64_t)r * m + col] : 0.0;
-#pragma unroll
-        for (int r = CB - 1; r >= 0; --r) {
-            if (r < nb) {
-                double sacc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-                for (int q = r + 1; q < CB; ++q)
-                    if (q < nb) sacc[q & 3] = fma(Ls[q][r], z[q], sacc[q & 3]);
-                z[r] = (z[r] - ((sacc[0] + sacc[1]) + (sacc[2] + sacc[3]))) * inv[r];
+    for (int c0 = 0; c0 < m; c0 += CB) {
+        const int nc = min(CB, m - c0);
+        __syncthreads();
+        for (int e = tid; e < CB * CB; e += 256) {
+            const int r = e / CB, c = e % CB;
+            Ws[r][c] = (r < nb && c < nc) ? B[(int64_t)r * m + c0 + c] : 0.0;
+        }
+        __syncthreads();
+        if (tid < nc) {
+            const int col = tid;
+            for (int r = nb - 1; r >= 0; --r) {
+                double s0 = 0.0, s1 = 0.0;
+                int q = r + 1;
+                for (; q + 1 < nb; q += 2) {
+                    s0 = fma(Ls[q][r], Ws[q][col], s0);
+                    s1 = fma(Ls[q + 1][r], Ws[q + 1][col], s1);
+                }
+                if (q < nb) s0 = fma(Ls[q][r], Ws[q][col], s0);
+                Ws[r][col] = (Ws[r][col] - (s0 + s1)) * inv[r];
             }
         }
-#pragma unroll
-        for (int r = 0; r < CB; ++r)
-            if (r < nb) B[(int64_t)r * m + col] = z[r];
+        __syncthreads();
+        for (int e = tid; e < nb * nc; e += 256) {
+            const int r = e / nc, c = e % nc;
+            B[(int64_t)r * m + c0 + c] = Ws[r][c];
+        }
     }
 }
 
@@ -351,6 +401,8 @@ int chol_solve(int P, int K, int m, double* A, double* B, const int32_t* usage, 
     if (!attr) {
         cudaFuncSetAttribute(k_chol_update, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
         cudaFuncSetAttribute(k_back_update, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+        cudaFuncSetAttribute(k_chol_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+        cudaFuncSetAttribute(k_back_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
         attr = true;
     }
     {
@@ -363,8 +415,8 @@ int chol_solve(int P, int K, int m, double* A, double* B, const int32_t* usage, 
         const int nb = std::min(CB, K - j0);
         k_chol_diag<<<P, 256, 0, st>>>(K, j0, A, tol, depmask, ndep);
         const int rows_below = K - j0 - nb;
-        dim3 gp((unsigned)(1 + (rows_below + 255) / 256), (unsigned)P);
-        k_chol_panel<<<gp, 256, 0, st>>>(K, m, j0, A, B, depmask);
+        dim3 gp((unsigned)(1 + (rows_below + CB - 1) / CB), (unsigned)P);
+        k_chol_panel<<<gp, 256, smem2, st>>>(K, m, j0, A, B, depmask);
         const int nt = (rows_below + CB - 1) / CB;
         const int tiles = nt * (nt + 1) / 2 + nt * nmc;
         if (tiles > 0) {
@@ -375,7 +427,7 @@ int chol_solve(int P, int K, int m, double* A, double* B, const int32_t* usage, 
     if (wsq) k_sumsq<<<P, 256, 0, st>>>((int64_t)K * m, B, wsq);
     const int last = (int)((nblk - 1) * CB);
     for (int j0 = last; j0 >= 0; j0 -= CB) {
-        k_back_diag<<<P, 256, 0, st>>>(K, m, j0, A, B);
+        k_back_diag<<<P, 256, smem2, st>>>(K, m, j0, A, B);
         if (j0 > 0) {
             const int ib = (j0 + CB - 1) / CB;
             dim3 gb((unsigned)(ib * nmc), (unsigned)P);

@@ -23,7 +23,7 @@
 
 namespace sdb {
 
-constexpr int CH = 256;  // signals per chunk (chunks never straddle shards)
+constexpr int CH = 1024;  // signals per chunk (chunks never straddle shards)
 
 // chunk_first[p] = first chunk of shard p; chunk_first[P] = total chunks
 __global__ void k_chunk_layout(const int64_t* __restrict__ off, int P, int64_t* __restrict__ cf) {
@@ -251,7 +251,9 @@ k_xxt(int P, int K, int cap, const int32_t* __restrict__ idx, const T* __restric
     }
 }
 
-// ---- per-signal residual ||y_i - D_p x_i||^2 (D in f64, atom-major)
+// ---- per-signal residual ||y_i - D_p x_i||^2 (D in f64, atom-major). With
+// `only_if`, shards whose flag is 0 are skipped; if no shard is flagged the
+// whole (grid-stride) launch exits after reading the P flags.
 template <typename T, int MPL>
 __global__ void __launch_bounds__(256)
 k_resid_sq(int64_t N, int m, int K, int cap, int P, const int64_t* __restrict__ off,
@@ -260,39 +262,54 @@ k_resid_sq(int64_t N, int m, int K, int cap, int P, const int64_t* __restrict__ 
            const double* __restrict__ D, double* __restrict__ out, double* __restrict__ ysq_out,
            const int32_t* __restrict__ only_if) {
     const int lane = threadIdx.x & 31;
-    const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-    if (i >= N) return;
-    const int p = shard_of(off, P, i);
-    if (only_if && only_if[p] == 0) return;  // replacement: shard has no target
-    const double* Dp = D + (int64_t)p * K * m;
-    const T* y = Y + i * ldy;
-    double r[MPL];
-    double yy = 0.0;
-#pragma unroll
-    for (int q = 0; q < MPL; ++q) {
-        const int row = lane + 32 * q;
-        r[q] = (row < m) ? (double)y[row] : 0.0;
-        yy = fma(r[q], r[q], yy);
+    if (only_if) {
+        __shared__ int s_any;
+        if (threadIdx.x == 0) s_any = 0;
+        __syncthreads();
+        int any = 0;
+        for (int q = threadIdx.x; q < P; q += blockDim.x) any |= only_if[q];
+        if (any) s_any = 1;
+        __syncthreads();
+        if (!s_any) return;
     }
-    const int n = counts[i];
-    for (int t = 0; t < n; ++t) {
-        const double* d = Dp + (int64_t)idx[i * cap + t] * m;
-        const double v = (double)val[i * cap + t];
+    const int64_t nw = (int64_t)gridDim.x * 8;
+    for (int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); i < N; i += nw) {
+        const int p = shard_of(off, P, i);
+        if (only_if && only_if[p] == 0) continue;  // warp-uniform
+        const double* Dp = D + (int64_t)p * K * m;
+        const T* y = Y + i * ldy;
+        double r[MPL];
+        double yy = 0.0;
 #pragma unroll
         for (int q = 0; q < MPL; ++q) {
             const int row = lane + 32 * q;
-            if (row < m) r[q] = fma(-d[row], v, r[q]);
+            r[q] = (row < m) ? (double)y[row] : 0.0;
+            yy = fma(r[q], r[q], yy);
+        }
+        const int n = counts[i];
+        for (int t = 0; t < n; ++t) {
+            const double* d = Dp + (int64_t)idx[i * cap + t] * m;
+            const double v = (double)val[i * cap + t];
+#pragma unroll
+            for (int q = 0; q < MPL; ++q) {
+                const int row = lane + 32 * q;
+                if (row < m) r[q] = fma(-d[row], v, r[q]);
+            }
+        }
+        double sacc = 0.0;
+#pragma unroll
+        for (int q = 0; q < MPL; ++q) sacc = fma(r[q], r[q], sacc);
+        sacc = warp_sum(sacc);
+        yy = warp_sum(yy);
+        if (lane == 0) {
+            out[i] = sacc;
+            if (ysq_out) ysq_out[i] = yy;
         }
     }
-    double s = 0.0;
-#pragma unroll
-    for (int q = 0; q < MPL; ++q) s = fma(r[q], r[q], s);
-    s = warp_sum(s);
-    yy = warp_sum(yy);
-    if (lane == 0) {
-        out[i] = s;
-        if (ysq_out) ysq_out[i] = yy;
-    }
+}
+
+static unsigned resid_grid(int64_t N) {
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>((N + 7) / 8, (int64_t)148 * 16));
 }
 
 // ---- ||y_i||^2 per signal
@@ -362,7 +379,7 @@ k_shard_sum(const int64_t* __restrict__ off, const double* __restrict__ v, doubl
 }
 
 // ---- (i) finish MOD: norms, dead atoms, restore, normalise (dictionary_update.py:103-113)
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(1024)
 k_mod_finish(int P, int K, int m, const double* __restrict__ Z, const double* __restrict__ Dprev,
              const int32_t* __restrict__ usage, const int64_t* __restrict__ nnz_shard,
              double* __restrict__ Dout, double* __restrict__ scales, int8_t* __restrict__ dead,
@@ -376,26 +393,40 @@ k_mod_finish(int P, int K, int m, const double* __restrict__ Z, const double* __
     __syncthreads();
     const bool empty = nnz_shard[p] == 0;
     // column norms of the raw solution
-    for (int a = wib; a < K; a += 8) {
+    for (int a = wib; a < K; a += 32) {
         double s = 0.0;
         for (int r = lane; r < m; r += 32) s = fma(Zp[(int64_t)a * m + r], Zp[(int64_t)a * m + r], s);
         s = warp_sum(s);
         if (lane == 0) scales[(int64_t)p * K + a] = sqrt(s);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    {
+        __shared__ double smx[1024];
+        __shared__ int srk[1024];
         double mx = 0.0;
         int rk = 0;
-        for (int a = 0; a < K; ++a) {
+        for (int a = threadIdx.x; a < K; a += 1024) {
             mx = fmax(mx, scales[(int64_t)p * K + a]);
             rk += usage[(int64_t)p * K + a] > 0;
         }
-        s_max = mx;
-        s_rank = empty ? 0 : rk;
+        smx[threadIdx.x] = mx;
+        srk[threadIdx.x] = rk;
+        __syncthreads();
+        for (int w = 512; w > 0; w >>= 1) {
+            if (threadIdx.x < w) {
+                smx[threadIdx.x] = fmax(smx[threadIdx.x], smx[threadIdx.x + w]);
+                srk[threadIdx.x] += srk[threadIdx.x + w];
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            s_max = smx[0];
+            s_rank = empty ? 0 : srk[0];
+        }
     }
     __syncthreads();
     const double thr = 1e-12 * fmax(s_max, 1.0);
-    for (int a = wib; a < K; a += 8) {
+    for (int a = wib; a < K; a += 32) {
         const int64_t e = (int64_t)p * K + a;
         const bool dd = empty || usage[e] == 0 || scales[e] <= thr;
         if (lane == 0) dead[e] = dd ? 1 : 0;
@@ -417,7 +448,7 @@ k_mod_finish(int P, int K, int m, const double* __restrict__ Z, const double* __
 // degenerate flags + twins, one CTA per shard: norms and "row has a twin"
 // flags in parallel, then the order-dependent rule (the lower index of a pair
 // is kept unless itself degenerate) sequentially over the rows with twins only.
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(1024)
 k_twins(int K, const double* __restrict__ C, const double* __restrict__ D, int m,
         const int32_t* __restrict__ usage, int8_t* __restrict__ deg, int32_t* __restrict__ ntarget) {
     extern __shared__ int8_t sh_flags[];
@@ -427,7 +458,7 @@ k_twins(int K, const double* __restrict__ C, const double* __restrict__ D, int m
     const int p = blockIdx.x;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const double* Cp = C + (int64_t)p * K * K;
-    for (int a = wib; a < K; a += 8) {
+    for (int a = wib; a < K; a += 32) {
         const double* d = D + ((int64_t)p * K + a) * m;
         double s = 0.0;
         for (int r = lane; r < m; r += 32) s = fma(d[r], d[r], s);
@@ -453,7 +484,7 @@ k_twins(int K, const double* __restrict__ C, const double* __restrict__ D, int m
     }
     __syncthreads();
     int cnt = 0;
-    for (int a = threadIdx.x; a < K; a += 256) {
+    for (int a = threadIdx.x; a < K; a += 1024) {
         deg[(int64_t)p * K + a] = dg[a];
         cnt += dg[a];
     }
@@ -713,14 +744,14 @@ int mod_update(const ModArgs<T>& a, cudaStream_t st) {
     k_ls_resid<<<(P + 127) / 128, 128, 0, st>>>(P, ysq, w.wsq, a.resid_fro, w.need);
     rc = with_mpl(m, [&](auto c) {
         constexpr int MPL = decltype(c)::value;
-        k_resid_sq<T, MPL><<<(unsigned)((N + 7) / 8), 256, 0, st>>>(
+        k_resid_sq<T, MPL><<<resid_grid(N), 256, 0, st>>>(
             N, m, K, cap, P, a.off, a.Y, a.ldy, a.idx, a.val, a.counts, w.B, w.rsq, nullptr, w.need);
         return (int)cudaGetLastError();
     });
     if (rc) return rc;
     k_shard_sum_masked<<<P, 256, 0, st>>>(a.off, w.rsq, w.need, a.resid_fro);
     k_shard_nnz<<<P, 256, 0, st>>>(a.off, a.counts, w.nnz);
-    k_mod_finish<<<P, 256, 0, st>>>(P, K, m, w.B, a.Dprev, a.usage, w.nnz, a.Dout, a.scales, a.dead,
+    k_mod_finish<<<P, 1024, 0, st>>>(P, K, m, w.B, a.Dprev, a.usage, w.nnz, a.Dout, a.scales, a.dead,
                                     a.rank, w.deficient);
     if (a.deficient_out)
         cudaMemcpyAsync(a.deficient_out, w.deficient, sizeof(int32_t) * P, cudaMemcpyDeviceToDevice, st);
@@ -763,12 +794,12 @@ int replace_degenerate(const ReplaceArgs<T>& a, cudaStream_t st) {
     k_normalize_rows<<<(unsigned)((PK + 7) / 8), 256, 0, st>>>(PK, m, a.D, Dn);
     int rc = gram_f64(Dn, P, m, K, C, st);
     if (rc) return rc;
-    k_twins<<<P, 256, 2 * K, st>>>(K, C, a.D, m, a.usage, deg, ntarget);
+    k_twins<<<P, 1024, 2 * K, st>>>(K, C, a.D, m, a.usage, deg, ntarget);
     // residuals with the current D and the given codes (always computed; the
     // reference skips them when no atom is degenerate, which changes nothing)
     rc = with_mpl(m, [&](auto c) {
         constexpr int MPL = decltype(c)::value;
-        k_resid_sq<T, MPL><<<(unsigned)((N + 7) / 8), 256, 0, st>>>(
+        k_resid_sq<T, MPL><<<resid_grid(N), 256, 0, st>>>(
             N, m, K, cap, P, a.off, a.Y, a.ldy, a.idx, a.val, a.counts, a.D, rsq, ysq, ntarget);
         return (int)cudaGetLastError();
     });
@@ -791,7 +822,7 @@ int residual_sq(int64_t N, int m, int K, int cap, int P, const int64_t* off, con
     if (N <= 0) return 0;
     return with_mpl(m, [&](auto c) {
         constexpr int MPL = decltype(c)::value;
-        k_resid_sq<T, MPL><<<(unsigned)((N + 7) / 8), 256, 0, st>>>(N, m, K, cap, P, off, Y, ldy, idx,
+        k_resid_sq<T, MPL><<<resid_grid(N), 256, 0, st>>>(N, m, K, cap, P, off, Y, ldy, idx,
                                                                    val, counts, D, rsq, ysq, nullptr);
         return (int)cudaGetLastError();
     });
