@@ -18,7 +18,10 @@
 namespace sdb {
 
 constexpr int CB = 64;       // panel / tile width
-constexpr int CBP = CB + 1;  // padded smem row
+constexpr int CBP = CB + 1;  // padded smem row (tile GEMMs: 16 consecutive rows per warp)
+// row stride for the sweep kernels: a warp touches 8 rows x 4 columns; stride
+// 68 doubles (== 4 mod 16 bank pairs) spreads them over all 16 pairs twice
+constexpr int CBD = 68;
 
 __global__ void __launch_bounds__(256)
 k_chol_prep(int K, double* __restrict__ Aall, const int32_t* __restrict__ usage,
@@ -52,7 +55,8 @@ k_chol_prep(int K, double* __restrict__ Aall, const int32_t* __restrict__ usage,
 
 // ---- row sweep X L^T = A for rows of Xs (4 lanes per row, 8 rows per warp):
 // x_c = (a_c - sum_{q<c} x_q L[c][q]) / L[c][c], written in place into Xs.
-__device__ __forceinline__ void rows_trsm(double (*Xs)[CBP], int nrows, double (*Ls)[CBP],
+template <int S>
+__device__ __forceinline__ void rows_trsm(double (*Xs)[S], int nrows, double (*Ls)[S],
                                           const double* inv, const int8_t* sdep, int nb) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int h = lane & 3;
@@ -68,61 +72,105 @@ __device__ __forceinline__ void rows_trsm(double (*Xs)[CBP], int nrows, double (
     }
 }
 
-// factor the diagonal block of panel j0, right-looking. Thread t owns row
-// t/4 and the columns q = t%4 (mod 4) of that row, so the rank-1 update of
-// each column needs no index arithmetic; the scaled pivot column goes through
-// a double-buffered smem vector: two CTA barriers per column.
+// ---- substitution on a 64-column tile W (smem, W[row][col]): column t is
+// handled by the 4 lanes 4t..4t+3 of one warp (8 columns per warp), each
+// summing a quarter of the dot product, combined by shuffles. lower: solve
+// L w = b (forward, dependent rows -> 0); !lower: solve L^T z = w (backward).
+template <int S>
+__device__ __forceinline__ void cols_trsv(double (*W)[S], int ncols, double (*Ls)[S],
+                                          const double* inv, const int8_t* sdep, int nb,
+                                          bool lower) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int h = lane & 3;
+    const int t = warp * 8 + (lane >> 2);
+    const bool act = t < ncols;
+    for (int k = 0; k < nb; ++k) {
+        const int rr = lower ? k : nb - 1 - k;
+        double v = 0.0;
+        if (act) {
+            if (lower) {
+                for (int q = h; q < rr; q += 4) v = fma(Ls[rr][q], W[q][t], v);
+            } else {
+                for (int q = rr + 1 + h; q < nb; q += 4) v = fma(Ls[q][rr], W[q][t], v);
+            }
+        }
+        v += __shfl_xor_sync(SDB_FULL, v, 1);
+        v += __shfl_xor_sync(SDB_FULL, v, 2);
+        if (act && h == 0) {
+            const double nv = (W[rr][t] - v) * inv[rr];
+            W[rr][t] = (lower && sdep[rr]) ? 0.0 : nv;
+        }
+        __syncwarp();
+    }
+}
+
+// factor the diagonal block of panel j0, right-looking, register resident:
+// thread t owns row r = t/4 and its 16 columns q = 4j + t%4 in registers for
+// the whole factorisation (the 64-column loop is unrolled so every register
+// index is static). Per column: the pivot owner publishes the pivot, the
+// column's owners publish the scaled column through a double-buffered smem
+// vector, every thread updates its 16 values — two CTA barriers per column.
 __global__ void __launch_bounds__(256)
 k_chol_diag(int K, int j0, double* __restrict__ Aall, const double* __restrict__ tol,
             int8_t* __restrict__ depmask, int32_t* __restrict__ ndep) {
-    __shared__ double Ls[CB][CBP];
     __shared__ double colv[2][CB];
-    __shared__ double s_inv;
+    __shared__ double s_inv[2];
     __shared__ int8_t sdep[CB];
     const int p = blockIdx.x;
     double* A = Aall + (int64_t)p * K * K;
     const int nb = min(CB, K - j0);
     const int tid = threadIdx.x;
     const int r = tid >> 2, g = tid & 3;
-    for (int e = tid; e < CB * CB; e += 256) {
-        const int rr = e / CB, c = e % CB;
-        Ls[rr][c] = (rr < nb && c <= rr) ? A[(int64_t)(j0 + rr) * K + j0 + c] : 0.0;
-    }
-    __syncthreads();
-    const double tl = tol[p];
-    for (int c = 0; c < nb; ++c) {
-        const int buf = c & 1;
-        if (r == c && g == (c & 3)) {  // owner of the pivot
-            const double d = Ls[c][c];
-            const bool dep = !(d > tl);
-            const double piv = dep ? 1.0 : sqrt(d);
-            Ls[c][c] = piv;
-            sdep[c] = dep ? 1 : 0;
-            s_inv = dep ? 0.0 : 1.0 / piv;  // dependent: column below becomes 0
-            colv[buf][c] = piv;
-        }
-        __syncthreads();
-        const double inv = s_inv;
-        if (r > c && r < nb && g == (c & 3)) {
-            const double l = Ls[r][c] * inv;
-            Ls[r][c] = l;
-            colv[buf][r] = l;
-        }
-        __syncthreads();
-        if (r > c && r < nb) {
-            const double lr = colv[buf][r];
+    double v[CB / 4];
+    {
+        const double* arow = A + (int64_t)(j0 + r) * K + j0;
 #pragma unroll
-            for (int j = 0; j < CB / 4; ++j) {
-                const int q = 4 * j + g;
-                if (q > c && q <= r) Ls[r][q] = fma(-lr, colv[buf][q], Ls[r][q]);
+        for (int j = 0; j < CB / 4; ++j) {
+            const int q = 4 * j + g;
+            v[j] = (r < nb && q <= r) ? arow[q] : 0.0;
+        }
+    }
+    const double tl = tol[p];
+#pragma unroll
+    for (int c = 0; c < CB; ++c) {
+        if (c < nb) {
+            const int buf = c & 1;
+            const int jc = c >> 2;
+            if (r == c && g == (c & 3)) {  // pivot owner
+                const double d = v[jc];
+                const bool dep = !(d > tl);
+                double y = (double)rsqrtf((float)d);
+                y = y * fma(-0.5 * d * y, y, 1.5);
+                y = y * fma(-0.5 * d * y, y, 1.5);
+                v[jc] = dep ? 1.0 : d * y;
+                sdep[c] = dep ? 1 : 0;
+                s_inv[buf] = dep ? 0.0 : y;
+            }
+            __syncthreads();
+            if (r > c && r < nb && g == (c & 3)) {
+                v[jc] *= s_inv[buf];
+                colv[buf][r] = v[jc];
+            }
+            __syncthreads();
+            if (r > c && r < nb) {
+                const double lr = colv[buf][r];
+#pragma unroll
+                for (int j = 0; j < CB / 4; ++j) {
+                    const int q = 4 * j + g;
+                    if (q > c && q <= r) v[j] = fma(-lr, colv[buf][q], v[j]);
+                }
             }
         }
     }
-    __syncthreads();
-    for (int e = tid; e < CB * CB; e += 256) {
-        const int rr = e / CB, c = e % CB;
-        if (rr < nb && c <= rr) A[(int64_t)(j0 + rr) * K + j0 + c] = Ls[rr][c];
+    {
+        double* arow = A + (int64_t)(j0 + r) * K + j0;
+#pragma unroll
+        for (int j = 0; j < CB / 4; ++j) {
+            const int q = 4 * j + g;
+            if (r < nb && q <= r) arow[q] = v[j];
+        }
     }
+    __syncthreads();
     if (tid < nb) depmask[(int64_t)p * K + j0 + tid] = sdep[tid];
     if (tid == 0) {
         int nd = 0;
@@ -138,8 +186,8 @@ __global__ void __launch_bounds__(256)
 k_chol_panel(int K, int m, int j0, double* __restrict__ Aall, double* __restrict__ Ball,
              const int8_t* __restrict__ depmask) {
     extern __shared__ double csm[];
-    double (*Ls)[CBP] = reinterpret_cast<double (*)[CBP]>(csm);
-    double (*Xs)[CBP] = reinterpret_cast<double (*)[CBP]>(csm + CB * CBP);
+    double (*Ls)[CBD] = reinterpret_cast<double (*)[CBD]>(csm);
+    double (*Xs)[CBD] = reinterpret_cast<double (*)[CBD]>(csm + CB * CBD);
     __shared__ double inv[CB];
     __shared__ int8_t sdep[CB];
     const int p = blockIdx.y;
@@ -164,19 +212,7 @@ k_chol_panel(int K, int m, int j0, double* __restrict__ Aall, double* __restrict
                 Xs[r][c] = (r < nb && c < nc) ? B[(int64_t)r * m + c0 + c] : 0.0;
             }
             __syncthreads();
-            if (tid < nc) {
-                const int col = tid;
-                for (int r = 0; r < nb; ++r) {
-                    double s0 = 0.0, s1 = 0.0;
-                    int q = 0;
-                    for (; q + 1 < r; q += 2) {
-                        s0 = fma(Ls[r][q], Xs[q][col], s0);
-                        s1 = fma(Ls[r][q + 1], Xs[q + 1][col], s1);
-                    }
-                    if (q < r) s0 = fma(Ls[r][q], Xs[q][col], s0);
-                    Xs[r][col] = sdep[r] ? 0.0 : (Xs[r][col] - (s0 + s1)) * inv[r];
-                }
-            }
+            cols_trsv(Xs, nc, Ls, inv, sdep, nb, true);
             __syncthreads();
             for (int e = tid; e < nb * nc; e += 256) {
                 const int r = e / nc, c = e % nc;
@@ -295,8 +331,8 @@ k_chol_update(int K, int m, int j0, double* __restrict__ Aall, double* __restric
 __global__ void __launch_bounds__(256)
 k_back_diag(int K, int m, int j0, const double* __restrict__ Aall, double* __restrict__ Ball) {
     extern __shared__ double csm[];
-    double (*Ls)[CBP] = reinterpret_cast<double (*)[CBP]>(csm);
-    double (*Ws)[CBP] = reinterpret_cast<double (*)[CBP]>(csm + CB * CBP);
+    double (*Ls)[CBD] = reinterpret_cast<double (*)[CBD]>(csm);
+    double (*Ws)[CBD] = reinterpret_cast<double (*)[CBD]>(csm + CB * CBD);
     __shared__ double inv[CB];
     const int p = blockIdx.x;
     const int nb = min(CB, K - j0);
@@ -317,19 +353,7 @@ k_back_diag(int K, int m, int j0, const double* __restrict__ Aall, double* __res
             Ws[r][c] = (r < nb && c < nc) ? B[(int64_t)r * m + c0 + c] : 0.0;
         }
         __syncthreads();
-        if (tid < nc) {
-            const int col = tid;
-            for (int r = nb - 1; r >= 0; --r) {
-                double s0 = 0.0, s1 = 0.0;
-                int q = r + 1;
-                for (; q + 1 < nb; q += 2) {
-                    s0 = fma(Ls[q][r], Ws[q][col], s0);
-                    s1 = fma(Ls[q + 1][r], Ws[q + 1][col], s1);
-                }
-                if (q < nb) s0 = fma(Ls[q][r], Ws[q][col], s0);
-                Ws[r][col] = (Ws[r][col] - (s0 + s1)) * inv[r];
-            }
-        }
+        cols_trsv(Ws, nc, Ls, inv, (const int8_t*)nullptr, nb, false);
         __syncthreads();
         for (int e = tid; e < nb * nc; e += 256) {
             const int r = e / nc, c = e % nc;
@@ -396,7 +420,7 @@ int chol_solve(int P, int K, int m, double* A, double* B, const int32_t* usage, 
                int8_t* depmask, int32_t* ndep, double* wsq, void* ws, cudaStream_t st) {
     const int64_t nblk = (K + CB - 1) / CB;
     double* tol = (double*)ws;
-    const int smem2 = 2 * CB * CBP * (int)sizeof(double);
+    const int smem2 = 2 * CB * CBD * (int)sizeof(double);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_chol_update, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
