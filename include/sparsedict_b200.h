@@ -198,6 +198,13 @@ int sdb_reconstruct(int dtype, int64_t H, int64_t W, int64_t p, int64_t s, const
 int sdb_reconstruct_dense(int64_t H, int64_t W, int64_t p, int64_t s, const double *P, double *out,
                           void *stream);
 
+/* HOST function (no GPU): numpy.random.default_rng(seed).permutation(n) of
+ * trainer.split_indices (trainer.py:208-209), bitwise identical, given the
+ * PCG64 state numpy derives from the seed (bit_generator.state: 128-bit state
+ * and increment split in hi/lo words, has_uint32, uinteger). out: n int64. */
+int sdb_pcg64_permutation(int64_t n, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                          uint64_t inc_lo, int has_uint32, uint32_t uinteger, int64_t *out);
+
 #ifdef __cplusplus
 }
 #endif

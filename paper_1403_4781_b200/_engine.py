@@ -170,6 +170,20 @@ class DeviceCodes:
         return self.counts.shape[0]
 
 
+_pinned_perm: torch.Tensor | None = None
+
+
+def split_permutation(N: int, seed) -> torch.Tensor:
+    """Device int64 copy of numpy.random.default_rng(seed).permutation(N)
+    (bit-identical, native host routine) via a reusable pinned buffer."""
+    global _pinned_perm
+    if _pinned_perm is None or _pinned_perm.numel() < N:
+        _pinned_perm = torch.empty((max(N, 1),), dtype=torch.int64, pin_memory=True)
+    host = _pinned_perm[:N]
+    _lib.permutation(N, seed, out=host.numpy())
+    return host.to(device(), non_blocking=True)
+
+
 def shard_offsets(sizes) -> tuple[torch.Tensor, int]:
     off = np.concatenate([[0], np.cumsum(np.asarray(sizes, dtype=np.int64))]).astype(np.int64)
     return torch.from_numpy(off).to(device()), int(max(sizes) if len(sizes) else 0)

@@ -61,6 +61,8 @@ SIGNATURES = {
     "sdb_reconstruct": (c_int, [c_int, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp,
                                 c_dbl, c_dbl, c_vp, c_vp]),
     "sdb_reconstruct_dense": (c_int, [c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
+    "sdb_pcg64_permutation": (c_int, [c_i64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                      ctypes.c_uint64, c_int, ctypes.c_uint32, c_vp]),
 }
 
 
@@ -98,6 +100,21 @@ def check(rc: int, what: str) -> None:
     if rc != 0:
         msg = load().sdb_last_error().decode(errors="replace")
         raise NativeError(f"{what} failed ({rc}): {msg}")
+
+
+def permutation(n: int, seed, out=None):
+    """numpy.random.default_rng(seed).permutation(n), bit-identical, computed
+    by the native host routine (prefetched Fisher-Yates). ``out``: optional
+    int64 buffer (e.g. a pinned torch tensor's numpy view)."""
+    import numpy as np
+    st = np.random.default_rng(seed).bit_generator.state
+    s, inc = st["state"]["state"], st["state"]["inc"]
+    M = (1 << 64) - 1
+    arr = np.empty(n, dtype=np.int64) if out is None else out
+    check(load().sdb_pcg64_permutation(n, s >> 64, s & M, inc >> 64, inc & M,
+                                       int(st["has_uint32"]), int(st["uinteger"]),
+                                       arr.ctypes.data if n else None), "sdb_pcg64_permutation")
+    return arr
 
 
 def call(name: str, *args) -> int:

@@ -308,7 +308,7 @@ def split_indices(N: int, L: int, seed: int) -> list[np.ndarray]:
     PCG64 permutation cut into consecutive blocks, the first N mod L one longer."""
     if L < 1 or L > N:
         raise InvalidInputError("require 1 <= L <= N")
-    perm = np.random.default_rng(seed).permutation(N)
+    perm = E._lib.permutation(N, seed)
     base, extra = divmod(N, L)
     ends = np.cumsum([base + (1 if t < extra else 0) for t in range(L)])
     return np.split(perm, ends[:-1])
@@ -403,7 +403,8 @@ class SplitMergeResult:
 def split_merge_device(Ydev: torch.Tensor, L: int, K1: int, local_cap: int, local_eps: float,
                        local_iters: int, K: int, s2: int, merge_iters: int, seed: int,
                        init="first-columns", prec: str = "fp64", use_tc: bool = True,
-                       t_start: float | None = None) -> SplitMergeResult:
+                       t_start: float | None = None, perm: torch.Tensor | None = None
+                       ) -> SplitMergeResult:
     """split_dataset -> all locals in one batched loop -> merge (trainer.py:
     291-313). ``Ydev`` is (N, m) device, signal-major."""
     if t_start is None:
@@ -413,10 +414,11 @@ def split_merge_device(Ydev: torch.Tensor, L: int, K1: int, local_cap: int, loca
     if not 1 <= L <= N:
         raise InvalidInputError("require 1 <= L <= N")
     # split_indices' blocks are consecutive slices of one PCG64 permutation
-    perm_h = np.random.default_rng(seed).permutation(N)
+    # (native, bit-identical to numpy; ``perm`` may be precomputed by the caller)
+    if perm is None:
+        perm = E.split_permutation(N, seed)
     base, extra = divmod(N, L)
     sizes = [base + (1 if t < extra else 0) for t in range(L)]
-    perm = torch.from_numpy(perm_h).to(E.device())
     Ys = E.gather_rows(Ydev, perm, prec)
     off, _ = E.shard_offsets(sizes)
     S = E.ShardSet(Ys, off, sizes, prec)
@@ -470,9 +472,14 @@ def train_split_merge(Y, cfg: TrainConfig, evaluate: bool = True) -> tuple[np.nd
     cap1, eps1 = coding_mode(m, cfg.K1, cfg.s1, cfg.eps, cfg.s_max)
     _sync()
     t0 = time.perf_counter()
-    Ydev = _ingest_checked(Y, prec)
+    # the split permutation (host, native) runs while Y streams to the device
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=1) as ex:
+        fut = ex.submit(E.split_permutation, N, cfg.seed)
+        Ydev = _ingest_checked(Y, prec)
+        perm = fut.result()
     r = split_merge_device(Ydev, cfg.L, cfg.K1, cap1, eps1, local_iters, cfg.K, cfg.s2,
-                           merge_iters, cfg.seed, cfg.init, prec, t_start=t0)
+                           merge_iters, cfg.seed, cfg.init, prec, t_start=t0, perm=perm)
     # evaluation pass (trainer.py:315-319), outside wall_time_s
     mse = float("nan")
     if evaluate:

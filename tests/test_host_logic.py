@@ -112,3 +112,12 @@ def test_overcomplete_dct_matches_reference():
     np.testing.assert_allclose(sdb.overcomplete_dct(4, 64), DN["dct4"], rtol=0, atol=1e-15)
     with pytest.raises(sdb.InvalidInputError):
         sdb.overcomplete_dct(8, 49)
+
+
+@pytest.mark.parametrize("n,seed", [(0, 1), (1, 2), (2, 3), (10, 0), (103, 11), (65537, 9),
+                                    (1_000_003, 1234), (2_040_200, 5)])
+def test_native_permutation_bitwise_numpy(n, seed):
+    """The native split permutation == numpy.random.default_rng(seed).permutation(n)
+    (trainer.py:208-209)."""
+    from paper_1403_4781_b200 import _lib
+    assert np.array_equal(_lib.permutation(n, seed), np.random.default_rng(seed).permutation(n))
