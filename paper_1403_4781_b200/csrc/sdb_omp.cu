@@ -410,7 +410,7 @@ __device__ __forceinline__ void load_row(float (&v)[KPL], const float* __restric
 }
 
 template <int KPL, int MPL>
-__global__ void __launch_bounds__(256, (KPL >= 16) ? 1 : 2)
+__global__ void __launch_bounds__(256, (KPL >= 16) ? 1 : (KPL >= 8 ? 3 : 4))
 k_omp_fast(OmpArgs<float> a) {
     extern __shared__ __align__(16) float fsm[];
     const int lane = threadIdx.x & 31;
