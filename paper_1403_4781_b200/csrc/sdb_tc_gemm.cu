@@ -18,6 +18,7 @@
 #include <cuda.h>
 
 #include <cstdint>
+#include <algorithm>
 #include <mutex>
 
 #include "sdb_common.cuh"
@@ -34,7 +35,7 @@ constexpr int STAGES = 2;
 constexpr int A_BYTES = TM * KB * 4;   // 16 KB
 constexpr int B_BYTES = TN * KB * 4;   // 32 KB
 constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // A_hi, A_lo, B_hi, B_lo
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256 + 4 * 32 * 33 * 4;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -238,6 +239,299 @@ k_corr_tc(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUten
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TN));
 }
 
+// ----------------------------------------------------------------------------
+// Persistent, warp-specialised version (the one used): one CTA per SM owns a
+// contiguous range of work items ordered (shard, 256-atom chunk, 128-signal
+// tile); roles:
+//   warp 0      TMA producer (one elected thread)
+//   warp 1      MMA issuer (one thread): 4 k-steps x 3 MMAs per k-block
+//   warps 2-5   epilogue: TMEM -> registers -> global (thread = signal row)
+//   warps 6-9   3xTF32 split of the Y k-block (hi in place, lo beside it)
+// RES (m <= 64): D_hi/D_lo of the current (shard, chunk) stay resident in
+// smem and are reloaded only when the segment changes; the 2-stage ring then
+// carries Y only. !RES: D k-blocks stream with Y through the ring.
+// The accumulator is double-buffered in TMEM (2 x 256 columns), so the
+// epilogue of item i overlaps the loads and MMAs of item i+1.
+// mbarriers: full[s] (TMA), split[s] (4 warps), empty[s] (MMA commit),
+//            tfull[b] (MMA commit), tempty[b] (4 epilogue warps),
+//            bfull (resident D landed), bfree (MMA done with resident D).
+// ----------------------------------------------------------------------------
+constexpr int NWARP2 = 10;
+constexpr int RES_KB = 2;                           // resident D: up to 2 k-blocks (m <= 64)
+constexpr int RES_A_STAGE = 2 * A_BYTES;             // Y hi + lo
+constexpr int RES_B_BYTES = RES_KB * 2 * B_BYTES;    // D hi + lo, 2 k-blocks
+constexpr int SMEM2_BYTES = 2 * STAGE_BYTES + 1024 + 256 + 4 * 2 * 32 * 32 * 4;  // + TMA store staging
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+struct Item {
+    int p, chunk;
+    int64_t tile, seg;  // seg: (p, chunk) segment id
+};
+
+__device__ __forceinline__ Item item_of(int64_t it, const int64_t* __restrict__ tile_start, int P,
+                                        int nchunk) {
+    // items of shard p: nchunk * ntiles_p, ordered (chunk, tile)
+    int lo = 0, hi = P - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (tile_start[mid] * nchunk <= it) lo = mid; else hi = mid - 1;
+    }
+    Item r;
+    r.p = lo;
+    const int64_t nt = tile_start[lo + 1] - tile_start[lo];
+    const int64_t local = it - tile_start[lo] * nchunk;
+    r.chunk = (int)(local / nt);
+    r.tile = local - (int64_t)r.chunk * nt;
+    r.seg = (int64_t)lo * nchunk + r.chunk;
+    return r;
+}
+
+template <bool RES>
+__global__ void __launch_bounds__(NWARP2 * 32, 1)
+k_corr_tc2(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmDh,
+           const __grid_constant__ CUtensorMap tmDl, const __grid_constant__ CUtensorMap tmA,
+           const int64_t* __restrict__ off,
+           const int64_t* __restrict__ tile_start, int P, int K, int nkb, int nchunk,
+           float* __restrict__ alpha, int64_t lda) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* base = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    // layout: RES: [A stage 0 | A stage 1 | D resident] ; !RES: [stage 0 | stage 1]
+    unsigned char* bar_base = base + 2 * STAGE_BYTES;
+    uint64_t* bars = (uint64_t*)bar_base;
+    // full[0..1], split[2..3], empty[4..5], tfull[6..7], tempty[8..9], bfull[10], bfree[11]
+    uint32_t* tmem_slot = (uint32_t*)(bars + 12);
+    // epilogue staging for TMA stores: 4 warps x 2 buffers x 32x32 fp32
+    float* stg_base = reinterpret_cast<float*>(bar_base + 256);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t n_items = tile_start[P] * nchunk;
+    const int64_t per = (n_items + gridDim.x - 1) / gridDim.x;
+    const int64_t it0 = (int64_t)blockIdx.x * per, it1 = min(n_items, it0 + per);
+
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(smem_u32(&bars[s]), 1);
+            mbar_init(smem_u32(&bars[2 + s]), 4);
+            mbar_init(smem_u32(&bars[4 + s]), 1);
+            mbar_init(smem_u32(&bars[6 + s]), 1);
+            mbar_init(smem_u32(&bars[8 + s]), 4);
+        }
+        mbar_init(smem_u32(&bars[10]), 1);
+        mbar_init(smem_u32(&bars[11]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)), "r"(2 * TN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    // A (Y) k-block buffers of stage s; D k-block kb buffers (resident or staged)
+    auto a_hi = [&](int s) -> unsigned char* { return RES ? base + s * RES_A_STAGE : base + s * STAGE_BYTES; };
+    auto a_lo = [&](int s) -> unsigned char* { return a_hi(s) + A_BYTES; };
+    auto b_hi = [&](int s, int kb) -> unsigned char* {
+        return RES ? base + 2 * RES_A_STAGE + kb * 2 * B_BYTES : base + s * STAGE_BYTES + 2 * A_BYTES;
+    };
+    auto b_lo = [&](int s, int kb) -> unsigned char* { return b_hi(s, kb) + B_BYTES; };
+
+    if (warp == 0) {
+        // ---------------- TMA producer
+        if (lane == 0) {
+            int64_t q = 0, seg_prev = -1, nseg = 0;
+            for (int64_t it = it0; it < it1; ++it) {
+                const Item I = item_of(it, tile_start, P, nchunk);
+                const int64_t row0 = off[I.p] + I.tile * TM;
+                const int64_t d_row0 = (int64_t)I.p * K + (int64_t)I.chunk * TN;
+                if (RES && I.seg != seg_prev) {
+                    if (nseg > 0) mbar_wait(smem_u32(&bars[11]), (uint32_t)((nseg - 1) & 1));
+                    const uint32_t bf = smem_u32(&bars[10]);
+                    mbar_expect_tx(bf, (uint32_t)(nkb * 2 * B_BYTES));
+                    for (int kb = 0; kb < nkb; ++kb) {
+                        tma_load_2d(smem_u32(b_hi(0, kb)), &tmDh, kb * KB, (int)d_row0, bf);
+                        tma_load_2d(smem_u32(b_lo(0, kb)), &tmDl, kb * KB, (int)d_row0, bf);
+                    }
+                    seg_prev = I.seg;
+                    ++nseg;
+                }
+                for (int kb = 0; kb < nkb; ++kb, ++q) {
+                    const int s = (int)(q % STAGES);
+                    const int64_t use = q / STAGES;
+                    if (use > 0) mbar_wait(smem_u32(&bars[4 + s]), (uint32_t)((use - 1) & 1));
+                    const uint32_t full = smem_u32(&bars[s]);
+                    mbar_expect_tx(full, RES ? A_BYTES : A_BYTES + 2 * B_BYTES);
+                    tma_load_2d(smem_u32(a_hi(s)), &tmY, kb * KB, (int)row0, full);
+                    if (!RES) {
+                        tma_load_2d(smem_u32(b_hi(s, kb)), &tmDh, kb * KB, (int)d_row0, full);
+                        tma_load_2d(smem_u32(b_lo(s, kb)), &tmDl, kb * KB, (int)d_row0, full);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer
+        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TN >> 3) << 17) |
+                               ((uint32_t)(TM >> 4) << 24);
+        int64_t q = 0, n = 0, seg_prev = -1, nseg = 0;
+        for (int64_t it = it0; it < it1; ++it, ++n) {
+            const Item I = item_of(it, tile_start, P, nchunk);
+            const int b = (int)(n & 1);
+            const int64_t buse = n >> 1;
+            if (lane == 0) {
+                if (RES && I.seg != seg_prev) {
+                    mbar_wait(smem_u32(&bars[10]), (uint32_t)(nseg & 1));
+                    seg_prev = I.seg;
+                    ++nseg;
+                }
+                if (buse > 0) mbar_wait(smem_u32(&bars[8 + b]), (uint32_t)((buse - 1) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t tacc = tmem + (uint32_t)(b * TN);
+                for (int kb = 0; kb < nkb; ++kb, ++q) {
+                    const int s = (int)(q % STAGES);
+                    mbar_wait(smem_u32(&bars[2 + s]), (uint32_t)((q / STAGES) & 1));
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint64_t dah = sw128_desc(smem_u32(a_hi(s)));
+                    const uint64_t dal = sw128_desc(smem_u32(a_lo(s)));
+                    const uint64_t dbh = sw128_desc(smem_u32(b_hi(s, kb)));
+                    const uint64_t dbl = sw128_desc(smem_u32(b_lo(s, kb)));
+#pragma unroll
+                    for (int k = 0; k < KB / 8; ++k) {
+                        const uint64_t adv = (uint64_t)((k * 8 * 4) >> 4);
+                        const uint32_t acc0 = (kb > 0 || k > 0) ? 1u : 0u;
+                        mma_tf32(tacc, dah + adv, dbh + adv, idesc, acc0);
+                        mma_tf32(tacc, dah + adv, dbl + adv, idesc, 1u);
+                        mma_tf32(tacc, dal + adv, dbh + adv, idesc, 1u);
+                    }
+                    mma_commit(smem_u32(&bars[4 + s]));                     // stage free
+                    if (kb == nkb - 1) mma_commit(smem_u32(&bars[6 + b]));  // accumulator ready
+                }
+                if (RES) {  // resident D no longer needed after this item?
+                    const bool last = (it + 1 >= it1) || item_of(it + 1, tile_start, P, nchunk).seg != I.seg;
+                    if (last) mma_commit(smem_u32(&bars[11]));
+                }
+            }
+            __syncwarp();
+        }
+    } else if (warp >= 2 && warp < 6) {
+        // ---------------- epilogue (TMEM lane quadrant = warp % 4): thread =
+        // signal row; each 32x32 block is staged in smem and written by one
+        // TMA store (async, full lines); quadrants straddling a shard end use
+        // plain stores so rows of the next shard are never touched
+        const int quad = warp & 3;
+        float* stg = stg_base + (warp - 2) * 2 * 1024;
+        int64_t n = 0;
+        int sb = 0;  // staging buffer toggle
+        for (int64_t it = it0; it < it1; ++it, ++n) {
+            const Item I = item_of(it, tile_start, P, nchunk);
+            const int b = (int)(n & 1);
+            mbar_wait(smem_u32(&bars[6 + b]), (uint32_t)((n >> 1) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const int64_t s_hi = off[I.p + 1];
+            const int64_t row_base = off[I.p] + I.tile * TM + quad * 32;
+            const int nrows = (int)max((int64_t)0, min((int64_t)32, s_hi - row_base));
+            const int n0 = I.chunk * TN;
+#pragma unroll 1
+            for (int c = 0; c < TN; c += 32) {
+                if (n0 + c >= K) break;
+                uint32_t v[32];
+                const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * TN + c);
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+                    "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                      "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+                      "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+                      "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+                      "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+                      "=r"(v[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                const int j0 = n0 + c;
+                if (nrows == 32) {
+                    float* buf = stg + sb * 1024;
+                    // the TMA store issued two blocks ago must have read this buffer
+                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                    __syncwarp();
+                    float4* row4 = reinterpret_cast<float4*>(buf + lane * 32);
+#pragma unroll
+                    for (int qq = 0; qq < 8; ++qq)
+                        row4[qq] = make_float4(__uint_as_float(v[4 * qq]), __uint_as_float(v[4 * qq + 1]),
+                                               __uint_as_float(v[4 * qq + 2]), __uint_as_float(v[4 * qq + 3]));
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) {
+                        asm volatile(
+                            "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                                (uint64_t)&tmA),
+                            "r"(j0), "r"((int)row_base), "r"(smem_u32(buf))
+                            : "memory");
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    }
+                    sb ^= 1;
+                } else if (lane < nrows) {
+                    float* out = alpha + (row_base + lane) * lda;
+#pragma unroll
+                    for (int qq = 0; qq < 32; ++qq)
+                        if (j0 + qq < K) out[j0 + qq] = __uint_as_float(v[qq]);
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&bars[8 + b]));
+        }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        __syncwarp();
+    } else {
+        // ---------------- 3xTF32 split of the Y k-block (warps 6-9)
+        const int st = tid - 6 * 32;  // 0..127
+        int64_t q = 0;
+        for (int64_t it = it0; it < it1; ++it) {
+            for (int kb = 0; kb < nkb; ++kb, ++q) {
+                const int s = (int)(q % STAGES);
+                mbar_wait(smem_u32(&bars[s]), (uint32_t)((q / STAGES) & 1));
+                float4* ah = (float4*)a_hi(s);
+                float4* al = (float4*)a_lo(s);
+#pragma unroll
+                for (int e = st; e < A_BYTES / 16; e += 128) {
+                    const float4 v = ah[e];
+                    float4 h, l;
+                    h.x = tf32_rna(v.x); l.x = v.x - h.x;
+                    h.y = tf32_rna(v.y); l.y = v.y - h.y;
+                    h.z = tf32_rna(v.z); l.z = v.z - h.z;
+                    h.w = tf32_rna(v.w); l.w = v.w - h.w;
+                    ah[e] = h;
+                    al[e] = l;
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&bars[2 + s]));
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * TN));
+}
+
+// tile_start[p] = first 128-signal tile of shard p (prefix over shards)
+__global__ void k_tile_layout(const int64_t* __restrict__ off, int P, int64_t* __restrict__ ts) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        int64_t t = 0;
+        for (int p = 0; p < P; ++p) {
+            ts[p] = t;
+            t += (off[p + 1] - off[p] + TM - 1) / TM;
+        }
+        ts[P] = t;
+    }
+}
+
 // D (P*K rows of m fp32, atom-major) -> D_hi, D_lo (P*K rows of m_pad, zero padded)
 __global__ void k_split_dict(int64_t rows, int m, int m_pad, const float* __restrict__ D,
                              float* __restrict__ Dh, float* __restrict__ Dl) {
@@ -268,6 +562,16 @@ void load_encode() {
         g_encode = (EncodeFn)fn;
 }
 
+bool make_map_plain(CUtensorMap* map, const float* ptr, int64_t cols, int64_t rows, int64_t ld_elems) {
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)(ld_elems * 4)};
+    cuuint32_t box[2] = {32, 32};
+    cuuint32_t estr[2] = {1, 1};
+    return g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)ptr, dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool make_map(CUtensorMap* map, const float* ptr, int64_t cols, int64_t rows, int64_t ld_elems,
               int box_rows) {
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
@@ -282,7 +586,7 @@ bool make_map(CUtensorMap* map, const float* ptr, int64_t cols, int64_t rows, in
 
 int64_t corr_tc_ws_bytes(int P, int64_t m, int64_t K) {
     const int64_t m_pad = (m + KB - 1) / KB * KB;
-    return 2 * (int64_t)P * K * m_pad * 4 + 256;
+    return 2 * (int64_t)P * K * m_pad * 4 + 256 + 8 * ((int64_t)P + 1) + 256;
 }
 
 int correlate_tc_f32(int64_t N, const float* Y, int64_t ldy, const int64_t* off, int64_t max_rows,
@@ -299,16 +603,36 @@ int correlate_tc_f32(int64_t N, const float* Y, int64_t ldy, const int64_t* off,
     // the Y map spans all N rows: tiles past a shard's end read neighbouring
     // signals (never stored), past N the TMA zero-fills
     CUtensorMap mY, mDh, mDl;
+    CUtensorMap mA;
     if (!make_map(&mY, Y, m, N, ldy, TM) || !make_map(&mDh, Dh, m_pad, rows, m_pad, TN) ||
-        !make_map(&mDl, Dl, m_pad, rows, m_pad, TN))
+        !make_map(&mDl, Dl, m_pad, rows, m_pad, TN) || (lda * 4) % 16 != 0 ||
+        ((uintptr_t)alpha & 15) != 0 || !make_map_plain(&mA, alpha, K, N, lda))
         return (int)cudaErrorNotSupported;
     static bool attr = false;
+    static int n_sm = 148;
     if (!attr) {
         cudaFuncSetAttribute(k_corr_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        cudaFuncSetAttribute(k_corr_tc2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES);
+        cudaFuncSetAttribute(k_corr_tc2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES);
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
         attr = true;
     }
-    dim3 grid((unsigned)((max_rows + TM - 1) / TM), (unsigned)((K + TN - 1) / TN), (unsigned)P);
-    k_corr_tc<<<grid, 128, SMEM_BYTES, st>>>(mY, mDh, mDl, off, (int)K, (int)(m_pad / KB), alpha, lda);
+    int64_t* tile_start = (int64_t*)((unsigned char*)ws + 2 * (int64_t)P * K * m_pad * 4 + 256);
+    tile_start = (int64_t*)(((uintptr_t)tile_start + 255) & ~(uintptr_t)255);
+    k_tile_layout<<<1, 32, 0, st>>>(off, P, tile_start);
+    const int nchunk = (int)((K + TN - 1) / TN);
+    // upper bound on work items (the kernel reads the exact count on device)
+    const int64_t max_items = ((N + TM - 1) / TM + P) * nchunk;
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(n_sm, max_items));
+    const int nkb = (int)(m_pad / KB);
+    if (nkb <= RES_KB)
+        k_corr_tc2<true><<<grid, NWARP2 * 32, SMEM2_BYTES, st>>>(mY, mDh, mDl, mA, off, tile_start, P, (int)K,
+                                                                 nkb, nchunk, alpha, lda);
+    else
+        k_corr_tc2<false><<<grid, NWARP2 * 32, SMEM2_BYTES, st>>>(mY, mDh, mDl, mA, off, tile_start, P, (int)K,
+                                                                  nkb, nchunk, alpha, lda);
     return (int)cudaGetLastError();
 }
 
