@@ -439,18 +439,18 @@ k_omp_fast(OmpArgs<float> a) {
     int64_t p_end = a.shard_off[p + 1];
 
     float c0n[KPL], yn[MPL];
-    auto fetch = [&](int64_t i) {
-        load_row<KPL>(c0n, a.alpha0 + i * a.lda, lane, K, vec_a);
-        const float* yr = a.Y + i * a.ldy + lane;
+    const float* arow_n = a.alpha0 + i_begin * a.lda;   // advanced by lda per signal
+    const float* yrow_n = a.Y + i_begin * a.ldy + lane;
+    auto fetch = [&]() {
+        load_row<KPL>(c0n, arow_n, lane, K, vec_a);
 #pragma unroll
-        for (int q = 0; q < MPL; ++q) yn[q] = (32 * q + lane < m) ? __ldg(yr + 32 * q) : 0.0f;
+        for (int q = 0; q < MPL; ++q) yn[q] = (32 * q + lane < m) ? __ldg(yrow_n + 32 * q) : 0.0f;
     };
-    // atoms this lane owns that exist (K not a multiple of 32*KPL)
-    float valid[KPL];
-#pragma unroll
-    for (int k = 0; k < KPL; ++k) valid[k] = (j0 + k < K) ? 1.0f : 0.0f;
+    // atoms this lane owns that exist (K not a multiple of 32*KPL): bit mask
+    const int nvalid = max(0, min(KPL, K - j0));
+    const bool all_valid = nvalid == KPL;
 
-    fetch(i_begin);
+    fetch();
     for (int64_t i = i_begin; i < i_end; ++i) {
         while (i >= p_end) { ++p; p_end = a.shard_off[p + 1]; }
         float c0[KPL], y[MPL];
@@ -458,10 +458,12 @@ k_omp_fast(OmpArgs<float> a) {
         for (int k = 0; k < KPL; ++k) c0[k] = c0n[k];
 #pragma unroll
         for (int q = 0; q < MPL; ++q) y[q] = yn[q];
-        if (i + 1 < i_end) fetch(i + 1);
+        const float* __restrict__ arow = arow_n;
+        arow_n += a.lda;
+        yrow_n += a.ldy;
+        if (i + 1 < i_end) fetch();
         const float* __restrict__ Gp = a.G + (int64_t)p * K * K;
         const float* __restrict__ Dp = a.D + (int64_t)p * K * m;
-        const float* __restrict__ arow = a.alpha0 + i * a.lda;
 
         float ysq = 0.0f;
 #pragma unroll
@@ -470,8 +472,13 @@ k_omp_fast(OmpArgs<float> a) {
         float rnorm = __fsqrt_rn(ysq);
         int n = 0, status = 0;
         float avail[KPL];  // 1: atom may be selected, 0: in the support / absent
+        if (all_valid) {
 #pragma unroll
-        for (int k = 0; k < KPL; ++k) avail[k] = valid[k];
+            for (int k = 0; k < KPL; ++k) avail[k] = 1.0f;
+        } else {
+#pragma unroll
+            for (int k = 0; k < KPL; ++k) avail[k] = (k < nvalid) ? 1.0f : 0.0f;
+        }
         if (!(rnorm <= eps || rnorm == 0.0f)) {
             for (int step = 0; step < cap; ++step) {
                 // ---- correlations of the residual, support excluded
@@ -484,7 +491,7 @@ k_omp_fast(OmpArgs<float> a) {
                     for (int k = 0; k < KPL; ++k) v[k] = c0[k];
                     for (int t = 0; t < n; ++t) {
                         float g[KPL];
-                        load_row<KPL>(g, Gp + (int64_t)ids[t] * K, lane, K, vec_g);
+                        load_row<KPL>(g, Gp + ids[t] * K, lane, K, vec_g);
                         const float coef = xs[t];
 #pragma unroll
                         for (int k = 0; k < KPL; ++k) v[k] = fmaf(-g[k], coef, v[k]);
@@ -505,9 +512,9 @@ k_omp_fast(OmpArgs<float> a) {
                 const int best = (int)__reduce_min_sync(SDB_FULL, (unsigned)cand);
 
                 // ---- Cholesky row of the new atom
-                float wme = 0.0f, dsq = __ldg(Gp + (int64_t)best * K + best);
+                float wme = 0.0f, dsq = __ldg(Gp + (best * K + best));
                 if (n > 0) {
-                    float gacc = (lane < n) ? __ldg(Gp + (int64_t)ids[lane] * K + best) : 0.0f;
+                    float gacc = (lane < n) ? __ldg(Gp + (ids[lane] * K + best)) : 0.0f;
                     for (int u = 0; u < n; ++u) {
                         const float wu = __shfl_sync(SDB_FULL, gacc, u) * invd[u];
                         if (lane == u) wme = wu;
@@ -524,7 +531,7 @@ k_omp_fast(OmpArgs<float> a) {
                 if (lane == 0) { Lrow[n] = ldiag; invd[n] = inv; ids[n] = best; }
                 float dv[MPL];  // the new atom's column (lane rows)
                 {
-                    const float* dcol = Dp + (int64_t)best * m + lane;
+                    const float* dcol = Dp + (best * m + lane);
                     float* dst = Dsel + n * m + lane;
 #pragma unroll
                     for (int q = 0; q < MPL; ++q) {
