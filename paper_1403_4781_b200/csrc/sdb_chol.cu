@@ -111,8 +111,12 @@ __device__ __forceinline__ void cols_trsv(double (*W)[S], int ncols, double (*Ls
 // column's owners publish the scaled column through a double-buffered smem
 // vector, every thread updates its 16 values — two CTA barriers per column.
 __global__ void __launch_bounds__(256)
-k_chol_diag(int K, int j0, double* __restrict__ Aall, const double* __restrict__ tol,
-            int8_t* __restrict__ depmask, int32_t* __restrict__ ndep) {
+k_chol_diag(int K, int j0, double* __restrict__ Aall, double* __restrict__ Tall,
+            const double* __restrict__ tol, int8_t* __restrict__ depmask, int32_t* __restrict__ ndep) {
+    extern __shared__ double dsm[];
+    double (*Ls)[CBP] = reinterpret_cast<double (*)[CBP]>(dsm);
+    double (*Ts)[CBP] = reinterpret_cast<double (*)[CBP]>(dsm + CB * CBP);
+    double (*Ms)[33] = reinterpret_cast<double (*)[33]>(dsm + 2 * CB * CBP);
     __shared__ double colv[2][CB];
     __shared__ double s_inv[2];
     __shared__ int8_t sdep[CB];
@@ -168,72 +172,53 @@ k_chol_diag(int K, int j0, double* __restrict__ Aall, const double* __restrict__
         for (int j = 0; j < CB / 4; ++j) {
             const int q = 4 * j + g;
             if (r < nb && q <= r) arow[q] = v[j];
+            Ls[r][q] = (r < nb && q <= r) ? v[j] : 0.0;
         }
     }
     __syncthreads();
+    // T = L^-1 (64x64 lower), blocked 2x2 of 32: warps 0/1 invert the diagonal
+    // sub-blocks column-parallel, then T21 = -T22 L21 T11 by two tile GEMMs.
+    // Dependent atoms get a zero row and column in T.
+    {
+        const int lane = tid & 31, warp = tid >> 5;
+        if (warp < 2) {
+            const int o = warp * 32, c = o + lane;
+            for (int rr2 = 0; rr2 < 32; ++rr2) Ts[o + rr2][c] = 0.0;
+            if (c < nb && !sdep[c]) {
+                Ts[c][c] = 1.0 / Ls[c][c];
+                for (int rr2 = c + 1; rr2 < min(o + 32, nb); ++rr2) {
+                    double acc = 0.0;
+                    for (int q = c; q < rr2; ++q) acc = fma(Ls[rr2][q], Ts[q][c], acc);
+                    Ts[rr2][c] = sdep[rr2] ? 0.0 : -acc / Ls[rr2][rr2];
+                }
+            }
+        }
+        // zero the upper-right block
+        for (int e = tid; e < 32 * 32; e += 256) Ts[e >> 5][32 + (e & 31)] = 0.0;
+        __syncthreads();
+        // M = L21 T11 (32x32), then T21 = -T22 M
+        for (int e = tid; e < 32 * 32; e += 256) {
+            const int rr2 = e >> 5, c = e & 31;
+            double acc = 0.0;
+            for (int q = c; q < 32; ++q) acc = fma(Ls[32 + rr2][q], Ts[q][c], acc);
+            Ms[rr2][c] = acc;
+        }
+        __syncthreads();
+        for (int e = tid; e < 32 * 32; e += 256) {
+            const int rr2 = e >> 5, c = e & 31;
+            double acc = 0.0;
+            for (int q = 0; q <= rr2; ++q) acc = fma(Ts[32 + rr2][32 + q], Ms[q][c], acc);
+            Ts[32 + rr2][c] = -acc;
+        }
+        __syncthreads();
+        double* T = Tall + ((int64_t)p * ((K + CB - 1) / CB) + j0 / CB) * CB * CB;
+        for (int e = tid; e < CB * CB; e += 256) T[e] = Ts[e / CB][e % CB];
+    }
     if (tid < nb) depmask[(int64_t)p * K + j0 + tid] = sdep[tid];
     if (tid == 0) {
         int nd = 0;
         for (int c = 0; c < nb; ++c) nd += sdep[c];
         ndep[p] += nd;
-    }
-}
-
-// blockIdx.x == 0: forward-solve the panel's RHS rows, W_j = L_jj^-1 B_j
-//                  (thread per right-hand-side column, tile in smem)
-// blockIdx.x >= 1: 64-row block of the panel: L_ij = A_ij L_jj^-T (row sweep)
-__global__ void __launch_bounds__(256)
-k_chol_panel(int K, int m, int j0, double* __restrict__ Aall, double* __restrict__ Ball,
-             const int8_t* __restrict__ depmask) {
-    extern __shared__ double csm[];
-    double (*Ls)[CBD] = reinterpret_cast<double (*)[CBD]>(csm);
-    double (*Xs)[CBD] = reinterpret_cast<double (*)[CBD]>(csm + CB * CBD);
-    __shared__ double inv[CB];
-    __shared__ int8_t sdep[CB];
-    const int p = blockIdx.y;
-    const int nb = min(CB, K - j0);
-    const int tid = threadIdx.x;
-    double* A = Aall + (int64_t)p * K * K;
-    for (int e = tid; e < CB * CB; e += 256) {
-        const int r = e / CB, c = e % CB;
-        Ls[r][c] = (r < nb && c <= r) ? A[(int64_t)(j0 + r) * K + j0 + c] : 0.0;
-    }
-    if (tid < nb) sdep[tid] = depmask[(int64_t)p * K + j0 + tid];
-    __syncthreads();
-    if (tid < nb) inv[tid] = 1.0 / Ls[tid][tid];
-    __syncthreads();
-    if (blockIdx.x == 0) {
-        double* B = Ball + (int64_t)p * K * m + (int64_t)j0 * m;
-        for (int c0 = 0; c0 < m; c0 += CB) {  // 64 RHS columns per pass, tile Xs[row][col]
-            const int nc = min(CB, m - c0);
-            __syncthreads();
-            for (int e = tid; e < CB * CB; e += 256) {
-                const int r = e / CB, c = e % CB;
-                Xs[r][c] = (r < nb && c < nc) ? B[(int64_t)r * m + c0 + c] : 0.0;
-            }
-            __syncthreads();
-            cols_trsv(Xs, nc, Ls, inv, sdep, nb, true);
-            __syncthreads();
-            for (int e = tid; e < nb * nc; e += 256) {
-                const int r = e / nc, c = e % nc;
-                B[(int64_t)r * m + c0 + c] = Xs[r][c];
-            }
-        }
-        return;
-    }
-    const int i0 = j0 + nb + (blockIdx.x - 1) * CB;
-    if (i0 >= K) return;
-    const int ni = min(CB, K - i0);
-    for (int e = tid; e < CB * CB; e += 256) {
-        const int r = e / CB, c = e % CB;
-        Xs[r][c] = (r < ni && c < nb) ? A[(int64_t)(i0 + r) * K + j0 + c] : 0.0;
-    }
-    __syncthreads();
-    rows_trsm(Xs, ni, Ls, inv, sdep, nb);
-    __syncthreads();
-    for (int e = tid; e < ni * nb; e += 256) {
-        const int r = e / nb, c = e % nb;
-        A[(int64_t)(i0 + r) * K + j0 + c] = Xs[r][c];
     }
 }
 
@@ -256,6 +241,66 @@ __device__ __forceinline__ void tile_update(double (*Xs)[CBP], double (*Ys)[CBP]
         for (int a = 0; a < 4; ++a)
 #pragma unroll
             for (int b = 0; b < 4; ++b) acc[a][b] = fma(xv[a], yv[b], acc[a][b]);
+    }
+}
+
+// blockIdx.x == 0: W_j = T_j B_j (the panel's right-hand-side rows)
+// blockIdx.x >= 1: 64-row block of the panel, L_ij = A_ij T_j^T
+// both as register-blocked 64x64 tile GEMMs (T_j = L_jj^-1 from k_chol_diag)
+__global__ void __launch_bounds__(256)
+k_chol_panel(int K, int m, int j0, double* __restrict__ Aall, double* __restrict__ Ball,
+             const double* __restrict__ Tall) {
+    extern __shared__ double csm[];
+    double (*Xs)[CBP] = reinterpret_cast<double (*)[CBP]>(csm);
+    double (*Ys)[CBP] = reinterpret_cast<double (*)[CBP]>(csm + CB * CBP);
+    const int p = blockIdx.y;
+    const int nb = min(CB, K - j0);
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const double* T = Tall + ((int64_t)p * ((K + CB - 1) / CB) + j0 / CB) * CB * CB;
+    double acc[4][4];
+    if (blockIdx.x == 0) {
+        double* B = Ball + (int64_t)p * K * m + (int64_t)j0 * m;
+        for (int e = tid; e < CB * CB; e += 256) Xs[e / CB][e % CB] = T[e];  // Xs[r][q] = T[r][q]
+        for (int c0 = 0; c0 < m; c0 += CB) {
+            const int nc = min(CB, m - c0);
+            __syncthreads();
+            for (int e = tid; e < CB * CB; e += 256) {  // Ys[col][q] = B[q][col]
+                const int q = e / CB, c = e % CB;
+                Ys[c][q] = (q < nb && c < nc) ? B[(int64_t)q * m + c0 + c] : 0.0;
+            }
+            __syncthreads();
+            tile_update(Xs, Ys, nb, acc);
+#pragma unroll
+            for (int a2 = 0; a2 < 4; ++a2) {
+                const int r = ty + 16 * a2;
+#pragma unroll
+                for (int b2 = 0; b2 < 4; ++b2) {
+                    const int c = tx + 16 * b2;
+                    if (r < nb && c < nc) B[(int64_t)r * m + c0 + c] = acc[a2][b2];
+                }
+            }
+        }
+        return;
+    }
+    const int i0 = j0 + nb + (blockIdx.x - 1) * CB;
+    if (i0 >= K) return;
+    const int ni = min(CB, K - i0);
+    double* A = Aall + (int64_t)p * K * K;
+    for (int e = tid; e < CB * CB; e += 256) {
+        const int r = e / CB, c = e % CB;
+        Xs[r][c] = (r < ni && c < nb) ? A[(int64_t)(i0 + r) * K + j0 + c] : 0.0;
+        Ys[r][c] = T[e];  // Ys[c][q] = T[c][q]  ->  out[r][c] = sum_q X[r][q] T[c][q]
+    }
+    __syncthreads();
+    tile_update(Xs, Ys, nb, acc);
+#pragma unroll
+    for (int a2 = 0; a2 < 4; ++a2) {
+        const int r = ty + 16 * a2;
+#pragma unroll
+        for (int b2 = 0; b2 < 4; ++b2) {
+            const int c = tx + 16 * b2;
+            if (r < ni && c < nb) A[(int64_t)(i0 + r) * K + j0 + c] = acc[a2][b2];
+        }
     }
 }
 
@@ -326,38 +371,39 @@ k_chol_update(int K, int m, int j0, double* __restrict__ Aall, double* __restric
     }
 }
 
-// back substitution, panel j0: solve L_jj^T Z_j = W_j in place (thread per
-// right-hand-side column, 64-column tiles in smem)
+// back substitution, panel j0: Z_j = T_j^T W_j in place (tile GEMM)
 __global__ void __launch_bounds__(256)
-k_back_diag(int K, int m, int j0, const double* __restrict__ Aall, double* __restrict__ Ball) {
+k_back_diag(int K, int m, int j0, const double* __restrict__ Tall, double* __restrict__ Ball) {
     extern __shared__ double csm[];
-    double (*Ls)[CBD] = reinterpret_cast<double (*)[CBD]>(csm);
-    double (*Ws)[CBD] = reinterpret_cast<double (*)[CBD]>(csm + CB * CBD);
-    __shared__ double inv[CB];
+    double (*Xs)[CBP] = reinterpret_cast<double (*)[CBP]>(csm);
+    double (*Ys)[CBP] = reinterpret_cast<double (*)[CBP]>(csm + CB * CBP);
     const int p = blockIdx.x;
     const int nb = min(CB, K - j0);
-    const int tid = threadIdx.x;
-    const double* A = Aall + (int64_t)p * K * K;
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const double* T = Tall + ((int64_t)p * ((K + CB - 1) / CB) + j0 / CB) * CB * CB;
     double* B = Ball + (int64_t)p * K * m + (int64_t)j0 * m;
-    for (int e = tid; e < CB * CB; e += 256) {
-        const int r = e / CB, c = e % CB;
-        Ls[r][c] = (r < nb && c <= r) ? A[(int64_t)(j0 + r) * K + j0 + c] : 0.0;
+    for (int e = tid; e < CB * CB; e += 256) {  // Xs[r][q] = T[q][r]
+        const int q = e / CB, r = e % CB;
+        Xs[r][q] = T[e];
     }
-    __syncthreads();
-    if (tid < nb) inv[tid] = 1.0 / Ls[tid][tid];
+    double acc[4][4];
     for (int c0 = 0; c0 < m; c0 += CB) {
         const int nc = min(CB, m - c0);
         __syncthreads();
-        for (int e = tid; e < CB * CB; e += 256) {
-            const int r = e / CB, c = e % CB;
-            Ws[r][c] = (r < nb && c < nc) ? B[(int64_t)r * m + c0 + c] : 0.0;
+        for (int e = tid; e < CB * CB; e += 256) {  // Ys[col][q] = W[q][col]
+            const int q = e / CB, c = e % CB;
+            Ys[c][q] = (q < nb && c < nc) ? B[(int64_t)q * m + c0 + c] : 0.0;
         }
         __syncthreads();
-        cols_trsv(Ws, nc, Ls, inv, (const int8_t*)nullptr, nb, false);
-        __syncthreads();
-        for (int e = tid; e < nb * nc; e += 256) {
-            const int r = e / nc, c = e % nc;
-            B[(int64_t)r * m + c0 + c] = Ws[r][c];
+        tile_update(Xs, Ys, nb, acc);
+#pragma unroll
+        for (int a2 = 0; a2 < 4; ++a2) {
+            const int r = ty + 16 * a2;
+#pragma unroll
+            for (int b2 = 0; b2 < 4; ++b2) {
+                const int c = tx + 16 * b2;
+                if (r < nb && c < nc) B[(int64_t)r * m + c0 + c] = acc[a2][b2];
+            }
         }
     }
 }
@@ -414,19 +460,26 @@ __global__ void __launch_bounds__(256) k_sumsq(int64_t n, const double* __restri
     if (threadIdx.x == 0) out[blockIdx.x] = sh[0];
 }
 
-int64_t chol_ws_bytes(int P, int K) { return (int64_t)P * sizeof(double) + 512; }
+int64_t chol_ws_bytes(int P, int K) {
+    const int64_t nblk = (K + CB - 1) / CB;
+    return (int64_t)P * nblk * CB * CB * sizeof(double) + (int64_t)P * sizeof(double) + 512;
+}
 
 int chol_solve(int P, int K, int m, double* A, double* B, const int32_t* usage, double rel_tol,
                int8_t* depmask, int32_t* ndep, double* wsq, void* ws, cudaStream_t st) {
     const int64_t nblk = (K + CB - 1) / CB;
-    double* tol = (double*)ws;
+    double* T = (double*)ws;
+    double* tol = T + (int64_t)P * nblk * CB * CB;
     const int smem2 = 2 * CB * CBD * (int)sizeof(double);
+    const int smemP = 2 * CB * CBP * (int)sizeof(double);
+    const int smemD = (2 * CB * CBP + 32 * 33) * (int)sizeof(double);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_chol_update, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
         cudaFuncSetAttribute(k_back_update, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
-        cudaFuncSetAttribute(k_chol_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
-        cudaFuncSetAttribute(k_back_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+        cudaFuncSetAttribute(k_chol_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, smemP);
+        cudaFuncSetAttribute(k_back_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, smemP);
+        cudaFuncSetAttribute(k_chol_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, smemD);
         attr = true;
     }
     {
@@ -437,10 +490,10 @@ int chol_solve(int P, int K, int m, double* A, double* B, const int32_t* usage, 
     const int nmc = (m + CB - 1) / CB;
     for (int j0 = 0; j0 < K; j0 += CB) {
         const int nb = std::min(CB, K - j0);
-        k_chol_diag<<<P, 256, 0, st>>>(K, j0, A, tol, depmask, ndep);
+        k_chol_diag<<<P, 256, smemD, st>>>(K, j0, A, T, tol, depmask, ndep);
         const int rows_below = K - j0 - nb;
         dim3 gp((unsigned)(1 + (rows_below + CB - 1) / CB), (unsigned)P);
-        k_chol_panel<<<gp, 256, smem2, st>>>(K, m, j0, A, B, depmask);
+        k_chol_panel<<<gp, 256, smemP, st>>>(K, m, j0, A, B, T);
         const int nt = (rows_below + CB - 1) / CB;
         const int tiles = nt * (nt + 1) / 2 + nt * nmc;
         if (tiles > 0) {
@@ -451,7 +504,7 @@ int chol_solve(int P, int K, int m, double* A, double* B, const int32_t* usage, 
     if (wsq) k_sumsq<<<P, 256, 0, st>>>((int64_t)K * m, B, wsq);
     const int last = (int)((nblk - 1) * CB);
     for (int j0 = last; j0 >= 0; j0 -= CB) {
-        k_back_diag<<<P, 256, smem2, st>>>(K, m, j0, A, B);
+        k_back_diag<<<P, 256, smemP, st>>>(K, m, j0, T, B);
         if (j0 > 0) {
             const int ib = (j0 + CB - 1) / CB;
             dim3 gb((unsigned)(ib * nmc), (unsigned)P);
