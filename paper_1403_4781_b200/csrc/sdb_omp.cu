@@ -364,20 +364,26 @@ k_omp(OmpArgs<T> a) {
 // ----------------------------------------------------------------------------
 // FP32 fast path (cap <= 32): same algorithm and stopping rules as k_omp, but
 //  * each warp owns a contiguous range of signals and prefetches the next
-//    signal's alpha0 row and y while the current one is coded;
+//    signal's alpha0 row and y into L1 while the current one is coded;
 //  * y and the residual live in registers (lane owns rows lane + 32q);
 //  * argmax is two redux.sync ops: |corr| >= 0 so its IEEE bits order like
 //    the values, and in FP32 the reference's 1e-12 tie window collapses to
 //    exact equality (cmax - 1e-12*cmax == cmax), i.e. lowest index among the
 //    maxima;
 //  * Cholesky / substitutions are lane-parallel column sweeps;
-//  * the selected atoms' columns are cached in shared memory for the residual.
+//  * ||r||^2 is tracked through the projection identity ||y||^2 - ||z||^2
+//    (z = L^-1 alpha0_S grows by one entry per step); the explicit residual
+//    is formed only when
+//    that estimate is within 1e-4 ||y||^2 of eps^2 and once for the output;
+//  * every load of a step (G[b,b], G[S,b], alpha0[b]) is issued together
+//    right after the argmax, so a step costs one L2 round trip;
+//  * the support is excluded by overwriting c0[b] with NaN (fmaxf skips it).
 // ----------------------------------------------------------------------------
 constexpr int FAST_CAP = 32;
 constexpr int FAST_TRI = FAST_CAP * (FAST_CAP + 1) / 2;
 
 __host__ __device__ inline int fast_warp_floats(int cap, int m) {
-    return FAST_TRI + 4 * FAST_CAP + cap * m;  // L, 1/diag, tmp, x, ids(as int), Dsel
+    return FAST_TRI + 4 * FAST_CAP;  // L, 1/diag, tmp, x, ids(as int)
 }
 
 // lane owns the KPL consecutive atoms [lane*KPL, lane*KPL + KPL): rows of
@@ -410,7 +416,7 @@ __device__ __forceinline__ void load_row(float (&v)[KPL], const float* __restric
 }
 
 template <int KPL, int MPL>
-__global__ void __launch_bounds__(256, (KPL >= 16) ? 1 : (KPL >= 8 ? 3 : 4))
+__global__ void __launch_bounds__(256, (KPL >= 16) ? 1 : (MPL >= 5 ? 3 : 4))
 k_omp_fast(OmpArgs<float> a) {
     extern __shared__ __align__(16) float fsm[];
     const int lane = threadIdx.x & 31;
@@ -422,8 +428,8 @@ k_omp_fast(OmpArgs<float> a) {
     float* tmp = invd + FAST_CAP;
     float* xs = tmp + FAST_CAP;
     int* ids = (int*)(xs + FAST_CAP);
-    float* Dsel = (float*)(ids + FAST_CAP);
     const float eps = a.eps;
+    const float eps2 = eps * eps;
     const int j0 = lane * KPL;
 
     const int64_t gw = (int64_t)blockIdx.x * wpb + wib;
@@ -437,55 +443,83 @@ k_omp_fast(OmpArgs<float> a) {
 
     int p = shard_of(a.shard_off, a.P, i_begin);
     int64_t p_end = a.shard_off[p + 1];
+    const float* __restrict__ Gp = a.G + (int64_t)p * K * K;
+    const float* __restrict__ Dp = a.D + (int64_t)p * K * m;
 
-    float c0n[KPL], yn[MPL];
     const float* arow_n = a.alpha0 + i_begin * a.lda;   // advanced by lda per signal
     const float* yrow_n = a.Y + i_begin * a.ldy + lane;
-    auto fetch = [&]() {
-        load_row<KPL>(c0n, arow_n, lane, K, vec_a);
+    // the next signal's alpha0 row and y are prefetched into L1 (no registers
+    // held across the signal, which keeps occupancy at 4 blocks / SM)
+    auto prefetch_next = [&]() {
+        const float* an = arow_n + a.lda;
+        if (j0 < K) asm volatile("prefetch.global.L1 [%0];" ::"l"(an + j0));
+        if constexpr (KPL > 8) {
+            if (j0 + 8 < K) asm volatile("prefetch.global.L1 [%0];" ::"l"(an + j0 + 8));
+        }
 #pragma unroll
-        for (int q = 0; q < MPL; ++q) yn[q] = (32 * q + lane < m) ? __ldg(yrow_n + 32 * q) : 0.0f;
+        for (int q = 0; q < MPL; ++q)
+            if (32 * q + lane < m && (lane & 7) == 0)
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(yrow_n + a.ldy + 32 * q));
     };
-    // atoms this lane owns that exist (K not a multiple of 32*KPL): bit mask
+    // atoms this lane owns that exist (K not a multiple of 32*KPL)
     const int nvalid = max(0, min(KPL, K - j0));
     const bool all_valid = nvalid == KPL;
+    const float kNaN = __int_as_float(0x7fffffff);
 
-    fetch();
     for (int64_t i = i_begin; i < i_end; ++i) {
-        while (i >= p_end) { ++p; p_end = a.shard_off[p + 1]; }
+        if (i >= p_end) {
+            while (i >= p_end) { ++p; p_end = a.shard_off[p + 1]; }
+            Gp = a.G + (int64_t)p * K * K;
+            Dp = a.D + (int64_t)p * K * m;
+        }
+        // c0 doubles as the selection mask: a selected (or absent) atom's entry
+        // is NaN, which fmaxf skips and whose bits never equal the maximum
         float c0[KPL], y[MPL];
+        load_row<KPL>(c0, arow_n, lane, K, vec_a);
 #pragma unroll
-        for (int k = 0; k < KPL; ++k) c0[k] = c0n[k];
+        for (int q = 0; q < MPL; ++q) y[q] = (32 * q + lane < m) ? __ldg(yrow_n + 32 * q) : 0.0f;
+        if (!all_valid) {
 #pragma unroll
-        for (int q = 0; q < MPL; ++q) y[q] = yn[q];
+            for (int k = 0; k < KPL; ++k) c0[k] = (k < nvalid) ? c0[k] : kNaN;
+        }
+        if (i + 1 < i_end) prefetch_next();
         const float* __restrict__ arow = arow_n;
         arow_n += a.lda;
         yrow_n += a.ldy;
-        if (i + 1 < i_end) fetch();
-        const float* __restrict__ Gp = a.G + (int64_t)p * K * K;
-        const float* __restrict__ Dp = a.D + (int64_t)p * K * m;
 
         float ysq = 0.0f;
 #pragma unroll
         for (int q = 0; q < MPL; ++q) ysq = fmaf(y[q], y[q], ysq);
         ysq = warp_sum(ysq);
         float rnorm = __fsqrt_rn(ysq);
+        float rsq = ysq;
         int n = 0, status = 0;
-        float avail[KPL];  // 1: atom may be selected, 0: in the support / absent
-        if (all_valid) {
+        // explicit ||y - D_S x|| (support columns read from L2, independent loads)
+        auto resid_norm = [&](int nn) {
+            __syncwarp();
+            float rr[MPL];
 #pragma unroll
-            for (int k = 0; k < KPL; ++k) avail[k] = 1.0f;
-        } else {
+            for (int q = 0; q < MPL; ++q) rr[q] = y[q];
+#pragma unroll 4
+            for (int t = 0; t < nn; ++t) {
+                const float xt = xs[t];
+                const float* dc = Dp + ids[t] * m + lane;
 #pragma unroll
-            for (int k = 0; k < KPL; ++k) avail[k] = (k < nvalid) ? 1.0f : 0.0f;
-        }
+                for (int q = 0; q < MPL; ++q)
+                    if (32 * q + lane < m) rr[q] = fmaf(-__ldg(dc + 32 * q), xt, rr[q]);
+            }
+            float rs = 0.0f;
+#pragma unroll
+            for (int q = 0; q < MPL; ++q) rs = fmaf(rr[q], rr[q], rs);
+            return __fsqrt_rn(warp_sum(rs));
+        };
         if (!(rnorm <= eps || rnorm == 0.0f)) {
             for (int step = 0; step < cap; ++step) {
                 // ---- correlations of the residual, support excluded
                 float v[KPL];
                 if (n == 0) {
 #pragma unroll
-                    for (int k = 0; k < KPL; ++k) v[k] = fabsf(c0[k]) * avail[k];
+                    for (int k = 0; k < KPL; ++k) v[k] = fabsf(c0[k]);
                 } else {
 #pragma unroll
                     for (int k = 0; k < KPL; ++k) v[k] = c0[k];
@@ -497,7 +531,7 @@ k_omp_fast(OmpArgs<float> a) {
                         for (int k = 0; k < KPL; ++k) v[k] = fmaf(-g[k], coef, v[k]);
                     }
 #pragma unroll
-                    for (int k = 0; k < KPL; ++k) v[k] = fabsf(v[k]) * avail[k];
+                    for (int k = 0; k < KPL; ++k) v[k] = fabsf(v[k]);
                 }
                 float lm = 0.0f;
 #pragma unroll
@@ -511,10 +545,18 @@ k_omp_fast(OmpArgs<float> a) {
                     if (__float_as_uint(v[k]) == cbits) cand = j0 + k;
                 const int best = (int)__reduce_min_sync(SDB_FULL, (unsigned)cand);
 
+                // ---- every load of this step issued at once: G[b,b], G[S,b], c0[b]
+                float dsq = __ldg(Gp + (best * K + best));
+                float gacc = (lane < n) ? __ldg(Gp + (ids[lane] * K + best)) : 0.0f;
+                const float cb = __ldg(arow + best);
+                {
+                    const int kk = best - j0;   // in [0, KPL) on the owning lane only
+#pragma unroll
+                    for (int k = 0; k < KPL; ++k) c0[k] = (kk == k) ? kNaN : c0[k];
+                }
                 // ---- Cholesky row of the new atom
-                float wme = 0.0f, dsq = __ldg(Gp + (best * K + best));
+                float wme = 0.0f;
                 if (n > 0) {
-                    float gacc = (lane < n) ? __ldg(Gp + (ids[lane] * K + best)) : 0.0f;
                     for (int u = 0; u < n; ++u) {
                         const float wu = __shfl_sync(SDB_FULL, gacc, u) * invd[u];
                         if (lane == u) wme = wu;
@@ -523,38 +565,19 @@ k_omp_fast(OmpArgs<float> a) {
                     dsq -= warp_sum(lane < n ? wme * wme : 0.0f);
                 }
                 if (dsq <= a.guard) { status = 2; break; }
-                const float cb = __ldg(arow + best);   // c0[best]
                 const float ldiag = __fsqrt_rn(dsq);
                 const float inv = 1.0f / ldiag;
                 float* Lrow = Ls + n * (n + 1) / 2;
                 if (lane < n) Lrow[lane] = wme;
                 if (lane == 0) { Lrow[n] = ldiag; invd[n] = inv; ids[n] = best; }
-                float dv[MPL];  // the new atom's column (lane rows)
-                {
-                    const float* dcol = Dp + (best * m + lane);
-                    float* dst = Dsel + n * m + lane;
-#pragma unroll
-                    for (int q = 0; q < MPL; ++q) {
-                        dv[q] = (32 * q + lane < m) ? __ldg(dcol + 32 * q) : 0.0f;
-                        if (32 * q + lane < m) dst[32 * q] = dv[q];
-                    }
-                }
-                if (lane == best / KPL) {
-#pragma unroll
-                    for (int k = 0; k < KPL; ++k)
-                        if (j0 + k == best) avail[k] = 0.0f;
-                }
-                float rr[MPL];
+                float tn;
                 if (n == 0) {
-                    // one atom: tmp = c0[b]/L00, x = tmp/L00, r = y - d_b x
-                    const float tn = cb * inv;
-                    const float x0 = tn * inv;
-                    if (lane == 0) { tmp[0] = tn; xs[0] = x0; }
-#pragma unroll
-                    for (int q = 0; q < MPL; ++q) rr[q] = fmaf(-dv[q], x0, y[q]);
+                    // one atom: tmp = c0[b]/L00, x = tmp/L00
+                    tn = cb * inv;
+                    if (lane == 0) { tmp[0] = tn; xs[0] = tn * inv; }
                     n = 1;
                 } else {
-                    const float tn = (cb - warp_sum(lane < n ? wme * tmp[lane] : 0.0f)) * inv;
+                    tn = (cb - warp_sum(lane < n ? wme * tmp[lane] : 0.0f)) * inv;
                     n += 1;
                     __syncwarp();
                     if (lane == 0) tmp[n - 1] = tn;
@@ -567,24 +590,22 @@ k_omp_fast(OmpArgs<float> a) {
                         else if (lane < u) bacc = fmaf(-Ls[u * (u + 1) / 2 + lane], xu, bacc);
                     }
                     if (lane < n) xs[lane] = xme;
-                    __syncwarp();
-#pragma unroll
-                    for (int q = 0; q < MPL; ++q) rr[q] = y[q];
-                    for (int t = 0; t < n; ++t) {
-                        const float xt = xs[t];
-                        const float* dc = Dsel + t * m + lane;
-#pragma unroll
-                        for (int q = 0; q < MPL; ++q)
-                            if (32 * q + lane < m) rr[q] = fmaf(-dc[32 * q], xt, rr[q]);
-                    }
                 }
-                float rs = 0.0f;
-#pragma unroll
-                for (int q = 0; q < MPL; ++q) rs = fmaf(rr[q], rr[q], rs);
-                rnorm = __fsqrt_rn(warp_sum(rs));
+                // ||r||^2 = ||y||^2 - ||L^-1 c0_S||^2 (projection identity): O(1) per
+                // step. Only near the threshold is the explicit residual formed, so
+                // the stopping decision is the one the explicit residual gives.
+                rsq = fmaxf(rsq - tn * tn, 0.0f);
+                rnorm = __fsqrt_rn(rsq);
                 __syncwarp();
-                if (rnorm <= eps) break;
+                if (fabsf(rsq - eps2) <= 1e-4f * ysq) {
+                    rnorm = resid_norm(n);
+                    if (rnorm <= eps) break;
+                } else if (rsq <= eps2) {
+                    break;
+                }
             }
+            // reported norm: explicit residual of the final support
+            if (n > 0) rnorm = resid_norm(n);
         }
         __syncwarp();
         if (lane < cap) {
