@@ -77,26 +77,50 @@ k_chunk_hist(const int64_t* __restrict__ off, const int64_t* __restrict__ cf, in
     for (int a = lane; a < K; a += 32) chunk_hist[c * K + a] = cnt[a];
 }
 
-// ---- (b) usage[p][a] = sum over the shard's chunks
-__global__ void k_usage_from_chunks(const int64_t* __restrict__ cf, int P, int K,
-                                    const int32_t* __restrict__ chunk_hist, int32_t* __restrict__ usage) {
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= (int64_t)P * K) return;
-    const int p = (int)(e / K), a = (int)(e % K);
-    int32_t s = 0;
-    for (int64_t c = cf[p]; c < cf[p + 1]; ++c) s += chunk_hist[c * K + a];
-    usage[e] = s;
+// ---- (b) usage[p][a] = sum over the shard's chunks. Block = (shard, 32
+// atoms); warp w sums the w-th eighth of the shard's chunks (lane = atom) and
+// keeps that partial for (d).
+__device__ __forceinline__ void chunk_piece(const int64_t* cf, int p, int w, int64_t& c0, int64_t& c1) {
+    const int64_t lo = cf[p], n = cf[p + 1] - lo;
+    c0 = lo + n * w / 8;
+    c1 = lo + n * (w + 1) / 8;
+}
+
+__global__ void __launch_bounds__(256)
+k_usage_from_chunks(const int64_t* __restrict__ cf, int P, int K, const int32_t* __restrict__ chunk_hist,
+                    int64_t* __restrict__ wpart, int32_t* __restrict__ usage) {
+    __shared__ int64_t part[8][32];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int p = blockIdx.y, a = blockIdx.x * 32 + lane;
+    int64_t c0, c1;
+    chunk_piece(cf, p, wib, c0, c1);
+    int64_t s = 0;
+    if (a < K)
+        for (int64_t c = c0; c < c1; ++c) s += chunk_hist[c * K + a];
+    part[wib][lane] = s;
+    if (a < K) wpart[((int64_t)p * 8 + wib) * K + a] = s;
+    __syncthreads();
+    if (wib == 0 && a < K) {
+        int64_t t = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) t += part[w][lane];
+        usage[(int64_t)p * K + a] = (int32_t)t;
+    }
 }
 
 // ---- (d) chunk_off[c][a] = bucket_off[p][a] + prefix over earlier chunks
-__global__ void k_chunk_offsets(const int64_t* __restrict__ cf, int P, int K,
-                                const int32_t* __restrict__ chunk_hist,
-                                const int64_t* __restrict__ bucket_off, int64_t* __restrict__ chunk_off) {
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= (int64_t)P * K) return;
-    const int p = (int)(e / K), a = (int)(e % K);
-    int64_t run = bucket_off[e];
-    for (int64_t c = cf[p]; c < cf[p + 1]; ++c) {
+__global__ void __launch_bounds__(256)
+k_chunk_offsets(const int64_t* __restrict__ cf, int P, int K, const int32_t* __restrict__ chunk_hist,
+                const int64_t* __restrict__ wpart, const int64_t* __restrict__ bucket_off,
+                int64_t* __restrict__ chunk_off) {
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int p = blockIdx.y, a = blockIdx.x * 32 + lane;
+    if (a >= K) return;
+    int64_t run = bucket_off[(int64_t)p * K + a];
+    for (int w = 0; w < wib; ++w) run += wpart[((int64_t)p * 8 + w) * K + a];
+    int64_t c0, c1;
+    chunk_piece(cf, p, wib, c0, c1);
+    for (int64_t c = c0; c < c1; ++c) {
         chunk_off[c * K + a] = run;
         run += chunk_hist[c * K + a];
     }
@@ -196,10 +220,13 @@ k_yxt(int P, int K, int m, const T* __restrict__ Y, int64_t ldy, const int64_t* 
     }
 }
 
-// ---- (g) A[p][a][:] = sum over bucket (x_ai * x_i). One CTA per (p, a):
-// warp w accumulates batches w, w+8, ... into its own smem row (code rows of
-// a batch staged in smem first, all loads in flight), rows combined in warp
-// order (deterministic).
+// ---- (g) A[p][a][:] = sum over bucket (x_ai * x_i). One CTA per (p, a);
+// warp w accumulates batches w, w+8, ... into its own smem row, rows combined
+// in warp order. Within a batch each lane owns one signal and the warp walks
+// the code rows in uniform rounds t: the diagonal term (every signal of the
+// bucket has x_a) is one warp sum per batch; off-diagonal entries colliding
+// on the same column in a round are applied in ascending lane order
+// (match.any). Every update order is a fixed function of the input.
 constexpr int XXT_CAP = 32;
 
 template <typename T>
@@ -210,13 +237,16 @@ k_xxt(int P, int K, int cap, const int32_t* __restrict__ idx, const T* __restric
     extern __shared__ double sh_row[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t e = blockIdx.x;
+    const int self = (int)(e % K);
     double* row = sh_row + (int64_t)wib * K;
-    int32_t* sidx = (int32_t*)(sh_row + 8 * (int64_t)K) + wib * 32 * XXT_CAP;
-    double* sval = (double*)(sh_row + 8 * (int64_t)K + 4 * 32 * XXT_CAP) + wib * 32 * XXT_CAP;
+    const bool staged = cap <= XXT_CAP;
+    const int rows = staged ? cap : 0;
+    int32_t* sidx = (int32_t*)(sh_row + 8 * (int64_t)K) + wib * 32 * rows;            // [t][lane]
+    double* sval = (double*)(sh_row + 8 * (int64_t)K + 4 * 32 * rows) + wib * 32 * rows;  // [t][lane]
     for (int b = lane; b < K; b += 32) row[b] = 0.0;
     __syncwarp();
     const int64_t lo = bucket_off[e], hi = bucket_off[e + 1];
-    const bool staged = cap <= XXT_CAP;
+    double diag = 0.0;
     for (int64_t q0 = lo + 32 * wib; q0 < hi; q0 += 32 * 8) {
         const int nbat = (int)min((int64_t)32, hi - q0);
         const int my_sig = lane < nbat ? bsig[q0 + lane] : 0;
@@ -224,23 +254,44 @@ k_xxt(int P, int K, int cap, const int32_t* __restrict__ idx, const T* __restric
         const int my_n = lane < nbat ? counts[my_sig] : 0;
         if (staged) {
             for (int t = 0; t < my_n; ++t) {
-                sidx[lane * XXT_CAP + t] = idx[(int64_t)my_sig * cap + t];
-                sval[lane * XXT_CAP + t] = (double)val[(int64_t)my_sig * cap + t];
+                sidx[t * 32 + lane] = idx[(int64_t)my_sig * cap + t];
+                sval[t * 32 + lane] = (double)val[(int64_t)my_sig * cap + t];
             }
             __syncwarp();
-        }
-        for (int j = 0; j < nbat; ++j) {
-            const double v = __shfl_sync(SDB_FULL, my_v, j);
-            const int n = __shfl_sync(SDB_FULL, my_n, j);
-            const int i = __shfl_sync(SDB_FULL, my_sig, j);
-            for (int t = lane; t < n; t += 32) {
-                const int b = staged ? sidx[j * XXT_CAP + t] : idx[(int64_t)i * cap + t];
-                const double w = staged ? sval[j * XXT_CAP + t] : (double)val[(int64_t)i * cap + t];
-                row[b] = fma(v, w, row[b]);
+            diag += warp_sum(my_v * my_v);
+            const int nmax = (int)__reduce_max_sync(SDB_FULL, (unsigned)my_n);
+            for (int t = 0; t < nmax; ++t) {
+                int b = -1;
+                double c = 0.0;
+                if (t < my_n) {
+                    b = sidx[t * 32 + lane];
+                    c = my_v * sval[t * 32 + lane];
+                    if (b == self) b = -1;  // diagonal: summed above
+                }
+                const bool act = b >= 0;
+                const unsigned peers = __match_any_sync(SDB_FULL, act ? b : K + lane);
+                const int rank = __popc(peers & ((1u << lane) - 1u));
+                const int gmax = (int)__reduce_max_sync(SDB_FULL, act ? (unsigned)__popc(peers) : 0u);
+                for (int r = 0; r < gmax; ++r) {
+                    if (act && rank == r) row[b] += c;
+                    __syncwarp();
+                }
             }
             __syncwarp();
+        } else {
+            for (int j = 0; j < nbat; ++j) {
+                const double v = __shfl_sync(SDB_FULL, my_v, j);
+                const int n = __shfl_sync(SDB_FULL, my_n, j);
+                const int i = __shfl_sync(SDB_FULL, my_sig, j);
+                for (int t = lane; t < n; t += 32) {
+                    const int b = idx[(int64_t)i * cap + t];
+                    row[b] = fma(v, (double)val[(int64_t)i * cap + t], row[b]);
+                }
+                __syncwarp();
+            }
         }
     }
+    if (staged && lane == 0) row[self] += diag;
     __syncthreads();
     double* out = A + e * K;
     for (int b = threadIdx.x; b < K; b += 256) {
@@ -445,52 +496,55 @@ k_mod_finish(int P, int K, int m, const double* __restrict__ Z, const double* __
 }
 
 // ---- replace_degenerate_atoms (dictionary_update.py:134-176)
-// degenerate flags + twins, one CTA per shard: norms and "row has a twin"
-// flags in parallel, then the order-dependent rule (the lower index of a pair
-// is kept unless itself degenerate) sequentially over the rows with twins only.
-__global__ void __launch_bounds__(1024)
-k_twins(int K, const double* __restrict__ C, const double* __restrict__ D, int m,
-        const int32_t* __restrict__ usage, int8_t* __restrict__ deg, int32_t* __restrict__ ntarget) {
-    extern __shared__ int8_t sh_flags[];
-    int8_t* dg = sh_flags;          // K
-    int8_t* tw = sh_flags + K;      // K
-    __shared__ int s_cnt;
-    const int p = blockIdx.x;
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const double* Cp = C + (int64_t)p * K * K;
-    for (int a = wib; a < K; a += 32) {
-        const double* d = D + ((int64_t)p * K + a) * m;
-        double s = 0.0;
-        for (int r = lane; r < m; r += 32) s = fma(d[r], d[r], s);
-        s = warp_sum(s);
-        const double* ci = Cp + (int64_t)a * K;
-        bool any = false;
-        for (int j = a + 1 + lane; j < K; j += 32) any |= fabs(ci[j]) > 0.999;
-        any = __any_sync(SDB_FULL, any);
-        if (lane == 0) {
-            dg[a] = (usage[(int64_t)p * K + a] == 0 || sqrt(s) <= 1e-12) ? 1 : 0;
-            tw[a] = any ? 1 : 0;
-        }
+// (1) warp per (shard, atom): degenerate flag (unused or zero norm) and "row
+// has a twin to its right" (|C_aj| > 0.999, j > a);
+__global__ void __launch_bounds__(256)
+k_twin_flags(int P, int K, const double* __restrict__ C, const double* __restrict__ D, int m,
+             const int32_t* __restrict__ usage, int8_t* __restrict__ deg, int8_t* __restrict__ tw) {
+    const int lane = threadIdx.x & 31;
+    const int64_t e = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (e >= (int64_t)P * K) return;
+    const int a = (int)(e % K);
+    const double* d = D + e * m;
+    double s = 0.0;
+    for (int r = lane; r < m; r += 32) s = fma(d[r], d[r], s);
+    s = warp_sum(s);
+    const double* ci = C + e * K;
+    bool any = false;
+    for (int j = a + 1 + lane; j < K; j += 32) any |= fabs(ci[j]) > 0.999;
+    any = __any_sync(SDB_FULL, any);
+    if (lane == 0) {
+        deg[e] = (usage[e] == 0 || sqrt(s) <= 1e-12) ? 1 : 0;
+        tw[e] = any ? 1 : 0;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < K; ++i) {
-            if (!tw[i] || dg[i]) continue;
+}
+
+// (2) one warp per shard: the order-dependent rule (the lower index of a pair
+// is kept unless itself degenerate) over the rows that have twins, ascending;
+// the columns of a row are marked lane-parallel.
+__global__ void __launch_bounds__(32)
+k_twins(int K, const double* __restrict__ C, const int8_t* __restrict__ tw, int8_t* __restrict__ deg,
+        int32_t* __restrict__ ntarget) {
+    const int p = blockIdx.x, lane = threadIdx.x;
+    const double* Cp = C + (int64_t)p * K * K;
+    int8_t* dg = deg + (int64_t)p * K;
+    const int8_t* twp = tw + (int64_t)p * K;
+    for (int i0 = 0; i0 < K; i0 += 32) {
+        const unsigned rows = __ballot_sync(SDB_FULL, i0 + lane < K && twp[i0 + lane] != 0);
+        for (unsigned r = rows; r; r &= r - 1) {
+            const int i = i0 + __ffs(r) - 1;
+            __syncwarp();
+            if (dg[i]) continue;  // warp-uniform (read after the barrier)
             const double* ci = Cp + (int64_t)i * K;
-            for (int j = i + 1; j < K; ++j)
+            for (int j = i + 1 + lane; j < K; j += 32)
                 if (fabs(ci[j]) > 0.999) dg[j] = 1;
         }
-        s_cnt = 0;
     }
-    __syncthreads();
+    __syncwarp();
     int cnt = 0;
-    for (int a = threadIdx.x; a < K; a += 1024) {
-        deg[(int64_t)p * K + a] = dg[a];
-        cnt += dg[a];
-    }
-    atomicAdd(&s_cnt, cnt);
-    __syncthreads();
-    if (threadIdx.x == 0) ntarget[p] = s_cnt;
+    for (int a = lane; a < K; a += 32) cnt += dg[a];
+    cnt = __reduce_add_sync(SDB_FULL, cnt);
+    if (lane == 0) ntarget[p] = cnt;
 }
 
 // normalised copy Dn = D / ||D|| (columns with zero norm untouched)
@@ -664,6 +718,7 @@ ModWs carve_mod_ws(void* base, int P, int64_t N, int m, int K, int cap) {
     w.cf = (int64_t*)take(sizeof(int64_t) * (P + 1));
     w.chunk_hist = (int32_t*)take(sizeof(int32_t) * nch * K);
     w.chunk_off = (int64_t*)take(sizeof(int64_t) * nch * K);
+    w.wpart = (int64_t*)take(sizeof(int64_t) * 8 * (int64_t)P * K);
     w.bucket_off = (int64_t*)take(sizeof(int64_t) * ((int64_t)P * K + 1));
     w.scan_ws = (int64_t*)take(scan_workspace_bytes((int64_t)P * K));
     w.bsig = (int32_t*)take(sizeof(int32_t) * std::max<int64_t>(N * cap, 1));
@@ -698,11 +753,11 @@ int mod_update(const ModArgs<T>& a, cudaStream_t st) {
     const unsigned hb = (unsigned)((nch_max + 7) / 8);
     k_chunk_hist<<<hb, 256, 8 * K * sizeof(int32_t), st>>>(a.off, w.cf, P, K, cap, a.idx, a.counts,
                                                           w.chunk_hist);
-    k_usage_from_chunks<<<(unsigned)((PK + 255) / 256), 256, 0, st>>>(w.cf, P, K, w.chunk_hist, a.usage);
+    const dim3 gpk((unsigned)((K + 31) / 32), (unsigned)P);
+    k_usage_from_chunks<<<gpk, 256, 0, st>>>(w.cf, P, K, w.chunk_hist, w.wpart, a.usage);
     int rc = exclusive_scan_counts(a.usage, PK, w.bucket_off, w.scan_ws, st);
     if (rc) return rc;
-    k_chunk_offsets<<<(unsigned)((PK + 255) / 256), 256, 0, st>>>(w.cf, P, K, w.chunk_hist,
-                                                                  w.bucket_off, w.chunk_off);
+    k_chunk_offsets<<<gpk, 256, 0, st>>>(w.cf, P, K, w.chunk_hist, w.wpart, w.bucket_off, w.chunk_off);
     {
         const int smem = 8 * K * (int)sizeof(int64_t);
         if (smem > 48 * 1024)
@@ -718,7 +773,7 @@ int mod_update(const ModArgs<T>& a, cudaStream_t st) {
     });
     if (rc) return rc;
     {
-        const int smem = 8 * K * (int)sizeof(double) + 8 * 32 * XXT_CAP * (4 + 8);
+        const int smem = 8 * K * (int)sizeof(double) + (cap <= XXT_CAP ? 8 * 32 * cap * (4 + 8) : 0);
         if (smem > 48 * 1024)
             cudaFuncSetAttribute(k_xxt<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         k_xxt<T><<<(unsigned)PK, 256, smem, st>>>(P, K, cap, a.idx, a.val, a.counts,
@@ -768,6 +823,7 @@ int64_t replace_ws_bytes(int P, int64_t N, int m, int K) {
     add(sizeof(double) * (int64_t)P * K * m);  // normalised copy
     add(sizeof(double) * (int64_t)P * K * K);  // |Dn^T Dn|
     add(sizeof(int8_t) * (int64_t)P * K);      // degenerate flags
+    add(sizeof(int8_t) * (int64_t)P * K);      // twin flags
     add(sizeof(int32_t) * P);                  // targets per shard
     add(sizeof(double) * std::max<int64_t>(N, 1));  // residual^2
     add(sizeof(double) * std::max<int64_t>(N, 1));  // ||y||^2
@@ -785,6 +841,7 @@ int replace_degenerate(const ReplaceArgs<T>& a, cudaStream_t st) {
     double* Dn = (double*)take(sizeof(double) * PK * m);
     double* C = (double*)take(sizeof(double) * PK * K);
     int8_t* deg = (int8_t*)take(PK);
+    int8_t* twin = (int8_t*)take(PK);
     int32_t* ntarget = (int32_t*)take(sizeof(int32_t) * P);
     double* rsq = (double*)take(sizeof(double) * std::max<int64_t>(N, 1));
     double* ysq = (double*)take(sizeof(double) * std::max<int64_t>(N, 1));
@@ -794,7 +851,8 @@ int replace_degenerate(const ReplaceArgs<T>& a, cudaStream_t st) {
     k_normalize_rows<<<(unsigned)((PK + 7) / 8), 256, 0, st>>>(PK, m, a.D, Dn);
     int rc = gram_f64(Dn, P, m, K, C, st);
     if (rc) return rc;
-    k_twins<<<P, 1024, 2 * K, st>>>(K, C, a.D, m, a.usage, deg, ntarget);
+    k_twin_flags<<<(unsigned)((PK + 7) / 8), 256, 0, st>>>(P, K, C, a.D, m, a.usage, deg, twin);
+    k_twins<<<P, 32, 0, st>>>(K, C, twin, deg, ntarget);
     // residuals with the current D and the given codes (always computed; the
     // reference skips them when no atom is degenerate, which changes nothing)
     rc = with_mpl(m, [&](auto c) {

@@ -9,6 +9,7 @@ struct ModWs {
     int64_t* cf;
     int32_t* chunk_hist;
     int64_t* chunk_off;
+    int64_t* wpart;  // per-warp chunk-range partial counts (P x 8 x K)
     int64_t* bucket_off;
     int64_t* scan_ws;
     int32_t* bsig;
