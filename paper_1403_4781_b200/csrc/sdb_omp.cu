@@ -538,7 +538,7 @@ k_omp_fast(OmpArgs<float> a) {
                 for (int k = 0; k < KPL; ++k) lm = fmaxf(lm, v[k]);
                 const uint32_t cbits = __reduce_max_sync(SDB_FULL, __float_as_uint(lm));
                 const float cmax = __uint_as_float(cbits);
-                if (cmax <= 1e-13f * rnorm) { status = 3; break; }
+                if (cmax * cmax <= 1e-26f * rsq) { status = 3; break; }  // cmax <= 1e-13 ||r||
                 int cand = 0x7fffffff;
 #pragma unroll
                 for (int k = KPL - 1; k >= 0; --k)
@@ -565,8 +565,8 @@ k_omp_fast(OmpArgs<float> a) {
                     dsq -= warp_sum(lane < n ? wme * wme : 0.0f);
                 }
                 if (dsq <= a.guard) { status = 2; break; }
-                const float ldiag = __fsqrt_rn(dsq);
-                const float inv = 1.0f / ldiag;
+                const float inv = rsqrtf(dsq);
+                const float ldiag = dsq * inv;
                 float* Lrow = Ls + n * (n + 1) / 2;
                 if (lane < n) Lrow[lane] = wme;
                 if (lane == 0) { Lrow[n] = ldiag; invd[n] = inv; ids[n] = best; }
@@ -595,7 +595,6 @@ k_omp_fast(OmpArgs<float> a) {
                 // step. Only near the threshold is the explicit residual formed, so
                 // the stopping decision is the one the explicit residual gives.
                 rsq = fmaxf(rsq - tn * tn, 0.0f);
-                rnorm = __fsqrt_rn(rsq);
                 __syncwarp();
                 if (fabsf(rsq - eps2) <= 1e-4f * ysq) {
                     rnorm = resid_norm(n);
