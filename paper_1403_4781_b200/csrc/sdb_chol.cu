@@ -15,6 +15,9 @@
 #include "sdb_internal.h"
 #include "sdb_chol.h"
 
+#include <cooperative_groups.h>
+#include <cstdlib>
+
 namespace sdb {
 
 constexpr int CB = 64;       // panel / tile width
@@ -460,6 +463,450 @@ __global__ void __launch_bounds__(256) k_sumsq(int64_t n, const double* __restri
     if (threadIdx.x == 0) out[blockIdx.x] = sh[0];
 }
 
+// =============================================================================
+// Single-launch clustered solve for K <= 4*64 (the MOD shapes of the paper's
+// split-and-merge runs). One thread-block cluster of NC = ceil(K/64) CTAs per
+// shard; CTA c keeps block row c of A (tiles (c, 0..c), 64 x 64 FP64) in its
+// shared memory for the whole solve, and the CTAs exchange panels through
+// distributed shared memory (DSMEM). Instead of cluster-wide barriers every
+// published object (T_J, L_cJ, W_J, Z_J) has a ready flag in its producer's
+// shared memory, so each CTA runs ahead as far as its own inputs allow (the
+// next CTA to factor defers its RHS update until after its factorisation):
+//   forward, J = 0..NC-1:
+//     CTA J    : factor A_JJ and form T_J = L_JJ^-1 in the same register sweep
+//                (T overwrites the tile; L_JJ itself is never needed again),
+//                W_J = T_J B_J
+//     CTA c > J: L_cJ = A_cJ T_J^T (T_J read from CTA J)
+//     CTA c > J: A_cK -= L_cJ L_KJ^T (J < K <= c, L_KJ from CTA K),
+//                B_c -= L_cJ W_J
+//   backward, J = NC-1..0:
+//     CTA J    : Z_J = T_J^T W_J
+//     CTA c < J: W_c -= L_Jc^T Z_J (L_Jc read from CTA J)
+// Unused-atom masking, the pivot tolerance and ||W||^2 are folded in; every
+// reduction runs in a fixed order (bitwise reproducible).
+// =============================================================================
+constexpr int CL_MAX = 4;
+constexpr int TILE_D = CB * CBP;
+
+// acc = X Y^T over q < nq on 64x64 smem tiles (rows padded to CBP);
+// XT: X stored transposed (Xs[q][r])
+template <bool XT>
+__device__ __forceinline__ void tile_mm(const double* __restrict__ Xs, const double* __restrict__ Ys,
+                                        int nq, double acc[4][4]) {
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    for (int q = 0; q < nq; ++q) {
+        double xv[4], yv[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) xv[a] = XT ? Xs[q * CBP + ty + 16 * a] : Xs[(ty + 16 * a) * CBP + q];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) yv[b] = Ys[(tx + 16 * b) * CBP + q];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b] = fma(xv[a], yv[b], acc[a][b]);
+    }
+}
+
+// S[col][q] = B[(row0 + q) * m + c0 + col] (q < nq, col < nc; zero padded)
+__device__ __forceinline__ void stage_rows_t(double* __restrict__ S, const double* __restrict__ B, int m,
+                                             int row0, int nq, int c0, int nc) {
+    const int col = threadIdx.x & 63, qb = threadIdx.x >> 6;  // all 16 loads in flight
+    double v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const int q = qb + 4 * k;
+        v[k] = (q < nq && col < nc) ? B[(int64_t)(row0 + q) * m + c0 + col] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) S[col * CBP + qb + 4 * k] = v[k];
+}
+
+// 64 x CBP tile copy (e.g. from a peer CTA through DSMEM): every load of the
+// thread is issued before the first store so the remote latency is paid once
+__device__ __forceinline__ void copy_tile(double* __restrict__ dst, const double* src) {
+    constexpr int N2 = TILE_D / 2, PER = (N2 + 255) / 256;
+    const double2* s2 = reinterpret_cast<const double2*>(src);
+    double2* d2 = reinterpret_cast<double2*>(dst);
+    double2 t[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        const int e = threadIdx.x + 256 * k;
+        if (e < N2) t[k] = s2[e];
+    }
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        const int e = threadIdx.x + 256 * k;
+        if (e < N2) d2[e] = t[k];
+    }
+}
+
+// factor the 64x64 tile in place into T = L^-1. Thread t owns row r = t/4
+// and the contiguous column chunk q = 16g + j (g = t%4, j < 16) of L and of T.
+// One CTA barrier per column k:
+//   publish: column k's owners publish it as a full vector (raw entries of
+//            rows >= k with every earlier rank-1 update applied, zeros above)
+//            and row k-1 of T is published (scaled by 1/L_{k-1,k-1});
+//   compute: every thread derives s_k = 1/sqrt(d_k) itself (0 for a dependent
+//            pivot or a padding row); rows r > k apply the rank-1 step
+//            v_r -= (a_rk s_k^2) a_k and rows r >= k apply
+//            T_r -= L_{r,k-1} T_{k-1} (the T sweep trails by one column).
+// Both updates are unconditional per element: they only touch entries that
+// are zero in the operand (T rows right of the diagonal, column entries above
+// the pivot) or that are never read again (already-published columns, the
+// strict upper triangle), so each is one FMA fed by 16-byte shared loads.
+// Published vectors use a stride of 18 per 16-entry chunk: 16-byte aligned
+// chunks, and the four chunk owners of a row hit distinct banks. Raw columns
+// are triple-buffered (the lagged T step still reads column k-1 while column
+// k+1 is published), T rows double-buffered. The loop over the four chunks
+// stays rolled so every register index is static in a quarter of the code.
+constexpr int FPW = 72;  // padded vector length (4 chunks x 18)
+
+__device__ __forceinline__ double inv_sqrt_f64(double d) {
+    double y = (double)rsqrtf((float)fmax(d, 1e-300));
+    y = y * fma(-0.5 * d * y, y, 1.5);
+    return y * fma(-0.5 * d * y, y, 1.5);
+}
+
+__device__ __forceinline__ void load_chunk(double (&x)[16], const double* __restrict__ src) {
+    const double2* s2 = reinterpret_cast<const double2*>(src);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const double2 t = s2[j];
+        x[2 * j] = t.x;
+        x[2 * j + 1] = t.y;
+    }
+}
+
+__device__ __forceinline__ void factor_inverse(double* __restrict__ Ts, int nr, double tl,
+                                               double* __restrict__ craw, double* __restrict__ trow,
+                                               int8_t* sdep) {
+    const int tid = threadIdx.x, r = tid >> 2, g = tid & 3;
+    const int my = 18 * g;                     // this thread's chunk in a padded vector
+    const int rp = 18 * (r >> 4) + (r & 15);   // padded index of row r
+    double v[16], tv[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const int q = 16 * g + j;
+        v[j] = (q <= r) ? Ts[r * CBP + q] : 0.0;
+        tv[j] = (q == r) ? 1.0 : 0.0;
+    }
+    double sprev = 0.0;
+    int b3 = 0, b3p = 2;  // k % 3, (k - 1) % 3
+#pragma unroll 1
+    for (int cg = 0; cg < 4; ++cg) {
+#pragma unroll
+        for (int jc = 0; jc < 16; ++jc) {
+            const int k = 16 * cg + jc;
+            double* cr = craw + b3 * FPW;
+            const double* crp = craw + b3p * FPW;
+            double* tr = trow + (jc & 1) * FPW;
+            if (g == cg) cr[rp] = (r >= k) ? v[jc] : 0.0;
+            if (k > 0 && r == k - 1) {
+                double2* t2 = reinterpret_cast<double2*>(tr + my);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    tv[2 * j] *= sprev;
+                    tv[2 * j + 1] *= sprev;
+                    t2[j] = make_double2(tv[2 * j], tv[2 * j + 1]);
+                }
+            }
+            __syncthreads();
+            const double d = cr[18 * cg + jc];
+            const bool dep = !(d > tl) || k >= nr;
+            const double sk = dep ? 0.0 : inv_sqrt_f64(d);
+            if (tid == 0) sdep[k] = dep ? 1 : 0;
+            if (r > k) {
+                const double coef = cr[rp] * (sk * sk);
+                double x[16];
+                load_chunk(x, cr + my);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[j] = fma(-coef, x[j], v[j]);
+            }
+            if (k > 0 && r >= k) {
+                const double lp = crp[rp] * sprev;
+                double x[16];
+                load_chunk(x, tr + my);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) tv[j] = fma(-lp, x[j], tv[j]);
+            }
+            sprev = sk;
+            b3p = b3;
+            b3 = (b3 == 2) ? 0 : b3 + 1;
+        }
+    }
+    if (r == CB - 1) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) tv[j] *= sprev;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) Ts[r * CBP + 16 * g + j] = tv[j];
+}
+
+// fixed-order CTA sum / max of one double per thread
+__device__ __forceinline__ double block_reduce(double x, double* red, bool is_max) {
+    red[threadIdx.x] = x;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w)
+            red[threadIdx.x] = is_max ? fmax(red[threadIdx.x], red[threadIdx.x + w])
+                                      : red[threadIdx.x] + red[threadIdx.x + w];
+        __syncthreads();
+    }
+    const double r = red[0];
+    __syncthreads();
+    return r;
+}
+
+// ready flags live in the producer's shared memory: written once per launch
+// with release semantics at cluster scope (after a CTA barrier, so the whole
+// CTA's smem / global writes are covered); consumers poll them with acquire
+// loads through the DSMEM window, then barrier.
+__device__ __forceinline__ void flag_publish(int* f) {
+    __syncthreads();
+    if (threadIdx.x == 0) asm volatile("st.release.cluster.u32 [%0], %1;" ::"l"(f), "r"(1) : "memory");
+}
+__device__ __forceinline__ void flag_wait(const int* remote) {
+    if (threadIdx.x == 0) {
+        unsigned v = 0;
+        do {
+            asm volatile("ld.acquire.cluster.u32 %0, [%1];" : "=r"(v) : "l"(remote) : "memory");
+        } while (v == 0);
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(256, 1)
+k_chol_cluster(int K, int m, double* __restrict__ Aall, double* __restrict__ Ball,
+               const int32_t* __restrict__ usage, double rel_tol, int8_t* __restrict__ depmask,
+               int32_t* __restrict__ ndep, double* __restrict__ wsq) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ double xsm[];
+    __shared__ __align__(16) double craw[3 * FPW];
+    __shared__ __align__(16) double trow[2 * FPW];
+    __shared__ double red[256];
+    __shared__ double s_part[2];  // [0] diag max, [1] ||W||^2 of this block row
+    __shared__ int8_t s_use[CL_MAX * CB];
+    __shared__ int8_t sdep[CB];
+    __shared__ int s_nd;
+    // fT: T_c ready; fW: W_c ready; fZ: Z_c ready; fL[J]: L_cJ ready
+    __shared__ int fT, fW, fZ, fL[CL_MAX];
+    const int NC = (int)cl.num_blocks();
+    const int c = (int)cl.block_rank();
+    const int p = blockIdx.x / NC;
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int r0 = c * CB, nr = min(CB, K - r0);
+    const double* A = Aall + (int64_t)p * K * K;
+    double* B = Ball + (int64_t)p * K * m;
+    const int32_t* use = usage + (int64_t)p * K;
+    double* S1 = xsm + NC * TILE_D;
+    double* S2 = S1 + TILE_D;
+    auto tile = [&](int J) { return xsm + J * TILE_D; };
+    auto nrows = [&](int J) { return min(CB, K - J * CB); };
+    double acc[4][4];
+
+    if (tid == 0) {
+        fT = fW = fZ = 0;
+        for (int J = 0; J < CL_MAX; ++J) fL[J] = 0;
+    }
+    // ---- load block row c with unused atoms masked to the identity
+    for (int q = tid; q < NC * CB; q += 256) s_use[q] = (q < K && use[q]) ? 1 : 0;
+    __syncthreads();
+    {
+        const int q = tid & 63, rb = tid >> 6;  // column q of every tile, rows rb + 4k
+        for (int J = 0; J <= c; ++J) {
+            double* T = tile(J);
+            const int gq = J * CB + q;
+            double v[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const int gr = r0 + rb + 4 * k;
+                const bool ld = s_use[gq] && gr < K && s_use[gr];
+                v[k] = ld ? A[(int64_t)gr * K + gq] : ((gr == gq) ? 1.0 : 0.0);
+            }
+#pragma unroll
+            for (int k = 0; k < 16; ++k) T[(rb + 4 * k) * CBP + q] = v[k];
+        }
+    }
+    {
+        double mx = 0.0;
+        if (tid < nr && use[r0 + tid]) mx = A[(int64_t)(r0 + tid) * K + r0 + tid];
+        mx = block_reduce(mx, red, true);
+        if (tid == 0) { s_part[0] = mx; s_part[1] = 0.0; s_nd = 0; }
+    }
+    cl.sync();  // flags initialised and diagonal maxima published everywhere
+    double dmax = 0.0;
+    for (int k = 0; k < NC; ++k) dmax = fmax(dmax, cl.map_shared_rank(s_part, k)[0]);
+    const double tl = rel_tol * dmax;
+
+    // B_c -= L_cJ W_J (W_J rows of block J, published by CTA J)
+    auto b_update = [&](int J) {
+        flag_wait(cl.map_shared_rank(&fW, J));
+        const int nJ = nrows(J);
+        for (int c0 = 0; c0 < m; c0 += CB) {
+            const int nc = min(CB, m - c0);
+            __syncthreads();
+            stage_rows_t(S1, B, m, J * CB, nJ, c0, nc);
+            __syncthreads();
+            tile_mm<false>(tile(J), S1, nJ, acc);
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const int rr = ty + 16 * a, cc = tx + 16 * b;
+                    if (rr < nr && cc < nc) B[(int64_t)(r0 + rr) * m + c0 + cc] -= acc[a][b];
+                }
+        }
+    };
+
+    // ---- forward: panels of the block columns left of the diagonal
+    bool b_pending[CL_MAX] = {false, false, false, false};
+    for (int J = 0; J < c; ++J) {
+        const int nJ = nrows(J);
+        flag_wait(cl.map_shared_rank(&fT, J));
+        copy_tile(S1, cl.map_shared_rank(tile(J), J));
+        __syncthreads();
+        tile_mm<false>(tile(J), S1, nJ, acc);  // L_cJ = A_cJ T_J^T
+        __syncthreads();
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) tile(J)[(ty + 16 * a) * CBP + tx + 16 * b] = acc[a][b];
+        flag_publish(&fL[J]);
+        // trailing tiles of this block row, next panel column first
+        for (int Kb = J + 1; Kb <= c; ++Kb) {
+            const double* Ly = tile(J);
+            if (Kb != c) {
+                flag_wait(cl.map_shared_rank(&fL[J], Kb));
+                copy_tile(S1, cl.map_shared_rank(tile(J), Kb));
+                Ly = S1;
+            }
+            __syncthreads();
+            tile_mm<false>(tile(J), Ly, nJ, acc);
+            double* T = tile(Kb);
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) T[(ty + 16 * a) * CBP + tx + 16 * b] -= acc[a][b];
+            __syncthreads();
+        }
+        // the next CTA to factor keeps the RHS update off its critical path
+        if (c > J + 1) b_update(J);
+        else b_pending[J] = true;
+    }
+    // ---- own diagonal block: T_c = L_cc^-1
+    factor_inverse(tile(c), nr, tl, craw, trow, sdep);
+    if (tid < nr) depmask[(int64_t)p * K + r0 + tid] = sdep[tid];
+    if (tid == 0) {
+        int nd = 0;
+        for (int q = 0; q < nr; ++q) nd += sdep[q];
+        s_nd = nd;
+    }
+    flag_publish(&fT);
+    for (int J = 0; J < c; ++J)
+        if (b_pending[J]) b_update(J);
+    // W_c = T_c B_c
+    double wloc = 0.0;
+    for (int c0 = 0; c0 < m; c0 += CB) {
+        const int nc = min(CB, m - c0);
+        __syncthreads();
+        stage_rows_t(S1, B, m, r0, nr, c0, nc);
+        __syncthreads();
+        tile_mm<false>(tile(c), S1, nr, acc);
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int rr = ty + 16 * a, cc = tx + 16 * b;
+                if (rr < nr && cc < nc) {
+                    B[(int64_t)(r0 + rr) * m + c0 + cc] = acc[a][b];
+                    wloc = fma(acc[a][b], acc[a][b], wloc);
+                }
+            }
+    }
+    flag_publish(&fW);
+    wloc = block_reduce(wloc, red, false);
+    if (tid == 0) s_part[1] = wloc;
+
+    // ---- backward: W_c -= L_Jc^T Z_J for J > c, then Z_c = T_c^T W_c
+    for (int J = NC - 1; J > c; --J) {
+        const int nJ = nrows(J);
+        flag_wait(cl.map_shared_rank(&fZ, J));
+        copy_tile(S2, cl.map_shared_rank(tile(c), J));  // L_Jc (rows of block J)
+        for (int c0 = 0; c0 < m; c0 += CB) {
+            const int nc = min(CB, m - c0);
+            __syncthreads();
+            stage_rows_t(S1, B, m, J * CB, nJ, c0, nc);
+            __syncthreads();
+            tile_mm<true>(S2, S1, nJ, acc);
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const int rr = ty + 16 * a, cc = tx + 16 * b;
+                    if (rr < nr && cc < nc) B[(int64_t)(r0 + rr) * m + c0 + cc] -= acc[a][b];
+                }
+        }
+    }
+    for (int c0 = 0; c0 < m; c0 += CB) {
+        const int nc = min(CB, m - c0);
+        __syncthreads();
+        stage_rows_t(S1, B, m, r0, nr, c0, nc);
+        __syncthreads();
+        tile_mm<true>(tile(c), S1, nr, acc);
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int rr = ty + 16 * a, cc = tx + 16 * b;
+                if (rr < nr && cc < nc) B[(int64_t)(r0 + rr) * m + c0 + cc] = acc[a][b];
+            }
+    }
+    flag_publish(&fZ);
+    cl.sync();
+    if (c == 0 && tid == 0) {
+        double w = 0.0;
+        int nd = 0;
+        for (int k = 0; k < NC; ++k) {
+            w += cl.map_shared_rank(s_part, k)[1];
+            nd += *cl.map_shared_rank(&s_nd, k);
+        }
+        if (wsq) wsq[p] = w;
+        ndep[p] = nd;
+    }
+    cl.sync();  // keep every CTA's shared memory alive until rank 0 has read it
+}
+
+static int chol_solve_cluster(int P, int K, int m, double* A, double* B, const int32_t* usage,
+                              double rel_tol, int8_t* depmask, int32_t* ndep, double* wsq, cudaStream_t st) {
+    const int NC = (K + CB - 1) / CB;
+    const int smem = (NC + 2) * TILE_D * (int)sizeof(double);
+    static int attr_smem = 0;
+    if (attr_smem < smem) {
+        cudaError_t e = cudaFuncSetAttribute(k_chol_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return (int)e;
+        attr_smem = smem;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(P * NC));
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)NC;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return (int)cudaLaunchKernelEx(&cfg, k_chol_cluster, K, m, A, B, usage, rel_tol, depmask, ndep, wsq);
+}
+
 int64_t chol_ws_bytes(int P, int K) {
     const int64_t nblk = (K + CB - 1) / CB;
     return (int64_t)P * nblk * CB * CB * sizeof(double) + (int64_t)P * sizeof(double) + 512;
@@ -467,6 +914,9 @@ int64_t chol_ws_bytes(int P, int K) {
 
 int chol_solve(int P, int K, int m, double* A, double* B, const int32_t* usage, double rel_tol,
                int8_t* depmask, int32_t* ndep, double* wsq, void* ws, cudaStream_t st) {
+    static const bool force_chain = getenv("SDB_CHOL_CHAIN") != nullptr;  // A/B switch for tests
+    if (K <= CL_MAX * CB && P > 0 && !force_chain)
+        return chol_solve_cluster(P, K, m, A, B, usage, rel_tol, depmask, ndep, wsq, st);
     const int64_t nblk = (K + CB - 1) / CB;
     double* T = (double*)ws;
     double* tol = T + (int64_t)P * nblk * CB * CB;
