@@ -260,7 +260,8 @@ constexpr int NWARP2 = 10;
 constexpr int RES_KB = 2;                           // resident D: up to 2 k-blocks (m <= 64)
 constexpr int RES_A_STAGE = 2 * A_BYTES;             // Y hi + lo
 constexpr int RES_B_BYTES = RES_KB * 2 * B_BYTES;    // D hi + lo, 2 k-blocks
-constexpr int SMEM2_BYTES = 2 * STAGE_BYTES + 1024 + 256 + 4 * 2 * 32 * 32 * 4;  // + TMA store staging
+// + TMA store staging (1024-aligned for the 128-byte swizzle)
+constexpr int SMEM2_BYTES = 2 * STAGE_BYTES + 1024 + 1024 + 4 * 2 * 32 * 32 * 4;
 
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
@@ -289,6 +290,19 @@ __device__ __forceinline__ Item item_of(int64_t it, const int64_t* __restrict__ 
     return r;
 }
 
+__device__ __forceinline__ void tmem_ld32(uint32_t (&v)[32], uint32_t taddr) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+        "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+          "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+          "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+          "=r"(v[31])
+        : "r"(taddr));
+}
+
 template <bool RES>
 __global__ void __launch_bounds__(NWARP2 * 32, 1)
 k_corr_tc2(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmDh,
@@ -303,8 +317,9 @@ k_corr_tc2(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUte
     uint64_t* bars = (uint64_t*)bar_base;
     // full[0..1], split[2..3], empty[4..5], tfull[6..7], tempty[8..9], bfull[10], bfree[11]
     uint32_t* tmem_slot = (uint32_t*)(bars + 12);
-    // epilogue staging for TMA stores: 4 warps x 2 buffers x 32x32 fp32
-    float* stg_base = reinterpret_cast<float*>(bar_base + 256);
+    // epilogue staging for TMA stores: 4 warps x 2 buffers x 32x32 fp32,
+    // 128-byte swizzled (row r's 16-byte chunk c at c ^ (r & 7))
+    float* stg_base = reinterpret_cast<float*>(bar_base + 1024);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t n_items = tile_start[P] * nchunk;
     const int64_t per = (n_items + gridDim.x - 1) / gridDim.x;
@@ -436,22 +451,11 @@ k_corr_tc2(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUte
             const int64_t row_base = off[I.p] + I.tile * TM + quad * 32;
             const int nrows = (int)max((int64_t)0, min((int64_t)32, s_hi - row_base));
             const int n0 = I.chunk * TN;
-#pragma unroll 1
-            for (int c = 0; c < TN; c += 32) {
-                if (n0 + c >= K) break;
-                uint32_t v[32];
-                const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * TN + c);
-                asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
-                    "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-                      "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-                      "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
-                      "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
-                      "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
-                      "=r"(v[31])
-                    : "r"(taddr));
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            const int ncols = min(TN, K - n0);
+            const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * TN);
+            // one 32x32 block: TMA store from swizzled staging (conflict-free
+            // 16-byte smem writes), or plain stores for a partial quadrant
+            auto put = [&](const uint32_t (&v)[32], int c) {
                 const int j0 = n0 + c;
                 if (nrows == 32) {
                     float* buf = stg + sb * 1024;
@@ -461,8 +465,8 @@ k_corr_tc2(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUte
                     float4* row4 = reinterpret_cast<float4*>(buf + lane * 32);
 #pragma unroll
                     for (int qq = 0; qq < 8; ++qq)
-                        row4[qq] = make_float4(__uint_as_float(v[4 * qq]), __uint_as_float(v[4 * qq + 1]),
-                                               __uint_as_float(v[4 * qq + 2]), __uint_as_float(v[4 * qq + 3]));
+                        row4[qq ^ (lane & 7)] = make_float4(__uint_as_float(v[4 * qq]), __uint_as_float(v[4 * qq + 1]),
+                                                            __uint_as_float(v[4 * qq + 2]), __uint_as_float(v[4 * qq + 3]));
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     __syncwarp();
                     if (lane == 0) {
@@ -480,6 +484,20 @@ k_corr_tc2(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUte
                     for (int qq = 0; qq < 32; ++qq)
                         if (j0 + qq < K) out[j0 + qq] = __uint_as_float(v[qq]);
                 }
+            };
+            // TMEM loads run one block ahead of the stores
+            uint32_t va[32], vb[32];
+            tmem_ld32(va, trow);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll 1
+            for (int c = 0; c < ncols; c += 64) {
+                if (c + 32 < ncols) tmem_ld32(vb, trow + (uint32_t)(c + 32));
+                put(va, c);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (c + 32 >= ncols) break;
+                if (c + 64 < ncols) tmem_ld32(va, trow + (uint32_t)(c + 64));
+                put(vb, c + 32);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
@@ -568,7 +586,7 @@ bool make_map_plain(CUtensorMap* map, const float* ptr, int64_t cols, int64_t ro
     cuuint32_t box[2] = {32, 32};
     cuuint32_t estr[2] = {1, 1};
     return g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)ptr, dims, strides, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                     CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
