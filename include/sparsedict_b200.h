@@ -78,13 +78,19 @@ int sdb_correlate(int dtype, int64_t N, int64_t m, int64_t K, int64_t P, const i
  * 1e-12 tie window and lowest-index tie-break, progressive Cholesky with the
  * singular guard `guard` (reference 1e-12), explicit residual, stop at
  * rnorm <= eps or cap atoms. Fixed sparsity: cap = s, eps = 0. K <= 1024.
- * scratch: sdb_omp_scratch_bytes() bytes (may be 0 -> pass NULL). */
+ * rnorm: optional output (NULL: residual norms not reported).
+ * ysq: optional FP32 ||y_i||^2 from sdb_signal_sq (SDB_F32 only; NULL: formed
+ * in the kernel). scratch: sdb_omp_scratch_bytes() bytes (may be 0 -> NULL). */
 int64_t sdb_omp_scratch_bytes(int dtype, int64_t N, int64_t m, int64_t cap);
 int sdb_omp(int dtype, int64_t N, int64_t m, int64_t K, int64_t P, const int64_t *shard_off,
             const void *alpha0, int64_t lda, const void *Y, int64_t ldy, const void *D,
             const void *G, int64_t cap, double eps, double guard, int32_t *idx, void *val,
-            int32_t *counts, int8_t *status, void *rnorm, void *scratch, int64_t scratch_bytes,
-            void *stream);
+            int32_t *counts, int8_t *status, void *rnorm, const float *ysq, void *scratch,
+            int64_t scratch_bytes, void *stream);
+/* ||y_i||^2 per signal (FP32, N floats) with the exact arithmetic of the
+ * FP32 OMP kernel: passing it as sdb_omp's ysq gives bitwise the same codes
+ * and lets the kernel skip loading y except near the eps threshold. */
+int sdb_signal_sq(int64_t N, int64_t m, const float *Y, int64_t ldy, float *out, void *stream);
 
 /* CSC packing (sparse_coding.py:294-303), in two stream-ordered phases:
  * indptr (N+1 int64) from counts, then indices (int64, ascending per column)

@@ -195,9 +195,13 @@ def alpha_chunk_rows(K: int, prec: str) -> int:
 
 
 def code(Ydev: torch.Tensor, off: torch.Tensor, max_rows: int, DT: torch.Tensor, G: torch.Tensor,
-         cap: int, eps: float, prec: str, use_tc: bool = True, out: DeviceCodes | None = None
-         ) -> DeviceCodes:
-    """OMP over every row of Ydev; row i uses the dictionary of its shard."""
+         cap: int, eps: float, prec: str, use_tc: bool = True, out: DeviceCodes | None = None,
+         ysq: torch.Tensor | None = None, want_rnorm: bool = True) -> DeviceCodes:
+    """OMP over every row of Ydev; row i uses the dictionary of its shard.
+
+    ysq: optional per-signal FP32 ||y||^2 from signal_sq (fp32 only; the
+    codes are bitwise the same with or without it). want_rnorm=False leaves
+    out.rnorm unwritten (the training loop never reads it)."""
     N, m = Ydev.shape
     P, K, _ = DT.shape
     dt = sdb_dtype(prec)
@@ -220,8 +224,18 @@ def code(Ydev: torch.Tensor, off: torch.Tensor, max_rows: int, DT: torch.Tensor,
     timed_call("omp", N * (K * es + m * es + cap * (4 + es) + 5 + es), 0.0,
                "sdb_omp", dt, N, m, K, P, ptr(off), ptr(alpha), K, ptr(Ydev), m, ptr(DT), ptr(G),
                cap, float(eps), GUARD[prec], ptr(out.idx), ptr(out.val), ptr(out.counts),
-               ptr(out.status), ptr(out.rnorm), ptr(scratch), int(sb), stream())
+               ptr(out.status), ptr(out.rnorm) if want_rnorm else None,
+               ptr(ysq) if (ysq is not None and prec == "fp32") else None, ptr(scratch), int(sb),
+               stream())
     return out
+
+
+def signal_sq(Ydev: torch.Tensor) -> torch.Tensor:
+    """Per-signal FP32 ||y||^2 with the fast OMP kernel's own arithmetic."""
+    N, m = Ydev.shape
+    out = empty((max(N, 1),), torch.float32)
+    _lib.call("sdb_signal_sq", N, m, ptr(Ydev), Ydev.stride(0), ptr(out), stream())
+    return out[:N]
 
 
 def code_single_dict(Ydev, D64, cap, eps, prec, use_tc=True) -> DeviceCodes:
@@ -295,6 +309,16 @@ class ShardSet:
         return int(max(self.sizes)) if self.sizes else 0
 
     _ysq: torch.Tensor | None = None
+    _sig_sq: torch.Tensor | None = None
+
+    def signal_sq(self) -> torch.Tensor | None:
+        """Per-signal FP32 ||y||^2 for the fast OMP path (computed once; None
+        in fp64 mode)."""
+        if self.prec != "fp32":
+            return None
+        if self._sig_sq is None:
+            self._sig_sq = signal_sq(self.Y)
+        return self._sig_sq
 
     def energy(self) -> torch.Tensor:
         """||Y_p||_F^2 per shard (computed once, reused by every MOD step)."""

@@ -55,7 +55,7 @@ __global__ void k_cast(int64_t n, const double* __restrict__ src, T* __restrict_
 
 extern "C" {
 
-int sdb_abi_version(void) { return 1; }
+int sdb_abi_version(void) { return 2; }
 const char* sdb_last_error(void) { return g_err.c_str(); }
 
 int sdb_device_cc(void) {
@@ -136,8 +136,8 @@ int64_t sdb_omp_scratch_bytes(int dtype, int64_t N, int64_t m, int64_t cap) {
 int sdb_omp(int dtype, int64_t N, int64_t m, int64_t K, int64_t P, const int64_t* shard_off,
             const void* alpha0, int64_t lda, const void* Y, int64_t ldy, const void* D,
             const void* G, int64_t cap, double eps, double guard, int32_t* idx, void* val,
-            int32_t* counts, int8_t* status, void* rnorm, void* scratch, int64_t scratch_bytes,
-            void* stream) {
+            int32_t* counts, int8_t* status, void* rnorm, const float* ysq, void* scratch,
+            int64_t scratch_bytes, void* stream) {
     if (!dtype_ok(dtype) || N < 0 || m < 1 || K < 1 || P < 1 || cap < 1 || ldy < m || lda < K)
         return fail(SDB_EINVAL, "sdb_omp: bad args");
     if (K > 1024) return fail(SDB_EINVAL, "sdb_omp: K=%lld > 1024 not supported", (long long)K);
@@ -169,9 +169,16 @@ int sdb_omp(int dtype, int64_t N, int64_t m, int64_t K, int64_t P, const int64_t
         a.eps = (float)eps; a.guard = (float)guard;
         a.alpha0 = (const float*)alpha0; a.Y = (const float*)Y; a.D = (const float*)D;
         a.G = (const float*)G; a.val = (float*)val; a.rnorm = (float*)rnorm;
+        a.ysq = ysq;
         rc = sdb::launch_omp<float>(a, S(stream));
     }
     return cuda_rc(rc, "sdb_omp");
+}
+
+int sdb_signal_sq(int64_t N, int64_t m, const float* Y, int64_t ldy, float* out, void* stream) {
+    if (N < 0 || m < 1 || m > 256 || ldy < m || (N > 0 && (Y == nullptr || out == nullptr)))
+        return fail(SDB_EINVAL, "sdb_signal_sq: bad args");
+    return cuda_rc(sdb::signal_sq_f32(N, (int)m, Y, ldy, out, S(stream)), "sdb_signal_sq");
 }
 
 int64_t sdb_csc_workspace_bytes(int64_t N) { return sdb::scan_workspace_bytes(N < 1 ? 1 : N); }

@@ -24,13 +24,15 @@ struct OmpArgs {
     T* val;                    // N x cap
     int32_t* counts;
     int8_t* status;
-    T* rnorm;
+    T* rnorm;                  // optional (nullptr: not requested)
+    const float* ysq;          // optional precomputed ||y||^2 (fast FP32 path only)
     unsigned char* gscratch;   // optional per-warp scratch in global memory
     int64_t gscratch_warps;
     int64_t warp_bytes;
 };
 
 int gram_f64(const double* D, int P, int64_t m, int64_t K, double* G, cudaStream_t st);
+int signal_sq_f32(int64_t N, int m, const float* Y, int64_t ldy, float* out, cudaStream_t st);
 int gram_f32(const double* D, int P, int64_t m, int64_t K, float* G, cudaStream_t st);
 int correlate_simt_f64(const double* Y, int64_t ldy, const int64_t* off, int64_t max_rows, int P,
                        const double* D, int64_t m, int64_t K, double* alpha, int64_t lda,

@@ -355,7 +355,7 @@ k_omp(OmpArgs<T> a) {
         if (lane == 0) {
             a.counts[i] = n;
             a.status[i] = (int8_t)status;
-            a.rnorm[i] = rnorm;
+            if (a.rnorm) a.rnorm[i] = rnorm;
         }
         __syncwarp();
     }
@@ -384,6 +384,41 @@ constexpr int FAST_TRI = FAST_CAP * (FAST_CAP + 1) / 2;
 
 __host__ __device__ inline int fast_warp_floats(int cap, int m) {
     return FAST_TRI + 4 * FAST_CAP;  // L, 1/diag, tmp, x, ids(as int)
+}
+
+// ||y||^2 in FP32 exactly as the fast OMP kernel forms it (lane owns rows
+// lane + 32q, fmaf over q, xor-butterfly warp sum), so a precomputed value is
+// bitwise the in-kernel one
+template <int MPL>
+__device__ __forceinline__ float signal_sq(const float* __restrict__ yrow, int lane, int m) {
+    float s = 0.0f;
+#pragma unroll
+    for (int q = 0; q < MPL; ++q) {
+        const float v = (32 * q + lane < m) ? __ldg(yrow + 32 * q) : 0.0f;
+        s = fmaf(v, v, s);
+    }
+    return warp_sum(s);
+}
+
+template <int MPL>
+__global__ void __launch_bounds__(256) k_signal_sq(int64_t N, int m, const float* __restrict__ Y, int64_t ldy,
+                                                   float* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (i >= N) return;
+    const float s = signal_sq<MPL>(Y + i * ldy + lane, lane, m);
+    if (lane == 0) out[i] = s;
+}
+
+int signal_sq_f32(int64_t N, int m, const float* Y, int64_t ldy, float* out, cudaStream_t st) {
+    if (N <= 0) return 0;
+    const unsigned g = (unsigned)((N + 7) / 8);
+    const int mpl = (m + 31) / 32;
+    if (mpl <= 1) k_signal_sq<1><<<g, 256, 0, st>>>(N, m, Y, ldy, out);
+    else if (mpl <= 2) k_signal_sq<2><<<g, 256, 0, st>>>(N, m, Y, ldy, out);
+    else if (mpl <= 5) k_signal_sq<5><<<g, 256, 0, st>>>(N, m, Y, ldy, out);
+    else k_signal_sq<8><<<g, 256, 0, st>>>(N, m, Y, ldy, out);
+    return (int)cudaGetLastError();
 }
 
 // lane owns the KPL consecutive atoms [lane*KPL, lane*KPL + KPL): rows of
@@ -456,10 +491,12 @@ k_omp_fast(OmpArgs<float> a) {
         if constexpr (KPL > 8) {
             if (j0 + 8 < K) asm volatile("prefetch.global.L1 [%0];" ::"l"(an + j0 + 8));
         }
+        if (!a.ysq) {
 #pragma unroll
-        for (int q = 0; q < MPL; ++q)
-            if (32 * q + lane < m && (lane & 7) == 0)
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(yrow_n + a.ldy + 32 * q));
+            for (int q = 0; q < MPL; ++q)
+                if (32 * q + lane < m && (lane & 7) == 0)
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(yrow_n + a.ldy + 32 * q));
+        }
     };
     // atoms this lane owns that exist (K not a multiple of 32*KPL)
     const int nvalid = max(0, min(KPL, K - j0));
@@ -474,10 +511,9 @@ k_omp_fast(OmpArgs<float> a) {
         }
         // c0 doubles as the selection mask: a selected (or absent) atom's entry
         // is NaN, which fmaxf skips and whose bits never equal the maximum
-        float c0[KPL], y[MPL];
+        float c0[KPL];
         load_row<KPL>(c0, arow_n, lane, K, vec_a);
-#pragma unroll
-        for (int q = 0; q < MPL; ++q) y[q] = (32 * q + lane < m) ? __ldg(yrow_n + 32 * q) : 0.0f;
+        const float* __restrict__ yrow = yrow_n;
         if (!all_valid) {
 #pragma unroll
             for (int k = 0; k < KPL; ++k) c0[k] = (k < nvalid) ? c0[k] : kNaN;
@@ -487,10 +523,14 @@ k_omp_fast(OmpArgs<float> a) {
         arow_n += a.lda;
         yrow_n += a.ldy;
 
-        float ysq = 0.0f;
-#pragma unroll
-        for (int q = 0; q < MPL; ++q) ysq = fmaf(y[q], y[q], ysq);
-        ysq = warp_sum(ysq);
+        // ||y||^2: precomputed (same arithmetic, sdb_signal_sq) or formed here;
+        // y itself is only loaded when an explicit residual is needed
+        float ysq;
+        if (a.ysq) {
+            ysq = __ldg(a.ysq + i);
+        } else {
+            ysq = signal_sq<MPL>(yrow, lane, m);
+        }
         float rnorm = __fsqrt_rn(ysq);
         float rsq = ysq;
         int n = 0, status = 0;
@@ -499,7 +539,7 @@ k_omp_fast(OmpArgs<float> a) {
             __syncwarp();
             float rr[MPL];
 #pragma unroll
-            for (int q = 0; q < MPL; ++q) rr[q] = y[q];
+            for (int q = 0; q < MPL; ++q) rr[q] = (32 * q + lane < m) ? __ldg(yrow + 32 * q) : 0.0f;
 #pragma unroll 4
             for (int t = 0; t < nn; ++t) {
                 const float xt = xs[t];
@@ -603,8 +643,8 @@ k_omp_fast(OmpArgs<float> a) {
                     break;
                 }
             }
-            // reported norm: explicit residual of the final support
-            if (n > 0) rnorm = resid_norm(n);
+            // reported norm (when requested): explicit residual of the final support
+            if (a.rnorm && n > 0) rnorm = resid_norm(n);
         }
         __syncwarp();
         if (lane < cap) {
@@ -614,7 +654,7 @@ k_omp_fast(OmpArgs<float> a) {
         if (lane == 0) {
             a.counts[i] = n;
             a.status[i] = (int8_t)status;
-            a.rnorm[i] = rnorm;
+            if (a.rnorm) a.rnorm[i] = rnorm;
         }
         __syncwarp();
     }

@@ -210,7 +210,7 @@ def _iteration(S: E.ShardSet, D: torch.Tensor, cap: int, eps: float, use_tc: boo
     Returns (new D, residual_fro per shard)."""
     prec = S.prec
     codes = E.code(S.Y, S.off, S.max_rows, E.working_dict(D, prec), E.gram(D, prec), cap, eps,
-                   prec, use_tc)
+                   prec, use_tc, ysq=S.signal_sq(), want_rnorm=False)
     r = E.mod_update(S, codes, D)
     E.replace_degenerate(S, codes, r.D, r.usage)
     return r.D, r.resid
@@ -254,7 +254,7 @@ def train_device(S: E.ShardSet, D0: torch.Tensor, cap: int, eps: float, iteratio
                 D, rr = _iteration(S, D, cap, eps, use_tc)
                 resid[it].copy_(rr)
     codes = E.code(S.Y, S.off, S.max_rows, E.working_dict(D, prec), E.gram(D, prec), cap, eps,
-                   prec, use_tc)
+                   prec, use_tc, ysq=S.signal_sq(), want_rnorm=False)
     return D, codes, resid
 
 

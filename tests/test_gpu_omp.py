@@ -82,3 +82,30 @@ def test_omp_fp32_tolerance(name):
     assert same >= 0.999
     rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
     assert rel <= 1e-4
+
+
+@pytest.mark.parametrize("eps_scale", [0.0, 0.3, 0.9])
+def test_omp_fp32_precomputed_ysq_is_bitwise_identical(eps_scale):
+    """The training path passes sdb_signal_sq's ||y||^2 and requests no
+    residual norms: the codes must equal the default call bit for bit."""
+    import torch
+    from paper_1403_4781_b200 import _engine as E
+    rng = np.random.default_rng(7)
+    m, K, N, cap = 64, 256, 5000, 16
+    D = rng.standard_normal((m, K)); D /= np.linalg.norm(D, axis=0)
+    X = np.zeros((K, N))
+    for i in range(N):
+        X[rng.choice(K, 6, replace=False), i] = rng.standard_normal(6)
+    Y = D @ X + 0.05 * rng.standard_normal((m, N))
+    eps = eps_scale * float(np.median(np.linalg.norm(Y, axis=0)))
+    Ydev, _ = E.ingest_signals(Y, "fp32")
+    ysq = E.signal_sq(Ydev)
+    ref = (Ydev.float() ** 2).sum(1)
+    assert torch.allclose(ysq, ref, rtol=1e-5)
+    D64 = E.dict_to_device(D)
+    off, mx = E.shard_offsets([N])
+    DT, G = E.working_dict(D64, "fp32"), E.gram(D64, "fp32")
+    a = E.code(Ydev, off, mx, DT, G, cap, eps, "fp32")
+    b = E.code(Ydev, off, mx, DT, G, cap, eps, "fp32", ysq=ysq, want_rnorm=False)
+    for f in ("idx", "val", "counts", "status"):
+        assert torch.equal(getattr(a, f), getattr(b, f)), f
