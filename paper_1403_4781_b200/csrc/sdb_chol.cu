@@ -544,9 +544,11 @@ __device__ __forceinline__ void copy_tile(double* __restrict__ dst, const double
     }
 }
 
-// factor the 64x64 tile in place into T = L^-1. Thread t owns row r = t/4
-// and the contiguous column chunk q = 16g + j (g = t%4, j < 16) of L and of T.
-// One CTA barrier per column k:
+// factor the 64x64 tile in place into T = L^-1. 2-D register blocking:
+// thread (tr, tc) = (t / 16, t % 16) owns rows tr + 16a and the contiguous
+// columns 4tc + b (a, b < 4) of L and of T, so every vector entry it loads
+// serves four rows (shared-memory wavefronts, not FP64 issue, bound the
+// 1-D layout). One CTA barrier per column k:
 //   publish: column k's owners publish it as a full vector (raw entries of
 //            rows >= k with every earlier rank-1 update applied, zeros above)
 //            and row k-1 of T is published (scaled by 1/L_{k-1,k-1});
@@ -557,13 +559,15 @@ __device__ __forceinline__ void copy_tile(double* __restrict__ dst, const double
 // Both updates are unconditional per element: they only touch entries that
 // are zero in the operand (T rows right of the diagonal, column entries above
 // the pivot) or that are never read again (already-published columns, the
-// strict upper triangle), so each is one FMA fed by 16-byte shared loads.
-// Published vectors use a stride of 18 per 16-entry chunk: 16-byte aligned
-// chunks, and the four chunk owners of a row hit distinct banks. Raw columns
-// are triple-buffered (the lagged T step still reads column k-1 while column
-// k+1 is published), T rows double-buffered. The loop over the four chunks
-// stays rolled so every register index is static in a quarter of the code.
+// strict upper triangle); row k-1 is the one row excluded from the T step.
+// Published vectors use a stride of 18 per 16-entry chunk (16-byte aligned
+// 4-column groups, conflict-free). Raw columns are triple-buffered (the
+// lagged T step still reads column k-1 while column k+1 is published), T rows
+// double-buffered. The loop over column quads stays rolled (static register
+// indices, small code).
 constexpr int FPW = 72;  // padded vector length (4 chunks x 18)
+
+__device__ __forceinline__ int fpad(int q) { return 18 * (q >> 4) + (q & 15); }
 
 __device__ __forceinline__ double inv_sqrt_f64(double d) {
     double y = (double)rsqrtf((float)fmax(d, 1e-300));
@@ -571,80 +575,93 @@ __device__ __forceinline__ double inv_sqrt_f64(double d) {
     return y * fma(-0.5 * d * y, y, 1.5);
 }
 
-__device__ __forceinline__ void load_chunk(double (&x)[16], const double* __restrict__ src) {
-    const double2* s2 = reinterpret_cast<const double2*>(src);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const double2 t = s2[j];
-        x[2 * j] = t.x;
-        x[2 * j + 1] = t.y;
-    }
+__device__ __forceinline__ void load4(double (&x)[4], const double* __restrict__ src) {
+    const double2 a = reinterpret_cast<const double2*>(src)[0];
+    const double2 b = reinterpret_cast<const double2*>(src)[1];
+    x[0] = a.x; x[1] = a.y; x[2] = b.x; x[3] = b.y;
 }
 
-__device__ __forceinline__ void factor_inverse(double* __restrict__ Ts, int nr, double tl,
-                                               double* __restrict__ craw, double* __restrict__ trow,
+// (no __restrict__ on the shared buffers: other threads write them between
+// barriers, and a restrict-qualified pointer lets the compiler reuse a load of
+// the same address from an earlier phase across __syncthreads)
+__device__ __forceinline__ void factor_inverse(double* Ts, int nr, double tl, double* craw, double* trow,
                                                int8_t* sdep) {
-    const int tid = threadIdx.x, r = tid >> 2, g = tid & 3;
-    const int my = 18 * g;                     // this thread's chunk in a padded vector
-    const int rp = 18 * (r >> 4) + (r & 15);   // padded index of row r
-    double v[16], tv[16];
+    const int tid = threadIdx.x, tr = tid >> 4, tc = tid & 15;
+    const int colp = fpad(4 * tc);  // padded index of this thread's first column
+    double v[4][4], tv[4][4];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-        const int q = 16 * g + j;
-        v[j] = (q <= r) ? Ts[r * CBP + q] : 0.0;
-        tv[j] = (q == r) ? 1.0 : 0.0;
-    }
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int r = tr + 16 * a, q = 4 * tc + b;
+            v[a][b] = (q <= r) ? Ts[r * CBP + q] : 0.0;
+            tv[a][b] = (q == r) ? 1.0 : 0.0;
+        }
     double sprev = 0.0;
     int b3 = 0, b3p = 2;  // k % 3, (k - 1) % 3
 #pragma unroll 1
-    for (int cg = 0; cg < 4; ++cg) {
+    for (int cq = 0; cq < 16; ++cq) {
 #pragma unroll
-        for (int jc = 0; jc < 16; ++jc) {
-            const int k = 16 * cg + jc;
+        for (int b = 0; b < 4; ++b) {
+            const int k = 4 * cq + b;
             double* cr = craw + b3 * FPW;
             const double* crp = craw + b3p * FPW;
-            double* tr = trow + (jc & 1) * FPW;
-            if (g == cg) cr[rp] = (r >= k) ? v[jc] : 0.0;
-            if (k > 0 && r == k - 1) {
-                double2* t2 = reinterpret_cast<double2*>(tr + my);
+            double* tw = trow + (b & 1) * FPW;
+            if (tc == cq) {
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    tv[2 * j] *= sprev;
-                    tv[2 * j + 1] *= sprev;
-                    t2[j] = make_double2(tv[2 * j], tv[2 * j + 1]);
-                }
+                for (int a = 0; a < 4; ++a) cr[18 * a + tr] = (tr + 16 * a >= k) ? v[a][b] : 0.0;
+            }
+            if (k > 0 && tr == ((k - 1) & 15)) {
+                const int as = (k - 1) >> 4;
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+                    if (a == as) {
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) tv[a][c] *= sprev;
+                        reinterpret_cast<double2*>(tw + colp)[0] = make_double2(tv[a][0], tv[a][1]);
+                        reinterpret_cast<double2*>(tw + colp)[1] = make_double2(tv[a][2], tv[a][3]);
+                    }
             }
             __syncthreads();
-            const double d = cr[18 * cg + jc];
+            const double d = cr[fpad(k)];
             const bool dep = !(d > tl) || k >= nr;
             const double sk = dep ? 0.0 : inv_sqrt_f64(d);
             if (tid == 0) sdep[k] = dep ? 1 : 0;
-            if (r > k) {
-                const double coef = cr[rp] * (sk * sk);
-                double x[16];
-                load_chunk(x, cr + my);
+            {
+                const double s2 = sk * sk;
+                double x[4];
+                load4(x, cr + colp);
 #pragma unroll
-                for (int j = 0; j < 16; ++j) v[j] = fma(-coef, x[j], v[j]);
+                for (int a = 0; a < 4; ++a) {
+                    const double coef = cr[18 * a + tr] * s2;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) v[a][c] = fma(-coef, x[c], v[a][c]);
+                }
             }
-            if (k > 0 && r >= k) {
-                const double lp = crp[rp] * sprev;
-                double x[16];
-                load_chunk(x, tr + my);
+            if (k > 0) {
+                double x[4];
+                load4(x, tw + colp);
 #pragma unroll
-                for (int j = 0; j < 16; ++j) tv[j] = fma(-lp, x[j], tv[j]);
+                for (int a = 0; a < 4; ++a) {
+                    const double lp = (tr + 16 * a == k - 1) ? 0.0 : crp[18 * a + tr] * sprev;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) tv[a][c] = fma(-lp, x[c], tv[a][c]);
+                }
             }
             sprev = sk;
             b3p = b3;
             b3 = (b3 == 2) ? 0 : b3 + 1;
         }
     }
-    if (r == CB - 1) {
+    if (tr == 15) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) tv[j] *= sprev;
+        for (int c = 0; c < 4; ++c) tv[3][c] *= sprev;
     }
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < 16; ++j) Ts[r * CBP + 16 * g + j] = tv[j];
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) Ts[(tr + 16 * a) * CBP + 4 * tc + b] = tv[a][b];
 }
 
 // fixed-order CTA sum / max of one double per thread
