@@ -276,10 +276,11 @@ def main():
         roof = {"kernel": kname, "bound": "hbm", "achieved": d["GBps"], "peak": hbm, "unit": "GB/s",
                 "frac": d["GBps"] / hbm, "traffic": ncu.get(kname), "peak_source": peak_src,
                 "share_of_step": d["ms_per_step"] / ms,
-                "algorithmic_bytes_per_signal": (4 * cfg["K1"] + 4 * m + 8 * cap + 9) if dom == "omp"
+                # omp: alpha0 row + ||y||^2 + code row (idx+val, cap wide) + count + status
+                "algorithmic_bytes_per_signal": (4 * cfg["K1"] + 4 + 8 * cap + 5) if dom == "omp"
                 else 4 * (m + cfg["K1"]),
                 "traffic_note": "ncu dram read+write of one C2 local-pass launch (2,040,200 signals), "
-                                "profiles/ncu_*_r01_raw.txt"}
+                                "profiles/ncu_*_r01b_raw.txt"}
     gemm = None
     if "correlate" in kt:
         evs = kt["correlate"]

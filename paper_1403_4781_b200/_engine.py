@@ -220,8 +220,10 @@ def code(Ydev: torch.Tensor, off: torch.Tensor, max_rows: int, DT: torch.Tensor,
                ptr(alpha), K, int(use_tc), ptr(cws), int(cwb), stream())
     sb = _lib.load().sdb_omp_scratch_bytes(dt, N, m, cap)
     scratch = empty((max(sb, 1),), torch.uint8) if sb > 0 else None
-    # algorithmic HBM bytes per signal: alpha0 row + y + code row (idx+val) + count/status/rnorm
-    timed_call("omp", N * (K * es + m * es + cap * (4 + es) + 5 + es), 0.0,
+    # algorithmic HBM bytes per signal: alpha0 row + code row (idx+val) + count/status, plus
+    # either ||y||^2 (precomputed) or y, plus rnorm when requested
+    yb = 4 if (ysq is not None and prec == "fp32") else m * es
+    timed_call("omp", N * (K * es + yb + cap * (4 + es) + 5 + (es if want_rnorm else 0)), 0.0,
                "sdb_omp", dt, N, m, K, P, ptr(off), ptr(alpha), K, ptr(Ydev), m, ptr(DT), ptr(G),
                cap, float(eps), GUARD[prec], ptr(out.idx), ptr(out.val), ptr(out.counts),
                ptr(out.status), ptr(out.rnorm) if want_rnorm else None,
