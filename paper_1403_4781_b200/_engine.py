@@ -232,10 +232,11 @@ def code(Ydev: torch.Tensor, off: torch.Tensor, max_rows: int, DT: torch.Tensor,
     return out
 
 
-def signal_sq(Ydev: torch.Tensor) -> torch.Tensor:
+def signal_sq(Ydev: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
     """Per-signal FP32 ||y||^2 with the fast OMP kernel's own arithmetic."""
     N, m = Ydev.shape
-    out = empty((max(N, 1),), torch.float32)
+    if out is None:
+        out = empty((max(N, 1),), torch.float32)
     _lib.call("sdb_signal_sq", N, m, ptr(Ydev), Ydev.stride(0), ptr(out), stream())
     return out[:N]
 
@@ -325,12 +326,23 @@ class ShardSet:
     def energy(self) -> torch.Tensor:
         """||Y_p||_F^2 per shard (computed once, reused by every MOD step)."""
         if self._ysq is None:
-            tmp = empty((max(self.N, 1),), torch.float64)
-            out = empty((self.P,), torch.float64)
-            _lib.call("sdb_shard_energy", sdb_dtype(self.prec), self.P, self.N, self.m,
-                      ptr(self.off), ptr(self.Y), self.m, ptr(tmp), ptr(out), stream())
-            self._ysq = out
+            self._ysq = empty((self.P,), torch.float64)
+            self._energy_into(self._ysq)
         return self._ysq
+
+    def _energy_into(self, out: torch.Tensor):
+        tmp = empty((max(self.N, 1),), torch.float64)
+        _lib.call("sdb_shard_energy", sdb_dtype(self.prec), self.P, self.N, self.m,
+                  ptr(self.off), ptr(self.Y), self.m, ptr(tmp), ptr(out), stream())
+
+    def refresh(self):
+        """Recompute the cached per-signal / per-shard quantities in place
+        after Y was overwritten (their storage is kept: captured graphs
+        hold these addresses)."""
+        if self._sig_sq is not None:
+            signal_sq(self.Y, out=self._sig_sq)
+        if self._ysq is not None:
+            self._energy_into(self._ysq)
 
     @classmethod
     def single(cls, Y: torch.Tensor, prec: str) -> "ShardSet":
