@@ -210,6 +210,16 @@ int sdb_reconstruct_dense(int64_t H, int64_t W, int64_t p, int64_t s, const doub
  * and increment split in hi/lo words, has_uint32, uinteger). out: n int64. */
 int sdb_pcg64_permutation(int64_t n, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
                           uint64_t inc_lo, int has_uint32, uint32_t uinteger, int64_t *out);
+/* The same permutation split between host and device (n >= 2, n - 1 < 2^32,
+ * has_uint32 = 0): the host parses the PCG64 stream into the Fisher-Yates
+ * swap targets (js: n - 1 uint32, step k swaps n-1-k and js[k]; host-only,
+ * js may be pinned memory), and the device resolves the swaps in parallel,
+ * exactly (perm: n int64 device, ws: sdb_permutation_workspace_bytes). */
+int sdb_pcg64_swap_targets(int64_t n, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                           uint64_t inc_lo, uint32_t *js);
+int64_t sdb_permutation_workspace_bytes(int64_t n);
+int sdb_permutation_from_targets(int64_t n, const uint32_t *js, int64_t *perm, void *ws,
+                                 int64_t ws_bytes, void *stream);
 
 #ifdef __cplusplus
 }

@@ -173,10 +173,28 @@ class DeviceCodes:
 _pinned_perm: torch.Tensor | None = None
 
 
+_pinned_js: torch.Tensor | None = None
+
+
 def split_permutation(N: int, seed) -> torch.Tensor:
-    """Device int64 copy of numpy.random.default_rng(seed).permutation(N)
-    (bit-identical, native host routine) via a reusable pinned buffer."""
-    global _pinned_perm
+    """Device int64 numpy.random.default_rng(seed).permutation(N), bit-identical.
+
+    The host parses the PCG64 stream into the Fisher-Yates swap targets
+    (native, multi-threaded, streamed into a pinned buffer); the device
+    resolves the swaps in parallel (sdb_permutation_from_targets). Falls back
+    to the all-host routine when the 32-bit draw path does not apply."""
+    global _pinned_perm, _pinned_js
+    if 2 <= N <= 0x7fffffff:
+        if _pinned_js is None or _pinned_js.numel() < N - 1:
+            _pinned_js = torch.empty((N - 1,), dtype=torch.int32, pin_memory=True)
+        host = _pinned_js[:N - 1]
+        if _lib.swap_targets(N, seed, host.numpy()):
+            js = host.to(device(), non_blocking=True)
+            wsb = _lib.load().sdb_permutation_workspace_bytes(N)
+            ws = empty((wsb,), torch.uint8)
+            perm = empty((N,), torch.int64)
+            _lib.call("sdb_permutation_from_targets", N, ptr(js), ptr(perm), ptr(ws), wsb, stream())
+            return perm
     if _pinned_perm is None or _pinned_perm.numel() < N:
         _pinned_perm = torch.empty((max(N, 1),), dtype=torch.int64, pin_memory=True)
     host = _pinned_perm[:N]

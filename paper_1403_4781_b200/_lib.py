@@ -62,6 +62,10 @@ SIGNATURES = {
     "sdb_reconstruct": (c_int, [c_int, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp,
                                 c_dbl, c_dbl, c_vp, c_vp]),
     "sdb_reconstruct_dense": (c_int, [c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
+    "sdb_pcg64_swap_targets": (c_int, [c_i64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                       ctypes.c_uint64, c_vp]),
+    "sdb_permutation_workspace_bytes": (c_i64, [c_i64]),
+    "sdb_permutation_from_targets": (c_int, [c_i64, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "sdb_pcg64_permutation": (c_int, [c_i64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                       ctypes.c_uint64, c_int, ctypes.c_uint32, c_vp]),
 }
@@ -116,6 +120,21 @@ def permutation(n: int, seed, out=None):
                                        int(st["has_uint32"]), int(st["uinteger"]),
                                        arr.ctypes.data if n else None), "sdb_pcg64_permutation")
     return arr
+
+
+def swap_targets(n: int, seed, out):
+    """Fisher-Yates swap targets of numpy.random.default_rng(seed).permutation(n)
+    into ``out`` (n - 1 uint32, e.g. a pinned tensor's numpy view). Returns
+    False when the 32-bit fast path does not apply (caller falls back)."""
+    import numpy as np
+    st = np.random.default_rng(seed).bit_generator.state
+    if n < 2 or n - 1 > 0xffffffff or int(st["has_uint32"]):
+        return False
+    s, inc = st["state"]["state"], st["state"]["inc"]
+    M = (1 << 64) - 1
+    check(load().sdb_pcg64_swap_targets(n, s >> 64, s & M, inc >> 64, inc & M, out.ctypes.data),
+          "sdb_pcg64_swap_targets")
+    return True
 
 
 def call(name: str, *args) -> int:

@@ -181,6 +181,15 @@ int sdb_signal_sq(int64_t N, int64_t m, const float* Y, int64_t ldy, float* out,
     return cuda_rc(sdb::signal_sq_f32(N, (int)m, Y, ldy, out, S(stream)), "sdb_signal_sq");
 }
 
+int64_t sdb_permutation_workspace_bytes(int64_t n) { return n < 1 ? 256 : sdb::perm_ws_bytes(n); }
+
+int sdb_permutation_from_targets(int64_t n, const uint32_t* js, int64_t* perm, void* ws, int64_t ws_bytes,
+                                 void* stream) {
+    if (n < 1 || n - 1 > 0x7fffffffll || perm == nullptr || (n > 1 && (js == nullptr || ws == nullptr)))
+        return fail(SDB_EINVAL, "sdb_permutation_from_targets: bad args");
+    return cuda_rc(sdb::perm_from_targets(n, js, perm, ws, ws_bytes, S(stream)), "sdb_permutation_from_targets");
+}
+
 int64_t sdb_csc_workspace_bytes(int64_t N) { return sdb::scan_workspace_bytes(N < 1 ? 1 : N); }
 
 int sdb_csc_indptr(int64_t N, const int32_t* counts, int64_t* indptr, void* ws, void* stream) {

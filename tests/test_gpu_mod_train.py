@@ -187,3 +187,12 @@ def test_denoise_fp32_psnr():
                             precision="fp32").pixels
     ref = O.denoise(noisy, DN["dct8"], 20.0)
     assert abs(O.psnr(clean, out) - O.psnr(clean, ref)) <= 0.05
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 17, 1025, 65537, 200003, 2040200])
+def test_device_split_permutation_equals_numpy(n):
+    """Host swap targets + parallel device resolution == numpy's permutation."""
+    from paper_1403_4781_b200 import _engine as E
+    for seed in (0, 1234):
+        got = E.d2h(E.split_permutation(n, seed))
+        assert np.array_equal(got, np.random.default_rng(seed).permutation(n))

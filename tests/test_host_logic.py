@@ -121,3 +121,43 @@ def test_native_permutation_bitwise_numpy(n, seed):
     (trainer.py:208-209)."""
     from paper_1403_4781_b200 import _lib
     assert np.array_equal(_lib.permutation(n, seed), np.random.default_rng(seed).permutation(n))
+
+
+def _numpy_swap_targets(n, seed):
+    """Fisher-Yates targets of Generator.permutation(n): numpy's masked
+    rejection on buffered 32-bit halves of the PCG64 output (restated)."""
+    bg = np.random.default_rng(seed).bit_generator
+    buf = []
+
+    def next32():
+        if not buf:
+            r = int(bg.random_raw())
+            buf.extend([r >> 32, r & 0xFFFFFFFF])
+        return buf.pop()
+
+    js = []
+    for i in range(n - 1, 0, -1):
+        mask = i
+        for sh in (1, 2, 4, 8, 16):
+            mask |= mask >> sh
+        while True:
+            v = next32() & mask
+            if v <= i:
+                break
+        js.append(v)
+    return np.array(js, dtype=np.uint32)
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 5, 9, 16, 17, 1000, 4097])
+def test_native_swap_targets_match_numpy(n):
+    from paper_1403_4781_b200 import _lib
+    for seed in (0, 11):
+        js = np.empty(n - 1, dtype=np.uint32)
+        assert _lib.swap_targets(n, seed, js)
+        ref = _numpy_swap_targets(n, seed)
+        assert np.array_equal(js, ref)
+        a = np.arange(n)
+        for k, j in enumerate(js):
+            i = n - 1 - k
+            a[i], a[j] = a[j], a[i]
+        assert np.array_equal(a, np.random.default_rng(seed).permutation(n))
