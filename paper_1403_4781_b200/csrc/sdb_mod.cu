@@ -432,17 +432,27 @@ k_shard_sum(const int64_t* __restrict__ off, const double* __restrict__ v, doubl
 // ---- (i) finish MOD: norms, dead atoms, restore, normalise (dictionary_update.py:103-113)
 __global__ void __launch_bounds__(1024)
 k_mod_finish(int P, int K, int m, const double* __restrict__ Z, const double* __restrict__ Dprev,
-             const int32_t* __restrict__ usage, const int64_t* __restrict__ nnz_shard,
+             const int32_t* __restrict__ usage, int64_t* __restrict__ nnz_shard,
              double* __restrict__ Dout, double* __restrict__ scales, int8_t* __restrict__ dead,
              int32_t* __restrict__ rank, const int32_t* __restrict__ deficient) {
     __shared__ double s_max;
     __shared__ int s_rank;
+    __shared__ long long s_nnz[32];
     const int p = blockIdx.x;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const double* Zp = Z + (int64_t)p * K * m;
     if (threadIdx.x == 0) { s_max = 0.0; s_rank = 0; }
+    {   // nonzeros of the shard's codes = sum of its atom usages
+        long long u = 0;
+        for (int a = threadIdx.x; a < K; a += 1024) u += usage[(int64_t)p * K + a];
+        for (int o = 16; o > 0; o >>= 1) u += __shfl_xor_sync(SDB_FULL, u, o);
+        if (lane == 0) s_nnz[wib] = u;
+    }
     __syncthreads();
-    const bool empty = nnz_shard[p] == 0;
+    long long nnz = 0;
+    for (int w = 0; w < 32; ++w) nnz += s_nnz[w];
+    if (threadIdx.x == 0) nnz_shard[p] = nnz;
+    const bool empty = nnz == 0;
     // column norms of the raw solution
     for (int a = wib; a < K; a += 32) {
         double s = 0.0;
@@ -637,20 +647,6 @@ __global__ void k_usage_direct(int64_t N, int K, int cap, int P, const int64_t* 
     for (int t = 0; t < n; ++t) atomicAdd(&usage[(int64_t)p * K + idx[i * cap + t]], 1);
 }
 
-__global__ void k_shard_nnz(const int64_t* __restrict__ off, const int32_t* __restrict__ counts,
-                            int64_t* __restrict__ out) {
-    __shared__ int64_t sh[256];
-    const int p = blockIdx.x;
-    int64_t s = 0;
-    for (int64_t i = off[p] + threadIdx.x; i < off[p + 1]; i += 256) s += counts[i];
-    sh[threadIdx.x] = s;
-    __syncthreads();
-    for (int w = 128; w > 0; w >>= 1) {
-        if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) out[p] = sh[0];
-}
 
 // ---- code energy per shard: sum of squared code values (w_t^2, trainer.py:250)
 template <typename T>
@@ -805,7 +801,6 @@ int mod_update(const ModArgs<T>& a, cudaStream_t st) {
     });
     if (rc) return rc;
     k_shard_sum_masked<<<P, 256, 0, st>>>(a.off, w.rsq, w.need, a.resid_fro);
-    k_shard_nnz<<<P, 256, 0, st>>>(a.off, a.counts, w.nnz);
     k_mod_finish<<<P, 1024, 0, st>>>(P, K, m, w.B, a.Dprev, a.usage, w.nnz, a.Dout, a.scales, a.dead,
                                     a.rank, w.deficient);
     if (a.deficient_out)
