@@ -544,30 +544,26 @@ __device__ __forceinline__ void copy_tile(double* __restrict__ dst, const double
     }
 }
 
-// factor the 64x64 tile in place into T = L^-1. 2-D register blocking:
-// thread (tr, tc) = (t / 16, t % 16) owns rows tr + 16a and the contiguous
-// columns 4tc + b (a, b < 4) of L and of T, so every vector entry it loads
-// serves four rows (shared-memory wavefronts, not FP64 issue, bound the
-// 1-D layout). One CTA barrier per column k:
-//   publish: column k's owners publish it as a full vector (raw entries of
-//            rows >= k with every earlier rank-1 update applied, zeros above)
-//            and row k-1 of T is published (scaled by 1/L_{k-1,k-1});
-//   compute: every thread derives s_k = 1/sqrt(d_k) itself (0 for a dependent
-//            pivot or a padding row); rows r > k apply the rank-1 step
-//            v_r -= (a_rk s_k^2) a_k and rows r >= k apply
-//            T_r -= L_{r,k-1} T_{k-1} (the T sweep trails by one column).
-// Both updates are unconditional per element: they only touch entries that
-// are zero in the operand (T rows right of the diagonal, column entries above
-// the pivot) or that are never read again (already-published columns, the
-// strict upper triangle); row k-1 is the one row excluded from the T step.
-// Published vectors use a stride of 18 per 16-entry chunk (16-byte aligned
-// 4-column groups, conflict-free). Raw columns are triple-buffered (the
-// lagged T step still reads column k-1 while column k+1 is published), T rows
-// double-buffered. The loop over column quads stays rolled (static register
-// indices, small code).
-constexpr int FPW = 72;  // padded vector length (4 chunks x 18)
-
-__device__ __forceinline__ int fpad(int q) { return 18 * (q >> 4) + (q & 15); }
+// factor the 64x64 tile in place into T = L^-1, as a producer/consumer
+// dataflow over columns (no CTA-wide barrier per column):
+//   ownership: warp w owns columns q = w (mod 8), lane l rows l and l + 32
+//              (16 entries of L and 16 of T per thread, in registers);
+//   column k is produced by its owner warp as soon as its own entries have
+//   received update k-1: the pivot d_k is shuffled from the owner lane,
+//   s_k = 1/sqrt(d_k) (0 for a dependent pivot or a padding row), and
+//   l_k = s_k * (raw column, rows > k; zero elsewhere) goes to a ring slot
+//   in shared memory with s_k, signalled by an mbarrier ("full");
+//   every warp then applies, for each owned entry (unconditional FMAs: the
+//   operands are zero where the update must not act, or the entry is never
+//   read again), the Cholesky rank-1 step v -= l_r l_q and the T step
+//   T_r -= l_r T_k, where row k of T is finalised (scaled by s_k) in the
+//   registers of the warp's lane k % 32 and broadcast by shuffles;
+//   a slot is released through an "empty" mbarrier (all 256 threads).
+// The producer of column k+1 updates that column first and publishes before
+// the rest of its work, so the critical path per column is one mbarrier
+// wait, a shuffle, the FP64 rsqrt chain and the store.
+constexpr int FNB = 4;           // ring slots
+constexpr int FSLOT = CB + 2;    // 64 l values + s_k (+ pad)
 
 __device__ __forceinline__ double inv_sqrt_f64(double d) {
     double y = (double)rsqrtf((float)fmax(d, 1e-300));
@@ -575,93 +571,124 @@ __device__ __forceinline__ double inv_sqrt_f64(double d) {
     return y * fma(-0.5 * d * y, y, 1.5);
 }
 
-__device__ __forceinline__ void load4(double (&x)[4], const double* __restrict__ src) {
-    const double2 a = reinterpret_cast<const double2*>(src)[0];
-    const double2 b = reinterpret_cast<const double2*>(src)[1];
-    x[0] = a.x; x[1] = a.y; x[2] = b.x; x[3] = b.y;
+__device__ __forceinline__ void mbar_init_cta(uint64_t* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)),
+                 "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_cta(uint64_t* b) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(b))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cta(uint64_t* b, unsigned parity) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(b);
+    unsigned done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+    }
 }
 
-// (no __restrict__ on the shared buffers: other threads write them between
-// barriers, and a restrict-qualified pointer lets the compiler reuse a load of
-// the same address from an earlier phase across __syncthreads)
-__device__ __forceinline__ void factor_inverse(double* Ts, int nr, double tl, double* craw, double* trow,
+// ring: FNB x FSLOT doubles; bars: 2 * FNB mbarriers (full, empty). The caller
+// has synchronised the CTA after writing Ts.
+__device__ __forceinline__ void factor_inverse(double* Ts, int nr, double tl, double* ring, uint64_t* bars,
                                                int8_t* sdep) {
-    const int tid = threadIdx.x, tr = tid >> 4, tc = tid & 15;
-    const int colp = fpad(4 * tc);  // padded index of this thread's first column
-    double v[4][4], tv[4][4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const int r = tr + 16 * a, q = 4 * tc + b;
-            v[a][b] = (q <= r) ? Ts[r * CBP + q] : 0.0;
-            tv[a][b] = (q == r) ? 1.0 : 0.0;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    uint64_t* full = bars;
+    uint64_t* empty = bars + FNB;
+    if (tid == 0) {
+        for (int b = 0; b < FNB; ++b) {
+            mbar_init_cta(&full[b], 32);
+            mbar_init_cta(&empty[b], 256);
         }
-    double sprev = 0.0;
-    int b3 = 0, b3p = 2;  // k % 3, (k - 1) % 3
-#pragma unroll 1
-    for (int cq = 0; cq < 16; ++cq) {
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const int k = 4 * cq + b;
-            double* cr = craw + b3 * FPW;
-            const double* crp = craw + b3p * FPW;
-            double* tw = trow + (b & 1) * FPW;
-            if (tc == cq) {
-#pragma unroll
-                for (int a = 0; a < 4; ++a) cr[18 * a + tr] = (tr + 16 * a >= k) ? v[a][b] : 0.0;
-            }
-            if (k > 0 && tr == ((k - 1) & 15)) {
-                const int as = (k - 1) >> 4;
-#pragma unroll
-                for (int a = 0; a < 4; ++a)
-                    if (a == as) {
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) tv[a][c] *= sprev;
-                        reinterpret_cast<double2*>(tw + colp)[0] = make_double2(tv[a][0], tv[a][1]);
-                        reinterpret_cast<double2*>(tw + colp)[1] = make_double2(tv[a][2], tv[a][3]);
-                    }
-            }
-            __syncthreads();
-            const double d = cr[fpad(k)];
-            const bool dep = !(d > tl) || k >= nr;
-            const double sk = dep ? 0.0 : inv_sqrt_f64(d);
-            if (tid == 0) sdep[k] = dep ? 1 : 0;
-            {
-                const double s2 = sk * sk;
-                double x[4];
-                load4(x, cr + colp);
-#pragma unroll
-                for (int a = 0; a < 4; ++a) {
-                    const double coef = cr[18 * a + tr] * s2;
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) v[a][c] = fma(-coef, x[c], v[a][c]);
-                }
-            }
-            if (k > 0) {
-                double x[4];
-                load4(x, tw + colp);
-#pragma unroll
-                for (int a = 0; a < 4; ++a) {
-                    const double lp = (tr + 16 * a == k - 1) ? 0.0 : crp[18 * a + tr] * sprev;
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) tv[a][c] = fma(-lp, x[c], tv[a][c]);
-                }
-            }
-            sprev = sk;
-            b3p = b3;
-            b3 = (b3 == 2) ? 0 : b3 + 1;
-        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (tr == 15) {
+    double v[8][2], tv[8][2];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tv[3][c] *= sprev;
+    for (int c = 0; c < 8; ++c)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int r = lane + 32 * h, q = 8 * c + w;
+            v[c][h] = (q <= r) ? Ts[r * CBP + q] : 0.0;
+            tv[c][h] = (q == r) ? 1.0 : 0.0;
+        }
+    __syncthreads();  // barriers initialised
+    // produce column k (called by warp k % 8 with its column entries final)
+    auto produce = [&](int k, double x0, double x1) {  // x0, x1: this lane's entries of column k
+        const int slot = k % FNB;
+        if (k >= FNB) mbar_wait_cta(&empty[slot], ((k / FNB) - 1) & 1);
+        const double d = __shfl_sync(SDB_FULL, (k < 32) ? x0 : x1, k & 31);
+        const bool dep = !(d > tl) || k >= nr;
+        const double s = dep ? 0.0 : inv_sqrt_f64(d);
+        double* col = ring + slot * FSLOT;
+        col[lane] = (lane > k) ? x0 * s : 0.0;
+        col[lane + 32] = (lane + 32 > k) ? x1 * s : 0.0;
+        if (lane == 0) {
+            col[CB] = s;
+            sdep[k] = dep ? 1 : 0;
+        }
+        mbar_arrive_cta(&full[slot]);
+    };
+    if (w == 0) produce(0, v[0][0], v[0][1]);
+#pragma unroll 1
+    for (int kb = 0; kb < CB; kb += 8) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+            const int k = kb + kk;           // column k, owned by warp kk
+            const int slot = k % FNB;
+            mbar_wait_cta(&full[slot], (k / FNB) & 1);
+            const double* col = ring + slot * FSLOT;
+            const double sk = col[CB];
+            const double lr0 = col[lane], lr1 = col[lane + 32];
+            double lq[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) lq[c] = col[8 * c + w];
+            // the producer of column k+1 (warp (kk+1) % 8) updates it first
+            const int nk = k + 1, nw = (kk + 1) & 7, nc = (kk == 7) ? (kb / 8 + 1) : (kb / 8);
+            if (nk < CB && w == nw) {
+                double x0 = 0.0, x1 = 0.0;
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    if (c == nc) {
+                        v[c][0] = fma(-lr0, lq[c], v[c][0]);
+                        v[c][1] = fma(-lr1, lq[c], v[c][1]);
+                        lq[c] = 0.0;  // applied
+                        x0 = v[c][0];
+                        x1 = v[c][1];
+                    }
+                produce(nk, x0, x1);
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                v[c][0] = fma(-lr0, lq[c], v[c][0]);
+                v[c][1] = fma(-lr1, lq[c], v[c][1]);
+            }
+            // row k of T: finalise in the owner lane, broadcast, apply
+            const int hk = k >> 5, lk = k & 31;
+            if (lane == lk) {
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    if (hk == 0) tv[c][0] *= sk; else tv[c][1] *= sk;
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const double tk = __shfl_sync(SDB_FULL, hk == 0 ? tv[c][0] : tv[c][1], lk);
+                tv[c][0] = fma(-lr0, tk, tv[c][0]);
+                tv[c][1] = fma(-lr1, tk, tv[c][1]);
+            }
+            mbar_arrive_cta(&empty[slot]);
+        }
     }
     __syncthreads();
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int c = 0; c < 8; ++c)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) Ts[(tr + 16 * a) * CBP + 4 * tc + b] = tv[a][b];
+        for (int h = 0; h < 2; ++h) Ts[(lane + 32 * h) * CBP + 8 * c + w] = tv[c][h];
 }
 
 // fixed-order CTA sum / max of one double per thread
@@ -704,8 +731,8 @@ k_chol_cluster(int K, int m, double* __restrict__ Aall, double* __restrict__ Bal
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     extern __shared__ double xsm[];
-    __shared__ __align__(16) double craw[3 * FPW];
-    __shared__ __align__(16) double trow[2 * FPW];
+    __shared__ __align__(16) double fring[FNB * FSLOT];
+    __shared__ uint64_t fbars[2 * FNB];
     __shared__ double red[256];
     __shared__ double s_part[2];  // [0] diag max, [1] ||W||^2 of this block row
     __shared__ int8_t s_use[CL_MAX * CB];
@@ -817,7 +844,7 @@ k_chol_cluster(int K, int m, double* __restrict__ Aall, double* __restrict__ Bal
         else b_pending[J] = true;
     }
     // ---- own diagonal block: T_c = L_cc^-1
-    factor_inverse(tile(c), nr, tl, craw, trow, sdep);
+    factor_inverse(tile(c), nr, tl, fring, fbars, sdep);
     if (tid < nr) depmask[(int64_t)p * K + r0 + tid] = sdep[tid];
     if (tid == 0) {
         int nd = 0;
