@@ -17,6 +17,7 @@
 
 #include <cooperative_groups.h>
 #include <cstdlib>
+#include <type_traits>
 
 namespace sdb {
 
@@ -547,28 +548,36 @@ __device__ __forceinline__ void copy_tile(double* __restrict__ dst, const double
 // factor the 64x64 tile in place into T = L^-1, as a producer/consumer
 // dataflow over columns (no CTA-wide barrier per column):
 //   ownership: warp w owns columns q = w (mod 8), lane l rows l and l + 32
-//              (16 entries of L and 16 of T per thread, in registers);
+//              (16 entries of A/L and 16 of T per thread, in registers);
 //   column k is produced by its owner warp as soon as its own entries have
-//   received update k-1: the pivot d_k is shuffled from the owner lane,
-//   s_k = 1/sqrt(d_k) (0 for a dependent pivot or a padding row), and
-//   l_k = s_k * (raw column, rows > k; zero elsewhere) goes to a ring slot
-//   in shared memory with s_k, signalled by an mbarrier ("full");
-//   every warp then applies, for each owned entry (unconditional FMAs: the
-//   operands are zero where the update must not act, or the entry is never
-//   read again), the Cholesky rank-1 step v -= l_r l_q and the T step
-//   T_r -= l_r T_k, where row k of T is finalised (scaled by s_k) in the
-//   registers of the warp's lane k % 32 and broadcast by shuffles;
-//   a slot is released through an "empty" mbarrier (all 256 threads).
+//   received update k-1: the RAW column a_k (rows > k, zero elsewhere) and
+//   the pivot d_k go to a ring slot in shared memory, signalled by an
+//   mbarrier ("full"); no square root on this path: every warp forms
+//   rd_k = 1/d_k itself (0 for a dependent pivot or a padding row), and
+//   applies, for each owned entry (unconditional FMAs: the operands are zero
+//   where the update must not act, or the entry is never read again),
+//     the Cholesky rank-1 step   v_rq -= (a_r rd_k) a_q   (= l_r l_q), and
+//     the inverse step           P_r  -= (a_r rd_k) P_k,
+//   with P the unscaled rows of T (T_r = P_r / sqrt(d_r), applied at the
+//   end); row k of P lives in the warp's lane k % 32 and is broadcast by
+//   shuffles. A slot is released through an "empty" mbarrier (256 threads).
 // The producer of column k+1 updates that column first and publishes before
 // the rest of its work, so the critical path per column is one mbarrier
-// wait, a shuffle, the FP64 rsqrt chain and the store.
+// hand-off, the reciprocal, one FMA and the store.
 constexpr int FNB = 4;           // ring slots
-constexpr int FSLOT = CB + 2;    // 64 l values + s_k (+ pad)
+constexpr int FSLOT = CB + 2;    // 64 raw values + d_k (+ pad)
 
 __device__ __forceinline__ double inv_sqrt_f64(double d) {
     double y = (double)rsqrtf((float)fmax(d, 1e-300));
     y = y * fma(-0.5 * d * y, y, 1.5);
     return y * fma(-0.5 * d * y, y, 1.5);
+}
+
+__device__ __forceinline__ double rcp_f64(double d) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+    y = fma(y, fma(-d, y, 1.0), y);
+    return fma(y, fma(-d, y, 1.0), y);
 }
 
 __device__ __forceinline__ void mbar_init_cta(uint64_t* b, unsigned count) {
@@ -593,10 +602,10 @@ __device__ __forceinline__ void mbar_wait_cta(uint64_t* b, unsigned parity) {
     }
 }
 
-// ring: FNB x FSLOT doubles; bars: 2 * FNB mbarriers (full, empty). The caller
-// has synchronised the CTA after writing Ts.
+// ring: FNB x FSLOT doubles; bars: 2 * FNB mbarriers (full, empty); dval:
+// CB doubles (pivots). The caller has synchronised the CTA after writing Ts.
 __device__ __forceinline__ void factor_inverse(double* Ts, int nr, double tl, double* ring, uint64_t* bars,
-                                               int8_t* sdep) {
+                                               double* dval, int8_t* sdep) {
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     uint64_t* full = bars;
     uint64_t* empty = bars + FNB;
@@ -621,74 +630,90 @@ __device__ __forceinline__ void factor_inverse(double* Ts, int nr, double tl, do
     auto produce = [&](int k, double x0, double x1) {  // x0, x1: this lane's entries of column k
         const int slot = k % FNB;
         if (k >= FNB) mbar_wait_cta(&empty[slot], ((k / FNB) - 1) & 1);
-        const double d = __shfl_sync(SDB_FULL, (k < 32) ? x0 : x1, k & 31);
-        const bool dep = !(d > tl) || k >= nr;
-        const double s = dep ? 0.0 : inv_sqrt_f64(d);
         double* col = ring + slot * FSLOT;
-        col[lane] = (lane > k) ? x0 * s : 0.0;
-        col[lane + 32] = (lane + 32 > k) ? x1 * s : 0.0;
-        if (lane == 0) {
-            col[CB] = s;
-            sdep[k] = dep ? 1 : 0;
+        col[lane] = (lane > k) ? x0 : 0.0;
+        col[lane + 32] = (lane + 32 > k) ? x1 : 0.0;
+        if (lane == (k & 31)) {
+            const double d = (k < 32) ? x0 : x1;
+            col[CB] = d;
+            dval[k] = d;
         }
         mbar_arrive_cta(&full[slot]);
     };
     if (w == 0) produce(0, v[0][0], v[0][1]);
-#pragma unroll 1
-    for (int kb = 0; kb < CB; kb += 8) {
+    // the two halves k < 32 / k >= 32 are separate loops so that k >> 5 is a
+    // compile-time constant: for k >= 32 rows < 32 are finished (their a_r is
+    // 0) and columns < 32 of L are dead; for k < 32 row k of P is zero in
+    // columns >= 32. Those updates are skipped statically.
+    auto step = [&](int kb, int kk, auto H) {
+        constexpr int hk = decltype(H)::value;
+        const int k = kb + kk;  // column k, owned by warp kk
+        const int slot = k % FNB;
+        mbar_wait_cta(&full[slot], (k / FNB) & 1);
+        const double* col = ring + slot * FSLOT;
+        const double d = col[CB];
+        const double rd = (!(d > tl) || k >= nr) ? 0.0 : rcp_f64(d);
+        const double lr0 = hk == 0 ? col[lane] * rd : 0.0;
+        const double lr1 = col[lane + 32] * rd;
+        double lq[8];
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-            const int k = kb + kk;           // column k, owned by warp kk
-            const int slot = k % FNB;
-            mbar_wait_cta(&full[slot], (k / FNB) & 1);
-            const double* col = ring + slot * FSLOT;
-            const double sk = col[CB];
-            const double lr0 = col[lane], lr1 = col[lane + 32];
-            double lq[8];
+        for (int c = 0; c < 8; ++c) lq[c] = (hk == 0 || c >= 4) ? col[8 * c + w] : 0.0;
+        const int nk = k + 1, nw = (kk + 1) & 7, nc = nk >> 3;
+        if (nk < CB && w == nw) {
+            double x0 = 0.0, x1 = 0.0;
 #pragma unroll
-            for (int c = 0; c < 8; ++c) lq[c] = col[8 * c + w];
-            // the producer of column k+1 (warp (kk+1) % 8) updates it first
-            const int nk = k + 1, nw = (kk + 1) & 7, nc = (kk == 7) ? (kb / 8 + 1) : (kb / 8);
-            if (nk < CB && w == nw) {
-                double x0 = 0.0, x1 = 0.0;
-#pragma unroll
-                for (int c = 0; c < 8; ++c)
-                    if (c == nc) {
-                        v[c][0] = fma(-lr0, lq[c], v[c][0]);
-                        v[c][1] = fma(-lr1, lq[c], v[c][1]);
-                        lq[c] = 0.0;  // applied
-                        x0 = v[c][0];
-                        x1 = v[c][1];
-                    }
-                produce(nk, x0, x1);
-            }
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                v[c][0] = fma(-lr0, lq[c], v[c][0]);
-                v[c][1] = fma(-lr1, lq[c], v[c][1]);
-            }
-            // row k of T: finalise in the owner lane, broadcast, apply
-            const int hk = k >> 5, lk = k & 31;
-            if (lane == lk) {
-#pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    if (hk == 0) tv[c][0] *= sk; else tv[c][1] *= sk;
+            for (int c = 0; c < 8; ++c)
+                if (c == nc) {
+                    if (hk == 0) v[c][0] = fma(-lr0, lq[c], v[c][0]);
+                    v[c][1] = fma(-lr1, lq[c], v[c][1]);
+                    lq[c] = 0.0;  // applied
+                    x0 = v[c][0];
+                    x1 = v[c][1];
                 }
-            }
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                const double tk = __shfl_sync(SDB_FULL, hk == 0 ? tv[c][0] : tv[c][1], lk);
-                tv[c][0] = fma(-lr0, tk, tv[c][0]);
-                tv[c][1] = fma(-lr1, tk, tv[c][1]);
-            }
-            mbar_arrive_cta(&empty[slot]);
+            produce(nk, x0, x1);
         }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            if (hk == 1 && c < 4) continue;  // dead columns of L
+            if (hk == 0) v[c][0] = fma(-lr0, lq[c], v[c][0]);
+            v[c][1] = fma(-lr1, lq[c], v[c][1]);
+        }
+        // row k of P (final: every earlier row has been applied to it)
+        const int lk = k & 31;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            if (hk == 0 && c >= 4) continue;  // zero right of the diagonal
+            const double tk = __shfl_sync(SDB_FULL, tv[c][hk], lk);
+            if (hk == 0) tv[c][0] = fma(-lr0, tk, tv[c][0]);
+            tv[c][1] = fma(-lr1, tk, tv[c][1]);
+        }
+        mbar_arrive_cta(&empty[slot]);
+    };
+#pragma unroll 1
+    for (int kb = 0; kb < 32; kb += 8) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) step(kb, kk, std::integral_constant<int, 0>{});
+    }
+#pragma unroll 1
+    for (int kb = 32; kb < CB; kb += 8) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) step(kb, kk, std::integral_constant<int, 1>{});
     }
     __syncthreads();
+    // T_r = P_r / sqrt(d_r) (0 for dependent pivots / padding rows)
+    if (tid < CB) {
+        const double d = dval[tid];
+        const bool dep = !(d > tl) || tid >= nr;
+        sdep[tid] = dep ? 1 : 0;
+        dval[tid] = dep ? 0.0 : inv_sqrt_f64(d);
+    }
+    __syncthreads();
+    const double s0 = dval[lane], s1 = dval[lane + 32];
 #pragma unroll
-    for (int c = 0; c < 8; ++c)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) Ts[(lane + 32 * h) * CBP + 8 * c + w] = tv[c][h];
+    for (int c = 0; c < 8; ++c) {
+        Ts[lane * CBP + 8 * c + w] = tv[c][0] * s0;
+        Ts[(lane + 32) * CBP + 8 * c + w] = tv[c][1] * s1;
+    }
 }
 
 // fixed-order CTA sum / max of one double per thread
@@ -733,6 +758,7 @@ k_chol_cluster(int K, int m, double* __restrict__ Aall, double* __restrict__ Bal
     extern __shared__ double xsm[];
     __shared__ __align__(16) double fring[FNB * FSLOT];
     __shared__ uint64_t fbars[2 * FNB];
+    __shared__ double fdval[CB];
     __shared__ double red[256];
     __shared__ double s_part[2];  // [0] diag max, [1] ||W||^2 of this block row
     __shared__ int8_t s_use[CL_MAX * CB];
@@ -844,7 +870,7 @@ k_chol_cluster(int K, int m, double* __restrict__ Aall, double* __restrict__ Bal
         else b_pending[J] = true;
     }
     // ---- own diagonal block: T_c = L_cc^-1
-    factor_inverse(tile(c), nr, tl, fring, fbars, sdep);
+    factor_inverse(tile(c), nr, tl, fring, fbars, fdval, sdep);
     if (tid < nr) depmask[(int64_t)p * K + r0 + tid] = sdep[tid];
     if (tid == 0) {
         int nd = 0;

@@ -8,13 +8,14 @@ __global__ void kf(const double* A, double* T, long long* cyc, int reps) {
     extern __shared__ double xs[];
     __shared__ __align__(16) double fring[FNB * FSLOT];
     __shared__ uint64_t fbars[2 * FNB];
+    __shared__ double fdval[CB];
     __shared__ int8_t sdep[CB];
     long long best = 1LL << 60;
     for (int r = 0; r < reps; ++r) {
         for (int e = threadIdx.x; e < CB * CB; e += 256) xs[(e / CB) * CBP + e % CB] = A[e];
         __syncthreads();
         long long t0 = clock64();
-        factor_inverse(xs, CB, 1e-12, fring, fbars, sdep);
+        factor_inverse(xs, CB, 1e-12, fring, fbars, fdval, sdep);
         __syncthreads();
         long long t1 = clock64();
         if (t1 - t0 < best) best = t1 - t0;
