@@ -23,10 +23,17 @@
 
 namespace sdb {
 
-constexpr int CH = 1024;  // signals per chunk (chunks never straddle shards)
+// signals per chunk (chunks never straddle shards): 1024 for large jobs,
+// down to one 32-signal warp group for small ones (the merge phase), so the
+// warp-per-chunk histogram / placement kernels always have enough warps
+__host__ __device__ inline int chunk_size(int64_t N) {
+    int ch = 1024;
+    while (ch > 32 && (int64_t)ch * 148 * 8 > N) ch >>= 1;
+    return ch;
+}
 
 // chunk_first[p] = first chunk of shard p; chunk_first[P] = total chunks
-__global__ void k_chunk_layout(const int64_t* __restrict__ off, int P, int64_t* __restrict__ cf) {
+__global__ void k_chunk_layout(const int64_t* __restrict__ off, int P, int CH, int64_t* __restrict__ cf) {
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         int64_t c = 0;
         for (int p = 0; p < P; ++p) {
@@ -42,7 +49,7 @@ struct ChunkInfo {
     int64_t lo, hi;
 };
 
-__device__ __forceinline__ ChunkInfo chunk_info(const int64_t* off, const int64_t* cf, int P, int64_t c) {
+__device__ __forceinline__ ChunkInfo chunk_info(const int64_t* off, const int64_t* cf, int P, int64_t c, int CH) {
     int lo = 0, hi = P - 1;
     while (lo < hi) {  // last p with cf[p] <= c (empty shards share cf values)
         int mid = (lo + hi + 1) >> 1;
@@ -57,7 +64,7 @@ __device__ __forceinline__ ChunkInfo chunk_info(const int64_t* off, const int64_
 
 // ---- (a) per-chunk atom histograms (warp per chunk, smem int atomics)
 __global__ void __launch_bounds__(256)
-k_chunk_hist(const int64_t* __restrict__ off, const int64_t* __restrict__ cf, int P, int K, int cap,
+k_chunk_hist(const int64_t* __restrict__ off, const int64_t* __restrict__ cf, int P, int K, int cap, int CH,
              const int32_t* __restrict__ idx, const int32_t* __restrict__ counts,
              int32_t* __restrict__ chunk_hist) {
     extern __shared__ int32_t sh_cnt[];
@@ -68,7 +75,7 @@ k_chunk_hist(const int64_t* __restrict__ off, const int64_t* __restrict__ cf, in
     if (c >= nch) return;
     for (int a = lane; a < K; a += 32) cnt[a] = 0;
     __syncwarp();
-    const ChunkInfo ci = chunk_info(off, cf, P, c);
+    const ChunkInfo ci = chunk_info(off, cf, P, c, CH);
     for (int64_t i = ci.lo + lane; i < ci.hi; i += 32) {
         const int n = counts[i];
         for (int t = 0; t < n; ++t) atomicAdd(&cnt[idx[i * cap + t]], 1);
@@ -130,7 +137,7 @@ k_chunk_offsets(const int64_t* __restrict__ cf, int P, int K, const int32_t* __r
 // slot, lane) — a fixed function of the input.
 template <typename T>
 __global__ void __launch_bounds__(256)
-k_place(const int64_t* __restrict__ off, const int64_t* __restrict__ cf, int P, int K, int cap,
+k_place(const int64_t* __restrict__ off, const int64_t* __restrict__ cf, int P, int K, int cap, int CH,
         const int32_t* __restrict__ idx, const T* __restrict__ val, const int32_t* __restrict__ counts,
         const int64_t* __restrict__ chunk_off, int32_t* __restrict__ bsig, double* __restrict__ bval) {
     extern __shared__ int64_t sh_pos[];
@@ -140,7 +147,7 @@ k_place(const int64_t* __restrict__ off, const int64_t* __restrict__ cf, int P, 
     int64_t* pos = sh_pos + (int64_t)wib * K;
     for (int a = lane; a < K; a += 32) pos[a] = chunk_off[c * K + a];
     __syncwarp();
-    const ChunkInfo ci = chunk_info(off, cf, P, c);
+    const ChunkInfo ci = chunk_info(off, cf, P, c, CH);
     for (int64_t g = ci.lo; g < ci.hi; g += 32) {
         const int64_t i = g + lane;
         const int n = (i < ci.hi) ? counts[i] : 0;
@@ -704,7 +711,7 @@ static int with_mpl(int m, F&& f) {
     return (int)cudaErrorInvalidValue;  // m > 256 rejected at the ABI
 }
 
-static int64_t nchunks_upper(int64_t N, int P) { return N / CH + P + 1; }
+static int64_t nchunks_upper(int64_t N, int P) { return N / chunk_size(N) + P + 1; }
 
 ModWs carve_mod_ws(void* base, int P, int64_t N, int m, int K, int cap) {
     ModWs w{};
@@ -745,9 +752,10 @@ int mod_update(const ModArgs<T>& a, cudaStream_t st) {
     ModWs w = carve_mod_ws(a.ws, P, N, m, K, cap);
     const int64_t PK = (int64_t)P * K;
     const int64_t nch_max = nchunks_upper(N, P);
-    k_chunk_layout<<<1, 32, 0, st>>>(a.off, P, w.cf);
+    const int ch = chunk_size(N);
+    k_chunk_layout<<<1, 32, 0, st>>>(a.off, P, ch, w.cf);
     const unsigned hb = (unsigned)((nch_max + 7) / 8);
-    k_chunk_hist<<<hb, 256, 8 * K * sizeof(int32_t), st>>>(a.off, w.cf, P, K, cap, a.idx, a.counts,
+    k_chunk_hist<<<hb, 256, 8 * K * sizeof(int32_t), st>>>(a.off, w.cf, P, K, cap, ch, a.idx, a.counts,
                                                           w.chunk_hist);
     const dim3 gpk((unsigned)((K + 31) / 32), (unsigned)P);
     k_usage_from_chunks<<<gpk, 256, 0, st>>>(w.cf, P, K, w.chunk_hist, w.wpart, a.usage);
@@ -758,7 +766,7 @@ int mod_update(const ModArgs<T>& a, cudaStream_t st) {
         const int smem = 8 * K * (int)sizeof(int64_t);
         if (smem > 48 * 1024)
             cudaFuncSetAttribute(k_place<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        k_place<T><<<hb, 256, smem, st>>>(a.off, w.cf, P, K, cap, a.idx, a.val, a.counts,
+        k_place<T><<<hb, 256, smem, st>>>(a.off, w.cf, P, K, cap, ch, a.idx, a.val, a.counts,
                                          w.chunk_off, w.bsig, w.bval);
     }
     rc = with_mpl(m, [&](auto c) {
