@@ -221,6 +221,8 @@ int sdb_mod_update(int dtype, int64_t P, int64_t N, int64_t m, int64_t K, int64_
                    int64_t ws_bytes, void* stream) {
     if (!dtype_ok(dtype) || P < 1 || N < 0 || m < 1 || m > 256 || K < 1 || K > 1024 || cap < 1 || ldy < m)
         return fail(SDB_EINVAL, "sdb_mod_update: bad args (m <= 256, K <= 1024)");
+    if (N * cap > 0x7fffffffll)  // bucket entries are 32-bit flat code indices
+        return fail(SDB_EINVAL, "sdb_mod_update: N * cap = %lld exceeds 2^31 - 1", (long long)(N * cap));
     if (ws == nullptr || ws_bytes < sdb::mod_ws_bytes((int)P, N, (int)m, (int)K, (int)cap))
         return fail(SDB_EINVAL, "sdb_mod_update: workspace too small");
     auto go = [&](auto* tag) {

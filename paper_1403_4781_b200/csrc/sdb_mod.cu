@@ -139,7 +139,7 @@ template <typename T>
 __global__ void __launch_bounds__(256)
 k_place(const int64_t* __restrict__ off, const int64_t* __restrict__ cf, int P, int K, int cap, int CH,
         const int32_t* __restrict__ idx, const T* __restrict__ val, const int32_t* __restrict__ counts,
-        const int64_t* __restrict__ chunk_off, int32_t* __restrict__ bsig, double* __restrict__ bval) {
+        const int64_t* __restrict__ chunk_off, int32_t* __restrict__ bent) {
     extern __shared__ int64_t sh_pos[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t c = (int64_t)blockIdx.x * 8 + wib;
@@ -167,8 +167,7 @@ k_place(const int64_t* __restrict__ off, const int64_t* __restrict__ cf, int P, 
             if (act) {
                 const int rank = __popc(peers & ((1u << lane) - 1u));
                 const int64_t q = base + rank;
-                bsig[q] = (int32_t)i;
-                bval[q] = (double)val[i * cap + t];
+                bent[q] = (int32_t)(i * cap + t);  // flat code index: signal i, slot t
                 if (rank == 0) pos[a] = base + __popc(peers);
             }
             __syncwarp();
@@ -183,7 +182,7 @@ k_place(const int64_t* __restrict__ off, const int64_t* __restrict__ cf, int P, 
 template <typename T, int MPL>
 __global__ void __launch_bounds__(256)
 k_yxt(int P, int K, int m, const T* __restrict__ Y, int64_t ldy, const int64_t* __restrict__ bucket_off,
-      const int32_t* __restrict__ bsig, const double* __restrict__ bval, double* __restrict__ B) {
+      int cap, const T* __restrict__ val, const int32_t* __restrict__ bent, double* __restrict__ B) {
     __shared__ double part[8][MPL * 32];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t e = blockIdx.x;  // (p, a)
@@ -193,8 +192,9 @@ k_yxt(int P, int K, int m, const T* __restrict__ Y, int64_t ldy, const int64_t* 
     const int64_t lo = bucket_off[e], hi = bucket_off[e + 1];
     for (int64_t b0 = lo + 32 * wib; b0 < hi; b0 += 32 * 8) {
         const int nbat = (int)min((int64_t)32, hi - b0);
-        const int my_sig = lane < nbat ? bsig[b0 + lane] : 0;
-        const double my_val = lane < nbat ? bval[b0 + lane] : 0.0;
+        const int my_e = lane < nbat ? bent[b0 + lane] : 0;
+        const int my_sig = my_e / cap;
+        const double my_val = lane < nbat ? (double)val[my_e] : 0.0;
         for (int j = 0; j < nbat; j += 4) {
             double yv[4][MPL];
             double vv[4];
@@ -240,7 +240,7 @@ template <typename T>
 __global__ void __launch_bounds__(256)
 k_xxt(int P, int K, int cap, const int32_t* __restrict__ idx, const T* __restrict__ val,
       const int32_t* __restrict__ counts, const int64_t* __restrict__ bucket_off,
-      const int32_t* __restrict__ bsig, const double* __restrict__ bval, double* __restrict__ A) {
+      const int32_t* __restrict__ bent, double* __restrict__ A) {
     extern __shared__ double sh_row[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t e = blockIdx.x;
@@ -256,8 +256,9 @@ k_xxt(int P, int K, int cap, const int32_t* __restrict__ idx, const T* __restric
     double diag = 0.0;
     for (int64_t q0 = lo + 32 * wib; q0 < hi; q0 += 32 * 8) {
         const int nbat = (int)min((int64_t)32, hi - q0);
-        const int my_sig = lane < nbat ? bsig[q0 + lane] : 0;
-        const double my_v = lane < nbat ? bval[q0 + lane] : 0.0;
+        const int my_e = lane < nbat ? bent[q0 + lane] : 0;
+        const int my_sig = my_e / cap;
+        const double my_v = lane < nbat ? (double)val[my_e] : 0.0;
         const int my_n = lane < nbat ? counts[my_sig] : 0;
         if (staged) {
             for (int t = 0; t < my_n; ++t) {
@@ -724,8 +725,7 @@ ModWs carve_mod_ws(void* base, int P, int64_t N, int m, int K, int cap) {
     w.wpart = (int64_t*)take(sizeof(int64_t) * 8 * (int64_t)P * K);
     w.bucket_off = (int64_t*)take(sizeof(int64_t) * ((int64_t)P * K + 1));
     w.scan_ws = (int64_t*)take(scan_workspace_bytes((int64_t)P * K));
-    w.bsig = (int32_t*)take(sizeof(int32_t) * std::max<int64_t>(N * cap, 1));
-    w.bval = (double*)take(sizeof(double) * std::max<int64_t>(N * cap, 1));
+    w.bent = (int32_t*)take(sizeof(int32_t) * std::max<int64_t>(N * cap, 1));
     w.A = (double*)take(sizeof(double) * (int64_t)P * K * K);
     w.B = (double*)take(sizeof(double) * (int64_t)P * K * m);
     w.rsq = (double*)take(sizeof(double) * std::max<int64_t>(N, 1));
@@ -767,12 +767,12 @@ int mod_update(const ModArgs<T>& a, cudaStream_t st) {
         if (smem > 48 * 1024)
             cudaFuncSetAttribute(k_place<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         k_place<T><<<hb, 256, smem, st>>>(a.off, w.cf, P, K, cap, ch, a.idx, a.val, a.counts,
-                                         w.chunk_off, w.bsig, w.bval);
+                                         w.chunk_off, w.bent);
     }
     rc = with_mpl(m, [&](auto c) {
         constexpr int MPL = decltype(c)::value;
         k_yxt<T, MPL><<<(unsigned)PK, 256, 0, st>>>(P, K, m, a.Y, a.ldy, w.bucket_off,
-                                                               w.bsig, w.bval, w.B);
+                                                               cap, a.val, w.bent, w.B);
         return (int)cudaGetLastError();
     });
     if (rc) return rc;
@@ -781,7 +781,7 @@ int mod_update(const ModArgs<T>& a, cudaStream_t st) {
         if (smem > 48 * 1024)
             cudaFuncSetAttribute(k_xxt<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         k_xxt<T><<<(unsigned)PK, 256, smem, st>>>(P, K, cap, a.idx, a.val, a.counts,
-                                                             w.bucket_off, w.bsig, w.bval, w.A);
+                                                             w.bucket_off, w.bent, w.A);
     }
     // masked RHS rows of unused atoms are irrelevant: A is the identity there
     // and B holds zeros (their buckets are empty).

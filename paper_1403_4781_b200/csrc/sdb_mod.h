@@ -12,8 +12,7 @@ struct ModWs {
     int64_t* wpart;  // per-warp chunk-range partial counts (P x 8 x K)
     int64_t* bucket_off;
     int64_t* scan_ws;
-    int32_t* bsig;
-    double* bval;
+    int32_t* bent;  // bucket entries: flat code index i * cap + slot
     double* A;
     double* B;
     double* rsq;
