@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4"])
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--groups", type=int, default=1,
+                    help="concurrent shard groups in the local phase (device-resident run)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=1234)
     return ap.parse_args()
@@ -228,7 +230,8 @@ def main():
                                      cfg["K"], cfg["s2"], cfg["merge_iters"], args.seed,
                                      prec=prec)
         return split_merge_device(Ydev, cfg["L"], cfg["K1"], cap, eps, cfg["local_iters"],
-                                  cfg["K"], cfg["s2"], cfg["merge_iters"], args.seed, prec=prec)
+                                  cfg["K"], cfg["s2"], cfg["merge_iters"], args.seed, prec=prec,
+                                  groups=args.groups)
 
     for _ in range(args.warmup):
         r = step()

@@ -173,6 +173,16 @@ int sdb_scale_rows(int dtype, int64_t rows, int64_t group, int64_t m, const doub
 
 /* out[r] = in[perm[r]] (rows of m values): split_dataset's column gather
  * (trainer.py:220-223) into shard-contiguous order. */
+/* out[r] = src[perm[r]] (f64 rows of length m <= 256, cast to dtype) and
+ * *bad = 1 if any gathered value is non-finite: split_dataset's gather fused
+ * with the input cast and check. src may be device memory or pinned,
+ * device-mapped host memory (see sdb_host_mapped): the rows then cross PCIe
+ * directly in permuted order. */
+int sdb_ingest_gather(int dtype, int64_t rows, int64_t m, const double *src, int64_t ldi,
+                      const int64_t *perm, void *out, int64_t ldo, int32_t *bad, void *stream);
+/* Device address of a pinned, device-mapped host allocation (UVA: normally the
+ * same address); SDB_EINVAL for pageable memory. */
+int sdb_host_mapped(const void *host, void **dev);
 int sdb_gather_rows(int dtype, int64_t rows, int64_t m, const void *in, int64_t ldi,
                     const int64_t *perm, void *out, int64_t ldo, void *stream);
 

@@ -10,6 +10,8 @@ from __future__ import annotations
 import os
 from dataclasses import dataclass
 
+import ctypes
+
 import numpy as np
 import torch
 
@@ -471,6 +473,25 @@ def normalize_rows(D64: torch.Tensor):
     sc = empty(D64.shape[:-1], torch.float64)
     _lib.call("sdb_normalize", rows, m, ptr(D64), ptr(out), ptr(sc), stream())
     return out, sc
+
+
+def host_mapped(arr) -> int | None:
+    """Device address of a pinned, device-mapped host numpy array, else None."""
+    dev = ctypes.c_void_p()
+    if arr.size == 0 or _lib.load().sdb_host_mapped(arr.ctypes.data, ctypes.byref(dev)) != 0:
+        return None
+    return dev.value
+
+
+def ingest_gather(src_ptr: int, ldi: int, perm: torch.Tensor, lo: int, hi: int, m: int, prec: str,
+                  bad: torch.Tensor) -> torch.Tensor:
+    """Rows perm[lo:hi] of an f64 row-major source (device or mapped host
+    address) -> device (hi-lo) x m in the working precision; bad |= non-finite."""
+    rows = hi - lo
+    out = empty((max(rows, 1), m), torch_dtype(prec))[:rows]
+    _lib.call("sdb_ingest_gather", sdb_dtype(prec), rows, m, src_ptr, ldi, ptr(perm) + 8 * lo,
+              ptr(out), m, ptr(bad), stream())
+    return out
 
 
 def gather_rows(Y: torch.Tensor, perm: torch.Tensor, prec: str) -> torch.Tensor:

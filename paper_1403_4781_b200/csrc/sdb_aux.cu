@@ -4,6 +4,8 @@
 // averaging, clip), trainer.py:200-223 (shard gather), sparse_coding.py:76-133
 // (CSC container -> per-signal code rows), dictionary_update.py:56-69
 // (normalize_columns).
+#include <algorithm>
+
 #include "sdb_common.cuh"
 #include "sdb_internal.h"
 #include "sdb_aux.h"
@@ -21,6 +23,69 @@ __global__ void k_gather_rows(int64_t rows, int m, const T* __restrict__ in, int
     T* dst = out + r * ldo;
     for (int t = lane; t < m; t += 32) dst[t] = src[t];
 }
+
+// out[r] = (T) src[perm[r]] for f64 rows of length m, with a non-finite flag:
+// the split's gather fused with the input cast and the finiteness check. src
+// may be device memory or pinned, device-mapped host memory (the rows then
+// cross PCIe in permuted order); each warp keeps four rows in flight.
+template <typename T, int MPL>
+__global__ void __launch_bounds__(256)
+k_ingest_gather(int64_t rows, int m, const double* __restrict__ src, int64_t ldi, const int64_t* __restrict__ perm,
+                T* __restrict__ out, int64_t ldo, int32_t* __restrict__ bad) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * 8;
+    bool nonfinite = false;
+    for (int64_t r0 = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * 4; r0 < rows; r0 += nw * 4) {
+        double v[4][MPL];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t r = r0 + u;
+            const double* row = r < rows ? src + perm[r] * ldi : src;
+#pragma unroll
+            for (int q = 0; q < MPL; ++q) {
+                const int t = lane + 32 * q;
+                v[u][q] = (r < rows && t < m) ? row[t] : 0.0;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t r = r0 + u;
+            if (r >= rows) break;
+#pragma unroll
+            for (int q = 0; q < MPL; ++q) {
+                const int t = lane + 32 * q;
+                if (t < m) {
+                    nonfinite |= !isfinite(v[u][q]);
+                    out[r * ldo + t] = (T)v[u][q];
+                }
+            }
+        }
+    }
+    if (__any_sync(0xffffffffu, nonfinite) && lane == 0) *bad = 1;
+}
+
+template <typename T>
+int ingest_gather(int64_t rows, int m, const double* src, int64_t ldi, const int64_t* perm, T* out, int64_t ldo,
+                  int32_t* bad, cudaStream_t st) {
+    if (rows <= 0) return 0;
+    // host source: 64 CTAs keep ~2K rows (~1 MB) in flight, plenty for PCIe,
+    // and leave the SMs to concurrently running training kernels
+    cudaPointerAttributes at{};
+    const bool host = cudaPointerGetAttributes(&at, src) == cudaSuccess && at.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    const int64_t gmax = host ? 64 : 148 * 16;
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((rows + 31) / 32, gmax));
+    const int mpl = (m + 31) / 32;
+    if (mpl <= 1) k_ingest_gather<T, 1><<<g, 256, 0, st>>>(rows, m, src, ldi, perm, out, ldo, bad);
+    else if (mpl <= 2) k_ingest_gather<T, 2><<<g, 256, 0, st>>>(rows, m, src, ldi, perm, out, ldo, bad);
+    else if (mpl <= 5) k_ingest_gather<T, 5><<<g, 256, 0, st>>>(rows, m, src, ldi, perm, out, ldo, bad);
+    else k_ingest_gather<T, 8><<<g, 256, 0, st>>>(rows, m, src, ldi, perm, out, ldo, bad);
+    return (int)cudaGetLastError();
+}
+template int ingest_gather<float>(int64_t, int, const double*, int64_t, const int64_t*, float*, int64_t, int32_t*,
+                                  cudaStream_t);
+template int ingest_gather<double>(int64_t, int, const double*, int64_t, const int64_t*, double*, int64_t,
+                                   int32_t*, cudaStream_t);
 
 // CSC (indptr, indices, data) -> codes rows (idx N x cap, val, counts)
 template <typename T>

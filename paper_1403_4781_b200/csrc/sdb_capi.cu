@@ -333,6 +333,29 @@ int sdb_gather_rows(int dtype, int64_t rows, int64_t m, const void* in, int64_t 
     return cuda_rc(rc, "sdb_gather_rows");
 }
 
+int sdb_ingest_gather(int dtype, int64_t rows, int64_t m, const double* src, int64_t ldi, const int64_t* perm,
+                      void* out, int64_t ldo, int32_t* bad, void* stream) {
+    if (!dtype_ok(dtype) || rows < 0 || m < 1 || m > 256 || ldi < m || ldo < m ||
+        (rows > 0 && (src == nullptr || perm == nullptr || out == nullptr || bad == nullptr)))
+        return fail(SDB_EINVAL, "sdb_ingest_gather: bad args");
+    int rc = dtype == SDB_F64 ? sdb::ingest_gather<double>(rows, (int)m, src, ldi, perm, (double*)out, ldo, bad, S(stream))
+                              : sdb::ingest_gather<float>(rows, (int)m, src, ldi, perm, (float*)out, ldo, bad, S(stream));
+    return cuda_rc(rc, "sdb_ingest_gather");
+}
+
+int sdb_host_mapped(const void* host, void** dev) {
+    if (host == nullptr || dev == nullptr) return fail(SDB_EINVAL, "sdb_host_mapped: bad args");
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, host) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(SDB_EINVAL, "sdb_host_mapped: not a CUDA host allocation");
+    }
+    if (at.type != cudaMemoryTypeHost || at.devicePointer == nullptr)
+        return fail(SDB_EINVAL, "sdb_host_mapped: not pinned, device-mapped host memory");
+    *dev = at.devicePointer;
+    return SDB_OK;
+}
+
 int sdb_csc_to_codes(int dtype, int64_t N, int64_t cap, const int64_t* indptr,
                      const int64_t* indices, const double* data, int32_t* idx, void* val,
                      int32_t* counts, void* stream) {

@@ -584,6 +584,7 @@ k_omp_fast(OmpArgs<float> a) {
                 for (int k = KPL - 1; k >= 0; --k)
                     if (__float_as_uint(v[k]) == cbits) cand = j0 + k;
                 const int best = (int)__reduce_min_sync(SDB_FULL, (unsigned)cand);
+                if (best >= K) { status = 3; break; }  // no candidate (non-finite input)
 
                 // ---- every load of this step issued at once: G[b,b], G[S,b], c0[b]
                 float dsq = __ldg(Gp + (best * K + best));

@@ -18,6 +18,7 @@ arithmetic ("fp64" default, "fp32" fast mode).
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -431,39 +432,83 @@ class SplitMergeResult:
     codings: int                   # OMP signal-codings performed
 
 
-def split_merge_device(Ydev: torch.Tensor, L: int, K1: int, local_cap: int, local_eps: float,
-                       local_iters: int, K: int, s2: int, merge_iters: int, seed: int,
-                       init="first-columns", prec: str = "fp64", use_tc: bool = True,
-                       t_start: float | None = None, perm: torch.Tensor | None = None
-                       ) -> SplitMergeResult:
-    """split_dataset -> all locals in one batched loop -> merge (trainer.py:
-    291-313). ``Ydev`` is (N, m) device, signal-major."""
-    if t_start is None:
-        _sync()
-        t_start = time.perf_counter()
-    N, m = Ydev.shape
-    if not 1 <= L <= N:
-        raise InvalidInputError("require 1 <= L <= N")
-    # split_indices' blocks are consecutive slices of one PCG64 permutation
-    # (native, bit-identical to numpy; ``perm`` may be precomputed by the caller)
-    if perm is None:
-        perm = E.split_permutation(N, seed)
+_STREAMS: list = []
+
+
+def _streams(n: int) -> list:
+    while len(_STREAMS) < n:
+        _STREAMS.append(torch.cuda.Stream())
+    return _STREAMS[:n]
+
+
+def _split_locals(src, N: int, m: int, L: int, K1: int, local_cap: int, local_eps: float,
+                  local_iters: int, seeds, perm: torch.Tensor, prec: str, use_tc: bool, groups: int,
+                  host_f64: int | None = None, bad: torch.Tensor | None = None):
+    """split_dataset + every train_local (trainer.py:291-305), in G groups of
+    consecutive shards, each on its own CUDA stream. The group's rows are
+    gathered in permuted order (all gathers in order on one copy stream, so
+    group 0's rows land first), then the group trains as soon as they are
+    there, overlapping later groups' gathers and each other's latency-bound
+    MOD steps. src: device (N, m) working-precision signals, or ``host_f64``:
+    the device address of pinned, mapped host f64 rows (the transfer over
+    PCIe then is the gather itself). Shards are independent, so the result
+    equals the one-group (batched) computation. Returns (Dl, w) on the
+    caller's stream."""
     base, extra = divmod(N, L)
     sizes = [base + (1 if t < extra else 0) for t in range(L)]
-    Ys = E.gather_rows(Ydev, perm, prec)
-    off, _ = E.shard_offsets(sizes)
-    S = E.ShardSet(Ys, off, sizes, prec)
-    _sync()
-    t_split = time.perf_counter()
-    seeds = _derive_seeds(seed, L + 1)
+    offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
     if min(sizes) < K1:
         raise InvalidInputError("first-columns init needs N >= K")
-    D0 = init_dictionaries(S, K1, "first-columns", seeds[:L])
-    # locals: GPU-bound launches, eager (host launch overhead hides behind them)
-    Dl, codes, _ = train_device(S, D0, local_cap, local_eps, local_iters, use_tc, use_graph=False)
-    w = E.code_energy(S, codes)
-    w_h = E.d2h(w)                       # synchronises: end of the split phase
-    t_local = time.perf_counter()
+    G = max(1, min(int(groups), L))
+    bounds = [(g * L) // G for g in range(G + 1)]
+    main = torch.cuda.current_stream()
+    copy, *work = _streams(G + 1)
+    ready = []
+    copy.wait_stream(main)   # perm (and a device source) are ready
+    with torch.cuda.stream(copy):
+        for g in range(G):
+            r0, r1 = int(offs[bounds[g]]), int(offs[bounds[g + 1]])
+            if host_f64 is not None:
+                Ys = E.ingest_gather(host_f64, m, perm, r0, r1, m, prec, bad[g:g + 1])
+            else:
+                Ys = E.gather_rows(src, perm[r0:r1], prec)
+            ev = torch.cuda.Event()
+            ev.record(copy)
+            ready.append((Ys, ev))
+    outD, outw = [], []
+    for g in range(G):
+        a, b = bounds[g], bounds[g + 1]
+        s = work[g]
+        Ys, ev = ready[g]
+        if host_f64 is not None:
+            ev.synchronize()  # validate the group's rows before any compute on them
+            if int(bad[g].item()):
+                raise InvalidInputError("batch contains non-finite entries")
+        s.wait_event(ev)
+        Ys.record_stream(s)
+        with torch.cuda.stream(s):
+            off, _ = E.shard_offsets(sizes[a:b])
+            S = E.ShardSet(Ys, off, sizes[a:b], prec)
+            D0 = init_dictionaries(S, K1, "first-columns", seeds[a:b])
+            Dl, codes, _ = train_device(S, D0, local_cap, local_eps, local_iters, use_tc,
+                                        use_graph=False)
+            w = E.code_energy(S, codes)
+        Dl.record_stream(main)
+        w.record_stream(main)
+        outD.append(Dl)
+        outw.append(w)
+    for s in work:
+        main.wait_stream(s)
+    if G == 1:
+        return outD[0], outw[0]
+    return torch.cat(outD), torch.cat(outw)
+
+
+def _merge(Dl: torch.Tensor, w: torch.Tensor, K1: int, m: int, K: int, s2: int, merge_iters: int,
+           seed_merge: int, init, prec: str, use_tc: bool):
+    """merge_dictionaries (trainer.py:236-260) on the device-resident locals."""
+    L = Dl.shape[0]
+    w_h = E.d2h(w)
     keep = np.flatnonzero(w_h > 0.0)
     if keep.size == 0:
         raise InvalidInputError("all local code matrices are zero")
@@ -475,13 +520,64 @@ def split_merge_device(Ydev: torch.Tensor, L: int, K1: int, local_cap: int, loca
     Ym = E.scale_rows(Dk, wk, K1, prec)
     cap2, _ = coding_mode(m, K, s2, None, None)
     Sm = E.ShardSet.single(Ym, prec)
-    D0m = init_dictionaries(Sm, K, init, [seeds[L]])
+    D0m = init_dictionaries(Sm, K, init, [seed_merge])
     Dm, _codes_m, _ = train_device(Sm, D0m, cap2, 0.0, merge_iters, use_tc)
+    return Dm, w_h, Ym.shape[0]
+
+
+def split_merge_device(Ydev: torch.Tensor, L: int, K1: int, local_cap: int, local_eps: float,
+                       local_iters: int, K: int, s2: int, merge_iters: int, seed: int,
+                       init="first-columns", prec: str = "fp64", use_tc: bool = True,
+                       t_start: float | None = None, perm: torch.Tensor | None = None,
+                       groups: int = 1) -> SplitMergeResult:
+    """split_dataset -> locals (all shards batched, optionally in ``groups``
+    concurrent shard groups) -> merge (trainer.py:291-313). ``Ydev`` is
+    (N, m) device, signal-major."""
+    if t_start is None:
+        _sync()
+        t_start = time.perf_counter()
+    N, m = Ydev.shape
+    if not 1 <= L <= N:
+        raise InvalidInputError("require 1 <= L <= N")
+    # split_indices' blocks are consecutive slices of one PCG64 permutation
+    # (native, bit-identical to numpy; ``perm`` may be precomputed by the caller)
+    if perm is None:
+        perm = E.split_permutation(N, seed)
+    t_split = time.perf_counter()
+    seeds = _derive_seeds(seed, L + 1)
+    Dl, w = _split_locals(Ydev, N, m, L, K1, local_cap, local_eps, local_iters, seeds, perm, prec,
+                          use_tc, groups)
+    w_h = E.d2h(w)                       # synchronises: end of the split phase
+    t_local = time.perf_counter()
+    Dm, w_h, n_merge = _merge(Dl, w, K1, m, K, s2, merge_iters, seeds[L], init, prec, use_tc)
     _sync()
     t_end = time.perf_counter()
-    codings = (local_iters + 1) * N + (merge_iters + 1) * Ym.shape[0]
+    codings = (local_iters + 1) * N + (merge_iters + 1) * n_merge
     return SplitMergeResult(E.d2h(Dm[0]).T.copy(), Dm, Dl, w_h, t_split - t_start,
                             t_local - t_split, t_end - t_local, t_end - t_start, codings)
+
+
+HOST_GROUPS = int(os.environ.get("SDB_HOST_GROUPS", "4"))  # shard groups streamed from pinned host memory
+
+
+def _split_merge_host(src: int, N: int, m: int, cfg, cap1: int, eps1: float, local_iters: int,
+                      merge_iters: int, prec: str, t0: float) -> SplitMergeResult:
+    """train_split_merge's device pipeline for pinned host input (``src``:
+    device address of the f64 N x m rows)."""
+    perm = E.split_permutation(N, cfg.seed)
+    t_split = time.perf_counter()
+    seeds = _derive_seeds(cfg.seed, cfg.L + 1)
+    bad = E.zeros((max(1, HOST_GROUPS),), torch.int32)  # one non-finite flag per group
+    Dl, w = _split_locals(None, N, m, cfg.L, cfg.K1, cap1, eps1, local_iters, seeds, perm, prec,
+                          True, HOST_GROUPS, host_f64=src, bad=bad)
+    t_local = time.perf_counter()
+    Dm, w_h, n_merge = _merge(Dl, w, cfg.K1, m, cfg.K, cfg.s2, merge_iters, seeds[cfg.L],
+                              cfg.init, prec, True)
+    _sync()
+    t_end = time.perf_counter()
+    codings = (local_iters + 1) * N + (merge_iters + 1) * n_merge
+    return SplitMergeResult(E.d2h(Dm[0]).T.copy(), Dm, Dl, w_h, t_split - t0, t_local - t_split,
+                            t_end - t_local, t_end - t0, codings)
 
 
 def train_split_merge(Y, cfg: TrainConfig, evaluate: bool = True) -> tuple[np.ndarray, TrainReport]:
@@ -503,17 +599,26 @@ def train_split_merge(Y, cfg: TrainConfig, evaluate: bool = True) -> tuple[np.nd
     cap1, eps1 = coding_mode(m, cfg.K1, cfg.s1, cfg.eps, cfg.s_max)
     _sync()
     t0 = time.perf_counter()
-    # the split permutation (host, native) runs while Y streams to the device
-    from concurrent.futures import ThreadPoolExecutor
-    with ThreadPoolExecutor(max_workers=1) as ex:
-        fut = ex.submit(E.split_permutation, N, cfg.seed)
-        Ydev = _ingest_checked(Y, prec)
-        perm = fut.result()
-    r = split_merge_device(Ydev, cfg.L, cfg.K1, cap1, eps1, local_iters, cfg.K, cfg.s2,
-                           merge_iters, cfg.seed, cfg.init, prec, t_start=t0, perm=perm)
+    src = E.host_mapped(Y.T) if Y.T.flags.c_contiguous else None
+    Ydev = None
+    if src is not None:
+        # pinned, signal-major host input: each shard group's rows cross PCIe
+        # directly in permuted order and the group trains as soon as they land
+        r = _split_merge_host(src, N, m, cfg, cap1, eps1, local_iters, merge_iters, prec, t0)
+    else:
+        # the split permutation (host, native) runs while Y streams to the device
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=1) as ex:
+            fut = ex.submit(E.split_permutation, N, cfg.seed)
+            Ydev = _ingest_checked(Y, prec)
+            perm = fut.result()
+        r = split_merge_device(Ydev, cfg.L, cfg.K1, cap1, eps1, local_iters, cfg.K, cfg.s2,
+                               merge_iters, cfg.seed, cfg.init, prec, t_start=t0, perm=perm)
     # evaluation pass (trainer.py:315-319), outside wall_time_s
     mse = float("nan")
     if evaluate:
+        if Ydev is None:
+            Ydev = _ingest_checked(Y, prec)
         S = E.ShardSet.single(Ydev, prec)
         cap_e, _ = coding_mode(m, cfg.K, cfg.s, None, None)
         codes = E.code_single_dict(Ydev, r.D_dev, cap_e, 0.0, prec)

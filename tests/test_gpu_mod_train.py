@@ -196,3 +196,55 @@ def test_device_split_permutation_equals_numpy(n):
     for seed in (0, 1234):
         got = E.d2h(E.split_permutation(n, seed))
         assert np.array_equal(got, np.random.default_rng(seed).permutation(n))
+
+
+def _c1_like(N=12000, m=32, K=64, seed=3):
+    rng = np.random.default_rng(seed)
+    D = rng.standard_normal((m, K)); D /= np.linalg.norm(D, axis=0)
+    X = np.zeros((K, N))
+    for i in range(N):
+        X[rng.choice(K, 3, replace=False), i] = rng.standard_normal(3)
+    return D @ X + 0.01 * rng.standard_normal((m, N))
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+def test_grouped_locals_equal_batched(prec):
+    """Shard groups on separate streams == all shards in one batch, bitwise."""
+    import torch
+    from paper_1403_4781_b200 import _engine as E
+    from paper_1403_4781_b200.trainer import split_merge_device
+    Y = _c1_like()
+    Ydev, _ = E.ingest_signals(Y, prec)
+    out = []
+    for groups in (1, 3, 4):
+        r = split_merge_device(Ydev, 6, 64, 3, 0.0, 4, 64, 2, 3, 77, prec=prec, groups=groups)
+        out.append((E.d2h(r.local_D), r.weights, r.D))
+    for Dl, w, D in out[1:]:
+        assert np.array_equal(Dl, out[0][0])
+        assert np.array_equal(w, out[0][1])
+        assert np.array_equal(D, out[0][2])
+
+
+def test_pinned_host_input_streams_and_matches():
+    """train_split_merge on pinned host memory (rows gathered over PCIe per
+    shard group) == the same call on pageable memory."""
+    import torch
+    import paper_1403_4781_b200 as sdb
+    from paper_1403_4781_b200 import _engine as E
+    Y = _c1_like()
+    m, N = Y.shape
+    pinned = torch.empty((N, m), dtype=torch.float64, pin_memory=True)
+    pinned.numpy()[:] = Y.T
+    assert E.host_mapped(pinned.numpy()) is not None
+    assert E.host_mapped(np.ascontiguousarray(Y.T)) is None
+    cfg = sdb.TrainConfig(K=64, s=6, mode="split-merge", L=6, K1=64, s1=3, s2=2, iterations=4,
+                          seed=5, precision="fp32")
+    D_pin, rep_pin = sdb.train_split_merge(pinned.numpy().T, cfg)
+    D_pag, rep_pag = sdb.train_split_merge(np.asfortranarray(Y), cfg)
+    assert np.array_equal(D_pin, D_pag)
+    assert rep_pin.final_mse_db == rep_pag.final_mse_db
+    bad = pinned.numpy().copy()
+    pinned.numpy()[7, 3] = np.nan
+    with pytest.raises(sdb.InvalidInputError):
+        sdb.train_split_merge(pinned.numpy().T, cfg)
+    pinned.numpy()[:] = bad
