@@ -482,6 +482,8 @@ k_omp_fast(OmpArgs<float> a) {
     const float* __restrict__ Dp = a.D + (int64_t)p * K * m;
 
     const float* arow_n = a.alpha0 + i_begin * a.lda;   // advanced by lda per signal
+    int32_t* code_idx = a.idx + i_begin * cap;         // this signal's code row (advanced by cap)
+    float* code_val = a.val + i_begin * cap;
     const float* yrow_n = a.Y + i_begin * a.ldy + lane;
     // the next signal's alpha0 row and y are prefetched into L1 (no registers
     // held across the signal, which keeps occupancy at 4 blocks / SM)
@@ -531,7 +533,7 @@ k_omp_fast(OmpArgs<float> a) {
         } else {
             ysq = signal_sq<MPL>(yrow, lane, m);
         }
-        float rnorm = __fsqrt_rn(ysq);
+        float rnorm = 0.0f;  // formed only when reported or needed near the threshold
         float rsq = ysq;
         int n = 0, status = 0;
         // explicit ||y - D_S x|| (support columns read from L2, independent loads)
@@ -553,7 +555,7 @@ k_omp_fast(OmpArgs<float> a) {
             for (int q = 0; q < MPL; ++q) rs = fmaf(rr[q], rr[q], rs);
             return __fsqrt_rn(warp_sum(rs));
         };
-        if (!(rnorm <= eps || rnorm == 0.0f)) {
+        if (!(ysq <= eps2 || ysq == 0.0f)) {  // ||y|| <= eps: no atom
             for (int step = 0; step < cap; ++step) {
                 // ---- correlations of the residual, support excluded
                 float v[KPL];
@@ -644,14 +646,16 @@ k_omp_fast(OmpArgs<float> a) {
                     break;
                 }
             }
-            // reported norm (when requested): explicit residual of the final support
-            if (a.rnorm && n > 0) rnorm = resid_norm(n);
         }
+        // reported norm (when requested): explicit residual of the final support
+        if (a.rnorm) rnorm = (n > 0) ? resid_norm(n) : __fsqrt_rn(ysq);
         __syncwarp();
         if (lane < cap) {
-            a.idx[i * cap + lane] = (lane < n) ? ids[lane] : 0;
-            a.val[i * cap + lane] = (lane < n) ? xs[lane] : 0.0f;
+            code_idx[lane] = (lane < n) ? ids[lane] : 0;
+            code_val[lane] = (lane < n) ? xs[lane] : 0.0f;
         }
+        code_idx += cap;
+        code_val += cap;
         if (lane == 0) {
             a.counts[i] = n;
             a.status[i] = (int8_t)status;
