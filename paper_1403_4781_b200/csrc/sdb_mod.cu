@@ -261,17 +261,20 @@ k_xxt(int P, int K, int cap, const int32_t* __restrict__ idx, const T* __restric
         const double my_v = lane < nbat ? (double)val[my_e] : 0.0;
         const int my_n = lane < nbat ? counts[my_sig] : 0;
         if (staged) {
-            for (int t = 0; t < my_n; ++t) {
+            // a single-atom code row holds only this bucket's atom: its whole
+            // contribution is the diagonal term, so its row is not read
+            const int my_no = my_n > 1 ? my_n : 0;
+            for (int t = 0; t < my_no; ++t) {
                 sidx[t * 32 + lane] = idx[(int64_t)my_sig * cap + t];
                 sval[t * 32 + lane] = (double)val[(int64_t)my_sig * cap + t];
             }
             __syncwarp();
             diag += warp_sum(my_v * my_v);
-            const int nmax = (int)__reduce_max_sync(SDB_FULL, (unsigned)my_n);
+            const int nmax = (int)__reduce_max_sync(SDB_FULL, (unsigned)my_no);
             for (int t = 0; t < nmax; ++t) {
                 int b = -1;
                 double c = 0.0;
-                if (t < my_n) {
+                if (t < my_no) {
                     b = sidx[t * 32 + lane];
                     c = my_v * sval[t * 32 + lane];
                     if (b == self) b = -1;  // diagonal: summed above
