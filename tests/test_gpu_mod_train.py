@@ -248,3 +248,26 @@ def test_pinned_host_input_streams_and_matches():
     with pytest.raises(sdb.InvalidInputError):
         sdb.train_split_merge(pinned.numpy().T, cfg)
     pinned.numpy()[:] = bad
+
+
+@pytest.mark.parametrize("K", [100, 130, 200, 255])
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_mod_cluster_solve_partial_blocks(K, prec):
+    """The clustered Cholesky with 2-4 CTAs per shard and a partial last
+    64-row block agrees with the oracle's lstsq MOD."""
+    import sys
+    sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parent.parent))
+    from oracle import oracle as O
+    import paper_1403_4781_b200 as sdb
+    rng = np.random.default_rng(K)
+    m, N = 48, 6 * K
+    Dp = rng.standard_normal((m, K)); Dp /= np.linalg.norm(Dp, axis=0)
+    Y = rng.standard_normal((m, N))
+    X, _ = O.omp_codes(Y, Dp, s=6)
+    Xs = sdb.SparseCodeMatrix(K, X[1], X[2], X[3])
+    D, dg = sdb.mod_update(Y, Xs, Dp, precision=prec)
+    Dr, resid, unused, _rank, _norms = O.mod_update(Y, X, Dp)
+    tol = 1e-9 if prec == "fp64" else 2e-4
+    np.testing.assert_allclose(D, Dr, rtol=0, atol=tol)
+    assert dg.unused_atoms == list(unused)
+    assert dg.residual_fro == pytest.approx(resid, rel=1e-9 if prec == "fp64" else 1e-5)
