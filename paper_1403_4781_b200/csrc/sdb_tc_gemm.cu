@@ -5,16 +5,13 @@
 //   y = y_hi + y_lo, d = d_hi + d_lo (hi = tf32 round-to-nearest)
 //   alpha0 ~= y_hi.d_hi + y_hi.d_lo + y_lo.d_hi   (FP32 accumulation in TMEM)
 //
-// One CTA (4 warps) per (128-signal tile, 256-atom chunk, shard):
-//   * TMA (cp.async.bulk.tensor, 128B swizzle) streams 32-wide k-blocks of Y
-//     (fp32) and of the pre-split D_hi / D_lo into a 2-stage smem ring
-//     guarded by mbarriers;
-//   * the CTA splits its Y k-block into hi/lo in place (element-wise, so the
-//     swizzled layout is preserved), fences the async proxy;
-//   * one elected thread issues 4 k-steps x 3 tcgen05.mma.kind::tf32
-//     (M=128, N=256, K=8) into a 256-column TMEM accumulator and commits to
-//     the stage's mbarrier;
-//   * epilogue: tcgen05.ld 32x32b (thread = signal row) -> global.
+// Work item = (128-signal tile, 256-atom chunk, shard): TMA
+// (cp.async.bulk.tensor, 128B swizzle) streams 32-wide k-blocks of Y (fp32)
+// and of the pre-split D_hi / D_lo into a 2-stage smem ring guarded by
+// mbarriers; the Y k-block is split into hi/lo in place (element-wise, so the
+// swizzled layout is preserved); one elected thread issues 4 k-steps x 3
+// tcgen05.mma.kind::tf32 (M=128, N=256, K=8) into a TMEM accumulator; the
+// epilogue drains TMEM through swizzled smem into TMA stores.
 #include <cuda.h>
 
 #include <cstdint>
@@ -35,7 +32,6 @@ constexpr int STAGES = 2;
 constexpr int A_BYTES = TM * KB * 4;   // 16 KB
 constexpr int B_BYTES = TN * KB * 4;   // 32 KB
 constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // A_hi, A_lo, B_hi, B_lo
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256 + 4 * 32 * 33 * 4;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -98,146 +94,6 @@ __device__ __forceinline__ float tf32_rna(float x) {
 }
 
 }  // namespace
-
-__global__ void __launch_bounds__(128, 1)
-k_corr_tc(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmDh,
-          const __grid_constant__ CUtensorMap tmDl, const int64_t* __restrict__ off, int K, int nkb,
-          float* __restrict__ alpha, int64_t lda) {
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
-    const int p = blockIdx.z;
-    const int64_t s_lo = off[p], s_hi = off[p + 1];
-    const int64_t row0 = s_lo + (int64_t)blockIdx.x * TM;
-    if (row0 >= s_hi) return;
-    const int n0 = blockIdx.y * TN;
-    if (n0 >= K) return;
-
-    unsigned char* base = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint64_t* bars = (uint64_t*)(base + STAGES * STAGE_BYTES);   // full[2], mma_done[2]
-    uint32_t* tmem_slot = (uint32_t*)(bars + 2 * STAGES);
-    const int tid = threadIdx.x, warp = tid >> 5;
-
-    if (tid == 0) {
-        for (int s = 0; s < 2 * STAGES; ++s) mbar_init(smem_u32(&bars[s]), 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                         smem_u32(tmem_slot)),
-                     "r"(TN));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tmem = *tmem_slot;
-
-    // UMMA instruction descriptor: D f32, A/B tf32, K-major, M=128, N=256
-    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TN >> 3) << 17) |
-                           ((uint32_t)(TM >> 4) << 24);
-    const int64_t d_row0 = (int64_t)p * K + n0;  // row in the (P*K, m_pad) D arrays
-
-    auto stage_ptr = [&](int s, int which) -> unsigned char* {
-        // which: 0 A_hi, 1 A_lo, 2 B_hi, 3 B_lo
-        unsigned char* st = base + s * STAGE_BYTES;
-        return which == 0 ? st : which == 1 ? st + A_BYTES : which == 2 ? st + 2 * A_BYTES
-                                                                       : st + 2 * A_BYTES + B_BYTES;
-    };
-    auto issue = [&](int kb) {
-        const int s = kb % STAGES;
-        const uint32_t full = smem_u32(&bars[s]);
-        mbar_expect_tx(full, A_BYTES + 2 * B_BYTES);
-        tma_load_2d(smem_u32(stage_ptr(s, 0)), &tmY, kb * KB, (int)row0, full);
-        tma_load_2d(smem_u32(stage_ptr(s, 2)), &tmDh, kb * KB, (int)d_row0, full);
-        tma_load_2d(smem_u32(stage_ptr(s, 3)), &tmDl, kb * KB, (int)d_row0, full);
-    };
-
-    if (tid == 0) issue(0);
-    for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % STAGES;
-        // prefetch the next k-block once the MMAs that last read its stage are done
-        if (tid == 0 && kb + 1 < nkb) {
-            const int s1 = (kb + 1) % STAGES;
-            if (kb + 1 >= STAGES) mbar_wait(smem_u32(&bars[STAGES + s1]), ((kb + 1) / STAGES - 1) & 1);
-            issue(kb + 1);
-        }
-        mbar_wait(smem_u32(&bars[s]), (kb / STAGES) & 1);
-        // split the Y block: hi in place, lo beside it (position-preserving)
-        float4* ah = (float4*)stage_ptr(s, 0);
-        float4* al = (float4*)stage_ptr(s, 1);
-        for (int e = tid; e < A_BYTES / 16; e += 128) {
-            const float4 v = ah[e];
-            float4 h, l;
-            h.x = tf32_rna(v.x); l.x = v.x - h.x;
-            h.y = tf32_rna(v.y); l.y = v.y - h.y;
-            h.z = tf32_rna(v.z); l.z = v.z - h.z;
-            h.w = tf32_rna(v.w); l.w = v.w - h.w;
-            ah[e] = h;
-            al[e] = l;
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncthreads();
-        if (tid == 0) {
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint64_t dah = sw128_desc(smem_u32(stage_ptr(s, 0)));
-            const uint64_t dal = sw128_desc(smem_u32(stage_ptr(s, 1)));
-            const uint64_t dbh = sw128_desc(smem_u32(stage_ptr(s, 2)));
-            const uint64_t dbl = sw128_desc(smem_u32(stage_ptr(s, 3)));
-#pragma unroll
-            for (int k = 0; k < KB / 8; ++k) {
-                const uint64_t adv = (uint64_t)((k * 8 * 4) >> 4);  // 32 bytes per k-step
-                const uint32_t acc0 = (kb > 0 || k > 0) ? 1u : 0u;
-                mma_tf32(tmem, dah + adv, dbh + adv, idesc, acc0);
-                mma_tf32(tmem, dah + adv, dbl + adv, idesc, 1u);
-                mma_tf32(tmem, dal + adv, dbh + adv, idesc, 1u);
-            }
-            mma_commit(smem_u32(&bars[STAGES + s]));
-        }
-    }
-    // wait for the last commit, then drain TMEM
-    {
-        const int kl = nkb - 1;
-        mbar_wait(smem_u32(&bars[STAGES + kl % STAGES]), (kl / STAGES) & 1);
-    }
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int r = warp * 32 + (tid & 31);
-    const int64_t grow = row0 + r;
-    const bool row_ok = grow < s_hi;
-    float* out = alpha + grow * lda;
-#pragma unroll 1
-    for (int c = 0; c < TN; c += 32) {
-        uint32_t v[32];
-        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c;
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-            "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-              "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
-              "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
-              "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-            : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (row_ok) {
-            const int j0 = n0 + c;
-            if (j0 + 32 <= K && ((lda & 3) == 0)) {
-                float4* o4 = (float4*)(out + j0);
-#pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    o4[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
-                                        __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
-            } else {
-#pragma unroll
-                for (int q = 0; q < 32; ++q)
-                    if (j0 + q < K) out[j0 + q] = __uint_as_float(v[q]);
-            }
-        }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (warp == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TN));
-}
 
 // ----------------------------------------------------------------------------
 // Persistent, warp-specialised version (the one used): one CTA per SM owns a
@@ -629,7 +485,6 @@ int correlate_tc_f32(int64_t N, const float* Y, int64_t ldy, const int64_t* off,
     static bool attr = false;
     static int n_sm = 148;
     if (!attr) {
-        cudaFuncSetAttribute(k_corr_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
         cudaFuncSetAttribute(k_corr_tc2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES);
         cudaFuncSetAttribute(k_corr_tc2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES);
         int dev = 0;
