@@ -283,7 +283,7 @@ def main():
                 "algorithmic_bytes_per_signal": (4 * cfg["K1"] + 4 + 8 * cap + 5) if dom == "omp"
                 else 4 * (m + cfg["K1"]),
                 "traffic_note": "ncu dram read+write of one C2 local-pass launch (2,040,200 signals), "
-                                "profiles/ncu_*_r01b_raw.txt"}
+                                "profiles/ncu_*_r01c_raw.txt"}
     gemm = None
     if "correlate" in kt:
         evs = kt["correlate"]
