@@ -175,26 +175,42 @@ k_place(const int64_t* __restrict__ off, const int64_t* __restrict__ cf, int P, 
     }
 }
 
-// ---- (f) B[p][a][:] = sum over bucket (y_i * x_ai). One CTA per (p, a):
-// warp w takes the bucket's 32-entry batches w, w+8, ... (entries fetched one
-// per lane, broadcast, four signal rows in flight); the 8 partial sums are
-// combined in warp order, so the result is a fixed function of the input.
+// ---- (f+g) both normal-equation rows of one bucket in one pass. CTA per
+// (shard p, atom a), 8 warps; warp w takes the bucket's 32-entry batches
+// w, w+8, ... and per batch
+//   B[p][a][:] += sum y_i x_ai   (four signal rows in flight, as k_yxt),
+//   A[p][a][:] += sum x_ai x_i   (diagonal as one warp sum; the other atoms
+//                                 of multi-atom code rows in lane-parallel
+//                                 rounds, collisions in lane order, as k_xxt)
+// so the X X^T work hides under the Y-row gathers and the bucket is read
+// once. Per-warp partials are combined in warp order: the result is a fixed
+// function of the input (bitwise that of the separate kernels).
 template <typename T, int MPL>
 __global__ void __launch_bounds__(256)
-k_yxt(int P, int K, int m, const T* __restrict__ Y, int64_t ldy, const int64_t* __restrict__ bucket_off,
-      int cap, const T* __restrict__ val, const int32_t* __restrict__ bent, double* __restrict__ B) {
-    __shared__ double part[8][MPL * 32];
+k_normal_eq(int P, int K, int m, const T* __restrict__ Y, int64_t ldy, const int64_t* __restrict__ bucket_off,
+            int cap, const int32_t* __restrict__ idx, const T* __restrict__ val,
+            const int32_t* __restrict__ counts, const int32_t* __restrict__ bent, double* __restrict__ B,
+            double* __restrict__ A) {
+    extern __shared__ double sh_row[];  // 8 warps x K (X X^T row partials), then 8 x 32*MPL (Y X^T)
+    double (*part)[MPL * 32] = reinterpret_cast<double (*)[MPL * 32]>(sh_row + 8 * (int64_t)K);
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t e = blockIdx.x;  // (p, a)
+    const int self = (int)(e % K);
+    double* row = sh_row + (int64_t)wib * K;
+    for (int b = lane; b < K; b += 32) row[b] = 0.0;
+    __syncwarp();
     double acc[MPL];
 #pragma unroll
     for (int q = 0; q < MPL; ++q) acc[q] = 0.0;
+    double diag = 0.0;
     const int64_t lo = bucket_off[e], hi = bucket_off[e + 1];
     for (int64_t b0 = lo + 32 * wib; b0 < hi; b0 += 32 * 8) {
         const int nbat = (int)min((int64_t)32, hi - b0);
         const int my_e = lane < nbat ? bent[b0 + lane] : 0;
         const int my_sig = my_e / cap;
         const double my_val = lane < nbat ? (double)val[my_e] : 0.0;
+        const int my_n = lane < nbat ? counts[my_sig] : 0;
+        // Y X^T
         for (int j = 0; j < nbat; j += 4) {
             double yv[4][MPL];
             double vv[4];
@@ -214,102 +230,47 @@ k_yxt(int P, int K, int m, const T* __restrict__ Y, int64_t ldy, const int64_t* 
 #pragma unroll
                 for (int q = 0; q < MPL; ++q) acc[q] = fma(yv[u][q], vv[u], acc[q]);
         }
+        // X X^T: a single-atom code row holds only this bucket's atom, whose
+        // contribution is the diagonal term
+        diag += warp_sum(my_val * my_val);
+        const int my_no = my_n > 1 ? my_n : 0;
+        const int nmax = (int)__reduce_max_sync(SDB_FULL, (unsigned)my_no);
+        for (int t = 0; t < nmax; ++t) {
+            int b = -1;
+            double c = 0.0;
+            if (t < my_no) {
+                b = idx[(int64_t)my_sig * cap + t];
+                c = my_val * (double)val[(int64_t)my_sig * cap + t];
+                if (b == self) b = -1;  // diagonal: summed above
+            }
+            const bool act = b >= 0;
+            const unsigned peers = __match_any_sync(SDB_FULL, act ? b : K + lane);
+            const int rank = __popc(peers & ((1u << lane) - 1u));
+            const int gmax = (int)__reduce_max_sync(SDB_FULL, act ? (unsigned)__popc(peers) : 0u);
+            for (int r = 0; r < gmax; ++r) {
+                if (act && rank == r) row[b] += c;
+                __syncwarp();
+            }
+        }
+        __syncwarp();
     }
+    if (lane == 0) row[self] += diag;
 #pragma unroll
     for (int q = 0; q < MPL; ++q) part[wib][lane + 32 * q] = acc[q];
     __syncthreads();
-    double* out = B + e * m;
+    double* outB = B + e * m;
     for (int r = threadIdx.x; r < m; r += 256) {
         double t = 0.0;
 #pragma unroll
         for (int w = 0; w < 8; ++w) t += part[w][r];
-        out[r] = t;
+        outB[r] = t;
     }
-}
-
-// ---- (g) A[p][a][:] = sum over bucket (x_ai * x_i). One CTA per (p, a);
-// warp w accumulates batches w, w+8, ... into its own smem row, rows combined
-// in warp order. Within a batch each lane owns one signal and the warp walks
-// the code rows in uniform rounds t: the diagonal term (every signal of the
-// bucket has x_a) is one warp sum per batch; off-diagonal entries colliding
-// on the same column in a round are applied in ascending lane order
-// (match.any). Every update order is a fixed function of the input.
-constexpr int XXT_CAP = 32;
-
-template <typename T>
-__global__ void __launch_bounds__(256)
-k_xxt(int P, int K, int cap, const int32_t* __restrict__ idx, const T* __restrict__ val,
-      const int32_t* __restrict__ counts, const int64_t* __restrict__ bucket_off,
-      const int32_t* __restrict__ bent, double* __restrict__ A) {
-    extern __shared__ double sh_row[];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int64_t e = blockIdx.x;
-    const int self = (int)(e % K);
-    double* row = sh_row + (int64_t)wib * K;
-    const bool staged = cap <= XXT_CAP;
-    const int rows = staged ? cap : 0;
-    int32_t* sidx = (int32_t*)(sh_row + 8 * (int64_t)K) + wib * 32 * rows;            // [t][lane]
-    double* sval = (double*)(sh_row + 8 * (int64_t)K + 4 * 32 * rows) + wib * 32 * rows;  // [t][lane]
-    for (int b = lane; b < K; b += 32) row[b] = 0.0;
-    __syncwarp();
-    const int64_t lo = bucket_off[e], hi = bucket_off[e + 1];
-    double diag = 0.0;
-    for (int64_t q0 = lo + 32 * wib; q0 < hi; q0 += 32 * 8) {
-        const int nbat = (int)min((int64_t)32, hi - q0);
-        const int my_e = lane < nbat ? bent[q0 + lane] : 0;
-        const int my_sig = my_e / cap;
-        const double my_v = lane < nbat ? (double)val[my_e] : 0.0;
-        const int my_n = lane < nbat ? counts[my_sig] : 0;
-        if (staged) {
-            // a single-atom code row holds only this bucket's atom: its whole
-            // contribution is the diagonal term, so its row is not read
-            const int my_no = my_n > 1 ? my_n : 0;
-            for (int t = 0; t < my_no; ++t) {
-                sidx[t * 32 + lane] = idx[(int64_t)my_sig * cap + t];
-                sval[t * 32 + lane] = (double)val[(int64_t)my_sig * cap + t];
-            }
-            __syncwarp();
-            diag += warp_sum(my_v * my_v);
-            const int nmax = (int)__reduce_max_sync(SDB_FULL, (unsigned)my_no);
-            for (int t = 0; t < nmax; ++t) {
-                int b = -1;
-                double c = 0.0;
-                if (t < my_no) {
-                    b = sidx[t * 32 + lane];
-                    c = my_v * sval[t * 32 + lane];
-                    if (b == self) b = -1;  // diagonal: summed above
-                }
-                const bool act = b >= 0;
-                const unsigned peers = __match_any_sync(SDB_FULL, act ? b : K + lane);
-                const int rank = __popc(peers & ((1u << lane) - 1u));
-                const int gmax = (int)__reduce_max_sync(SDB_FULL, act ? (unsigned)__popc(peers) : 0u);
-                for (int r = 0; r < gmax; ++r) {
-                    if (act && rank == r) row[b] += c;
-                    __syncwarp();
-                }
-            }
-            __syncwarp();
-        } else {
-            for (int j = 0; j < nbat; ++j) {
-                const double v = __shfl_sync(SDB_FULL, my_v, j);
-                const int n = __shfl_sync(SDB_FULL, my_n, j);
-                const int i = __shfl_sync(SDB_FULL, my_sig, j);
-                for (int t = lane; t < n; t += 32) {
-                    const int b = idx[(int64_t)i * cap + t];
-                    row[b] = fma(v, (double)val[(int64_t)i * cap + t], row[b]);
-                }
-                __syncwarp();
-            }
-        }
-    }
-    if (staged && lane == 0) row[self] += diag;
-    __syncthreads();
-    double* out = A + e * K;
+    double* outA = A + e * K;
     for (int b = threadIdx.x; b < K; b += 256) {
         double t = 0.0;
 #pragma unroll
         for (int w = 0; w < 8; ++w) t += sh_row[(int64_t)w * K + b];
-        out[b] = t;
+        outA[b] = t;
     }
 }
 
@@ -774,18 +735,14 @@ int mod_update(const ModArgs<T>& a, cudaStream_t st) {
     }
     rc = with_mpl(m, [&](auto c) {
         constexpr int MPL = decltype(c)::value;
-        k_yxt<T, MPL><<<(unsigned)PK, 256, 0, st>>>(P, K, m, a.Y, a.ldy, w.bucket_off,
-                                                               cap, a.val, w.bent, w.B);
+        const int smem = 8 * (K + 32 * MPL) * (int)sizeof(double);
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(k_normal_eq<T, MPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        k_normal_eq<T, MPL><<<(unsigned)PK, 256, smem, st>>>(P, K, m, a.Y, a.ldy, w.bucket_off, cap, a.idx,
+                                                             a.val, a.counts, w.bent, w.B, w.A);
         return (int)cudaGetLastError();
     });
     if (rc) return rc;
-    {
-        const int smem = 8 * K * (int)sizeof(double) + (cap <= XXT_CAP ? 8 * 32 * cap * (4 + 8) : 0);
-        if (smem > 48 * 1024)
-            cudaFuncSetAttribute(k_xxt<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        k_xxt<T><<<(unsigned)PK, 256, smem, st>>>(P, K, cap, a.idx, a.val, a.counts,
-                                                             w.bucket_off, w.bent, w.A);
-    }
     // masked RHS rows of unused atoms are irrelevant: A is the identity there
     // and B holds zeros (their buckets are empty).
     rc = chol_solve(P, K, m, w.A, w.B, a.usage, a.rank_rcond, w.depmask, w.deficient, w.wsq, w.chol, st);

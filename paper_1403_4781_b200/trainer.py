@@ -460,6 +460,14 @@ def _split_locals(src, N: int, m: int, L: int, K1: int, local_cap: int, local_ep
     if min(sizes) < K1:
         raise InvalidInputError("first-columns init needs N >= K")
     G = max(1, min(int(groups), L))
+    if G == 1 and host_f64 is None:
+        # one batch on the caller's stream (no cross-stream allocations)
+        Ys = E.gather_rows(src, perm, prec)
+        off, _ = E.shard_offsets(sizes)
+        S = E.ShardSet(Ys, off, sizes, prec)
+        D0 = init_dictionaries(S, K1, "first-columns", seeds[:L])
+        Dl, codes, _ = train_device(S, D0, local_cap, local_eps, local_iters, use_tc, use_graph=False)
+        return Dl, E.code_energy(S, codes)
     bounds = [(g * L) // G for g in range(G + 1)]
     main = torch.cuda.current_stream()
     copy, *work = _streams(G + 1)
