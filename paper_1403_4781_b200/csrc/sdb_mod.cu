@@ -401,80 +401,87 @@ k_shard_sum(const int64_t* __restrict__ off, const double* __restrict__ v, doubl
     if (threadIdx.x == 0) out[p] = do_sqrt ? sqrt(sh[0]) : sh[0];
 }
 
-// ---- (i) finish MOD: norms, dead atoms, restore, normalise (dictionary_update.py:103-113)
-__global__ void __launch_bounds__(1024)
-k_mod_finish(int P, int K, int m, const double* __restrict__ Z, const double* __restrict__ Dprev,
-             const int32_t* __restrict__ usage, int64_t* __restrict__ nnz_shard,
-             double* __restrict__ Dout, double* __restrict__ scales, int8_t* __restrict__ dead,
-             int32_t* __restrict__ rank, const int32_t* __restrict__ deficient) {
-    __shared__ double s_max;
-    __shared__ int s_rank;
-    __shared__ long long s_nnz[32];
-    const int p = blockIdx.x;
+// ---- (i) finish MOD: norms, dead atoms, restore, normalise (dictionary_update.py:103-113),
+// in two wide launches (warp per atom, 8 atoms per CTA, grid = atom blocks x
+// shards): (1) column norms of the raw solution plus per-CTA partials of the
+// shard's max norm, used-atom count and code nonzeros; (2) each CTA reduces
+// its shard's partials (max / integer sums: order-free) and restores or
+// normalises its atoms.
+__global__ void __launch_bounds__(256)
+k_mod_norms(int P, int K, int m, const double* __restrict__ Z, const int32_t* __restrict__ usage,
+            double* __restrict__ scales, double* __restrict__ pmax, int64_t* __restrict__ pnnz,
+            int32_t* __restrict__ prank) {
+    __shared__ double smx[8];
+    __shared__ long long snz[8];
+    __shared__ int srk[8];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const double* Zp = Z + (int64_t)p * K * m;
-    if (threadIdx.x == 0) { s_max = 0.0; s_rank = 0; }
-    {   // nonzeros of the shard's codes = sum of its atom usages
-        long long u = 0;
-        for (int a = threadIdx.x; a < K; a += 1024) u += usage[(int64_t)p * K + a];
-        for (int o = 16; o > 0; o >>= 1) u += __shfl_xor_sync(SDB_FULL, u, o);
-        if (lane == 0) s_nnz[wib] = u;
-    }
-    __syncthreads();
-    long long nnz = 0;
-    for (int w = 0; w < 32; ++w) nnz += s_nnz[w];
-    if (threadIdx.x == 0) nnz_shard[p] = nnz;
-    const bool empty = nnz == 0;
-    // column norms of the raw solution
-    for (int a = wib; a < K; a += 32) {
+    const int p = blockIdx.y, nb = gridDim.x;
+    const int a = blockIdx.x * 8 + wib;
+    double nrm = 0.0;
+    int u = 0;
+    if (a < K) {
+        const double* z = Z + ((int64_t)p * K + a) * m;
         double s = 0.0;
-        for (int r = lane; r < m; r += 32) s = fma(Zp[(int64_t)a * m + r], Zp[(int64_t)a * m + r], s);
-        s = warp_sum(s);
-        if (lane == 0) scales[(int64_t)p * K + a] = sqrt(s);
+        for (int r = lane; r < m; r += 32) s = fma(z[r], z[r], s);
+        nrm = sqrt(warp_sum(s));
+        u = usage[(int64_t)p * K + a];
+        if (lane == 0) scales[(int64_t)p * K + a] = nrm;
     }
+    if (lane == 0) { smx[wib] = nrm; snz[wib] = u; srk[wib] = u > 0; }
     __syncthreads();
-    {
-        __shared__ double smx[1024];
-        __shared__ int srk[1024];
+    if (threadIdx.x == 0) {
         double mx = 0.0;
+        long long nz = 0;
         int rk = 0;
-        for (int a = threadIdx.x; a < K; a += 1024) {
-            mx = fmax(mx, scales[(int64_t)p * K + a]);
-            rk += usage[(int64_t)p * K + a] > 0;
+        for (int w = 0; w < 8; ++w) { mx = fmax(mx, smx[w]); nz += snz[w]; rk += srk[w]; }
+        const int64_t q = (int64_t)p * nb + blockIdx.x;
+        pmax[q] = mx; pnnz[q] = nz; prank[q] = rk;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+k_mod_apply(int P, int K, int m, const double* __restrict__ Z, const double* __restrict__ Dprev,
+            const int32_t* __restrict__ usage, const double* __restrict__ scales, const double* __restrict__ pmax,
+            const int64_t* __restrict__ pnnz, const int32_t* __restrict__ prank, int64_t* __restrict__ nnz_shard,
+            double* __restrict__ Dout, int8_t* __restrict__ dead, int32_t* __restrict__ rank,
+            const int32_t* __restrict__ deficient) {
+    __shared__ double s_max;
+    __shared__ long long s_nnz;
+    __shared__ int s_rank;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int p = blockIdx.y, nb = gridDim.x;
+    if (threadIdx.x == 0) {
+        double mx = 0.0;
+        long long nz = 0;
+        int rk = 0;
+        for (int b = 0; b < nb; ++b) {
+            const int64_t q = (int64_t)p * nb + b;
+            mx = fmax(mx, pmax[q]); nz += pnnz[q]; rk += prank[q];
         }
-        smx[threadIdx.x] = mx;
-        srk[threadIdx.x] = rk;
-        __syncthreads();
-        for (int w = 512; w > 0; w >>= 1) {
-            if (threadIdx.x < w) {
-                smx[threadIdx.x] = fmax(smx[threadIdx.x], smx[threadIdx.x + w]);
-                srk[threadIdx.x] += srk[threadIdx.x + w];
-            }
-            __syncthreads();
-        }
-        if (threadIdx.x == 0) {
-            s_max = smx[0];
-            s_rank = empty ? 0 : srk[0];
+        s_max = mx; s_nnz = nz; s_rank = rk;
+        if (blockIdx.x == 0) {
+            nnz_shard[p] = nz;
+            rank[p] = nz == 0 ? 0 : rk - deficient[p];
         }
     }
     __syncthreads();
+    const int a = blockIdx.x * 8 + wib;
+    if (a >= K) return;
+    const bool empty = s_nnz == 0;
     const double thr = 1e-12 * fmax(s_max, 1.0);
-    for (int a = wib; a < K; a += 32) {
-        const int64_t e = (int64_t)p * K + a;
-        const bool dd = empty || usage[e] == 0 || scales[e] <= thr;
-        if (lane == 0) dead[e] = dd ? 1 : 0;
-        const double* src = dd ? (Dprev + e * m) : (Zp + (int64_t)a * m);
-        double* dst = Dout + e * m;
-        if (empty) {  // all-zero codes: D_prev returned unchanged (:92-95)
-            for (int r = lane; r < m; r += 32) dst[r] = src[r];
-            continue;
-        }
-        double s = 0.0;
-        for (int r = lane; r < m; r += 32) s = fma(src[r], src[r], s);
-        const double nrm = sqrt(warp_sum(s));
-        for (int r = lane; r < m; r += 32) dst[r] = nrm > 0.0 ? src[r] / nrm : src[r];
+    const int64_t e = (int64_t)p * K + a;
+    const bool dd = empty || usage[e] == 0 || scales[e] <= thr;
+    if (lane == 0) dead[e] = dd ? 1 : 0;
+    const double* src = dd ? (Dprev + e * m) : (Z + e * m);
+    double* dst = Dout + e * m;
+    if (empty) {  // all-zero codes: D_prev returned unchanged (:92-95)
+        for (int r = lane; r < m; r += 32) dst[r] = src[r];
+        return;
     }
-    if (threadIdx.x == 0) rank[p] = empty ? 0 : s_rank - deficient[p];
+    double s = 0.0;
+    for (int r = lane; r < m; r += 32) s = fma(src[r], src[r], s);
+    const double nrm = sqrt(warp_sum(s));
+    for (int r = lane; r < m; r += 32) dst[r] = nrm > 0.0 ? src[r] / nrm : src[r];
 }
 
 // ---- replace_degenerate_atoms (dictionary_update.py:134-176)
@@ -694,6 +701,12 @@ ModWs carve_mod_ws(void* base, int P, int64_t N, int m, int K, int cap) {
     w.B = (double*)take(sizeof(double) * (int64_t)P * K * m);
     w.rsq = (double*)take(sizeof(double) * std::max<int64_t>(N, 1));
     w.nnz = (int64_t*)take(sizeof(int64_t) * P);
+    {
+        const int64_t nbp = (int64_t)P * ((K + 7) / 8);  // per-CTA partials of the MOD finish
+        w.fmax = (double*)take(sizeof(double) * nbp);
+        w.fnnz = (int64_t*)take(sizeof(int64_t) * nbp);
+        w.frank = (int32_t*)take(sizeof(int32_t) * nbp);
+    }
     w.deficient = (int32_t*)take(sizeof(int32_t) * P);
     w.depmask = (int8_t*)take((int64_t)P * K);
     w.chol = take(chol_ws_bytes(P, K));
@@ -769,8 +782,12 @@ int mod_update(const ModArgs<T>& a, cudaStream_t st) {
     });
     if (rc) return rc;
     k_shard_sum_masked<<<P, 256, 0, st>>>(a.off, w.rsq, w.need, a.resid_fro);
-    k_mod_finish<<<P, 1024, 0, st>>>(P, K, m, w.B, a.Dprev, a.usage, w.nnz, a.Dout, a.scales, a.dead,
-                                    a.rank, w.deficient);
+    {
+        const dim3 g((unsigned)((K + 7) / 8), (unsigned)P);
+        k_mod_norms<<<g, 256, 0, st>>>(P, K, m, w.B, a.usage, a.scales, w.fmax, w.fnnz, w.frank);
+        k_mod_apply<<<g, 256, 0, st>>>(P, K, m, w.B, a.Dprev, a.usage, a.scales, w.fmax, w.fnnz, w.frank,
+                                       w.nnz, a.Dout, a.dead, a.rank, w.deficient);
+    }
     if (a.deficient_out)
         cudaMemcpyAsync(a.deficient_out, w.deficient, sizeof(int32_t) * P, cudaMemcpyDeviceToDevice, st);
     if (a.nnz_out)

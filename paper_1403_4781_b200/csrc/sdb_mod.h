@@ -17,6 +17,9 @@ struct ModWs {
     double* B;
     double* rsq;
     int64_t* nnz;
+    double* fmax;    // MOD-finish partials per (shard, 8-atom block)
+    int64_t* fnnz;
+    int32_t* frank;
     int32_t* deficient;
     int8_t* depmask;
     void* chol;
