@@ -62,26 +62,25 @@ __device__ __forceinline__ ChunkInfo chunk_info(const int64_t* off, const int64_
     return ci;
 }
 
-// ---- (a) per-chunk atom histograms (warp per chunk, smem int atomics)
+// ---- (a) per-chunk atom histograms: CTA per chunk, each thread a strided
+// share of the chunk's signals, shared-memory integer atomics (counts are
+// order-free)
 __global__ void __launch_bounds__(256)
 k_chunk_hist(const int64_t* __restrict__ off, const int64_t* __restrict__ cf, int P, int K, int cap, int CH,
              const int32_t* __restrict__ idx, const int32_t* __restrict__ counts,
              int32_t* __restrict__ chunk_hist) {
-    extern __shared__ int32_t sh_cnt[];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int64_t c = (int64_t)blockIdx.x * 8 + wib;
-    const int64_t nch = cf[P];
-    int32_t* cnt = sh_cnt + wib * K;
-    if (c >= nch) return;
-    for (int a = lane; a < K; a += 32) cnt[a] = 0;
-    __syncwarp();
+    extern __shared__ int32_t cnt[];
+    const int64_t c = blockIdx.x;
+    if (c >= cf[P]) return;
+    for (int a = threadIdx.x; a < K; a += blockDim.x) cnt[a] = 0;
+    __syncthreads();
     const ChunkInfo ci = chunk_info(off, cf, P, c, CH);
-    for (int64_t i = ci.lo + lane; i < ci.hi; i += 32) {
+    for (int64_t i = ci.lo + threadIdx.x; i < ci.hi; i += blockDim.x) {
         const int n = counts[i];
         for (int t = 0; t < n; ++t) atomicAdd(&cnt[idx[i * cap + t]], 1);
     }
-    __syncwarp();
-    for (int a = lane; a < K; a += 32) chunk_hist[c * K + a] = cnt[a];
+    __syncthreads();
+    for (int a = threadIdx.x; a < K; a += blockDim.x) chunk_hist[c * K + a] = cnt[a];
 }
 
 // ---- (b) usage[p][a] = sum over the shard's chunks. Block = (shard, 32
@@ -732,8 +731,8 @@ int mod_update(const ModArgs<T>& a, cudaStream_t st) {
     const int ch = chunk_size(N);
     k_chunk_layout<<<1, 32, 0, st>>>(a.off, P, ch, w.cf);
     const unsigned hb = (unsigned)((nch_max + 7) / 8);
-    k_chunk_hist<<<hb, 256, 8 * K * sizeof(int32_t), st>>>(a.off, w.cf, P, K, cap, ch, a.idx, a.counts,
-                                                          w.chunk_hist);
+    k_chunk_hist<<<(unsigned)nch_max, std::min(256, std::max(32, ch)), K * sizeof(int32_t), st>>>(
+        a.off, w.cf, P, K, cap, ch, a.idx, a.counts, w.chunk_hist);
     const dim3 gpk((unsigned)((K + 31) / 32), (unsigned)P);
     k_usage_from_chunks<<<gpk, 256, 0, st>>>(w.cf, P, K, w.chunk_hist, w.wpart, a.usage);
     int rc = exclusive_scan_counts(a.usage, PK, w.bucket_off, w.scan_ws, st);
