@@ -23,12 +23,13 @@
 
 namespace sdb {
 
-// signals per chunk (chunks never straddle shards): 1024 for large jobs,
-// down to one 32-signal warp group for small ones (the merge phase), so the
-// warp-per-chunk histogram / placement kernels always have enough warps
+// signals per chunk (chunks never straddle shards): aims at ~32 chunks per SM
+// (256 signals for the C2 locals, down to one 32-signal warp group for the
+// merge phase), so the per-chunk histogram / placement kernels always have
+// enough parallel work; up to 1024 for very large jobs
 __host__ __device__ inline int chunk_size(int64_t N) {
     int ch = 1024;
-    while (ch > 32 && (int64_t)ch * 148 * 8 > N) ch >>= 1;
+    while (ch > 32 && (int64_t)ch * 148 * 32 > N) ch >>= 1;
     return ch;
 }
 
