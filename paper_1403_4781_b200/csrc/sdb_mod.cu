@@ -87,16 +87,18 @@ k_chunk_hist(const int64_t* __restrict__ off, const int64_t* __restrict__ cf, in
 // ---- (b) usage[p][a] = sum over the shard's chunks. Block = (shard, 32
 // atoms); warp w sums the w-th eighth of the shard's chunks (lane = atom) and
 // keeps that partial for (d).
+constexpr int SCW = 16;  // warps splitting a shard's chunk range in the usage / offset scans
+
 __device__ __forceinline__ void chunk_piece(const int64_t* cf, int p, int w, int64_t& c0, int64_t& c1) {
     const int64_t lo = cf[p], n = cf[p + 1] - lo;
-    c0 = lo + n * w / 8;
-    c1 = lo + n * (w + 1) / 8;
+    c0 = lo + n * w / SCW;
+    c1 = lo + n * (w + 1) / SCW;
 }
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(SCW * 32)
 k_usage_from_chunks(const int64_t* __restrict__ cf, int P, int K, const int32_t* __restrict__ chunk_hist,
                     int64_t* __restrict__ wpart, int32_t* __restrict__ usage) {
-    __shared__ int64_t part[8][32];
+    __shared__ int64_t part[SCW][32];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int p = blockIdx.y, a = blockIdx.x * 32 + lane;
     int64_t c0, c1;
@@ -105,18 +107,18 @@ k_usage_from_chunks(const int64_t* __restrict__ cf, int P, int K, const int32_t*
     if (a < K)
         for (int64_t c = c0; c < c1; ++c) s += chunk_hist[c * K + a];
     part[wib][lane] = s;
-    if (a < K) wpart[((int64_t)p * 8 + wib) * K + a] = s;
+    if (a < K) wpart[((int64_t)p * SCW + wib) * K + a] = s;
     __syncthreads();
     if (wib == 0 && a < K) {
         int64_t t = 0;
 #pragma unroll
-        for (int w = 0; w < 8; ++w) t += part[w][lane];
+        for (int w = 0; w < SCW; ++w) t += part[w][lane];
         usage[(int64_t)p * K + a] = (int32_t)t;
     }
 }
 
 // ---- (d) chunk_off[c][a] = bucket_off[p][a] + prefix over earlier chunks
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(SCW * 32)
 k_chunk_offsets(const int64_t* __restrict__ cf, int P, int K, const int32_t* __restrict__ chunk_hist,
                 const int64_t* __restrict__ wpart, const int64_t* __restrict__ bucket_off,
                 int64_t* __restrict__ chunk_off) {
@@ -124,7 +126,7 @@ k_chunk_offsets(const int64_t* __restrict__ cf, int P, int K, const int32_t* __r
     const int p = blockIdx.y, a = blockIdx.x * 32 + lane;
     if (a >= K) return;
     int64_t run = bucket_off[(int64_t)p * K + a];
-    for (int w = 0; w < wib; ++w) run += wpart[((int64_t)p * 8 + w) * K + a];
+    for (int w = 0; w < wib; ++w) run += wpart[((int64_t)p * SCW + w) * K + a];
     int64_t c0, c1;
     chunk_piece(cf, p, wib, c0, c1);
     for (int64_t c = c0; c < c1; ++c) {
@@ -693,7 +695,7 @@ ModWs carve_mod_ws(void* base, int P, int64_t N, int m, int K, int cap) {
     w.cf = (int64_t*)take(sizeof(int64_t) * (P + 1));
     w.chunk_hist = (int32_t*)take(sizeof(int32_t) * nch * K);
     w.chunk_off = (int64_t*)take(sizeof(int64_t) * nch * K);
-    w.wpart = (int64_t*)take(sizeof(int64_t) * 8 * (int64_t)P * K);
+    w.wpart = (int64_t*)take(sizeof(int64_t) * SCW * (int64_t)P * K);
     w.bucket_off = (int64_t*)take(sizeof(int64_t) * ((int64_t)P * K + 1));
     w.scan_ws = (int64_t*)take(scan_workspace_bytes((int64_t)P * K));
     w.bent = (int32_t*)take(sizeof(int32_t) * std::max<int64_t>(N * cap, 1));
@@ -735,10 +737,10 @@ int mod_update(const ModArgs<T>& a, cudaStream_t st) {
     k_chunk_hist<<<(unsigned)nch_max, std::min(256, std::max(32, ch)), K * sizeof(int32_t), st>>>(
         a.off, w.cf, P, K, cap, ch, a.idx, a.counts, w.chunk_hist);
     const dim3 gpk((unsigned)((K + 31) / 32), (unsigned)P);
-    k_usage_from_chunks<<<gpk, 256, 0, st>>>(w.cf, P, K, w.chunk_hist, w.wpart, a.usage);
+    k_usage_from_chunks<<<gpk, SCW * 32, 0, st>>>(w.cf, P, K, w.chunk_hist, w.wpart, a.usage);
     int rc = exclusive_scan_counts(a.usage, PK, w.bucket_off, w.scan_ws, st);
     if (rc) return rc;
-    k_chunk_offsets<<<gpk, 256, 0, st>>>(w.cf, P, K, w.chunk_hist, w.wpart, w.bucket_off, w.chunk_off);
+    k_chunk_offsets<<<gpk, SCW * 32, 0, st>>>(w.cf, P, K, w.chunk_hist, w.wpart, w.bucket_off, w.chunk_off);
     {
         const int smem = 8 * K * (int)sizeof(int64_t);
         if (smem > 48 * 1024)
