@@ -117,7 +117,11 @@ def ncu_traffic() -> dict:
         for line in f.read_text().splitlines():
             parts = line.split()
             if line.startswith("Kernel Name"):
-                name = "k_omp_fast" if "k_omp_fast" in line else ("k_corr_tc2" if "k_corr_tc2" in line else None)
+                name = None
+                for base, tag in (("k_omp_fast", "k_omp_fast<LIST>"), ("k_corr_tc2", "k_corr_tc2<CODE>")):
+                    if base + "<" in line:
+                        targs = line.split(base + "<", 1)[1].split(">", 1)[0].replace(" ", "").split(",")
+                        name = tag if len(targs) >= 2 and targs[-1] in ("1", "true") else base
             elif len(parts) >= 3 and parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
                 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(parts[1], 1)
                 vals[parts[0]] = float(parts[2]) * scale
@@ -239,16 +243,24 @@ def main():
     # ---- timed region: barrier + sync on both sides, device-timed, max over ranks
     clk = Clocks(local)
     E.KTIMER = {}
+    E.KSTAT.clear()
+    E.KSTAT.update(deferred=E.zeros((1,), torch.int64), coded=0)   # allocated before the timed region
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record()
+    marks = []
     for _ in range(args.steps):
         r = step()
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        marks.append(e)
     ev1.record()
     torch.cuda.synchronize()
+    step_ms = [ev0.elapsed_time(marks[0])] + [a.elapsed_time(b) for a, b in zip(marks, marks[1:])]
+    print("per-step ms: " + " ".join(f"{x:.2f}" for x in step_ms), file=sys.stderr)
     if world > 1:
         dist.barrier()
     clocks = clk.stop()
@@ -262,40 +274,68 @@ def main():
 
     # ---- per-kernel breakdown (CUDA events recorded around each C-ABI call)
     hbm, bf16, peak_src = peaks()
+    tf32_peak = bf16 / 2.0
+    kstat = dict(E.KSTAT)
+    E.KSTAT.clear()
+    deferred = int(kstat["deferred"].item()) if "deferred" in kstat else 0
+    coded = int(kstat.get("coded", 0))
+    K1 = cfg["K1"]
+    # algorithmic bytes per signal (fp32):
+    #   omp (all signals): alpha0 row + ||y||^2 + code row (idx+val, cap wide) + count + status
+    #   omp_deferred: the same per deferred signal + its (signal, shard) list entry
+    #   step1: y row + ||y||^2 per signal; settled signals' code row + count + status;
+    #          deferred signals' alpha0 row + list entry
+    omp_b = 4 * K1 + 4 + 8 * cap + 5
+    extra_bytes = {
+        "omp_deferred": deferred * (omp_b + 8),
+        "step1": (coded - deferred) * (8 * cap + 5) + deferred * (4 * K1 + 8),
+    }
     breakdown = {}
     for name, evs in kt.items():
         tot = sum(a.elapsed_time(b) for a, b, _, _ in evs)
-        byts = sum(x for _, _, x, _ in evs)
+        byts = sum(x for _, _, x, _ in evs) + extra_bytes.get(name, 0)
+        fl = sum(f for _, _, _, f in evs)
         breakdown[name] = {"launches": len(evs), "ms_per_step": tot / args.steps,
-                           "avg_ms": tot / len(evs), "GBps": byts / (tot / 1000.0) / 1e9}
+                           "avg_ms": tot / len(evs), "GBps": byts / (tot / 1000.0) / 1e9,
+                           "bytes_per_launch": byts / len(evs)}
+        if fl > 0:
+            breakdown[name]["useful_TFLOPs"] = fl / (tot / 1000.0) / 1e12
+    if coded:
+        breakdown["omp_deferred"]["deferred_fraction"] = deferred / coded
     # dominant single kernel (mod_update / replace are multi-kernel pipelines)
-    singles = {k: v for k, v in breakdown.items() if k in ("omp", "correlate")}
+    kernel_of = {"omp": "k_omp_fast", "omp_deferred": "k_omp_fast<LIST>",
+                 "correlate": "k_corr_tc2", "step1": "k_corr_tc2<CODE>"}
+    singles = {k: v for k, v in breakdown.items() if k in kernel_of}
     dom = max(singles, key=lambda k: singles[k]["ms_per_step"]) if singles else None
     roof = None
     ncu = ncu_traffic()
     if dom:
         d = breakdown[dom]
-        kname = "k_omp_fast" if dom == "omp" else "k_corr_tc2"
-        roof = {"kernel": kname, "bound": "hbm", "achieved": d["GBps"], "peak": hbm, "unit": "GB/s",
-                "frac": d["GBps"] / hbm, "traffic": ncu.get(kname), "peak_source": peak_src,
-                "share_of_step": d["ms_per_step"] / ms,
-                # omp: alpha0 row + ||y||^2 + code row (idx+val, cap wide) + count + status
-                "algorithmic_bytes_per_signal": (4 * cfg["K1"] + 4 + 8 * cap + 5) if dom == "omp"
-                else 4 * (m + cfg["K1"]),
-                "traffic_note": "ncu dram read+write of one C2 local-pass launch (2,040,200 signals), "
-                                "profiles/ncu_*_r01c_raw.txt"}
+        kname = kernel_of[dom]
+        if dom in ("omp", "omp_deferred"):
+            roof = {"kernel": kname, "bound": "hbm", "achieved": d["GBps"], "peak": hbm, "unit": "GB/s",
+                    "frac": d["GBps"] / hbm, "traffic": ncu.get(kname), "peak_source": peak_src,
+                    "share_of_step": d["ms_per_step"] / ms,
+                    "algorithmic_bytes_per_signal": omp_b + (8 if dom == "omp_deferred" else 0)}
+        else:
+            ach = 3 * d["useful_TFLOPs"]
+            roof = {"kernel": kname, "bound": "tensor", "achieved": ach, "peak": tf32_peak,
+                    "unit": "TFLOP/s", "frac": ach / tf32_peak, "traffic": ncu.get(kname),
+                    "peak_source": peak_src + "; TF32 dense = bf16/2",
+                    "share_of_step": d["ms_per_step"] / ms, "hbm_GBps": d["GBps"],
+                    "hbm_frac": d["GBps"] / hbm,
+                    "algorithmic_flops_per_signal": 3 * 2 * m * K1,
+                    "note": "3xTF32 issues 3 MMAs per useful product (achieved counts all 3)"}
+        roof["traffic_note"] = ("ncu dram read+write per launch of one C2 local pass (2,040,200 "
+                                "signals), profiles/ncu_*_raw.txt")
     gemm = None
-    if "correlate" in kt:
-        evs = kt["correlate"]
-        tot = sum(a.elapsed_time(b) for a, b, _, _ in evs) / 1000.0
-        fl = sum(f for _, _, _, f in evs)
-        tf32_peak = bf16 / 2.0
-        gemm = {"kernel": "k_corr_tc2", "bound": "tensor", "achieved": 3 * fl / tot / 1e12,
-                "peak": tf32_peak, "unit": "TFLOP/s", "frac": 3 * fl / tot / 1e12 / tf32_peak,
-                "useful_tflops": fl / tot / 1e12, "hbm_GBps": breakdown["correlate"]["GBps"],
-                "hbm_frac": breakdown["correlate"]["GBps"] / hbm,
-                "note": "3xTF32 issues 3 MMAs per useful product; TF32 dense peak = measured bf16/2; "
-                        "at m=64 the kernel is HBM-bound (alpha0 writes)"}
+    gname = "step1" if "step1" in kt else ("correlate" if "correlate" in kt else None)
+    if gname:
+        d = breakdown[gname]
+        gemm = {"kernel": kernel_of[gname], "bound": "tensor", "achieved": 3 * d["useful_TFLOPs"],
+                "peak": tf32_peak, "unit": "TFLOP/s", "frac": 3 * d["useful_TFLOPs"] / tf32_peak,
+                "useful_tflops": d["useful_TFLOPs"], "hbm_GBps": d["GBps"], "hbm_frac": d["GBps"] / hbm,
+                "note": "3xTF32 issues 3 MMAs per useful product; TF32 dense peak = measured bf16/2"}
     # ---- launch count (one extra untimed step under the CUDA profiler)
     per_step = count_launches(step)
     gpu_launches = per_step * args.steps if per_step >= 0 else None

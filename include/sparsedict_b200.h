@@ -42,6 +42,7 @@ extern "C" {
 #define SDB_ENOMEM (-12)
 #define SDB_ECUDA (-5)
 #define SDB_ENODEV (-19)
+#define SDB_ENOTSUP (-95)
 
 int sdb_abi_version(void);
 const char *sdb_last_error(void);
@@ -87,6 +88,29 @@ int sdb_omp(int dtype, int64_t N, int64_t m, int64_t K, int64_t P, const int64_t
             const void *G, int64_t cap, double eps, double guard, int32_t *idx, void *val,
             int32_t *counts, int8_t *status, void *rnorm, const float *ysq, void *scratch,
             int64_t scratch_bytes, void *stream);
+/* Error-bounded FP32 coding in two launches (replaces sdb_correlate +
+ * sdb_omp for the training loop's ε-mode passes, configs 2-3):
+ * sdb_code_step1 is the tcgen05 correlation GEMM whose epilogue also runs the
+ * first iteration of omp_single (_kernels.py:61-154: ||y|| <= eps early exit,
+ * argmax with lowest-index tie-break, stall and singular tests, the
+ * one-atom Cholesky solve and the eps test) on each signal's accumulator row,
+ * with the exact arithmetic of sdb_omp's FP32 kernel. Signals it settles get
+ * idx/val/counts/status written; the others get their alpha0 row stored and
+ * status -1, and their number is added to *n_deferred (device int32; the
+ * caller zeroes nothing: the launch resets it). sdb_omp_deferred then codes
+ * exactly the status -1 signals. The union is bitwise sdb_omp's output
+ * (rnorm not produced). Needs K <= 256, m <= 256, cap <= 32, eps > 0 and ysq
+ * (sdb_signal_sq); SDB_ENOTSUP otherwise (the caller uses sdb_correlate +
+ * sdb_omp). ws: sdb_code_step1_workspace_bytes(). */
+int64_t sdb_code_step1_workspace_bytes(int64_t P, int64_t m, int64_t K);
+int sdb_code_step1(int64_t N, int64_t m, int64_t K, int64_t P, const int64_t *shard_off, const float *Y,
+                   int64_t ldy, const float *D, const float *G, const float *ysq, int64_t cap, double eps,
+                   double guard, float *alpha0, int64_t lda, int32_t *idx, float *val, int32_t *counts,
+                   int8_t *status, int32_t *n_deferred, void *ws, int64_t ws_bytes, void *stream);
+int sdb_omp_deferred(int64_t N, int64_t m, int64_t K, int64_t P, const int64_t *shard_off,
+                     const float *alpha0, int64_t lda, const float *Y, int64_t ldy, const float *D,
+                     const float *G, const float *ysq, int64_t cap, double eps, double guard, int32_t *idx,
+                     float *val, int32_t *counts, int8_t *status, void *stream);
 /* ||y_i||^2 per signal (FP32, N floats) with the exact arithmetic of the
  * FP32 OMP kernel: passing it as sdb_omp's ysq gives bitwise the same codes
  * and lets the kernel skip loading y except near the eps threshold. */

@@ -59,6 +59,9 @@ _dev_checked = False
 # Optional per-call CUDA-event timers (bench.py roofline): name -> list of
 # (start_event, end_event, algorithmic_bytes, flops). None = disabled.
 KTIMER: dict | None = None
+# with KTIMER on: device counters of the fused coding path (signals coded by
+# sdb_code_step1, signals it deferred to sdb_omp_deferred)
+KSTAT: dict = {}
 
 
 def timed_call(name: str, nbytes: float, flops: float, fn, *args):
@@ -233,6 +236,27 @@ def code(Ydev: torch.Tensor, off: torch.Tensor, max_rows: int, DT: torch.Tensor,
         return out
     alpha = empty((N, K), tdt)
     es = 8 if prec == "fp64" else 4
+    if (prec == "fp32" and use_tc and ysq is not None and eps > 0.0 and not want_rnorm
+            and K <= 256 and m <= 256 and cap <= 32 and K % 4 == 0 and m % 4 == 0):
+        # error-bounded mode: GEMM + first greedy step fused, OMP only for the
+        # signals that need more (bitwise the same codes as the path below)
+        wb = _lib.load().sdb_code_step1_workspace_bytes(P, m, K)
+        ws = empty((wb,), torch.uint8)
+        ndef = ws[wb - 256:wb - 252].view(torch.int32)
+        timed_call("step1", N * (4 * m + 4), 2.0 * N * m * K, "sdb_code_step1", N, m, K, P, ptr(off),
+                   ptr(Ydev), m, ptr(DT), ptr(G), ptr(ysq), cap, float(eps), GUARD[prec], ptr(alpha), K,
+                   ptr(out.idx), ptr(out.val), ptr(out.counts), ptr(out.status), ptr(ndef), ptr(ws),
+                   int(wb), stream())
+        timed_call("omp_deferred", 0.0, 0.0, "sdb_omp_deferred", N, m, K, P, ptr(off), ptr(alpha), K,
+                   ptr(Ydev), m, ptr(DT), ptr(G), ptr(ysq), cap, float(eps), GUARD[prec], ptr(out.idx),
+                   ptr(out.val), ptr(out.counts), ptr(out.status), stream())
+        if KTIMER is not None and not torch.cuda.is_current_stream_capturing():
+            if "deferred" not in KSTAT:
+                KSTAT["deferred"] = zeros((1,), torch.int64)
+                KSTAT["coded"] = 0
+            KSTAT["deferred"].add_(ndef)
+            KSTAT["coded"] += N
+        return out
     cwb = _lib.load().sdb_correlate_workspace_bytes(dt, P, m, K) if use_tc else 0
     cws = empty((cwb,), torch.uint8) if cwb > 0 else None
     timed_call("correlate", N * (m + K) * es, 2.0 * N * m * K,

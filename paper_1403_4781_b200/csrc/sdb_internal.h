@@ -26,6 +26,7 @@ struct OmpArgs {
     int8_t* status;
     T* rnorm;                  // optional (nullptr: not requested)
     const float* ysq;          // optional precomputed ||y||^2 (fast FP32 path only)
+    int deferred;              // fast FP32 path: code only the signals with status == -1
     unsigned char* gscratch;   // optional per-warp scratch in global memory
     int64_t gscratch_warps;
     int64_t warp_bytes;
@@ -49,6 +50,13 @@ int correlate_tc_f32(int64_t N, const float* Y, int64_t ldy, const int64_t* off,
                      int P, const float* D, int64_t m, int64_t K, float* alpha, int64_t lda, void* ws,
                      int64_t ws_bytes, cudaStream_t st);
 int64_t corr_tc_ws_bytes(int P, int64_t m, int64_t K);
+// the same GEMM with the first greedy OMP step fused into its epilogue (K <=
+// 256): settled signals get their codes, the rest their alpha0 row and
+// status -1 (their number added to *n_deferred)
+int code_step1_tc_f32(int64_t N, const float* Y, int64_t ldy, const int64_t* off, int P, const float* D,
+                      int64_t m, int64_t K, float* alpha, int64_t lda, void* ws, int64_t ws_bytes,
+                      const float* ysq, const float* G, float eps, float guard, int cap, int32_t* idx,
+                      float* val, int32_t* counts, int8_t* status, int* n_deferred, cudaStream_t st);
 
 template <typename T>
 int launch_omp(OmpArgs<T> a, cudaStream_t st);

@@ -450,7 +450,10 @@ __device__ __forceinline__ void load_row(float (&v)[KPL], const float* __restric
     for (int k = 0; k < KPL; ++k) v[k] = (j0 + k < K) ? __ldg(row + j0 + k) : 0.0f;
 }
 
-template <int KPL, int MPL>
+// DEFER: code only the signals whose status is -1 (marked by the correlation
+// GEMM's step-1 epilogue, sdb_code_step1, for the signals it could not settle);
+// each warp scans its contiguous range 32 status bytes at a time (ballot).
+template <int KPL, int MPL, bool DEFER>
 __global__ void __launch_bounds__(256, (KPL >= 16) ? 1 : (MPL >= 5 ? 3 : 4))
 k_omp_fast(OmpArgs<float> a) {
     extern __shared__ __align__(16) float fsm[];
@@ -476,54 +479,72 @@ k_omp_fast(OmpArgs<float> a) {
     const bool vec_a = (K == 32 * KPL) && ((a.lda * 4) % 16 == 0) && (((uintptr_t)a.alpha0 & 15) == 0);
     const bool vec_g = (K == 32 * KPL) && ((K * 4) % 16 == 0) && (((uintptr_t)a.G & 15) == 0);
 
-    int p = shard_of(a.shard_off, a.P, i_begin);
+    // DEFER: flags of the current 32-signal chunk not yet visited
+    int64_t fc = i_begin;
+    unsigned fl = 0;
+    auto flags_at = [&](int64_t c) -> unsigned {
+        if (c + 32 + lane < i_end && (lane & 31) == 0)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(a.status + c + 32));
+        const bool f = (c + lane < i_end) && (__ldg(a.status + c + lane) == (int8_t)-1);
+        return __ballot_sync(SDB_FULL, f);
+    };
+    auto next_flagged = [&]() -> int64_t {
+        while (!fl) {
+            if (fc >= i_end) return i_end;
+            fl = flags_at(fc);
+            fc += 32;
+        }
+        const int64_t r = fc - 32 + __ffs(fl) - 1;
+        fl &= fl - 1u;
+        return r;
+    };
+    int64_t i = DEFER ? next_flagged() : i_begin;
+    if (i >= i_end) return;
+
+    int p = shard_of(a.shard_off, a.P, i);
     int64_t p_end = a.shard_off[p + 1];
     const float* __restrict__ Gp = a.G + (int64_t)p * K * K;
     const float* __restrict__ Dp = a.D + (int64_t)p * K * m;
 
-    const float* arow_n = a.alpha0 + i_begin * a.lda;   // advanced by lda per signal
-    int32_t* code_idx = a.idx + i_begin * cap;         // this signal's code row (advanced by cap)
-    float* code_val = a.val + i_begin * cap;
-    const float* yrow_n = a.Y + i_begin * a.ldy + lane;
-    // the next signal's alpha0 row and y are prefetched into L1 (no registers
-    // held across the signal, which keeps occupancy at 4 blocks / SM)
-    auto prefetch_next = [&]() {
-        const float* an = arow_n + a.lda;
-        if (j0 < K) asm volatile("prefetch.global.L1 [%0];" ::"l"(an + j0));
-        if constexpr (KPL > 8) {
-            if (j0 + 8 < K) asm volatile("prefetch.global.L1 [%0];" ::"l"(an + j0 + 8));
-        }
-        if (!a.ysq) {
-#pragma unroll
-            for (int q = 0; q < MPL; ++q)
-                if (32 * q + lane < m && (lane & 7) == 0)
-                    asm volatile("prefetch.global.L1 [%0];" ::"l"(yrow_n + a.ldy + 32 * q));
-        }
-    };
     // atoms this lane owns that exist (K not a multiple of 32*KPL)
     const int nvalid = max(0, min(KPL, K - j0));
     const bool all_valid = nvalid == KPL;
     const float kNaN = __int_as_float(0x7fffffff);
 
-    for (int64_t i = i_begin; i < i_end; ++i) {
+    for (int64_t i_next; i < i_end; i = i_next) {
+        i_next = DEFER ? next_flagged() : i + 1;
         if (i >= p_end) {
             while (i >= p_end) { ++p; p_end = a.shard_off[p + 1]; }
             Gp = a.G + (int64_t)p * K * K;
             Dp = a.D + (int64_t)p * K * m;
         }
+        const float* __restrict__ arow = a.alpha0 + i * a.lda;
+        int32_t* code_idx = a.idx + i * cap;
+        float* code_val = a.val + i * cap;
+        const float* __restrict__ yrow = a.Y + i * a.ldy + lane;
         // c0 doubles as the selection mask: a selected (or absent) atom's entry
         // is NaN, which fmaxf skips and whose bits never equal the maximum
         float c0[KPL];
-        load_row<KPL>(c0, arow_n, lane, K, vec_a);
-        const float* __restrict__ yrow = yrow_n;
+        load_row<KPL>(c0, arow, lane, K, vec_a);
         if (!all_valid) {
 #pragma unroll
             for (int k = 0; k < KPL; ++k) c0[k] = (k < nvalid) ? c0[k] : kNaN;
         }
-        if (i + 1 < i_end) prefetch_next();
-        const float* __restrict__ arow = arow_n;
-        arow_n += a.lda;
-        yrow_n += a.ldy;
+        // the next signal's alpha0 row (and y) are prefetched into L1 (no
+        // registers held across the signal, which keeps occupancy at 4 blocks / SM)
+        if (i_next < i_end) {
+            const float* an = a.alpha0 + i_next * a.lda;
+            if (j0 < K) asm volatile("prefetch.global.L1 [%0];" ::"l"(an + j0));
+            if constexpr (KPL > 8) {
+                if (j0 + 8 < K) asm volatile("prefetch.global.L1 [%0];" ::"l"(an + j0 + 8));
+            }
+            if (!a.ysq) {
+#pragma unroll
+                for (int q = 0; q < MPL; ++q)
+                    if (32 * q + lane < m && (lane & 7) == 0)
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"(a.Y + i_next * a.ldy + lane + 32 * q));
+            }
+        }
 
         // ||y||^2: precomputed (same arithmetic, sdb_signal_sq) or formed here;
         // y itself is only loaded when an explicit residual is needed
@@ -637,7 +658,7 @@ k_omp_fast(OmpArgs<float> a) {
                 // ||r||^2 = ||y||^2 - ||L^-1 c0_S||^2 (projection identity): O(1) per
                 // step. Only near the threshold is the explicit residual formed, so
                 // the stopping decision is the one the explicit residual gives.
-                rsq = fmaxf(rsq - tn * tn, 0.0f);
+                rsq = fmaxf(fmaf(-tn, tn, rsq), 0.0f);
                 __syncwarp();
                 if (fabsf(rsq - eps2) <= 1e-4f * ysq) {
                     rnorm = resid_norm(n);
@@ -654,8 +675,6 @@ k_omp_fast(OmpArgs<float> a) {
             code_idx[lane] = (lane < n) ? ids[lane] : 0;
             code_val[lane] = (lane < n) ? xs[lane] : 0.0f;
         }
-        code_idx += cap;
-        code_val += cap;
         if (lane == 0) {
             a.counts[i] = n;
             a.status[i] = (int8_t)status;
@@ -671,7 +690,7 @@ static int launch_fast_k(const OmpArgs<float>& a, cudaStream_t st) {
     int wpb = 8;
     while (wpb > 1 && wpb * wf * 4 > 200 * 1024) wpb >>= 1;
     const int smem = wpb * wf * 4;
-    auto fn = k_omp_fast<KPL, MPL>;
+    auto fn = a.deferred ? k_omp_fast<KPL, MPL, true> : k_omp_fast<KPL, MPL, false>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return (int)e;

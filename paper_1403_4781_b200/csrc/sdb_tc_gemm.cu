@@ -159,13 +159,176 @@ __device__ __forceinline__ void tmem_ld32(uint32_t (&v)[32], uint32_t taddr) {
         : "r"(taddr));
 }
 
-template <bool RES>
+// CODE: the epilogue also runs the first greedy step of the error-bounded
+// FP32 OMP (k_omp_fast, sdb_omp.cu) on each signal's TMEM row, with the same
+// arithmetic: argmax |alpha0| (lowest index among equal maxima), stall and
+// singular tests, x = c0[b] / G[b,b], ||r||^2 = ||y||^2 - c0[b]^2 / G[b,b].
+// A signal that this settles (no atom, one atom, or a stop status) gets its
+// code row, count and status written here and its alpha0 row is never
+// stored; every other signal (a second atom is needed, or ||r|| is within
+// the band where the explicit residual decides) has its alpha0 row stored
+// and status -1, and k_omp_fast<DEFER> codes it from scratch. Needs K <= 256
+// (the whole row in one accumulator).
+struct Step1 {
+    const float* ysq;     // N: ||y||^2 (sdb_signal_sq)
+    const float* G;       // P x K x K
+    float eps2, guard;
+    int cap;
+    int32_t* idx;         // N x cap
+    float* val;           // N x cap
+    int32_t* counts;
+    int8_t* status;
+    int* n_deferred;      // zeroed by k_tile_layout
+};
+
+__device__ __forceinline__ void tmem_wait_ld() {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// argmax over one 32-column block of a row: a pairwise tree (the left,
+// lower-index operand wins ties, so the result is the lowest index attaining
+// the maximum, as the reference's ascending scan gives); NaN and columns
+// past K enter as 0, which can never be selected (selection needs > 0).
+// key = column | sign bit of alpha0.
+__device__ __forceinline__ void block_argmax(const uint32_t (&v)[32], int c, int K, float& bv, uint32_t& bk) {
+    float a[32];
+    uint32_t k[32];
+    const bool full = c + 32 <= K;
+#pragma unroll
+    for (int t = 0; t < 32; ++t) {
+        const float x = __uint_as_float(v[t]);
+        a[t] = (full || c + t < K) ? fmaxf(fabsf(x), 0.0f) : 0.0f;
+        k[t] = (uint32_t)(c + t) | (v[t] & 0x80000000u);
+    }
+#pragma unroll
+    for (int w = 1; w < 32; w <<= 1)
+#pragma unroll
+        for (int t = 0; t < 32; t += 2 * w) {
+            const bool r = a[t + w] > a[t];
+            a[t] = r ? a[t + w] : a[t];
+            k[t] = r ? k[t + w] : k[t];
+        }
+    bv = a[0];
+    bk = k[0];
+}
+
+// One warp, 32 signal rows (thread = row_base + lane) of a K <= 256 accumulator.
+// diag: warp-private smem copy of the shard's G diagonal (reloaded when the
+// shard changes, *dp = its shard).
+__device__ __forceinline__ void code_step1(const Step1& s1, uint32_t trow, int64_t row_base, int nrows,
+                                           int p, int K, float* diag, int* dp, float* __restrict__ alpha,
+                                           int64_t lda, int lane) {
+    const int64_t i = row_base + lane;
+    const bool valid = lane < nrows;
+    const float ysq = valid ? __ldg(s1.ysq + i) : 0.0f;      // in flight during the scan
+    if (*dp != p) {
+        __syncwarp();
+        for (int k = lane; k < K; k += 32) diag[k] = __ldg(s1.G + ((int64_t)p * K + k) * K + k);
+        *dp = p;
+    }
+    // ---- argmax |alpha0| over the row
+    float cur = 0.0f;
+    uint32_t key = 0xffffffffu;
+    uint32_t va[32], vb[32];
+    auto scan = [&](const uint32_t (&v)[32], int c) {
+        float bv;
+        uint32_t bk;
+        block_argmax(v, c, K, bv, bk);
+        if (bv > cur) { cur = bv; key = bk; }
+    };
+    tmem_ld32(va, trow);
+    tmem_wait_ld();
+#pragma unroll 1
+    for (int c = 0; c < K; c += 64) {
+        if (c + 32 < K) tmem_ld32(vb, trow + (uint32_t)(c + 32));
+        scan(va, c);
+        tmem_wait_ld();
+        if (c + 32 >= K) break;
+        if (c + 64 < K) tmem_ld32(va, trow + (uint32_t)(c + 64));
+        scan(vb, c + 32);
+        tmem_wait_ld();
+    }
+    __syncwarp();
+    // ---- the first greedy step (k_omp_fast, step 0)
+    bool defer = false;
+    int n = 0, status = 0, best = 0;
+    float x0 = 0.0f;
+    if (valid) {
+        if (ysq <= s1.eps2 || ysq == 0.0f) {
+            // ||y|| <= eps: no atom
+        } else if (cur * cur <= 1e-26f * ysq) {
+            status = 3;                       // cmax <= 1e-13 ||r|| (also: no candidate)
+        } else {
+            best = (int)(key & 0x7fffffffu);
+            const float cb = __uint_as_float(__float_as_uint(cur) | (key & 0x80000000u));
+            const float dsq = diag[best];
+            if (dsq <= s1.guard) {
+                status = 2;
+                best = 0;
+            } else {
+                const float inv = rsqrtf(dsq);
+                const float tn = cb * inv;
+                x0 = tn * inv;
+                n = 1;
+                const float rsq = fmaxf(fmaf(-tn, tn, ysq), 0.0f);
+                if (s1.cap > 1 && (fabsf(rsq - s1.eps2) <= 1e-4f * ysq || rsq > s1.eps2)) defer = true;
+            }
+        }
+        if (!defer) {
+            int32_t* ci = s1.idx + i * s1.cap;
+            float* cv = s1.val + i * s1.cap;
+            if ((s1.cap & 3) == 0) {
+                int4* ci4 = reinterpret_cast<int4*>(ci);
+                float4* cv4 = reinterpret_cast<float4*>(cv);
+                ci4[0] = make_int4(best, 0, 0, 0);
+                cv4[0] = make_float4(x0, 0.0f, 0.0f, 0.0f);
+                for (int t = 1; t < (s1.cap >> 2); ++t) {
+                    ci4[t] = make_int4(0, 0, 0, 0);
+                    cv4[t] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                }
+            } else {
+                for (int t = 0; t < s1.cap; ++t) {
+                    ci[t] = (t < n) ? best : 0;
+                    cv[t] = (t < n) ? x0 : 0.0f;
+                }
+            }
+            s1.counts[i] = n;
+        }
+        s1.status[i] = defer ? (int8_t)-1 : (int8_t)status;
+    }
+    // ---- deferred rows: the alpha0 row, each thread its own (8 x 16-byte
+    // stores fill one 128-byte line per 32 columns)
+    const unsigned dmask = __ballot_sync(SDB_FULL, defer);
+    if (dmask == 0u) return;
+    if (lane == 0) atomicAdd(s1.n_deferred, __popc(dmask));   // result unused: a fire-and-forget RED
+    float* out = alpha + i * lda;
+#pragma unroll 1
+    for (int c = 0; c < K; c += 32) {
+        tmem_ld32(va, trow + (uint32_t)c);
+        tmem_wait_ld();
+        if (defer) {
+            if (c + 32 <= K) {
+                float4* o4 = reinterpret_cast<float4*>(out + c);
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    o4[q] = make_float4(__uint_as_float(va[4 * q]), __uint_as_float(va[4 * q + 1]),
+                                        __uint_as_float(va[4 * q + 2]), __uint_as_float(va[4 * q + 3]));
+            } else {
+#pragma unroll
+                for (int q = 0; q < 32; ++q)
+                    if (c + q < K) out[c + q] = __uint_as_float(va[q]);
+            }
+        }
+    }
+}
+
+template <bool RES, bool CODE>
 __global__ void __launch_bounds__(NWARP2 * 32, 1)
 k_corr_tc2(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmDh,
            const __grid_constant__ CUtensorMap tmDl, const __grid_constant__ CUtensorMap tmA,
            const int64_t* __restrict__ off,
            const int64_t* __restrict__ tile_start, int P, int K, int nkb, int nchunk,
-           float* __restrict__ alpha, int64_t lda) {
+           float* __restrict__ alpha, int64_t lda, const Step1 s1) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* base = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     // layout: RES: [A stage 0 | A stage 1 | D resident] ; !RES: [stage 0 | stage 1]
@@ -296,6 +459,8 @@ k_corr_tc2(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUte
         // plain stores so rows of the next shard are never touched
         const int quad = warp & 3;
         float* stg = stg_base + (warp - 2) * 2 * 1024;
+        int diag_shard = -1;                    // CODE: shard whose G diagonal is in stg
+        int* diag_p = &diag_shard;
         int64_t n = 0;
         int sb = 0;  // staging buffer toggle
         for (int64_t it = it0; it < it1; ++it, ++n) {
@@ -309,6 +474,13 @@ k_corr_tc2(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUte
             const int n0 = I.chunk * TN;
             const int ncols = min(TN, K - n0);
             const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * TN);
+            if constexpr (CODE) {
+                code_step1(s1, trow, row_base, nrows, I.p, K, stg, diag_p, alpha, lda, lane);
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&bars[8 + b]));
+                continue;
+            }
             // one 32x32 block: TMA store from swizzled staging (conflict-free
             // 16-byte smem writes), or plain stores for a partial quadrant
             auto put = [&](const uint32_t (&v)[32], int c) {
@@ -395,8 +567,10 @@ k_corr_tc2(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUte
 }
 
 // tile_start[p] = first 128-signal tile of shard p (prefix over shards)
-__global__ void k_tile_layout(const int64_t* __restrict__ off, int P, int64_t* __restrict__ ts) {
+__global__ void k_tile_layout(const int64_t* __restrict__ off, int P, int64_t* __restrict__ ts,
+                              int* __restrict__ zero) {
     if (threadIdx.x == 0 && blockIdx.x == 0) {
+        if (zero) *zero = 0;
         int64_t t = 0;
         for (int p = 0; p < P; ++p) {
             ts[p] = t;
@@ -463,9 +637,9 @@ int64_t corr_tc_ws_bytes(int P, int64_t m, int64_t K) {
     return 2 * (int64_t)P * K * m_pad * 4 + 256 + 8 * ((int64_t)P + 1) + 256;
 }
 
-int correlate_tc_f32(int64_t N, const float* Y, int64_t ldy, const int64_t* off, int64_t max_rows,
-                     int P, const float* D, int64_t m, int64_t K, float* alpha, int64_t lda, void* ws,
-                     int64_t ws_bytes, cudaStream_t st) {
+static int corr_tc_launch(int64_t N, const float* Y, int64_t ldy, const int64_t* off, int P,
+                          const float* D, int64_t m, int64_t K, float* alpha, int64_t lda, void* ws,
+                          int64_t ws_bytes, const Step1* s1, cudaStream_t st) {
     std::call_once(g_once, load_encode);
     if (!g_encode || ws == nullptr || ws_bytes < corr_tc_ws_bytes(P, m, K)) return (int)cudaErrorNotSupported;
     if ((ldy * 4) % 16 != 0 || ((uintptr_t)Y & 15) != 0) return (int)cudaErrorNotSupported;
@@ -485,8 +659,10 @@ int correlate_tc_f32(int64_t N, const float* Y, int64_t ldy, const int64_t* off,
     static bool attr = false;
     static int n_sm = 148;
     if (!attr) {
-        cudaFuncSetAttribute(k_corr_tc2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES);
-        cudaFuncSetAttribute(k_corr_tc2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES);
+        cudaFuncSetAttribute(k_corr_tc2<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES);
+        cudaFuncSetAttribute(k_corr_tc2<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES);
+        cudaFuncSetAttribute(k_corr_tc2<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES);
+        cudaFuncSetAttribute(k_corr_tc2<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES);
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
@@ -494,19 +670,36 @@ int correlate_tc_f32(int64_t N, const float* Y, int64_t ldy, const int64_t* off,
     }
     int64_t* tile_start = (int64_t*)((unsigned char*)ws + 2 * (int64_t)P * K * m_pad * 4 + 256);
     tile_start = (int64_t*)(((uintptr_t)tile_start + 255) & ~(uintptr_t)255);
-    k_tile_layout<<<1, 32, 0, st>>>(off, P, tile_start);
+    k_tile_layout<<<1, 32, 0, st>>>(off, P, tile_start, s1 ? s1->n_deferred : nullptr);
     const int nchunk = (int)((K + TN - 1) / TN);
     // upper bound on work items (the kernel reads the exact count on device)
     const int64_t max_items = ((N + TM - 1) / TM + P) * nchunk;
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(n_sm, max_items));
     const int nkb = (int)(m_pad / KB);
-    if (nkb <= RES_KB)
-        k_corr_tc2<true><<<grid, NWARP2 * 32, SMEM2_BYTES, st>>>(mY, mDh, mDl, mA, off, tile_start, P, (int)K,
-                                                                 nkb, nchunk, alpha, lda);
-    else
-        k_corr_tc2<false><<<grid, NWARP2 * 32, SMEM2_BYTES, st>>>(mY, mDh, mDl, mA, off, tile_start, P, (int)K,
-                                                                  nkb, nchunk, alpha, lda);
+    const Step1 sv = s1 ? *s1 : Step1{};
+    auto fn = nkb <= RES_KB ? (s1 ? k_corr_tc2<true, true> : k_corr_tc2<true, false>)
+                            : (s1 ? k_corr_tc2<false, true> : k_corr_tc2<false, false>);
+    fn<<<grid, NWARP2 * 32, SMEM2_BYTES, st>>>(mY, mDh, mDl, mA, off, tile_start, P, (int)K, nkb, nchunk,
+                                               alpha, lda, sv);
     return (int)cudaGetLastError();
+}
+
+int correlate_tc_f32(int64_t N, const float* Y, int64_t ldy, const int64_t* off, int64_t max_rows,
+                     int P, const float* D, int64_t m, int64_t K, float* alpha, int64_t lda, void* ws,
+                     int64_t ws_bytes, cudaStream_t st) {
+    return corr_tc_launch(N, Y, ldy, off, P, D, m, K, alpha, lda, ws, ws_bytes, nullptr, st);
+}
+
+int code_step1_tc_f32(int64_t N, const float* Y, int64_t ldy, const int64_t* off, int P, const float* D,
+                      int64_t m, int64_t K, float* alpha, int64_t lda, void* ws, int64_t ws_bytes,
+                      const float* ysq, const float* G, float eps, float guard, int cap, int32_t* idx,
+                      float* val, int32_t* counts, int8_t* status, int* n_deferred, cudaStream_t st) {
+    if (K > TN || N > 0x7fffffffll || cap < 1) return (int)cudaErrorNotSupported;
+    Step1 s1;
+    s1.ysq = ysq; s1.G = G; s1.eps2 = eps * eps; s1.guard = guard; s1.cap = cap;
+    s1.idx = idx; s1.val = val; s1.counts = counts; s1.status = status;
+    s1.n_deferred = n_deferred;
+    return corr_tc_launch(N, Y, ldy, off, P, D, m, K, alpha, lda, ws, ws_bytes, &s1, st);
 }
 
 }  // namespace sdb
