@@ -63,7 +63,7 @@ def dist_env():
 class Clocks:
     """nvidia-smi sampled every 200 ms during the timed region."""
 
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    Q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -71,10 +71,26 @@ class Clocks:
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except FileNotFoundError:
             self.p = None
+        self.t0 = self.t1 = None
+
+    def ready(self, timeout: float = 5.0) -> None:
+        """Block until the sampler has written its first line (its start-up
+        NVML queries must not land inside the timed region)."""
+        end = time.time() + timeout
+        while self.p is not None and time.time() < end:
+            if Path(self.f.name).stat().st_size > 0:
+                return
+            time.sleep(0.02)
+
+    def mark(self, start: bool) -> None:
+        if start:
+            self.t0 = time.time()
+        else:
+            self.t1 = time.time()
 
     def stop(self) -> dict:
         if self.p is None:
@@ -85,6 +101,20 @@ class Clocks:
         rows = [r.split(",") for r in Path(self.f.name).read_text().strip().splitlines() if r]
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        timed = []
+        for r in rows:
+            try:
+                ts = time.mktime(time.strptime(r[0].strip().split(".")[0], "%Y/%m/%d %H:%M:%S")) + \
+                    float("0." + r[0].strip().split(".")[1])
+            except (ValueError, IndexError):
+                ts = None
+            if ts is not None and self.t0 is not None and self.t1 is not None and \
+                    self.t0 - 0.05 <= ts <= self.t1 + 0.05:
+                timed.append(r[1:])
+        if timed:
+            rows = timed
+        else:
+            rows = [r[1:] for r in rows]
         for r in rows:
             try:
                 sm.append(float(r[0]))
@@ -96,7 +126,7 @@ class Clocks:
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "window": "timed region" if timed else "whole sampler run"}
 
 
 # ----------------------------------------------------------------- peaks
@@ -237,11 +267,14 @@ def main():
                                   cfg["K"], cfg["s2"], cfg["merge_iters"], args.seed, prec=prec,
                                   groups=args.groups)
 
-    for _ in range(args.warmup):
+    clk = Clocks(local)
+    clk.ready()
+    for w in range(args.warmup):
+        if w == args.warmup - 1:
+            E.KTIMER = {}   # the per-call event path warms up too (its first use is slow)
         r = step()
     codings = r.codings
     # ---- timed region: barrier + sync on both sides, device-timed, max over ranks
-    clk = Clocks(local)
     E.KTIMER = {}
     E.KSTAT.clear()
     E.KSTAT.update(deferred=E.zeros((1,), torch.int64), coded=0)   # allocated before the timed region
@@ -250,6 +283,7 @@ def main():
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    clk.mark(True)
     ev0.record()
     marks = []
     for _ in range(args.steps):
@@ -259,6 +293,7 @@ def main():
         marks.append(e)
     ev1.record()
     torch.cuda.synchronize()
+    clk.mark(False)
     step_ms = [ev0.elapsed_time(marks[0])] + [a.elapsed_time(b) for a, b in zip(marks, marks[1:])]
     print("per-step ms: " + " ".join(f"{x:.2f}" for x in step_ms), file=sys.stderr)
     if world > 1:

@@ -28,7 +28,6 @@ namespace {
 constexpr int TM = 128;      // signals per tile (UMMA M)
 constexpr int TN = 256;      // atoms per chunk (UMMA N)
 constexpr int KB = 32;       // fp32 elements per 128-byte swizzle row
-constexpr int STAGES = 2;
 constexpr int A_BYTES = TM * KB * 4;   // 16 KB
 constexpr int B_BYTES = TN * KB * 4;   // 32 KB
 constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // A_hi, A_lo, B_hi, B_lo
@@ -112,12 +111,22 @@ __device__ __forceinline__ float tf32_rna(float x) {
 //            tfull[b] (MMA commit), tempty[b] (4 epilogue warps),
 //            bfull (resident D landed), bfree (MMA done with resident D).
 // ----------------------------------------------------------------------------
-constexpr int NWARP2 = 10;
+constexpr int NWARP2 = 14;  // warps 10-13: second epilogue half (CODE only)
 constexpr int RES_KB = 2;                           // resident D: up to 2 k-blocks (m <= 64)
 constexpr int RES_A_STAGE = 2 * A_BYTES;             // Y hi + lo
 constexpr int RES_B_BYTES = RES_KB * 2 * B_BYTES;    // D hi + lo, 2 k-blocks
 // + TMA store staging (1024-aligned for the 128-byte swizzle)
 constexpr int SMEM2_BYTES = 2 * STAGE_BYTES + 1024 + 1024 + 4 * 2 * 32 * 32 * 4;
+// shared memory per variant (CODE needs no TMA-store staging; a third Y stage
+// fits there for RES but measured no faster: the MMA is tensor-pipe bound)
+template <bool RES, bool CODE>
+struct Cfg {
+    static constexpr int NST = 2;
+    static constexpr int DATA = RES ? NST * RES_A_STAGE + RES_KB * 2 * B_BYTES : 2 * STAGE_BYTES;
+    static constexpr int XCHG = 4 * 272;                       // CODE: per-quadrant pair exchange
+    static constexpr int SMEM = 1024 + DATA + (CODE ? 256 + XCHG : 1024 + 4 * 2 * 32 * 32 * 4);
+};
+static_assert(Cfg<true, true>::SMEM <= 232448, "smem");
 
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
@@ -144,6 +153,14 @@ __device__ __forceinline__ Item item_of(int64_t it, const int64_t* __restrict__ 
     r.tile = local - (int64_t)r.chunk * nt;
     r.seg = (int64_t)lo * nchunk + r.chunk;
     return r;
+}
+
+// 64 consecutive TMEM columns of the warp's 32 lanes in one instruction
+__device__ __forceinline__ void tmem_ld64(uint32_t (&a)[32], uint32_t (&b)[32], uint32_t taddr) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+        : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3]), "=r"(a[4]), "=r"(a[5]), "=r"(a[6]), "=r"(a[7]), "=r"(a[8]), "=r"(a[9]), "=r"(a[10]), "=r"(a[11]), "=r"(a[12]), "=r"(a[13]), "=r"(a[14]), "=r"(a[15]), "=r"(a[16]), "=r"(a[17]), "=r"(a[18]), "=r"(a[19]), "=r"(a[20]), "=r"(a[21]), "=r"(a[22]), "=r"(a[23]), "=r"(a[24]), "=r"(a[25]), "=r"(a[26]), "=r"(a[27]), "=r"(a[28]), "=r"(a[29]), "=r"(a[30]), "=r"(a[31]), "=r"(b[0]), "=r"(b[1]), "=r"(b[2]), "=r"(b[3]), "=r"(b[4]), "=r"(b[5]), "=r"(b[6]), "=r"(b[7]), "=r"(b[8]), "=r"(b[9]), "=r"(b[10]), "=r"(b[11]), "=r"(b[12]), "=r"(b[13]), "=r"(b[14]), "=r"(b[15]), "=r"(b[16]), "=r"(b[17]), "=r"(b[18]), "=r"(b[19]), "=r"(b[20]), "=r"(b[21]), "=r"(b[22]), "=r"(b[23]), "=r"(b[24]), "=r"(b[25]), "=r"(b[26]), "=r"(b[27]), "=r"(b[28]), "=r"(b[29]), "=r"(b[30]), "=r"(b[31])
+        : "r"(taddr));
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t (&v)[32], uint32_t taddr) {
@@ -212,21 +229,24 @@ __device__ __forceinline__ void block_argmax(const uint32_t (&v)[32], int c, int
     bk = k[0];
 }
 
-// One warp, 32 signal rows (thread = row_base + lane) of a K <= 256 accumulator.
-// diag: warp-private smem copy of the shard's G diagonal (reloaded when the
-// shard changes, *dp = its shard).
+__device__ __forceinline__ void pair_sync(int quad) {
+    // the two epilogue warps of one TMEM lane quadrant (named barrier 1 + quad)
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + quad) : "memory");
+}
+
+// Step-1 epilogue for 32 signal rows (thread = row_base + lane) of a K <= 256
+// accumulator, split over the two warps of the lane quadrant: warp half h
+// scans columns [c_lo, c_hi); the halves meet in shared memory (xv/xk: the
+// upper half's per-row max and key, *xm: the deferred-row mask).
 __device__ __forceinline__ void code_step1(const Step1& s1, uint32_t trow, int64_t row_base, int nrows,
-                                           int p, int K, float* diag, int* dp, float* __restrict__ alpha,
-                                           int64_t lda, int lane) {
+                                           int p, int K, int half, int c_lo, int c_hi,
+                                           float* xv, uint32_t* xk, unsigned* xm, int quad,
+                                           float* __restrict__ alpha, int64_t lda, int lane) {
     const int64_t i = row_base + lane;
     const bool valid = lane < nrows;
-    const float ysq = valid ? __ldg(s1.ysq + i) : 0.0f;      // in flight during the scan
-    if (*dp != p) {
-        __syncwarp();
-        for (int k = lane; k < K; k += 32) diag[k] = __ldg(s1.G + ((int64_t)p * K + k) * K + k);
-        *dp = p;
-    }
-    // ---- argmax |alpha0| over the row
+    float ysq = 0.0f;
+    if (half == 0) ysq = valid ? __ldg(s1.ysq + i) : 0.0f;      // in flight during the scan
+    // ---- argmax |alpha0| over this warp's columns
     float cur = 0.0f;
     uint32_t key = 0xffffffffu;
     uint32_t va[32], vb[32];
@@ -236,88 +256,114 @@ __device__ __forceinline__ void code_step1(const Step1& s1, uint32_t trow, int64
         block_argmax(v, c, K, bv, bk);
         if (bv > cur) { cur = bv; key = bk; }
     };
-    tmem_ld32(va, trow);
-    tmem_wait_ld();
 #pragma unroll 1
-    for (int c = 0; c < K; c += 64) {
-        if (c + 32 < K) tmem_ld32(vb, trow + (uint32_t)(c + 32));
-        scan(va, c);
-        tmem_wait_ld();
-        if (c + 32 >= K) break;
-        if (c + 64 < K) tmem_ld32(va, trow + (uint32_t)(c + 64));
-        scan(vb, c + 32);
-        tmem_wait_ld();
-    }
-    __syncwarp();
-    // ---- the first greedy step (k_omp_fast, step 0)
-    bool defer = false;
-    int n = 0, status = 0, best = 0;
-    float x0 = 0.0f;
-    if (valid) {
-        if (ysq <= s1.eps2 || ysq == 0.0f) {
-            // ||y|| <= eps: no atom
-        } else if (cur * cur <= 1e-26f * ysq) {
-            status = 3;                       // cmax <= 1e-13 ||r|| (also: no candidate)
+    for (int c = c_lo; c < c_hi; c += 64) {
+        if (c + 32 < c_hi) {
+            tmem_ld64(va, vb, trow + (uint32_t)c);
+            tmem_wait_ld();
+            scan(va, c);
+            scan(vb, c + 32);
         } else {
-            best = (int)(key & 0x7fffffffu);
-            const float cb = __uint_as_float(__float_as_uint(cur) | (key & 0x80000000u));
-            const float dsq = diag[best];
-            if (dsq <= s1.guard) {
-                status = 2;
-                best = 0;
-            } else {
-                const float inv = rsqrtf(dsq);
-                const float tn = cb * inv;
-                x0 = tn * inv;
-                n = 1;
-                const float rsq = fmaxf(fmaf(-tn, tn, ysq), 0.0f);
-                if (s1.cap > 1 && (fabsf(rsq - s1.eps2) <= 1e-4f * ysq || rsq > s1.eps2)) defer = true;
-            }
+            tmem_ld32(va, trow + (uint32_t)c);
+            tmem_wait_ld();
+            scan(va, c);
         }
-        if (!defer) {
-            int32_t* ci = s1.idx + i * s1.cap;
-            float* cv = s1.val + i * s1.cap;
-            if ((s1.cap & 3) == 0) {
-                int4* ci4 = reinterpret_cast<int4*>(ci);
-                float4* cv4 = reinterpret_cast<float4*>(cv);
-                ci4[0] = make_int4(best, 0, 0, 0);
-                cv4[0] = make_float4(x0, 0.0f, 0.0f, 0.0f);
-                for (int t = 1; t < (s1.cap >> 2); ++t) {
-                    ci4[t] = make_int4(0, 0, 0, 0);
-                    cv4[t] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-                }
-            } else {
-                for (int t = 0; t < s1.cap; ++t) {
-                    ci[t] = (t < n) ? best : 0;
-                    cv[t] = (t < n) ? x0 : 0.0f;
-                }
-            }
-            s1.counts[i] = n;
-        }
-        s1.status[i] = defer ? (int8_t)-1 : (int8_t)status;
     }
-    // ---- deferred rows: the alpha0 row, each thread its own (8 x 16-byte
-    // stores fill one 128-byte line per 32 columns)
-    const unsigned dmask = __ballot_sync(SDB_FULL, defer);
-    if (dmask == 0u) return;
-    if (lane == 0) atomicAdd(s1.n_deferred, __popc(dmask));   // result unused: a fire-and-forget RED
-    float* out = alpha + i * lda;
-#pragma unroll 1
-    for (int c = 0; c < K; c += 32) {
-        tmem_ld32(va, trow + (uint32_t)c);
-        tmem_wait_ld();
-        if (defer) {
-            if (c + 32 <= K) {
-                float4* o4 = reinterpret_cast<float4*>(out + c);
-#pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    o4[q] = make_float4(__uint_as_float(va[4 * q]), __uint_as_float(va[4 * q + 1]),
-                                        __uint_as_float(va[4 * q + 2]), __uint_as_float(va[4 * q + 3]));
+    // ---- combine the halves (the lower half's columns win ties)
+    if (half == 1) { xv[lane] = cur; xk[lane] = key; }
+    pair_sync(quad);
+    bool defer = false;
+    unsigned dmask;
+    if (half == 0) {
+        const float cu = xv[lane];
+        const uint32_t ku = xk[lane];
+        if (cu > cur) { cur = cu; key = ku; }
+        // ---- the first greedy step (k_omp_fast, step 0)
+        int n = 0, status = 0, best = 0;
+        float x0 = 0.0f;
+        if (valid) {
+            if (ysq <= s1.eps2 || ysq == 0.0f) {
+                // ||y|| <= eps: no atom
+            } else if (cur * cur <= 1e-26f * ysq) {
+                status = 3;                       // cmax <= 1e-13 ||r|| (also: no candidate)
             } else {
-#pragma unroll
-                for (int q = 0; q < 32; ++q)
-                    if (c + q < K) out[c + q] = __uint_as_float(va[q]);
+                best = (int)(key & 0x7fffffffu);
+                const float cb = __uint_as_float(__float_as_uint(cur) | (key & 0x80000000u));
+                const float dsq = __ldg(s1.G + ((int64_t)p * K + best) * K + best);   // L1-resident per shard
+                if (dsq <= s1.guard) {
+                    status = 2;
+                    best = 0;
+                } else {
+                    const float inv = rsqrtf(dsq);
+                    const float tn = cb * inv;
+                    x0 = tn * inv;
+                    n = 1;
+                    const float rsq = fmaxf(fmaf(-tn, tn, ysq), 0.0f);
+                    if (s1.cap > 1 && (fabsf(rsq - s1.eps2) <= 1e-4f * ysq || rsq > s1.eps2)) defer = true;
+                }
             }
+            if (!defer) {
+                int32_t* ci = s1.idx + i * s1.cap;
+                float* cv = s1.val + i * s1.cap;
+                if ((s1.cap & 3) == 0) {
+                    int4* ci4 = reinterpret_cast<int4*>(ci);
+                    float4* cv4 = reinterpret_cast<float4*>(cv);
+                    ci4[0] = make_int4(best, 0, 0, 0);
+                    cv4[0] = make_float4(x0, 0.0f, 0.0f, 0.0f);
+                    for (int t = 1; t < (s1.cap >> 2); ++t) {
+                        ci4[t] = make_int4(0, 0, 0, 0);
+                        cv4[t] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                    }
+                } else {
+                    for (int t = 0; t < s1.cap; ++t) {
+                        ci[t] = (t < n) ? best : 0;
+                        cv[t] = (t < n) ? x0 : 0.0f;
+                    }
+                }
+                s1.counts[i] = n;
+            }
+            s1.status[i] = defer ? (int8_t)-1 : (int8_t)status;
+        }
+        dmask = __ballot_sync(SDB_FULL, defer);
+        if (lane == 0) {
+            *xm = dmask;
+            if (dmask) atomicAdd(s1.n_deferred, __popc(dmask));   // result unused: a fire-and-forget RED
+        }
+    }
+    pair_sync(quad);
+    if (half == 1) {
+        dmask = *xm;
+        defer = (dmask >> lane) & 1u;
+    }
+    // ---- deferred rows: this warp's columns of the alpha0 row, each thread
+    // its own (8 x 16-byte stores fill one 128-byte line per 32 columns)
+    if (dmask == 0u || c_lo >= c_hi) return;
+    float* out = alpha + i * lda;
+    auto put = [&](const uint32_t (&v)[32], int c) {
+        if (!defer) return;
+        if (c + 32 <= K) {
+            float4* o4 = reinterpret_cast<float4*>(out + c);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                o4[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                                    __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+        } else {
+#pragma unroll
+            for (int q = 0; q < 32; ++q)
+                if (c + q < K) out[c + q] = __uint_as_float(v[q]);
+        }
+    };
+#pragma unroll 1
+    for (int c = c_lo; c < c_hi; c += 64) {
+        if (c + 32 < c_hi) {
+            tmem_ld64(va, vb, trow + (uint32_t)c);
+            tmem_wait_ld();
+            put(va, c);
+            put(vb, c + 32);
+        } else {
+            tmem_ld32(va, trow + (uint32_t)c);
+            tmem_wait_ld();
+            put(va, c);
         }
     }
 }
@@ -331,29 +377,36 @@ k_corr_tc2(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUte
            float* __restrict__ alpha, int64_t lda, const Step1 s1) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* base = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    // layout: RES: [A stage 0 | A stage 1 | D resident] ; !RES: [stage 0 | stage 1]
-    unsigned char* bar_base = base + 2 * STAGE_BYTES;
+    constexpr int NST = Cfg<RES, CODE>::NST;
+    // layout: RES: [A stage 0 .. NST-1 | D resident] ; !RES: [stage 0 | stage 1]
+    unsigned char* bar_base = base + Cfg<RES, CODE>::DATA;
     uint64_t* bars = (uint64_t*)bar_base;
-    // full[0..1], split[2..3], empty[4..5], tfull[6..7], tempty[8..9], bfull[10], bfree[11]
-    uint32_t* tmem_slot = (uint32_t*)(bars + 12);
+    // full[s] = s, split[s] = NST + s, empty[s] = 2 NST + s, tfull[b] = 3 NST + b,
+    // tempty[b] = 3 NST + 2 + b, bfull = 3 NST + 4, bfree = 3 NST + 5
+    constexpr int B_SPLIT = NST, B_EMPTY = 2 * NST, B_TFULL = 3 * NST, B_TEMPTY = 3 * NST + 2;
+    constexpr int B_BFULL = 3 * NST + 4, B_BFREE = 3 * NST + 5;
+    uint32_t* tmem_slot = (uint32_t*)(bars + 3 * NST + 6);
     // epilogue staging for TMA stores: 4 warps x 2 buffers x 32x32 fp32,
-    // 128-byte swizzled (row r's 16-byte chunk c at c ^ (r & 7))
-    float* stg_base = reinterpret_cast<float*>(bar_base + 1024);
+    // 128-byte swizzled (row r's 16-byte chunk c at c ^ (r & 7)); CODE: the
+    // pair exchange slots instead
+    float* stg_base = reinterpret_cast<float*>(bar_base + (CODE ? 256 : 1024));
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t n_items = tile_start[P] * nchunk;
     const int64_t per = (n_items + gridDim.x - 1) / gridDim.x;
     const int64_t it0 = (int64_t)blockIdx.x * per, it1 = min(n_items, it0 + per);
 
     if (tid == 0) {
-        for (int s = 0; s < STAGES; ++s) {
+        for (int s = 0; s < NST; ++s) {
             mbar_init(smem_u32(&bars[s]), 1);
-            mbar_init(smem_u32(&bars[2 + s]), 4);
-            mbar_init(smem_u32(&bars[4 + s]), 1);
-            mbar_init(smem_u32(&bars[6 + s]), 1);
-            mbar_init(smem_u32(&bars[8 + s]), 4);
+            mbar_init(smem_u32(&bars[B_SPLIT + s]), 4);
+            mbar_init(smem_u32(&bars[B_EMPTY + s]), 1);
         }
-        mbar_init(smem_u32(&bars[10]), 1);
-        mbar_init(smem_u32(&bars[11]), 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(smem_u32(&bars[B_TFULL + b]), 1);
+            mbar_init(smem_u32(&bars[B_TEMPTY + b]), CODE ? 8 : 4);
+        }
+        mbar_init(smem_u32(&bars[B_BFULL]), 1);
+        mbar_init(smem_u32(&bars[B_BFREE]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -371,7 +424,7 @@ k_corr_tc2(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUte
     auto a_hi = [&](int s) -> unsigned char* { return RES ? base + s * RES_A_STAGE : base + s * STAGE_BYTES; };
     auto a_lo = [&](int s) -> unsigned char* { return a_hi(s) + A_BYTES; };
     auto b_hi = [&](int s, int kb) -> unsigned char* {
-        return RES ? base + 2 * RES_A_STAGE + kb * 2 * B_BYTES : base + s * STAGE_BYTES + 2 * A_BYTES;
+        return RES ? base + NST * RES_A_STAGE + kb * 2 * B_BYTES : base + s * STAGE_BYTES + 2 * A_BYTES;
     };
     auto b_lo = [&](int s, int kb) -> unsigned char* { return b_hi(s, kb) + B_BYTES; };
 
@@ -384,8 +437,8 @@ k_corr_tc2(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUte
                 const int64_t row0 = off[I.p] + I.tile * TM;
                 const int64_t d_row0 = (int64_t)I.p * K + (int64_t)I.chunk * TN;
                 if (RES && I.seg != seg_prev) {
-                    if (nseg > 0) mbar_wait(smem_u32(&bars[11]), (uint32_t)((nseg - 1) & 1));
-                    const uint32_t bf = smem_u32(&bars[10]);
+                    if (nseg > 0) mbar_wait(smem_u32(&bars[B_BFREE]), (uint32_t)((nseg - 1) & 1));
+                    const uint32_t bf = smem_u32(&bars[B_BFULL]);
                     mbar_expect_tx(bf, (uint32_t)(nkb * 2 * B_BYTES));
                     for (int kb = 0; kb < nkb; ++kb) {
                         tma_load_2d(smem_u32(b_hi(0, kb)), &tmDh, kb * KB, (int)d_row0, bf);
@@ -395,9 +448,9 @@ k_corr_tc2(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUte
                     ++nseg;
                 }
                 for (int kb = 0; kb < nkb; ++kb, ++q) {
-                    const int s = (int)(q % STAGES);
-                    const int64_t use = q / STAGES;
-                    if (use > 0) mbar_wait(smem_u32(&bars[4 + s]), (uint32_t)((use - 1) & 1));
+                    const int s = (int)(q % NST);
+                    const int64_t use = q / NST;
+                    if (use > 0) mbar_wait(smem_u32(&bars[B_EMPTY + s]), (uint32_t)((use - 1) & 1));
                     const uint32_t full = smem_u32(&bars[s]);
                     mbar_expect_tx(full, RES ? A_BYTES : A_BYTES + 2 * B_BYTES);
                     tma_load_2d(smem_u32(a_hi(s)), &tmY, kb * KB, (int)row0, full);
@@ -419,16 +472,16 @@ k_corr_tc2(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUte
             const int64_t buse = n >> 1;
             if (lane == 0) {
                 if (RES && I.seg != seg_prev) {
-                    mbar_wait(smem_u32(&bars[10]), (uint32_t)(nseg & 1));
+                    mbar_wait(smem_u32(&bars[B_BFULL]), (uint32_t)(nseg & 1));
                     seg_prev = I.seg;
                     ++nseg;
                 }
-                if (buse > 0) mbar_wait(smem_u32(&bars[8 + b]), (uint32_t)((buse - 1) & 1));
+                if (buse > 0) mbar_wait(smem_u32(&bars[B_TEMPTY + b]), (uint32_t)((buse - 1) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t tacc = tmem + (uint32_t)(b * TN);
                 for (int kb = 0; kb < nkb; ++kb, ++q) {
-                    const int s = (int)(q % STAGES);
-                    mbar_wait(smem_u32(&bars[2 + s]), (uint32_t)((q / STAGES) & 1));
+                    const int s = (int)(q % NST);
+                    mbar_wait(smem_u32(&bars[B_SPLIT + s]), (uint32_t)((q / NST) & 1));
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     const uint64_t dah = sw128_desc(smem_u32(a_hi(s)));
                     const uint64_t dal = sw128_desc(smem_u32(a_lo(s)));
@@ -442,31 +495,32 @@ k_corr_tc2(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUte
                         mma_tf32(tacc, dah + adv, dbl + adv, idesc, 1u);
                         mma_tf32(tacc, dal + adv, dbh + adv, idesc, 1u);
                     }
-                    mma_commit(smem_u32(&bars[4 + s]));                     // stage free
-                    if (kb == nkb - 1) mma_commit(smem_u32(&bars[6 + b]));  // accumulator ready
+                    mma_commit(smem_u32(&bars[B_EMPTY + s]));               // stage free
+                    if (kb == nkb - 1) mma_commit(smem_u32(&bars[B_TFULL + b]));  // accumulator ready
                 }
                 if (RES) {  // resident D no longer needed after this item?
                     const bool last = (it + 1 >= it1) || item_of(it + 1, tile_start, P, nchunk).seg != I.seg;
-                    if (last) mma_commit(smem_u32(&bars[11]));
+                    if (last) mma_commit(smem_u32(&bars[B_BFREE]));
                 }
             }
             __syncwarp();
         }
-    } else if (warp >= 2 && warp < 6) {
+    } else if ((warp >= 2 && warp < 6) || (CODE && warp >= 10)) {
         // ---------------- epilogue (TMEM lane quadrant = warp % 4): thread =
         // signal row; each 32x32 block is staged in smem and written by one
         // TMA store (async, full lines); quadrants straddling a shard end use
         // plain stores so rows of the next shard are never touched
         const int quad = warp & 3;
-        float* stg = stg_base + (warp - 2) * 2 * 1024;
-        int diag_shard = -1;                    // CODE: shard whose G diagonal is in stg
-        int* diag_p = &diag_shard;
+        const int half = warp >= 10 ? 1 : 0;
+        float* stg = stg_base + (warp - 2) * 2 * 1024;     // !CODE only
+        float* xch = stg_base + quad * 68;                 // CODE: the quadrant pair's exchange slots
+        const int c_mid = ((K + 63) / 64) * 32;
         int64_t n = 0;
         int sb = 0;  // staging buffer toggle
         for (int64_t it = it0; it < it1; ++it, ++n) {
             const Item I = item_of(it, tile_start, P, nchunk);
             const int b = (int)(n & 1);
-            mbar_wait(smem_u32(&bars[6 + b]), (uint32_t)((n >> 1) & 1));
+            mbar_wait(smem_u32(&bars[B_TFULL + b]), (uint32_t)((n >> 1) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const int64_t s_hi = off[I.p + 1];
             const int64_t row_base = off[I.p] + I.tile * TM + quad * 32;
@@ -475,10 +529,12 @@ k_corr_tc2(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUte
             const int ncols = min(TN, K - n0);
             const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * TN);
             if constexpr (CODE) {
-                code_step1(s1, trow, row_base, nrows, I.p, K, stg, diag_p, alpha, lda, lane);
+                code_step1(s1, trow, row_base, nrows, I.p, K, half, half ? c_mid : 0, half ? K : min(c_mid, K),
+                           xch, reinterpret_cast<uint32_t*>(xch + 32), reinterpret_cast<unsigned*>(xch + 64),
+                           quad, alpha, lda, lane);
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 __syncwarp();
-                if (lane == 0) mbar_arrive(smem_u32(&bars[8 + b]));
+                if (lane == 0) mbar_arrive(smem_u32(&bars[B_TEMPTY + b]));
                 continue;
             }
             // one 32x32 block: TMA store from swizzled staging (conflict-free
@@ -529,18 +585,18 @@ k_corr_tc2(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUte
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(&bars[8 + b]));
+            if (lane == 0) mbar_arrive(smem_u32(&bars[B_TEMPTY + b]));
         }
         if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
         __syncwarp();
-    } else {
+    } else if (warp >= 6 && warp < 10) {
         // ---------------- 3xTF32 split of the Y k-block (warps 6-9)
         const int st = tid - 6 * 32;  // 0..127
         int64_t q = 0;
         for (int64_t it = it0; it < it1; ++it) {
             for (int kb = 0; kb < nkb; ++kb, ++q) {
-                const int s = (int)(q % STAGES);
-                mbar_wait(smem_u32(&bars[s]), (uint32_t)((q / STAGES) & 1));
+                const int s = (int)(q % NST);
+                mbar_wait(smem_u32(&bars[s]), (uint32_t)((q / NST) & 1));
                 float4* ah = (float4*)a_hi(s);
                 float4* al = (float4*)a_lo(s);
 #pragma unroll
@@ -556,7 +612,7 @@ k_corr_tc2(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUte
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
-                if (lane == 0) mbar_arrive(smem_u32(&bars[2 + s]));
+                if (lane == 0) mbar_arrive(smem_u32(&bars[B_SPLIT + s]));
             }
         }
     }
@@ -659,10 +715,14 @@ static int corr_tc_launch(int64_t N, const float* Y, int64_t ldy, const int64_t*
     static bool attr = false;
     static int n_sm = 148;
     if (!attr) {
-        cudaFuncSetAttribute(k_corr_tc2<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES);
-        cudaFuncSetAttribute(k_corr_tc2<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES);
-        cudaFuncSetAttribute(k_corr_tc2<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES);
-        cudaFuncSetAttribute(k_corr_tc2<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES);
+        cudaFuncSetAttribute(k_corr_tc2<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Cfg<true, false>::SMEM);
+        cudaFuncSetAttribute(k_corr_tc2<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Cfg<false, false>::SMEM);
+        cudaFuncSetAttribute(k_corr_tc2<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Cfg<true, true>::SMEM);
+        cudaFuncSetAttribute(k_corr_tc2<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Cfg<false, true>::SMEM);
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
@@ -679,7 +739,9 @@ static int corr_tc_launch(int64_t N, const float* Y, int64_t ldy, const int64_t*
     const Step1 sv = s1 ? *s1 : Step1{};
     auto fn = nkb <= RES_KB ? (s1 ? k_corr_tc2<true, true> : k_corr_tc2<true, false>)
                             : (s1 ? k_corr_tc2<false, true> : k_corr_tc2<false, false>);
-    fn<<<grid, NWARP2 * 32, SMEM2_BYTES, st>>>(mY, mDh, mDl, mA, off, tile_start, P, (int)K, nkb, nchunk,
+    const int smem = nkb <= RES_KB ? (s1 ? Cfg<true, true>::SMEM : Cfg<true, false>::SMEM)
+                                   : (s1 ? Cfg<false, true>::SMEM : Cfg<false, false>::SMEM);
+    fn<<<grid, NWARP2 * 32, smem, st>>>(mY, mDh, mDl, mA, off, tile_start, P, (int)K, nkb, nchunk,
                                                alpha, lda, sv);
     return (int)cudaGetLastError();
 }

@@ -52,6 +52,13 @@ for _ in range(args.reps):
     c = run()
 b.record()
 torch.cuda.synchronize()
+E.KTIMER = {}
+for _ in range(args.reps):
+    run()
+torch.cuda.synchronize()
+kt, E.KTIMER = E.KTIMER, None
+per = {k: sum(x.elapsed_time(y) for x, y, _, _ in v) / len(v) for k, v in kt.items()}
+print("per launch (ms): " + ", ".join(f"{k} {v:.3f}" for k, v in per.items()))
 cnt = c.counts.cpu().numpy()
 print(f"{'plain' if args.plain else 'fused'}: {a.elapsed_time(b) / args.reps:.3f} ms per pass; "
       f"mean n {cnt.mean():.3f}, n>=2 {(cnt >= 2).mean():.3f}, hist {np.bincount(cnt)[:6].tolist()}")
