@@ -363,6 +363,16 @@ def main():
                     "note": "3xTF32 issues 3 MMAs per useful product (achieved counts all 3)"}
         roof["traffic_note"] = ("ncu dram read+write per launch of one C2 local pass (2,040,200 "
                                 "signals), profiles/ncu_*_raw.txt")
+    omp_roof = None
+    oname = "omp_deferred" if "omp_deferred" in kt else ("omp" if "omp" in kt else None)
+    if oname:
+        d = breakdown[oname]
+        omp_roof = {"kernel": kernel_of[oname], "bound": "hbm", "achieved": d["GBps"], "peak": hbm,
+                    "unit": "GB/s", "frac": d["GBps"] / hbm, "traffic": ncu.get(kernel_of[oname]),
+                    "share_of_step": d["ms_per_step"] / ms,
+                    "algorithmic_bytes_per_signal": omp_b + (8 if oname == "omp_deferred" else 0),
+                    "note": "signals needing >= 2 atoms only (the fused GEMM epilogue settles the rest); "
+                            "issue/latency bound, not HBM bound"}
     gemm = None
     gname = "step1" if "step1" in kt else ("correlate" if "correlate" in kt else None)
     if gname:
@@ -420,7 +430,7 @@ def main():
                        "phase_s": {"split": r.split_s, "locals": r.local_s, "merge": r.merge_s},
                        "precision": prec, "parallelism": f"shards over {world} GPU(s)",
                        "l2": "inputs larger than L2 (Y is %.0f MB)" % (N * m * 4 / 1e6)},
-            "roofline": roof, "roofline_gemm": gemm, "kernels": breakdown, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "roofline_gemm": gemm, "roofline_omp": omp_roof, "kernels": breakdown, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": gpu_launches, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
