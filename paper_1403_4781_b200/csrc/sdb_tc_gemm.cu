@@ -123,7 +123,7 @@ template <bool RES, bool CODE>
 struct Cfg {
     static constexpr int NST = 2;
     static constexpr int DATA = RES ? NST * RES_A_STAGE + RES_KB * 2 * B_BYTES : 2 * STAGE_BYTES;
-    static constexpr int XCHG = 4 * 272;                       // CODE: per-quadrant pair exchange
+    static constexpr int XCHG = 4 * 272 + 4 * 1024;            // CODE: pair exchange + per-warp G diagonal
     static constexpr int SMEM = 1024 + DATA + (CODE ? 256 + XCHG : 1024 + 4 * 2 * 32 * 32 * 4);
 };
 static_assert(Cfg<true, true>::SMEM <= 232448, "smem");
@@ -207,15 +207,15 @@ __device__ __forceinline__ void tmem_wait_ld() {
 // the maximum, as the reference's ascending scan gives); NaN and columns
 // past K enter as 0, which can never be selected (selection needs > 0).
 // key = column | sign bit of alpha0.
+template <bool FULL>
 __device__ __forceinline__ void block_argmax(const uint32_t (&v)[32], int c, int K, float& bv, uint32_t& bk) {
     float a[32];
     uint32_t k[32];
-    const bool full = c + 32 <= K;
 #pragma unroll
     for (int t = 0; t < 32; ++t) {
         const float x = __uint_as_float(v[t]);
-        a[t] = (full || c + t < K) ? fmaxf(fabsf(x), 0.0f) : 0.0f;
-        k[t] = (uint32_t)(c + t) | (v[t] & 0x80000000u);
+        a[t] = (FULL || c + t < K) ? fmaxf(fabsf(x), 0.0f) : 0.0f;
+        k[t] = (uint32_t)t | (v[t] & 0x80000000u);       // block column | sign
     }
 #pragma unroll
     for (int w = 1; w < 32; w <<= 1)
@@ -226,7 +226,7 @@ __device__ __forceinline__ void block_argmax(const uint32_t (&v)[32], int c, int
             k[t] = r ? k[t + w] : k[t];
         }
     bv = a[0];
-    bk = k[0];
+    bk = k[0] + (uint32_t)c;
 }
 
 __device__ __forceinline__ void pair_sync(int quad) {
@@ -240,12 +240,11 @@ __device__ __forceinline__ void pair_sync(int quad) {
 // upper half's per-row max and key, *xm: the deferred-row mask).
 __device__ __forceinline__ void code_step1(const Step1& s1, uint32_t trow, int64_t row_base, int nrows,
                                            int p, int K, int half, int c_lo, int c_hi,
-                                           float* xv, uint32_t* xk, unsigned* xm, int quad,
+                                           float* xv, uint32_t* xk, unsigned* xm, const float* diag,
+                                           float ysq, int quad,
                                            float* __restrict__ alpha, int64_t lda, int lane) {
     const int64_t i = row_base + lane;
     const bool valid = lane < nrows;
-    float ysq = 0.0f;
-    if (half == 0) ysq = valid ? __ldg(s1.ysq + i) : 0.0f;      // in flight during the scan
     // ---- argmax |alpha0| over this warp's columns
     float cur = 0.0f;
     uint32_t key = 0xffffffffu;
@@ -253,20 +252,23 @@ __device__ __forceinline__ void code_step1(const Step1& s1, uint32_t trow, int64
     auto scan = [&](const uint32_t (&v)[32], int c) {
         float bv;
         uint32_t bk;
-        block_argmax(v, c, K, bv, bk);
+        if (c + 32 <= K) block_argmax<true>(v, c, K, bv, bk);   // warp-uniform
+        else block_argmax<false>(v, c, K, bv, bk);
         if (bv > cur) { cur = bv; key = bk; }
     };
+    // 32-column blocks, the next block's TMEM load in flight during each scan
+    if (c_lo < c_hi) {
+        tmem_ld32(va, trow + (uint32_t)c_lo);
+        tmem_wait_ld();
 #pragma unroll 1
-    for (int c = c_lo; c < c_hi; c += 64) {
-        if (c + 32 < c_hi) {
-            tmem_ld64(va, vb, trow + (uint32_t)c);
-            tmem_wait_ld();
+        for (int c = c_lo; c < c_hi; c += 64) {
+            if (c + 32 < c_hi) tmem_ld32(vb, trow + (uint32_t)(c + 32));
             scan(va, c);
+            tmem_wait_ld();
+            if (c + 32 >= c_hi) break;
+            if (c + 64 < c_hi) tmem_ld32(va, trow + (uint32_t)(c + 64));
             scan(vb, c + 32);
-        } else {
-            tmem_ld32(va, trow + (uint32_t)c);
             tmem_wait_ld();
-            scan(va, c);
         }
     }
     // ---- combine the halves (the lower half's columns win ties)
@@ -278,7 +280,8 @@ __device__ __forceinline__ void code_step1(const Step1& s1, uint32_t trow, int64
         const float cu = xv[lane];
         const uint32_t ku = xk[lane];
         if (cu > cur) { cur = cu; key = ku; }
-        // ---- the first greedy step (k_omp_fast, step 0)
+        // ---- the first greedy step (k_omp_fast, step 0); the deferral mask
+        // is published before any store, so the upper warp is released early
         int n = 0, status = 0, best = 0;
         float x0 = 0.0f;
         if (valid) {
@@ -289,7 +292,7 @@ __device__ __forceinline__ void code_step1(const Step1& s1, uint32_t trow, int64
             } else {
                 best = (int)(key & 0x7fffffffu);
                 const float cb = __uint_as_float(__float_as_uint(cur) | (key & 0x80000000u));
-                const float dsq = __ldg(s1.G + ((int64_t)p * K + best) * K + best);   // L1-resident per shard
+                const float dsq = diag[best];
                 if (dsq <= s1.guard) {
                     status = 2;
                     best = 0;
@@ -302,6 +305,12 @@ __device__ __forceinline__ void code_step1(const Step1& s1, uint32_t trow, int64
                     if (s1.cap > 1 && (fabsf(rsq - s1.eps2) <= 1e-4f * ysq || rsq > s1.eps2)) defer = true;
                 }
             }
+        }
+        dmask = __ballot_sync(SDB_FULL, defer);
+        if (lane == 0) *xm = dmask;
+        pair_sync(quad);
+        if (lane == 0 && dmask) atomicAdd(s1.n_deferred, __popc(dmask));   // result unused: a fire-and-forget RED
+        if (valid) {
             if (!defer) {
                 int32_t* ci = s1.idx + i * s1.cap;
                 float* cv = s1.val + i * s1.cap;
@@ -324,13 +333,9 @@ __device__ __forceinline__ void code_step1(const Step1& s1, uint32_t trow, int64
             }
             s1.status[i] = defer ? (int8_t)-1 : (int8_t)status;
         }
-        dmask = __ballot_sync(SDB_FULL, defer);
-        if (lane == 0) {
-            *xm = dmask;
-            if (dmask) atomicAdd(s1.n_deferred, __popc(dmask));   // result unused: a fire-and-forget RED
-        }
+    } else {
+        pair_sync(quad);
     }
-    pair_sync(quad);
     if (half == 1) {
         dmask = *xm;
         defer = (dmask >> lane) & 1u;
@@ -514,12 +519,30 @@ k_corr_tc2(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUte
         const int half = warp >= 10 ? 1 : 0;
         float* stg = stg_base + (warp - 2) * 2 * 1024;     // !CODE only
         float* xch = stg_base + quad * 68;                 // CODE: the quadrant pair's exchange slots
+        float* diag = stg_base + 4 * 68 + quad * 256;      // CODE: lower warp's copy of the shard's G diagonal
+        int diag_p = -1;
         const int c_mid = ((K + 63) / 64) * 32;
         int64_t n = 0;
         int sb = 0;  // staging buffer toggle
         for (int64_t it = it0; it < it1; ++it, ++n) {
             const Item I = item_of(it, tile_start, P, nchunk);
             const int b = (int)(n & 1);
+            // CODE: ||y||^2 of this warp's rows and the shard's G diagonal are
+            // fetched before the accumulator is waited for (their latency then
+            // overlaps the MMA instead of the epilogue)
+            float ysq_pre = 0.0f;
+            if constexpr (CODE) {
+                if (half == 0) {
+                    const int64_t r = off[I.p] + I.tile * TM + quad * 32 + lane;
+                    if (r < off[I.p + 1]) ysq_pre = __ldg(s1.ysq + r);
+                    if (diag_p != I.p) {
+                        __syncwarp();
+                        for (int k = lane; k < K; k += 32) diag[k] = __ldg(s1.G + ((int64_t)I.p * K + k) * K + k);
+                        diag_p = I.p;
+                        __syncwarp();
+                    }
+                }
+            }
             mbar_wait(smem_u32(&bars[B_TFULL + b]), (uint32_t)((n >> 1) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const int64_t s_hi = off[I.p + 1];
@@ -531,7 +554,7 @@ k_corr_tc2(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUte
             if constexpr (CODE) {
                 code_step1(s1, trow, row_base, nrows, I.p, K, half, half ? c_mid : 0, half ? K : min(c_mid, K),
                            xch, reinterpret_cast<uint32_t*>(xch + 32), reinterpret_cast<unsigned*>(xch + 64),
-                           quad, alpha, lda, lane);
+                           diag, ysq_pre, quad, alpha, lda, lane);
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 __syncwarp();
                 if (lane == 0) mbar_arrive(smem_u32(&bars[B_TEMPTY + b]));
@@ -761,6 +784,7 @@ int code_step1_tc_f32(int64_t N, const float* Y, int64_t ldy, const int64_t* off
     s1.ysq = ysq; s1.G = G; s1.eps2 = eps * eps; s1.guard = guard; s1.cap = cap;
     s1.idx = idx; s1.val = val; s1.counts = counts; s1.status = status;
     s1.n_deferred = n_deferred;
+
     return corr_tc_launch(N, Y, ldy, off, P, D, m, K, alpha, lda, ws, ws_bytes, &s1, st);
 }
 
