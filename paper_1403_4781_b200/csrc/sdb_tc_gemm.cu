@@ -202,30 +202,30 @@ __device__ __forceinline__ void tmem_wait_ld() {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// argmax over one 32-column block of a row: a pairwise tree (the left,
-// lower-index operand wins ties, so the result is the lowest index attaining
-// the maximum, as the reference's ascending scan gives); NaN and columns
-// past K enter as 0, which can never be selected (selection needs > 0).
-// key = column | sign bit of alpha0.
+// argmax |x| over one 32-column block of a row: a pairwise tree on the raw
+// values compared by magnitude (the left, lower-index operand wins ties, so
+// the result is the lowest index attaining the maximum, as the reference's
+// ascending scan gives). Columns past K enter as 0, which is never selected
+// (selection needs |x| > the running maximum >= 0). alpha0 is finite here:
+// rows whose ||y||^2 is not finite are deferred before this is consulted.
 template <bool FULL>
-__device__ __forceinline__ void block_argmax(const uint32_t (&v)[32], int c, int K, float& bv, uint32_t& bk) {
+__device__ __forceinline__ void block_argmax(const uint32_t (&v)[32], int c, int K, float& bx, uint32_t& bk) {
     float a[32];
     uint32_t k[32];
 #pragma unroll
     for (int t = 0; t < 32; ++t) {
-        const float x = __uint_as_float(v[t]);
-        a[t] = (FULL || c + t < K) ? fmaxf(fabsf(x), 0.0f) : 0.0f;
-        k[t] = (uint32_t)t | (v[t] & 0x80000000u);       // block column | sign
+        a[t] = (FULL || c + t < K) ? __uint_as_float(v[t]) : 0.0f;
+        k[t] = (uint32_t)t;
     }
 #pragma unroll
     for (int w = 1; w < 32; w <<= 1)
 #pragma unroll
         for (int t = 0; t < 32; t += 2 * w) {
-            const bool r = a[t + w] > a[t];
+            const bool r = fabsf(a[t + w]) > fabsf(a[t]);
             a[t] = r ? a[t + w] : a[t];
             k[t] = r ? k[t + w] : k[t];
         }
-    bv = a[0];
+    bx = a[0];
     bk = k[0] + (uint32_t)c;
 }
 
@@ -246,15 +246,15 @@ __device__ __forceinline__ void code_step1(const Step1& s1, uint32_t trow, int64
     const int64_t i = row_base + lane;
     const bool valid = lane < nrows;
     // ---- argmax |alpha0| over this warp's columns
-    float cur = 0.0f;
+    float cur = 0.0f, cx = 0.0f;      // running max |alpha0|, its signed value
     uint32_t key = 0xffffffffu;
     uint32_t va[32], vb[32];
     auto scan = [&](const uint32_t (&v)[32], int c) {
-        float bv;
+        float bx;
         uint32_t bk;
-        if (c + 32 <= K) block_argmax<true>(v, c, K, bv, bk);   // warp-uniform
-        else block_argmax<false>(v, c, K, bv, bk);
-        if (bv > cur) { cur = bv; key = bk; }
+        if (c + 32 <= K) block_argmax<true>(v, c, K, bx, bk);   // warp-uniform
+        else block_argmax<false>(v, c, K, bx, bk);
+        if (fabsf(bx) > cur) { cur = fabsf(bx); cx = bx; key = bk; }
     };
     // 32-column blocks, the next block's TMEM load in flight during each scan
     if (c_lo < c_hi) {
@@ -272,14 +272,14 @@ __device__ __forceinline__ void code_step1(const Step1& s1, uint32_t trow, int64
         }
     }
     // ---- combine the halves (the lower half's columns win ties)
-    if (half == 1) { xv[lane] = cur; xk[lane] = key; }
+    if (half == 1) { xv[lane] = cx; xk[lane] = key; }
     pair_sync(quad);
     bool defer = false;
     unsigned dmask;
     if (half == 0) {
         const float cu = xv[lane];
         const uint32_t ku = xk[lane];
-        if (cu > cur) { cur = cu; key = ku; }
+        if (fabsf(cu) > cur) { cur = fabsf(cu); cx = cu; key = ku; }
         // ---- the first greedy step (k_omp_fast, step 0); the deferral mask
         // is published before any store, so the upper warp is released early
         int n = 0, status = 0, best = 0;
@@ -287,11 +287,13 @@ __device__ __forceinline__ void code_step1(const Step1& s1, uint32_t trow, int64
         if (valid) {
             if (ysq <= s1.eps2 || ysq == 0.0f) {
                 // ||y|| <= eps: no atom
+            } else if (!(ysq <= 3.0e38f)) {
+                defer = true;                     // ||y||^2 not finite: alpha0 may be too; k_omp_fast decides
             } else if (cur * cur <= 1e-26f * ysq) {
                 status = 3;                       // cmax <= 1e-13 ||r|| (also: no candidate)
             } else {
-                best = (int)(key & 0x7fffffffu);
-                const float cb = __uint_as_float(__float_as_uint(cur) | (key & 0x80000000u));
+                best = (int)key;
+                const float cb = cx;
                 const float dsq = diag[best];
                 if (dsq <= s1.guard) {
                     status = 2;

@@ -4,7 +4,8 @@ same. The fused GEMM epilogue runs omp_single's first iteration
 (_kernels.py:61-154) per signal row and defers the rest to the list-driven
 OMP kernel, so every branch of that first step is exercised here: ||y|| <=
 eps (including zero signals), one-atom stops, signals within the explicit-
-residual band around eps, multi-atom signals, cap = 1, ragged shards whose
+residual band around eps, multi-atom signals, ||y||^2 past the FP32 range,
+cap = 1, ragged shards whose
 ends straddle 32-row quadrants and 128-row tiles, K < 256 and K not a
 multiple of 32.
 """
@@ -16,7 +17,7 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-def _data(m, K, sizes, seed):
+def _data(m, K, sizes, seed, huge=True):
     rng = np.random.default_rng(seed)
     P, N = len(sizes), sum(sizes)
     D = rng.standard_normal((P, K, m))
@@ -24,6 +25,8 @@ def _data(m, K, sizes, seed):
     off = np.concatenate([[0], np.cumsum(sizes)])
     Y = np.empty((N, m))
     kind = rng.integers(0, 5, N)
+    if huge:
+        kind[rng.random(N) < 0.01] = 5
     for p in range(P):
         for i in range(off[p], off[p + 1]):
             k = kind[i]
@@ -37,8 +40,10 @@ def _data(m, K, sizes, seed):
                 Y[i] = (rng.standard_normal(s) * 10) @ D[p, sup] + rng.standard_normal(m) * 0.3
             elif k == 3:    # exact atom (one step, residual ~0)
                 Y[i] = 7.0 * D[p, rng.integers(K)]
-            else:           # zero signal
+            elif k == 4:    # zero signal
                 Y[i] = 0.0
+            else:           # ||y||^2 overflows FP32: deferred by the fused epilogue
+                Y[i] = 3e19 * D[p, rng.integers(K)] + 1e18 * rng.standard_normal(m)
     return Y, D, off
 
 
@@ -102,7 +107,7 @@ def test_fused_vs_oracle_supports():
     """Cross-check with the CPU oracle (FP64 restatement of _kernels.py) on
     the FP32-rounded inputs: identical supports on >= 99.9% of signals."""
     from oracle import oracle as O
-    Y, D, off = _data(64, 256, [1500, 1500], seed=5)
+    Y, D, off = _data(64, 256, [1500, 1500], seed=5, huge=False)   # FP32 range only
     sizes = [1500, 1500]
     eps = float(np.sqrt(64) * 0.9)
     idx, val, counts, status = _code(Y, D, sizes, 16, eps, fused=True)
