@@ -148,7 +148,7 @@ def ncu_traffic() -> dict:
             parts = line.split()
             if line.startswith("Kernel Name"):
                 name = None
-                for base, tag in (("k_omp_fast", "k_omp_fast<LIST>"), ("k_corr_tc2", "k_corr_tc2<CODE>")):
+                for base, tag in (("k_omp_fast", "k_omp_fast<DEFER>"), ("k_corr_tc2", "k_corr_tc2<CODE>")):
                     if base + "<" in line:
                         targs = line.split(base + "<", 1)[1].split(">", 1)[0].replace(" ", "").split(",")
                         name = tag if len(targs) >= 2 and targs[-1] in ("1", "true") else base
@@ -338,7 +338,7 @@ def main():
     if coded:
         breakdown["omp_deferred"]["deferred_fraction"] = deferred / coded
     # dominant single kernel (mod_update / replace are multi-kernel pipelines)
-    kernel_of = {"omp": "k_omp_fast", "omp_deferred": "k_omp_fast<LIST>",
+    kernel_of = {"omp": "k_omp_fast", "omp_deferred": "k_omp_fast<DEFER>",
                  "correlate": "k_corr_tc2", "step1": "k_corr_tc2<CODE>"}
     singles = {k: v for k, v in breakdown.items() if k in kernel_of}
     dom = max(singles, key=lambda k: singles[k]["ms_per_step"]) if singles else None
