@@ -204,7 +204,9 @@ def coding_mode(m: int, K: int, s: int, eps, s_max) -> tuple[int, float]:
 
 
 USE_GRAPHS = True   # small jobs replay a cached graph (captured once per shape)
-GRAPH_MAX_N = 262144
+# jobs up to this many signals replay a graph per iteration (the static copy of
+# the signals costs one device copy per training; larger jobs launch eagerly)
+GRAPH_MAX_N = int(os.environ.get("SDB_GRAPH_MAX_N", str(1 << 23)))
 
 
 def _iteration(S: E.ShardSet, D: torch.Tensor, cap: int, eps: float, use_tc: bool):
@@ -223,7 +225,8 @@ class _GraphedLoop:
     later call with the same shapes: the inputs (signals, initial
     dictionary) are copied in, ||y||^2 recomputed in place, and the graph is
     replayed once per iteration. The merge phase is host-launch bound
-    (~40 small launches per iteration), which a replay removes."""
+    (~40 small launches per iteration), which a replay removes; in the local
+    phase it removes the inter-launch gaps and most of the host enqueue."""
 
     def __init__(self, S: E.ShardSet, D0: torch.Tensor, cap: int, eps: float, use_tc: bool):
         self.S = E.ShardSet(S.Y.clone(), S.off.clone(), list(S.sizes), S.prec)
@@ -273,6 +276,8 @@ def train_device(S: E.ShardSet, D0: torch.Tensor, cap: int, eps: float, iteratio
     P = D0.shape[0]
     resid = E.empty((iterations, P), torch.float64)
     graph = (USE_GRAPHS and S.N <= GRAPH_MAX_N) if use_graph is None else use_graph
+    if E.KTIMER is not None:
+        graph = False   # per-call kernel timing (bench breakdown) needs eager launches
     if graph and iterations > 0:
         g = _graphed(S, D0, cap, eps, use_tc)
         g.load(S, D0)
@@ -466,7 +471,7 @@ def _split_locals(src, N: int, m: int, L: int, K1: int, local_cap: int, local_ep
         off, _ = E.shard_offsets(sizes)
         S = E.ShardSet(Ys, off, sizes, prec)
         D0 = init_dictionaries(S, K1, "first-columns", seeds[:L])
-        Dl, codes, _ = train_device(S, D0, local_cap, local_eps, local_iters, use_tc, use_graph=False)
+        Dl, codes, _ = train_device(S, D0, local_cap, local_eps, local_iters, use_tc)
         return Dl, E.code_energy(S, codes)
     bounds = [(g * L) // G for g in range(G + 1)]
     main = torch.cuda.current_stream()
@@ -498,6 +503,8 @@ def _split_locals(src, N: int, m: int, L: int, K1: int, local_cap: int, local_ep
             off, _ = E.shard_offsets(sizes[a:b])
             S = E.ShardSet(Ys, off, sizes[a:b], prec)
             D0 = init_dictionaries(S, K1, "first-columns", seeds[a:b])
+            # eager: groups of equal shape would share one cached graph's
+            # static buffers while running concurrently on their own streams
             Dl, codes, _ = train_device(S, D0, local_cap, local_eps, local_iters, use_tc,
                                         use_graph=False)
             w = E.code_energy(S, codes)
