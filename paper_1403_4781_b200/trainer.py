@@ -437,13 +437,26 @@ class SplitMergeResult:
     codings: int                   # OMP signal-codings performed
 
 
-_STREAMS: list = []
+_STREAMS: dict = {}
 
 
-def _streams(n: int) -> list:
-    while len(_STREAMS) < n:
-        _STREAMS.append(torch.cuda.Stream())
-    return _STREAMS[:n]
+def _group_streams(G: int) -> tuple:
+    """(copy stream, [work stream per shard group]) with priorities: the row
+    gathers highest (PCIe is the bottleneck while rows arrive), then later
+    groups above earlier ones — the last group to land has the longest
+    remaining chain of iterations, the earlier groups have slack to fill the
+    gaps (makespan ordering)."""
+    key = G
+    if key not in _STREAMS:
+        lo, hi = torch.cuda.Stream.priority_range()   # (least, greatest); greatest is numerically lower
+        levels = list(range(lo, hi - 1, -1))         # least ... greatest
+        copy = torch.cuda.Stream(priority=levels[-1])
+        work_levels = levels[:-1] or levels
+        work = [torch.cuda.Stream(priority=work_levels[min(len(work_levels) - 1,
+                                                           (g * len(work_levels)) // max(G, 1))])
+                for g in range(G)]
+        _STREAMS[key] = (copy, work)
+    return _STREAMS[key]
 
 
 def _split_locals(src, N: int, m: int, L: int, K1: int, local_cap: int, local_eps: float,
@@ -475,7 +488,7 @@ def _split_locals(src, N: int, m: int, L: int, K1: int, local_cap: int, local_ep
         return Dl, E.code_energy(S, codes)
     bounds = [(g * L) // G for g in range(G + 1)]
     main = torch.cuda.current_stream()
-    copy, *work = _streams(G + 1)
+    copy, work = _group_streams(G)
     ready = []
     copy.wait_stream(main)   # perm (and a device source) are ready
     with torch.cuda.stream(copy):
