@@ -254,9 +254,12 @@ class _GraphedLoop:
 _GRAPH_CACHE: dict = {}
 
 
-def _graphed(S: E.ShardSet, D0: torch.Tensor, cap: int, eps: float, use_tc: bool) -> "_GraphedLoop":
+def _graphed(S: E.ShardSet, D0: torch.Tensor, cap: int, eps: float, use_tc: bool,
+             tag=None) -> "_GraphedLoop":
+    # tag: callers that run several trainings of equal shape concurrently (shard
+    # groups on their own streams) get one graph -- and static buffers -- each
     key = (S.prec, tuple(S.Y.shape), tuple(S.sizes), tuple(D0.shape), cap, float(eps), bool(use_tc),
-           E.get_precision(None), torch.cuda.current_device())
+           E.get_precision(None), torch.cuda.current_device(), tag)
     g = _GRAPH_CACHE.get(key)
     if g is None:
         g = _GRAPH_CACHE[key] = _GraphedLoop(S, D0, cap, eps, use_tc)
@@ -264,7 +267,7 @@ def _graphed(S: E.ShardSet, D0: torch.Tensor, cap: int, eps: float, use_tc: bool
 
 
 def train_device(S: E.ShardSet, D0: torch.Tensor, cap: int, eps: float, iterations: int,
-                 use_tc: bool = True, use_graph: bool | None = None):
+                 use_tc: bool = True, use_graph: bool | None = None, graph_tag=None):
     """The alternating loop (trainer.py:183-188) on every shard at once.
 
     Returns (D (P,K,m) f64, final codes, residuals (iterations, P) f64 device).
@@ -279,7 +282,7 @@ def train_device(S: E.ShardSet, D0: torch.Tensor, cap: int, eps: float, iteratio
     if E.KTIMER is not None:
         graph = False   # per-call kernel timing (bench breakdown) needs eager launches
     if graph and iterations > 0:
-        g = _graphed(S, D0, cap, eps, use_tc)
+        g = _graphed(S, D0, cap, eps, use_tc, graph_tag)
         g.load(S, D0)
         for it in range(iterations):
             g.graph.replay()
@@ -486,7 +489,7 @@ def _split_locals(src, N: int, m: int, L: int, K1: int, local_cap: int, local_ep
         D0 = init_dictionaries(S, K1, "first-columns", seeds[:L])
         Dl, codes, _ = train_device(S, D0, local_cap, local_eps, local_iters, use_tc)
         return Dl, E.code_energy(S, codes)
-    bounds = [(g * L) // G for g in range(G + 1)]
+    bounds = [(g * L) // G for g in range(G + 1)]   # (unequal splits measured no better)
     main = torch.cuda.current_stream()
     copy, work = _group_streams(G)
     ready = []
@@ -516,10 +519,10 @@ def _split_locals(src, N: int, m: int, L: int, K1: int, local_cap: int, local_ep
             off, _ = E.shard_offsets(sizes[a:b])
             S = E.ShardSet(Ys, off, sizes[a:b], prec)
             D0 = init_dictionaries(S, K1, "first-columns", seeds[a:b])
-            # eager: groups of equal shape would share one cached graph's
-            # static buffers while running concurrently on their own streams
+            # one graph per group: equal-shaped groups run concurrently on their
+            # own streams and must not share a graph's static buffers
             Dl, codes, _ = train_device(S, D0, local_cap, local_eps, local_iters, use_tc,
-                                        use_graph=False)
+                                        graph_tag=("group", g, G))
             w = E.code_energy(S, codes)
         Dl.record_stream(main)
         w.record_stream(main)
@@ -595,7 +598,7 @@ def _split_merge_host(src: int, N: int, m: int, cfg, cap1: int, eps1: float, loc
     perm = E.split_permutation(N, cfg.seed)
     t_split = time.perf_counter()
     seeds = _derive_seeds(cfg.seed, cfg.L + 1)
-    bad = E.zeros((max(1, HOST_GROUPS),), torch.int32)  # one non-finite flag per group
+    bad = E.zeros((max(1, cfg.L),), torch.int32)  # one non-finite flag per group (<= L groups)
     Dl, w = _split_locals(None, N, m, cfg.L, cfg.K1, cap1, eps1, local_iters, seeds, perm, prec,
                           True, HOST_GROUPS, host_f64=src, bad=bad)
     t_local = time.perf_counter()
