@@ -62,6 +62,9 @@ KTIMER: dict | None = None
 # with KTIMER on: device counters of the fused coding path (signals coded by
 # sdb_code_step1, signals it deferred to sdb_omp_deferred)
 KSTAT: dict = {}
+# error-bounded FP32 coding through sdb_code_step1 + sdb_omp_deferred (False:
+# sdb_correlate + sdb_omp; the codes are bitwise the same, tests compare both)
+FUSE_STEP1 = True
 
 
 def timed_call(name: str, nbytes: float, flops: float, fn, *args):
@@ -236,7 +239,7 @@ def code(Ydev: torch.Tensor, off: torch.Tensor, max_rows: int, DT: torch.Tensor,
         return out
     alpha = empty((N, K), tdt)
     es = 8 if prec == "fp64" else 4
-    if (prec == "fp32" and use_tc and ysq is not None and eps > 0.0 and not want_rnorm
+    if (FUSE_STEP1 and prec == "fp32" and use_tc and ysq is not None and eps > 0.0 and not want_rnorm
             and K <= 256 and m <= 256 and cap <= 32 and K % 4 == 0 and m % 4 == 0):
         # error-bounded mode: GEMM + first greedy step fused, OMP only for the
         # signals that need more (bitwise the same codes as the path below)

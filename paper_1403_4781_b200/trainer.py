@@ -259,7 +259,7 @@ def _graphed(S: E.ShardSet, D0: torch.Tensor, cap: int, eps: float, use_tc: bool
     # tag: callers that run several trainings of equal shape concurrently (shard
     # groups on their own streams) get one graph -- and static buffers -- each
     key = (S.prec, tuple(S.Y.shape), tuple(S.sizes), tuple(D0.shape), cap, float(eps), bool(use_tc),
-           E.get_precision(None), torch.cuda.current_device(), tag)
+           E.get_precision(None), torch.cuda.current_device(), E.FUSE_STEP1, tag)
     g = _GRAPH_CACHE.get(key)
     if g is None:
         g = _GRAPH_CACHE[key] = _GraphedLoop(S, D0, cap, eps, use_tc)

@@ -120,3 +120,23 @@ def test_fused_vs_oracle_supports():
             i = off[p] + r
             same += int(counts[i] == oc[r] and np.array_equal(np.sort(idx[i, :counts[i]]), np.sort(oi[r, :oc[r]])))
     assert same >= 0.999 * len(Y), same
+
+
+def test_fused_training_bitwise_equals_unfused():
+    """A whole error-bounded FP32 split-and-merge training (15 local
+    iterations, graph-replayed) gives bitwise the same dictionary with the
+    fused coding path as with sdb_correlate + sdb_omp."""
+    import benchdata
+    from paper_1403_4781_b200 import _engine as E
+    from paper_1403_4781_b200.trainer import split_merge_device
+    Y = benchdata.make_training_data("c2", 7, N=60000)
+    Ydev, _ = E.ingest_signals(Y.T, "fp32")
+    out = []
+    for fuse in (True, False):
+        E.FUSE_STEP1 = fuse
+        try:
+            r = split_merge_device(Ydev, 4, 256, 16, 184.0, 6, 256, 4, 4, 11, prec="fp32")
+        finally:
+            E.FUSE_STEP1 = True
+        out.append(r.D)
+    assert np.array_equal(out[0].view(np.uint8), out[1].view(np.uint8))
