@@ -96,9 +96,9 @@ int sdb_omp(int dtype, int64_t N, int64_t m, int64_t K, int64_t P, const int64_t
  * one-atom Cholesky solve and the eps test) on each signal's accumulator row,
  * with the exact arithmetic of sdb_omp's FP32 kernel. Signals it settles get
  * idx/val/counts/status written; the others get their alpha0 row stored and
- * status -1, and their number is added to *n_deferred (device int32; the
- * caller zeroes nothing: the launch resets it). sdb_omp_deferred then codes
- * exactly the status -1 signals. The union is bitwise sdb_omp's output
+ * status -1; their number is the int32 at ws + ws_bytes - 256 (reset by the
+ * launch). sdb_omp_deferred (same ws, which also holds its work counter)
+ * then codes exactly the status -1 signals. The union is bitwise sdb_omp's output
  * (rnorm not produced). Needs K <= 256, m <= 256, cap <= 32, eps > 0 and ysq
  * (sdb_signal_sq); SDB_ENOTSUP otherwise (the caller uses sdb_correlate +
  * sdb_omp). ws: sdb_code_step1_workspace_bytes(). */
@@ -106,11 +106,11 @@ int64_t sdb_code_step1_workspace_bytes(int64_t P, int64_t m, int64_t K);
 int sdb_code_step1(int64_t N, int64_t m, int64_t K, int64_t P, const int64_t *shard_off, const float *Y,
                    int64_t ldy, const float *D, const float *G, const float *ysq, int64_t cap, double eps,
                    double guard, float *alpha0, int64_t lda, int32_t *idx, float *val, int32_t *counts,
-                   int8_t *status, int32_t *n_deferred, void *ws, int64_t ws_bytes, void *stream);
+                   int8_t *status, void *ws, int64_t ws_bytes, void *stream);
 int sdb_omp_deferred(int64_t N, int64_t m, int64_t K, int64_t P, const int64_t *shard_off,
                      const float *alpha0, int64_t lda, const float *Y, int64_t ldy, const float *D,
                      const float *G, const float *ysq, int64_t cap, double eps, double guard, int32_t *idx,
-                     float *val, int32_t *counts, int8_t *status, void *stream);
+                     float *val, int32_t *counts, int8_t *status, void *ws, int64_t ws_bytes, void *stream);
 /* ||y_i||^2 per signal (FP32, N floats) with the exact arithmetic of the
  * FP32 OMP kernel: passing it as sdb_omp's ysq gives bitwise the same codes
  * and lets the kernel skip loading y except near the eps threshold. */

@@ -245,14 +245,14 @@ def code(Ydev: torch.Tensor, off: torch.Tensor, max_rows: int, DT: torch.Tensor,
         # signals that need more (bitwise the same codes as the path below)
         wb = _lib.load().sdb_code_step1_workspace_bytes(P, m, K)
         ws = empty((wb,), torch.uint8)
-        ndef = ws[wb - 256:wb - 252].view(torch.int32)
+        ndef = ws[wb - 256:wb - 252].view(torch.int32)   # deferred count (written by the launch)
         timed_call("step1", N * (4 * m + 4), 2.0 * N * m * K, "sdb_code_step1", N, m, K, P, ptr(off),
                    ptr(Ydev), m, ptr(DT), ptr(G), ptr(ysq), cap, float(eps), GUARD[prec], ptr(alpha), K,
-                   ptr(out.idx), ptr(out.val), ptr(out.counts), ptr(out.status), ptr(ndef), ptr(ws),
-                   int(wb), stream())
+                   ptr(out.idx), ptr(out.val), ptr(out.counts), ptr(out.status), ptr(ws), int(wb),
+                   stream())
         timed_call("omp_deferred", 0.0, 0.0, "sdb_omp_deferred", N, m, K, P, ptr(off), ptr(alpha), K,
                    ptr(Ydev), m, ptr(DT), ptr(G), ptr(ysq), cap, float(eps), GUARD[prec], ptr(out.idx),
-                   ptr(out.val), ptr(out.counts), ptr(out.status), stream())
+                   ptr(out.val), ptr(out.counts), ptr(out.status), ptr(ws), int(wb), stream())
         if KTIMER is not None and not torch.cuda.is_current_stream_capturing():
             if "deferred" not in KSTAT:
                 KSTAT["deferred"] = zeros((1,), torch.int64)

@@ -188,17 +188,18 @@ int64_t sdb_code_step1_workspace_bytes(int64_t P, int64_t m, int64_t K) {
 int sdb_code_step1(int64_t N, int64_t m, int64_t K, int64_t P, const int64_t* shard_off, const float* Y,
                    int64_t ldy, const float* D, const float* G, const float* ysq, int64_t cap, double eps,
                    double guard, float* alpha0, int64_t lda, int32_t* idx, float* val, int32_t* counts,
-                   int8_t* status, int32_t* n_deferred, void* ws, int64_t ws_bytes, void* stream) {
+                   int8_t* status, void* ws, int64_t ws_bytes, void* stream) {
     if (N < 0 || m < 1 || K < 1 || P < 1 || cap < 1 || ldy < m || lda < K)
         return fail(SDB_EINVAL, "sdb_code_step1: bad args");
-    if (K > 256 || m > 256 || cap > 32 || !(eps > 0.0) || ysq == nullptr || n_deferred == nullptr)
+    if (K > 256 || m > 256 || cap > 32 || !(eps > 0.0) || ysq == nullptr)
         return fail(SDB_ENOTSUP, "sdb_code_step1: needs K <= 256, m <= 256, cap <= 32, eps > 0, ysq");
     if (ws == nullptr || ws_bytes < sdb_code_step1_workspace_bytes(P, m, K))
         return fail(SDB_EINVAL, "sdb_code_step1: workspace too small");
     if (N == 0) return SDB_OK;
+    int32_t* counters = (int32_t*)((unsigned char*)ws + step1_corr_bytes(P, m, K));
     int rc = sdb::code_step1_tc_f32(N, Y, ldy, shard_off, (int)P, D, m, K, alpha0, lda, ws,
                                     step1_corr_bytes(P, m, K), ysq, G, (float)eps, (float)guard, (int)cap,
-                                    idx, val, counts, status, n_deferred, S(stream));
+                                    idx, val, counts, status, counters, S(stream));
     if (rc == cudaErrorNotSupported) return fail(SDB_ENOTSUP, "sdb_code_step1: shape outside the tcgen05 tiling");
     return cuda_rc(rc, "sdb_code_step1");
 }
@@ -206,11 +207,13 @@ int sdb_code_step1(int64_t N, int64_t m, int64_t K, int64_t P, const int64_t* sh
 int sdb_omp_deferred(int64_t N, int64_t m, int64_t K, int64_t P, const int64_t* shard_off,
                      const float* alpha0, int64_t lda, const float* Y, int64_t ldy, const float* D,
                      const float* G, const float* ysq, int64_t cap, double eps, double guard, int32_t* idx,
-                     float* val, int32_t* counts, int8_t* status, void* stream) {
+                     float* val, int32_t* counts, int8_t* status, void* ws, int64_t ws_bytes, void* stream) {
     if (N < 0 || m < 1 || K < 1 || P < 1 || cap < 1 || ldy < m || lda < K)
         return fail(SDB_EINVAL, "sdb_omp_deferred: bad args");
     if (K > 1024 || m > 256 || cap > 32 || ysq == nullptr)
         return fail(SDB_ENOTSUP, "sdb_omp_deferred: needs K <= 1024, m <= 256, cap <= 32 and ysq");
+    if (ws == nullptr || ws_bytes < sdb_code_step1_workspace_bytes(P, m, K))
+        return fail(SDB_EINVAL, "sdb_omp_deferred: the sdb_code_step1 workspace is required");
     if (N == 0) return SDB_OK;
     sdb::OmpArgs<float> a{};
     a.N = N; a.m = (int)m; a.K = (int)K; a.cap = (int)cap; a.P = (int)P;
@@ -219,6 +222,7 @@ int sdb_omp_deferred(int64_t N, int64_t m, int64_t K, int64_t P, const int64_t* 
     a.eps = (float)eps; a.guard = (float)guard;
     a.alpha0 = alpha0; a.Y = Y; a.D = D; a.G = G; a.val = val; a.rnorm = nullptr; a.ysq = ysq;
     a.deferred = 1;
+    a.work = (int*)((unsigned char*)ws + step1_corr_bytes(P, m, K)) + 1;   // zeroed by sdb_code_step1
     return cuda_rc(sdb::launch_omp<float>(a, S(stream)), "sdb_omp_deferred");
 }
 

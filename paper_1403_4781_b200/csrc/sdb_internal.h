@@ -27,6 +27,7 @@ struct OmpArgs {
     T* rnorm;                  // optional (nullptr: not requested)
     const float* ysq;          // optional precomputed ||y||^2 (fast FP32 path only)
     int deferred;              // fast FP32 path: code only the signals with status == -1
+    int* work;                 //   ... claiming 32-signal chunks from this zeroed counter
     unsigned char* gscratch;   // optional per-warp scratch in global memory
     int64_t gscratch_warps;
     int64_t warp_bytes;

@@ -479,27 +479,37 @@ k_omp_fast(OmpArgs<float> a) {
     const bool vec_a = (K == 32 * KPL) && ((a.lda * 4) % 16 == 0) && (((uintptr_t)a.alpha0 & 15) == 0);
     const bool vec_g = (K == 32 * KPL) && ((K * 4) % 16 == 0) && (((uintptr_t)a.G & 15) == 0);
 
-    // DEFER: flags of the current 32-signal chunk not yet visited
-    int64_t fc = i_begin;
+    // DEFER: the warps claim 32-signal chunks from a device counter (a.work,
+    // zeroed by the step-1 launch) — deferred signals cost 2..cap greedy steps,
+    // so static ranges would leave the kernel waiting on its unluckiest warp —
+    // and code the flagged signals of each chunk (one ballot per chunk); the
+    // next claim is issued one chunk ahead so its latency is hidden
+    constexpr int CH = 32;
+    int64_t fc = 0;
     unsigned fl = 0;
+    int claim_pending = 0;   // lane 0: result of the claim issued ahead
+    auto issue_claim = [&]() {
+        if (lane == 0) claim_pending = atomicAdd(a.work, CH);
+    };
     auto flags_at = [&](int64_t c) -> unsigned {
-        if (c + 32 + lane < i_end && (lane & 31) == 0)
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(a.status + c + 32));
-        const bool f = (c + lane < i_end) && (__ldg(a.status + c + lane) == (int8_t)-1);
+        const bool f = (c + lane < a.N) && (__ldg(a.status + c + lane) == (int8_t)-1);
         return __ballot_sync(SDB_FULL, f);
     };
     auto next_flagged = [&]() -> int64_t {
         while (!fl) {
-            if (fc >= i_end) return i_end;
+            fc = (int64_t)__shfl_sync(SDB_FULL, claim_pending, 0);
+            if (fc >= a.N) return a.N;
+            issue_claim();
             fl = flags_at(fc);
-            fc += 32;
         }
-        const int64_t r = fc - 32 + __ffs(fl) - 1;
+        const int64_t r = fc + __ffs(fl) - 1;
         fl &= fl - 1u;
         return r;
     };
+    if constexpr (DEFER) issue_claim();
+    const int64_t i_stop = DEFER ? a.N : i_end;
     int64_t i = DEFER ? next_flagged() : i_begin;
-    if (i >= i_end) return;
+    if (i >= i_stop) return;
 
     int p = shard_of(a.shard_off, a.P, i);
     int64_t p_end = a.shard_off[p + 1];
@@ -511,7 +521,7 @@ k_omp_fast(OmpArgs<float> a) {
     const bool all_valid = nvalid == KPL;
     const float kNaN = __int_as_float(0x7fffffff);
 
-    for (int64_t i_next; i < i_end; i = i_next) {
+    for (int64_t i_next; i < i_stop; i = i_next) {
         i_next = DEFER ? next_flagged() : i + 1;
         if (i >= p_end) {
             while (i >= p_end) { ++p; p_end = a.shard_off[p + 1]; }
@@ -532,7 +542,7 @@ k_omp_fast(OmpArgs<float> a) {
         }
         // the next signal's alpha0 row (and y) are prefetched into L1 (no
         // registers held across the signal, which keeps occupancy at 4 blocks / SM)
-        if (i_next < i_end) {
+        if (i_next < i_stop) {
             const float* an = a.alpha0 + i_next * a.lda;
             if (j0 < K) asm volatile("prefetch.global.L1 [%0];" ::"l"(an + j0));
             if constexpr (KPL > 8) {

@@ -651,7 +651,7 @@ k_corr_tc2(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUte
 __global__ void k_tile_layout(const int64_t* __restrict__ off, int P, int64_t* __restrict__ ts,
                               int* __restrict__ zero) {
     if (threadIdx.x == 0 && blockIdx.x == 0) {
-        if (zero) *zero = 0;
+        if (zero) { zero[0] = 0; zero[1] = 0; }   // CODE: deferred count, deferred-OMP work counter
         int64_t t = 0;
         for (int p = 0; p < P; ++p) {
             ts[p] = t;
