@@ -5,6 +5,7 @@ import sys
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import benchdata  # noqa: E402
@@ -28,6 +29,9 @@ off, mx = E.shard_offsets(sizes)
 S = E.ShardSet(Ys, off, sizes, "fp32")
 codes = E.code(Ys, off, mx, E.working_dict(Dl, "fp32"), E.gram(Dl, "fp32"), cap, eps, "fp32", True,
                ysq=S.signal_sq(), want_rnorm=False)
+u = E.code_usage(S, codes).cpu().numpy()
+print(f"bucket sizes (entries per (shard, atom)): mean {u.mean():.0f} max {u.max()} p99 {np.percentile(u, 99):.0f} "
+      f"top5 {np.sort(u.ravel())[-5:].tolist()}")
 for _ in range(3):
     E.mod_update(S, codes, Dl)
 torch.cuda.synchronize()
