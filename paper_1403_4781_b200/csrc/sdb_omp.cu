@@ -865,6 +865,34 @@ __global__ void k_scan_add(int64_t* __restrict__ out, int64_t N, const int64_t* 
 
 int64_t scan_workspace_bytes(int64_t N) { return sizeof(int64_t) * ((N + SCAN_TILE - 1) / SCAN_TILE + 1); }
 
+// small N (the MOD's P*K bucket counts): one block walks the tiles with a
+// running carry — one launch instead of three
+__global__ void __launch_bounds__(SCAN_TPB)
+k_scan_single(const int32_t* __restrict__ counts, int64_t N, int64_t* __restrict__ out) {
+    __shared__ int64_t sh[32];
+    int64_t carry = 0;
+    for (int64_t t0 = 0; t0 < N; t0 += SCAN_TILE) {
+        const int64_t base = t0 + (int64_t)threadIdx.x * SCAN_IPT;
+        int64_t loc[SCAN_IPT];
+        int64_t s = 0;
+#pragma unroll
+        for (int q = 0; q < SCAN_IPT; ++q) {
+            const int64_t i = base + q;
+            loc[q] = s;
+            s += (i < N) ? counts[i] : 0;
+        }
+        int64_t total;
+        const int64_t pre = block_exclusive_scan(s, sh, &total);
+#pragma unroll
+        for (int q = 0; q < SCAN_IPT; ++q) {
+            const int64_t i = base + q;
+            if (i < N) out[i] = carry + pre + loc[q];
+        }
+        carry += total;
+    }
+    if (threadIdx.x == 0) out[N] = carry;
+}
+
 // indptr[0..N] (N+1 entries): indptr[0] = 0, indptr[i+1] = sum_{u<=i} counts[u]
 int exclusive_scan_counts(const int32_t* counts, int64_t N, int64_t* indptr, int64_t* ws,
                           cudaStream_t st) {
@@ -873,6 +901,10 @@ int exclusive_scan_counts(const int32_t* counts, int64_t N, int64_t* indptr, int
         return (int)cudaGetLastError();
     }
     const int64_t ntiles = (N + SCAN_TILE - 1) / SCAN_TILE;
+    if (ntiles <= 8) {
+        k_scan_single<<<1, SCAN_TPB, 0, st>>>(counts, N, indptr);
+        return (int)cudaGetLastError();
+    }
     k_scan_tiles<<<(unsigned)ntiles, SCAN_TPB, 0, st>>>(counts, N, indptr, ws);
     k_scan_sums<<<1, SCAN_TPB, 0, st>>>(ws, ntiles, indptr + N);
     k_scan_add<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(indptr, N, ws);
