@@ -288,16 +288,21 @@ def signal_sq(Ydev: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tens
     return out[:N]
 
 
-def code_single_dict(Ydev, D64, cap, eps, prec, use_tc=True) -> DeviceCodes:
-    """Code all rows of Ydev against one dictionary (P = 1), chunked."""
+def code_single_dict(Ydev, D64, cap, eps, prec, use_tc=True, want_rnorm=True) -> DeviceCodes:
+    """Code all rows of Ydev against one dictionary (P = 1), chunked.
+    want_rnorm=False (callers that never read the residual norms, e.g. the
+    denoiser) lets FP32 error-bounded coding take the fused path."""
     N = Ydev.shape[0]
     DT = working_dict(D64, prec)
     G = gram(D64, prec)
     K = D64.shape[1]
     rows = alpha_chunk_rows(K, prec)
+    ysq = None
+    if not want_rnorm and prec == "fp32" and eps > 0.0:
+        ysq = signal_sq(Ydev)
     if N <= rows:
         off, mx = shard_offsets([N])
-        return code(Ydev, off, mx, DT, G, cap, eps, prec, use_tc)
+        return code(Ydev, off, mx, DT, G, cap, eps, prec, use_tc, ysq=ysq, want_rnorm=want_rnorm)
     tdt = torch_dtype(prec)
     res = DeviceCodes(K, cap, empty((N, cap), torch.int32), empty((N, cap), tdt),
                       empty((N,), torch.int32), empty((N,), torch.int8), empty((N,), tdt))
@@ -306,7 +311,8 @@ def code_single_dict(Ydev, D64, cap, eps, prec, use_tc=True) -> DeviceCodes:
         off, mx = shard_offsets([hi - lo])
         view = DeviceCodes(K, cap, res.idx[lo:hi], res.val[lo:hi], res.counts[lo:hi],
                            res.status[lo:hi], res.rnorm[lo:hi])
-        code(Ydev[lo:hi], off, mx, DT, G, cap, eps, prec, use_tc, out=view)
+        code(Ydev[lo:hi], off, mx, DT, G, cap, eps, prec, use_tc, out=view,
+             ysq=None if ysq is None else ysq[lo:hi], want_rnorm=want_rnorm)
     return res
 
 
