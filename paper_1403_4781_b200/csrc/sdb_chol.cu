@@ -904,6 +904,61 @@ k_chol_cluster(int K, int m, double* __restrict__ Aall, double* __restrict__ Bal
     if (tid == 0) s_part[1] = wloc;
 
     // ---- backward: W_c -= L_Jc^T Z_J for J > c, then Z_c = T_c^T W_c
+    if (m <= CB) {
+        // one column chunk: W_c stays in registers across the J updates (no
+        // global read-modify-write per link, no restaging for Z_c), and L_Jc
+        // is copied before Z_J is waited for
+        double wr[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int rr = ty + 16 * a, cc = tx + 16 * b;
+                wr[a][b] = (rr < nr && cc < m) ? B[(int64_t)(r0 + rr) * m + cc] : 0.0;
+            }
+        for (int J = NC - 1; J > c; --J) {
+            const int nJ = nrows(J);
+            flag_wait(cl.map_shared_rank(&fL[c], J));
+            copy_tile(S2, cl.map_shared_rank(tile(c), J));  // L_Jc (rows of block J)
+            flag_wait(cl.map_shared_rank(&fZ, J));
+            stage_rows_t(S1, B, m, J * CB, nJ, 0, m);
+            __syncthreads();
+            tile_mm<true>(S2, S1, nJ, acc);
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) wr[a][b] -= acc[a][b];
+            __syncthreads();
+        }
+        // S1[col][q] = W_c[q][col] (the stage_rows_t layout)
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) S1[(tx + 16 * b) * CBP + ty + 16 * a] = wr[a][b];
+        __syncthreads();
+        tile_mm<true>(tile(c), S1, nr, acc);
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int rr = ty + 16 * a, cc = tx + 16 * b;
+                if (rr < nr && cc < m) B[(int64_t)(r0 + rr) * m + cc] = acc[a][b];
+            }
+        flag_publish(&fZ);
+        cl.sync();
+        if (c == 0 && tid == 0) {
+            double w = 0.0;
+            int nd = 0;
+            for (int k = 0; k < NC; ++k) {
+                w += cl.map_shared_rank(s_part, k)[1];
+                nd += *cl.map_shared_rank(&s_nd, k);
+            }
+            if (wsq) wsq[p] = w;
+            ndep[p] = nd;
+        }
+        cl.sync();  // keep every CTA's shared memory alive until rank 0 has read it
+        return;
+    }
     for (int J = NC - 1; J > c; --J) {
         const int nJ = nrows(J);
         flag_wait(cl.map_shared_rank(&fZ, J));
