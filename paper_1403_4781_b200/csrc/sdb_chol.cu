@@ -878,10 +878,51 @@ k_chol_cluster(int K, int m, double* __restrict__ Aall, double* __restrict__ Bal
         s_nd = nd;
     }
     flag_publish(&fT);
+    double wloc = 0.0;
+    if (m <= CB) {
+        // one column chunk: the deferred RHS update (B_c -= L_cJ W_J, on this
+        // CTA's critical path) is applied in registers and W_c = T_c B_c
+        // formed from them, without a global round trip
+        double br[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int rr = ty + 16 * a, cc = tx + 16 * b;
+                br[a][b] = (rr < nr && cc < m) ? B[(int64_t)(r0 + rr) * m + cc] : 0.0;
+            }
+        for (int J = 0; J < c; ++J) {
+            if (!b_pending[J]) continue;
+            flag_wait(cl.map_shared_rank(&fW, J));
+            stage_rows_t(S1, B, m, J * CB, nrows(J), 0, m);
+            __syncthreads();
+            tile_mm<false>(tile(J), S1, nrows(J), acc);
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) br[a][b] -= acc[a][b];
+            __syncthreads();
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) S1[(tx + 16 * b) * CBP + ty + 16 * a] = br[a][b];
+        __syncthreads();
+        tile_mm<false>(tile(c), S1, nr, acc);
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int rr = ty + 16 * a, cc = tx + 16 * b;
+                if (rr < nr && cc < m) {
+                    B[(int64_t)(r0 + rr) * m + cc] = acc[a][b];
+                    wloc = fma(acc[a][b], acc[a][b], wloc);
+                }
+            }
+    } else {
     for (int J = 0; J < c; ++J)
         if (b_pending[J]) b_update(J);
     // W_c = T_c B_c
-    double wloc = 0.0;
     for (int c0 = 0; c0 < m; c0 += CB) {
         const int nc = min(CB, m - c0);
         __syncthreads();
@@ -898,6 +939,7 @@ k_chol_cluster(int K, int m, double* __restrict__ Aall, double* __restrict__ Bal
                     wloc = fma(acc[a][b], acc[a][b], wloc);
                 }
             }
+    }
     }
     flag_publish(&fW);
     wloc = block_reduce(wloc, red, false);
