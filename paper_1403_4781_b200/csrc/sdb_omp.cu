@@ -28,7 +28,11 @@ template <typename TIn, typename TOut>
 __global__ void __launch_bounds__(256)
 k_rowdot(const TIn* __restrict__ A, int64_t lda, const int64_t* __restrict__ a_off,
          int64_t a_rows_per_shard, const TIn* __restrict__ B, int64_t ldb, int64_t b_stride,
-         int64_t nb, int64_t kdim, TOut* __restrict__ C, int64_t ldc) {
+         int64_t nb, int64_t kdim, TOut* __restrict__ C, int64_t ldc, bool sym) {
+    // sym (Gram, A == B per shard): only tiles on or above the diagonal are
+    // computed; an upper tile also writes its mirror (products commute, so the
+    // mirrored entry is bitwise the one its own tile would compute)
+    if (sym && blockIdx.y < blockIdx.x) return;
     using R = Ar<TIn>;
     __shared__ TIn As[RD_BK][RD_BM + 1];
     __shared__ TIn Bs[RD_BK][RD_BN + 1];
@@ -79,7 +83,10 @@ k_rowdot(const TIn* __restrict__ A, int64_t lda, const int64_t* __restrict__ a_o
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int64_t gb = b0 + tx + 16 * j;
-            if (gb < nb) C[ga * ldc + gb] = (TOut)acc[i][j];
+            if (gb < nb) {
+                C[ga * ldc + gb] = (TOut)acc[i][j];
+                if (sym && blockIdx.y > blockIdx.x) C[(a_lo + gb) * ldc + (ga - a_lo)] = (TOut)acc[i][j];
+            }
         }
     }
 }
@@ -88,20 +95,20 @@ template <typename TIn, typename TOut>
 static int launch_rowdot(const TIn* A, int64_t lda, const int64_t* a_off, int64_t a_rows_max,
                          int64_t a_rows_per_shard, const TIn* B, int64_t ldb, int64_t b_stride,
                          int64_t nb, int64_t kdim, TOut* C, int64_t ldc, int P,
-                         cudaStream_t st) {
+                         cudaStream_t st, bool sym = false) {
     if (a_rows_max <= 0 || nb <= 0 || P <= 0) return 0;
     dim3 grid((unsigned)((a_rows_max + RD_BM - 1) / RD_BM), (unsigned)((nb + RD_BN - 1) / RD_BN),
               (unsigned)P);
     k_rowdot<TIn, TOut><<<grid, 256, 0, st>>>(A, lda, a_off, a_rows_per_shard, B, ldb, b_stride,
-                                              nb, kdim, C, ldc);
+                                              nb, kdim, C, ldc, sym);
     return (int)cudaGetLastError();
 }
 
 int gram_f64(const double* D, int P, int64_t m, int64_t K, double* G, cudaStream_t st) {
-    return launch_rowdot<double, double>(D, m, nullptr, K, K, D, m, K * m, K, m, G, K, P, st);
+    return launch_rowdot<double, double>(D, m, nullptr, K, K, D, m, K * m, K, m, G, K, P, st, true);
 }
 int gram_f32(const double* D, int P, int64_t m, int64_t K, float* G, cudaStream_t st) {
-    return launch_rowdot<double, float>(D, m, nullptr, K, K, D, m, K * m, K, m, G, K, P, st);
+    return launch_rowdot<double, float>(D, m, nullptr, K, K, D, m, K * m, K, m, G, K, P, st, true);
 }
 int correlate_simt_f64(const double* Y, int64_t ldy, const int64_t* off, int64_t max_rows, int P,
                        const double* D, int64_t m, int64_t K, double* alpha, int64_t lda,
