@@ -22,7 +22,7 @@ import torch.distributed as dist
 from . import _engine as E
 from .exceptions import InvalidInputError
 from .trainer import (SplitMergeResult, _derive_seeds, _sync, coding_mode, init_dictionaries,
-                      split_indices, train_device)
+                      train_device)
 
 
 def shard_block(L: int, world: int, rank: int) -> tuple[int, int]:
@@ -66,15 +66,20 @@ def split_merge_ranks(Ydev: torch.Tensor, L: int, K1: int, local_cap: int, local
         _sync()
         t_start = time.perf_counter()
     N, m = Ydev.shape
-    blocks = split_indices(N, L, seed)
+    if not 1 <= L <= N:
+        raise InvalidInputError("require 1 <= L <= N")
+    # split_indices' blocks are consecutive slices of one PCG64 permutation,
+    # formed natively and bit-identically on the device (every rank the same)
+    base, extra = divmod(N, L)
+    all_sizes = [base + (1 if t < extra else 0) for t in range(L)]
+    offs = np.concatenate([[0], np.cumsum(all_sizes)]).astype(np.int64)
     lo, hi = shard_block(L, world, rank)
-    mine = blocks[lo:hi]
-    sizes = [b.size for b in mine]
-    if min(b.size for b in blocks) < K1:
+    sizes = all_sizes[lo:hi]
+    if min(all_sizes) < K1:
         raise InvalidInputError("first-columns init needs N >= K")
     seeds = _derive_seeds(seed, L + 1)
     if sizes:
-        perm = torch.from_numpy(np.concatenate(mine).astype(np.int64)).to(E.device())
+        perm = E.split_permutation(N, seed)[int(offs[lo]):int(offs[hi])]
         Ys = E.gather_rows(Ydev, perm, prec)
         off, _ = E.shard_offsets(sizes)
         S = E.ShardSet(Ys, off, sizes, prec)

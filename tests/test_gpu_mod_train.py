@@ -271,3 +271,30 @@ def test_mod_cluster_solve_partial_blocks(K, prec):
     np.testing.assert_allclose(D, Dr, rtol=0, atol=tol)
     assert dg.unused_atoms == list(unused)
     assert dg.residual_fro == pytest.approx(resid, rel=1e-9 if prec == "fp64" else 1e-5)
+
+
+def test_split_merge_ranks_nccl_world1_equals_device():
+    """The multi-GPU split-and-merge path (NCCL, here with one rank) gives
+    bitwise the same dictionary as the single-GPU batched path."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    import benchdata
+    from paper_1403_4781_b200 import _engine as E
+    from paper_1403_4781_b200.distributed import split_merge_ranks
+    from paper_1403_4781_b200.trainer import split_merge_device
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        Y = benchdata.make_training_data("c2", 3, N=40000)
+        Ydev, _ = E.ingest_signals(Y.T, "fp32")
+        a = split_merge_ranks(Ydev, 4, 256, 16, 184.0, 4, 256, 4, 4, 9, prec="fp32")
+        b = split_merge_device(Ydev, 4, 256, 16, 184.0, 4, 256, 4, 4, 9, prec="fp32")
+        assert np.array_equal(a.D, b.D)
+    finally:
+        dist.destroy_process_group()
