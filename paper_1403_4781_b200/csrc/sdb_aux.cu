@@ -210,10 +210,58 @@ int reconstruct_dense(int H, int W, int p, int s, const double* P, double* out, 
     return (int)cudaGetLastError();
 }
 
+// 16-byte row pieces: a half-warp per row (lane l of the half moves 16-byte
+// piece l, l + 16, ...), each warp keeps 8 rows (4 row pairs) in flight
+template <int PPL>
+__global__ void __launch_bounds__(256)
+k_gather_rows_v4(int64_t rows, int pieces, const float4* __restrict__ in, int64_t ldi4,
+                 const int64_t* __restrict__ perm, float4* __restrict__ out, int64_t ldo4) {
+    const int lane = threadIdx.x & 31, h = lane >> 4, l16 = lane & 15;
+    const int64_t r0 = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * 8;
+    int64_t src[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int64_t r = r0 + 2 * u + h;
+        src[u] = r < rows ? perm[r] : -1;
+    }
+    float4 v[4][PPL];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int q = 0; q < PPL; ++q) {
+            const int pc = l16 + 16 * q;
+            if (src[u] >= 0 && pc < pieces) v[u][q] = __ldg(in + src[u] * ldi4 + pc);
+        }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int64_t r = r0 + 2 * u + h;
+#pragma unroll
+        for (int q = 0; q < PPL; ++q) {
+            const int pc = l16 + 16 * q;
+            if (src[u] >= 0 && pc < pieces) out[r * ldo4 + pc] = v[u][q];
+        }
+    }
+}
+
 template <typename T>
 int gather_rows(int64_t rows, int m, const T* in, int64_t ldi, const int64_t* perm, T* out, int64_t ldo,
                 cudaStream_t st) {
     if (rows <= 0) return 0;
+    const int64_t bytes = (int64_t)m * sizeof(T);
+    const bool v4 = bytes % 16 == 0 && (ldi * (int64_t)sizeof(T)) % 16 == 0 && (ldo * (int64_t)sizeof(T)) % 16 == 0 &&
+                    ((uintptr_t)in & 15) == 0 && ((uintptr_t)out & 15) == 0 && bytes <= 2048;
+    if (v4) {
+        const int pieces = (int)(bytes / 16);
+        const int64_t ldi4 = ldi * (int64_t)sizeof(T) / 16, ldo4 = ldo * (int64_t)sizeof(T) / 16;
+        const unsigned g = (unsigned)((rows + 63) / 64);
+        const float4* i4 = reinterpret_cast<const float4*>(in);
+        float4* o4 = reinterpret_cast<float4*>(out);
+        if (pieces <= 16) k_gather_rows_v4<1><<<g, 256, 0, st>>>(rows, pieces, i4, ldi4, perm, o4, ldo4);
+        else if (pieces <= 32) k_gather_rows_v4<2><<<g, 256, 0, st>>>(rows, pieces, i4, ldi4, perm, o4, ldo4);
+        else if (pieces <= 64) k_gather_rows_v4<4><<<g, 256, 0, st>>>(rows, pieces, i4, ldi4, perm, o4, ldo4);
+        else k_gather_rows_v4<8><<<g, 256, 0, st>>>(rows, pieces, i4, ldi4, perm, o4, ldo4);
+        return (int)cudaGetLastError();
+    }
     k_gather_rows<T><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(rows, m, in, ldi, perm, out, ldo);
     return (int)cudaGetLastError();
 }
