@@ -240,7 +240,7 @@ def code(Ydev: torch.Tensor, off: torch.Tensor, max_rows: int, DT: torch.Tensor,
     alpha = empty((N, K), tdt)
     es = 8 if prec == "fp64" else 4
     if (FUSE_STEP1 and prec == "fp32" and use_tc and ysq is not None and eps > 0.0 and not want_rnorm
-            and K <= 256 and m <= 256 and cap <= 32 and K % 4 == 0 and m % 4 == 0):
+            and K <= 256 and m <= 256 and cap <= 32 and K % 4 == 0 and m % 4 == 0 and N < 2**31):
         # error-bounded mode: GEMM + first greedy step fused, OMP only for the
         # signals that need more (bitwise the same codes as the path below)
         wb = _lib.load().sdb_code_step1_workspace_bytes(P, m, K)
