@@ -704,9 +704,9 @@ k_omp_fast(OmpArgs<float> a) {
 template <int KPL, int MPL>
 static int launch_fast_k(const OmpArgs<float>& a, cudaStream_t st) {
     const int wf = fast_warp_floats(a.cap, a.m);
-    // deferred signals: 4-warp blocks (register-limited residency 36 instead of
-    // 32 warps per SM; the kernel is bound by per-signal latency chains)
-    int wpb = a.deferred ? 4 : 8;
+    // 4-warp blocks: register-limited residency of 36 instead of 32 warps per
+    // SM (the kernel is bound by per-signal latency chains)
+    int wpb = 4;
     while (wpb > 1 && wpb * wf * 4 > 200 * 1024) wpb >>= 1;
     const int smem = wpb * wf * 4;
     auto fn = a.deferred ? k_omp_fast<KPL, MPL, true> : k_omp_fast<KPL, MPL, false>;
