@@ -10,6 +10,8 @@ import benchdata  # noqa: E402
 from paper_1403_4781_b200 import _engine as E  # noqa: E402
 
 m, K, s, N = 64, 256, 4, 1_000_000
+if len(sys.argv) > 3:
+    m, K, s = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
 rng = np.random.default_rng(3)
 D = benchdata.gen_dictionary(m, K, 11) if hasattr(benchdata, "gen_dictionary") else None
 if D is None:
