@@ -461,7 +461,7 @@ __device__ __forceinline__ void load_row(float (&v)[KPL], const float* __restric
 // GEMM's step-1 epilogue, sdb_code_step1, for the signals it could not settle);
 // each warp scans its contiguous range 32 status bytes at a time (ballot).
 template <int KPL, int MPL, bool DEFER>
-__global__ void __launch_bounds__(256, (KPL >= 32) ? 1 : (KPL >= 16 ? 3 : (MPL >= 5 ? 3 : 4)))
+__global__ void __launch_bounds__(256, (KPL >= 32) ? 2 : (KPL >= 16 ? 3 : (MPL >= 5 ? 3 : 4)))
 k_omp_fast(OmpArgs<float> a) {
     extern __shared__ __align__(16) float fsm[];
     const int lane = threadIdx.x & 31;
