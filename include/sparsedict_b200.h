@@ -81,7 +81,9 @@ int sdb_correlate(int dtype, int64_t N, int64_t m, int64_t K, int64_t P, const i
  * rnorm <= eps or cap atoms. Fixed sparsity: cap = s, eps = 0. K <= 1024.
  * rnorm: optional output (NULL: residual norms not reported).
  * ysq: optional FP32 ||y_i||^2 from sdb_signal_sq (SDB_F32 only; NULL: formed
- * in the kernel). scratch: sdb_omp_scratch_bytes() bytes (may be 0 -> NULL). */
+ * in the kernel). scratch: sdb_omp_scratch_bytes() bytes; its first 256 bytes carry the FP32
+ * kernel's work counter (signals are claimed in 32-signal chunks), the rest any per-warp
+ * global scratch the generic kernel needs (NULL: static signal ranges). */
 int64_t sdb_omp_scratch_bytes(int dtype, int64_t N, int64_t m, int64_t cap);
 int sdb_omp(int dtype, int64_t N, int64_t m, int64_t K, int64_t P, const int64_t *shard_off,
             const void *alpha0, int64_t lda, const void *Y, int64_t ldy, const void *D,

@@ -124,13 +124,17 @@ int sdb_correlate(int dtype, int64_t N, int64_t m, int64_t K, int64_t P, const i
     return cuda_rc(rc, "sdb_correlate");
 }
 
+// scratch: [256 B: the FP32 kernel's work counter][per-warp global scratch
+// when the generic kernel's state does not fit shared memory]
+constexpr int64_t OMP_CTR_BYTES = 256;
+
 int64_t sdb_omp_scratch_bytes(int dtype, int64_t N, int64_t m, int64_t cap) {
     if (!dtype_ok(dtype) || cap < 1 || m < 1) return fail(SDB_EINVAL, "sdb_omp_scratch_bytes: bad args");
     const int64_t wb = dtype == SDB_F64 ? sdb::omp_warp_bytes_f64((int)cap, (int)m)
                                         : sdb::omp_warp_bytes_f32((int)cap, (int)m);
-    if (wb * 8 <= 200 * 1024) return 0;  // fits shared memory
+    if (wb * 8 <= 200 * 1024) return OMP_CTR_BYTES;  // the state fits shared memory
     const int64_t warps = std::max<int64_t>(8, std::min<int64_t>(((N + 7) / 8) * 8, (int64_t)148 * 32));
-    return wb * warps;
+    return OMP_CTR_BYTES + wb * warps;
 }
 
 int sdb_omp(int dtype, int64_t N, int64_t m, int64_t K, int64_t P, const int64_t* shard_off,
@@ -145,14 +149,19 @@ int sdb_omp(int dtype, int64_t N, int64_t m, int64_t K, int64_t P, const int64_t
     const int64_t wb = dtype == SDB_F64 ? sdb::omp_warp_bytes_f64((int)cap, (int)m)
                                         : sdb::omp_warp_bytes_f32((int)cap, (int)m);
     const bool need_global = wb * 8 > 200 * 1024;
-    if (need_global && (scratch == nullptr || scratch_bytes < wb * 8))
-        return fail(SDB_EINVAL, "sdb_omp: scratch of %lld bytes required", (long long)(wb * 8));
+    if (need_global && (scratch == nullptr || scratch_bytes < OMP_CTR_BYTES + wb * 8))
+        return fail(SDB_EINVAL, "sdb_omp: scratch of %lld bytes required", (long long)(OMP_CTR_BYTES + wb * 8));
+    // a scratch of >= 256 bytes carries the FP32 kernel's chunk counter (zeroed here)
+    int* work = (scratch != nullptr && scratch_bytes >= OMP_CTR_BYTES) ? (int*)scratch : nullptr;
+    if (work) cudaMemsetAsync(work, 0, sizeof(int), S(stream));
+    unsigned char* gscr = need_global ? (unsigned char*)scratch + OMP_CTR_BYTES : nullptr;
+    const int64_t gscr_bytes = need_global ? scratch_bytes - OMP_CTR_BYTES : 0;
     auto fill = [&](auto& a) {
         a.N = N; a.m = (int)m; a.K = (int)K; a.cap = (int)cap; a.P = (int)P;
         a.shard_off = shard_off; a.lda = lda; a.ldy = ldy;
         a.idx = idx; a.counts = counts; a.status = status;
-        a.gscratch = need_global ? (unsigned char*)scratch : nullptr;
-        a.gscratch_warps = need_global ? scratch_bytes / wb : 0;
+        a.gscratch = gscr;
+        a.gscratch_warps = need_global ? gscr_bytes / wb : 0;
         a.warp_bytes = wb;
     };
     int rc;
@@ -170,6 +179,7 @@ int sdb_omp(int dtype, int64_t N, int64_t m, int64_t K, int64_t P, const int64_t
         a.alpha0 = (const float*)alpha0; a.Y = (const float*)Y; a.D = (const float*)D;
         a.G = (const float*)G; a.val = (float*)val; a.rnorm = (float*)rnorm;
         a.ysq = ysq;
+        a.work = work;
         rc = sdb::launch_omp<float>(a, S(stream));
     }
     return cuda_rc(rc, "sdb_omp");

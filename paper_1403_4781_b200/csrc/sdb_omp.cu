@@ -482,7 +482,11 @@ k_omp_fast(OmpArgs<float> a) {
     const int64_t per = (a.N + nw - 1) / nw;
     const int64_t i_begin = gw * per;
     const int64_t i_end = min(a.N, i_begin + per);
-    if (i_begin >= i_end) return;
+    // dynamic: chunks claimed from a.work (always for DEFER; for all signals
+    // when the caller supplies the counter — warps then sweep the signals in
+    // order, so only a few shards' G matrices are hot in L2 at a time)
+    const bool dyn = DEFER || a.work != nullptr;
+    if (!dyn && i_begin >= i_end) return;
     const bool vec_a = (K == 32 * KPL) && ((a.lda * 4) % 16 == 0) && (((uintptr_t)a.alpha0 & 15) == 0);
     const bool vec_g = (K == 32 * KPL) && ((K * 4) % 16 == 0) && (((uintptr_t)a.G & 15) == 0);
 
@@ -499,7 +503,7 @@ k_omp_fast(OmpArgs<float> a) {
         if (lane == 0) claim_pending = atomicAdd(a.work, CH);
     };
     auto flags_at = [&](int64_t c) -> unsigned {
-        const bool f = (c + lane < a.N) && (__ldg(a.status + c + lane) == (int8_t)-1);
+        const bool f = (c + lane < a.N) && (!DEFER || __ldg(a.status + c + lane) == (int8_t)-1);
         return __ballot_sync(SDB_FULL, f);
     };
     auto next_flagged = [&]() -> int64_t {
@@ -513,9 +517,9 @@ k_omp_fast(OmpArgs<float> a) {
         fl &= fl - 1u;
         return r;
     };
-    if constexpr (DEFER) issue_claim();
-    const int64_t i_stop = DEFER ? a.N : i_end;
-    int64_t i = DEFER ? next_flagged() : i_begin;
+    if (dyn) issue_claim();
+    const int64_t i_stop = dyn ? a.N : i_end;
+    int64_t i = dyn ? next_flagged() : i_begin;
     if (i >= i_stop) return;
 
     int p = shard_of(a.shard_off, a.P, i);
@@ -529,7 +533,7 @@ k_omp_fast(OmpArgs<float> a) {
     const float kNaN = __int_as_float(0x7fffffff);
 
     for (int64_t i_next; i < i_stop; i = i_next) {
-        i_next = DEFER ? next_flagged() : i + 1;
+        i_next = dyn ? next_flagged() : i + 1;
         if (i >= p_end) {
             while (i >= p_end) { ++p; p_end = a.shard_off[p + 1]; }
             Gp = a.G + (int64_t)p * K * K;
