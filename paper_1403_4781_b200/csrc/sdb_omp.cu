@@ -495,7 +495,7 @@ k_omp_fast(OmpArgs<float> a) {
     // so static ranges would leave the kernel waiting on its unluckiest warp —
     // and code the flagged signals of each chunk (one ballot per chunk); the
     // next claim is issued one chunk ahead so its latency is hidden
-    constexpr int CH = 32;
+    constexpr int CH = 32;   // = warp width: one ballot covers exactly one chunk
     int64_t fc = 0;
     unsigned fl = 0;
     int claim_pending = 0;   // lane 0: result of the claim issued ahead
