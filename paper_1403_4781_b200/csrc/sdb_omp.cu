@@ -718,10 +718,16 @@ static int launch_fast_k(const OmpArgs<float>& a, cudaStream_t st) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return (int)e;
     }
-    // enough warps to fill every SM several times, a contiguous range each
-    const int64_t warps = std::min<int64_t>(a.N, (int64_t)148 * 64);
+    // dynamic claiming (a work counter) only pays when every resident warp
+    // gets several 32-signal chunks; small batches keep static ranges (one
+    // signal per warp when N is below the warp count)
+    OmpArgs<float> b = a;
+    if (!b.deferred && b.N < (int64_t)32 * 148 * 36) b.work = nullptr;
+    const bool dyn = b.deferred || b.work != nullptr;
+    const int64_t warps = dyn ? std::min<int64_t>((b.N + 31) / 32, (int64_t)148 * 36)
+                              : std::min<int64_t>(b.N, (int64_t)148 * 64);
     const int64_t blocks = (warps + wpb - 1) / wpb;
-    fn<<<(unsigned)blocks, wpb * 32, smem, st>>>(a);
+    fn<<<(unsigned)blocks, wpb * 32, smem, st>>>(b);
     return (int)cudaGetLastError();
 }
 
