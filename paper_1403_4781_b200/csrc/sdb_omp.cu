@@ -767,7 +767,7 @@ static int launch_omp_k(const OmpArgs<T>& a, int blocks, int smem, cudaStream_t 
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return (int)e;
     }
-    fn<<<blocks, 256, smem, st>>>(a);
+    fn<<<blocks, 128, smem, st>>>(a);
     return (int)cudaGetLastError();
 }
 
@@ -783,12 +783,15 @@ int launch_omp(OmpArgs<T> a, cudaStream_t st) {
     int smem = 0;
     int64_t warps_needed = a.N;
     int64_t blocks;
+    // 4-warp blocks: finer residency granularity under the register limit
+    // (the exact FP64 kernel holds ~96 registers per thread)
+    constexpr int WPB = 4;
     if (a.gscratch) {
         // global scratch holds a.gscratch_warps warps
-        blocks = std::max<int64_t>(1, std::min<int64_t>(a.gscratch_warps / 8, (warps_needed + 7) / 8));
+        blocks = std::max<int64_t>(1, std::min<int64_t>(a.gscratch_warps / WPB, (warps_needed + WPB - 1) / WPB));
     } else {
-        smem = (int)(wb * 8);
-        blocks = std::min<int64_t>((warps_needed + 7) / 8, (int64_t)148 * 64);
+        smem = (int)(wb * WPB);
+        blocks = std::min<int64_t>((warps_needed + WPB - 1) / WPB, (int64_t)148 * 128);
     }
     const int kpl = (a.K + 31) / 32;
     if (kpl <= 1) return launch_omp_k<T, 1>(a, (int)blocks, smem, st);
