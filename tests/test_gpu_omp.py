@@ -109,3 +109,42 @@ def test_omp_fp32_precomputed_ysq_is_bitwise_identical(eps_scale):
     b = E.code(Ydev, off, mx, DT, G, cap, eps, "fp32", ysq=ysq, want_rnorm=False)
     for f in ("idx", "val", "counts", "status"):
         assert torch.equal(getattr(a, f), getattr(b, f)), f
+
+
+def test_fp32_dynamic_chunks_equal_static_ranges():
+    """The FP32 OMP kernel claims 32-signal chunks from a counter when the
+    sdb_omp scratch is given and the batch is large; the codes must be bitwise
+    those of static per-warp ranges (scratch NULL)."""
+    import torch
+    from paper_1403_4781_b200 import _engine as E
+    from paper_1403_4781_b200 import _lib
+    rng = np.random.default_rng(21)
+    m, K, N, cap = 64, 256, 200_000, 6
+    D = rng.standard_normal((K, m))
+    D /= np.linalg.norm(D, axis=1, keepdims=True)
+    Y = (rng.standard_normal((N, 4)) @ D[rng.integers(0, K, 4)] + 0.05 * rng.standard_normal((N, m)))
+    Yd = torch.from_numpy(Y.astype(np.float32)).cuda()
+    D64 = torch.from_numpy(D[None]).cuda()
+    DT, G = E.working_dict(D64, "fp32"), E.gram(D64, "fp32")
+    off, _ = E.shard_offsets([N])
+    alpha = torch.empty((N, K), dtype=torch.float32, device="cuda")
+    wb = _lib.load().sdb_correlate_workspace_bytes(0, 1, m, K)
+    cws = torch.empty((wb,), dtype=torch.uint8, device="cuda")
+    _lib.call("sdb_correlate", 0, N, m, K, 1, off.data_ptr(), N, Yd.data_ptr(), m, DT.data_ptr(),
+              alpha.data_ptr(), K, 1, cws.data_ptr(), wb, E.stream())
+    outs = []
+    for dynamic in (True, False):
+        idx = torch.empty((N, cap), dtype=torch.int32, device="cuda")
+        val = torch.empty((N, cap), dtype=torch.float32, device="cuda")
+        cnt = torch.empty((N,), dtype=torch.int32, device="cuda")
+        sts = torch.empty((N,), dtype=torch.int8, device="cuda")
+        sb = _lib.load().sdb_omp_scratch_bytes(0, N, m, cap)
+        scr = torch.empty((sb,), dtype=torch.uint8, device="cuda") if dynamic else None
+        _lib.call("sdb_omp", 0, N, m, K, 1, off.data_ptr(), alpha.data_ptr(), K, Yd.data_ptr(), m,
+                  DT.data_ptr(), G.data_ptr(), cap, 0.0, 1e-6, idx.data_ptr(), val.data_ptr(),
+                  cnt.data_ptr(), sts.data_ptr(), None, None, scr.data_ptr() if dynamic else None,
+                  sb if dynamic else 0, E.stream())
+        torch.cuda.synchronize()
+        outs.append([t.cpu().numpy() for t in (idx, val, cnt, sts)])
+    for a, b in zip(*outs):
+        assert np.array_equal(a.view(np.uint8), b.view(np.uint8))
