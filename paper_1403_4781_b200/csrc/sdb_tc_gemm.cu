@@ -237,7 +237,9 @@ __device__ __forceinline__ void pair_sync(int quad) {
 // Step-1 epilogue for 32 signal rows (thread = row_base + lane) of a K <= 256
 // accumulator, split over the two warps of the lane quadrant: warp half h
 // scans columns [c_lo, c_hi); the halves meet in shared memory (xv/xk: the
-// upper half's per-row max and key, *xm: the deferred-row mask).
+// upper half's per-row signed maximum and its column, *xm: the deferred-row
+// mask). diag: the lower warp's smem copy of the shard's G diagonal; ysq:
+// ||y||^2 of the lower warp's rows, fetched before the accumulator wait.
 __device__ __forceinline__ void code_step1(const Step1& s1, uint32_t trow, int64_t row_base, int nrows,
                                            int p, int K, int half, int c_lo, int c_hi,
                                            float* xv, uint32_t* xk, unsigned* xm, const float* diag,
