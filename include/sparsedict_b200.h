@@ -206,6 +206,15 @@ int sdb_scale_rows(int dtype, int64_t rows, int64_t group, int64_t m, const doub
  * directly in permuted order. */
 int sdb_ingest_gather(int dtype, int64_t rows, int64_t m, const double *src, int64_t ldi,
                       const int64_t *perm, void *out, int64_t ldo, int32_t *bad, void *stream);
+/* The same with the source's first drows rows also available in device memory
+ * (dsrc, same row stride): those are read from HBM, the rest over PCIe. Lets
+ * train_split_merge move the head of a host batch while the split permutation
+ * is still being formed on the host. */
+int sdb_ingest_gather_split(int dtype, int64_t rows, int64_t m, const double *src, int64_t ldi,
+                            const int64_t *perm, const double *dsrc, int64_t drows, void *out, int64_t ldo,
+                            int32_t *bad, void *stream);
+/* Stream-ordered copy between any two UVA addresses (cudaMemcpyDefault). */
+int sdb_copy_async(void *dst, const void *src, int64_t bytes, void *stream);
 /* Device address of a pinned, device-mapped host allocation (UVA: normally the
  * same address); SDB_EINVAL for pageable memory. */
 int sdb_host_mapped(const void *host, void **dev);

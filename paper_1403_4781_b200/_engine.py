@@ -517,13 +517,19 @@ def host_mapped(arr) -> int | None:
 
 
 def ingest_gather(src_ptr: int, ldi: int, perm: torch.Tensor, lo: int, hi: int, m: int, prec: str,
-                  bad: torch.Tensor) -> torch.Tensor:
+                  bad: torch.Tensor, head=(None, 0)) -> torch.Tensor:
     """Rows perm[lo:hi] of an f64 row-major source (device or mapped host
-    address) -> device (hi-lo) x m in the working precision; bad |= non-finite."""
+    address) -> device (hi-lo) x m in the working precision; bad |= non-finite.
+    head = (device copy of the source's first rows, their number)."""
     rows = hi - lo
     out = empty((max(rows, 1), m), torch_dtype(prec))[:rows]
-    _lib.call("sdb_ingest_gather", sdb_dtype(prec), rows, m, src_ptr, ldi, ptr(perm) + 8 * lo,
-              ptr(out), m, ptr(bad), stream())
+    dsrc, drows = head
+    if dsrc is not None and drows > 0:
+        _lib.call("sdb_ingest_gather_split", sdb_dtype(prec), rows, m, src_ptr, ldi, ptr(perm) + 8 * lo,
+                  ptr(dsrc), drows, ptr(out), m, ptr(bad), stream())
+    else:
+        _lib.call("sdb_ingest_gather", sdb_dtype(prec), rows, m, src_ptr, ldi, ptr(perm) + 8 * lo,
+                  ptr(out), m, ptr(bad), stream())
     return out
 
 

@@ -70,6 +70,9 @@ SIGNATURES = {
                                 c_dbl, c_dbl, c_vp, c_vp]),
     "sdb_reconstruct_dense": (c_int, [c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
     "sdb_ingest_gather": (c_int, [c_int, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "sdb_ingest_gather_split": (c_int, [c_int, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_i64,
+                                        c_vp, c_vp]),
+    "sdb_copy_async": (c_int, [c_vp, c_vp, c_i64, c_vp]),
     "sdb_host_mapped": (c_int, [c_vp, ctypes.POINTER(c_vp)]),
     "sdb_pcg64_swap_targets": (c_int, [c_i64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                        ctypes.c_uint64, c_vp]),

@@ -31,7 +31,8 @@ __global__ void k_gather_rows(int64_t rows, int m, const T* __restrict__ in, int
 template <typename T, int MPL, int U>
 __global__ void __launch_bounds__(256)
 k_ingest_gather(int64_t rows, int m, const double* __restrict__ src, int64_t ldi, const int64_t* __restrict__ perm,
-                T* __restrict__ out, int64_t ldo, int32_t* __restrict__ bad) {
+                T* __restrict__ out, int64_t ldo, int32_t* __restrict__ bad, const double* __restrict__ dsrc,
+                int64_t drows) {
     const int lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
     const int64_t nw = (int64_t)gridDim.x * wpb;
@@ -41,7 +42,9 @@ k_ingest_gather(int64_t rows, int m, const double* __restrict__ src, int64_t ldi
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int64_t r = r0 + u;
-            const double* row = r < rows ? src + perm[r] * ldi : src;
+            const int64_t pr = r < rows ? perm[r] : 0;
+            // source rows below drows were copied to the device beforehand
+            const double* row = pr < drows ? dsrc + pr * ldi : src + pr * ldi;
 #pragma unroll
             for (int q = 0; q < MPL; ++q) {
                 const int t = lane + 32 * q;
@@ -67,37 +70,37 @@ k_ingest_gather(int64_t rows, int m, const double* __restrict__ src, int64_t ldi
 
 template <typename T, int MPL>
 static void launch_gather(bool host, int64_t rows, int m, const double* src, int64_t ldi, const int64_t* perm,
-                          T* out, int64_t ldo, int32_t* bad, cudaStream_t st) {
+                          T* out, int64_t ldo, int32_t* bad, const double* dsrc, int64_t drows, cudaStream_t st) {
     if (host) {
         // pinned host source: 64 CTAs keep ~2K rows (~1 MB) in flight, plenty
         // for PCIe, and leave the SMs to concurrently running training kernels
         // (measured: one 2-warp CTA per SM reads PCIe ~15% slower)
         const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((rows + 31) / 32, 64));
-        k_ingest_gather<T, MPL, 4><<<g, 256, 0, st>>>(rows, m, src, ldi, perm, out, ldo, bad);
+        k_ingest_gather<T, MPL, 4><<<g, 256, 0, st>>>(rows, m, src, ldi, perm, out, ldo, bad, dsrc, drows);
     } else {
         const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((rows + 31) / 32, 148 * 16));
-        k_ingest_gather<T, MPL, 4><<<g, 256, 0, st>>>(rows, m, src, ldi, perm, out, ldo, bad);
+        k_ingest_gather<T, MPL, 4><<<g, 256, 0, st>>>(rows, m, src, ldi, perm, out, ldo, bad, dsrc, drows);
     }
 }
 
 template <typename T>
 int ingest_gather(int64_t rows, int m, const double* src, int64_t ldi, const int64_t* perm, T* out, int64_t ldo,
-                  int32_t* bad, cudaStream_t st) {
+                  int32_t* bad, cudaStream_t st, const double* dsrc, int64_t drows) {
     if (rows <= 0) return 0;
     cudaPointerAttributes at{};
     const bool host = cudaPointerGetAttributes(&at, src) == cudaSuccess && at.type == cudaMemoryTypeHost;
     cudaGetLastError();
     const int mpl = (m + 31) / 32;
-    if (mpl <= 1) launch_gather<T, 1>(host, rows, m, src, ldi, perm, out, ldo, bad, st);
-    else if (mpl <= 2) launch_gather<T, 2>(host, rows, m, src, ldi, perm, out, ldo, bad, st);
-    else if (mpl <= 5) launch_gather<T, 5>(host, rows, m, src, ldi, perm, out, ldo, bad, st);
-    else launch_gather<T, 8>(host, rows, m, src, ldi, perm, out, ldo, bad, st);
+    if (mpl <= 1) launch_gather<T, 1>(host, rows, m, src, ldi, perm, out, ldo, bad, dsrc, drows, st);
+    else if (mpl <= 2) launch_gather<T, 2>(host, rows, m, src, ldi, perm, out, ldo, bad, dsrc, drows, st);
+    else if (mpl <= 5) launch_gather<T, 5>(host, rows, m, src, ldi, perm, out, ldo, bad, dsrc, drows, st);
+    else launch_gather<T, 8>(host, rows, m, src, ldi, perm, out, ldo, bad, dsrc, drows, st);
     return (int)cudaGetLastError();
 }
 template int ingest_gather<float>(int64_t, int, const double*, int64_t, const int64_t*, float*, int64_t, int32_t*,
-                                  cudaStream_t);
+                                  cudaStream_t, const double*, int64_t);
 template int ingest_gather<double>(int64_t, int, const double*, int64_t, const int64_t*, double*, int64_t,
-                                   int32_t*, cudaStream_t);
+                                   int32_t*, cudaStream_t, const double*, int64_t);
 
 // CSC (indptr, indices, data) -> codes rows (idx N x cap, val, counts)
 template <typename T>

@@ -9,7 +9,7 @@ int gather_rows(int64_t rows, int m, const T* in, int64_t ldi, const int64_t* pe
                 cudaStream_t st);
 template <typename T>
 int ingest_gather(int64_t rows, int m, const double* src, int64_t ldi, const int64_t* perm, T* out, int64_t ldo,
-                  int32_t* bad, cudaStream_t st);
+                  int32_t* bad, cudaStream_t st, const double* dsrc = nullptr, int64_t drows = 0);
 template <typename T>
 int csc_to_codes(int64_t N, int cap, const int64_t* indptr, const int64_t* indices, const double* data,
                  int32_t* idx, T* val, int32_t* counts, cudaStream_t st);

@@ -404,6 +404,26 @@ int sdb_ingest_gather(int dtype, int64_t rows, int64_t m, const double* src, int
     return cuda_rc(rc, "sdb_ingest_gather");
 }
 
+int sdb_ingest_gather_split(int dtype, int64_t rows, int64_t m, const double* src, int64_t ldi,
+                            const int64_t* perm, const double* dsrc, int64_t drows, void* out, int64_t ldo,
+                            int32_t* bad, void* stream) {
+    if (!dtype_ok(dtype) || rows < 0 || m < 1 || m > 256 || ldi < m || ldo < m || drows < 0 ||
+        (drows > 0 && dsrc == nullptr) ||
+        (rows > 0 && (src == nullptr || perm == nullptr || out == nullptr || bad == nullptr)))
+        return fail(SDB_EINVAL, "sdb_ingest_gather_split: bad args");
+    int rc = dtype == SDB_F64
+                 ? sdb::ingest_gather<double>(rows, (int)m, src, ldi, perm, (double*)out, ldo, bad, S(stream), dsrc, drows)
+                 : sdb::ingest_gather<float>(rows, (int)m, src, ldi, perm, (float*)out, ldo, bad, S(stream), dsrc, drows);
+    return cuda_rc(rc, "sdb_ingest_gather_split");
+}
+
+int sdb_copy_async(void* dst, const void* src, int64_t bytes, void* stream) {
+    if (bytes < 0 || (bytes > 0 && (dst == nullptr || src == nullptr)))
+        return fail(SDB_EINVAL, "sdb_copy_async: bad args");
+    if (bytes == 0) return SDB_OK;
+    return cuda_rc((int)cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDefault, S(stream)), "sdb_copy_async");
+}
+
 int sdb_host_mapped(const void* host, void** dev) {
     if (host == nullptr || dev == nullptr) return fail(SDB_EINVAL, "sdb_host_mapped: bad args");
     cudaPointerAttributes at{};

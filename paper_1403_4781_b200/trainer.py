@@ -464,7 +464,7 @@ def _group_streams(G: int) -> tuple:
 
 def _split_locals(src, N: int, m: int, L: int, K1: int, local_cap: int, local_eps: float,
                   local_iters: int, seeds, perm: torch.Tensor, prec: str, use_tc: bool, groups: int,
-                  host_f64: int | None = None, bad: torch.Tensor | None = None):
+                  host_f64: int | None = None, bad: torch.Tensor | None = None, head=(None, 0)):
     """split_dataset + every train_local (trainer.py:291-305), in G groups of
     consecutive shards, each on its own CUDA stream. The group's rows are
     gathered in permuted order (all gathers in order on one copy stream, so
@@ -498,7 +498,7 @@ def _split_locals(src, N: int, m: int, L: int, K1: int, local_cap: int, local_ep
         for g in range(G):
             r0, r1 = int(offs[bounds[g]]), int(offs[bounds[g + 1]])
             if host_f64 is not None:
-                Ys = E.ingest_gather(host_f64, m, perm, r0, r1, m, prec, bad[g:g + 1])
+                Ys = E.ingest_gather(host_f64, m, perm, r0, r1, m, prec, bad[g:g + 1], head=head)
             else:
                 Ys = E.gather_rows(src, perm[r0:r1], prec)
             ev = torch.cuda.Event()
@@ -589,18 +589,32 @@ def split_merge_device(Ydev: torch.Tensor, L: int, K1: int, local_cap: int, loca
 
 
 HOST_GROUPS = int(os.environ.get("SDB_HOST_GROUPS", "4"))  # shard groups streamed from pinned host memory
+# 1/HEAD_DIV of a host batch is copied ahead (during the host permutation)
+HEAD_DIV = int(os.environ.get("SDB_HEAD_DIV", "8"))
 
 
 def _split_merge_host(src: int, N: int, m: int, cfg, cap1: int, eps1: float, local_iters: int,
                       merge_iters: int, prec: str, t0: float) -> SplitMergeResult:
     """train_split_merge's device pipeline for pinned host input (``src``:
-    device address of the f64 N x m rows)."""
+    device address of the f64 N x m rows). While the host forms the split
+    permutation, the first rows of the batch (in source order) are copied to
+    the device; the group gathers then read those from HBM and only the rest
+    over PCIe."""
+    G = max(1, min(int(HOST_GROUPS), cfg.L))
+    copy, _ = _group_streams(G)
+    head = N // HEAD_DIV if HEAD_DIV > 0 else 0
+    Yhead = None
+    if head > 0:
+        Yhead = E.empty((head, m), torch.float64)
+        copy.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(copy):
+            E._lib.call("sdb_copy_async", E.ptr(Yhead), src, head * m * 8, E.stream())
     perm = E.split_permutation(N, cfg.seed)
     t_split = time.perf_counter()
     seeds = _derive_seeds(cfg.seed, cfg.L + 1)
     bad = E.zeros((max(1, cfg.L),), torch.int32)  # one non-finite flag per group (<= L groups)
     Dl, w = _split_locals(None, N, m, cfg.L, cfg.K1, cap1, eps1, local_iters, seeds, perm, prec,
-                          True, HOST_GROUPS, host_f64=src, bad=bad)
+                          True, HOST_GROUPS, host_f64=src, bad=bad, head=(Yhead, head))
     t_local = time.perf_counter()
     Dm, w_h, n_merge = _merge(Dl, w, cfg.K1, m, cfg.K, cfg.s2, merge_iters, seeds[cfg.L],
                               cfg.init, prec, True)
