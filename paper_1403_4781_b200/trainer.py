@@ -252,6 +252,7 @@ class _GraphedLoop:
 
 
 _GRAPH_CACHE: dict = {}
+GRAPH_CACHE_MAX = 16
 
 
 def _graphed(S: E.ShardSet, D0: torch.Tensor, cap: int, eps: float, use_tc: bool,
@@ -262,6 +263,11 @@ def _graphed(S: E.ShardSet, D0: torch.Tensor, cap: int, eps: float, use_tc: bool
            E.get_precision(None), torch.cuda.current_device(), E.FUSE_STEP1, tag)
     g = _GRAPH_CACHE.get(key)
     if g is None:
+        if len(_GRAPH_CACHE) >= GRAPH_CACHE_MAX:
+            # bounded: each entry holds a graph and its static buffers (a copy of
+            # the signals); the oldest shape goes, once nothing can still replay it
+            torch.cuda.synchronize()
+            _GRAPH_CACHE.pop(next(iter(_GRAPH_CACHE)))
         g = _GRAPH_CACHE[key] = _GraphedLoop(S, D0, cap, eps, use_tc)
     return g
 
