@@ -90,6 +90,23 @@ int sdb_omp(int dtype, int64_t N, int64_t m, int64_t K, int64_t P, const int64_t
             const void *G, int64_t cap, double eps, double guard, int32_t *idx, void *val,
             int32_t *counts, int8_t *status, void *rnorm, const float *ysq, void *scratch,
             int64_t scratch_bytes, void *stream);
+/* Fused tensor-core Batch-OMP, FP32 (replaces sdb_correlate + sdb_omp for
+ * _kernels.omp_batch_range, _kernels.py:161-173, when m <= 64, K <= 512 and
+ * cap <= 8): tiles of 128 signals of one shard; every greedy step's
+ * correlations D^T r are one tcgen05 kind::tf32 MMA of the tile's residuals
+ * against the shard's dictionary resident in shared memory; the argmax is
+ * decided exactly by re-evaluating in FP32 every atom within the TF32 error
+ * window of the maximum (lowest index on ties); stall, singular-guard and eps
+ * rules of omp_single (_kernels.py:61-154). No alpha0 matrix is formed.
+ * D: P x K x m fp32 atom-major; G: P x K x K fp32. rnorm, gap optional
+ * (gap[i] = smallest relative margin of the chosen atom over the runner-up
+ * across the steps: the near-tie log). ws: sdb_omp_tc_workspace_bytes(). */
+int sdb_omp_tc_supported(int64_t m, int64_t K, int64_t cap);
+int64_t sdb_omp_tc_workspace_bytes(int64_t P, int64_t m, int64_t K);
+int sdb_omp_tc(int64_t N, int64_t m, int64_t K, int64_t P, const int64_t *shard_off, const float *Y,
+               int64_t ldy, const float *D, const float *G, int64_t cap, double eps, double guard,
+               int32_t *idx, float *val, int32_t *counts, int8_t *status, float *rnorm, float *gap,
+               void *ws, int64_t ws_bytes, void *stream);
 /* Error-bounded FP32 coding in two launches (replaces sdb_correlate +
  * sdb_omp for the training loop's ε-mode passes, configs 2-3):
  * sdb_code_step1 is the tcgen05 correlation GEMM whose epilogue also runs the

@@ -65,6 +65,10 @@ KSTAT: dict = {}
 # error-bounded FP32 coding through sdb_code_step1 + sdb_omp_deferred (False:
 # sdb_correlate + sdb_omp; the codes are bitwise the same, tests compare both)
 FUSE_STEP1 = True
+# FP32 coding with m <= 64, K <= 512, cap <= 8 through the fused tensor-core
+# Batch-OMP (sdb_omp_tc: per-step D^T r on tcgen05, no alpha0 in HBM); False:
+# sdb_correlate + sdb_omp (k_omp_fast)
+OMP_TC = os.environ.get("SDB_OMP_TC", "1") != "0"
 
 
 def timed_call(name: str, nbytes: float, flops: float, fn, *args):
@@ -172,6 +176,7 @@ class DeviceCodes:
     counts: torch.Tensor   # (N,) int32
     status: torch.Tensor   # (N,) int8
     rnorm: torch.Tensor    # (N,) working precision
+    gap: torch.Tensor | None = None   # (N,) fp32 near-tie margin (sdb_omp_tc, when requested)
 
     @property
     def N(self) -> int:
@@ -220,9 +225,14 @@ def alpha_chunk_rows(K: int, prec: str) -> int:
     return max(1, (4 << 30) // (K * (8 if prec == "fp64" else 4)))
 
 
+def omp_tc_applies(m: int, K: int, cap: int, prec: str, use_tc: bool = True) -> bool:
+    return (OMP_TC and use_tc and prec == "fp32"
+            and bool(_lib.load().sdb_omp_tc_supported(m, K, cap)))
+
+
 def code(Ydev: torch.Tensor, off: torch.Tensor, max_rows: int, DT: torch.Tensor, G: torch.Tensor,
          cap: int, eps: float, prec: str, use_tc: bool = True, out: DeviceCodes | None = None,
-         ysq: torch.Tensor | None = None, want_rnorm: bool = True) -> DeviceCodes:
+         ysq: torch.Tensor | None = None, want_rnorm: bool = True, want_gap: bool = False) -> DeviceCodes:
     """OMP over every row of Ydev; row i uses the dictionary of its shard.
 
     ysq: optional per-signal FP32 ||y||^2 from signal_sq (fp32 only; the
@@ -237,10 +247,22 @@ def code(Ydev: torch.Tensor, off: torch.Tensor, max_rows: int, DT: torch.Tensor,
                           empty((N,), torch.int32), empty((N,), torch.int8), empty((N,), tdt))
     if N == 0:
         return out
-    alpha = empty((N, K), tdt)
     es = 8 if prec == "fp64" else 4
-    if (FUSE_STEP1 and prec == "fp32" and use_tc and ysq is not None and eps > 0.0 and not want_rnorm
-            and K <= 256 and m <= 256 and cap <= 32 and K % 4 == 0 and m % 4 == 0 and N < 2**31):
+    fused1 = (FUSE_STEP1 and prec == "fp32" and use_tc and ysq is not None and eps > 0.0 and not want_rnorm
+              and K <= 256 and m <= 256 and cap <= 32 and K % 4 == 0 and m % 4 == 0 and N < 2**31)
+    if not fused1 and N < 2**31 and omp_tc_applies(m, K, cap, prec, use_tc):
+        wb = _lib.load().sdb_omp_tc_workspace_bytes(P, m, K)
+        ws = empty((wb,), torch.uint8)
+        if want_gap:
+            out.gap = empty((N,), torch.float32)
+        # algorithmic HBM bytes per signal: y row in, code row + count + status out
+        timed_call("omp_tc", N * (4 * m + cap * 8 + 5 + (4 if want_rnorm else 0)), 2.0 * N * m * K * cap,
+                   "sdb_omp_tc", N, m, K, P, ptr(off), ptr(Ydev), Ydev.stride(0), ptr(DT), ptr(G), cap,
+                   float(eps), GUARD[prec], ptr(out.idx), ptr(out.val), ptr(out.counts), ptr(out.status),
+                   ptr(out.rnorm) if want_rnorm else None, ptr(out.gap), ptr(ws), int(wb), stream())
+        return out
+    alpha = empty((N, K), tdt)
+    if fused1:
         # error-bounded mode: GEMM + first greedy step fused, OMP only for the
         # signals that need more (bitwise the same codes as the path below)
         wb = _lib.load().sdb_code_step1_workspace_bytes(P, m, K)

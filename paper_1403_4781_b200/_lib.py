@@ -44,6 +44,10 @@ SIGNATURES = {
     "sdb_omp_deferred": (c_int, [c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp,
                                  c_vp, c_vp, c_i64, c_dbl, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp,
                                  c_i64, c_vp]),
+    "sdb_omp_tc_supported": (c_int, [c_i64, c_i64, c_i64]),
+    "sdb_omp_tc_workspace_bytes": (c_i64, [c_i64, c_i64, c_i64]),
+    "sdb_omp_tc": (c_int, [c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_dbl, c_dbl,
+                           c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "sdb_csc_workspace_bytes": (c_i64, [c_i64]),
     "sdb_csc_indptr": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp]),
     "sdb_csc_fill": (c_int, [c_int, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),

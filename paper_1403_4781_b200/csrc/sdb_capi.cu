@@ -55,7 +55,7 @@ __global__ void k_cast(int64_t n, const double* __restrict__ src, T* __restrict_
 
 extern "C" {
 
-int sdb_abi_version(void) { return 3; }
+int sdb_abi_version(void) { return 5; }
 const char* sdb_last_error(void) { return g_err.c_str(); }
 
 int sdb_device_cc(void) {
@@ -183,6 +183,31 @@ int sdb_omp(int dtype, int64_t N, int64_t m, int64_t K, int64_t P, const int64_t
         rc = sdb::launch_omp<float>(a, S(stream));
     }
     return cuda_rc(rc, "sdb_omp");
+}
+
+// ---- fused tensor-core Batch-OMP (FP32): corr = D^T r per step on tcgen05
+int64_t sdb_omp_tc_workspace_bytes(int64_t P, int64_t m, int64_t K) {
+    if (P < 1 || m < 1 || K < 1) return fail(SDB_EINVAL, "sdb_omp_tc_workspace_bytes: bad args");
+    return sdb::omp_tc_ws_bytes(P, m, K);
+}
+
+int sdb_omp_tc_supported(int64_t m, int64_t K, int64_t cap) { return sdb::omp_tc_supported(m, K, cap) ? 1 : 0; }
+
+int sdb_omp_tc(int64_t N, int64_t m, int64_t K, int64_t P, const int64_t* shard_off, const float* Y,
+               int64_t ldy, const float* D, const float* G, int64_t cap, double eps, double guard,
+               int32_t* idx, float* val, int32_t* counts, int8_t* status, float* rnorm, float* gap,
+               void* ws, int64_t ws_bytes, void* stream) {
+    if (N < 0 || m < 1 || K < 1 || P < 1 || cap < 1 || ldy < m || eps < 0.0)
+        return fail(SDB_EINVAL, "sdb_omp_tc: bad args");
+    if (!sdb::omp_tc_supported(m, K, cap))
+        return fail(SDB_ENOTSUP, "sdb_omp_tc: needs m <= 64, K <= 512, cap <= 8");
+    if (N > 0x7fffffffll) return fail(SDB_EINVAL, "sdb_omp_tc: N >= 2^31");
+    if (N == 0) return SDB_OK;
+    if (ws == nullptr || ws_bytes < sdb::omp_tc_ws_bytes(P, m, K))
+        return fail(SDB_EINVAL, "sdb_omp_tc: workspace of %lld bytes required", (long long)sdb::omp_tc_ws_bytes(P, m, K));
+    int rc = sdb::omp_tc_f32(N, (int)m, (int)K, (int)P, shard_off, Y, ldy, D, G, (int)cap, (float)eps,
+                             (float)guard, idx, val, counts, status, rnorm, gap, ws, ws_bytes, S(stream));
+    return cuda_rc(rc, "sdb_omp_tc");
 }
 
 // ---- fused first greedy step (error-bounded FP32 coding)

@@ -61,6 +61,13 @@ int code_step1_tc_f32(int64_t N, const float* Y, int64_t ldy, const int64_t* off
 
 template <typename T>
 int launch_omp(OmpArgs<T> a, cudaStream_t st);
+
+// fused tensor-core Batch-OMP (sdb_omp_tc.cu): FP32, m <= 64, K <= 512, cap <= 8
+bool omp_tc_supported(int64_t m, int64_t K, int64_t cap);
+int64_t omp_tc_ws_bytes(int64_t P, int64_t m, int64_t K);
+int omp_tc_f32(int64_t N, int m, int K, int P, const int64_t* off, const float* Y, int64_t ldy, const float* D,
+               const float* G, int cap, float eps, float guard, int32_t* idx, float* val, int32_t* counts,
+               int8_t* status, float* rnorm, float* gap, void* ws, int64_t ws_bytes, cudaStream_t st);
 int64_t omp_warp_bytes_f32(int cap, int m);
 int64_t omp_warp_bytes_f64(int cap, int m);
 

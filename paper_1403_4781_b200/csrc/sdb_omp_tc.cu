@@ -1,0 +1,648 @@
+// Fused tensor-core Batch-OMP (FP32 mode, sm_100a): omp_single
+// (_kernels.py:38-158) for tiles of 128 signals of one shard, where every
+// greedy step's correlations corr = D^T r are ONE tcgen05 MMA of the tile's
+// residual matrix R (128 x m, shared memory) against the shard's dictionary
+// (K x m, resident in shared memory) into TMEM — the alpha0 = D^T Y GEMM is the
+// first step's MMA, so no correlation matrix ever touches HBM and no G row is
+// streamed per step (the Batch-OMP update corr = c0 - G_S x of k_omp_fast is
+// replaced by recomputing D^T r on the tensor pipe).
+//
+// Precision. The MMA is kind::tf32 (operands truncated to 10-bit mantissas,
+// fp32 accumulation), so |corr_tf32 - d.r| <= 2^-9 ||d|| ||r|| (+ 2^-16 ||r||
+// accumulation). The argmax is decided exactly: every atom whose TF32 value
+// lies within a window (2^-7 ||r||, twice the bound, plus 1e-6 ||y|| for the
+// numerical residue of support atoms) of the TF32 maximum is a candidate, and
+// the candidates' correlations are recomputed in FP32 on the CUDA cores from
+// the resident dictionary and the exact residual (both in shared memory);
+// the largest |d.r| wins, lowest index on ties (the reference's 1e-12 tie
+// window is below FP32 resolution, as in k_omp_fast). More than OT_CMAX
+// candidates (or none outside the support) fall back to an exact sweep over
+// all atoms. The per-signal relative gap between the winner and the runner-up
+// is reported (near-tie log, north_star).
+//
+// Per step and signal (thread = signal, TMEM lane = tile row):
+//   scan:   block maxima of |corr_tf32| over the row (tcgen05.ld), then the
+//           candidates above the threshold (second TMEM pass on the blocks
+//           some lane needs)
+//   refine: exact d_j.r for the candidates (shared memory)
+//   stop:   stall (cmax <= 1e-13 ||r||, _kernels.py:97-100); Cholesky append
+//           with G[S,b], G[b,b] (L2) and the singular guard (_kernels.py:109-127)
+//   solve:  forward/back substitution with L in registers (_kernels.py:129-139)
+//   update: r -= D_S (x_new - x_old) in place in R (the next MMA's A operand),
+//           ||r||^2 explicit (_kernels.py:141-154); eps test on ||r||
+//
+// Roles (one persistent CTA per SM, 10 warps):
+//   warp 0    TMA producer: the shard's padded dictionary (4 boxes of 256 x 32)
+//   warp 1    TMEM allocation (512 columns) + MMA issuer (one thread)
+//   warps 2-5 signal group 0, warps 6-9 signal group 1: each group codes its
+//             own tile; the MMA of one group's step overlaps the other
+//             group's CUDA-core work. K > 256: the two 256-column chunk
+//             buffers alternate between the groups; K <= 256: one buffer each.
+// Tiles: each CTA owns a contiguous range of the (shard, tile) sequence and
+// walks it in rounds of two tiles of the same shard; the dictionary is
+// reloaded when the shard changes (after both groups released the old one).
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "sdb_common.cuh"
+#include "sdb_internal.h"
+#include "sdb_tc.cuh"
+
+namespace sdb {
+
+bool tc_map_f32(CUtensorMap* map, const float* ptr, int64_t cols, int64_t rows, int64_t ld_elems,
+                int box_rows);
+
+namespace {
+
+constexpr int OT_M = 128;          // signals per tile (UMMA M, TMEM lanes)
+constexpr int OT_N = 256;          // atoms per MMA chunk (UMMA N)
+constexpr int OT_NGRP = 2;         // signal groups (tiles in flight per CTA)
+constexpr int OT_WARPS = 2 + 4 * OT_NGRP;
+constexpr int OT_CMAX = 6;         // candidates refined per step before the exact sweep
+constexpr float OT_WIN = 0.0078125f;   // 2^-7: candidate window, relative to ||r||
+constexpr int OT_RB = OT_M * 128;  // bytes of one 32-column k-block of R
+
+struct OtArgs {
+    int64_t N;
+    int m, K, P, cap, nkb, nch, kpad;
+    const int64_t* off;   // P+1 signal offsets
+    const int64_t* ts;    // P+1 tile prefix (first tile of each shard)
+    const float* Y;
+    int64_t ldy;
+    const float* G;       // P x K x K
+    float eps, guard;
+    int32_t* idx;
+    float* val;
+    int32_t* counts;
+    int8_t* status;
+    float* rnorm;         // optional
+    float* gap;           // optional: min relative gap best vs runner-up over the steps
+};
+
+__device__ __forceinline__ int tile_shard(const int64_t* __restrict__ ts, int P, int64_t t) {
+    int lo = 0, hi = P - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (__ldg(ts + mid) <= t) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+// A round: up to two consecutive tiles of one shard (one per signal group).
+struct Round {
+    int p;
+    int64_t t0;
+    bool has1, first, last;
+};
+
+struct RoundIter {
+    const int64_t* ts;
+    int P;
+    int64_t pos, end;
+    int prev;
+    __device__ bool next(Round& r) {
+        if (pos >= end) return false;
+        r.p = tile_shard(ts, P, pos);
+        const int64_t pend = __ldg(ts + r.p + 1);
+        r.t0 = pos;
+        r.has1 = pos + 1 < end && pos + 1 < pend;
+        pos += r.has1 ? 2 : 1;
+        r.first = r.p != prev;
+        prev = r.p;
+        r.last = pos >= end || pos >= pend;
+        return true;
+    }
+};
+
+__device__ __forceinline__ float4 lds4(const unsigned char* p) { return *reinterpret_cast<const float4*>(p); }
+
+template <int CAP>
+__global__ void __launch_bounds__(OT_WARPS * 32, 1)
+k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* base = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    const int dbytes = a.nkb * a.kpad * 128;
+    const int rbytes = a.nkb * OT_RB;
+    unsigned char* Ds = base;
+    uint64_t* bars = (uint64_t*)(base + dbytes + OT_NGRP * rbytes);
+    // full[g] 0..1, empty[b] 2..3, rfull[g] 4..5, dfull 6, dfree 7
+    int* votes = (int*)(bars + 8);            // [step parity][group][warp]
+    volatile int* contf = votes + 16;         // [group]
+    uint32_t* tslot = (uint32_t*)(votes + 20);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int K = a.K;
+
+    const int64_t ntiles = __ldg(a.ts + a.P);
+    const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
+    const int64_t tb = min(ntiles, (int64_t)blockIdx.x * per);
+    const int64_t te = min(ntiles, tb + per);
+
+    if (threadIdx.x == 0) {
+        for (int g = 0; g < 2; ++g) {
+            mbar_init(smem_u32(&bars[g]), 1);
+            mbar_init(smem_u32(&bars[2 + g]), 4);
+            mbar_init(smem_u32(&bars[4 + g]), 4);
+        }
+        mbar_init(smem_u32(&bars[6]), 1);
+        mbar_init(smem_u32(&bars[7]), 4 * OT_NGRP);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                     "r"(2 * OT_N));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    const uint32_t tmem = *tslot;
+
+    if (warp == 0) {
+        // ------------------------------------------------ dictionary producer
+        if (lane == 0) {
+            RoundIter it{a.ts, a.P, tb, te, -1};
+            Round r;
+            int k = 0;
+            while (it.next(r)) {
+                if (!r.first) continue;
+                if (k > 0) mbar_wait(smem_u32(&bars[7]), (uint32_t)((k - 1) & 1));
+                const uint32_t bf = smem_u32(&bars[6]);
+                mbar_expect_tx(bf, (uint32_t)dbytes);
+                for (int kb = 0; kb < a.nkb; ++kb)
+                    for (int c = 0; c < a.nch; ++c)
+                        tma_load_2d(smem_u32(Ds + kb * a.kpad * 128 + c * OT_N * 128), &tmD, kb * 32,
+                                    r.p * a.kpad + c * OT_N, bf);
+                ++k;
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(OT_N >> 3) << 17) |
+                                   ((uint32_t)(OT_M >> 4) << 24);
+            uint32_t uses[2] = {0, 0}, rph[2] = {0, 0};
+            int k = 0;
+            RoundIter it{a.ts, a.P, tb, te, -1};
+            Round r;
+            while (it.next(r)) {
+                if (r.first) {
+                    mbar_wait(smem_u32(&bars[6]), (uint32_t)(k & 1));
+                    ++k;
+                }
+                bool act[2] = {true, r.has1};
+                while (act[0] || act[1]) {
+                    for (int g = 0; g < 2; ++g) {
+                        if (!act[g]) continue;
+                        mbar_wait(smem_u32(&bars[4 + g]), rph[g] & 1u);
+                        ++rph[g];
+                        if (!contf[g]) {
+                            // tile done: acknowledge on full[g] so the group cannot
+                            // publish its next tile before this phase was consumed
+                            mbar_arrive(smem_u32(&bars[g]));
+                            act[g] = false;
+                            continue;
+                        }
+                        const unsigned char* Rg = base + dbytes + g * rbytes;
+                        for (int c = 0; c < a.nch; ++c) {
+                            const int b = a.nch == 2 ? c : g;
+                            if (uses[b]) mbar_wait(smem_u32(&bars[2 + b]), (uses[b] - 1) & 1u);
+                            ++uses[b];
+                            tmem_fence_after();
+                            const uint32_t tacc = tmem + (uint32_t)(b * OT_N);
+                            for (int kb = 0; kb < a.nkb; ++kb) {
+                                const uint64_t ad = sw128_desc(smem_u32(Rg + kb * OT_RB));
+                                const uint64_t bd = sw128_desc(smem_u32(Ds + kb * a.kpad * 128 + c * OT_N * 128));
+#pragma unroll
+                                for (int kk = 0; kk < 4; ++kk)
+                                    mma_tf32(tacc, ad + (uint64_t)(2 * kk), bd + (uint64_t)(2 * kk), idesc,
+                                             (kb | kk) ? 1u : 0u);
+                            }
+                        }
+                        mma_commit(smem_u32(&bars[g]));
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        // ------------------------------------------------ signal groups
+        const int g = (warp - 2) >> 2;
+        const int wi = (warp - 2) & 3;
+        const int q = warp & 3;                 // TMEM lane quadrant of this warp
+        const int row = q * 32 + lane;          // tile row = TMEM lane
+        unsigned char* R = base + dbytes + g * rbytes;
+        const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+        const int swz = row & 7;
+        uint32_t fph = 0;
+        int sp = 0;
+        int k = 0;
+        RoundIter it{a.ts, a.P, tb, te, -1};
+        Round rd;
+        auto rrow = [&](int kb, int cc) -> unsigned char* { return R + kb * OT_RB + row * 128 + ((cc ^ swz) << 4); };
+        auto drow = [&](int kb, int j, int cc) -> const unsigned char* {
+            return Ds + kb * a.kpad * 128 + j * 128 + ((cc ^ (j & 7)) << 4);
+        };
+        // d_j . r (exact FP32, both operands in shared memory)
+        auto dot = [&](int j) -> float {
+            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+            for (int kb = 0; kb < a.nkb; ++kb) {
+#pragma unroll
+                for (int cc = 0; cc < 8; ++cc) {
+                    const float4 d = lds4(drow(kb, j, cc));
+                    const float4 v = lds4(rrow(kb, cc));
+                    s0 = fmaf(d.x, v.x, s0);
+                    s1 = fmaf(d.y, v.y, s1);
+                    s2 = fmaf(d.z, v.z, s2);
+                    s3 = fmaf(d.w, v.w, s3);
+                }
+            }
+            return (s0 + s1) + (s2 + s3);
+        };
+        // votes of the group's four warps -> 1 if any lane wants another MMA
+        auto publish = [&](bool want) -> int {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // R writes -> MMA (async proxy)
+            const unsigned bal = __ballot_sync(SDB_FULL, want);
+            if (lane == 0) votes[sp * 8 + g * 4 + wi] = bal != 0u;
+            asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
+            const int c = votes[sp * 8 + g * 4] | votes[sp * 8 + g * 4 + 1] | votes[sp * 8 + g * 4 + 2] |
+                          votes[sp * 8 + g * 4 + 3];
+            sp ^= 1;
+            __syncwarp();
+            if (lane == 0) {
+                if (wi == 0) contf[g] = c;
+                mbar_arrive(smem_u32(&bars[4 + g]));
+            }
+            return c;
+        };
+
+        while (it.next(rd)) {
+            if (rd.first) {
+                mbar_wait(smem_u32(&bars[6]), (uint32_t)(k & 1));   // the shard's dictionary landed
+                ++k;
+            }
+            if (g == 0 || rd.has1) {
+                const int p = rd.p;
+                const int64_t tile = rd.t0 + g;
+                const int64_t row0 = __ldg(a.off + p) + (tile - __ldg(a.ts + p)) * OT_M;
+                const int64_t i = row0 + row;
+                const bool valid = i < __ldg(a.off + p + 1);
+                const float* __restrict__ Gp = a.G + (int64_t)p * K * K;
+                // ---- the tile's signals -> R (the first step's A operand), ||y||^2
+                float ysq = 0.0f;
+                {
+                    const float* yr = a.Y + i * a.ldy;
+                    const bool vec = ((a.ldy & 3) == 0) && ((((uintptr_t)a.Y) & 15) == 0);
+                    for (int kb = 0; kb < a.nkb; ++kb) {
+#pragma unroll
+                        for (int cc = 0; cc < 8; ++cc) {
+                            const int col = kb * 32 + cc * 4;
+                            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                            if (valid) {
+                                if (vec && col + 3 < a.m) {
+                                    v = __ldg(reinterpret_cast<const float4*>(yr + col));
+                                } else {
+                                    if (col < a.m) v.x = __ldg(yr + col);
+                                    if (col + 1 < a.m) v.y = __ldg(yr + col + 1);
+                                    if (col + 2 < a.m) v.z = __ldg(yr + col + 2);
+                                    if (col + 3 < a.m) v.w = __ldg(yr + col + 3);
+                                }
+                            }
+                            ysq = fmaf(v.x, v.x, ysq);
+                            ysq = fmaf(v.y, v.y, ysq);
+                            ysq = fmaf(v.z, v.z, ysq);
+                            ysq = fmaf(v.w, v.w, ysq);
+                            *reinterpret_cast<float4*>(rrow(kb, cc)) = v;
+                        }
+                    }
+                }
+                const float eps2 = a.eps * a.eps;
+                int n = 0, status = 0;
+                bool act = valid && !(ysq <= eps2 || ysq == 0.0f);
+                float rsq = ysq;
+                float gmin = 1.0f;
+                const float ynorm = sqrtf(ysq);
+                float L[CAP * (CAP + 1) / 2], invd[CAP], x[CAP], z[CAP];
+                int ids[CAP];
+#pragma unroll
+                for (int t = 0; t < CAP; ++t) { ids[t] = -1; x[t] = 0.f; z[t] = 0.f; invd[t] = 0.f; }
+#pragma unroll
+                for (int t = 0; t < CAP * (CAP + 1) / 2; ++t) L[t] = 0.f;
+                auto in_support = [&](int j) {
+                    bool s = false;
+#pragma unroll
+                    for (int t = 0; t < CAP; ++t) s |= (ids[t] == j);
+                    return s;
+                };
+
+                int cont = publish(act);
+                while (cont) {
+                    mbar_wait(smem_u32(&bars[g]), fph & 1u);
+                    ++fph;
+                    tmem_fence_after();
+                    // ---------------- scan: candidates within the window of the TF32 max
+                    const float rn = sqrtf(rsq);
+                    float thr = __int_as_float(0x7f800000);   // +inf: no candidates
+                    float win = 0.f;
+                    int nc = 0;
+                    int cand[OT_CMAX];
+#pragma unroll
+                    for (int s = 0; s < OT_CMAX; ++s) cand[s] = 0;
+                    if (__any_sync(SDB_FULL, act)) {
+                        float bm[16];
+#pragma unroll
+                        for (int bp = 0; bp < 8; ++bp) {
+                            const int c = bp >> 2;
+                            const int j0 = c * OT_N + (bp & 3) * 64;
+                            bm[2 * bp] = 0.f;
+                            bm[2 * bp + 1] = 0.f;
+                            if (c < a.nch && j0 < K) {
+                                uint32_t va[32], vb[32];
+                                const uint32_t col = (uint32_t)((a.nch == 2 ? c : g) * OT_N + (bp & 3) * 64);
+                                tmem_ld64(va, vb, trow + col);
+                                tmem_wait_ld();
+                                float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f;
+#pragma unroll
+                                for (int t = 0; t < 32; t += 2) {
+                                    m0 = fmaxf(m0, fabsf(__uint_as_float(va[t])));
+                                    m1 = fmaxf(m1, fabsf(__uint_as_float(va[t + 1])));
+                                    m2 = fmaxf(m2, fabsf(__uint_as_float(vb[t])));
+                                    m3 = fmaxf(m3, fabsf(__uint_as_float(vb[t + 1])));
+                                }
+                                bm[2 * bp] = fmaxf(m0, m1);
+                                bm[2 * bp + 1] = fmaxf(m2, m3);
+                            }
+                        }
+                        float cmax = 0.f;
+#pragma unroll
+                        for (int b = 0; b < 16; ++b) cmax = fmaxf(cmax, bm[b]);
+                        win = OT_WIN * rn + 1e-6f * ynorm;
+                        if (act) thr = cmax - win;
+#pragma unroll
+                        for (int blk = 0; blk < 16; ++blk) {
+                            const int c = blk >> 3;
+                            const int j0 = c * OT_N + (blk & 7) * 32;
+                            if (c < a.nch && j0 < K) {
+                                const bool mine = bm[blk] >= thr;
+                                if (__any_sync(SDB_FULL, mine)) {
+                                    uint32_t v[32];
+                                    const uint32_t col = (uint32_t)((a.nch == 2 ? c : g) * OT_N + (blk & 7) * 32);
+                                    tmem_ld32(v, trow + col);
+                                    tmem_wait_ld();
+                                    if (mine) {
+                                        unsigned msk = 0u;
+#pragma unroll
+                                        for (int t = 0; t < 32; ++t)
+                                            if (fabsf(__uint_as_float(v[t])) >= thr) msk |= 1u << t;
+                                        while (msk) {
+                                            const int j = j0 + __ffs(msk) - 1;
+                                            msk &= msk - 1u;
+                                            if (j < K && !in_support(j)) {
+                                                if (nc < OT_CMAX) {
+#pragma unroll
+                                                    for (int s = OT_CMAX - 1; s > 0; --s) cand[s] = cand[s - 1];
+                                                    cand[0] = j;
+                                                }
+                                                ++nc;
+                                            }
+                                        }
+                                    }
+                                }
+                            }
+                        }
+                    }
+                    // the chunk buffers go back to the MMA issuer
+                    tmem_fence_before();
+                    __syncwarp();
+                    if (lane == 0) {
+                        for (int c = 0; c < a.nch; ++c) mbar_arrive(smem_u32(&bars[2 + (a.nch == 2 ? c : g)]));
+                    }
+                    if (act) {
+                        // ---------------- exact selection among the candidates
+                        float best = -1.f, second = -1.f, eb = 0.f;
+                        int bj = -1;
+                        auto consider = [&](int j) {
+                            const float d = dot(j);
+                            const float ad = fabsf(d);
+                            if (ad > best || (ad == best && j < bj)) {
+                                second = best;
+                                best = ad;
+                                eb = d;
+                                bj = j;
+                            } else if (ad > second) {
+                                second = ad;
+                            }
+                        };
+                        if (nc >= 1 && nc <= OT_CMAX) {
+#pragma unroll
+                            for (int s = 0; s < OT_CMAX; ++s)
+                                if (s < nc) consider(cand[s]);
+                            // every non-candidate atom has |d.r| < thr + win/2
+                            second = fmaxf(second, thr + 0.5f * win);
+                        } else {
+                            for (int j = 0; j < K; ++j)
+                                if (!in_support(j)) consider(j);
+                        }
+                        if (best >= 0.f && best > 0.f) gmin = fminf(gmin, fmaxf(0.f, (best - second) / best));
+                        if (bj < 0 || best * best <= 1e-26f * rsq) {   // cmax <= 1e-13 ||r|| (_kernels.py:97)
+                            status = 3;
+                            act = false;
+                        } else {
+                            // ---------------- Cholesky append (_kernels.py:109-127)
+                            const float* __restrict__ Gb = Gp + (int64_t)bj * K;
+                            const float gbb = __ldg(Gb + bj);
+                            float gb[CAP];
+#pragma unroll
+                            for (int t = 0; t < CAP; ++t) gb[t] = (t < n) ? __ldg(Gb + ids[t]) : 0.f;
+                            float c0b = eb;   // d_b.y = d_b.r + G[b,S] x
+#pragma unroll
+                            for (int t = 0; t < CAP; ++t) c0b = fmaf(gb[t], x[t], c0b);
+                            float w[CAP];
+                            float dsq = gbb;
+#pragma unroll
+                            for (int t = 0; t < CAP; ++t) {
+                                float acc = gb[t];
+#pragma unroll
+                                for (int u = 0; u < t; ++u) acc = fmaf(-L[t * (t + 1) / 2 + u], w[u], acc);
+                                w[t] = (t < n) ? acc * invd[t] : 0.f;
+                                dsq = fmaf(-w[t], w[t], dsq);
+                            }
+                            if (dsq <= a.guard) {   // numerically singular support Gram
+                                status = 2;
+                                act = false;
+                            } else {
+                                const float inv = rsqrtf(dsq);
+                                float zn = c0b;
+#pragma unroll
+                                for (int t = 0; t < CAP; ++t) zn = fmaf(-w[t], z[t], zn);
+                                zn *= inv;
+#pragma unroll
+                                for (int rr = 0; rr < CAP; ++rr) {
+                                    if (rr == n) {
+#pragma unroll
+                                        for (int t = 0; t < rr; ++t) L[rr * (rr + 1) / 2 + t] = w[t];
+                                        L[rr * (rr + 1) / 2 + rr] = dsq * inv;
+                                        invd[rr] = inv;
+                                        ids[rr] = bj;
+                                        z[rr] = zn;
+                                    }
+                                }
+                                ++n;
+                                // back substitution L^T x = z
+                                float xn[CAP], dx[CAP];
+#pragma unroll
+                                for (int t = CAP - 1; t >= 0; --t) {
+                                    float acc = z[t];
+#pragma unroll
+                                    for (int u = t + 1; u < CAP; ++u)
+                                        if (u < n) acc = fmaf(-L[u * (u + 1) / 2 + t], xn[u], acc);
+                                    xn[t] = (t < n) ? acc * invd[t] : 0.f;
+                                }
+#pragma unroll
+                                for (int t = 0; t < CAP; ++t) {
+                                    dx[t] = xn[t] - x[t];
+                                    x[t] = xn[t];
+                                }
+                                const bool need_r = n < a.cap || a.rnorm != nullptr || a.eps > 0.f;
+                                if (need_r) {
+                                    // r -= D_S dx in place (the next MMA's A operand)
+                                    float r0 = 0.f, r1 = 0.f;
+                                    for (int kb = 0; kb < a.nkb; ++kb) {
+#pragma unroll
+                                        for (int cc = 0; cc < 8; ++cc) {
+                                            float4 v = lds4(rrow(kb, cc));
+#pragma unroll
+                                            for (int t = 0; t < CAP; ++t) {
+                                                if (t < n) {
+                                                    const float4 d = lds4(drow(kb, ids[t], cc));
+                                                    v.x = fmaf(-dx[t], d.x, v.x);
+                                                    v.y = fmaf(-dx[t], d.y, v.y);
+                                                    v.z = fmaf(-dx[t], d.z, v.z);
+                                                    v.w = fmaf(-dx[t], d.w, v.w);
+                                                }
+                                            }
+                                            *reinterpret_cast<float4*>(rrow(kb, cc)) = v;
+                                            r0 = fmaf(v.x, v.x, r0);
+                                            r1 = fmaf(v.y, v.y, r1);
+                                            r0 = fmaf(v.z, v.z, r0);
+                                            r1 = fmaf(v.w, v.w, r1);
+                                        }
+                                    }
+                                    rsq = r0 + r1;
+                                }
+                                if (n >= a.cap) act = false;
+                                else if (__fsqrt_rn(rsq) <= a.eps) act = false;   // _kernels.py:153
+                            }
+                        }
+                    }
+                    cont = publish(act);
+                }
+                // the MMA issuer's acknowledgement of the tile end
+                mbar_wait(smem_u32(&bars[g]), fph & 1u);
+                ++fph;
+                // ---- codes in selection order (entries >= n zeroed like the reference)
+                if (valid) {
+                    int32_t* ci = a.idx + i * a.cap;
+                    float* cv = a.val + i * a.cap;
+#pragma unroll
+                    for (int t = 0; t < CAP; ++t) {
+                        if (t < a.cap) {
+                            ci[t] = (t < n) ? ids[t] : 0;
+                            cv[t] = (t < n) ? x[t] : 0.f;
+                        }
+                    }
+                    a.counts[i] = n;
+                    a.status[i] = (int8_t)status;
+                    if (a.rnorm) a.rnorm[i] = __fsqrt_rn(rsq);
+                    if (a.gap) a.gap[i] = gmin;
+                }
+            }
+            if (rd.last) {
+                // this group no longer reads the shard's dictionary
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&bars[7]));
+            }
+        }
+    }
+    tmem_fence_before();
+    __syncthreads();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * OT_N));
+}
+
+// D (P x K x m fp32, atom-major) -> P x kpad x m_pad, zero padded
+__global__ void k_pad_dict(int64_t P, int K, int m, int kpad, int m_pad, const float* __restrict__ D,
+                           float* __restrict__ out) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t tot = P * kpad * m_pad;
+    if (e >= tot) return;
+    const int c = (int)(e % m_pad);
+    const int64_t rr = e / m_pad;
+    const int j = (int)(rr % kpad);
+    const int64_t p = rr / kpad;
+    out[e] = (j < K && c < m) ? D[(p * K + j) * m + c] : 0.0f;
+}
+
+__global__ void k_omp_tc_tiles(const int64_t* __restrict__ off, int P, int64_t* __restrict__ ts) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        int64_t t = 0;
+        for (int p = 0; p < P; ++p) {
+            ts[p] = t;
+            t += (off[p + 1] - off[p] + OT_M - 1) / OT_M;
+        }
+        ts[P] = t;
+    }
+}
+
+inline int64_t al256(int64_t b) { return (b + 255) & ~int64_t(255); }
+
+}  // namespace
+
+bool omp_tc_supported(int64_t m, int64_t K, int64_t cap) {
+    return m >= 1 && m <= 64 && K >= 1 && K <= 512 && cap >= 1 && cap <= 8;
+}
+
+int64_t omp_tc_ws_bytes(int64_t P, int64_t m, int64_t K) {
+    const int64_t m_pad = (m + 31) / 32 * 32, kpad = (K + OT_N - 1) / OT_N * OT_N;
+    return al256(P * kpad * m_pad * 4) + al256(8 * (P + 1));
+}
+
+int omp_tc_f32(int64_t N, int m, int K, int P, const int64_t* off, const float* Y, int64_t ldy, const float* D,
+               const float* G, int cap, float eps, float guard, int32_t* idx, float* val, int32_t* counts,
+               int8_t* status, float* rnorm, float* gap, void* ws, int64_t ws_bytes, cudaStream_t st) {
+    if (!omp_tc_supported(m, K, cap)) return (int)cudaErrorNotSupported;
+    if (N <= 0) return 0;
+    if (ws == nullptr || ws_bytes < omp_tc_ws_bytes(P, m, K)) return (int)cudaErrorInvalidValue;
+    const int m_pad = (m + 31) / 32 * 32;
+    const int nch = (K + OT_N - 1) / OT_N;
+    const int kpad = nch * OT_N;
+    float* Dp = (float*)ws;
+    int64_t* ts = (int64_t*)((unsigned char*)ws + al256((int64_t)P * kpad * m_pad * 4));
+    const int64_t tot = (int64_t)P * kpad * m_pad;
+    k_pad_dict<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(P, K, m, kpad, m_pad, D, Dp);
+    k_omp_tc_tiles<<<1, 32, 0, st>>>(off, P, ts);
+    CUtensorMap mD;
+    if (!tc_map_f32(&mD, Dp, m_pad, (int64_t)P * kpad, m_pad, OT_N)) return (int)cudaErrorNotSupported;
+    OtArgs a{};
+    a.N = N; a.m = m; a.K = K; a.P = P; a.cap = cap; a.nkb = m_pad / 32; a.nch = nch; a.kpad = kpad;
+    a.off = off; a.ts = ts; a.Y = Y; a.ldy = ldy; a.G = G; a.eps = eps; a.guard = guard;
+    a.idx = idx; a.val = val; a.counts = counts; a.status = status; a.rnorm = rnorm; a.gap = gap;
+    const int smem = 1024 + a.nkb * kpad * 128 + OT_NGRP * a.nkb * OT_RB + 256;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int n_sm = 148;
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    auto fn = cap <= 4 ? k_omp_tc<4> : k_omp_tc<8>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return (int)e;
+    const int64_t max_tiles = (N + OT_M - 1) / OT_M + P;
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(n_sm, max_tiles));
+    fn<<<grid, OT_WARPS * 32, smem, st>>>(mD, a);
+    return (int)cudaGetLastError();
+}
+
+}  // namespace sdb
