@@ -96,6 +96,8 @@ class NativeError(RuntimeError):
 
 
 _lib = None
+# must equal sdb_abi_version() in csrc/sdb_capi.cu (bumped whenever exports change)
+ABI_VERSION = 5
 
 
 def load():
@@ -109,6 +111,11 @@ def load():
         from . import build as _build
         _build.build()
     lib = ctypes.CDLL(str(LIB_PATH))
+    lib.sdb_abi_version.restype = c_int
+    got = lib.sdb_abi_version()
+    if got != ABI_VERSION:
+        raise NativeUnavailable(f"{LIB_PATH} has ABI {got}, expected {ABI_VERSION}: stale build "
+                                "(run python -m paper_1403_4781_b200.build --force)")
     for name, (res, args) in SIGNATURES.items():
         fn = getattr(lib, name)
         fn.restype = res

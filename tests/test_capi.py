@@ -37,7 +37,7 @@ def test_python_binding_covers_header():
 def test_abi_version_and_no_device():
     from paper_1403_4781_b200 import _lib
     lib = _lib.load()
-    assert lib.sdb_abi_version() == 3
+    assert lib.sdb_abi_version() == _lib.ABI_VERSION
     import torch
     if not torch.cuda.is_available():
         assert lib.sdb_device_cc() < 0
