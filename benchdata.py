@@ -45,6 +45,14 @@ def sparse_signals(D: np.ndarray, N: int, s: int, sigma: float, seed: int,
     return Y
 
 
+def sparse_signals_device(D: np.ndarray, N: int, s: int, sigma: float, seed: int, prec: str = "fp32"):
+    """The same sparse model generated on the GPU (sdb_synth_sparse, counter-
+    based Philox stream): (N, m) device tensor. The oracle is fed the very same
+    values (copy back the rows it needs)."""
+    from paper_1403_4781_b200 import _engine as E
+    return E.synth_sparse(D, N, s, sigma, seed, prec)
+
+
 def synthetic_image(rng, size: int = 512, n_components: int = 20) -> np.ndarray:
     """Sum of random-oriented step edges, 2-D sinusoids (0.01-0.2 cyc/px) and
     Gaussian blobs, min-max scaled to [0, 255]."""
@@ -102,6 +110,19 @@ CONFIGS = {
     "c4": dict(kind="sparse", m=64, K_true=512, N=4_000_000, s_true=8, sigma=0.02, L=256,
                K1=512, s1=8, eps=None, s_max=None, local_iters=8, K=512, s2=4, merge_iters=8),
 }
+
+
+def make_training_data_device(name: str, seed: int = 1234, prec: str = "fp32", N: int | None = None):
+    """Device (N, m) training signals of config ``name``: sparse-model configs
+    are generated on the GPU (sdb_synth_sparse); image configs are made on the
+    host (3 s for C2) and ingested."""
+    c = CONFIGS[name]
+    if c["kind"] == "sparse":
+        D = gen_dictionary(c["m"], c["K_true"], seed)
+        return sparse_signals_device(D, N or c["N"], c["s_true"], c["sigma"], seed + 1, prec)
+    from paper_1403_4781_b200 import _engine as E
+    Y = make_training_data(name, seed, N)
+    return E.ingest_signals(Y.T, prec)[0]
 
 
 def make_training_data(name: str, seed: int = 1234, N: int | None = None) -> np.ndarray:

@@ -249,6 +249,16 @@ int sdb_csc_to_codes(int dtype, int64_t N, int64_t cap, const int64_t *indptr,
 int sdb_normalize(int64_t rows, int64_t m, const double *in, double *out, double *scales,
                   void *stream);
 
+/* On-device synthetic sparse-model signals (replaces the host generator
+ * synthesis.py:56-79 gen_signals, with the additive N(0, sigma^2) noise of the
+ * BASELINE configs): Y[i*ldy + c] = sum_t coef_it D[a_it*m + c] + sigma n_ic,
+ * s distinct uniform atoms a_it, coef, n ~ N(0,1) from a counter-based
+ * Philox4x32-10 stream keyed by seed (each signal a fixed function of
+ * (seed, i)). D: K x m f64 atom-major (unit columns). sup_out: optional
+ * N x s int32 supports (draw order). dtype: output precision. */
+int sdb_synth_sparse(int dtype, int64_t N, int64_t m, int64_t K, int64_t s, const double *D, double sigma,
+                     uint64_t seed, void *Y, int64_t ldy, int32_t *sup_out, void *stream);
+
 /* extract_patches (denoising.py:118-135): img H x W f64 row-major -> patches
  * (R*C) x p^2 signal-major in dtype, R = (H-p)/s+1, C = (W-p)/s+1. */
 int sdb_extract_patches(int dtype, const double *img, int64_t H, int64_t W, int64_t p, int64_t s,

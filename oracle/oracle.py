@@ -319,18 +319,45 @@ def merge_dataset(locals_):
     return np.concatenate(blocks, axis=1)
 
 
+def _local_job(args):
+    """One train_local in a worker process (1 BLAS thread, like the
+    reference's process pool, trainer.py:301-305)."""
+    Yt, K1, s1, its, seed_t, eps, s_max = args
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(1):
+        D_t, X_t, _ = train_standard(Yt, K1, s1, its, "first-columns", seed_t, eps=eps, s_max=s_max)
+    return D_t, X_t
+
+
+def train_locals(Y, L, K1, s1, local_iters, seed, eps=None, s_max=None, threads=1, procs=1,
+                 only=None):
+    """split_dataset -> train_local for every shard (or the shard indices in
+    ``only``); ``procs`` > 1 trains shards in a process pool."""
+    Y = np.asarray(Y, dtype=np.float64)
+    seeds = derive_seeds(seed, L + 1)
+    parts = split_indices(Y.shape[1], L, seed)
+    todo = list(range(L)) if only is None else list(only)
+    jobs = [(np.ascontiguousarray(Y[:, parts[t]]), K1, s1, local_iters, seeds[t], eps, s_max) for t in todo]
+    if procs > 1 and len(jobs) > 1:
+        import multiprocessing as mp
+        with mp.get_context("fork").Pool(min(procs, len(jobs))) as pool:
+            return pool.map(_local_job, jobs, chunksize=1)
+    out = []
+    for j in jobs:
+        D_t, X_t, _ = train_standard(j[0], K1, s1, local_iters, "first-columns", j[4], eps=eps,
+                                     s_max=s_max, threads=threads)
+        out.append((D_t, X_t))
+    return out
+
+
 def split_merge(Y, L, K1, s1, local_iters, K, s2, merge_iters, seed, init="first-columns",
-                eps=None, s_max=None, merge_eps=None, merge_s_max=None, threads=1):
+                eps=None, s_max=None, merge_eps=None, merge_s_max=None, threads=1, procs=1):
     """split_dataset -> train_local -> merge_dictionaries (trainer.py:220-260,
     295-311), i.e. train_split_merge without its evaluation pass (SURVEY
     Appendix A). Returns (D, locals)."""
     Y = np.asarray(Y, dtype=np.float64)
     seeds = derive_seeds(seed, L + 1)
-    locals_ = []
-    for t, ids in enumerate(split_indices(Y.shape[1], L, seed)):
-        D_t, X_t, _ = train_standard(Y[:, ids], K1, s1, local_iters, "first-columns", seeds[t],
-                                     eps=eps, s_max=s_max, threads=threads)
-        locals_.append((D_t, X_t))
+    locals_ = train_locals(Y, L, K1, s1, local_iters, seed, eps, s_max, threads, procs)
     Ym = merge_dataset(locals_)
     kw = {} if merge_eps is None else dict(eps=merge_eps, s_max=merge_s_max)
     D, _X, _ = train_standard(Ym, K, s2, merge_iters, init, seeds[L], threads=threads, **kw)

@@ -69,6 +69,8 @@ FUSE_STEP1 = True
 # Batch-OMP (sdb_omp_tc: per-step D^T r on tcgen05, no alpha0 in HBM); False:
 # sdb_correlate + sdb_omp (k_omp_fast)
 OMP_TC = os.environ.get("SDB_OMP_TC", "1") != "0"
+# the kernels' 32-bit chunk counters overshoot N by < 2^22 (sdb_capi.cu OMP_DYN_MAX_N)
+DYN_MAX_N = (1 << 31) - (1 << 22)
 
 
 def timed_call(name: str, nbytes: float, flops: float, fn, *args):
@@ -249,8 +251,8 @@ def code(Ydev: torch.Tensor, off: torch.Tensor, max_rows: int, DT: torch.Tensor,
         return out
     es = 8 if prec == "fp64" else 4
     fused1 = (FUSE_STEP1 and prec == "fp32" and use_tc and ysq is not None and eps > 0.0 and not want_rnorm
-              and K <= 256 and m <= 256 and cap <= 32 and K % 4 == 0 and m % 4 == 0 and N < 2**31)
-    if not fused1 and N < 2**31 and omp_tc_applies(m, K, cap, prec, use_tc):
+              and K <= 256 and m <= 256 and cap <= 32 and K % 4 == 0 and m % 4 == 0 and N <= DYN_MAX_N)
+    if not fused1 and N <= DYN_MAX_N and omp_tc_applies(m, K, cap, prec, use_tc):
         wb = _lib.load().sdb_omp_tc_workspace_bytes(P, m, K)
         ws = empty((wb,), torch.uint8)
         if want_gap:
@@ -351,6 +353,21 @@ def csc(codes: DeviceCodes, prec: str):
         _lib.call("sdb_csc_fill", sdb_dtype(prec), N, codes.cap, ptr(codes.idx), ptr(codes.val),
                   ptr(codes.counts), ptr(indptr), ptr(indices), ptr(data), stream())
     return indptr, indices[:nnz], data[:nnz]
+
+
+def synth_sparse(D: np.ndarray, N: int, s: int, sigma: float, seed: int, prec: str,
+                 want_support: bool = False):
+    """On-device sparse-model signals (sdb_synth_sparse; synthesis.py:56-79
+    plus additive noise): (N, m) device rows in the working precision, and
+    optionally the (N, s) int32 supports in draw order."""
+    D = np.asarray(D, dtype=np.float64)
+    m, K = D.shape
+    Dd = torch.from_numpy(np.ascontiguousarray(D.T)).to(device())
+    Y = empty((N, m), torch_dtype(prec))
+    sup = empty((N, s), torch.int32) if want_support else None
+    _lib.call("sdb_synth_sparse", sdb_dtype(prec), N, m, K, s, ptr(Dd), float(sigma),
+              int(seed) & ((1 << 64) - 1), ptr(Y), m, ptr(sup), stream())
+    return (Y, sup) if want_support else Y
 
 
 def d2h(t: torch.Tensor) -> np.ndarray:

@@ -78,6 +78,8 @@ SIGNATURES = {
                                         c_vp, c_vp]),
     "sdb_copy_async": (c_int, [c_vp, c_vp, c_i64, c_vp]),
     "sdb_host_mapped": (c_int, [c_vp, ctypes.POINTER(c_vp)]),
+    "sdb_synth_sparse": (c_int, [c_int, c_i64, c_i64, c_i64, c_i64, c_vp, c_dbl, ctypes.c_uint64, c_vp, c_i64,
+                                 c_vp, c_vp]),
     "sdb_pcg64_swap_targets": (c_int, [c_i64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                        ctypes.c_uint64, c_vp]),
     "sdb_permutation_workspace_bytes": (c_i64, [c_i64]),
@@ -97,7 +99,7 @@ class NativeError(RuntimeError):
 
 _lib = None
 # must equal sdb_abi_version() in csrc/sdb_capi.cu (bumped whenever exports change)
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 
 def load():

@@ -55,7 +55,7 @@ __global__ void k_cast(int64_t n, const double* __restrict__ src, T* __restrict_
 
 extern "C" {
 
-int sdb_abi_version(void) { return 5; }
+int sdb_abi_version(void) { return 6; }
 const char* sdb_last_error(void) { return g_err.c_str(); }
 
 int sdb_device_cc(void) {
@@ -127,6 +127,10 @@ int sdb_correlate(int dtype, int64_t N, int64_t m, int64_t K, int64_t P, const i
 // scratch: [256 B: the FP32 kernel's work counter][per-warp global scratch
 // when the generic kernel's state does not fit shared memory]
 constexpr int64_t OMP_CTR_BYTES = 256;
+// The dynamic chunk counter is a 32-bit int and every warp claims one chunk
+// ahead, so it can overshoot N by up to 2 * warps * 32 (< 2^22): batches
+// closer than that to 2^31 use static warp ranges / are rejected.
+constexpr int64_t OMP_DYN_MAX_N = (int64_t(1) << 31) - (int64_t(1) << 22);
 
 int64_t sdb_omp_scratch_bytes(int dtype, int64_t N, int64_t m, int64_t cap) {
     if (!dtype_ok(dtype) || cap < 1 || m < 1) return fail(SDB_EINVAL, "sdb_omp_scratch_bytes: bad args");
@@ -152,7 +156,8 @@ int sdb_omp(int dtype, int64_t N, int64_t m, int64_t K, int64_t P, const int64_t
     if (need_global && (scratch == nullptr || scratch_bytes < OMP_CTR_BYTES + wb * 8))
         return fail(SDB_EINVAL, "sdb_omp: scratch of %lld bytes required", (long long)(OMP_CTR_BYTES + wb * 8));
     // a scratch of >= 256 bytes carries the FP32 kernel's chunk counter (zeroed here)
-    int* work = (scratch != nullptr && scratch_bytes >= OMP_CTR_BYTES) ? (int*)scratch : nullptr;
+    int* work = (scratch != nullptr && scratch_bytes >= OMP_CTR_BYTES && N <= OMP_DYN_MAX_N) ? (int*)scratch
+                                                                                            : nullptr;
     if (work) cudaMemsetAsync(work, 0, sizeof(int), S(stream));
     unsigned char* gscr = need_global ? (unsigned char*)scratch + OMP_CTR_BYTES : nullptr;
     const int64_t gscr_bytes = need_global ? scratch_bytes - OMP_CTR_BYTES : 0;
@@ -249,6 +254,7 @@ int sdb_omp_deferred(int64_t N, int64_t m, int64_t K, int64_t P, const int64_t* 
         return fail(SDB_ENOTSUP, "sdb_omp_deferred: needs K <= 1024, m <= 256, cap <= 32 and ysq");
     if (ws == nullptr || ws_bytes < sdb_code_step1_workspace_bytes(P, m, K))
         return fail(SDB_EINVAL, "sdb_omp_deferred: the sdb_code_step1 workspace is required");
+    if (N > OMP_DYN_MAX_N) return fail(SDB_ENOTSUP, "sdb_omp_deferred: N too close to 2^31 for the chunk counter");
     if (N == 0) return SDB_OK;
     sdb::OmpArgs<float> a{};
     a.N = N; a.m = (int)m; a.K = (int)K; a.cap = (int)cap; a.P = (int)P;
@@ -474,6 +480,15 @@ int sdb_csc_to_codes(int dtype, int64_t N, int64_t cap, const int64_t* indptr,
 int sdb_normalize(int64_t rows, int64_t m, const double* in, double* out, double* scales, void* stream) {
     if (rows < 0 || m < 1) return fail(SDB_EINVAL, "sdb_normalize: bad args");
     return cuda_rc(sdb::normalize_rows(rows, (int)m, in, out, scales, S(stream)), "sdb_normalize");
+}
+
+int sdb_synth_sparse(int dtype, int64_t N, int64_t m, int64_t K, int64_t s, const double* D, double sigma,
+                     uint64_t seed, void* Y, int64_t ldy, int32_t* sup_out, void* stream) {
+    if (!dtype_ok(dtype) || N < 0 || m < 1 || K < 1 || s < 1 || s > K || s > 64 || ldy < m || !(sigma >= 0.0))
+        return fail(SDB_EINVAL, "sdb_synth_sparse: bad args");
+    return cuda_rc(sdb::synth_sparse(dtype == SDB_F64, N, (int)m, (int)K, (int)s, D, sigma, seed, Y, ldy, sup_out,
+                                     S(stream)),
+                   "sdb_synth_sparse");
 }
 
 int sdb_extract_patches(int dtype, const double* img, int64_t H, int64_t W, int64_t p, int64_t s,

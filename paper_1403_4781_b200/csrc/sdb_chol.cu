@@ -1053,11 +1053,9 @@ static int chol_solve_cluster(int P, int K, int m, double* A, double* B, const i
                               double rel_tol, int8_t* depmask, int32_t* ndep, double* wsq, cudaStream_t st) {
     const int NC = (K + CB - 1) / CB;
     const int smem = (NC + 2) * TILE_D * (int)sizeof(double);
-    static int attr_smem = 0;
-    if (attr_smem < smem) {
-        cudaError_t e = cudaFuncSetAttribute(k_chol_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    {
+        cudaError_t e = set_max_smem((const void*)k_chol_cluster, smem);
         if (e != cudaSuccess) return (int)e;
-        attr_smem = smem;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(P * NC));
@@ -1090,14 +1088,13 @@ int chol_solve(int P, int K, int m, double* A, double* B, const int32_t* usage, 
     const int smem2 = 2 * CB * CBD * (int)sizeof(double);
     const int smemP = 2 * CB * CBP * (int)sizeof(double);
     const int smemD = (2 * CB * CBP + 32 * 33) * (int)sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_chol_update, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
-        cudaFuncSetAttribute(k_back_update, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
-        cudaFuncSetAttribute(k_chol_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, smemP);
-        cudaFuncSetAttribute(k_back_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, smemP);
-        cudaFuncSetAttribute(k_chol_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, smemD);
-        attr = true;
+    {
+        cudaError_t e = set_max_smem((const void*)k_chol_update, smem2);
+        if (e == cudaSuccess) e = set_max_smem((const void*)k_back_update, smem2);
+        if (e == cudaSuccess) e = set_max_smem((const void*)k_chol_panel, smemP);
+        if (e == cudaSuccess) e = set_max_smem((const void*)k_back_diag, smemP);
+        if (e == cudaSuccess) e = set_max_smem((const void*)k_chol_diag, smemD);
+        if (e != cudaSuccess) return (int)e;
     }
     {
         const int64_t KK = (int64_t)K * K;

@@ -11,6 +11,8 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <mutex>
+#include <unordered_map>
 
 #define SDB_WARP 32
 #define SDB_FULL 0xffffffffu
@@ -75,6 +77,24 @@ __device__ __forceinline__ int shard_of(const int64_t* __restrict__ off, int P, 
         if (__ldg(off + mid) <= i) lo = mid; else hi = mid - 1;
     }
     return lo;
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) applies per device
+// context: cache the largest size already set per (kernel, device) so a
+// process driving several GPUs sets it on each of them.
+inline cudaError_t set_max_smem(const void* fn, int smem) {
+    static std::mutex mu;
+    static std::unordered_map<uint64_t, int> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t key = ((uint64_t)(uintptr_t)fn << 8) ^ (uint64_t)dev;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = done.find(key);
+    if (it != done.end() && it->second >= smem) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess) done[key] = smem;
+    return e;
 }
 
 }  // namespace sdb

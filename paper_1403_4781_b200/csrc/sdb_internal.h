@@ -78,4 +78,7 @@ template <typename T>
 int pack_csc(int64_t N, int cap, const int32_t* idx, const T* val, const int32_t* counts,
              const int64_t* indptr, int64_t* out_idx, double* out_val, cudaStream_t st);
 
+int synth_sparse(int dtype_f64, int64_t N, int m, int K, int s, const double* D, double sigma, uint64_t seed,
+                 void* Y, int64_t ldy, int32_t* sup_out, cudaStream_t st);
+
 }  // namespace sdb

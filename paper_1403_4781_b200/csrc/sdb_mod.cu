@@ -366,7 +366,8 @@ __global__ void k_ls_resid(int P, const double* __restrict__ ysq, const double* 
     if (p >= P) return;
     const double r2 = ysq[p] - wsq[p];
     resid[p] = sqrt(fmax(r2, 0.0));
-    need[p] = (r2 <= 1e-4 * ysq[p]) ? 1 : 0;
+    // wsq < 0: minimum-norm fallback solution (no Cholesky identity)
+    need[p] = (wsq[p] < 0.0 || r2 <= 1e-4 * ysq[p]) ? 1 : 0;
 }
 
 __global__ void __launch_bounds__(256)
@@ -715,6 +716,7 @@ ModWs carve_mod_ws(void* base, int P, int64_t N, int m, int K, int cap) {
     w.wsq = (double*)take(sizeof(double) * P);
     w.ysqp = (double*)take(sizeof(double) * P);
     w.need = (int32_t*)take(sizeof(int32_t) * P);
+    w.mn = (double*)take(minnorm_ws_bytes(P, m, K));
     w.end = p;
     return w;
 }
@@ -743,16 +745,20 @@ int mod_update(const ModArgs<T>& a, cudaStream_t st) {
     k_chunk_offsets<<<gpk, SCW * 32, 0, st>>>(w.cf, P, K, w.chunk_hist, w.wpart, w.bucket_off, w.chunk_off);
     {
         const int smem = 8 * K * (int)sizeof(int64_t);
-        if (smem > 48 * 1024)
-            cudaFuncSetAttribute(k_place<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (smem > 48 * 1024) {
+            cudaError_t e = set_max_smem((const void*)k_place<T>, smem);
+            if (e != cudaSuccess) return (int)e;
+        }
         k_place<T><<<hb, 256, smem, st>>>(a.off, w.cf, P, K, cap, ch, a.idx, a.val, a.counts,
                                          w.chunk_off, w.bent);
     }
     rc = with_mpl(m, [&](auto c) {
         constexpr int MPL = decltype(c)::value;
         const int smem = 8 * (K + 32 * MPL) * (int)sizeof(double);
-        if (smem > 48 * 1024)
-            cudaFuncSetAttribute(k_normal_eq<T, MPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (smem > 48 * 1024) {
+            cudaError_t e = set_max_smem((const void*)k_normal_eq<T, MPL>, smem);
+            if (e != cudaSuccess) return (int)e;
+        }
         k_normal_eq<T, MPL><<<(unsigned)PK, 256, smem, st>>>(P, K, m, a.Y, a.ldy, w.bucket_off, cap, a.idx,
                                                              a.val, a.counts, w.bent, w.B, w.A);
         return (int)cudaGetLastError();
@@ -760,7 +766,13 @@ int mod_update(const ModArgs<T>& a, cudaStream_t st) {
     if (rc) return rc;
     // masked RHS rows of unused atoms are irrelevant: A is the identity there
     // and B holds zeros (their buckets are empty).
-    rc = chol_solve(P, K, m, w.A, w.B, a.usage, a.rank_rcond, w.depmask, w.deficient, w.wsq, w.chol, st);
+    // the Cholesky flags shards with a (near-)dependent pivot; those get the
+    // reference's minimum-norm lstsq solution (rank rule rcond) instead
+    rc = chol_solve(P, K, m, w.A, w.B, a.usage, std::max(a.rank_rcond, MN_FLAG_TOL), w.depmask, w.deficient,
+                    w.wsq, w.chol, st);
+    if (rc) return rc;
+    rc = minnorm_solve<T>(P, K, m, a.Y, a.ldy, cap, a.idx, a.val, a.counts, w.bucket_off, w.bent, a.usage,
+                          a.rank_rcond, w.A, w.B, w.deficient, w.wsq, w.mn, st);
     if (rc) return rc;
     // residual before normalisation: ||Y - Z^T X||^2 = ||Y||^2 - <Z, B> and
     // <Z, B> = ||L^-1 B||^2 (captured between the forward and back phases)

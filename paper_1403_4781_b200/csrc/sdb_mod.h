@@ -26,6 +26,7 @@ struct ModWs {
     double* wsq;
     double* ysqp;
     int32_t* need;
+    double* mn;      // minimum-norm fallback slots (sdb_minnorm.cu)
     unsigned char* end;
 };
 
@@ -71,6 +72,15 @@ struct ReplaceArgs {
 };
 
 int64_t mod_ws_bytes(int P, int64_t N, int m, int K, int cap);
+// pivot tolerance (relative to the largest used diagonal of X X^T) at which the
+// Cholesky flags a shard for the minimum-norm (Jacobi pseudo-inverse) solve
+constexpr double MN_FLAG_TOL = 1e-8;
+int64_t minnorm_ws_bytes(int P, int m, int K);
+template <typename T>
+int minnorm_solve(int P, int K, int m, const T* Y, int64_t ldy, int cap, const int32_t* idx, const T* val,
+                  const int32_t* counts, const int64_t* bucket_off, const int32_t* bent, const int32_t* usage,
+                  double rcond, double* A, double* B, int32_t* deficient, double* wsq, double* slots,
+                  cudaStream_t st);
 template <typename T> int mod_update(const ModArgs<T>& a, cudaStream_t st);
 int64_t replace_ws_bytes(int P, int64_t N, int m, int K);
 template <typename T> int replace_degenerate(const ReplaceArgs<T>& a, cudaStream_t st);

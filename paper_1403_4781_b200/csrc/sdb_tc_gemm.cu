@@ -660,21 +660,16 @@ static int corr_tc_launch(int64_t N, const float* Y, int64_t ldy, const int64_t*
         !make_map(&mDl, Dl, m_pad, rows, m_pad, TN) || (lda * 4) % 16 != 0 ||
         ((uintptr_t)alpha & 15) != 0 || !make_map_plain(&mA, alpha, K, N, lda))
         return (int)cudaErrorNotSupported;
-    static bool attr = false;
-    static int n_sm = 148;
-    if (!attr) {
-        cudaFuncSetAttribute(k_corr_tc2<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             Cfg<true, false>::SMEM);
-        cudaFuncSetAttribute(k_corr_tc2<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             Cfg<false, false>::SMEM);
-        cudaFuncSetAttribute(k_corr_tc2<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             Cfg<true, true>::SMEM);
-        cudaFuncSetAttribute(k_corr_tc2<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             Cfg<false, true>::SMEM);
+    int n_sm = 148;
+    {
+        cudaError_t e = set_max_smem((const void*)k_corr_tc2<true, false>, Cfg<true, false>::SMEM);
+        if (e == cudaSuccess) e = set_max_smem((const void*)k_corr_tc2<false, false>, Cfg<false, false>::SMEM);
+        if (e == cudaSuccess) e = set_max_smem((const void*)k_corr_tc2<true, true>, Cfg<true, true>::SMEM);
+        if (e == cudaSuccess) e = set_max_smem((const void*)k_corr_tc2<false, true>, Cfg<false, true>::SMEM);
+        if (e != cudaSuccess) return (int)e;
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-        attr = true;
     }
     int64_t* tile_start = (int64_t*)((unsigned char*)ws + 2 * (int64_t)P * K * m_pad * 4 + 256);
     tile_start = (int64_t*)(((uintptr_t)tile_start + 255) & ~(uintptr_t)255);

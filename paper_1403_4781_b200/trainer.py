@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import os
 import time
+from collections import OrderedDict
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -251,8 +252,29 @@ class _GraphedLoop:
         self.D.copy_(D0)
 
 
-_GRAPH_CACHE: dict = {}
+_GRAPH_CACHE: "OrderedDict" = OrderedDict()
 GRAPH_CACHE_MAX = 16
+# total bytes the cached graphs may pin (static signal copy + the captured
+# iteration's private pool: alpha, codes, MOD workspaces); LRU beyond that
+GRAPH_CACHE_BYTES = 8 << 30
+
+
+def _graph_bytes(S: E.ShardSet, D0: torch.Tensor, cap: int) -> int:
+    """Estimate of what one cached graph keeps resident."""
+    P, K, m = D0.shape
+    es = 8 if S.prec == "fp64" else 4
+    N = S.N
+    return (N * m * es * 2            # static Y copy + split/tf32 staging
+            + N * K * es              # alpha0 (the coding pass's largest buffer)
+            + N * cap * (4 + es) + N * 16
+            + P * (K * K + 4 * K * m) * 8)
+
+
+def _evict_one() -> None:
+    key, g = _GRAPH_CACHE.popitem(last=False)
+    dev = key[-3]
+    torch.cuda.synchronize(dev)   # nothing may still replay it
+    del g
 
 
 def _graphed(S: E.ShardSet, D0: torch.Tensor, cap: int, eps: float, use_tc: bool,
@@ -260,15 +282,25 @@ def _graphed(S: E.ShardSet, D0: torch.Tensor, cap: int, eps: float, use_tc: bool
     # tag: callers that run several trainings of equal shape concurrently (shard
     # groups on their own streams) get one graph -- and static buffers -- each
     key = (S.prec, tuple(S.Y.shape), tuple(S.sizes), tuple(D0.shape), cap, float(eps), bool(use_tc),
-           E.get_precision(None), torch.cuda.current_device(), E.FUSE_STEP1, tag)
+           E.get_precision(None), E.FUSE_STEP1, torch.cuda.current_device(), _graph_bytes(S, D0, cap), tag)
     g = _GRAPH_CACHE.get(key)
-    if g is None:
-        if len(_GRAPH_CACHE) >= GRAPH_CACHE_MAX:
-            # bounded: each entry holds a graph and its static buffers (a copy of
-            # the signals); the oldest shape goes, once nothing can still replay it
-            torch.cuda.synchronize()
-            _GRAPH_CACHE.pop(next(iter(_GRAPH_CACHE)))
-        g = _GRAPH_CACHE[key] = _GraphedLoop(S, D0, cap, eps, use_tc)
+    if g is not None:
+        _GRAPH_CACHE.move_to_end(key)   # LRU: the hot shapes stay
+        return g
+    need = key[-2]
+    while _GRAPH_CACHE and (len(_GRAPH_CACHE) >= GRAPH_CACHE_MAX or
+                            sum(k[-2] for k in _GRAPH_CACHE) + need > GRAPH_CACHE_BYTES):
+        _evict_one()
+    while True:
+        try:
+            g = _GraphedLoop(S, D0, cap, eps, use_tc)
+            break
+        except torch.cuda.OutOfMemoryError:
+            if not _GRAPH_CACHE:
+                raise
+            _evict_one()
+            torch.cuda.empty_cache()
+    _GRAPH_CACHE[key] = g
     return g
 
 
@@ -518,6 +550,12 @@ def _split_locals(src, N: int, m: int, L: int, K1: int, local_cap: int, local_ep
         if host_f64 is not None:
             ev.synchronize()  # validate the group's rows before any compute on them
             if int(bad[g].item()):
+                # later gathers (copy stream) and earlier groups (work streams)
+                # still use perm / bad / the head rows: drain them before the
+                # allocator may hand those blocks out again
+                copy.synchronize()
+                for w_s in work:
+                    w_s.synchronize()
                 raise InvalidInputError("batch contains non-finite entries")
         s.wait_event(ev)
         Ys.record_stream(s)

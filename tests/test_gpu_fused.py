@@ -53,9 +53,14 @@ def _code(Y, D, sizes, cap, eps, fused):
     D64 = torch.from_numpy(D).cuda()
     off, mx = E.shard_offsets(sizes)
     ysq = E.signal_sq(Yd)
-    codes = E.code(Yd, off, mx, E.working_dict(D64, "fp32"), E.gram(D64, "fp32"), cap, eps, "fp32",
-                   True, ysq=ysq, want_rnorm=not fused)
-    torch.cuda.synchronize()
+    old = E.OMP_TC
+    E.OMP_TC = False   # the two-kernel reference path (sdb_correlate + sdb_omp)
+    try:
+        codes = E.code(Yd, off, mx, E.working_dict(D64, "fp32"), E.gram(D64, "fp32"), cap, eps, "fp32",
+                       True, ysq=ysq, want_rnorm=not fused)
+        torch.cuda.synchronize()
+    finally:
+        E.OMP_TC = old
     return (codes.idx.cpu().numpy(), codes.val.cpu().numpy(), codes.counts.cpu().numpy(),
             codes.status.cpu().numpy())
 

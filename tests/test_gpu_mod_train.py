@@ -32,13 +32,7 @@ def test_mod_update_fp64(name):
     c = case(MOD, name)
     X = _X(c)
     D, dg = sdb.mod_update(c["Y"], X, c["Dprev"], precision="fp64")
-    if name == "rank_deficient":
-        # reference: minimum-norm lstsq; ours drops the dependent atom
-        assert np.all(np.isfinite(D))
-        used = [0, 1, 2]
-        np.testing.assert_allclose(np.linalg.norm(D[:, used], axis=0), 1.0, atol=1e-12)
-        assert dg.rank < D.shape[1]
-        return
+    # rank_deficient: the minimum-norm lstsq solution (sdb_minnorm.cu) like the reference
     np.testing.assert_allclose(D, c["D"], rtol=0, atol=1e-10)
     assert dg.residual_fro == pytest.approx(float(c["resid"]), rel=1e-10)
     assert dg.unused_atoms == list(c["unused"])
@@ -47,7 +41,7 @@ def test_mod_update_fp64(name):
         np.testing.assert_allclose(dg.scales, c["scales"], rtol=1e-10, atol=1e-12)
 
 
-@pytest.mark.parametrize("name", [n for n in golden_cases(MOD) if n != "rank_deficient"])
+@pytest.mark.parametrize("name", golden_cases(MOD))
 def test_replace_fp64(name):
     import paper_1403_4781_b200 as sdb
     c = case(MOD, name)
@@ -56,6 +50,43 @@ def test_replace_fp64(name):
     assert rep.replaced == list(c["replaced"])
     assert rep.unreplaced == list(c["unreplaced"])
     np.testing.assert_allclose(Dr, c["Drep"], rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("K,m,N,dups,prec", [(6, 8, 100, 1, "fp64"), (64, 16, 2000, 3, "fp64"),
+                                              (256, 64, 5000, 5, "fp32"), (300, 32, 4000, 4, "fp64"),
+                                              (512, 64, 6000, 2, "fp32")])
+def test_mod_min_norm_rank_deficient_vs_oracle(K, m, N, dups, prec):
+    """Used blocks with exactly dependent code rows (duplicated rows and a
+    row that is the sum of two others): the minimum-norm solution
+    (dictionary_update.py:100) on both the clustered (K <= 256) and the
+    chained (K > 256) Cholesky paths, vs the oracle's numpy lstsq."""
+    import paper_1403_4781_b200 as sdb
+    from oracle import oracle as O
+    rng = np.random.default_rng(K + dups)
+    Dp = rng.standard_normal((m, K))
+    Dp /= np.linalg.norm(Dp, axis=0)
+    Xd = np.zeros((K, N))
+    for i in range(N):
+        sup = rng.choice(K - 8, 3, replace=False)
+        Xd[sup, i] = rng.standard_normal(3)
+    for d in range(dups):
+        Xd[K - 8 + d] = Xd[d]                 # a duplicated code row
+    Xd[K - 1] = Xd[10] + Xd[11]               # a sum of two rows
+    Xd[K - 2] = 0.0                           # an unused atom
+    Y = rng.standard_normal((m, N))
+    if prec == "fp32":
+        Y = Y.astype(np.float32).astype(np.float64)
+        Xd = Xd.astype(np.float32).astype(np.float64)
+    from scipy import sparse
+    Xc = sparse.csc_array(Xd)
+    X = sdb.SparseCodeMatrix(K, Xc.indptr.astype(np.int64), Xc.indices.astype(np.int64), Xc.data)
+    D, dg = sdb.mod_update(Y, X, Dp, precision=prec)
+    Dr, resid, unused, rank, scales = O.mod_update(Y, (K, Xc.indptr.astype(np.int64),
+                                                       Xc.indices.astype(np.int64), Xc.data), Dp)
+    np.testing.assert_allclose(D, Dr, rtol=0, atol=1e-9)
+    assert dg.rank == rank
+    assert dg.unused_atoms == list(unused)
+    assert dg.residual_fro == pytest.approx(resid, rel=1e-9)
 
 
 def test_replace_twins():
