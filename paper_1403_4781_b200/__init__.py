@@ -5,8 +5,9 @@ Drop-in surface for the hot path (reference __init__.py:67-117): OMP coding,
 MOD update and atom replacement, standard / local / merge / split-merge
 training, the denoising pipeline and mse_db. All arithmetic runs in
 libsdb200.so (hand-written CUDA for sm_100a behind a C ABI); there is no CPU
-fallback. Out of scope: SDICT/SDATA storage, the CLI,
-PGM I/O, synthetic generators, the cost model and bench harness.
+fallback. The sparse-model generators (synthesis) are included, with an
+on-device variant. Out of scope: PGM I/O, the cost model
+and bench harness.
 """
 
 __version__ = "0.1.0"
@@ -49,6 +50,7 @@ from .denoising import (
     reconstruct_from_patches,
 )
 from .metrics import atom_recovery, mse_db, psnr
+from .synthesis import gen_dictionary, gen_signals, gen_signals_device
 
 __all__ = [
     "get_precision", "set_precision",
@@ -62,4 +64,5 @@ __all__ = [
     "DenoiseConfig", "GrayImage", "add_gaussian_noise", "denoise_image", "extract_patches",
     "overcomplete_dct", "reconstruct_from_patches",
     "atom_recovery", "mse_db", "psnr",
+    "gen_dictionary", "gen_signals", "gen_signals_device",
 ]

@@ -477,7 +477,10 @@ def replace_degenerate(S: ShardSet, codes: DeviceCodes, D64: torch.Tensor, usage
     wsb = _lib.load().sdb_replace_workspace_bytes(P, S.N, m, K)
     ws = empty((wsb,), torch.uint8)
     es = 8 if S.prec == "fp64" else 4
-    timed_call("replace", S.N * (m * es + codes.cap * (4 + es) + 4), 0.0, "sdb_replace_degenerate", sdb_dtype(S.prec), P, S.N, m, K, codes.cap, ptr(S.off),
+    # algorithmic bytes of the part that always runs (normalised copy of D,
+    # |Dn^T Dn| twins, flags); the residual ranking pass over Y runs only for
+    # shards with replacement targets and is not counted
+    timed_call("replace", P * K * (2 * m + 2 * K) * 8 + P * K * 6, 0.0, "sdb_replace_degenerate", sdb_dtype(S.prec), P, S.N, m, K, codes.cap, ptr(S.off),
               ptr(S.Y), m, ptr(codes.idx), ptr(codes.val), ptr(codes.counts), ptr(usage),
               ptr(D64), ptr(flags), ptr(ntarget), ptr(ws), wsb, stream())
     return flags, ntarget

@@ -65,13 +65,15 @@ def test_mod_min_norm_rank_deficient_vs_oracle(K, m, N, dups, prec):
     rng = np.random.default_rng(K + dups)
     Dp = rng.standard_normal((m, K))
     Dp /= np.linalg.norm(Dp, axis=0)
+    res = 8 if K >= 32 else 3                 # reserved atoms for the dependent rows
     Xd = np.zeros((K, N))
     for i in range(N):
-        sup = rng.choice(K - 8, 3, replace=False)
-        Xd[sup, i] = rng.standard_normal(3)
+        sup = rng.choice(K - res, min(3, K - res), replace=False)
+        Xd[sup, i] = rng.standard_normal(sup.size)
     for d in range(dups):
-        Xd[K - 8 + d] = Xd[d]                 # a duplicated code row
-    Xd[K - 1] = Xd[10] + Xd[11]               # a sum of two rows
+        Xd[K - res + d] = Xd[d]               # a duplicated code row
+    if K >= 32:
+        Xd[K - 1] = Xd[10] + Xd[11]           # a sum of two rows
     Xd[K - 2] = 0.0                           # an unused atom
     Y = rng.standard_normal((m, N))
     if prec == "fp32":

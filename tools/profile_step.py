@@ -1,4 +1,4 @@
-"""One warm C2 split-and-merge training (fp32) for ncu launch lists / captures.
+"""One warm split-and-merge training (fp32) for ncu launch lists / captures.
 Usage: python tools/profile_step.py [config] [steps]"""
 import sys
 from pathlib import Path
@@ -10,11 +10,10 @@ import benchdata  # noqa: E402
 from paper_1403_4781_b200 import _engine as E  # noqa: E402
 from paper_1403_4781_b200.trainer import split_merge_device  # noqa: E402
 
-name = sys.argv[1] if len(sys.argv) > 1 else "c2"
+name = sys.argv[1] if len(sys.argv) > 1 else "c4"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 cfg = benchdata.CONFIGS[name]
-Yh = benchdata.make_training_data(name)
-Ydev, _ = E.ingest_signals(Yh.T, "fp32")
+Ydev = benchdata.make_training_data_device(name, 1234, "fp32")
 cap = cfg["s_max"] if cfg["eps"] is not None else cfg["s1"]
 eps = cfg["eps"] or 0.0
 for _ in range(steps):
