@@ -81,14 +81,18 @@ int sdb_correlate(int dtype, int64_t N, int64_t m, int64_t K, int64_t P, const i
  * rnorm <= eps or cap atoms. Fixed sparsity: cap = s, eps = 0. K <= 1024.
  * rnorm: optional output (NULL: residual norms not reported).
  * ysq: optional FP32 ||y_i||^2 from sdb_signal_sq (SDB_F32 only; NULL: formed
- * in the kernel). scratch: sdb_omp_scratch_bytes() bytes; its first 256 bytes carry the FP32
+ * in the kernel). gap: optional FP32 output (SDB_F32 only; NULL: not reported):
+ * the signal's smallest decision margin relative to ||y|| (best minus runner-up
+ * |corr| above the rounding floor; | ||r|| - eps | at the explicit stopping
+ * tests) -- the near-tie log sdb_certify re-decides in FP64.
+ * scratch: sdb_omp_scratch_bytes() bytes; its first 256 bytes carry the FP32
  * kernel's work counter (signals are claimed in 32-signal chunks), the rest any per-warp
  * global scratch the generic kernel needs (NULL: static signal ranges). */
 int64_t sdb_omp_scratch_bytes(int dtype, int64_t N, int64_t m, int64_t cap);
 int sdb_omp(int dtype, int64_t N, int64_t m, int64_t K, int64_t P, const int64_t *shard_off,
             const void *alpha0, int64_t lda, const void *Y, int64_t ldy, const void *D,
             const void *G, int64_t cap, double eps, double guard, int32_t *idx, void *val,
-            int32_t *counts, int8_t *status, void *rnorm, const float *ysq, void *scratch,
+            int32_t *counts, int8_t *status, void *rnorm, const float *ysq, float *gap, void *scratch,
             int64_t scratch_bytes, void *stream);
 /* Fused tensor-core Batch-OMP, FP32 (replaces sdb_correlate + sdb_omp for
  * _kernels.omp_batch_range, _kernels.py:161-173, when m <= 64, K <= 512 and
@@ -99,8 +103,25 @@ int sdb_omp(int dtype, int64_t N, int64_t m, int64_t K, int64_t P, const int64_t
  * window of the maximum (lowest index on ties); stall, singular-guard and eps
  * rules of omp_single (_kernels.py:61-154). No alpha0 matrix is formed.
  * D: P x K x m fp32 atom-major; G: P x K x K fp32. rnorm, gap optional
- * (gap[i] = smallest relative margin of the chosen atom over the runner-up
- * across the steps: the near-tie log). ws: sdb_omp_tc_workspace_bytes(). */
+ * (gap[i] = the signal's smallest decision margin relative to ||y||: best
+ * minus runner-up |corr| over the non-negligible steps and, in eps mode,
+ * | ||r|| - eps | at every stopping test -- the near-tie log that
+ * sdb_certify re-decides in FP64). ws: sdb_omp_tc_workspace_bytes(). */
+/* FP64 certification of FP32 codes (the certified FP32 mode; replaces the
+ * FP32 kernels' rounding by the reference's FP64 results, _kernels.py:38-173):
+ * signals with status != 0 or a decision margin gap[i] < tau (gap may be NULL:
+ * status only) are re-coded from scratch by the exact FP64 kernel (bitwise the
+ * reference's omp_single for the same D, G, y) and listed in list[0..*nlist);
+ * every other signal keeps its support and gets FP64 least-squares
+ * coefficients on it. Y: the FP32 signal rows the FP32 kernels coded; Y64
+ * (optional): the authoritative FP64 rows (used instead of Y when the FP32
+ * rows are a rounding of them); D: P x K x m f64; G: the FP64
+ * Gram (sdb_gram). idx/counts/status in-out; val (N x cap f64), rnorm (f64,
+ * optional) out. list: N int32; nlist: 1 int32 (device). */
+int sdb_certify(int64_t N, int64_t m, int64_t K, int64_t P, const int64_t *shard_off, const float *Y,
+                const double *Y64, int64_t ldy, const double *D, const double *G, int64_t cap, double eps, double tau,
+                int32_t *idx, double *val, int32_t *counts, int8_t *status, double *rnorm, const float *gap,
+                int32_t *list, int32_t *nlist, void *stream);
 int sdb_omp_tc_supported(int64_t m, int64_t K, int64_t cap);
 int64_t sdb_omp_tc_workspace_bytes(int64_t P, int64_t m, int64_t K);
 int sdb_omp_tc(int64_t N, int64_t m, int64_t K, int64_t P, const int64_t *shard_off, const float *Y,
@@ -129,7 +150,7 @@ int sdb_code_step1(int64_t N, int64_t m, int64_t K, int64_t P, const int64_t *sh
 int sdb_omp_deferred(int64_t N, int64_t m, int64_t K, int64_t P, const int64_t *shard_off,
                      const float *alpha0, int64_t lda, const float *Y, int64_t ldy, const float *D,
                      const float *G, const float *ysq, int64_t cap, double eps, double guard, int32_t *idx,
-                     float *val, int32_t *counts, int8_t *status, void *ws, int64_t ws_bytes, void *stream);
+                     float *val, int32_t *counts, int8_t *status, float *gap, void *ws, int64_t ws_bytes, void *stream);
 /* ||y_i||^2 per signal (FP32, N floats) with the exact arithmetic of the
  * FP32 OMP kernel: passing it as sdb_omp's ysq gives bitwise the same codes
  * and lets the kernel skip loading y except near the eps threshold. */

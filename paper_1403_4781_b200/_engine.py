@@ -65,6 +65,13 @@ KSTAT: dict = {}
 # error-bounded FP32 coding through sdb_code_step1 + sdb_omp_deferred (False:
 # sdb_correlate + sdb_omp; the codes are bitwise the same, tests compare both)
 FUSE_STEP1 = True
+# certified FP32 coding (sdb_certify): the FP32/TF32 kernels decide, signals
+# whose decision margin is within CERT_TAU * ||y|| (or whose FP32 status is not
+# OK) are re-coded by the exact FP64 kernel, every other signal's coefficients
+# are refitted in FP64 on its support -> the reference's FP64 codes; MOD and
+# replacement then run in FP64 on an FP64 copy of the signals
+CERTIFY = os.environ.get("SDB_CERTIFY", "1") != "0"
+CERT_TAU = float(os.environ.get("SDB_CERT_TAU", "4e-6"))
 # FP32 coding with m <= 64, K <= 512, cap <= 8 through the fused tensor-core
 # Batch-OMP (sdb_omp_tc: per-step D^T r on tcgen05, no alpha0 in HBM); False:
 # sdb_correlate + sdb_omp (k_omp_fast)
@@ -177,8 +184,10 @@ class DeviceCodes:
     val: torch.Tensor      # (N, cap) working precision
     counts: torch.Tensor   # (N,) int32
     status: torch.Tensor   # (N,) int8
-    rnorm: torch.Tensor    # (N,) working precision
-    gap: torch.Tensor | None = None   # (N,) fp32 near-tie margin (sdb_omp_tc, when requested)
+    rnorm: torch.Tensor    # (N,) working precision (fp64 when certified)
+    gap: torch.Tensor | None = None   # (N,) fp32 decision margin / ||y|| (sdb_omp_tc, when requested)
+    vprec: str | None = None          # precision of val / rnorm when not the working one
+    nfrag: torch.Tensor | None = None  # (1,) int32: signals re-decided in FP64 (certified codes)
 
     @property
     def N(self) -> int:
@@ -250,13 +259,16 @@ def code(Ydev: torch.Tensor, off: torch.Tensor, max_rows: int, DT: torch.Tensor,
     if N == 0:
         return out
     es = 8 if prec == "fp64" else 4
+    # the fused step-1 epilogue reports no decision margins: certified coding
+    # (want_gap) takes the two-kernel path
     fused1 = (FUSE_STEP1 and prec == "fp32" and use_tc and ysq is not None and eps > 0.0 and not want_rnorm
-              and K <= 256 and m <= 256 and cap <= 32 and K % 4 == 0 and m % 4 == 0 and N <= DYN_MAX_N)
+              and not want_gap and K <= 256 and m <= 256 and cap <= 32 and K % 4 == 0 and m % 4 == 0
+              and N <= DYN_MAX_N)
+    if want_gap and prec == "fp32" and out.gap is None:
+        out.gap = empty((N,), torch.float32)
     if not fused1 and N <= DYN_MAX_N and omp_tc_applies(m, K, cap, prec, use_tc):
         wb = _lib.load().sdb_omp_tc_workspace_bytes(P, m, K)
         ws = empty((wb,), torch.uint8)
-        if want_gap:
-            out.gap = empty((N,), torch.float32)
         # algorithmic HBM bytes per signal: y row in, code row + count + status out
         timed_call("omp_tc", N * (4 * m + cap * 8 + 5 + (4 if want_rnorm else 0)), 2.0 * N * m * K * cap,
                    "sdb_omp_tc", N, m, K, P, ptr(off), ptr(Ydev), Ydev.stride(0), ptr(DT), ptr(G), cap,
@@ -276,7 +288,7 @@ def code(Ydev: torch.Tensor, off: torch.Tensor, max_rows: int, DT: torch.Tensor,
                    stream())
         timed_call("omp_deferred", 0.0, 0.0, "sdb_omp_deferred", N, m, K, P, ptr(off), ptr(alpha), K,
                    ptr(Ydev), m, ptr(DT), ptr(G), ptr(ysq), cap, float(eps), GUARD[prec], ptr(out.idx),
-                   ptr(out.val), ptr(out.counts), ptr(out.status), ptr(ws), int(wb), stream())
+                   ptr(out.val), ptr(out.counts), ptr(out.status), None, ptr(ws), int(wb), stream())
         if KTIMER is not None and not torch.cuda.is_current_stream_capturing():
             if "deferred" not in KSTAT:
                 KSTAT["deferred"] = zeros((1,), torch.int64)
@@ -298,9 +310,61 @@ def code(Ydev: torch.Tensor, off: torch.Tensor, max_rows: int, DT: torch.Tensor,
                "sdb_omp", dt, N, m, K, P, ptr(off), ptr(alpha), K, ptr(Ydev), m, ptr(DT), ptr(G),
                cap, float(eps), GUARD[prec], ptr(out.idx), ptr(out.val), ptr(out.counts),
                ptr(out.status), ptr(out.rnorm) if want_rnorm else None,
-               ptr(ysq) if (ysq is not None and prec == "fp32") else None, ptr(scratch), int(sb),
-               stream())
+               ptr(ysq) if (ysq is not None and prec == "fp32") else None,
+               ptr(out.gap) if (want_gap and prec == "fp32") else None, ptr(scratch), int(sb), stream())
     return out
+
+
+def certify(Y32: torch.Tensor, off: torch.Tensor, D64: torch.Tensor, G64: torch.Tensor, codes: DeviceCodes,
+            eps: float, want_rnorm: bool = False, Y64: torch.Tensor | None = None) -> DeviceCodes:
+    """FP64 certification of FP32 codes (sdb_certify): returns codes with FP64
+    values (vprec "fp64"); idx / counts / status are updated in place for the
+    re-decided signals. Y64: authoritative FP64 rows when Y32 rounds them.
+    Shapes outside the certification kernels (cap > 32) return the FP32
+    codes unchanged."""
+    N, m = Y32.shape
+    if codes.cap > 32 or m > 256 or D64.shape[1] > 1024:
+        return codes
+    P, K, _ = D64.shape
+    cap = codes.cap
+    val = empty((N, cap), torch.float64)
+    rn = empty((N,), torch.float64) if want_rnorm else codes.rnorm
+    lst = empty((max(N, 1),), torch.int32)
+    nl = empty((1,), torch.int32)
+    if N:
+        assert Y64 is None or (Y64.shape == Y32.shape and Y64.stride(0) == Y32.stride(0))
+        timed_call("certify", N * ((8 if Y64 is not None else 4) * m + cap * 12 + 9), 0.0, "sdb_certify", N, m, K,
+                   P, ptr(off), ptr(Y32), ptr(Y64), Y32.stride(0), ptr(D64), ptr(G64), cap, float(eps), CERT_TAU, ptr(codes.idx), ptr(val),
+                   ptr(codes.counts), ptr(codes.status), ptr(rn) if want_rnorm else None, ptr(codes.gap),
+                   ptr(lst), ptr(nl), stream())
+        if KTIMER is not None and not torch.cuda.is_current_stream_capturing():
+            if "fragile" not in KSTAT:
+                KSTAT["fragile"] = zeros((1,), torch.int64)
+                KSTAT["certified"] = 0
+            KSTAT["fragile"].add_(nl)
+            KSTAT["certified"] += N
+    else:
+        nl.zero_()
+    return DeviceCodes(K, cap, codes.idx, val, codes.counts, codes.status, rn, gap=codes.gap,
+                       vprec="fp64", nfrag=nl)
+
+
+def certifies(prec: str) -> bool:
+    return prec == "fp32" and CERTIFY
+
+
+def code_shards(S: "ShardSet", D64: torch.Tensor, cap: int, eps: float, use_tc: bool = True,
+                want_rnorm: bool = False) -> DeviceCodes:
+    """The training loop's coding pass over every shard: FP32 kernels plus the
+    FP64 certification in certified mode, the plain kernels otherwise."""
+    prec = S.prec
+    codes = code(S.Y, S.off, S.max_rows, working_dict(D64, prec), gram(D64, prec), cap, eps, prec, use_tc,
+                 ysq=S.signal_sq(), want_rnorm=want_rnorm and not certifies(prec),
+                 want_gap=certifies(prec))
+    if not certifies(prec):
+        return codes
+    return certify(S.Y, S.off, D64, gram(D64, "fp64"), codes, eps, want_rnorm,
+                   Y64=S._exact.Y if (S._exact is not None and S._exact_auth) else None)
 
 
 def signal_sq(Ydev: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
@@ -324,15 +388,36 @@ def code_single_dict(Ydev, D64, cap, eps, prec, use_tc=True, want_rnorm=True) ->
     ysq = None
     if not want_rnorm and prec == "fp32" and eps > 0.0:
         ysq = signal_sq(Ydev)
+    cert = certifies(prec)
+    if cert:
+        G64 = gram(D64, "fp64")
     if N <= rows:
         off, mx = shard_offsets([N])
-        return code(Ydev, off, mx, DT, G, cap, eps, prec, use_tc, ysq=ysq, want_rnorm=want_rnorm)
+        c = code(Ydev, off, mx, DT, G, cap, eps, prec, use_tc, ysq=ysq, want_rnorm=want_rnorm and not cert,
+                 want_gap=cert)
+        return certify(Ydev, off, D64, G64, c, eps, want_rnorm) if cert else c
     tdt = torch_dtype(prec)
     res = DeviceCodes(K, cap, empty((N, cap), torch.int32), empty((N, cap), tdt),
                       empty((N,), torch.int32), empty((N,), torch.int8), empty((N,), tdt))
+    if cert:
+        res.val = empty((N, cap), torch.float64)
+        res.rnorm = empty((N,), torch.float64)
+        res.vprec = "fp64"
+        res.nfrag = zeros((1,), torch.int32)
     for lo in range(0, N, rows):
         hi = min(N, lo + rows)
         off, mx = shard_offsets([hi - lo])
+        if cert:
+            view = DeviceCodes(K, cap, res.idx[lo:hi], empty((hi - lo, cap), tdt), res.counts[lo:hi],
+                               res.status[lo:hi], empty((hi - lo,), tdt))
+            c = code(Ydev[lo:hi], off, mx, DT, G, cap, eps, prec, use_tc, out=view,
+                     ysq=None if ysq is None else ysq[lo:hi], want_rnorm=False, want_gap=True)
+            cc = certify(Ydev[lo:hi], off, D64, G64, c, eps, want_rnorm)
+            res.val[lo:hi].copy_(cc.val)
+            if want_rnorm:
+                res.rnorm[lo:hi].copy_(cc.rnorm)
+            res.nfrag.add_(cc.nfrag)
+            continue
         view = DeviceCodes(K, cap, res.idx[lo:hi], res.val[lo:hi], res.counts[lo:hi],
                            res.status[lo:hi], res.rnorm[lo:hi])
         code(Ydev[lo:hi], off, mx, DT, G, cap, eps, prec, use_tc, out=view,
@@ -342,6 +427,7 @@ def code_single_dict(Ydev, D64, cap, eps, prec, use_tc=True, want_rnorm=True) ->
 
 def csc(codes: DeviceCodes, prec: str):
     """Device CSC packing -> (indptr, indices int64, data f64) device tensors."""
+    prec = codes.vprec or prec
     N = codes.N
     indptr = empty((N + 1,), torch.int64)
     ws = empty((max(_lib.load().sdb_csc_workspace_bytes(N), 8),), torch.uint8)
@@ -427,6 +513,30 @@ class ShardSet:
         _lib.call("sdb_shard_energy", sdb_dtype(self.prec), self.P, self.N, self.m,
                   ptr(self.off), ptr(self.Y), self.m, ptr(tmp), ptr(out), stream())
 
+    _exact: "ShardSet | None" = None
+    _exact_auth: bool = False   # the FP64 copy is the authoritative data (Y rounds it)
+
+    def exact(self) -> "ShardSet":
+        """FP64 copy of the signals (same shards) for the certified mode's
+        FP64 MOD / replacement; created once, refreshed with the signals."""
+        if self.prec == "fp64":
+            return self
+        if self._exact is None:
+            self._exact = ShardSet(self.Y.double(), self.off, self.sizes, "fp64")
+        return self._exact
+
+    @classmethod
+    def with_exact(cls, Y64: torch.Tensor, off: torch.Tensor, sizes: list, prec: str) -> "ShardSet":
+        """Shards whose data are FP64 (e.g. the merge phase's scaled atoms):
+        the working-precision copy for the coding kernels plus the FP64
+        original for certification, MOD and replacement."""
+        if prec == "fp64":
+            return cls(Y64, off, sizes, "fp64")
+        S = cls(Y64.to(torch_dtype(prec)), off, sizes, prec)
+        S._exact = cls(Y64, off, sizes, "fp64")
+        S._exact_auth = True
+        return S
+
     def refresh(self):
         """Recompute the cached per-signal / per-shard quantities in place
         after Y was overwritten (their storage is kept: captured graphs
@@ -435,6 +545,10 @@ class ShardSet:
             signal_sq(self.Y, out=self._sig_sq)
         if self._ysq is not None:
             self._energy_into(self._ysq)
+        if self._exact is not None:
+            if not self._exact_auth:
+                self._exact.Y.copy_(self.Y)
+            self._exact.refresh()
 
     @classmethod
     def single(cls, Y: torch.Tensor, prec: str) -> "ShardSet":
@@ -453,7 +567,17 @@ class ModResult:
     deficient: torch.Tensor  # (P,) int32
 
 
+def _for_codes(S: "ShardSet", codes: DeviceCodes) -> "ShardSet":
+    """The shard set whose precision matches the codes' values (certified FP32
+    codes carry FP64 values: MOD / replacement / residuals run in FP64 on the
+    FP64 copy of the signals)."""
+    if codes.vprec == "fp64" and S.prec != "fp64":
+        return S.exact()
+    return S
+
+
 def mod_update(S: ShardSet, codes: DeviceCodes, D64: torch.Tensor) -> ModResult:
+    S = _for_codes(S, codes)
     P, K, m = D64.shape
     dt = sdb_dtype(S.prec)
     r = ModResult(empty((P, K, m), torch.float64), empty((P, K), torch.float64),
@@ -471,6 +595,7 @@ def mod_update(S: ShardSet, codes: DeviceCodes, D64: torch.Tensor) -> ModResult:
 
 def replace_degenerate(S: ShardSet, codes: DeviceCodes, D64: torch.Tensor, usage: torch.Tensor):
     """In place on D64; returns (flags (P,K) int8, ntarget (P,) int32)."""
+    S = _for_codes(S, codes)
     P, K, m = D64.shape
     flags = empty((P, K), torch.int8)
     ntarget = empty((P,), torch.int32)
@@ -494,6 +619,7 @@ def code_usage(S: ShardSet, codes: DeviceCodes) -> torch.Tensor:
 
 
 def residual_sq(S: ShardSet, codes: DeviceCodes, D64: torch.Tensor, want_ysq=False):
+    S = _for_codes(S, codes)
     P, K, m = D64.shape
     rsq = empty((max(S.N, 1),), torch.float64)
     ysq = empty((max(S.N, 1),), torch.float64) if want_ysq else None
@@ -512,6 +638,7 @@ def shard_sum(S: ShardSet, v: torch.Tensor, do_sqrt: bool) -> torch.Tensor:
 
 def code_energy(S: ShardSet, codes: DeviceCodes) -> torch.Tensor:
     """||X_p||_F per shard (trainer.py:250)."""
+    S = _for_codes(S, codes)
     e = empty((max(S.N, 1),), torch.float64)
     if S.N:
         _lib.call("sdb_code_energy", sdb_dtype(S.prec), S.N, codes.cap, ptr(codes.val),

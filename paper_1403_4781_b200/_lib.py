@@ -34,7 +34,7 @@ SIGNATURES = {
                               c_vp, c_i64, c_int, c_vp, c_i64, c_vp]),
     "sdb_omp_scratch_bytes": (c_i64, [c_int, c_i64, c_i64, c_i64]),
     "sdb_omp": (c_int, [c_int, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp,
-                        c_vp, c_i64, c_dbl, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                        c_vp, c_i64, c_dbl, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                         c_i64, c_vp]),
     "sdb_signal_sq": (c_int, [c_i64, c_i64, c_vp, c_i64, c_vp, c_vp]),
     "sdb_code_step1_workspace_bytes": (c_i64, [c_i64, c_i64, c_i64]),
@@ -42,8 +42,10 @@ SIGNATURES = {
                                c_i64, c_dbl, c_dbl, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp,
                                c_i64, c_vp]),
     "sdb_omp_deferred": (c_int, [c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp,
-                                 c_vp, c_vp, c_i64, c_dbl, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                 c_vp, c_vp, c_i64, c_dbl, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                  c_i64, c_vp]),
+    "sdb_certify": (c_int, [c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_dbl, c_dbl,
+                            c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "sdb_omp_tc_supported": (c_int, [c_i64, c_i64, c_i64]),
     "sdb_omp_tc_workspace_bytes": (c_i64, [c_i64, c_i64, c_i64]),
     "sdb_omp_tc": (c_int, [c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_dbl, c_dbl,
@@ -99,7 +101,7 @@ class NativeError(RuntimeError):
 
 _lib = None
 # must equal sdb_abi_version() in csrc/sdb_capi.cu (bumped whenever exports change)
-ABI_VERSION = 6
+ABI_VERSION = 8
 
 
 def load():

@@ -55,7 +55,7 @@ __global__ void k_cast(int64_t n, const double* __restrict__ src, T* __restrict_
 
 extern "C" {
 
-int sdb_abi_version(void) { return 6; }
+int sdb_abi_version(void) { return 8; }
 const char* sdb_last_error(void) { return g_err.c_str(); }
 
 int sdb_device_cc(void) {
@@ -144,7 +144,7 @@ int64_t sdb_omp_scratch_bytes(int dtype, int64_t N, int64_t m, int64_t cap) {
 int sdb_omp(int dtype, int64_t N, int64_t m, int64_t K, int64_t P, const int64_t* shard_off,
             const void* alpha0, int64_t lda, const void* Y, int64_t ldy, const void* D,
             const void* G, int64_t cap, double eps, double guard, int32_t* idx, void* val,
-            int32_t* counts, int8_t* status, void* rnorm, const float* ysq, void* scratch,
+            int32_t* counts, int8_t* status, void* rnorm, const float* ysq, float* gap, void* scratch,
             int64_t scratch_bytes, void* stream) {
     if (!dtype_ok(dtype) || N < 0 || m < 1 || K < 1 || P < 1 || cap < 1 || ldy < m || lda < K)
         return fail(SDB_EINVAL, "sdb_omp: bad args");
@@ -185,12 +185,37 @@ int sdb_omp(int dtype, int64_t N, int64_t m, int64_t K, int64_t P, const int64_t
         a.G = (const float*)G; a.val = (float*)val; a.rnorm = (float*)rnorm;
         a.ysq = ysq;
         a.work = work;
+        a.gap = gap;
         rc = sdb::launch_omp<float>(a, S(stream));
     }
     return cuda_rc(rc, "sdb_omp");
 }
 
 // ---- fused tensor-core Batch-OMP (FP32): corr = D^T r per step on tcgen05
+int sdb_certify(int64_t N, int64_t m, int64_t K, int64_t P, const int64_t* shard_off, const float* Y,
+                const double* Y64, int64_t ldy, const double* D, const double* G, int64_t cap, double eps, double tau, int32_t* idx, double* val,
+                int32_t* counts, int8_t* status, double* rnorm, const float* gap, int32_t* list, int32_t* nlist,
+                void* stream) {
+    if (N < 0 || m < 1 || K < 1 || P < 1 || cap < 1 || ldy < m || !(tau >= 0.0) || list == nullptr ||
+        nlist == nullptr)
+        return fail(SDB_EINVAL, "sdb_certify: bad args");
+    if (K > 1024 || m > 256 || cap > 32) return fail(SDB_ENOTSUP, "sdb_certify: needs K <= 1024, m <= 256, cap <= 32");
+    if (N == 0) return SDB_OK;
+    cudaMemsetAsync(nlist, 0, sizeof(int32_t), S(stream));
+    int rc = sdb::certify_refit(N, (int)m, (int)K, (int)cap, (int)P, shard_off, Y, Y64, ldy, D, G, idx, counts, status,
+                                gap, (float)tau, val, rnorm, list, nlist, S(stream));
+    if (rc) return cuda_rc(rc, "sdb_certify (refit)");
+    sdb::OmpArgs<double> a{};
+    a.N = N; a.m = (int)m; a.K = (int)K; a.cap = (int)cap; a.P = (int)P;
+    a.shard_off = shard_off; a.lda = K; a.ldy = ldy;
+    a.idx = idx; a.counts = counts; a.status = status;
+    a.eps = eps; a.guard = 1e-12;              // the reference's guard (_kernels.py:18)
+    a.alpha0 = nullptr; a.Y = Y64; a.Yf = Y64 ? nullptr : Y; a.D = D; a.G = G; a.val = val; a.rnorm = rnorm;
+    a.list = list; a.nlist = nlist;
+    a.warp_bytes = sdb::omp_warp_bytes_f64((int)cap, (int)m);
+    return cuda_rc(sdb::launch_omp<double>(a, S(stream)), "sdb_certify (exact)");
+}
+
 int64_t sdb_omp_tc_workspace_bytes(int64_t P, int64_t m, int64_t K) {
     if (P < 1 || m < 1 || K < 1) return fail(SDB_EINVAL, "sdb_omp_tc_workspace_bytes: bad args");
     return sdb::omp_tc_ws_bytes(P, m, K);
@@ -247,7 +272,8 @@ int sdb_code_step1(int64_t N, int64_t m, int64_t K, int64_t P, const int64_t* sh
 int sdb_omp_deferred(int64_t N, int64_t m, int64_t K, int64_t P, const int64_t* shard_off,
                      const float* alpha0, int64_t lda, const float* Y, int64_t ldy, const float* D,
                      const float* G, const float* ysq, int64_t cap, double eps, double guard, int32_t* idx,
-                     float* val, int32_t* counts, int8_t* status, void* ws, int64_t ws_bytes, void* stream) {
+                     float* val, int32_t* counts, int8_t* status, float* gap, void* ws, int64_t ws_bytes,
+                     void* stream) {
     if (N < 0 || m < 1 || K < 1 || P < 1 || cap < 1 || ldy < m || lda < K)
         return fail(SDB_EINVAL, "sdb_omp_deferred: bad args");
     if (K > 1024 || m > 256 || cap > 32 || ysq == nullptr)
@@ -263,6 +289,7 @@ int sdb_omp_deferred(int64_t N, int64_t m, int64_t K, int64_t P, const int64_t* 
     a.eps = (float)eps; a.guard = (float)guard;
     a.alpha0 = alpha0; a.Y = Y; a.D = D; a.G = G; a.val = val; a.rnorm = nullptr; a.ysq = ysq;
     a.deferred = 1;
+    a.gap = gap;
     a.work = (int*)((unsigned char*)ws + step1_corr_bytes(P, m, K)) + 1;   // zeroed by sdb_code_step1
     return cuda_rc(sdb::launch_omp<float>(a, S(stream)), "sdb_omp_deferred");
 }

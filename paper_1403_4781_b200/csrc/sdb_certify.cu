@@ -1,0 +1,233 @@
+// FP64 certification of FP32 OMP codes (the "certified FP32" coding mode).
+//
+// The FP32 / TF32 kernels decide every greedy step with FP32 arithmetic; a
+// decision can differ from the reference's FP64 one only when its margin is
+// within the FP32 error (~1e-7 ||y||), and the FP32 coefficients carry ~1e-7
+// relative error that the MOD step would propagate into the dictionary. This
+// pass makes the codes the reference's FP64 codes:
+//
+//  * signals whose smallest decision margin (gap[i], reported by the FP32
+//    kernel: best vs runner-up |corr| and | ||r|| - eps | relative to ||y||)
+//    is below `tau`, or whose FP32 status is not OK, are appended to a list
+//    and re-coded from scratch by the exact FP64 kernel (k_omp<double>,
+//    bitwise the reference's omp_single given the same D, G, y);
+//  * every other signal keeps its FP32 support (decided with a margin far
+//    above the FP32 error, hence the reference's support) and gets its
+//    coefficients refitted in FP64: x = (D_S^T D_S)^-1 D_S^T y with G_SS from
+//    the FP64 Gram and D_S^T y from the FP64 dictionary -- the reference's
+//    least-squares coefficients on that support (_kernels.py:129-139) to
+//    rounding.
+//
+// Layout: LPS lanes per signal (8 for m <= 64 and cap <= 8: four signals per
+// warp; 32 otherwise), lane l holds y[l + LPS v]; the dot products are
+// reduced within the lane group; the small SPD solve is a lane-parallel
+// right-looking Cholesky in shared memory. Reads y (4m bytes), the support's
+// dictionary rows (8 m n bytes, L2-resident per shard) and n(n+1)/2 Gram
+// entries; writes the FP64 code row.
+#include <algorithm>
+#include <cstdint>
+
+#include "sdb_common.cuh"
+#include "sdb_internal.h"
+
+namespace sdb {
+namespace {
+
+struct CertArgs {
+    int64_t N;
+    int m, K, cap, P;
+    const int64_t* off;
+    const float* Y;
+    const double* Y64;  // optional: authoritative FP64 rows (same ldy), read instead of Y
+    int64_t ldy;
+    const double* D;    // P x K x m
+    const double* G;    // P x K x K
+    const int32_t* idx;
+    const int32_t* counts;
+    const int8_t* status;
+    const float* gap;   // optional
+    float tau;
+    double* val;        // N x cap (out)
+    double* rnorm;      // optional (out)
+    int32_t* list;      // fragile signals (out)
+    int32_t* nlist;     // count (zeroed by the caller's stream before)
+};
+
+template <int LPS>
+__device__ __forceinline__ double gsum(double v) {
+#pragma unroll
+    for (int o = LPS / 2; o > 0; o >>= 1) v += __shfl_xor_sync(SDB_FULL, v, o, LPS);
+    return v;
+}
+
+// One lane group of LPS lanes per signal; LPS is also the largest support
+// (lane r owns row r of the n x n normal equations). Everything between the
+// loads is register-resident: the support Gram row, a lane-parallel right-
+// looking Cholesky (columns broadcast by group shuffles), forward substitution
+// by broadcasts, back substitution through the factor rows staged in shared
+// memory.
+template <int LPS, int VPL, int WPB>
+__global__ void __launch_bounds__(WPB * 32)
+k_certify(CertArgs a) {
+    constexpr int GPW = 32 / LPS;                      // signals per warp
+    __shared__ double sL[WPB * GPW][LPS][LPS + 1];
+    __shared__ int64_t s_off[257];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int l = lane & (LPS - 1), g = lane / LPS;
+    const int gbase = g * LPS;                         // first lane of the group
+    double (*Ls)[LPS + 1] = sL[wib * GPW + g];
+    const int m = a.m, K = a.K, cap = a.cap, P = a.P;
+    const bool off_smem = P <= 256;
+    if (off_smem)
+        for (int q = threadIdx.x; q <= P; q += blockDim.x) s_off[q] = a.off[q];
+    __syncthreads();
+    const int64_t nsig_per_iter = (int64_t)gridDim.x * WPB * GPW;
+    // every lane of the warp runs the same number of iterations (group
+    // shuffles need the whole warp converged)
+    const int64_t iters = (a.N + nsig_per_iter - 1) / nsig_per_iter;
+    for (int64_t it = 0; it < iters; ++it) {
+        const int64_t i = it * nsig_per_iter + ((int64_t)blockIdx.x * WPB + wib) * GPW + g;
+        const bool valid = i < a.N;
+        int n = valid ? a.counts[i] : 0;
+        const bool frag = valid && (a.status[i] != 0 || (a.gap != nullptr && !(a.gap[i] >= a.tau)));
+        if (frag) {
+            if (l == 0) {
+                const int pos = atomicAdd(a.nlist, 1);
+                a.list[pos] = (int32_t)i;
+            }
+            n = 0;
+        }
+        const bool work = valid && !frag;
+        int p = 0;
+        if (work) {
+            int lo = 0, hi = P - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                const int64_t o = off_smem ? s_off[mid] : __ldg(a.off + mid);
+                if (o <= i) lo = mid; else hi = mid - 1;
+            }
+            p = lo;
+        }
+        const double* Dp = a.D + (int64_t)p * K * m;
+        const double* Gp = a.G + (int64_t)p * K * K;
+        const int32_t* ids_row = a.idx + (valid ? i : 0) * cap;
+        const int my_atom = (l < n) ? ids_row[l] : 0;       // lane r: atom r of the support
+        // ---- b = D_S^T y: lane l holds y[l + LPS v]; part[t] for every support atom
+        double part[LPS];
+#pragma unroll
+        for (int t = 0; t < LPS; ++t) part[t] = 0.0;
+        int at[LPS];
+#pragma unroll
+        for (int t = 0; t < LPS; ++t) at[t] = __shfl_sync(SDB_FULL, my_atom, gbase + t);
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+            const int c = l + LPS * v;
+            const double yv = (work && c < m) ? (a.Y64 ? __ldg(a.Y64 + i * a.ldy + c)
+                                                       : (double)__ldg(a.Y + i * a.ldy + c)) : 0.0;
+#pragma unroll
+            for (int t = 0; t < LPS; ++t)
+                if (t < n && c < m) part[t] = fma(__ldg(Dp + (int64_t)at[t] * m + c), yv, part[t]);
+        }
+        double b = 0.0;
+#pragma unroll
+        for (int t = 0; t < LPS; ++t) {
+            const double bt = gsum<LPS>(part[t]);
+            if (l == t) b = bt;
+        }
+        // ---- row r of G_SS (columns u <= r), independent loads
+        double gr[LPS];
+#pragma unroll
+        for (int u = 0; u < LPS; ++u)
+            gr[u] = (u <= l && l < n) ? __ldg(Gp + (int64_t)my_atom * K + at[u]) : 0.0;
+        // ---- Cholesky (right-looking; lane r keeps row r: gr[k] -> L[r][k])
+        const int nmax = __reduce_max_sync(SDB_FULL, n);
+#pragma unroll
+        for (int k = 0; k < LPS; ++k) {
+            if (k < nmax) {
+                const double dk = sqrt(__shfl_sync(SDB_FULL, gr[k], gbase + k));   // lane k's diagonal
+                const double ik = 1.0 / dk;
+                if (l > k) gr[k] *= ik;
+                if (l == k) gr[k] = dk;
+#pragma unroll
+                for (int c = k + 1; c < LPS; ++c) {
+                    const double lck = __shfl_sync(SDB_FULL, gr[k], gbase + c);   // L[c][k]
+                    if (l >= c && l < n) gr[c] = fma(-gr[k], lck, gr[c]);
+                }
+            }
+        }
+        // ---- forward L z = b (broadcasts), stage L rows for the back pass
+        double z = b;
+#pragma unroll
+        for (int k = 0; k < LPS; ++k) {
+            if (k < nmax) {
+                const double zk = __shfl_sync(SDB_FULL, z / gr[k], gbase + k);   // evaluated on lane k
+                if (l == k) z = zk;
+                if (l > k) z = fma(-gr[k], zk, z);
+            }
+        }
+        if (l < n) {
+#pragma unroll
+            for (int u = 0; u < LPS; ++u) Ls[l][u] = gr[u];
+        }
+        __syncwarp();
+        // ---- back L^T x = z: lane k solves x_k once every x_j, j > k, is in
+        double acc = z;
+        double x = 0.0;
+#pragma unroll
+        for (int k = LPS - 1; k >= 0; --k) {
+            if (k < nmax) {
+                const double xk = __shfl_sync(SDB_FULL, acc / Ls[k < n ? k : 0][k], gbase + k);
+                if (l == k) x = xk;
+                if (l < k && k < n) acc = fma(-Ls[k][l], xk, acc);
+            }
+        }
+        __syncwarp();
+        if (work && l < cap) a.val[i * cap + l] = (l < n) ? x : 0.0;   // cap <= LPS: lane t holds x_t
+        if (a.rnorm != nullptr) {
+            double rs = 0.0;
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+                const int c = l + LPS * v;
+                double rv = (work && c < m) ? (a.Y64 ? __ldg(a.Y64 + i * a.ldy + c)
+                                                     : (double)__ldg(a.Y + i * a.ldy + c)) : 0.0;
+#pragma unroll
+                for (int t = 0; t < LPS; ++t) {
+                    const double xt = __shfl_sync(SDB_FULL, x, gbase + t);
+                    if (t < n && c < m) rv = fma(-xt, __ldg(Dp + (int64_t)at[t] * m + c), rv);
+                }
+                rs = fma(rv, rv, rs);
+            }
+            rs = gsum<LPS>(rs);
+            if (work && l == 0) a.rnorm[i] = sqrt(rs);
+        }
+        __syncwarp();
+    }
+}
+
+template <int LPS, int VPL, int WPB>
+int launch_cert(const CertArgs& a, cudaStream_t st) {
+    constexpr int GPW = 32 / LPS;
+    const int64_t per = (int64_t)WPB * GPW;
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((a.N + per - 1) / per, 148 * 64 / WPB));
+    k_certify<LPS, VPL, WPB><<<(unsigned)blocks, WPB * 32, 0, st>>>(a);
+    return (int)cudaGetLastError();
+}
+
+}  // namespace
+
+int certify_refit(int64_t N, int m, int K, int cap, int P, const int64_t* off, const float* Y, const double* Y64,
+                  int64_t ldy, const double* D, const double* G, const int32_t* idx, const int32_t* counts,
+                  const int8_t* status, const float* gap, float tau, double* val, double* rnorm, int32_t* list,
+                  int32_t* nlist, cudaStream_t st) {
+    if (N <= 0) return 0;
+    CertArgs a{N, m, K, cap, P, off, Y, Y64, ldy, D, G, idx, counts, status, gap, tau, val, rnorm, list, nlist};
+    if (cap <= 8 && m <= 64) return launch_cert<8, 8, 8>(a, st);
+    if (cap <= 16 && m <= 64) return launch_cert<16, 4, 8>(a, st);
+    if (cap <= 16 && m <= 256) return launch_cert<16, 16, 4>(a, st);
+    if (cap <= 32 && m <= 64) return launch_cert<32, 2, 4>(a, st);
+    if (cap <= 32 && m <= 128) return launch_cert<32, 4, 4>(a, st);
+    if (cap <= 32 && m <= 256) return launch_cert<32, 8, 4>(a, st);
+    return (int)cudaErrorNotSupported;
+}
+
+}  // namespace sdb

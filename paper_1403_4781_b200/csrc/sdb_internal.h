@@ -31,9 +31,25 @@ struct OmpArgs {
     unsigned char* gscratch;   // optional per-warp scratch in global memory
     int64_t gscratch_warps;
     int64_t warp_bytes;
+    // exact kernel, certification mode: code only the signals list[0..*nlist)
+    // (global row indices, outputs at those rows), y read from the FP32 rows
+    // Yf, alpha0 == nullptr: c0 = D^T y formed in-kernel (reference order)
+    const int32_t* list;
+    const int32_t* nlist;
+    const float* Yf;
+    // FP32 fast kernel: optional per-signal smallest decision margin / ||y||
+    // (best vs runner-up |corr| above the rounding floor; | ||r|| - eps | at
+    // every stopping test) for the FP64 certification pass
+    float* gap;
 };
 
 int gram_f64(const double* D, int P, int64_t m, int64_t K, double* G, cudaStream_t st);
+// FP64 certification of FP32 codes (sdb_certify.cu)
+int certify_refit(int64_t N, int m, int K, int cap, int P, const int64_t* off, const float* Y, const double* Y64,
+                  int64_t ldy,
+                  const double* D, const double* G, const int32_t* idx, const int32_t* counts,
+                  const int8_t* status, const float* gap, float tau, double* val, double* rnorm, int32_t* list,
+                  int32_t* nlist, cudaStream_t st);
 int64_t perm_ws_bytes(int64_t n);
 int perm_from_targets(int64_t n, const uint32_t* js, int64_t* perm, void* ws, int64_t ws_bytes,
                       cudaStream_t st);

@@ -190,18 +190,39 @@ k_omp(OmpArgs<T> a) {
     const int m = a.m, K = a.K, cap = a.cap;
     const T eps = a.eps;
 
-    for (int64_t i = gw; i < a.N; i += nw) {
+    const int64_t n_items = a.list ? ((int64_t)*a.nlist < a.N ? (int64_t)*a.nlist : a.N) : a.N;
+    for (int64_t e = gw; e < n_items; e += nw) {
+        const int64_t i = a.list ? (int64_t)a.list[e] : e;
         const int p = shard_of(a.shard_off, a.P, i);
         const T* __restrict__ Gp = a.G + (int64_t)p * K * K;
         const T* __restrict__ Dp = a.D + (int64_t)p * K * m;
-        T c0[KPL];
-#pragma unroll
-        for (int k = 0; k < KPL; ++k) {
-            const int j = lane + 32 * k;
-            c0[k] = (j < K) ? a.alpha0[i * a.lda + j] : T(0);
+        if (a.Yf) {
+            for (int t = lane; t < m; t += 32) w.y[t] = (T)a.Yf[i * a.ldy + t];
+        } else {
+            for (int t = lane; t < m; t += 32) w.y[t] = a.Y[i * a.ldy + t];
         }
-        for (int t = lane; t < m; t += 32) w.y[t] = a.Y[i * a.ldy + t];
         __syncwarp();
+        T c0[KPL];
+        if (a.alpha0) {
+#pragma unroll
+            for (int k = 0; k < KPL; ++k) {
+                const int j = lane + 32 * k;
+                c0[k] = (j < K) ? a.alpha0[i * a.lda + j] : T(0);
+            }
+        } else {
+            // c0 = D^T y with the reference's loop order (sequential over the
+            // m rows, separately rounded products: _kernels.py:54-59)
+#pragma unroll
+            for (int k = 0; k < KPL; ++k) {
+                const int j = lane + 32 * k;
+                T acc = T(0);
+                if (j < K) {
+                    const T* __restrict__ dj = Dp + (int64_t)j * m;
+                    for (int t = 0; t < m; ++t) acc = R::mac(acc, __ldg(dj + t), w.y[t]);
+                }
+                c0[k] = acc;
+            }
+        }
         T ysq;
         if constexpr (R::kExact) {
             ysq = T(0);
@@ -578,6 +599,9 @@ k_omp_fast(OmpArgs<float> a) {
         float rnorm = 0.0f;  // formed only when reported or needed near the threshold
         float rsq = ysq;
         int n = 0, status = 0;
+        // smallest decision margin relative to ||y|| (certification; 1: none close)
+        const float ynorm = __fsqrt_rn(ysq);
+        float gmin = (a.gap && eps > 0.0f && ynorm > 0.0f) ? fminf(1.0f, fabsf(ynorm - eps) / ynorm) : 1.0f;
         // explicit ||y - D_S x|| (support columns read from L2, independent loads)
         auto resid_norm = [&](int nn) {
             __syncwarp();
@@ -629,6 +653,14 @@ k_omp_fast(OmpArgs<float> a) {
                     if (__float_as_uint(v[k]) == cbits) cand = j0 + k;
                 const int best = (int)__reduce_min_sync(SDB_FULL, (unsigned)cand);
                 if (best >= K) { status = 3; break; }  // no candidate (non-finite input)
+                if (a.gap && cmax >= 1e-6f * ynorm) {
+                    // runner-up |corr| (the best atom excluded)
+                    float l2 = 0.0f;
+#pragma unroll
+                    for (int k = 0; k < KPL; ++k) l2 = (j0 + k == best) ? l2 : fmaxf(l2, v[k]);
+                    const float second = __uint_as_float(__reduce_max_sync(SDB_FULL, __float_as_uint(l2)));
+                    gmin = fminf(gmin, (cmax - second) / ynorm);
+                }
 
                 // ---- every load of this step issued at once: G[b,b], G[S,b], c0[b]
                 float dsq = __ldg(Gp + (best * K + best));
@@ -683,6 +715,7 @@ k_omp_fast(OmpArgs<float> a) {
                 __syncwarp();
                 if (fabsf(rsq - eps2) <= 1e-4f * ysq) {
                     rnorm = resid_norm(n);
+                    if (a.gap) gmin = fminf(gmin, fabsf(rnorm - eps) / ynorm);
                     if (rnorm <= eps) break;
                 } else if (rsq <= eps2) {
                     break;
@@ -700,6 +733,7 @@ k_omp_fast(OmpArgs<float> a) {
             a.counts[i] = n;
             a.status[i] = (int8_t)status;
             if (a.rnorm) a.rnorm[i] = rnorm;
+            if (a.gap) a.gap[i] = gmin;
         }
         __syncwarp();
     }
@@ -791,7 +825,9 @@ int launch_omp(OmpArgs<T> a, cudaStream_t st) {
         blocks = std::max<int64_t>(1, std::min<int64_t>(a.gscratch_warps / WPB, (warps_needed + WPB - 1) / WPB));
     } else {
         smem = (int)(wb * WPB);
-        blocks = std::min<int64_t>((warps_needed + WPB - 1) / WPB, (int64_t)148 * 128);
+        // list mode: the count is only known on the device -- a grid of a few
+        // waves strides over it
+        blocks = std::min<int64_t>((warps_needed + WPB - 1) / WPB, (int64_t)148 * (a.list ? 16 : 128));
     }
     const int kpl = (a.K + 31) / 32;
     if (kpl <= 1) return launch_omp_k<T, 1>(a, (int)blocks, smem, st);

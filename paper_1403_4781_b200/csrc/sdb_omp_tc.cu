@@ -17,8 +17,13 @@
 // the largest |d.r| wins, lowest index on ties (the reference's 1e-12 tie
 // window is below FP32 resolution, as in k_omp_fast). More than OT_CMAX
 // candidates (or none outside the support) fall back to an exact sweep over
-// all atoms. The per-signal relative gap between the winner and the runner-up
-// is reported (near-tie log, north_star).
+// all atoms. Per signal the smallest decision margin is reported (near-tie
+// log, north_star; the FP64 certification pass re-decides signals whose
+// margin is below its tolerance, sdb_certify.cu): over the steps whose best
+// |d.r| is above the rounding floor (1e-6 ||y||), (best - runner-up) / ||y||
+// with the runner-up exact among the candidates and bounded above by
+// thr + win/2 for the rest; and in error-bounded mode |(||r|| - eps)| / ||y||
+// at every stopping test.
 //
 // Per step and signal (thread = signal, TMEM lane = tile row):
 //   scan:   block maxima of |corr_tf32| over the row (tcgen05.ld), then the
@@ -79,7 +84,7 @@ struct OtArgs {
     int32_t* counts;
     int8_t* status;
     float* rnorm;         // optional
-    float* gap;           // optional: min relative gap best vs runner-up over the steps
+    float* gap;           // optional: smallest decision margin / ||y|| over the steps
 };
 
 __device__ __forceinline__ int tile_shard(const int64_t* __restrict__ ts, int P, int64_t t) {
@@ -243,6 +248,7 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
         RoundIter it{a.ts, a.P, tb, te, -1};
         Round rd;
         auto rrow = [&](int kb, int cc) -> unsigned char* { return R + kb * OT_RB + row * 128 + ((cc ^ swz) << 4); };
+        const uint32_t ds_u32 = smem_u32(Ds);
         auto drow = [&](int kb, int j, int cc) -> const unsigned char* {
             return Ds + kb * a.kpad * 128 + j * 128 + ((cc ^ (j & 7)) << 4);
         };
@@ -281,7 +287,7 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
 
         while (it.next(rd)) {
             if (rd.first) {
-                mbar_wait(smem_u32(&bars[6]), (uint32_t)(k & 1));   // the shard's dictionary landed
+                mbar_wait_sleep(smem_u32(&bars[6]), (uint32_t)(k & 1));   // the shard's dictionary landed
                 ++k;
             }
             if (g == 0 || rd.has1) {
@@ -323,8 +329,9 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
                 int n = 0, status = 0;
                 bool act = valid && !(ysq <= eps2 || ysq == 0.0f);
                 float rsq = ysq;
-                float gmin = 1.0f;
                 const float ynorm = sqrtf(ysq);
+                // smallest decision margin relative to ||y|| (1: none close)
+                float gmin = (a.eps > 0.f && ynorm > 0.f) ? fminf(1.0f, fabsf(ynorm - a.eps) / ynorm) : 1.0f;
                 float L[CAP * (CAP + 1) / 2], invd[CAP], x[CAP], z[CAP];
                 int ids[CAP];
 #pragma unroll
@@ -340,7 +347,7 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
 
                 int cont = publish(act);
                 while (cont) {
-                    mbar_wait(smem_u32(&bars[g]), fph & 1u);
+                    mbar_wait_sleep(smem_u32(&bars[g]), fph & 1u);
                     ++fph;
                     tmem_fence_after();
                     // ---------------- scan: candidates within the window of the TF32 max
@@ -446,7 +453,7 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
                             for (int j = 0; j < K; ++j)
                                 if (!in_support(j)) consider(j);
                         }
-                        if (best >= 0.f && best > 0.f) gmin = fminf(gmin, fmaxf(0.f, (best - second) / best));
+                        if (best >= 1e-6f * ynorm) gmin = fminf(gmin, fmaxf(0.f, best - second) / ynorm);
                         if (bj < 0 || best * best <= 1e-26f * rsq) {   // cmax <= 1e-13 ||r|| (_kernels.py:97)
                             status = 3;
                             act = false;
@@ -508,7 +515,15 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
                                 }
                                 const bool need_r = n < a.cap || a.rnorm != nullptr || a.eps > 0.f;
                                 if (need_r) {
-                                    // r -= D_S dx in place (the next MMA's A operand)
+                                    // r -= D_S dx in place (the next MMA's A operand); the
+                                    // support rows' shared addresses are formed once
+                                    uint32_t dsa[CAP], dsw[CAP];
+#pragma unroll
+                                    for (int t = 0; t < CAP; ++t) {
+                                        const int jt = (t < n) ? ids[t] : 0;
+                                        dsa[t] = ds_u32 + (uint32_t)jt * 128u;
+                                        dsw[t] = (uint32_t)(jt & 7) << 4;
+                                    }
                                     float r0 = 0.f, r1 = 0.f;
                                     for (int kb = 0; kb < a.nkb; ++kb) {
 #pragma unroll
@@ -517,7 +532,8 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
 #pragma unroll
                                             for (int t = 0; t < CAP; ++t) {
                                                 if (t < n) {
-                                                    const float4 d = lds4(drow(kb, ids[t], cc));
+                                                    const float4 d = lds4_u32(dsa[t] + (uint32_t)(kb * a.kpad * 128) +
+                                                                              (((uint32_t)cc << 4) ^ dsw[t]));
                                                     v.x = fmaf(-dx[t], d.x, v.x);
                                                     v.y = fmaf(-dx[t], d.y, v.y);
                                                     v.z = fmaf(-dx[t], d.z, v.z);
@@ -533,6 +549,7 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
                                     }
                                     rsq = r0 + r1;
                                 }
+                                if (a.eps > 0.f) gmin = fminf(gmin, fabsf(__fsqrt_rn(rsq) - a.eps) / ynorm);
                                 if (n >= a.cap) act = false;
                                 else if (__fsqrt_rn(rsq) <= a.eps) act = false;   // _kernels.py:153
                             }
@@ -541,7 +558,7 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
                     cont = publish(act);
                 }
                 // the MMA issuer's acknowledgement of the tile end
-                mbar_wait(smem_u32(&bars[g]), fph & 1u);
+                mbar_wait_sleep(smem_u32(&bars[g]), fph & 1u);
                 ++fph;
                 // ---- codes in selection order (entries >= n zeroed like the reference)
                 if (valid) {

@@ -29,6 +29,26 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
             : "memory");
     }
 }
+// as mbar_wait, but the waiting threads are suspended by the hardware (up to
+// the time hint per try) instead of spinning on issue slots that the other
+// warps of the SM need
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t phase) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(bar), "r"(phase), "r"(0x989680)
+            : "memory");
+    }
+}
+__device__ __forceinline__ float4 lds4_u32(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+    return v;
+}
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
                                             uint32_t bar) {
     asm volatile(

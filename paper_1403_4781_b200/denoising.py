@@ -152,7 +152,7 @@ def denoise_device(px: torch.Tensor, D64: torch.Tensor, p: int, stride: int, eps
     Pt = patches_device(px, p, stride, prec)
     codes = E.code_single_dict(Pt, D64, cap, eps, prec, want_rnorm=False)   # norms are never read
     out = E.empty((H, W), torch.float64)
-    E._lib.call("sdb_reconstruct", E.sdb_dtype(prec), H, W, p, stride, E.ptr(D64), codes.cap,
+    E._lib.call("sdb_reconstruct", E.sdb_dtype(codes.vprec or prec), H, W, p, stride, E.ptr(D64), codes.cap,
                 E.ptr(codes.idx), E.ptr(codes.val), E.ptr(codes.counts), 0.0, 255.0,
                 E.ptr(out), E.stream())
     return out

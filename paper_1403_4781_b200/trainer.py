@@ -213,9 +213,7 @@ GRAPH_MAX_N = int(os.environ.get("SDB_GRAPH_MAX_N", str(1 << 23)))
 def _iteration(S: E.ShardSet, D: torch.Tensor, cap: int, eps: float, use_tc: bool):
     """One alternating step (trainer.py:184-187): code, MOD, replace.
     Returns (new D, residual_fro per shard)."""
-    prec = S.prec
-    codes = E.code(S.Y, S.off, S.max_rows, E.working_dict(D, prec), E.gram(D, prec), cap, eps,
-                   prec, use_tc, ysq=S.signal_sq(), want_rnorm=False)
+    codes = E.code_shards(S, D, cap, eps, use_tc)
     r = E.mod_update(S, codes, D)
     E.replace_degenerate(S, codes, r.D, r.usage)
     return r.D, r.resid
@@ -230,7 +228,10 @@ class _GraphedLoop:
     phase it removes the inter-launch gaps and most of the host enqueue."""
 
     def __init__(self, S: E.ShardSet, D0: torch.Tensor, cap: int, eps: float, use_tc: bool):
-        self.S = E.ShardSet(S.Y.clone(), S.off.clone(), list(S.sizes), S.prec)
+        if S._exact is not None and S._exact_auth:
+            self.S = E.ShardSet.with_exact(S._exact.Y.clone(), S.off.clone(), list(S.sizes), S.prec)
+        else:
+            self.S = E.ShardSet(S.Y.clone(), S.off.clone(), list(S.sizes), S.prec)
         self.S.signal_sq()
         self.D = D0.clone()
         # warm-up outside capture (first launches set kernel attributes and
@@ -248,6 +249,8 @@ class _GraphedLoop:
 
     def load(self, S: E.ShardSet, D0: torch.Tensor):
         self.S.Y.copy_(S.Y)
+        if self.S._exact_auth:
+            self.S._exact.Y.copy_(S._exact.Y)
         self.S.refresh()
         self.D.copy_(D0)
 
@@ -265,6 +268,7 @@ def _graph_bytes(S: E.ShardSet, D0: torch.Tensor, cap: int) -> int:
     es = 8 if S.prec == "fp64" else 4
     N = S.N
     return (N * m * es * 2            # static Y copy + split/tf32 staging
+            + (N * m * 8 + N * cap * 8 if E.certifies(S.prec) else 0)   # FP64 copy + FP64 code values
             + N * K * es              # alpha0 (the coding pass's largest buffer)
             + N * cap * (4 + es) + N * 16
             + P * (K * K + 4 * K * m) * 8)
@@ -282,7 +286,7 @@ def _graphed(S: E.ShardSet, D0: torch.Tensor, cap: int, eps: float, use_tc: bool
     # tag: callers that run several trainings of equal shape concurrently (shard
     # groups on their own streams) get one graph -- and static buffers -- each
     key = (S.prec, tuple(S.Y.shape), tuple(S.sizes), tuple(D0.shape), cap, float(eps), bool(use_tc),
-           E.get_precision(None), E.FUSE_STEP1, torch.cuda.current_device(), _graph_bytes(S, D0, cap), tag)
+           E.get_precision(None), E.FUSE_STEP1, E.CERTIFY, E.CERT_TAU, bool(S._exact_auth), torch.cuda.current_device(), _graph_bytes(S, D0, cap), tag)
     g = _GRAPH_CACHE.get(key)
     if g is not None:
         _GRAPH_CACHE.move_to_end(key)   # LRU: the hot shapes stay
@@ -331,8 +335,7 @@ def train_device(S: E.ShardSet, D0: torch.Tensor, cap: int, eps: float, iteratio
         for it in range(iterations):
             D, rr = _iteration(S, D, cap, eps, use_tc)
             resid[it].copy_(rr)
-    codes = E.code(S.Y, S.off, S.max_rows, E.working_dict(D, prec), E.gram(D, prec), cap, eps,
-                   prec, use_tc, ysq=S.signal_sq(), want_rnorm=False)
+    codes = E.code_shards(S, D, cap, eps, use_tc)
     return D, codes, resid
 
 
@@ -592,10 +595,18 @@ def _merge(Dl: torch.Tensor, w: torch.Tensor, K1: int, m: int, K: int, s2: int, 
         Dk, wk = Dl.index_select(0, kt).contiguous(), w.index_select(0, kt).contiguous()
     else:
         Dk, wk = Dl, w
-    Ym = E.scale_rows(Dk, wk, K1, prec)
     cap2, _ = coding_mode(m, K, s2, None, None)
-    Sm = E.ShardSet.single(Ym, prec)
-    D0m = init_dictionaries(Sm, K, init, [seed_merge])
+    if E.certifies(prec):
+        # certified mode: the pooled scaled atoms stay FP64 (the FP32 copy is
+        # only the coding kernels' input), like the reference's merge data
+        Ym64 = E.scale_rows(Dk, wk, K1, "fp64")
+        Sm = E.ShardSet.with_exact(Ym64, E.shard_offsets([Ym64.shape[0]])[0], [Ym64.shape[0]], prec)
+        Ym = Sm.Y
+        D0m = init_dictionaries(Sm.exact(), K, init, [seed_merge])
+    else:
+        Ym = E.scale_rows(Dk, wk, K1, prec)
+        Sm = E.ShardSet.single(Ym, prec)
+        D0m = init_dictionaries(Sm, K, init, [seed_merge])
     Dm, _codes_m, _ = train_device(Sm, D0m, cap2, 0.0, merge_iters, use_tc)
     return Dm, w_h, Ym.shape[0]
 

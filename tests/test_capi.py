@@ -48,7 +48,7 @@ def test_bad_args_rejected_without_launch():
     from paper_1403_4781_b200 import _lib
     lib = _lib.load()
     rc = lib.sdb_omp(7, 1, 1, 1, 1, None, None, 1, None, 1, None, None, 1, 0.0, 1e-12,
-                     None, None, None, None, None, None, None, 0, None)
+                     None, None, None, None, None, None, None, None, 0, None)
     assert rc == -22
     assert b"bad args" in lib.sdb_last_error()
     assert lib.sdb_signal_sq(-1, 64, None, 64, None, None) == -22

@@ -142,7 +142,7 @@ def test_fp32_dynamic_chunks_equal_static_ranges():
         scr = torch.empty((sb,), dtype=torch.uint8, device="cuda") if dynamic else None
         _lib.call("sdb_omp", 0, N, m, K, 1, off.data_ptr(), alpha.data_ptr(), K, Yd.data_ptr(), m,
                   DT.data_ptr(), G.data_ptr(), cap, 0.0, 1e-6, idx.data_ptr(), val.data_ptr(),
-                  cnt.data_ptr(), sts.data_ptr(), None, None, scr.data_ptr() if dynamic else None,
+                  cnt.data_ptr(), sts.data_ptr(), None, None, None, scr.data_ptr() if dynamic else None,
                   sb if dynamic else 0, E.stream())
         torch.cuda.synchronize()
         outs.append([t.cpu().numpy() for t in (idx, val, cnt, sts)])

@@ -91,6 +91,7 @@ def trace(name, t):
             top = np.argsort(-res_ref)[:6]
             rec["top_resid_ref"] = [(int(i), float(res_ref[i])) for i in top]
         print(json.dumps(rec), flush=True)
+        D = r.D                                                # continue the GPU trajectory
 
 
 if __name__ == "__main__":
