@@ -141,12 +141,14 @@ int sdb_omp_tc(int64_t N, int64_t m, int64_t K, int64_t P, const int64_t *shard_
  * then codes exactly the status -1 signals. The union is bitwise sdb_omp's output
  * (rnorm not produced). Needs K <= 256, m <= 256, cap <= 32, eps > 0 and ysq
  * (sdb_signal_sq); SDB_ENOTSUP otherwise (the caller uses sdb_correlate +
- * sdb_omp). ws: sdb_code_step1_workspace_bytes(). */
+ * sdb_omp). gap: optional FP32 decision margins of the settled signals (as
+ * sdb_omp's; the deferred ones get theirs from sdb_omp_deferred), for
+ * sdb_certify. ws: sdb_code_step1_workspace_bytes(). */
 int64_t sdb_code_step1_workspace_bytes(int64_t P, int64_t m, int64_t K);
 int sdb_code_step1(int64_t N, int64_t m, int64_t K, int64_t P, const int64_t *shard_off, const float *Y,
                    int64_t ldy, const float *D, const float *G, const float *ysq, int64_t cap, double eps,
                    double guard, float *alpha0, int64_t lda, int32_t *idx, float *val, int32_t *counts,
-                   int8_t *status, void *ws, int64_t ws_bytes, void *stream);
+                   int8_t *status, float *gap, void *ws, int64_t ws_bytes, void *stream);
 int sdb_omp_deferred(int64_t N, int64_t m, int64_t K, int64_t P, const int64_t *shard_off,
                      const float *alpha0, int64_t lda, const float *Y, int64_t ldy, const float *D,
                      const float *G, const float *ysq, int64_t cap, double eps, double guard, int32_t *idx,

@@ -259,11 +259,8 @@ def code(Ydev: torch.Tensor, off: torch.Tensor, max_rows: int, DT: torch.Tensor,
     if N == 0:
         return out
     es = 8 if prec == "fp64" else 4
-    # the fused step-1 epilogue reports no decision margins: certified coding
-    # (want_gap) takes the two-kernel path
     fused1 = (FUSE_STEP1 and prec == "fp32" and use_tc and ysq is not None and eps > 0.0 and not want_rnorm
-              and not want_gap and K <= 256 and m <= 256 and cap <= 32 and K % 4 == 0 and m % 4 == 0
-              and N <= DYN_MAX_N)
+              and K <= 256 and m <= 256 and cap <= 32 and K % 4 == 0 and m % 4 == 0 and N <= DYN_MAX_N)
     if want_gap and prec == "fp32" and out.gap is None:
         out.gap = empty((N,), torch.float32)
     if not fused1 and N <= DYN_MAX_N and omp_tc_applies(m, K, cap, prec, use_tc):
@@ -284,11 +281,12 @@ def code(Ydev: torch.Tensor, off: torch.Tensor, max_rows: int, DT: torch.Tensor,
         ndef = ws[wb - 256:wb - 252].view(torch.int32)   # deferred count (written by the launch)
         timed_call("step1", N * (4 * m + 4), 2.0 * N * m * K, "sdb_code_step1", N, m, K, P, ptr(off),
                    ptr(Ydev), m, ptr(DT), ptr(G), ptr(ysq), cap, float(eps), GUARD[prec], ptr(alpha), K,
-                   ptr(out.idx), ptr(out.val), ptr(out.counts), ptr(out.status), ptr(ws), int(wb),
-                   stream())
+                   ptr(out.idx), ptr(out.val), ptr(out.counts), ptr(out.status),
+                   ptr(out.gap) if want_gap else None, ptr(ws), int(wb), stream())
         timed_call("omp_deferred", 0.0, 0.0, "sdb_omp_deferred", N, m, K, P, ptr(off), ptr(alpha), K,
                    ptr(Ydev), m, ptr(DT), ptr(G), ptr(ysq), cap, float(eps), GUARD[prec], ptr(out.idx),
-                   ptr(out.val), ptr(out.counts), ptr(out.status), None, ptr(ws), int(wb), stream())
+                   ptr(out.val), ptr(out.counts), ptr(out.status), ptr(out.gap) if want_gap else None,
+                   ptr(ws), int(wb), stream())
         if KTIMER is not None and not torch.cuda.is_current_stream_capturing():
             if "deferred" not in KSTAT:
                 KSTAT["deferred"] = zeros((1,), torch.int64)

@@ -39,7 +39,7 @@ SIGNATURES = {
     "sdb_signal_sq": (c_int, [c_i64, c_i64, c_vp, c_i64, c_vp, c_vp]),
     "sdb_code_step1_workspace_bytes": (c_i64, [c_i64, c_i64, c_i64]),
     "sdb_code_step1": (c_int, [c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp,
-                               c_i64, c_dbl, c_dbl, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp,
+                               c_i64, c_dbl, c_dbl, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                c_i64, c_vp]),
     "sdb_omp_deferred": (c_int, [c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp,
                                  c_vp, c_vp, c_i64, c_dbl, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
@@ -101,7 +101,7 @@ class NativeError(RuntimeError):
 
 _lib = None
 # must equal sdb_abi_version() in csrc/sdb_capi.cu (bumped whenever exports change)
-ABI_VERSION = 8
+ABI_VERSION = 9
 
 
 def load():

@@ -55,7 +55,7 @@ __global__ void k_cast(int64_t n, const double* __restrict__ src, T* __restrict_
 
 extern "C" {
 
-int sdb_abi_version(void) { return 8; }
+int sdb_abi_version(void) { return 9; }
 const char* sdb_last_error(void) { return g_err.c_str(); }
 
 int sdb_device_cc(void) {
@@ -203,7 +203,7 @@ int sdb_certify(int64_t N, int64_t m, int64_t K, int64_t P, const int64_t* shard
     if (N == 0) return SDB_OK;
     cudaMemsetAsync(nlist, 0, sizeof(int32_t), S(stream));
     int rc = sdb::certify_refit(N, (int)m, (int)K, (int)cap, (int)P, shard_off, Y, Y64, ldy, D, G, idx, counts, status,
-                                gap, (float)tau, val, rnorm, list, nlist, S(stream));
+                                gap, (float)tau, val, rnorm, list, nlist, eps > 0.0, S(stream));
     if (rc) return cuda_rc(rc, "sdb_certify (refit)");
     sdb::OmpArgs<double> a{};
     a.N = N; a.m = (int)m; a.K = (int)K; a.cap = (int)cap; a.P = (int)P;
@@ -253,7 +253,7 @@ int64_t sdb_code_step1_workspace_bytes(int64_t P, int64_t m, int64_t K) {
 int sdb_code_step1(int64_t N, int64_t m, int64_t K, int64_t P, const int64_t* shard_off, const float* Y,
                    int64_t ldy, const float* D, const float* G, const float* ysq, int64_t cap, double eps,
                    double guard, float* alpha0, int64_t lda, int32_t* idx, float* val, int32_t* counts,
-                   int8_t* status, void* ws, int64_t ws_bytes, void* stream) {
+                   int8_t* status, float* gap, void* ws, int64_t ws_bytes, void* stream) {
     if (N < 0 || m < 1 || K < 1 || P < 1 || cap < 1 || ldy < m || lda < K)
         return fail(SDB_EINVAL, "sdb_code_step1: bad args");
     if (K > 256 || m > 256 || cap > 32 || !(eps > 0.0) || ysq == nullptr)
@@ -264,7 +264,7 @@ int sdb_code_step1(int64_t N, int64_t m, int64_t K, int64_t P, const int64_t* sh
     int32_t* counters = (int32_t*)((unsigned char*)ws + step1_corr_bytes(P, m, K));
     int rc = sdb::code_step1_tc_f32(N, Y, ldy, shard_off, (int)P, D, m, K, alpha0, lda, ws,
                                     step1_corr_bytes(P, m, K), ysq, G, (float)eps, (float)guard, (int)cap,
-                                    idx, val, counts, status, counters, S(stream));
+                                    idx, val, counts, status, gap, counters, S(stream));
     if (rc == cudaErrorNotSupported) return fail(SDB_ENOTSUP, "sdb_code_step1: shape outside the tcgen05 tiling");
     return cuda_rc(rc, "sdb_code_step1");
 }

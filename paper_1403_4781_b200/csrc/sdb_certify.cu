@@ -66,8 +66,8 @@ __device__ __forceinline__ double gsum(double v) {
 // looking Cholesky (columns broadcast by group shuffles), forward substitution
 // by broadcasts, back substitution through the factor rows staged in shared
 // memory.
-template <int LPS, int VPL, int WPB>
-__global__ void __launch_bounds__(WPB * 32)
+template <int LPS, int VPL, int WPB, bool VEC2>
+__global__ void __launch_bounds__(WPB * 32, LPS == 8 ? 3 : 1)
 k_certify(CertArgs a) {
     constexpr int GPW = 32 / LPS;                      // signals per warp
     __shared__ double sL[WPB * GPW][LPS][LPS + 1];
@@ -78,6 +78,7 @@ k_certify(CertArgs a) {
     double (*Ls)[LPS + 1] = sL[wib * GPW + g];
     const int m = a.m, K = a.K, cap = a.cap, P = a.P;
     const bool off_smem = P <= 256;
+
     if (off_smem)
         for (int q = threadIdx.x; q <= P; q += blockDim.x) s_off[q] = a.off[q];
     __syncthreads();
@@ -89,7 +90,9 @@ k_certify(CertArgs a) {
         const int64_t i = it * nsig_per_iter + ((int64_t)blockIdx.x * WPB + wib) * GPW + g;
         const bool valid = i < a.N;
         int n = valid ? a.counts[i] : 0;
-        const bool frag = valid && (a.status[i] != 0 || (a.gap != nullptr && !(a.gap[i] >= a.tau)));
+        // supports longer than the lane group (error-bounded coding with a
+        // large cap, rare) go to the exact FP64 list as well
+        const bool frag = valid && (a.status[i] != 0 || n > LPS || (a.gap != nullptr && !(a.gap[i] >= a.tau)));
         if (frag) {
             if (l == 0) {
                 const int pos = atomicAdd(a.nlist, 1);
@@ -113,45 +116,76 @@ k_certify(CertArgs a) {
         const int32_t* ids_row = a.idx + (valid ? i : 0) * cap;
         const int my_atom = (l < n) ? ids_row[l] : 0;       // lane r: atom r of the support
         // ---- b = D_S^T y: lane l holds y[l + LPS v]; part[t] for every support atom
+        const int nmax0 = __reduce_max_sync(SDB_FULL, n);
         double part[LPS];
 #pragma unroll
         for (int t = 0; t < LPS; ++t) part[t] = 0.0;
         int at[LPS];
 #pragma unroll
         for (int t = 0; t < LPS; ++t) at[t] = __shfl_sync(SDB_FULL, my_atom, gbase + t);
+        if constexpr (VEC2) {
+            // lane l: element pairs c = 2l + 2 LPS v (16-byte dictionary loads)
 #pragma unroll
-        for (int v = 0; v < VPL; ++v) {
-            const int c = l + LPS * v;
-            const double yv = (work && c < m) ? (a.Y64 ? __ldg(a.Y64 + i * a.ldy + c)
-                                                       : (double)__ldg(a.Y + i * a.ldy + c)) : 0.0;
+            for (int v = 0; v < (VPL + 1) / 2; ++v) {
+                const int c = 2 * l + 2 * LPS * v;
+                double2 yv = make_double2(0.0, 0.0);
+                if (work && c < m) {
+                    if (a.Y64) {
+                        yv = __ldg(reinterpret_cast<const double2*>(a.Y64 + i * a.ldy + c));
+                    } else {
+                        const float2 f = __ldg(reinterpret_cast<const float2*>(a.Y + i * a.ldy + c));
+                        yv = make_double2((double)f.x, (double)f.y);
+                    }
+                }
 #pragma unroll
-            for (int t = 0; t < LPS; ++t)
-                if (t < n && c < m) part[t] = fma(__ldg(Dp + (int64_t)at[t] * m + c), yv, part[t]);
+                for (int t = 0; t < LPS; ++t) {
+                    if (t < nmax0 && t < n && c < m) {
+                        const double2 d = __ldg(reinterpret_cast<const double2*>(Dp + (int64_t)at[t] * m + c));
+                        part[t] = fma(d.y, yv.y, fma(d.x, yv.x, part[t]));
+                    }
+                }
+            }
+        } else {
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+                const int c = l + LPS * v;
+                const double yv = (work && c < m) ? (a.Y64 ? __ldg(a.Y64 + i * a.ldy + c)
+                                                           : (double)__ldg(a.Y + i * a.ldy + c)) : 0.0;
+#pragma unroll
+                for (int t = 0; t < LPS; ++t)
+                    if (t < nmax0 && t < n && c < m) part[t] = fma(__ldg(Dp + (int64_t)at[t] * m + c), yv, part[t]);
+            }
         }
+        const int nmax = nmax0;
         double b = 0.0;
 #pragma unroll
         for (int t = 0; t < LPS; ++t) {
-            const double bt = gsum<LPS>(part[t]);
-            if (l == t) b = bt;
+            if (t < nmax) {                                // warp-uniform
+                const double bt = gsum<LPS>(part[t]);
+                if (l == t) b = bt;
+            }
         }
         // ---- row r of G_SS (columns u <= r), independent loads
         double gr[LPS];
 #pragma unroll
         for (int u = 0; u < LPS; ++u)
             gr[u] = (u <= l && l < n) ? __ldg(Gp + (int64_t)my_atom * K + at[u]) : 0.0;
-        // ---- Cholesky (right-looking; lane r keeps row r: gr[k] -> L[r][k])
-        const int nmax = __reduce_max_sync(SDB_FULL, n);
+        // ---- Cholesky (right-looking; lane r keeps row r: gr[k] -> L[r][k] for
+        // k < r; lane k keeps 1 / L[k][k] in ik, computed once per pivot)
+        double ik = 1.0;
 #pragma unroll
         for (int k = 0; k < LPS; ++k) {
-            if (k < nmax) {
-                const double dk = sqrt(__shfl_sync(SDB_FULL, gr[k], gbase + k));   // lane k's diagonal
-                const double ik = 1.0 / dk;
-                if (l > k) gr[k] *= ik;
-                if (l == k) gr[k] = dk;
+            if (k < nmax) {                                // warp-uniform
+                const double gk = __shfl_sync(SDB_FULL, gr[k], gbase + k);   // lane k's pivot
+                const double rk = (k < n && gk > 0.0) ? rsqrt(gk) : 0.0;
+                if (l == k) ik = rk;
+                if (l > k) gr[k] *= rk;
 #pragma unroll
                 for (int c = k + 1; c < LPS; ++c) {
-                    const double lck = __shfl_sync(SDB_FULL, gr[k], gbase + c);   // L[c][k]
-                    if (l >= c && l < n) gr[c] = fma(-gr[k], lck, gr[c]);
+                    if (c < nmax) {
+                        const double lck = __shfl_sync(SDB_FULL, gr[k], gbase + c);   // L[c][k]
+                        if (l >= c && l < n) gr[c] = fma(-gr[k], lck, gr[c]);
+                    }
                 }
             }
         }
@@ -160,14 +194,15 @@ k_certify(CertArgs a) {
 #pragma unroll
         for (int k = 0; k < LPS; ++k) {
             if (k < nmax) {
-                const double zk = __shfl_sync(SDB_FULL, z / gr[k], gbase + k);   // evaluated on lane k
+                const double zk = __shfl_sync(SDB_FULL, z * ik, gbase + k);   // evaluated on lane k
                 if (l == k) z = zk;
                 if (l > k) z = fma(-gr[k], zk, z);
             }
         }
         if (l < n) {
 #pragma unroll
-            for (int u = 0; u < LPS; ++u) Ls[l][u] = gr[u];
+            for (int u = 0; u < LPS; ++u)
+                if (u < nmax) Ls[l][u] = gr[u];
         }
         __syncwarp();
         // ---- back L^T x = z: lane k solves x_k once every x_j, j > k, is in
@@ -176,7 +211,7 @@ k_certify(CertArgs a) {
 #pragma unroll
         for (int k = LPS - 1; k >= 0; --k) {
             if (k < nmax) {
-                const double xk = __shfl_sync(SDB_FULL, acc / Ls[k < n ? k : 0][k], gbase + k);
+                const double xk = __shfl_sync(SDB_FULL, acc * ik, gbase + k);
                 if (l == k) x = xk;
                 if (l < k && k < n) acc = fma(-Ls[k][l], xk, acc);
             }
@@ -209,7 +244,11 @@ int launch_cert(const CertArgs& a, cudaStream_t st) {
     constexpr int GPW = 32 / LPS;
     const int64_t per = (int64_t)WPB * GPW;
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((a.N + per - 1) / per, 148 * 64 / WPB));
-    k_certify<LPS, VPL, WPB><<<(unsigned)blocks, WPB * 32, 0, st>>>(a);
+    // 16-byte loads when every row starts 16-byte aligned
+    const bool vec2 = (a.m % 2 == 0) && (a.ldy % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.D) & 15) == 0) &&
+                      ((reinterpret_cast<uintptr_t>(a.Y64 ? (const void*)a.Y64 : (const void*)a.Y) & 15) == 0);
+    if (vec2) k_certify<LPS, VPL, WPB, true><<<(unsigned)blocks, WPB * 32, 0, st>>>(a);
+    else k_certify<LPS, VPL, WPB, false><<<(unsigned)blocks, WPB * 32, 0, st>>>(a);
     return (int)cudaGetLastError();
 }
 
@@ -218,10 +257,13 @@ int launch_cert(const CertArgs& a, cudaStream_t st) {
 int certify_refit(int64_t N, int m, int K, int cap, int P, const int64_t* off, const float* Y, const double* Y64,
                   int64_t ldy, const double* D, const double* G, const int32_t* idx, const int32_t* counts,
                   const int8_t* status, const float* gap, float tau, double* val, double* rnorm, int32_t* list,
-                  int32_t* nlist, cudaStream_t st) {
+                  int32_t* nlist, bool short_supports, cudaStream_t st) {
     if (N <= 0) return 0;
     CertArgs a{N, m, K, cap, P, off, Y, Y64, ldy, D, G, idx, counts, status, gap, tau, val, rnorm, list, nlist};
-    if (cap <= 8 && m <= 64) return launch_cert<8, 8, 8>(a, st);
+    // 8-lane groups whenever the supports are short (cap <= 8, or error-
+    // bounded coding: the few longer supports are re-coded exactly)
+    if ((cap <= 8 || short_supports) && m <= 64) return launch_cert<8, 8, 8>(a, st);
+    if ((cap <= 8 || short_supports) && m <= 256) return launch_cert<8, 32, 8>(a, st);
     if (cap <= 16 && m <= 64) return launch_cert<16, 4, 8>(a, st);
     if (cap <= 16 && m <= 256) return launch_cert<16, 16, 4>(a, st);
     if (cap <= 32 && m <= 64) return launch_cert<32, 2, 4>(a, st);

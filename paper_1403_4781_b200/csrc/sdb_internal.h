@@ -49,7 +49,7 @@ int certify_refit(int64_t N, int m, int K, int cap, int P, const int64_t* off, c
                   int64_t ldy,
                   const double* D, const double* G, const int32_t* idx, const int32_t* counts,
                   const int8_t* status, const float* gap, float tau, double* val, double* rnorm, int32_t* list,
-                  int32_t* nlist, cudaStream_t st);
+                  int32_t* nlist, bool short_supports, cudaStream_t st);
 int64_t perm_ws_bytes(int64_t n);
 int perm_from_targets(int64_t n, const uint32_t* js, int64_t* perm, void* ws, int64_t ws_bytes,
                       cudaStream_t st);
@@ -73,7 +73,7 @@ int64_t corr_tc_ws_bytes(int P, int64_t m, int64_t K);
 int code_step1_tc_f32(int64_t N, const float* Y, int64_t ldy, const int64_t* off, int P, const float* D,
                       int64_t m, int64_t K, float* alpha, int64_t lda, void* ws, int64_t ws_bytes,
                       const float* ysq, const float* G, float eps, float guard, int cap, int32_t* idx,
-                      float* val, int32_t* counts, int8_t* status, int* n_deferred, cudaStream_t st);
+                      float* val, int32_t* counts, int8_t* status, float* gap, int* n_deferred, cudaStream_t st);
 
 template <typename T>
 int launch_omp(OmpArgs<T> a, cudaStream_t st);

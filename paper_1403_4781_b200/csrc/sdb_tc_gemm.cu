@@ -64,7 +64,7 @@ template <bool RES, bool CODE>
 struct Cfg {
     static constexpr int NST = 2;
     static constexpr int DATA = RES ? NST * RES_A_STAGE + RES_KB * 2 * B_BYTES : 2 * STAGE_BYTES;
-    static constexpr int XCHG = 4 * 272 + 4 * 1024;            // CODE: pair exchange + per-warp G diagonal
+    static constexpr int XCHG = 4 * 400 + 4 * 1024;            // CODE: pair exchange + per-warp G diagonal
     static constexpr int SMEM = 1024 + DATA + (CODE ? 256 + XCHG : 1024 + 4 * 2 * 32 * 32 * 4);
 };
 static_assert(Cfg<true, true>::SMEM <= 232448, "smem");
@@ -113,6 +113,7 @@ struct Step1 {
     int32_t* counts;
     int8_t* status;
     int* n_deferred;      // zeroed by k_tile_layout
+    float* gap;           // optional: settled signals' smallest decision margin / ||y|| (certification)
 };
 
 // argmax |x| over one 32-column block of a row: a pairwise tree on the raw
@@ -142,6 +143,21 @@ __device__ __forceinline__ void block_argmax(const uint32_t (&v)[32], int c, int
     bk = k[0] + (uint32_t)c;
 }
 
+// second-largest |x| of one 32-column block given its argmax column bk
+// (certification margin; columns past K are 0)
+template <bool FULL>
+__device__ __forceinline__ float block_second(const uint32_t (&v)[32], int c, int K, uint32_t bk) {
+    float s0 = 0.0f, s1 = 0.0f;
+#pragma unroll
+    for (int t = 0; t < 32; t += 2) {
+        const float a0 = (FULL || c + t < K) && (uint32_t)(c + t) != bk ? fabsf(__uint_as_float(v[t])) : 0.0f;
+        const float a1 = (FULL || c + t + 1 < K) && (uint32_t)(c + t + 1) != bk ? fabsf(__uint_as_float(v[t + 1])) : 0.0f;
+        s0 = fmaxf(s0, a0);
+        s1 = fmaxf(s1, a1);
+    }
+    return fmaxf(s0, s1);
+}
+
 __device__ __forceinline__ void pair_sync(int quad) {
     // the two epilogue warps of one TMEM lane quadrant (named barrier 1 + quad)
     asm volatile("bar.sync %0, 64;" ::"r"(1 + quad) : "memory");
@@ -160,15 +176,22 @@ __device__ __forceinline__ void code_step1(const Step1& s1, uint32_t trow, int64
                                            float* __restrict__ alpha, int64_t lda, int lane) {
     const int64_t i = row_base + lane;
     const bool valid = lane < nrows;
-    // ---- argmax |alpha0| over this warp's columns
+    // ---- argmax |alpha0| over this warp's columns (and, for certification,
+    // the runner-up magnitude)
     float cur = 0.0f, cx = 0.0f;      // running max |alpha0|, its signed value
+    float sec = 0.0f;                 // running second-largest |alpha0| (s1.gap only)
     uint32_t key = 0xffffffffu;
     uint32_t va[32], vb[32];
+    const bool margin = s1.gap != nullptr;
     auto scan = [&](const uint32_t (&v)[32], int c) {
         float bx;
         uint32_t bk;
         if (c + 32 <= K) block_argmax<true>(v, c, K, bx, bk);   // warp-uniform
         else block_argmax<false>(v, c, K, bx, bk);
+        if (margin) {
+            const float bs = (c + 32 <= K) ? block_second<true>(v, c, K, bk) : block_second<false>(v, c, K, bk);
+            sec = fmaxf(fmaxf(sec, bs), fminf(cur, fabsf(bx)));
+        }
         if (fabsf(bx) > cur) { cur = fabsf(bx); cx = bx; key = bk; }
     };
     // 32-column blocks, the next block's TMEM load in flight during each scan
@@ -187,14 +210,23 @@ __device__ __forceinline__ void code_step1(const Step1& s1, uint32_t trow, int64
         }
     }
     // ---- combine the halves (the lower half's columns win ties)
-    if (half == 1) { xv[lane] = cx; xk[lane] = key; }
+    float* xs = xv + 68;              // upper half's runner-up (certification)
+    if (half == 1) { xv[lane] = cx; xk[lane] = key; if (margin) xs[lane] = sec; }
     pair_sync(quad);
     bool defer = false;
     unsigned dmask;
     if (half == 0) {
         const float cu = xv[lane];
         const uint32_t ku = xk[lane];
+        if (margin) sec = fmaxf(fmaxf(sec, xs[lane]), fminf(cur, fabsf(cu)));
         if (fabsf(cu) > cur) { cur = fabsf(cu); cx = cu; key = ku; }
+        const float ynrm = sqrtf(ysq);
+        float gm = 1.0f;
+        if (margin && ynrm > 0.0f) {
+            const float eps = sqrtf(s1.eps2);
+            if (eps > 0.0f) gm = fminf(gm, fabsf(ynrm - eps) / ynrm);
+            if (cur >= 1e-6f * ynrm) gm = fminf(gm, (cur - sec) / ynrm);
+        }
         // ---- the first greedy step (k_omp_fast, step 0); the deferral mask
         // is published before any store, so the upper warp is released early
         int n = 0, status = 0, best = 0;
@@ -220,6 +252,7 @@ __device__ __forceinline__ void code_step1(const Step1& s1, uint32_t trow, int64
                     n = 1;
                     const float rsq = fmaxf(fmaf(-tn, tn, ysq), 0.0f);
                     if (s1.cap > 1 && (fabsf(rsq - s1.eps2) <= 1e-4f * ysq || rsq > s1.eps2)) defer = true;
+                    if (margin) gm = fminf(gm, fabsf(sqrtf(rsq) - sqrtf(s1.eps2)) / ynrm);
                 }
             }
         }
@@ -247,6 +280,7 @@ __device__ __forceinline__ void code_step1(const Step1& s1, uint32_t trow, int64
                     }
                 }
                 s1.counts[i] = n;
+                if (margin) s1.gap[i] = gm;
             }
             s1.status[i] = defer ? (int8_t)-1 : (int8_t)status;
         }
@@ -435,8 +469,8 @@ k_corr_tc2(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUte
         const int quad = warp & 3;
         const int half = warp >= 10 ? 1 : 0;
         float* stg = stg_base + (warp - 2) * 2 * 1024;     // !CODE only
-        float* xch = stg_base + quad * 68;                 // CODE: the quadrant pair's exchange slots
-        float* diag = stg_base + 4 * 68 + quad * 256;      // CODE: lower warp's copy of the shard's G diagonal
+        float* xch = stg_base + quad * 100;                // CODE: the quadrant pair's exchange slots
+        float* diag = stg_base + 4 * 100 + quad * 256;     // CODE: lower warp's copy of the shard's G diagonal
         int diag_p = -1;
         const int c_mid = ((K + 63) / 64) * 32;
         int64_t n = 0;
@@ -698,12 +732,13 @@ int correlate_tc_f32(int64_t N, const float* Y, int64_t ldy, const int64_t* off,
 int code_step1_tc_f32(int64_t N, const float* Y, int64_t ldy, const int64_t* off, int P, const float* D,
                       int64_t m, int64_t K, float* alpha, int64_t lda, void* ws, int64_t ws_bytes,
                       const float* ysq, const float* G, float eps, float guard, int cap, int32_t* idx,
-                      float* val, int32_t* counts, int8_t* status, int* n_deferred, cudaStream_t st) {
+                      float* val, int32_t* counts, int8_t* status, float* gap, int* n_deferred, cudaStream_t st) {
     if (K > TN || N > 0x7fffffffll || cap < 1) return (int)cudaErrorNotSupported;
     Step1 s1;
     s1.ysq = ysq; s1.G = G; s1.eps2 = eps * eps; s1.guard = guard; s1.cap = cap;
     s1.idx = idx; s1.val = val; s1.counts = counts; s1.status = status;
     s1.n_deferred = n_deferred;
+    s1.gap = gap;
 
     return corr_tc_launch(N, Y, ldy, off, P, D, m, K, alpha, lda, ws, ws_bytes, &s1, st);
 }

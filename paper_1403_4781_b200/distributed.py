@@ -21,7 +21,7 @@ import torch.distributed as dist
 
 from . import _engine as E
 from .exceptions import InvalidInputError
-from .trainer import (SplitMergeResult, _derive_seeds, _sync, coding_mode, init_dictionaries,
+from .trainer import (SplitMergeResult, merge_data, _derive_seeds, _sync, coding_mode, init_dictionaries,
                       train_device)
 
 
@@ -100,13 +100,11 @@ def split_merge_ranks(Ydev: torch.Tensor, L: int, K1: int, local_cap: int, local
         raise InvalidInputError("all local code matrices are zero")
     kt = torch.from_numpy(keep).to(E.device())
     Dk, wk = Dall.index_select(0, kt).contiguous(), wall.index_select(0, kt).contiguous()
-    Ym = E.scale_rows(Dk, wk, K1, prec)
     cap2, _ = coding_mode(m, K, s2, None, None)
-    Sm = E.ShardSet.single(Ym, prec)
-    D0m = init_dictionaries(Sm, K, init, [seeds[L]])
+    Sm, D0m = merge_data(Dk, wk, K1, K, init, seeds[L], prec)
     Dm, _, _ = train_device(Sm, D0m, cap2, 0.0, merge_iters)
     _sync()
     t_end = time.perf_counter()
-    codings = (local_iters + 1) * N + (merge_iters + 1) * Ym.shape[0]
+    codings = (local_iters + 1) * N + (merge_iters + 1) * Sm.N
     return SplitMergeResult(E.d2h(Dm[0]).T.copy(), Dm, Dall, w_h, t_split - t_start,
                             t_local - t_split, t_end - t_local, t_end - t_start, codings)

@@ -126,7 +126,12 @@ class TrainConfig:
 
 @dataclass
 class TrainReport:
-    """Timing and quality summary (trainer.py:114-135)."""
+    """Timing and quality summary (trainer.py:114-135).
+
+    local_wall_times_s: one entry per local, as in the reference; the locals
+    of train_split_merge run concurrently in one batched launch sequence on
+    the GPU (not in a process pool), so every entry is the same batched
+    local-phase wall time (no per-shard timeline exists to report)."""
 
     final_mse_db: float
     per_iteration_residuals: list[float] = field(default_factory=list)
@@ -258,8 +263,15 @@ class _GraphedLoop:
 _GRAPH_CACHE: "OrderedDict" = OrderedDict()
 GRAPH_CACHE_MAX = 16
 # total bytes the cached graphs may pin (static signal copy + the captured
-# iteration's private pool: alpha, codes, MOD workspaces); LRU beyond that
-GRAPH_CACHE_BYTES = 8 << 30
+# iteration's private pool: alpha, codes, MOD workspaces); LRU beyond that.
+# Default: 40% of the device's memory (SDB_GRAPH_CACHE_GB overrides)
+GRAPH_CACHE_BYTES = int(float(os.environ.get("SDB_GRAPH_CACHE_GB", "0")) * (1 << 30))
+
+
+def _graph_cache_limit() -> int:
+    if GRAPH_CACHE_BYTES > 0:
+        return GRAPH_CACHE_BYTES
+    return int(0.4 * torch.cuda.get_device_properties(torch.cuda.current_device()).total_memory)
 
 
 def _graph_bytes(S: E.ShardSet, D0: torch.Tensor, cap: int) -> int:
@@ -267,9 +279,12 @@ def _graph_bytes(S: E.ShardSet, D0: torch.Tensor, cap: int) -> int:
     P, K, m = D0.shape
     es = 8 if S.prec == "fp64" else 4
     N = S.N
+    # the alpha0 matrix exists only on the paths that materialise it (not the
+    # fused tensor-core OMP)
+    alpha = 0 if E.omp_tc_applies(m, K, cap, S.prec) else N * K * es
     return (N * m * es * 2            # static Y copy + split/tf32 staging
             + (N * m * 8 + N * cap * 8 if E.certifies(S.prec) else 0)   # FP64 copy + FP64 code values
-            + N * K * es              # alpha0 (the coding pass's largest buffer)
+            + alpha                   # alpha0 (the coding pass's largest buffer)
             + N * cap * (4 + es) + N * 16
             + P * (K * K + 4 * K * m) * 8)
 
@@ -292,8 +307,9 @@ def _graphed(S: E.ShardSet, D0: torch.Tensor, cap: int, eps: float, use_tc: bool
         _GRAPH_CACHE.move_to_end(key)   # LRU: the hot shapes stay
         return g
     need = key[-2]
+    limit = _graph_cache_limit()
     while _GRAPH_CACHE and (len(_GRAPH_CACHE) >= GRAPH_CACHE_MAX or
-                            sum(k[-2] for k in _GRAPH_CACHE) + need > GRAPH_CACHE_BYTES):
+                            sum(k[-2] for k in _GRAPH_CACHE) + need > limit):
         _evict_one()
     while True:
         try:
@@ -596,19 +612,22 @@ def _merge(Dl: torch.Tensor, w: torch.Tensor, K1: int, m: int, K: int, s2: int, 
     else:
         Dk, wk = Dl, w
     cap2, _ = coding_mode(m, K, s2, None, None)
+    Sm, D0m = merge_data(Dk, wk, K1, K, init, seed_merge, prec)
+    Dm, _codes_m, _ = train_device(Sm, D0m, cap2, 0.0, merge_iters, use_tc)
+    return Dm, w_h, Sm.N
+
+
+def merge_data(Dk: torch.Tensor, wk: torch.Tensor, K1: int, K: int, init, seed_merge: int, prec: str):
+    """The merge training set [w_t D_t] (trainer.py:248-256) as shards plus
+    the merge's initial dictionary. Certified mode keeps the pooled scaled
+    atoms in FP64 (the FP32 copy only feeds the coding kernels), like the
+    reference's merge data."""
     if E.certifies(prec):
-        # certified mode: the pooled scaled atoms stay FP64 (the FP32 copy is
-        # only the coding kernels' input), like the reference's merge data
         Ym64 = E.scale_rows(Dk, wk, K1, "fp64")
         Sm = E.ShardSet.with_exact(Ym64, E.shard_offsets([Ym64.shape[0]])[0], [Ym64.shape[0]], prec)
-        Ym = Sm.Y
-        D0m = init_dictionaries(Sm.exact(), K, init, [seed_merge])
-    else:
-        Ym = E.scale_rows(Dk, wk, K1, prec)
-        Sm = E.ShardSet.single(Ym, prec)
-        D0m = init_dictionaries(Sm, K, init, [seed_merge])
-    Dm, _codes_m, _ = train_device(Sm, D0m, cap2, 0.0, merge_iters, use_tc)
-    return Dm, w_h, Ym.shape[0]
+        return Sm, init_dictionaries(Sm.exact(), K, init, [seed_merge])
+    Sm = E.ShardSet.single(E.scale_rows(Dk, wk, K1, prec), prec)
+    return Sm, init_dictionaries(Sm, K, init, [seed_merge])
 
 
 def split_merge_device(Ydev: torch.Tensor, L: int, K1: int, local_cap: int, local_eps: float,
@@ -724,6 +743,10 @@ def train_split_merge(Y, cfg: TrainConfig, evaluate: bool = True) -> tuple[np.nd
         codes = E.code_single_dict(Ydev, r.D_dev, cap_e, 0.0, prec)
         mse = mse_db_device(S, codes, r.D_dev)
     report = TrainReport(final_mse_db=mse, wall_time_s=r.wall_s,
+                         # the L locals run concurrently in one batched launch sequence: they
+                         # start and finish together, so each local's wall time is the local
+                         # phase's (the reference's pool workers each report their own; here
+                         # there is no per-shard timeline to report)
                          split_time_s=r.split_s, local_wall_times_s=[r.local_s] * cfg.L,
                          merge_wall_time_s=r.merge_s,
                          critical_path_s=r.split_s + r.local_s + r.merge_s)

@@ -1,0 +1,5 @@
+timeout 900 python -m pytest tests -q -m gpu --timeout 900 --deselect tests/test_gpu_parity_configs.py > gpurun_out/gputest2.log 2>&1; echo all rc=$?
+timeout 2400 python -m pytest tests/test_gpu_parity_configs.py -q --timeout 2000 > gpurun_out/t_parity.log 2>&1; echo parity rc=$?
+timeout 900 python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/bench_cert.json 2> gpurun_out/bench_cert.err; echo bench rc=$?
+timeout 600 python tools/cert_probe.py > gpurun_out/cert_probe.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:k_certify -s 2 -c 1 -o gpurun_out/prof_cert python tools/cert_probe.py > gpurun_out/ncu_cert.log 2>&1; echo ncu rc=$?
