@@ -6,8 +6,9 @@ MOD update and atom replacement, standard / local / merge / split-merge
 training, the denoising pipeline and mse_db. All arithmetic runs in
 libsdb200.so (hand-written CUDA for sm_100a behind a C ABI); there is no CPU
 fallback. The sparse-model generators (synthesis) are included, with an
-on-device variant. Out of scope: PGM I/O, the cost model
-and bench harness.
+on-device variant, and the reference's file formats (storage: SDICT, SDATA,
+PGM) and command line (cli: gen / train / denoise / eval). Out of scope
+(DESIGN.md): the cost model and the bench sweep harness.
 """
 
 __version__ = "0.1.0"
@@ -51,6 +52,7 @@ from .denoising import (
 )
 from .metrics import atom_recovery, mse_db, psnr
 from .synthesis import gen_dictionary, gen_signals, gen_signals_device
+from .storage import load_dictionary, load_dataset, load_pgm, save_dataset, save_dictionary, save_pgm
 
 __all__ = [
     "get_precision", "set_precision",
@@ -65,4 +67,5 @@ __all__ = [
     "overcomplete_dct", "reconstruct_from_patches",
     "atom_recovery", "mse_db", "psnr",
     "gen_dictionary", "gen_signals", "gen_signals_device",
+    "load_dictionary", "load_dataset", "load_pgm", "save_dataset", "save_dictionary", "save_pgm",
 ]
