@@ -276,6 +276,91 @@ k_normal_eq(int P, int K, int m, const T* __restrict__ Y, int64_t ldy, const int
     }
 }
 
+// ---- (f+g), one warp per (shard, atom) bucket: the same two rows as
+// k_normal_eq, for launches with enough buckets to fill the GPU with warps
+// (P K >= 148 x 32). The warp walks its bucket's 32-entry batches in order
+// (four Y rows in flight per batch), keeps its lanes' Y X^T columns in
+// registers and its X X^T row in a private shared-memory row, so there is no
+// cross-warp combine and no block barrier; the summation order is fixed by
+// the bucket order (deterministic).
+template <typename T, int MPL>
+__global__ void __launch_bounds__(256)
+k_normal_eq_w(int64_t PK, int K, int m, const T* __restrict__ Y, int64_t ldy,
+              const int64_t* __restrict__ bucket_off, int cap, const int32_t* __restrict__ idx,
+              const T* __restrict__ val, const int32_t* __restrict__ counts, const int32_t* __restrict__ bent,
+              double* __restrict__ B, double* __restrict__ A) {
+    extern __shared__ double sh_rows[];  // 8 warps x K
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t e = (int64_t)blockIdx.x * 8 + wib;  // (p, a)
+    if (e >= PK) return;
+    const int self = (int)(e % K);
+    double* row = sh_rows + (int64_t)wib * K;
+    for (int b = lane; b < K; b += 32) row[b] = 0.0;
+    __syncwarp();
+    double acc[MPL];
+#pragma unroll
+    for (int q = 0; q < MPL; ++q) acc[q] = 0.0;
+    double diag = 0.0;
+    const int64_t lo = bucket_off[e], hi = bucket_off[e + 1];
+    for (int64_t b0 = lo; b0 < hi; b0 += 32) {
+        const int nbat = (int)min((int64_t)32, hi - b0);
+        const int my_e = lane < nbat ? bent[b0 + lane] : 0;
+        const int my_sig = my_e / cap;
+        const double my_val = lane < nbat ? (double)val[my_e] : 0.0;
+        const int my_n = lane < nbat ? counts[my_sig] : 0;
+        for (int j = 0; j < nbat; j += 4) {
+            double yv[4][MPL];
+            double vv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = __shfl_sync(SDB_FULL, my_sig, (j + u) & 31);
+                vv[u] = __shfl_sync(SDB_FULL, my_val, (j + u) & 31);
+                const T* y = Y + (int64_t)i * ldy;
+#pragma unroll
+                for (int q = 0; q < MPL; ++q) {
+                    const int r = lane + 32 * q;
+                    yv[u][q] = (j + u < nbat && r < m) ? (double)y[r] : 0.0;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int q = 0; q < MPL; ++q) acc[q] = fma(yv[u][q], vv[u], acc[q]);
+        }
+        diag += warp_sum(my_val * my_val);
+        const int my_no = my_n > 1 ? my_n : 0;
+        const int nmax = (int)__reduce_max_sync(SDB_FULL, (unsigned)my_no);
+        for (int t = 0; t < nmax; ++t) {
+            int b = -1;
+            double c = 0.0;
+            if (t < my_no) {
+                b = idx[(int64_t)my_sig * cap + t];
+                c = my_val * (double)val[(int64_t)my_sig * cap + t];
+                if (b == self) b = -1;
+            }
+            const bool act = b >= 0;
+            const unsigned peers = __match_any_sync(SDB_FULL, act ? b : K + lane);
+            const int rank = __popc(peers & ((1u << lane) - 1u));
+            const int gmax = (int)__reduce_max_sync(SDB_FULL, act ? (unsigned)__popc(peers) : 0u);
+            for (int r = 0; r < gmax; ++r) {
+                if (act && rank == r) row[b] += c;
+                __syncwarp();
+            }
+        }
+        __syncwarp();
+    }
+    if (lane == 0) row[self] += diag;
+    __syncwarp();
+    double* outB = B + e * m;
+#pragma unroll
+    for (int q = 0; q < MPL; ++q) {
+        const int r = lane + 32 * q;
+        if (r < m) outB[r] = acc[q];
+    }
+    double* outA = A + e * K;
+    for (int b = lane; b < K; b += 32) outA[b] = row[b];
+}
+
 // ---- per-signal residual ||y_i - D_p x_i||^2 (D in f64, atom-major). With
 // `only_if`, shards whose flag is 0 are skipped; if no shard is flagged the
 // whole (grid-stride) launch exits after reading the P flags.
@@ -754,6 +839,17 @@ int mod_update(const ModArgs<T>& a, cudaStream_t st) {
     }
     rc = with_mpl(m, [&](auto c) {
         constexpr int MPL = decltype(c)::value;
+        if (PK >= (int64_t)148 * 32) {
+            // enough buckets for a warp each
+            const int smem = 8 * K * (int)sizeof(double);
+            if (smem > 48 * 1024) {
+                cudaError_t e = set_max_smem((const void*)k_normal_eq_w<T, MPL>, smem);
+                if (e != cudaSuccess) return (int)e;
+            }
+            k_normal_eq_w<T, MPL><<<(unsigned)((PK + 7) / 8), 256, smem, st>>>(
+                PK, K, m, a.Y, a.ldy, w.bucket_off, cap, a.idx, a.val, a.counts, w.bent, w.B, w.A);
+            return (int)cudaGetLastError();
+        }
         const int smem = 8 * (K + 32 * MPL) * (int)sizeof(double);
         if (smem > 48 * 1024) {
             cudaError_t e = set_max_smem((const void*)k_normal_eq<T, MPL>, smem);

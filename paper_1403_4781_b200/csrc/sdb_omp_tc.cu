@@ -10,7 +10,7 @@
 // Precision. The MMA is kind::tf32 (operands truncated to 10-bit mantissas,
 // fp32 accumulation), so |corr_tf32 - d.r| <= 2^-9 ||d|| ||r|| (+ 2^-16 ||r||
 // accumulation). The argmax is decided exactly: every atom whose TF32 value
-// lies within a window (2^-7 ||r||, twice the bound, plus 1e-6 ||y|| for the
+// lies within a window (2^-8 ||r||, twice the bound, plus 1e-6 ||y|| for the
 // numerical residue of support atoms) of the TF32 maximum is a candidate, and
 // the candidates' correlations are recomputed in FP32 on the CUDA cores from
 // the resident dictionary and the exact residual (both in shared memory);
@@ -67,7 +67,7 @@ constexpr int OT_N = 256;          // atoms per MMA chunk (UMMA N)
 constexpr int OT_NGRP = 2;         // signal groups (tiles in flight per CTA)
 constexpr int OT_WARPS = 2 + 4 * OT_NGRP;
 constexpr int OT_CMAX = 6;         // candidates refined per step before the exact sweep
-constexpr float OT_WIN = 0.0078125f;   // 2^-7: candidate window, relative to ||r||
+constexpr float OT_WIN = 0.00390625f;   // 2^-8: candidate window, relative to ||r||
 constexpr int OT_RB = OT_M * 128;  // bytes of one 32-column k-block of R
 
 struct OtArgs {

@@ -31,10 +31,11 @@ def test_gen_train_eval_denoise(tmp_path, capsys):
     assert json.loads((tmp_path / "t" / "manifest.json").read_text())["command"] == "train"
     D2, _ = sdb.train_split_merge(Y, sdb.TrainConfig.from_dict(dict(conf)))
     assert np.array_equal(D, D2)
+    capsys.readouterr()
     assert cli.main(["eval", "--dict", str(tmp_path / "t" / "dictionary.sdict"), "--truth-dict",
                      str(tmp_path / "g" / "truth_dictionary.sdict"), "--data",
                      str(tmp_path / "g" / "training_set.sdata"), "--sparsity", "3"]) == 0
-    res = json.loads(capsys.readouterr().out.split("\n", 1)[1])
+    res = json.loads(capsys.readouterr().out)
     assert "atom_recovery_pct" in res and "mse_db" in res
     # denoise a small synthetic image with an overcomplete DCT dictionary
     rng = np.random.default_rng(0)
