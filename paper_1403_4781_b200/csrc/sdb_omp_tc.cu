@@ -429,17 +429,6 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
                     }
                     if (act) {
                         // ---------------- exact selection among the candidates
-                        // the first candidate is usually the winner: its G row
-                        // entries (L2 / HBM latency) are requested before the
-                        // refinement and used if it wins
-                        const int spec = (nc >= 1) ? cand[0] : 0;
-                        float gbb_s, gb_s[CAP];
-                        {
-                            const float* __restrict__ Gs = Gp + (int64_t)spec * K;
-                            gbb_s = __ldg(Gs + spec);
-#pragma unroll
-                            for (int t = 0; t < CAP; ++t) gb_s[t] = (t < n) ? __ldg(Gs + ids[t]) : 0.f;
-                        }
                         float best = -1.f, second = -1.f, eb = 0.f;
                         int bj = -1;
                         auto consider = [&](int j) {
@@ -470,15 +459,11 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
                             act = false;
                         } else {
                             // ---------------- Cholesky append (_kernels.py:109-127)
-                            float gbb = gbb_s, gb[CAP];
+                            const float* __restrict__ Gb = Gp + (int64_t)bj * K;
+                            const float gbb = __ldg(Gb + bj);
+                            float gb[CAP];
 #pragma unroll
-                            for (int t = 0; t < CAP; ++t) gb[t] = gb_s[t];
-                            if (bj != spec) {
-                                const float* __restrict__ Gb = Gp + (int64_t)bj * K;
-                                gbb = __ldg(Gb + bj);
-#pragma unroll
-                                for (int t = 0; t < CAP; ++t) gb[t] = (t < n) ? __ldg(Gb + ids[t]) : 0.f;
-                            }
+                            for (int t = 0; t < CAP; ++t) gb[t] = (t < n) ? __ldg(Gb + ids[t]) : 0.f;
                             float c0b = eb;   // d_b.y = d_b.r + G[b,S] x
 #pragma unroll
                             for (int t = 0; t < CAP; ++t) c0b = fmaf(gb[t], x[t], c0b);
