@@ -49,6 +49,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 
 #include "sdb_common.cuh"
@@ -64,8 +65,7 @@ namespace {
 
 constexpr int OT_M = 128;          // signals per tile (UMMA M, TMEM lanes)
 constexpr int OT_N = 256;          // atoms per MMA chunk (UMMA N)
-constexpr int OT_NGRP = 2;         // signal groups (tiles in flight per CTA)
-constexpr int OT_WARPS = 2 + 4 * OT_NGRP;
+constexpr int OT_NGMAX = 3;        // signal groups (tiles in flight per CTA): 2, or 3 when K > 256
 constexpr int OT_CMAX = 6;         // candidates refined per step before the exact sweep
 constexpr float OT_WIN = 0.00390625f;   // 2^-8: candidate window, relative to ||r||
 constexpr int OT_RB = OT_M * 128;  // bytes of one 32-column k-block of R
@@ -100,9 +100,11 @@ __device__ __forceinline__ int tile_shard(const int64_t* __restrict__ ts, int P,
 struct Round {
     int p;
     int64_t t0;
-    bool has1, first, last;
+    int cnt;            // tiles in this round (1..NG), one per signal group
+    bool first, last;
 };
 
+template <int NG>
 struct RoundIter {
     const int64_t* ts;
     int P;
@@ -113,8 +115,9 @@ struct RoundIter {
         r.p = tile_shard(ts, P, pos);
         const int64_t pend = __ldg(ts + r.p + 1);
         r.t0 = pos;
-        r.has1 = pos + 1 < end && pos + 1 < pend;
-        pos += r.has1 ? 2 : 1;
+        const int64_t lim = min(end, pend);
+        r.cnt = (int)min((int64_t)NG, lim - pos);
+        pos += r.cnt;
         r.first = r.p != prev;
         prev = r.p;
         r.last = pos >= end || pos >= pend;
@@ -124,19 +127,21 @@ struct RoundIter {
 
 __device__ __forceinline__ float4 lds4(const unsigned char* p) { return *reinterpret_cast<const float4*>(p); }
 
-template <int CAP>
-__global__ void __launch_bounds__(OT_WARPS * 32, 1)
+template <int CAP, int NG>
+__global__ void __launch_bounds__((2 + 4 * NG) * 32, 1)
 k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
+    // barriers: full[g] (MMA done / tile end ack), empty[b] (TMEM chunk buffer
+    // free), rfull[g] (residual published), dfull (dictionary landed), dfree
+    constexpr int B_FULL = 0, B_EMPTY = NG, B_RFULL = NG + 2, B_DFULL = 2 * NG + 2, B_DFREE = 2 * NG + 3;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* base = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     const int dbytes = a.nkb * a.kpad * 128;
     const int rbytes = a.nkb * OT_RB;
     unsigned char* Ds = base;
-    uint64_t* bars = (uint64_t*)(base + dbytes + OT_NGRP * rbytes);
-    // full[g] 0..1, empty[b] 2..3, rfull[g] 4..5, dfull 6, dfree 7
-    int* votes = (int*)(bars + 8);            // [step parity][group][warp]
-    volatile int* contf = votes + 16;         // [group]
-    uint32_t* tslot = (uint32_t*)(votes + 20);
+    uint64_t* bars = (uint64_t*)(base + dbytes + NG * rbytes);
+    int* votes = (int*)(bars + 2 * NG + 4);   // [step parity][group][warp]
+    volatile int* contf = votes + 8 * NG;     // [group]
+    uint32_t* tslot = (uint32_t*)(votes + 9 * NG);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int K = a.K;
 
@@ -146,13 +151,13 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
     const int64_t te = min(ntiles, tb + per);
 
     if (threadIdx.x == 0) {
-        for (int g = 0; g < 2; ++g) {
-            mbar_init(smem_u32(&bars[g]), 1);
-            mbar_init(smem_u32(&bars[2 + g]), 4);
-            mbar_init(smem_u32(&bars[4 + g]), 4);
+        for (int g = 0; g < NG; ++g) {
+            mbar_init(smem_u32(&bars[B_FULL + g]), 1);
+            mbar_init(smem_u32(&bars[B_RFULL + g]), 4);
         }
-        mbar_init(smem_u32(&bars[6]), 1);
-        mbar_init(smem_u32(&bars[7]), 4 * OT_NGRP);
+        for (int b = 0; b < 2; ++b) mbar_init(smem_u32(&bars[B_EMPTY + b]), 4);
+        mbar_init(smem_u32(&bars[B_DFULL]), 1);
+        mbar_init(smem_u32(&bars[B_DFREE]), 4 * NG);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -169,13 +174,13 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
     if (warp == 0) {
         // ------------------------------------------------ dictionary producer
         if (lane == 0) {
-            RoundIter it{a.ts, a.P, tb, te, -1};
+            RoundIter<NG> it{a.ts, a.P, tb, te, -1};
             Round r;
             int k = 0;
             while (it.next(r)) {
                 if (!r.first) continue;
-                if (k > 0) mbar_wait(smem_u32(&bars[7]), (uint32_t)((k - 1) & 1));
-                const uint32_t bf = smem_u32(&bars[6]);
+                if (k > 0) mbar_wait(smem_u32(&bars[B_DFREE]), (uint32_t)((k - 1) & 1));
+                const uint32_t bf = smem_u32(&bars[B_DFULL]);
                 mbar_expect_tx(bf, (uint32_t)dbytes);
                 for (int kb = 0; kb < a.nkb; ++kb)
                     for (int c = 0; c < a.nch; ++c)
@@ -189,32 +194,36 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
         if (lane == 0) {
             const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(OT_N >> 3) << 17) |
                                    ((uint32_t)(OT_M >> 4) << 24);
-            uint32_t uses[2] = {0, 0}, rph[2] = {0, 0};
+            uint32_t uses[2] = {0, 0}, rph[NG];
+            for (int g = 0; g < NG; ++g) rph[g] = 0;
             int k = 0;
-            RoundIter it{a.ts, a.P, tb, te, -1};
+            RoundIter<NG> it{a.ts, a.P, tb, te, -1};
             Round r;
             while (it.next(r)) {
                 if (r.first) {
-                    mbar_wait(smem_u32(&bars[6]), (uint32_t)(k & 1));
+                    mbar_wait(smem_u32(&bars[B_DFULL]), (uint32_t)(k & 1));
                     ++k;
                 }
-                bool act[2] = {true, r.has1};
-                while (act[0] || act[1]) {
-                    for (int g = 0; g < 2; ++g) {
+                bool act[NG];
+                int nact = r.cnt;
+                for (int g = 0; g < NG; ++g) act[g] = g < r.cnt;
+                while (nact > 0) {
+                    for (int g = 0; g < NG; ++g) {
                         if (!act[g]) continue;
-                        mbar_wait(smem_u32(&bars[4 + g]), rph[g] & 1u);
+                        mbar_wait(smem_u32(&bars[B_RFULL + g]), rph[g] & 1u);
                         ++rph[g];
                         if (!contf[g]) {
                             // tile done: acknowledge on full[g] so the group cannot
                             // publish its next tile before this phase was consumed
-                            mbar_arrive(smem_u32(&bars[g]));
+                            mbar_arrive(smem_u32(&bars[B_FULL + g]));
                             act[g] = false;
+                            --nact;
                             continue;
                         }
                         const unsigned char* Rg = base + dbytes + g * rbytes;
                         for (int c = 0; c < a.nch; ++c) {
-                            const int b = a.nch == 2 ? c : g;
-                            if (uses[b]) mbar_wait(smem_u32(&bars[2 + b]), (uses[b] - 1) & 1u);
+                            const int b = a.nch == 2 ? c : (g & 1);
+                            if (uses[b]) mbar_wait(smem_u32(&bars[B_EMPTY + b]), (uses[b] - 1) & 1u);
                             ++uses[b];
                             tmem_fence_after();
                             const uint32_t tacc = tmem + (uint32_t)(b * OT_N);
@@ -227,7 +236,7 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
                                              (kb | kk) ? 1u : 0u);
                             }
                         }
-                        mma_commit(smem_u32(&bars[g]));
+                        mma_commit(smem_u32(&bars[B_FULL + g]));
                     }
                 }
             }
@@ -245,7 +254,7 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
         uint32_t fph = 0;
         int sp = 0;
         int k = 0;
-        RoundIter it{a.ts, a.P, tb, te, -1};
+        RoundIter<NG> it{a.ts, a.P, tb, te, -1};
         Round rd;
         auto rrow = [&](int kb, int cc) -> unsigned char* { return R + kb * OT_RB + row * 128 + ((cc ^ swz) << 4); };
         const uint32_t ds_u32 = smem_u32(Ds);
@@ -272,25 +281,25 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
         auto publish = [&](bool want) -> int {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // R writes -> MMA (async proxy)
             const unsigned bal = __ballot_sync(SDB_FULL, want);
-            if (lane == 0) votes[sp * 8 + g * 4 + wi] = bal != 0u;
+            int* vs = votes + (sp * NG + g) * 4;
+            if (lane == 0) vs[wi] = bal != 0u;
             asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
-            const int c = votes[sp * 8 + g * 4] | votes[sp * 8 + g * 4 + 1] | votes[sp * 8 + g * 4 + 2] |
-                          votes[sp * 8 + g * 4 + 3];
+            const int c = vs[0] | vs[1] | vs[2] | vs[3];
             sp ^= 1;
             __syncwarp();
             if (lane == 0) {
                 if (wi == 0) contf[g] = c;
-                mbar_arrive(smem_u32(&bars[4 + g]));
+                mbar_arrive(smem_u32(&bars[B_RFULL + g]));
             }
             return c;
         };
 
         while (it.next(rd)) {
             if (rd.first) {
-                mbar_wait_sleep(smem_u32(&bars[6]), (uint32_t)(k & 1));   // the shard's dictionary landed
+                mbar_wait_sleep(smem_u32(&bars[B_DFULL]), (uint32_t)(k & 1));   // the shard's dictionary landed
                 ++k;
             }
-            if (g == 0 || rd.has1) {
+            if (g < rd.cnt) {
                 const int p = rd.p;
                 const int64_t tile = rd.t0 + g;
                 const int64_t row0 = __ldg(a.off + p) + (tile - __ldg(a.ts + p)) * OT_M;
@@ -347,7 +356,7 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
 
                 int cont = publish(act);
                 while (cont) {
-                    mbar_wait_sleep(smem_u32(&bars[g]), fph & 1u);
+                    mbar_wait_sleep(smem_u32(&bars[B_FULL + g]), fph & 1u);
                     ++fph;
                     tmem_fence_after();
                     // ---------------- scan: candidates within the window of the TF32 max
@@ -367,20 +376,20 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
                             bm[2 * bp] = 0.f;
                             bm[2 * bp + 1] = 0.f;
                             if (c < a.nch && j0 < K) {
-                                uint32_t va[32], vb[32];
-                                const uint32_t col = (uint32_t)((a.nch == 2 ? c : g) * OT_N + (bp & 3) * 64);
-                                tmem_ld64(va, vb, trow + col);
-                                tmem_wait_ld();
-                                float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f;
+                                uint32_t va[32];
+                                const uint32_t col = (uint32_t)((a.nch == 2 ? c : (g & 1)) * OT_N + (bp & 3) * 64);
 #pragma unroll
-                                for (int t = 0; t < 32; t += 2) {
-                                    m0 = fmaxf(m0, fabsf(__uint_as_float(va[t])));
-                                    m1 = fmaxf(m1, fabsf(__uint_as_float(va[t + 1])));
-                                    m2 = fmaxf(m2, fabsf(__uint_as_float(vb[t])));
-                                    m3 = fmaxf(m3, fabsf(__uint_as_float(vb[t + 1])));
+                                for (int hh = 0; hh < 2; ++hh) {
+                                    tmem_ld32(va, trow + col + (uint32_t)(32 * hh));
+                                    tmem_wait_ld();
+                                    float m0 = 0.f, m1 = 0.f;
+#pragma unroll
+                                    for (int t = 0; t < 32; t += 2) {
+                                        m0 = fmaxf(m0, fabsf(__uint_as_float(va[t])));
+                                        m1 = fmaxf(m1, fabsf(__uint_as_float(va[t + 1])));
+                                    }
+                                    bm[2 * bp + hh] = fmaxf(m0, m1);
                                 }
-                                bm[2 * bp] = fmaxf(m0, m1);
-                                bm[2 * bp + 1] = fmaxf(m2, m3);
                             }
                         }
                         float cmax = 0.f;
@@ -396,7 +405,7 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
                                 const bool mine = bm[blk] >= thr;
                                 if (__any_sync(SDB_FULL, mine)) {
                                     uint32_t v[32];
-                                    const uint32_t col = (uint32_t)((a.nch == 2 ? c : g) * OT_N + (blk & 7) * 32);
+                                    const uint32_t col = (uint32_t)((a.nch == 2 ? c : (g & 1)) * OT_N + (blk & 7) * 32);
                                     tmem_ld32(v, trow + col);
                                     tmem_wait_ld();
                                     if (mine) {
@@ -425,7 +434,7 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
                     tmem_fence_before();
                     __syncwarp();
                     if (lane == 0) {
-                        for (int c = 0; c < a.nch; ++c) mbar_arrive(smem_u32(&bars[2 + (a.nch == 2 ? c : g)]));
+                        for (int c = 0; c < a.nch; ++c) mbar_arrive(smem_u32(&bars[B_EMPTY + (a.nch == 2 ? c : (g & 1))]));
                     }
                     if (act) {
                         // ---------------- exact selection among the candidates
@@ -558,7 +567,7 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
                     cont = publish(act);
                 }
                 // the MMA issuer's acknowledgement of the tile end
-                mbar_wait_sleep(smem_u32(&bars[g]), fph & 1u);
+                mbar_wait_sleep(smem_u32(&bars[B_FULL + g]), fph & 1u);
                 ++fph;
                 // ---- codes in selection order (entries >= n zeroed like the reference)
                 if (valid) {
@@ -581,7 +590,7 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
                 // this group no longer reads the shard's dictionary
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
-                if (lane == 0) mbar_arrive(smem_u32(&bars[7]));
+                if (lane == 0) mbar_arrive(smem_u32(&bars[B_DFREE]));
             }
         }
     }
@@ -648,17 +657,22 @@ int omp_tc_f32(int64_t N, int m, int K, int P, const int64_t* off, const float* 
     a.N = N; a.m = m; a.K = K; a.P = P; a.cap = cap; a.nkb = m_pad / 32; a.nch = nch; a.kpad = kpad;
     a.off = off; a.ts = ts; a.Y = Y; a.ldy = ldy; a.G = G; a.eps = eps; a.guard = guard;
     a.idx = idx; a.val = val; a.counts = counts; a.status = status; a.rnorm = rnorm; a.gap = gap;
-    const int smem = 1024 + a.nkb * kpad * 128 + OT_NGRP * a.nkb * OT_RB + 256;
+    // three signal groups when K > 256 (the groups share both TMEM chunk
+    // buffers anyway) and the residual tiles fit next to the dictionary
+    const int smem3 = 1024 + a.nkb * kpad * 128 + 3 * a.nkb * OT_RB + 256;
+    const bool three = nch == 2 && smem3 <= 232448 && !getenv("SDB_OMP_TC_2GRP");
+    const int ng = three ? 3 : 2;
+    const int smem = 1024 + a.nkb * kpad * 128 + ng * a.nkb * OT_RB + 256;
     int dev = 0;
     cudaGetDevice(&dev);
     int n_sm = 148;
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    auto fn = cap <= 4 ? k_omp_tc<4> : k_omp_tc<8>;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    auto fn = three ? (cap <= 4 ? k_omp_tc<4, 3> : k_omp_tc<8, 3>) : (cap <= 4 ? k_omp_tc<4, 2> : k_omp_tc<8, 2>);
+    cudaError_t e = set_max_smem((const void*)fn, smem);
     if (e != cudaSuccess) return (int)e;
     const int64_t max_tiles = (N + OT_M - 1) / OT_M + P;
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(n_sm, max_tiles));
-    fn<<<grid, OT_WARPS * 32, smem, st>>>(mD, a);
+    fn<<<grid, (2 + 4 * ng) * 32, smem, st>>>(mD, a);
     return (int)cudaGetLastError();
 }
 
