@@ -657,10 +657,13 @@ int omp_tc_f32(int64_t N, int m, int K, int P, const int64_t* off, const float* 
     a.N = N; a.m = m; a.K = K; a.P = P; a.cap = cap; a.nkb = m_pad / 32; a.nch = nch; a.kpad = kpad;
     a.off = off; a.ts = ts; a.Y = Y; a.ldy = ldy; a.G = G; a.eps = eps; a.guard = guard;
     a.idx = idx; a.val = val; a.counts = counts; a.status = status; a.rnorm = rnorm; a.gap = gap;
-    // three signal groups when K > 256 (the groups share both TMEM chunk
-    // buffers anyway) and the residual tiles fit next to the dictionary
+    // three signal groups are possible when K > 256 (the groups share both
+    // TMEM chunk buffers anyway) and the residual tiles fit next to the
+    // dictionary; measured no faster than two at C4 (the tile-steps serialise
+    // on the TMEM accumulator, and 128 registers spill), so opt-in only
     const int smem3 = 1024 + a.nkb * kpad * 128 + 3 * a.nkb * OT_RB + 256;
-    const bool three = nch == 2 && smem3 <= 232448 && !getenv("SDB_OMP_TC_2GRP");
+    static const bool want3 = getenv("SDB_OMP_TC_3GRP") != nullptr;
+    const bool three = want3 && nch == 2 && smem3 <= 232448;
     const int ng = three ? 3 : 2;
     const int smem = 1024 + a.nkb * kpad * 128 + ng * a.nkb * OT_RB + 256;
     int dev = 0;
