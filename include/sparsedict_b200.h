@@ -36,6 +36,9 @@ extern "C" {
 
 #define SDB_F32 0
 #define SDB_F64 1
+/* sdb_mod_update only: FP32 signal rows with FP64 code values (certified FP32
+ * mode; the rows' values are exact in FP64 and all arithmetic is FP64) */
+#define SDB_F32X 2
 
 #define SDB_OK 0
 #define SDB_EINVAL (-22)

@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import SDB_F32, SDB_F64
+from ._lib import SDB_F32, SDB_F32X, SDB_F64
 
 PRECISIONS = ("fp64", "fp32")
 # Singular-support guard on the Cholesky pivot (_kernels.py:18). FP64 keeps the
@@ -575,16 +575,25 @@ def _for_codes(S: "ShardSet", codes: DeviceCodes) -> "ShardSet":
 
 
 def mod_update(S: ShardSet, codes: DeviceCodes, D64: torch.Tensor) -> ModResult:
+    Yrows = None
+    if codes.vprec == "fp64" and S.prec == "fp32" and not S._exact_auth:
+        # certified FP32: the FP32 rows hold the exact values of the FP64
+        # copy -- read them (half the gather bytes), compute in FP64
+        Yrows = S.Y
     S = _for_codes(S, codes)
     P, K, m = D64.shape
-    dt = sdb_dtype(S.prec)
+    dt = sdb_dtype(S.prec) if Yrows is None else SDB_F32X
     r = ModResult(empty((P, K, m), torch.float64), empty((P, K), torch.float64),
                   empty((P, K), torch.int32), empty((P, K), torch.int8),
                   empty((P,), torch.float64), empty((P,), torch.int32), empty((P,), torch.int32))
     wsb = _lib.load().sdb_mod_workspace_bytes(P, S.N, m, K, codes.cap)
     ws = empty((wsb,), torch.uint8)
     es = 8 if S.prec == "fp64" else 4
-    timed_call("mod_update", S.N * (2 * m * es + codes.cap * (4 + es) + 4), 0.0, "sdb_mod_update", dt, P, S.N, m, K, codes.cap, ptr(S.off), ptr(S.Y), m,
+    if Yrows is not None:
+        es = 4
+    vb = 8 if (codes.vprec == "fp64" or S.prec == "fp64") else 4
+    timed_call("mod_update", S.N * (2 * m * es + codes.cap * (4 + vb) + 4), 0.0, "sdb_mod_update", dt, P, S.N, m, K,
+               codes.cap, ptr(S.off), ptr(S.Y if Yrows is None else Yrows), m,
               ptr(codes.idx), ptr(codes.val), ptr(codes.counts), ptr(D64), ptr(r.D),
               ptr(r.scales), ptr(r.usage), ptr(r.dead), ptr(r.resid), ptr(r.rank),
               ptr(r.deficient), RANK_RCOND, ptr(S.energy()), ptr(ws), wsb, stream())

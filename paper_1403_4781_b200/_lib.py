@@ -14,7 +14,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 LIB_PATH = PKG / "libsdb200.so"
 
-SDB_F32, SDB_F64 = 0, 1
+SDB_F32, SDB_F64, SDB_F32X = 0, 1, 2
 
 c_i64 = ctypes.c_int64
 c_int = ctypes.c_int
@@ -101,7 +101,7 @@ class NativeError(RuntimeError):
 
 _lib = None
 # must equal sdb_abi_version() in csrc/sdb_capi.cu (bumped whenever exports change)
-ABI_VERSION = 9
+ABI_VERSION = 10
 
 
 def load():

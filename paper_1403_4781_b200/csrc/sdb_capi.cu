@@ -55,7 +55,7 @@ __global__ void k_cast(int64_t n, const double* __restrict__ src, T* __restrict_
 
 extern "C" {
 
-int sdb_abi_version(void) { return 9; }
+int sdb_abi_version(void) { return 10; }
 const char* sdb_last_error(void) { return g_err.c_str(); }
 
 int sdb_device_cc(void) {
@@ -338,7 +338,10 @@ int sdb_mod_update(int dtype, int64_t P, int64_t N, int64_t m, int64_t K, int64_
                    double* scales, int32_t* usage, int8_t* dead, double* resid_fro, int32_t* rank,
                    int32_t* deficient, double rank_rcond, const double* ysq_shard, void* ws,
                    int64_t ws_bytes, void* stream) {
-    if (!dtype_ok(dtype) || P < 1 || N < 0 || m < 1 || m > 256 || K < 1 || K > 1024 || cap < 1 || ldy < m)
+    // dtype SDB_F32X: FP32 signal rows with FP64 code values (certified FP32
+    // mode; the rows' values are exact, the arithmetic is FP64)
+    if (!(dtype_ok(dtype) || dtype == SDB_F32X) || P < 1 || N < 0 || m < 1 || m > 256 || K < 1 || K > 1024 ||
+        cap < 1 || ldy < m)
         return fail(SDB_EINVAL, "sdb_mod_update: bad args (m <= 256, K <= 1024)");
     if (N * cap > 0x7fffffffll)  // bucket entries are 32-bit flat code indices
         return fail(SDB_EINVAL, "sdb_mod_update: N * cap = %lld exceeds 2^31 - 1", (long long)(N * cap));
@@ -352,9 +355,12 @@ int sdb_mod_update(int dtype, int64_t P, int64_t N, int64_t m, int64_t K, int64_
         a.counts = counts; a.Dprev = D_prev; a.Dout = D_out; a.scales = scales; a.usage = usage;
         a.dead = dead; a.resid_fro = resid_fro; a.rank = rank; a.deficient_out = deficient;
         a.nnz_out = nullptr; a.rank_rcond = rank_rcond; a.ysq_shard = ysq_shard; a.ws = ws;
+        if constexpr (std::is_same_v<T, double>) {
+            if (dtype == SDB_F32X) { a.Y = nullptr; a.Yf = (const float*)Y; }
+        }
         return sdb::mod_update<T>(a, S(stream));
     };
-    int rc = dtype == SDB_F64 ? go((double*)nullptr) : go((float*)nullptr);
+    int rc = (dtype == SDB_F64 || dtype == SDB_F32X) ? go((double*)nullptr) : go((float*)nullptr);
     return cuda_rc(rc, "sdb_mod_update");
 }
 

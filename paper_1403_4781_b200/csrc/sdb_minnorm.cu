@@ -57,9 +57,9 @@ __device__ double block_max_diag(const double* A, int K, double* s_red) {
     return v;
 }
 
-template <typename T>
+template <typename TY, typename T>
 __global__ void __launch_bounds__(MN_THREADS, 1)
-k_minnorm(int P, int K, int m, const T* __restrict__ Y, int64_t ldy, int cap, const int32_t* __restrict__ idx,
+k_minnorm(int P, int K, int m, const TY* __restrict__ Y, int64_t ldy, int cap, const int32_t* __restrict__ idx,
           const T* __restrict__ val, const int32_t* __restrict__ counts, const int64_t* __restrict__ bucket_off,
           const int32_t* __restrict__ bent, const int32_t* __restrict__ usage, double rcond,
           double* __restrict__ Aall, double* __restrict__ Ball, int32_t* __restrict__ deficient,
@@ -103,7 +103,7 @@ k_minnorm(int P, int K, int m, const T* __restrict__ Y, int64_t ldy, int cap, co
                         Ar[b] += xa * (double)val[i * cap + lane];   // distinct b per lane
                     }
                     __syncwarp();
-                    const T* y = Y + i * ldy;
+                    const TY* y = Y + i * ldy;
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
                         const int c = lane + 32 * k;
@@ -252,21 +252,24 @@ int64_t minnorm_ws_bytes(int P, int m, int K) {
     return (int64_t)std::min(P, MN_CTAS) * ((int64_t)K * K + (int64_t)K * m) * (int64_t)sizeof(double);
 }
 
-template <typename T>
-int minnorm_solve(int P, int K, int m, const T* Y, int64_t ldy, int cap, const int32_t* idx, const T* val,
+template <typename TY, typename T>
+int minnorm_solve(int P, int K, int m, const TY* Y, int64_t ldy, int cap, const int32_t* idx, const T* val,
                   const int32_t* counts, const int64_t* bucket_off, const int32_t* bent, const int32_t* usage,
                   double rcond, double* A, double* B, int32_t* deficient, double* wsq, double* slots,
                   cudaStream_t st) {
     if (m > 256 || cap > 32) return (int)cudaErrorNotSupported;
-    k_minnorm<T><<<std::min(P, MN_CTAS), MN_THREADS, 0, st>>>(P, K, m, Y, ldy, cap, idx, val, counts, bucket_off,
-                                                              bent, usage, rcond, A, B, deficient, wsq, slots);
+    k_minnorm<TY, T><<<std::min(P, MN_CTAS), MN_THREADS, 0, st>>>(P, K, m, Y, ldy, cap, idx, val, counts,
+                                                                 bucket_off, bent, usage, rcond, A, B, deficient,
+                                                                 wsq, slots);
     return (int)cudaGetLastError();
 }
-template int minnorm_solve<float>(int, int, int, const float*, int64_t, int, const int32_t*, const float*,
-                                  const int32_t*, const int64_t*, const int32_t*, const int32_t*, double, double*,
-                                  double*, int32_t*, double*, double*, cudaStream_t);
-template int minnorm_solve<double>(int, int, int, const double*, int64_t, int, const int32_t*, const double*,
-                                   const int32_t*, const int64_t*, const int32_t*, const int32_t*, double,
-                                   double*, double*, int32_t*, double*, double*, cudaStream_t);
+#define SDB_MN_INST(TY, T)                                                                                     \
+    template int minnorm_solve<TY, T>(int, int, int, const TY*, int64_t, int, const int32_t*, const T*,       \
+                                      const int32_t*, const int64_t*, const int32_t*, const int32_t*, double, \
+                                      double*, double*, int32_t*, double*, double*, cudaStream_t);
+SDB_MN_INST(float, float)
+SDB_MN_INST(double, double)
+SDB_MN_INST(float, double)
+#undef SDB_MN_INST
 
 }  // namespace sdb

@@ -15,6 +15,7 @@
 // identity, which equals the minimum-norm lstsq solution on the used block);
 // D_new = Z^T (atom-major storage == Z row-major).
 #include <cfloat>
+#include <type_traits>
 
 #include "sdb_common.cuh"
 #include "sdb_internal.h"
@@ -187,9 +188,9 @@ k_place(const int64_t* __restrict__ off, const int64_t* __restrict__ cf, int P, 
 // so the X X^T work hides under the Y-row gathers and the bucket is read
 // once. Per-warp partials are combined in warp order: the result is a fixed
 // function of the input (bitwise that of the separate kernels).
-template <typename T, int MPL>
+template <typename TY, typename T, int MPL>
 __global__ void __launch_bounds__(256)
-k_normal_eq(int P, int K, int m, const T* __restrict__ Y, int64_t ldy, const int64_t* __restrict__ bucket_off,
+k_normal_eq(int P, int K, int m, const TY* __restrict__ Y, int64_t ldy, const int64_t* __restrict__ bucket_off,
             int cap, const int32_t* __restrict__ idx, const T* __restrict__ val,
             const int32_t* __restrict__ counts, const int32_t* __restrict__ bent, double* __restrict__ B,
             double* __restrict__ A) {
@@ -220,7 +221,7 @@ k_normal_eq(int P, int K, int m, const T* __restrict__ Y, int64_t ldy, const int
             for (int u = 0; u < 4; ++u) {
                 const int i = __shfl_sync(SDB_FULL, my_sig, (j + u) & 31);
                 vv[u] = __shfl_sync(SDB_FULL, my_val, (j + u) & 31);
-                const T* y = Y + (int64_t)i * ldy;
+                const TY* y = Y + (int64_t)i * ldy;
 #pragma unroll
                 for (int q = 0; q < MPL; ++q) {
                     const int r = lane + 32 * q;
@@ -283,9 +284,9 @@ k_normal_eq(int P, int K, int m, const T* __restrict__ Y, int64_t ldy, const int
 // registers and its X X^T row in a private shared-memory row, so there is no
 // cross-warp combine and no block barrier; the summation order is fixed by
 // the bucket order (deterministic).
-template <typename T, int MPL>
+template <typename TY, typename T, int MPL>
 __global__ void __launch_bounds__(256)
-k_normal_eq_w(int64_t PK, int K, int m, const T* __restrict__ Y, int64_t ldy,
+k_normal_eq_w(int64_t PK, int K, int m, const TY* __restrict__ Y, int64_t ldy,
               const int64_t* __restrict__ bucket_off, int cap, const int32_t* __restrict__ idx,
               const T* __restrict__ val, const int32_t* __restrict__ counts, const int32_t* __restrict__ bent,
               double* __restrict__ B, double* __restrict__ A) {
@@ -315,7 +316,7 @@ k_normal_eq_w(int64_t PK, int K, int m, const T* __restrict__ Y, int64_t ldy,
             for (int u = 0; u < 4; ++u) {
                 const int i = __shfl_sync(SDB_FULL, my_sig, (j + u) & 31);
                 vv[u] = __shfl_sync(SDB_FULL, my_val, (j + u) & 31);
-                const T* y = Y + (int64_t)i * ldy;
+                const TY* y = Y + (int64_t)i * ldy;
 #pragma unroll
                 for (int q = 0; q < MPL; ++q) {
                     const int r = lane + 32 * q;
@@ -364,10 +365,10 @@ k_normal_eq_w(int64_t PK, int K, int m, const T* __restrict__ Y, int64_t ldy,
 // ---- per-signal residual ||y_i - D_p x_i||^2 (D in f64, atom-major). With
 // `only_if`, shards whose flag is 0 are skipped; if no shard is flagged the
 // whole (grid-stride) launch exits after reading the P flags.
-template <typename T, int MPL>
+template <typename TY, typename T, int MPL>
 __global__ void __launch_bounds__(256)
 k_resid_sq(int64_t N, int m, int K, int cap, int P, const int64_t* __restrict__ off,
-           const T* __restrict__ Y, int64_t ldy, const int32_t* __restrict__ idx,
+           const TY* __restrict__ Y, int64_t ldy, const int32_t* __restrict__ idx,
            const T* __restrict__ val, const int32_t* __restrict__ counts,
            const double* __restrict__ D, double* __restrict__ out, double* __restrict__ ysq_out,
            const int32_t* __restrict__ only_if) {
@@ -387,7 +388,7 @@ k_resid_sq(int64_t N, int m, int K, int cap, int P, const int64_t* __restrict__ 
         const int p = shard_of(off, P, i);
         if (only_if && only_if[p] == 0) continue;  // warp-uniform
         const double* Dp = D + (int64_t)p * K * m;
-        const T* y = Y + i * ldy;
+        const TY* y = Y + i * ldy;
         double r[MPL];
         double yy = 0.0;
 #pragma unroll
@@ -811,8 +812,10 @@ int64_t mod_ws_bytes(int P, int64_t N, int m, int K, int cap) {
     return (int64_t)(w.end - (unsigned char*)nullptr) + 256;
 }
 
-template <typename T>
-int mod_update(const ModArgs<T>& a, cudaStream_t st) {
+// TY: the signal rows' type (float rows with FP64 codes in the certified
+// FP32 mode: the values are exactly the FP64 copy's, at half the gather bytes)
+template <typename TY, typename T>
+static int mod_update_impl(const ModArgs<T>& a, const TY* Ysrc, cudaStream_t st) {
     const int P = a.P, K = a.K, m = a.m, cap = a.cap;
     const int64_t N = a.N;
     ModWs w = carve_mod_ws(a.ws, P, N, m, K, cap);
@@ -843,19 +846,19 @@ int mod_update(const ModArgs<T>& a, cudaStream_t st) {
             // enough buckets for a warp each
             const int smem = 8 * K * (int)sizeof(double);
             if (smem > 48 * 1024) {
-                cudaError_t e = set_max_smem((const void*)k_normal_eq_w<T, MPL>, smem);
+                cudaError_t e = set_max_smem((const void*)k_normal_eq_w<TY, T, MPL>, smem);
                 if (e != cudaSuccess) return (int)e;
             }
-            k_normal_eq_w<T, MPL><<<(unsigned)((PK + 7) / 8), 256, smem, st>>>(
-                PK, K, m, a.Y, a.ldy, w.bucket_off, cap, a.idx, a.val, a.counts, w.bent, w.B, w.A);
+            k_normal_eq_w<TY, T, MPL><<<(unsigned)((PK + 7) / 8), 256, smem, st>>>(
+                PK, K, m, Ysrc, a.ldy, w.bucket_off, cap, a.idx, a.val, a.counts, w.bent, w.B, w.A);
             return (int)cudaGetLastError();
         }
         const int smem = 8 * (K + 32 * MPL) * (int)sizeof(double);
         if (smem > 48 * 1024) {
-            cudaError_t e = set_max_smem((const void*)k_normal_eq<T, MPL>, smem);
+            cudaError_t e = set_max_smem((const void*)k_normal_eq<TY, T, MPL>, smem);
             if (e != cudaSuccess) return (int)e;
         }
-        k_normal_eq<T, MPL><<<(unsigned)PK, 256, smem, st>>>(P, K, m, a.Y, a.ldy, w.bucket_off, cap, a.idx,
+        k_normal_eq<TY, T, MPL><<<(unsigned)PK, 256, smem, st>>>(P, K, m, Ysrc, a.ldy, w.bucket_off, cap, a.idx,
                                                              a.val, a.counts, w.bent, w.B, w.A);
         return (int)cudaGetLastError();
     });
@@ -867,7 +870,7 @@ int mod_update(const ModArgs<T>& a, cudaStream_t st) {
     rc = chol_solve(P, K, m, w.A, w.B, a.usage, std::max(a.rank_rcond, MN_FLAG_TOL), w.depmask, w.deficient,
                     w.wsq, w.chol, st);
     if (rc) return rc;
-    rc = minnorm_solve<T>(P, K, m, a.Y, a.ldy, cap, a.idx, a.val, a.counts, w.bucket_off, w.bent, a.usage,
+    rc = minnorm_solve<TY, T>(P, K, m, Ysrc, a.ldy, cap, a.idx, a.val, a.counts, w.bucket_off, w.bent, a.usage,
                           a.rank_rcond, w.A, w.B, w.deficient, w.wsq, w.mn, st);
     if (rc) return rc;
     // residual before normalisation: ||Y - Z^T X||^2 = ||Y||^2 - <Z, B> and
@@ -876,7 +879,7 @@ int mod_update(const ModArgs<T>& a, cudaStream_t st) {
     if (ysq == nullptr) {
         rc = with_mpl(m, [&](auto c) {
             constexpr int MPL = decltype(c)::value;
-            k_row_sq<T, MPL><<<(unsigned)((N + 7) / 8), 256, 0, st>>>(N, m, a.Y, a.ldy, w.rsq);
+            k_row_sq<TY, MPL><<<(unsigned)((N + 7) / 8), 256, 0, st>>>(N, m, Ysrc, a.ldy, w.rsq);
             return (int)cudaGetLastError();
         });
         if (rc) return rc;
@@ -886,8 +889,8 @@ int mod_update(const ModArgs<T>& a, cudaStream_t st) {
     k_ls_resid<<<(P + 127) / 128, 128, 0, st>>>(P, ysq, w.wsq, a.resid_fro, w.need);
     rc = with_mpl(m, [&](auto c) {
         constexpr int MPL = decltype(c)::value;
-        k_resid_sq<T, MPL><<<resid_grid(N), 256, 0, st>>>(
-            N, m, K, cap, P, a.off, a.Y, a.ldy, a.idx, a.val, a.counts, w.B, w.rsq, nullptr, w.need);
+        k_resid_sq<TY, T, MPL><<<resid_grid(N), 256, 0, st>>>(
+            N, m, K, cap, P, a.off, Ysrc, a.ldy, a.idx, a.val, a.counts, w.B, w.rsq, nullptr, w.need);
         return (int)cudaGetLastError();
     });
     if (rc) return rc;
@@ -903,6 +906,13 @@ int mod_update(const ModArgs<T>& a, cudaStream_t st) {
     if (a.nnz_out)
         cudaMemcpyAsync(a.nnz_out, w.nnz, sizeof(int64_t) * P, cudaMemcpyDeviceToDevice, st);
     return (int)cudaGetLastError();
+}
+template <typename T>
+int mod_update(const ModArgs<T>& a, cudaStream_t st) {
+    if constexpr (std::is_same_v<T, double>) {
+        if (a.Yf != nullptr) return mod_update_impl<float, double>(a, a.Yf, st);
+    }
+    return mod_update_impl<T, T>(a, a.Y, st);
 }
 template int mod_update<float>(const ModArgs<float>&, cudaStream_t);
 template int mod_update<double>(const ModArgs<double>&, cudaStream_t);
@@ -947,7 +957,7 @@ int replace_degenerate(const ReplaceArgs<T>& a, cudaStream_t st) {
     // reference skips them when no atom is degenerate, which changes nothing)
     rc = with_mpl(m, [&](auto c) {
         constexpr int MPL = decltype(c)::value;
-        k_resid_sq<T, MPL><<<resid_grid(N), 256, 0, st>>>(
+        k_resid_sq<T, T, MPL><<<resid_grid(N), 256, 0, st>>>(
             N, m, K, cap, P, a.off, a.Y, a.ldy, a.idx, a.val, a.counts, a.D, rsq, ysq, ntarget);
         return (int)cudaGetLastError();
     });
@@ -970,7 +980,7 @@ int residual_sq(int64_t N, int m, int K, int cap, int P, const int64_t* off, con
     if (N <= 0) return 0;
     return with_mpl(m, [&](auto c) {
         constexpr int MPL = decltype(c)::value;
-        k_resid_sq<T, MPL><<<resid_grid(N), 256, 0, st>>>(N, m, K, cap, P, off, Y, ldy, idx,
+        k_resid_sq<T, T, MPL><<<resid_grid(N), 256, 0, st>>>(N, m, K, cap, P, off, Y, ldy, idx,
                                                                    val, counts, D, rsq, ysq, nullptr);
         return (int)cudaGetLastError();
     });

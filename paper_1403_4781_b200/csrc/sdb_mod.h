@@ -36,6 +36,7 @@ struct ModArgs {
     int64_t N;
     const int64_t* off;
     const T* Y;
+    const float* Yf;       // optional (T = double): FP32 rows whose values are the FP64 ones
     int64_t ldy;
     const int32_t* idx;
     const T* val;
@@ -76,8 +77,8 @@ int64_t mod_ws_bytes(int P, int64_t N, int m, int K, int cap);
 // Cholesky flags a shard for the minimum-norm (Jacobi pseudo-inverse) solve
 constexpr double MN_FLAG_TOL = 1e-8;
 int64_t minnorm_ws_bytes(int P, int m, int K);
-template <typename T>
-int minnorm_solve(int P, int K, int m, const T* Y, int64_t ldy, int cap, const int32_t* idx, const T* val,
+template <typename TY, typename T>
+int minnorm_solve(int P, int K, int m, const TY* Y, int64_t ldy, int cap, const int32_t* idx, const T* val,
                   const int32_t* counts, const int64_t* bucket_off, const int32_t* bent, const int32_t* usage,
                   double rcond, double* A, double* B, int32_t* deficient, double* wsq, double* slots,
                   cudaStream_t st);

@@ -179,7 +179,7 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
             int k = 0;
             while (it.next(r)) {
                 if (!r.first) continue;
-                if (k > 0) mbar_wait(smem_u32(&bars[B_DFREE]), (uint32_t)((k - 1) & 1));
+                if (k > 0) mbar_wait_sleep(smem_u32(&bars[B_DFREE]), (uint32_t)((k - 1) & 1));
                 const uint32_t bf = smem_u32(&bars[B_DFULL]);
                 mbar_expect_tx(bf, (uint32_t)dbytes);
                 for (int kb = 0; kb < a.nkb; ++kb)
@@ -201,7 +201,7 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
             Round r;
             while (it.next(r)) {
                 if (r.first) {
-                    mbar_wait(smem_u32(&bars[B_DFULL]), (uint32_t)(k & 1));
+                    mbar_wait_sleep(smem_u32(&bars[B_DFULL]), (uint32_t)(k & 1));
                     ++k;
                 }
                 bool act[NG];
@@ -210,7 +210,7 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
                 while (nact > 0) {
                     for (int g = 0; g < NG; ++g) {
                         if (!act[g]) continue;
-                        mbar_wait(smem_u32(&bars[B_RFULL + g]), rph[g] & 1u);
+                        mbar_wait_sleep(smem_u32(&bars[B_RFULL + g]), rph[g] & 1u);
                         ++rph[g];
                         if (!contf[g]) {
                             // tile done: acknowledge on full[g] so the group cannot
@@ -223,7 +223,7 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
                         const unsigned char* Rg = base + dbytes + g * rbytes;
                         for (int c = 0; c < a.nch; ++c) {
                             const int b = a.nch == 2 ? c : (g & 1);
-                            if (uses[b]) mbar_wait(smem_u32(&bars[B_EMPTY + b]), (uses[b] - 1) & 1u);
+                            if (uses[b]) mbar_wait_sleep(smem_u32(&bars[B_EMPTY + b]), (uses[b] - 1) & 1u);
                             ++uses[b];
                             tmem_fence_after();
                             const uint32_t tacc = tmem + (uint32_t)(b * OT_N);
