@@ -228,43 +228,24 @@ k_chol_diag(int K, int j0, double* __restrict__ Aall, double* __restrict__ Tall,
 
 // 64x64 tile update  C -= X Y^T  with X (64 x nb), Y (64 x nb) from smem;
 // each thread owns a 4x4 micro-tile (rows ty+16a, cols tx+16b).
-// acc[a][b] = sum_q Xs[ty + 16a][q] * Ys[tx + 16b][q] (thread (tx, ty) of 256)
-// on the FP64 tensor cores: warp w computes output rows 8w..8w+7 against all
-// 64 columns with mma.sync m8n8k4 f64 (eight 8x8 accumulators), the result is
-// staged through Ys (free once the products are formed) back into the
-// callers' register layout. Called by all 256 threads; Xs / Ys hold zeros
-// past nb.
 __device__ __forceinline__ void tile_update(double (*Xs)[CBP], double (*Ys)[CBP], int nb,
                                             double acc[4][4]) {
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const int tx = tid & 15, ty = tid >> 4;
-    double c[8][2];
-#pragma unroll
-    for (int t = 0; t < 8; ++t) { c[t][0] = 0.0; c[t][1] = 0.0; }
-    const int ar = 8 * w + (lane >> 2), kq = lane & 3;
-    const int kend = (nb + 3) & ~3;
-    for (int q = 0; q < kend; q += 4) {
-        const double av = Xs[ar][q + kq];
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-            const double bv = Ys[8 * t + (lane >> 2)][q + kq];
-            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-                         : "+d"(c[t][0]), "+d"(c[t][1])
-                         : "d"(av), "d"(bv));
-        }
-    }
-    __syncthreads();   // every warp is done reading Ys
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-        const int col = 8 * t + 2 * (lane & 3);
-        Ys[8 * w + (lane >> 2)][col] = c[t][0];
-        Ys[8 * w + (lane >> 2)][col + 1] = c[t][1];
-    }
-    __syncthreads();
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = Ys[ty + 16 * a][tx + 16 * b];
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    for (int q = 0; q < nb; ++q) {
+        double xv[4], yv[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) xv[a] = Xs[ty + 16 * a][q];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) yv[b] = Ys[tx + 16 * b][q];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b] = fma(xv[a], yv[b], acc[a][b]);
+    }
 }
 
 // blockIdx.x == 0: W_j = T_j B_j (the panel's right-hand-side rows)
