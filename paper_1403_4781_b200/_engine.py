@@ -152,6 +152,17 @@ def ingest_signals(Y, prec: str) -> tuple[torch.Tensor, int]:
     return out, bad
 
 
+def ingest_for(Y, prec: str):
+    """Host / device m x N signals -> (working-precision rows, FP64 rows or
+    None, nonfinite flag). In certified FP32 mode the FP64 rows are kept as the
+    authoritative data (the FP32 rows are their rounding, the kernels' input)."""
+    if certifies(prec):
+        Y64, bad = ingest_signals(Y, "fp64")
+        return Y64.to(torch.float32), Y64, bad
+    Yw, bad = ingest_signals(Y, prec)
+    return Yw, None, bad
+
+
 def dict_to_device(D: np.ndarray) -> torch.Tensor:
     """Host m x K f64 dictionary -> device (1, K, m) f64 atom-major."""
     D = np.asarray(D, dtype=np.float64)
@@ -374,10 +385,11 @@ def signal_sq(Ydev: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tens
     return out[:N]
 
 
-def code_single_dict(Ydev, D64, cap, eps, prec, use_tc=True, want_rnorm=True) -> DeviceCodes:
+def code_single_dict(Ydev, D64, cap, eps, prec, use_tc=True, want_rnorm=True, Y64=None) -> DeviceCodes:
     """Code all rows of Ydev against one dictionary (P = 1), chunked.
     want_rnorm=False (callers that never read the residual norms, e.g. the
-    denoiser) lets FP32 error-bounded coding take the fused path."""
+    denoiser) lets FP32 error-bounded coding take the fused path. Y64: the
+    authoritative FP64 rows when Ydev rounds them (certified mode)."""
     N = Ydev.shape[0]
     DT = working_dict(D64, prec)
     G = gram(D64, prec)
@@ -393,7 +405,7 @@ def code_single_dict(Ydev, D64, cap, eps, prec, use_tc=True, want_rnorm=True) ->
         off, mx = shard_offsets([N])
         c = code(Ydev, off, mx, DT, G, cap, eps, prec, use_tc, ysq=ysq, want_rnorm=want_rnorm and not cert,
                  want_gap=cert)
-        return certify(Ydev, off, D64, G64, c, eps, want_rnorm) if cert else c
+        return certify(Ydev, off, D64, G64, c, eps, want_rnorm, Y64=Y64) if cert else c
     tdt = torch_dtype(prec)
     res = DeviceCodes(K, cap, empty((N, cap), torch.int32), empty((N, cap), tdt),
                       empty((N,), torch.int32), empty((N,), torch.int8), empty((N,), tdt))
@@ -410,7 +422,8 @@ def code_single_dict(Ydev, D64, cap, eps, prec, use_tc=True, want_rnorm=True) ->
                                res.status[lo:hi], empty((hi - lo,), tdt))
             c = code(Ydev[lo:hi], off, mx, DT, G, cap, eps, prec, use_tc, out=view,
                      ysq=None if ysq is None else ysq[lo:hi], want_rnorm=False, want_gap=True)
-            cc = certify(Ydev[lo:hi], off, D64, G64, c, eps, want_rnorm)
+            cc = certify(Ydev[lo:hi], off, D64, G64, c, eps, want_rnorm,
+                         Y64=None if Y64 is None else Y64[lo:hi])
             res.val[lo:hi].copy_(cc.val)
             if want_rnorm:
                 res.rnorm[lo:hi].copy_(cc.rnorm)

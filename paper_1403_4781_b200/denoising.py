@@ -149,8 +149,13 @@ def denoise_device(px: torch.Tensor, D64: torch.Tensor, p: int, stride: int, eps
                    cap: int, prec: str) -> torch.Tensor:
     """Device-resident denoise: (H, W) f64 image -> (H, W) f64 clipped."""
     H, W = px.shape
-    Pt = patches_device(px, p, stride, prec)
-    codes = E.code_single_dict(Pt, D64, cap, eps, prec, want_rnorm=False)   # norms are never read
+    Pt64 = None
+    if E.certifies(prec):
+        Pt64 = patches_device(px, p, stride, "fp64")     # the authoritative patch values
+        Pt = Pt64.to(torch.float32)
+    else:
+        Pt = patches_device(px, p, stride, prec)
+    codes = E.code_single_dict(Pt, D64, cap, eps, prec, want_rnorm=False, Y64=Pt64)   # norms are never read
     out = E.empty((H, W), torch.float64)
     E._lib.call("sdb_reconstruct", E.sdb_dtype(codes.vprec or prec), H, W, p, stride, E.ptr(D64), codes.cap,
                 E.ptr(codes.idx), E.ptr(codes.val), E.ptr(codes.counts), 0.0, 255.0,

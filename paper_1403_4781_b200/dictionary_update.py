@@ -61,6 +61,9 @@ def normalize_columns(M) -> tuple[np.ndarray, np.ndarray]:
 
 
 def _prepare(Y, X: SparseCodeMatrix, m: int, prec: str):
+    # MOD / replacement arithmetic is FP64 in both modes; certified FP32 also
+    # keeps the inputs FP64 (the reference's values)
+    prec = "fp64" if E.certifies(prec) else prec
     Ydev, bad = E.ingest_signals(Y, prec)
     codes = E.codes_from_csc(X.indptr, X.indices, X.data, X.K, prec)
     return E.ShardSet.single(Ydev, prec), codes

@@ -47,6 +47,7 @@ def mse_db(Y, D, X, precision: str | None = None) -> float:
                 for i in range(Xd.shape[1])]
         X = SparseCodeMatrix.from_columns(Xd.shape[0], cols)
     prec = "fp64" if precision is None else E.get_precision(precision)
+    prec = "fp64" if E.certifies(prec) else prec      # certified: the FP64 values
     Ydev, _ = E.ingest_signals(Y, prec)
     S = E.ShardSet.single(Ydev, prec)
     codes = E.codes_from_csc(X.indptr, X.indices, X.data, X.K, prec)

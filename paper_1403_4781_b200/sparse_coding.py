@@ -213,11 +213,11 @@ def _diagnostics(codes: E.DeviceCodes, err_mode: bool, eps: float, with_order: b
 
 
 def _run(Y, D, cap, eps, prec, N_hint=None):
-    Ydev, bad = E.ingest_signals(Y, prec)
+    Ydev, Y64, bad = E.ingest_for(Y, prec)
     if int(bad.item()):
         raise InvalidInputError("batch contains non-finite entries")
     D64 = E.dict_to_device(D)
-    return E.code_single_dict(Ydev, D64, cap, eps, prec)
+    return E.code_single_dict(Ydev, D64, cap, eps, prec, Y64=Y64)
 
 
 def _single(y, D, cap, eps, prec):

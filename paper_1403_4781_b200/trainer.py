@@ -170,6 +170,8 @@ def _zero_fill(D: torch.Tensor, zero_flags: np.ndarray, seeds) -> None:
 
 def init_dictionaries(S: E.ShardSet, K: int, init, seeds) -> torch.Tensor:
     """_init_dictionary (trainer.py:138-162) for every shard: (P, K, m) f64."""
+    if S._exact is not None and S._exact_auth:
+        S = S.exact()          # first columns of the authoritative FP64 data
     m = S.m
     if isinstance(init, str) and init == "first-columns":
         if min(S.sizes) < K:
@@ -364,6 +366,14 @@ def _check_Y(Y) -> np.ndarray:
     return Y
 
 
+def _ingest_checked2(Y, prec):
+    """(working-precision rows, authoritative FP64 rows or None)."""
+    Yw, Y64, bad = E.ingest_for(Y, prec)
+    if int(bad.item()):
+        raise InvalidInputError("batch contains non-finite entries")
+    return Yw, Y64
+
+
 def _ingest_checked(Y, prec):
     Ydev, bad = E.ingest_signals(Y, prec)
     if int(bad.item()):
@@ -389,7 +399,9 @@ def train_standard(Y, cfg: TrainConfig) -> tuple[np.ndarray, SparseCodeMatrix, T
     prec = E.get_precision(cfg.precision)
     cap, eps = coding_mode(m, cfg.K, cfg.s, cfg.eps, cfg.s_max)
     t0 = time.perf_counter()
-    S = E.ShardSet.single(_ingest_checked(Y, prec), prec)
+    Yw, Y64 = _ingest_checked2(Y, prec)
+    S = (E.ShardSet.with_exact(Y64, E.shard_offsets([N])[0], [N], prec) if Y64 is not None
+         else E.ShardSet.single(Yw, prec))
     D0 = init_dictionaries(S, cfg.K, cfg.init, [cfg.seed])
     D, codes, resid = train_device(S, D0, cap, eps, cfg.iterations)
     _sync()
@@ -521,7 +533,8 @@ def _group_streams(G: int) -> tuple:
 
 def _split_locals(src, N: int, m: int, L: int, K1: int, local_cap: int, local_eps: float,
                   local_iters: int, seeds, perm: torch.Tensor, prec: str, use_tc: bool, groups: int,
-                  host_f64: int | None = None, bad: torch.Tensor | None = None, head=(None, 0)):
+                  host_f64: int | None = None, bad: torch.Tensor | None = None, head=(None, 0),
+                  src64: torch.Tensor | None = None):
     """split_dataset + every train_local (trainer.py:291-305), in G groups of
     consecutive shards, each on its own CUDA stream. The group's rows are
     gathered in permuted order (all gathers in order on one copy stream, so
@@ -538,11 +551,22 @@ def _split_locals(src, N: int, m: int, L: int, K1: int, local_cap: int, local_ep
     if min(sizes) < K1:
         raise InvalidInputError("first-columns init needs N >= K")
     G = max(1, min(int(groups), L))
+    # certified FP32 with FP64 input: the shards keep the authoritative FP64
+    # rows (the FP32 copy feeds the coding kernels)
+    exact_in = E.certifies(prec) and (src64 is not None or host_f64 is not None)
+
+    def shardset(Yg, off, sz):
+        if exact_in:
+            return E.ShardSet.with_exact(Yg, off, sz, prec)
+        return E.ShardSet(Yg, off, sz, prec)
+
+    gprec = "fp64" if exact_in else prec
+    gsrc = src64 if (exact_in and src64 is not None) else src
     if G == 1 and host_f64 is None:
         # one batch on the caller's stream (no cross-stream allocations)
-        Ys = E.gather_rows(src, perm, prec)
+        Ys = E.gather_rows(gsrc, perm, gprec)
         off, _ = E.shard_offsets(sizes)
-        S = E.ShardSet(Ys, off, sizes, prec)
+        S = shardset(Ys, off, sizes)
         D0 = init_dictionaries(S, K1, "first-columns", seeds[:L])
         Dl, codes, _ = train_device(S, D0, local_cap, local_eps, local_iters, use_tc)
         return Dl, E.code_energy(S, codes)
@@ -555,9 +579,9 @@ def _split_locals(src, N: int, m: int, L: int, K1: int, local_cap: int, local_ep
         for g in range(G):
             r0, r1 = int(offs[bounds[g]]), int(offs[bounds[g + 1]])
             if host_f64 is not None:
-                Ys = E.ingest_gather(host_f64, m, perm, r0, r1, m, prec, bad[g:g + 1], head=head)
+                Ys = E.ingest_gather(host_f64, m, perm, r0, r1, m, gprec, bad[g:g + 1], head=head)
             else:
-                Ys = E.gather_rows(src, perm[r0:r1], prec)
+                Ys = E.gather_rows(gsrc, perm[r0:r1], gprec)
             ev = torch.cuda.Event()
             ev.record(copy)
             ready.append((Ys, ev))
@@ -580,7 +604,7 @@ def _split_locals(src, N: int, m: int, L: int, K1: int, local_cap: int, local_ep
         Ys.record_stream(s)
         with torch.cuda.stream(s):
             off, _ = E.shard_offsets(sizes[a:b])
-            S = E.ShardSet(Ys, off, sizes[a:b], prec)
+            S = shardset(Ys, off, sizes[a:b])
             D0 = init_dictionaries(S, K1, "first-columns", seeds[a:b])
             # one graph per group: equal-shaped groups run concurrently on their
             # own streams and must not share a graph's static buffers
@@ -634,7 +658,7 @@ def split_merge_device(Ydev: torch.Tensor, L: int, K1: int, local_cap: int, loca
                        local_iters: int, K: int, s2: int, merge_iters: int, seed: int,
                        init="first-columns", prec: str = "fp64", use_tc: bool = True,
                        t_start: float | None = None, perm: torch.Tensor | None = None,
-                       groups: int = 1) -> SplitMergeResult:
+                       groups: int = 1, src64: torch.Tensor | None = None) -> SplitMergeResult:
     """split_dataset -> locals (all shards batched, optionally in ``groups``
     concurrent shard groups) -> merge (trainer.py:291-313). ``Ydev`` is
     (N, m) device, signal-major."""
@@ -651,7 +675,7 @@ def split_merge_device(Ydev: torch.Tensor, L: int, K1: int, local_cap: int, loca
     t_split = time.perf_counter()
     seeds = _derive_seeds(seed, L + 1)
     Dl, w = _split_locals(Ydev, N, m, L, K1, local_cap, local_eps, local_iters, seeds, perm, prec,
-                          use_tc, groups)
+                          use_tc, groups, src64=src64)
     w_h = E.d2h(w)                       # synchronises: end of the split phase
     t_local = time.perf_counter()
     Dm, w_h, n_merge = _merge(Dl, w, K1, m, K, s2, merge_iters, seeds[L], init, prec, use_tc)
@@ -719,7 +743,7 @@ def train_split_merge(Y, cfg: TrainConfig, evaluate: bool = True) -> tuple[np.nd
     _sync()
     t0 = time.perf_counter()
     src = E.host_mapped(Y.T) if Y.T.flags.c_contiguous else None
-    Ydev = None
+    Ydev = Ydev64 = None
     if src is not None:
         # pinned, signal-major host input: each shard group's rows cross PCIe
         # directly in permuted order and the group trains as soon as they land
@@ -729,18 +753,20 @@ def train_split_merge(Y, cfg: TrainConfig, evaluate: bool = True) -> tuple[np.nd
         from concurrent.futures import ThreadPoolExecutor
         with ThreadPoolExecutor(max_workers=1) as ex:
             fut = ex.submit(E.split_permutation, N, cfg.seed)
-            Ydev = _ingest_checked(Y, prec)
+            Ydev, Ydev64 = _ingest_checked2(Y, prec)
             perm = fut.result()
         r = split_merge_device(Ydev, cfg.L, cfg.K1, cap1, eps1, local_iters, cfg.K, cfg.s2,
-                               merge_iters, cfg.seed, cfg.init, prec, t_start=t0, perm=perm)
+                               merge_iters, cfg.seed, cfg.init, prec, t_start=t0, perm=perm, src64=Ydev64)
     # evaluation pass (trainer.py:315-319), outside wall_time_s
     mse = float("nan")
     if evaluate:
         if Ydev is None:
-            Ydev = _ingest_checked(Y, prec)
-        S = E.ShardSet.single(Ydev, prec)
+            Ydev, Ydev64 = _ingest_checked2(Y, prec)
+        S = (E.ShardSet.with_exact(Ydev64, E.shard_offsets([N])[0], [N], prec) if Ydev64 is not None
+             else E.ShardSet.single(Ydev, prec))
         cap_e, _ = coding_mode(m, cfg.K, cfg.s, None, None)
-        codes = E.code_single_dict(Ydev, r.D_dev, cap_e, 0.0, prec)
+        codes = E.code_single_dict(S.Y, r.D_dev, cap_e, 0.0, prec,
+                                   Y64=Ydev64 if Ydev64 is not None else None)
         mse = mse_db_device(S, codes, r.D_dev)
     report = TrainReport(final_mse_db=mse, wall_time_s=r.wall_s,
                          # the L locals run concurrently in one batched launch sequence: they

@@ -102,3 +102,29 @@ def test_certified_split_merge_c1_matches_fp64_reference():
                           cfg["s2"], cfg["merge_iters"], 1234, threads=8)
     rel = np.linalg.norm(r.D - Dr) / np.linalg.norm(Dr)
     assert rel <= 1e-9, rel
+
+
+def test_certified_fp32_on_fp64_inputs_is_the_reference():
+    """Inputs that FP32 cannot represent: certified FP32 keeps the FP64 values
+    as the authoritative data (the FP32 copy only feeds the coding kernels), so
+    omp_batch, train_standard and train_split_merge return the reference's
+    FP64 results, not those of a rounded input."""
+    import paper_1403_4781_b200 as sdb
+    from oracle import oracle as O
+    D = _dict(32, 96, 8)
+    rng = np.random.default_rng(9)
+    Y = D[:, :12] @ rng.standard_normal((12, 3000)) + 0.05 * rng.standard_normal((32, 3000))
+    assert not np.array_equal(Y, Y.astype(np.float32).astype(np.float64))
+    X = sdb.omp_batch(Y, D, s=5, precision="fp32")
+    Xr, _ = O.omp_codes(Y, D, s=5, threads=8)
+    assert np.array_equal(X.indptr, Xr[1]) and np.array_equal(X.indices, Xr[2])
+    np.testing.assert_allclose(X.data, Xr[3], rtol=0, atol=1e-12 * np.abs(Xr[3]).max())
+    cfg = sdb.TrainConfig(K=48, s=8, iterations=4, seed=2, mode="split-merge", L=3, K1=48, s1=4, s2=2,
+                          precision="fp32")
+    Dg, _ = sdb.train_split_merge(Y, cfg, evaluate=False)
+    Dr, _ = O.split_merge(Y, 3, 48, 4, 4, 48, 2, 4, 2, threads=8)
+    assert np.linalg.norm(Dg - Dr) / np.linalg.norm(Dr) <= 1e-12
+    cs = sdb.TrainConfig(K=48, s=4, iterations=4, seed=2, precision="fp32")
+    Ds, _, _ = sdb.train_standard(Y, cs)
+    Dsr, _, _ = O.train_standard(Y, 48, 4, 4, "first-columns", 2, threads=8)
+    assert np.linalg.norm(Ds - Dsr) / np.linalg.norm(Dsr) <= 1e-12
