@@ -118,11 +118,12 @@ int sdb_omp(int dtype, int64_t N, int64_t m, int64_t K, int64_t P, const int64_t
  * every other signal keeps its support and gets FP64 least-squares
  * coefficients on it. Y: the FP32 signal rows the FP32 kernels coded; Y64
  * (optional): the authoritative FP64 rows (used instead of Y when the FP32
- * rows are a rounding of them); D: P x K x m f64; G: the FP64
+ * rows are a rounding of them); D: P x K x m f64; Dt (optional): its P x m x K
+ * transpose (coalesced c0 for the re-coded signals); G: the FP64
  * Gram (sdb_gram). idx/counts/status in-out; val (N x cap f64), rnorm (f64,
  * optional) out. list: N int32; nlist: 1 int32 (device). */
 int sdb_certify(int64_t N, int64_t m, int64_t K, int64_t P, const int64_t *shard_off, const float *Y,
-                const double *Y64, int64_t ldy, const double *D, const double *G, int64_t cap, double eps, double tau,
+                const double *Y64, int64_t ldy, const double *D, const double *Dt, const double *G, int64_t cap, double eps, double tau,
                 int32_t *idx, double *val, int32_t *counts, int8_t *status, double *rnorm, const float *gap,
                 int32_t *list, int32_t *nlist, void *stream);
 int sdb_omp_tc_supported(int64_t m, int64_t K, int64_t cap);

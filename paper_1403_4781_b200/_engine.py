@@ -342,8 +342,9 @@ def certify(Y32: torch.Tensor, off: torch.Tensor, D64: torch.Tensor, G64: torch.
     nl = empty((1,), torch.int32)
     if N:
         assert Y64 is None or (Y64.shape == Y32.shape and Y64.stride(0) == Y32.stride(0))
+        Dt64 = D64.transpose(1, 2).contiguous()      # P x m x K: coalesced c0 of the re-coded signals
         timed_call("certify", N * ((8 if Y64 is not None else 4) * m + cap * 12 + 9), 0.0, "sdb_certify", N, m, K,
-                   P, ptr(off), ptr(Y32), ptr(Y64), Y32.stride(0), ptr(D64), ptr(G64), cap, float(eps), CERT_TAU, ptr(codes.idx), ptr(val),
+                   P, ptr(off), ptr(Y32), ptr(Y64), Y32.stride(0), ptr(D64), ptr(Dt64), ptr(G64), cap, float(eps), CERT_TAU, ptr(codes.idx), ptr(val),
                    ptr(codes.counts), ptr(codes.status), ptr(rn) if want_rnorm else None, ptr(codes.gap),
                    ptr(lst), ptr(nl), stream())
         if KTIMER is not None and not torch.cuda.is_current_stream_capturing():

@@ -44,7 +44,7 @@ SIGNATURES = {
     "sdb_omp_deferred": (c_int, [c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp,
                                  c_vp, c_vp, c_i64, c_dbl, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                  c_i64, c_vp]),
-    "sdb_certify": (c_int, [c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_dbl, c_dbl,
+    "sdb_certify": (c_int, [c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_dbl, c_dbl,
                             c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "sdb_omp_tc_supported": (c_int, [c_i64, c_i64, c_i64]),
     "sdb_omp_tc_workspace_bytes": (c_i64, [c_i64, c_i64, c_i64]),
@@ -101,7 +101,7 @@ class NativeError(RuntimeError):
 
 _lib = None
 # must equal sdb_abi_version() in csrc/sdb_capi.cu (bumped whenever exports change)
-ABI_VERSION = 10
+ABI_VERSION = 11
 
 
 def load():

@@ -55,7 +55,7 @@ __global__ void k_cast(int64_t n, const double* __restrict__ src, T* __restrict_
 
 extern "C" {
 
-int sdb_abi_version(void) { return 10; }
+int sdb_abi_version(void) { return 11; }
 const char* sdb_last_error(void) { return g_err.c_str(); }
 
 int sdb_device_cc(void) {
@@ -193,7 +193,7 @@ int sdb_omp(int dtype, int64_t N, int64_t m, int64_t K, int64_t P, const int64_t
 
 // ---- fused tensor-core Batch-OMP (FP32): corr = D^T r per step on tcgen05
 int sdb_certify(int64_t N, int64_t m, int64_t K, int64_t P, const int64_t* shard_off, const float* Y,
-                const double* Y64, int64_t ldy, const double* D, const double* G, int64_t cap, double eps, double tau, int32_t* idx, double* val,
+                const double* Y64, int64_t ldy, const double* D, const double* Dt, const double* G, int64_t cap, double eps, double tau, int32_t* idx, double* val,
                 int32_t* counts, int8_t* status, double* rnorm, const float* gap, int32_t* list, int32_t* nlist,
                 void* stream) {
     if (N < 0 || m < 1 || K < 1 || P < 1 || cap < 1 || ldy < m || !(tau >= 0.0) || list == nullptr ||
@@ -211,7 +211,7 @@ int sdb_certify(int64_t N, int64_t m, int64_t K, int64_t P, const int64_t* shard
     a.idx = idx; a.counts = counts; a.status = status;
     a.eps = eps; a.guard = 1e-12;              // the reference's guard (_kernels.py:18)
     a.alpha0 = nullptr; a.Y = Y64; a.Yf = Y64 ? nullptr : Y; a.D = D; a.G = G; a.val = val; a.rnorm = rnorm;
-    a.list = list; a.nlist = nlist;
+    a.list = list; a.nlist = nlist; a.Dt = Dt;
     a.warp_bytes = sdb::omp_warp_bytes_f64((int)cap, (int)m);
     return cuda_rc(sdb::launch_omp<double>(a, S(stream)), "sdb_certify (exact)");
 }

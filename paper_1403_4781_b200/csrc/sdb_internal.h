@@ -37,6 +37,7 @@ struct OmpArgs {
     const int32_t* list;
     const int32_t* nlist;
     const float* Yf;
+    const T* Dt;               // optional: P x m x K transposed dictionary (coalesced in-kernel c0)
     // FP32 fast kernel: optional per-signal smallest decision margin / ||y||
     // (best vs runner-up |corr| above the rounding floor; | ||r|| - eps | at
     // every stopping test) for the FP64 certification pass

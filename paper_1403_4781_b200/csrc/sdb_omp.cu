@@ -212,15 +212,30 @@ k_omp(OmpArgs<T> a) {
         } else {
             // c0 = D^T y with the reference's loop order (sequential over the
             // m rows, separately rounded products: _kernels.py:54-59)
+            if (a.Dt) {
+                // transposed copy: lanes read consecutive atoms of one row t
+                const T* __restrict__ Dtp = a.Dt + (int64_t)p * m * K;
 #pragma unroll
-            for (int k = 0; k < KPL; ++k) {
-                const int j = lane + 32 * k;
-                T acc = T(0);
-                if (j < K) {
-                    const T* __restrict__ dj = Dp + (int64_t)j * m;
-                    for (int t = 0; t < m; ++t) acc = R::mac(acc, __ldg(dj + t), w.y[t]);
+                for (int k = 0; k < KPL; ++k) c0[k] = T(0);
+                for (int t = 0; t < m; ++t) {
+                    const T yt = w.y[t];
+#pragma unroll
+                    for (int k = 0; k < KPL; ++k) {
+                        const int j = lane + 32 * k;
+                        if (j < K) c0[k] = R::mac(c0[k], __ldg(Dtp + (int64_t)t * K + j), yt);
+                    }
                 }
-                c0[k] = acc;
+            } else {
+#pragma unroll
+                for (int k = 0; k < KPL; ++k) {
+                    const int j = lane + 32 * k;
+                    T acc = T(0);
+                    if (j < K) {
+                        const T* __restrict__ dj = Dp + (int64_t)j * m;
+                        for (int t = 0; t < m; ++t) acc = R::mac(acc, __ldg(dj + t), w.y[t]);
+                    }
+                    c0[k] = acc;
+                }
             }
         }
         T ysq;
