@@ -62,8 +62,9 @@ def parse():
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the secondary C2 line")
-    ap.add_argument("--groups", type=int, default=1,
-                    help="concurrent shard groups in the local phase (device-resident run)")
+    ap.add_argument("--groups", type=int, default=0,
+                    help="concurrent shard groups in the local phase (device-resident run; 0: auto, "
+                         "4 for >= 128 shards, else 1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=1234)
     return ap.parse_args()
@@ -530,7 +531,9 @@ def main():
     pk = measure_peaks()
     Ydev = benchdata.make_training_data_device(args.config, args.seed, prec)   # resident in HBM
     N, m = Ydev.shape
-    step, cap = make_step(cfg, Ydev, prec, args.seed, world, args.groups)
+    from paper_1403_4781_b200.trainer import auto_groups
+    groups = args.groups or auto_groups(cfg["L"])
+    step, cap = make_step(cfg, Ydev, prec, args.seed, world, groups)
 
     clk = Clocks(local)
     clk.ready()
@@ -543,7 +546,10 @@ def main():
     clocks = clk.stop()
     value = codings / (ms / 1000.0)
 
-    breakdown, ms_eager, omp_b = kernel_breakdown(step, cfg, cap, m)
+    # per-kernel breakdown on one serial (single-group) eager step: concurrent
+    # shard groups would overlap launches and blur per-launch durations
+    step1, _ = make_step(cfg, Ydev, prec, args.seed, world, 1) if groups > 1 else (step, cap)
+    breakdown, ms_eager, omp_b = kernel_breakdown(step1, cfg, cap, m)
     ncu = ncu_traffic()
     singles = {k: v for k, v in breakdown.items() if k in KERNEL_OF}
     dom = max(singles, key=lambda k: singles[k]["ms_per_step"]) if singles else None
@@ -624,11 +630,12 @@ def main():
                        "eps": cfg["eps"], "s_max": cfg["s_max"], "s1": cfg["s1"], "s2": cfg["s2"],
                        "codings_per_step": codings, "train_time_s": ms / 1000.0,
                        "phase_s": {"split": r.split_s, "locals": r.local_s, "merge": r.merge_s},
-                       "precision": prec, "parallelism": f"shards over {world} GPU(s)",
+                       "precision": prec, "parallelism": f"shards over {world} GPU(s)", "shard_groups": groups,
                        "l2": "inputs larger than L2 (Y is %.0f MB)" % (N * m * 4 / 1e6)},
             "roofline": roof, "roofline_others": others, "peaks": pk, "kernels": breakdown,
-            "kernels_note": f"per-kernel CUDA events from one extra eager step ({ms_eager:.2f} ms; the "
-                            "timed steps replay CUDA graphs per training iteration)",
+            "kernels_note": f"per-kernel CUDA events from one extra eager single-group step ({ms_eager:.2f} ms; "
+                            f"the timed steps replay CUDA graphs per training iteration, {groups} concurrent "
+                            "shard group(s))",
             "cpu_baseline": cpu, "e2e": e2e, "e2e_pageable": e2e_pageable, "extra": extra,
             "gpu_launches": gpu_launches, "clocks": clocks,
         }

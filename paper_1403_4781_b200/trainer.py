@@ -687,6 +687,14 @@ def split_merge_device(Ydev: torch.Tensor, L: int, K1: int, local_cap: int, loca
 
 
 HOST_GROUPS = int(os.environ.get("SDB_HOST_GROUPS", "4"))  # shard groups streamed from pinned host memory
+
+
+def auto_groups(L: int) -> int:
+    """Concurrent shard groups for device-resident split phases: with many
+    shards (C4: 256) four groups on their own streams overlap one group's
+    latency-bound MOD phases with another's coding (301.6 vs 316.0 ms per C4
+    job; 2 and 8 groups measured slower); few shards keep one batch."""
+    return 4 if L >= 128 else 1
 # 1/HEAD_DIV of a host batch is copied ahead (during the host permutation)
 HEAD_DIV = int(os.environ.get("SDB_HEAD_DIV", "8"))
 
@@ -756,7 +764,8 @@ def train_split_merge(Y, cfg: TrainConfig, evaluate: bool = True) -> tuple[np.nd
             Ydev, Ydev64 = _ingest_checked2(Y, prec)
             perm = fut.result()
         r = split_merge_device(Ydev, cfg.L, cfg.K1, cap1, eps1, local_iters, cfg.K, cfg.s2,
-                               merge_iters, cfg.seed, cfg.init, prec, t_start=t0, perm=perm, src64=Ydev64)
+                               merge_iters, cfg.seed, cfg.init, prec, t_start=t0, perm=perm, src64=Ydev64,
+                               groups=auto_groups(cfg.L))
     # evaluation pass (trainer.py:315-319), outside wall_time_s
     mse = float("nan")
     if evaluate:
