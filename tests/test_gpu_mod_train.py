@@ -331,3 +331,20 @@ def test_split_merge_ranks_nccl_world1_equals_device():
         assert np.array_equal(a.D, b.D)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+def test_shard_groups_equal_one_batch(prec):
+    """Concurrent shard groups on their own streams (auto for >= 128 shards)
+    give bitwise the dictionaries of the single batched launch: shards are
+    independent and every kernel's per-shard arithmetic is fixed."""
+    import benchdata
+    from paper_1403_4781_b200 import _engine as E
+    from paper_1403_4781_b200.trainer import split_merge_device
+    Yd = benchdata.make_training_data_device("c4", 5, prec, N=8 * 4000)
+    out = []
+    for groups in (1, 4):
+        r = split_merge_device(Yd, 8, 96, 6, 0.0, 3, 96, 3, 3, 17, prec=prec, groups=groups)
+        out.append((E.d2h(r.local_D), r.D))
+    assert np.array_equal(out[0][0].view(np.uint8), out[1][0].view(np.uint8))
+    assert np.array_equal(out[0][1].view(np.uint8), out[1][1].view(np.uint8))
