@@ -217,7 +217,10 @@ k_certify(CertArgs a) {
             }
         }
         __syncwarp();
-        if (work && l < cap) a.val[i * cap + l] = (l < n) ? x : 0.0;   // cap <= LPS: lane t holds x_t
+        // lane t holds x_t (n <= LPS here); slots past n, including those past
+        // LPS when cap > LPS, are zeroed like the reference's
+        if (work)
+            for (int t = l; t < cap; t += LPS) a.val[i * cap + t] = (t < n) ? x : 0.0;
         if (a.rnorm != nullptr) {
             double rs = 0.0;
 #pragma unroll
