@@ -12,7 +12,8 @@ import os
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libsdb200.so"
+# SDB_LIB: an alternative build of the same ABI (A/B comparisons of kernel versions)
+LIB_PATH = Path(os.environ["SDB_LIB"]) if os.environ.get("SDB_LIB") else PKG / "libsdb200.so"
 
 SDB_F32, SDB_F64, SDB_F32X = 0, 1, 2
 

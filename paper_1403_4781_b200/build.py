@@ -11,6 +11,7 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
@@ -18,8 +19,9 @@ CSRC = PKG / "csrc"
 LIB = PKG / "libsdb200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
          "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
+OBJ = PKG / "build"
 
 
 def sources():
@@ -38,10 +40,24 @@ def stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not stale():
         return LIB
-    cmd = [NVCC, *ARCH, *FLAGS, "-o", str(LIB), *map(str, sources())]
+    # one nvcc per translation unit in parallel, then one link
+    OBJ.mkdir(exist_ok=True)
+    jobs = []
+    for src in sources():
+        obj = OBJ / (src.stem + ".o")
+        jobs.append((obj, [NVCC, *ARCH, *FLAGS, "-c", "-o", str(obj), str(src)]))
     if verbose:
-        print(" ".join(cmd), flush=True)
-    subprocess.run(cmd, check=True)
+        for _, cmd in jobs:
+            print(" ".join(cmd), flush=True)
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        for r in ex.map(lambda j: subprocess.run(j[1]), jobs):
+            if r.returncode != 0:
+                raise subprocess.CalledProcessError(r.returncode, r.args)
+    link = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", str(LIB),
+            *(str(o) for o, _ in jobs)]
+    if verbose:
+        print(" ".join(link), flush=True)
+    subprocess.run(link, check=True)
     return LIB
 
 

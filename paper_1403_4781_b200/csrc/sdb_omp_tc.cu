@@ -138,7 +138,9 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
     const int dbytes = a.nkb * a.kpad * 128;
     const int rbytes = a.nkb * OT_RB;
     unsigned char* Ds = base;
-    uint64_t* bars = (uint64_t*)(base + dbytes + NG * rbytes);
+    // per-lane slots (128 B: the block of the running maximum), then the barriers
+    unsigned char* Sl = base + dbytes + NG * rbytes;
+    uint64_t* bars = (uint64_t*)(Sl + NG * OT_M * 128);
     int* votes = (int*)(bars + 2 * NG + 4);   // [step parity][group][warp]
     volatile int* contf = votes + 8 * NG;     // [group]
     uint32_t* tslot = (uint32_t*)(votes + 9 * NG);
@@ -251,6 +253,7 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
         unsigned char* R = base + dbytes + g * rbytes;
         const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
         const int swz = row & 7;
+        unsigned char* slot = Sl + (g * OT_M + row) * 128;
         uint32_t fph = 0;
         int sp = 0;
         int k = 0;
@@ -359,16 +362,65 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
                     mbar_wait_sleep(smem_u32(&bars[B_FULL + g]), fph & 1u);
                     ++fph;
                     tmem_fence_after();
-                    // ---------------- scan: candidates within the window of the TF32 max
+                    // ---------------- scan: ONE pass over the TMEM row. Block maxima
+                    // (32 columns each); the block holding the running maximum is
+                    // copied to the lane's shared-memory slot, so the candidates of
+                    // the maximum's block come from the slot (every lane at once);
+                    // only other blocks within the window (a near tie in another
+                    // block) are re-read from TMEM, for the lanes that need them.
                     const float rn = sqrtf(rsq);
                     float thr = __int_as_float(0x7f800000);   // +inf: no candidates
                     float win = 0.f;
                     int nc = 0;
-                    int cand[OT_CMAX];
+                    int cand[OT_CMAX];   // the OT_CMAX smallest candidate indices, ascending
 #pragma unroll
-                    for (int s = 0; s < OT_CMAX; ++s) cand[s] = 0;
+                    for (int s = 0; s < OT_CMAX; ++s) cand[s] = 0x7fffffff;
+                    // candidate j (not in the support): sorted insert, the largest index drops out
+                    auto add = [&](int j) {
+                        if (j < K && !in_support(j)) {
+                            int x = j;
+#pragma unroll
+                            for (int s = 0; s < OT_CMAX; ++s) {
+                                const int lo = min(cand[s], x);
+                                x = max(cand[s], x);
+                                cand[s] = lo;
+                            }
+                            ++nc;
+                        }
+                    };
+                    auto extract = [&](const float (&v)[32], int j0) {
+                        unsigned msk = 0u;
+#pragma unroll
+                        for (int t = 0; t < 32; ++t)
+                            if (fabsf(v[t]) >= thr) msk |= 1u << t;
+                        while (msk) {
+                            const int j = j0 + __ffs(msk) - 1;
+                            msk &= msk - 1u;
+                            add(j);
+                        }
+                    };
                     if (__any_sync(SDB_FULL, act)) {
                         float bm[16];
+                        float cmax = -1.f;
+                        int sb = 0;
+                        auto keep = [&](const uint32_t (&v)[32], int blk) {
+                            float m0 = 0.f, m1 = 0.f;
+#pragma unroll
+                            for (int t = 0; t < 32; t += 2) {
+                                m0 = fmaxf(m0, fabsf(__uint_as_float(v[t])));
+                                m1 = fmaxf(m1, fabsf(__uint_as_float(v[t + 1])));
+                            }
+                            const float b = fmaxf(m0, m1);
+                            bm[blk] = b;
+                            if (b > cmax) {
+                                cmax = b;
+                                sb = blk;
+#pragma unroll
+                                for (int cc = 0; cc < 8; ++cc)
+                                    *reinterpret_cast<uint4*>(slot + ((cc ^ swz) << 4)) =
+                                        make_uint4(v[4 * cc], v[4 * cc + 1], v[4 * cc + 2], v[4 * cc + 3]);
+                            }
+                        };
 #pragma unroll
                         for (int bp = 0; bp < 8; ++bp) {
                             const int c = bp >> 2;
@@ -376,57 +428,50 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
                             bm[2 * bp] = 0.f;
                             bm[2 * bp + 1] = 0.f;
                             if (c < a.nch && j0 < K) {
-                                uint32_t va[32];
                                 const uint32_t col = (uint32_t)((a.nch == 2 ? c : (g & 1)) * OT_N + (bp & 3) * 64);
 #pragma unroll
                                 for (int hh = 0; hh < 2; ++hh) {
+                                    uint32_t va[32];
                                     tmem_ld32(va, trow + col + (uint32_t)(32 * hh));
                                     tmem_wait_ld();
-                                    float m0 = 0.f, m1 = 0.f;
-#pragma unroll
-                                    for (int t = 0; t < 32; t += 2) {
-                                        m0 = fmaxf(m0, fabsf(__uint_as_float(va[t])));
-                                        m1 = fmaxf(m1, fabsf(__uint_as_float(va[t + 1])));
-                                    }
-                                    bm[2 * bp + hh] = fmaxf(m0, m1);
+                                    keep(va, 2 * bp + hh);
                                 }
                             }
                         }
-                        float cmax = 0.f;
-#pragma unroll
-                        for (int b = 0; b < 16; ++b) cmax = fmaxf(cmax, bm[b]);
                         win = OT_WIN * rn + 1e-6f * ynorm;
-                        if (act) thr = cmax - win;
+                        if (act) {
+                            thr = cmax - win;
+                            float v[32];
 #pragma unroll
-                        for (int blk = 0; blk < 16; ++blk) {
-                            const int c = blk >> 3;
-                            const int j0 = c * OT_N + (blk & 7) * 32;
-                            if (c < a.nch && j0 < K) {
-                                const bool mine = bm[blk] >= thr;
-                                if (__any_sync(SDB_FULL, mine)) {
-                                    uint32_t v[32];
-                                    const uint32_t col = (uint32_t)((a.nch == 2 ? c : (g & 1)) * OT_N + (blk & 7) * 32);
-                                    tmem_ld32(v, trow + col);
-                                    tmem_wait_ld();
-                                    if (mine) {
-                                        unsigned msk = 0u;
+                            for (int cc = 0; cc < 8; ++cc) {
+                                const float4 f = lds4(slot + ((cc ^ swz) << 4));
+                                v[4 * cc] = f.x;
+                                v[4 * cc + 1] = f.y;
+                                v[4 * cc + 2] = f.z;
+                                v[4 * cc + 3] = f.w;
+                            }
+                            extract(v, sb * 32);
+                        }
+                        // other blocks within the window (the lane's own need mask; the
+                        // warp re-reads the union of them)
+                        unsigned need = 0u;
 #pragma unroll
-                                        for (int t = 0; t < 32; ++t)
-                                            if (fabsf(__uint_as_float(v[t])) >= thr) msk |= 1u << t;
-                                        while (msk) {
-                                            const int j = j0 + __ffs(msk) - 1;
-                                            msk &= msk - 1u;
-                                            if (j < K && !in_support(j)) {
-                                                if (nc < OT_CMAX) {
+                        for (int blk = 0; blk < 16; ++blk)
+                            if ((blk >> 3) < a.nch && blk * 32 < K && bm[blk] >= thr && blk != sb) need |= 1u << blk;
+                        unsigned wneed = __reduce_or_sync(SDB_FULL, need);
+#pragma unroll 1
+                        while (wneed) {
+                            const int blk = __ffs(wneed) - 1;
+                            wneed &= wneed - 1u;
+                            uint32_t u[32];
+                            const uint32_t col = (uint32_t)((a.nch == 2 ? (blk >> 3) : (g & 1)) * OT_N + (blk & 7) * 32);
+                            tmem_ld32(u, trow + col);
+                            tmem_wait_ld();
+                            if ((need >> blk) & 1u) {
+                                float v[32];
 #pragma unroll
-                                                    for (int s = OT_CMAX - 1; s > 0; --s) cand[s] = cand[s - 1];
-                                                    cand[0] = j;
-                                                }
-                                                ++nc;
-                                            }
-                                        }
-                                    }
-                                }
+                                for (int t = 0; t < 32; ++t) v[t] = __uint_as_float(u[t]);
+                                extract(v, blk * 32);
                             }
                         }
                     }
@@ -459,9 +504,14 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
                         // so the listed candidates are refined instead of all K atoms
                         const bool noise = (thr + win) < 1e-6f * ynorm;
                         if (nc >= 1 && (nc <= OT_CMAX || noise)) {
+                            // one inlined refinement: the list is consumed from the front
+                            const int ncl = min(nc, OT_CMAX);
+#pragma unroll 1
+                            for (int s = 0; s < ncl; ++s) {
+                                consider(cand[0]);
 #pragma unroll
-                            for (int s = 0; s < OT_CMAX; ++s)
-                                if (s < nc) consider(cand[s]);
+                                for (int q = 0; q + 1 < OT_CMAX; ++q) cand[q] = cand[q + 1];
+                            }
                             // every non-candidate atom has |d.r| < thr + win/2
                             second = fmaxf(second, thr + 0.5f * win);
                         } else {
@@ -673,11 +723,11 @@ int omp_tc_f32(int64_t N, int m, int K, int P, const int64_t* off, const float* 
     // TMEM chunk buffers anyway) and the residual tiles fit next to the
     // dictionary; measured no faster than two at C4 (the tile-steps serialise
     // on the TMEM accumulator, and 128 registers spill), so opt-in only
-    const int smem3 = 1024 + a.nkb * kpad * 128 + 3 * a.nkb * OT_RB + 256;
+    const int smem3 = 1024 + a.nkb * kpad * 128 + 3 * (a.nkb * OT_RB + OT_M * 128) + 256;
     static const bool want3 = getenv("SDB_OMP_TC_3GRP") != nullptr;
     const bool three = want3 && nch == 2 && smem3 <= 232448;
     const int ng = three ? 3 : 2;
-    const int smem = 1024 + a.nkb * kpad * 128 + ng * a.nkb * OT_RB + 256;
+    const int smem = 1024 + a.nkb * kpad * 128 + ng * (a.nkb * OT_RB + OT_M * 128) + 256;
     int dev = 0;
     cudaGetDevice(&dev);
     int n_sm = 148;
