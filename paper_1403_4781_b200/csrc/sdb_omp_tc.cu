@@ -125,20 +125,23 @@ struct RoundIter {
     }
 };
 
-__device__ __forceinline__ float4 lds4(const unsigned char* p) { return *reinterpret_cast<const float4*>(p); }
 
-template <int CAP, int NG>
+// CAP: code slots; NG: signal groups; NKB: 32-column k-blocks of m (m_pad / 32);
+// NCH: 256-atom chunks of K
+template <int CAP, int NG, int NKB, int NCH>
 __global__ void __launch_bounds__((2 + 4 * NG) * 32, 1)
 k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
+    constexpr int KPAD = NCH * OT_N;
     // barriers: full[g] (MMA done / tile end ack), empty[b] (TMEM chunk buffer
     // free), rfull[g] (residual published), dfull (dictionary landed), dfree
     constexpr int B_FULL = 0, B_EMPTY = NG, B_RFULL = NG + 2, B_DFULL = 2 * NG + 2, B_DFREE = 2 * NG + 3;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* base = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    const int dbytes = a.nkb * a.kpad * 128;
-    const int rbytes = a.nkb * OT_RB;
+    constexpr int dbytes = NKB * KPAD * 128;
+    constexpr int rbytes = NKB * OT_RB;
     unsigned char* Ds = base;
-    // per-lane slots (128 B: the block of the running maximum), then the barriers
+    // per-lane slots (128 B: the block of the running maximum; chunk-major, 16 B
+    // of every lane side by side), then the barriers
     unsigned char* Sl = base + dbytes + NG * rbytes;
     uint64_t* bars = (uint64_t*)(Sl + NG * OT_M * 128);
     int* votes = (int*)(bars + 2 * NG + 4);   // [step parity][group][warp]
@@ -184,10 +187,10 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
                 if (k > 0) mbar_wait_sleep(smem_u32(&bars[B_DFREE]), (uint32_t)((k - 1) & 1));
                 const uint32_t bf = smem_u32(&bars[B_DFULL]);
                 mbar_expect_tx(bf, (uint32_t)dbytes);
-                for (int kb = 0; kb < a.nkb; ++kb)
-                    for (int c = 0; c < a.nch; ++c)
-                        tma_load_2d(smem_u32(Ds + kb * a.kpad * 128 + c * OT_N * 128), &tmD, kb * 32,
-                                    r.p * a.kpad + c * OT_N, bf);
+                for (int kb = 0; kb < NKB; ++kb)
+                    for (int c = 0; c < NCH; ++c)
+                        tma_load_2d(smem_u32(Ds + kb * KPAD * 128 + c * OT_N * 128), &tmD, kb * 32,
+                                    r.p * KPAD + c * OT_N, bf);
                 ++k;
             }
         }
@@ -223,15 +226,15 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
                             continue;
                         }
                         const unsigned char* Rg = base + dbytes + g * rbytes;
-                        for (int c = 0; c < a.nch; ++c) {
-                            const int b = a.nch == 2 ? c : (g & 1);
+                        for (int c = 0; c < NCH; ++c) {
+                            const int b = NCH == 2 ? c : (g & 1);
                             if (uses[b]) mbar_wait_sleep(smem_u32(&bars[B_EMPTY + b]), (uses[b] - 1) & 1u);
                             ++uses[b];
                             tmem_fence_after();
                             const uint32_t tacc = tmem + (uint32_t)(b * OT_N);
-                            for (int kb = 0; kb < a.nkb; ++kb) {
+                            for (int kb = 0; kb < NKB; ++kb) {
                                 const uint64_t ad = sw128_desc(smem_u32(Rg + kb * OT_RB));
-                                const uint64_t bd = sw128_desc(smem_u32(Ds + kb * a.kpad * 128 + c * OT_N * 128));
+                                const uint64_t bd = sw128_desc(smem_u32(Ds + kb * KPAD * 128 + c * OT_N * 128));
 #pragma unroll
                                 for (int kk = 0; kk < 4; ++kk)
                                     mma_tf32(tacc, ad + (uint64_t)(2 * kk), bd + (uint64_t)(2 * kk), idesc,
@@ -250,28 +253,29 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
         const int wi = (warp - 2) & 3;
         const int q = warp & 3;                 // TMEM lane quadrant of this warp
         const int row = q * 32 + lane;          // tile row = TMEM lane
-        unsigned char* R = base + dbytes + g * rbytes;
         const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
-        const int swz = row & 7;
-        unsigned char* slot = Sl + (g * OT_M + row) * 128;
+        // shared-space addresses: the lane's residual row (chunk cc of k-block kb at
+        // (rpre ^ (cc << 4)) + kb * OT_RB, 128-byte swizzle) and slot
+        const uint32_t ds_u32 = smem_u32(Ds);
+        const uint32_t rpre = (smem_u32(base + dbytes + g * rbytes) + (uint32_t)row * 128u) ^ ((uint32_t)(row & 7) << 4);
+        const uint32_t slot = smem_u32(Sl) + (uint32_t)(g * OT_M * 128 + row * 16);
         uint32_t fph = 0;
         int sp = 0;
         int k = 0;
         RoundIter<NG> it{a.ts, a.P, tb, te, -1};
         Round rd;
-        auto rrow = [&](int kb, int cc) -> unsigned char* { return R + kb * OT_RB + row * 128 + ((cc ^ swz) << 4); };
-        const uint32_t ds_u32 = smem_u32(Ds);
-        auto drow = [&](int kb, int j, int cc) -> const unsigned char* {
-            return Ds + kb * a.kpad * 128 + j * 128 + ((cc ^ (j & 7)) << 4);
-        };
+        // atom j's dictionary row: chunk cc of k-block kb at (dpre(j) ^ (cc << 4)) + kb * KPAD * 128
+        auto dpre = [&](int j) -> uint32_t { return (ds_u32 + ((uint32_t)j << 7)) ^ (((uint32_t)j & 7u) << 4); };
         // d_j . r (exact FP32, both operands in shared memory)
         auto dot = [&](int j) -> float {
             float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-            for (int kb = 0; kb < a.nkb; ++kb) {
+            const uint32_t dp = dpre(j);
+#pragma unroll
+            for (int kb = 0; kb < NKB; ++kb) {
 #pragma unroll
                 for (int cc = 0; cc < 8; ++cc) {
-                    const float4 d = lds4(drow(kb, j, cc));
-                    const float4 v = lds4(rrow(kb, cc));
+                    const float4 d = lds4_u32((dp ^ (uint32_t)(cc << 4)) + (uint32_t)(kb * KPAD * 128));
+                    const float4 v = lds4_u32((rpre ^ (uint32_t)(cc << 4)) + (uint32_t)(kb * OT_RB));
                     s0 = fmaf(d.x, v.x, s0);
                     s1 = fmaf(d.y, v.y, s1);
                     s2 = fmaf(d.z, v.z, s2);
@@ -314,7 +318,8 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
                 {
                     const float* yr = a.Y + i * a.ldy;
                     const bool vec = ((a.ldy & 3) == 0) && ((((uintptr_t)a.Y) & 15) == 0);
-                    for (int kb = 0; kb < a.nkb; ++kb) {
+#pragma unroll
+                    for (int kb = 0; kb < NKB; ++kb) {
 #pragma unroll
                         for (int cc = 0; cc < 8; ++cc) {
                             const int col = kb * 32 + cc * 4;
@@ -333,7 +338,7 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
                             ysq = fmaf(v.y, v.y, ysq);
                             ysq = fmaf(v.z, v.z, ysq);
                             ysq = fmaf(v.w, v.w, ysq);
-                            *reinterpret_cast<float4*>(rrow(kb, cc)) = v;
+                            sts4_u32((rpre ^ (uint32_t)(cc << 4)) + (uint32_t)(kb * OT_RB), v);
                         }
                     }
                 }
@@ -417,8 +422,8 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
                                 sb = blk;
 #pragma unroll
                                 for (int cc = 0; cc < 8; ++cc)
-                                    *reinterpret_cast<uint4*>(slot + ((cc ^ swz) << 4)) =
-                                        make_uint4(v[4 * cc], v[4 * cc + 1], v[4 * cc + 2], v[4 * cc + 3]);
+                                    sts4u_u32(slot + (uint32_t)(cc * OT_M * 16), v[4 * cc], v[4 * cc + 1], v[4 * cc + 2],
+                                              v[4 * cc + 3]);
                             }
                         };
 #pragma unroll
@@ -427,8 +432,8 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
                             const int j0 = c * OT_N + (bp & 3) * 64;
                             bm[2 * bp] = 0.f;
                             bm[2 * bp + 1] = 0.f;
-                            if (c < a.nch && j0 < K) {
-                                const uint32_t col = (uint32_t)((a.nch == 2 ? c : (g & 1)) * OT_N + (bp & 3) * 64);
+                            if (c < NCH && j0 < K) {
+                                const uint32_t col = (uint32_t)((NCH == 2 ? c : (g & 1)) * OT_N + (bp & 3) * 64);
 #pragma unroll
                                 for (int hh = 0; hh < 2; ++hh) {
                                     uint32_t va[32];
@@ -444,7 +449,7 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
                             float v[32];
 #pragma unroll
                             for (int cc = 0; cc < 8; ++cc) {
-                                const float4 f = lds4(slot + ((cc ^ swz) << 4));
+                                const float4 f = lds4_u32(slot + (uint32_t)(cc * OT_M * 16));
                                 v[4 * cc] = f.x;
                                 v[4 * cc + 1] = f.y;
                                 v[4 * cc + 2] = f.z;
@@ -457,14 +462,14 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
                         unsigned need = 0u;
 #pragma unroll
                         for (int blk = 0; blk < 16; ++blk)
-                            if ((blk >> 3) < a.nch && blk * 32 < K && bm[blk] >= thr && blk != sb) need |= 1u << blk;
+                            if ((blk >> 3) < NCH && blk * 32 < K && bm[blk] >= thr && blk != sb) need |= 1u << blk;
                         unsigned wneed = __reduce_or_sync(SDB_FULL, need);
 #pragma unroll 1
                         while (wneed) {
                             const int blk = __ffs(wneed) - 1;
                             wneed &= wneed - 1u;
                             uint32_t u[32];
-                            const uint32_t col = (uint32_t)((a.nch == 2 ? (blk >> 3) : (g & 1)) * OT_N + (blk & 7) * 32);
+                            const uint32_t col = (uint32_t)((NCH == 2 ? (blk >> 3) : (g & 1)) * OT_N + (blk & 7) * 32);
                             tmem_ld32(u, trow + col);
                             tmem_wait_ld();
                             if ((need >> blk) & 1u) {
@@ -479,7 +484,7 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
                     tmem_fence_before();
                     __syncwarp();
                     if (lane == 0) {
-                        for (int c = 0; c < a.nch; ++c) mbar_arrive(smem_u32(&bars[B_EMPTY + (a.nch == 2 ? c : (g & 1))]));
+                        for (int c = 0; c < NCH; ++c) mbar_arrive(smem_u32(&bars[B_EMPTY + (NCH == 2 ? c : (g & 1))]));
                     }
                     if (act) {
                         // ---------------- exact selection among the candidates
@@ -586,36 +591,40 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
                                 }
                                 const bool need_r = n < a.cap || a.rnorm != nullptr || a.eps > 0.f;
                                 if (need_r) {
-                                    // r -= D_S dx in place (the next MMA's A operand); the
-                                    // support rows' shared addresses are formed once
-                                    uint32_t dsa[CAP], dsw[CAP];
-#pragma unroll
-                                    for (int t = 0; t < CAP; ++t) {
-                                        const int jt = (t < n) ? ids[t] : 0;
-                                        dsa[t] = ds_u32 + (uint32_t)jt * 128u;
-                                        dsw[t] = (uint32_t)(jt & 7) << 4;
-                                    }
+                                    // r -= D_S dx in place (the next MMA's A operand), one
+                                    // k-block (32 floats in registers) at a time. Every active
+                                    // lane of the warp is at the same step, so the branches on
+                                    // t < n are uniform
                                     float r0 = 0.f, r1 = 0.f;
-                                    for (int kb = 0; kb < a.nkb; ++kb) {
 #pragma unroll
-                                        for (int cc = 0; cc < 8; ++cc) {
-                                            float4 v = lds4(rrow(kb, cc));
+                                    for (int kb = 0; kb < NKB; ++kb) {
+                                        float4 v[8];
 #pragma unroll
-                                            for (int t = 0; t < CAP; ++t) {
-                                                if (t < n) {
-                                                    const float4 d = lds4_u32(dsa[t] + (uint32_t)(kb * a.kpad * 128) +
-                                                                              (((uint32_t)cc << 4) ^ dsw[t]));
-                                                    v.x = fmaf(-dx[t], d.x, v.x);
-                                                    v.y = fmaf(-dx[t], d.y, v.y);
-                                                    v.z = fmaf(-dx[t], d.z, v.z);
-                                                    v.w = fmaf(-dx[t], d.w, v.w);
+                                        for (int cc = 0; cc < 8; ++cc)
+                                            v[cc] = lds4_u32((rpre ^ (uint32_t)(cc << 4)) + (uint32_t)(kb * OT_RB));
+#pragma unroll
+                                        for (int t = 0; t < CAP; ++t) {
+                                            if (t < n) {
+                                                const uint32_t dp = dpre(ids[t]);
+                                                const float c = -dx[t];
+#pragma unroll
+                                                for (int cc = 0; cc < 8; ++cc) {
+                                                    const float4 d = lds4_u32((dp ^ (uint32_t)(cc << 4)) +
+                                                                              (uint32_t)(kb * KPAD * 128));
+                                                    v[cc].x = fmaf(c, d.x, v[cc].x);
+                                                    v[cc].y = fmaf(c, d.y, v[cc].y);
+                                                    v[cc].z = fmaf(c, d.z, v[cc].z);
+                                                    v[cc].w = fmaf(c, d.w, v[cc].w);
                                                 }
                                             }
-                                            *reinterpret_cast<float4*>(rrow(kb, cc)) = v;
-                                            r0 = fmaf(v.x, v.x, r0);
-                                            r1 = fmaf(v.y, v.y, r1);
-                                            r0 = fmaf(v.z, v.z, r0);
-                                            r1 = fmaf(v.w, v.w, r1);
+                                        }
+#pragma unroll
+                                        for (int cc = 0; cc < 8; ++cc) {
+                                            sts4_u32((rpre ^ (uint32_t)(cc << 4)) + (uint32_t)(kb * OT_RB), v[cc]);
+                                            r0 = fmaf(v[cc].x, v[cc].x, r0);
+                                            r1 = fmaf(v[cc].y, v[cc].y, r1);
+                                            r0 = fmaf(v[cc].z, v[cc].z, r0);
+                                            r1 = fmaf(v[cc].w, v[cc].w, r1);
                                         }
                                     }
                                     rsq = r0 + r1;
@@ -732,7 +741,15 @@ int omp_tc_f32(int64_t N, int m, int K, int P, const int64_t* off, const float* 
     cudaGetDevice(&dev);
     int n_sm = 148;
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    auto fn = three ? (cap <= 4 ? k_omp_tc<4, 3> : k_omp_tc<8, 3>) : (cap <= 4 ? k_omp_tc<4, 2> : k_omp_tc<8, 2>);
+    using Fn = void (*)(const CUtensorMap, const OtArgs);
+    Fn fn = nullptr;
+#define SDB_OT_PICK(C, G, B, H) \
+    if ((cap <= 4 ? 4 : 8) == C && ng == G && a.nkb == B && nch == H) fn = k_omp_tc<C, G, B, H>;
+    SDB_OT_PICK(4, 2, 1, 1) SDB_OT_PICK(4, 2, 2, 1) SDB_OT_PICK(4, 2, 1, 2) SDB_OT_PICK(4, 2, 2, 2)
+    SDB_OT_PICK(8, 2, 1, 1) SDB_OT_PICK(8, 2, 2, 1) SDB_OT_PICK(8, 2, 1, 2) SDB_OT_PICK(8, 2, 2, 2)
+    SDB_OT_PICK(4, 3, 1, 2) SDB_OT_PICK(4, 3, 2, 2) SDB_OT_PICK(8, 3, 1, 2) SDB_OT_PICK(8, 3, 2, 2)
+#undef SDB_OT_PICK
+    if (fn == nullptr) return (int)cudaErrorNotSupported;
     cudaError_t e = set_max_smem((const void*)fn, smem);
     if (e != cudaSuccess) return (int)e;
     const int64_t max_tiles = (N + OT_M - 1) / OT_M + P;
