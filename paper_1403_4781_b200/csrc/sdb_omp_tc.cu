@@ -51,6 +51,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstdint>
+#include <type_traits>
 
 #include "sdb_common.cuh"
 #include "sdb_internal.h"
@@ -426,20 +427,27 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
                                               v[4 * cc + 3]);
                             }
                         };
+                        // the TMEM load of the next block is in flight while this one
+                        // is reduced (two register buffers)
+                        constexpr int NB = NCH * 8;
+                        const int nblk = ((K + 63) >> 6) << 1;   // blocks holding atoms (in pairs)
+                        auto tcol = [&](int blk) -> uint32_t {
+                            return trow + (uint32_t)((NCH == 2 ? (blk >> 3) : (g & 1)) * OT_N + (blk & 7) * 32);
+                        };
 #pragma unroll
-                        for (int bp = 0; bp < 8; ++bp) {
-                            const int c = bp >> 2;
-                            const int j0 = c * OT_N + (bp & 3) * 64;
-                            bm[2 * bp] = 0.f;
-                            bm[2 * bp + 1] = 0.f;
-                            if (c < NCH && j0 < K) {
-                                const uint32_t col = (uint32_t)((NCH == 2 ? c : (g & 1)) * OT_N + (bp & 3) * 64);
+                        for (int blk = 0; blk < 16; ++blk) bm[blk] = 0.f;
+                        {
+                            uint32_t va[32], vb[32];
+                            tmem_ld32(va, tcol(0));
 #pragma unroll
-                                for (int hh = 0; hh < 2; ++hh) {
-                                    uint32_t va[32];
-                                    tmem_ld32(va, trow + col + (uint32_t)(32 * hh));
+                            for (int blk = 0; blk < NB; blk += 2) {
+                                if (blk < nblk) {
                                     tmem_wait_ld();
-                                    keep(va, 2 * bp + hh);
+                                    tmem_ld32(vb, tcol(blk + 1));
+                                    keep(va, blk);
+                                    tmem_wait_ld();
+                                    if (blk + 2 < NB && blk + 2 < nblk) tmem_ld32(va, tcol(blk + 2));
+                                    keep(vb, blk + 1);
                                 }
                             }
                         }
@@ -534,61 +542,76 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
                             status = 3;
                             act = false;
                         } else {
-                            // ---------------- Cholesky append (_kernels.py:109-127)
-                            const float* __restrict__ Gb = Gp + (int64_t)bj * K;
-                            const float gbb = __ldg(Gb + bj);
-                            float gb[CAP];
+                            // ---------------- Cholesky append (_kernels.py:109-127) and the
+                            // solve (_kernels.py:129-139), specialised on the support size
+                            // n0 (every active lane of the warp is at the same step, so the
+                            // switch is uniform): static triangular indices, no padding terms
+                            float dx[CAP];
 #pragma unroll
-                            for (int t = 0; t < CAP; ++t) gb[t] = (t < n) ? __ldg(Gb + ids[t]) : 0.f;
-                            float c0b = eb;   // d_b.y = d_b.r + G[b,S] x
+                            for (int t = 0; t < CAP; ++t) dx[t] = 0.f;
+                            auto append = [&](auto nc) -> bool {
+                                constexpr int n0 = decltype(nc)::value;
+                                const float* __restrict__ Gb = Gp + (int64_t)bj * K;
+                                const float gbb = __ldg(Gb + bj);
+                                float gb[n0 + 1], w[n0 + 1];
 #pragma unroll
-                            for (int t = 0; t < CAP; ++t) c0b = fmaf(gb[t], x[t], c0b);
-                            float w[CAP];
-                            float dsq = gbb;
+                                for (int t = 0; t < n0; ++t) gb[t] = __ldg(Gb + ids[t]);
+                                float c0b = eb;   // d_b.y = d_b.r + G[b,S] x
 #pragma unroll
-                            for (int t = 0; t < CAP; ++t) {
-                                float acc = gb[t];
+                                for (int t = 0; t < n0; ++t) c0b = fmaf(gb[t], x[t], c0b);
+                                float dsq = gbb;
 #pragma unroll
-                                for (int u = 0; u < t; ++u) acc = fmaf(-L[t * (t + 1) / 2 + u], w[u], acc);
-                                w[t] = (t < n) ? acc * invd[t] : 0.f;
-                                dsq = fmaf(-w[t], w[t], dsq);
-                            }
-                            if (dsq <= a.guard) {   // numerically singular support Gram
-                                status = 2;
-                                act = false;
-                            } else {
+                                for (int t = 0; t < n0; ++t) {
+                                    float acc = gb[t];
+#pragma unroll
+                                    for (int u = 0; u < t; ++u) acc = fmaf(-L[t * (t + 1) / 2 + u], w[u], acc);
+                                    w[t] = acc * invd[t];
+                                    dsq = fmaf(-w[t], w[t], dsq);
+                                }
+                                if (dsq <= a.guard) return false;   // numerically singular support Gram
                                 const float inv = rsqrtf(dsq);
                                 float zn = c0b;
 #pragma unroll
-                                for (int t = 0; t < CAP; ++t) zn = fmaf(-w[t], z[t], zn);
+                                for (int t = 0; t < n0; ++t) zn = fmaf(-w[t], z[t], zn);
                                 zn *= inv;
 #pragma unroll
-                                for (int rr = 0; rr < CAP; ++rr) {
-                                    if (rr == n) {
-#pragma unroll
-                                        for (int t = 0; t < rr; ++t) L[rr * (rr + 1) / 2 + t] = w[t];
-                                        L[rr * (rr + 1) / 2 + rr] = dsq * inv;
-                                        invd[rr] = inv;
-                                        ids[rr] = bj;
-                                        z[rr] = zn;
-                                    }
-                                }
-                                ++n;
+                                for (int t = 0; t < n0; ++t) L[n0 * (n0 + 1) / 2 + t] = w[t];
+                                L[n0 * (n0 + 1) / 2 + n0] = dsq * inv;
+                                invd[n0] = inv;
+                                ids[n0] = bj;
+                                z[n0] = zn;
                                 // back substitution L^T x = z
-                                float xn[CAP], dx[CAP];
+                                float xn[n0 + 1];
 #pragma unroll
-                                for (int t = CAP - 1; t >= 0; --t) {
+                                for (int t = n0; t >= 0; --t) {
                                     float acc = z[t];
 #pragma unroll
-                                    for (int u = t + 1; u < CAP; ++u)
-                                        if (u < n) acc = fmaf(-L[u * (u + 1) / 2 + t], xn[u], acc);
-                                    xn[t] = (t < n) ? acc * invd[t] : 0.f;
+                                    for (int u = t + 1; u <= n0; ++u) acc = fmaf(-L[u * (u + 1) / 2 + t], xn[u], acc);
+                                    xn[t] = acc * invd[t];
                                 }
 #pragma unroll
-                                for (int t = 0; t < CAP; ++t) {
+                                for (int t = 0; t <= n0; ++t) {
                                     dx[t] = xn[t] - x[t];
                                     x[t] = xn[t];
                                 }
+                                return true;
+                            };
+                            bool ok = false;
+                            switch (n) {
+#define SDB_OT_CASE(I) \
+    case I:            \
+        if constexpr (I < CAP) ok = append(std::integral_constant<int, I>{}); \
+        break;
+                                SDB_OT_CASE(0) SDB_OT_CASE(1) SDB_OT_CASE(2) SDB_OT_CASE(3)
+                                SDB_OT_CASE(4) SDB_OT_CASE(5) SDB_OT_CASE(6) SDB_OT_CASE(7)
+#undef SDB_OT_CASE
+                                default: break;
+                            }
+                            if (!ok) {
+                                status = 2;
+                                act = false;
+                            } else {
+                                ++n;
                                 const bool need_r = n < a.cap || a.rnorm != nullptr || a.eps > 0.f;
                                 if (need_r) {
                                     // r -= D_S dx in place (the next MMA's A operand), one
