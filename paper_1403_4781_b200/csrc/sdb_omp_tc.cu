@@ -73,7 +73,7 @@ constexpr int OT_RB = OT_M * 128;  // bytes of one 32-column k-block of R
 
 struct OtArgs {
     int64_t N;
-    int m, K, P, cap, nkb, nch, kpad;
+    int m, K, P, cap, nkb, nch, kpad, clen;
     const int64_t* off;   // P+1 signal offsets
     const int64_t* ts;    // P+1 tile prefix (first tile of each shard)
     const float* Y;
@@ -97,31 +97,58 @@ __device__ __forceinline__ int tile_shard(const int64_t* __restrict__ ts, int P,
     return lo;
 }
 
-// A round: up to two consecutive tiles of one shard (one per signal group).
+// A round: up to NG consecutive tiles of one shard (one per signal group).
 struct Round {
     int p;
     int64_t t0;
     int cnt;            // tiles in this round (1..NG), one per signal group
-    bool first, last;
+    bool first, last;   // the CTA's first / last round on this shard's dictionary
 };
 
+// The (shard, tile) sequence is cut into chunks of `clen` consecutive tiles,
+// dealt round-robin to the CTAs: at any time the grid works on ~grid * clen
+// consecutive tiles (a few shards), so the Gram rows the Cholesky appends
+// gather stay in L2 (a contiguous range per CTA had ~100 shards' Gram matrices
+// live at once: 5.6 GB of HBM sector reads per C4 pass). Within a chunk the
+// shard index advances linearly; one binary search per chunk.
 template <int NG>
 struct RoundIter {
     const int64_t* ts;
-    int P;
-    int64_t pos, end;
-    int prev;
+    int P, clen;
+    int64_t ntiles, cnext, cstride;
+    int64_t pos, cend, pend;
+    int p, prev, pnext;
+    __device__ RoundIter(const int64_t* ts_, int P_, int clen_)
+        : ts(ts_), P(P_), clen(clen_), pos(0), cend(0), pend(0), p(0), prev(-1) {
+        ntiles = __ldg(ts + P);
+        cnext = (int64_t)blockIdx.x * clen;
+        cstride = (int64_t)gridDim.x * clen;
+        pnext = cnext < ntiles ? tile_shard(ts, P, cnext) : -1;
+    }
     __device__ bool next(Round& r) {
-        if (pos >= end) return false;
-        r.p = tile_shard(ts, P, pos);
-        const int64_t pend = __ldg(ts + r.p + 1);
+        if (pos >= cend) {
+            if (cnext >= ntiles) return false;
+            pos = cnext;
+            cend = min(ntiles, cnext + clen);
+            p = pnext;
+            pend = __ldg(ts + p + 1);
+            cnext += cstride;
+            pnext = cnext < ntiles ? tile_shard(ts, P, cnext) : -1;
+        } else {
+            while (pos >= pend) {   // next shard (empty shards own no tiles)
+                ++p;
+                pend = __ldg(ts + p + 1);
+            }
+        }
+        r.p = p;
         r.t0 = pos;
-        const int64_t lim = min(end, pend);
+        const int64_t lim = min(cend, pend);
         r.cnt = (int)min((int64_t)NG, lim - pos);
         pos += r.cnt;
-        r.first = r.p != prev;
-        prev = r.p;
-        r.last = pos >= end || pos >= pend;
+        r.first = p != prev;
+        prev = p;
+        // the dictionary is released when the CTA's next round is on another shard
+        r.last = pos >= cend ? (pnext != p) : (pos >= pend);
         return true;
     }
 };
@@ -151,11 +178,6 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int K = a.K;
 
-    const int64_t ntiles = __ldg(a.ts + a.P);
-    const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
-    const int64_t tb = min(ntiles, (int64_t)blockIdx.x * per);
-    const int64_t te = min(ntiles, tb + per);
-
     if (threadIdx.x == 0) {
         for (int g = 0; g < NG; ++g) {
             mbar_init(smem_u32(&bars[B_FULL + g]), 1);
@@ -180,7 +202,7 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
     if (warp == 0) {
         // ------------------------------------------------ dictionary producer
         if (lane == 0) {
-            RoundIter<NG> it{a.ts, a.P, tb, te, -1};
+            RoundIter<NG> it(a.ts, a.P, a.clen);
             Round r;
             int k = 0;
             while (it.next(r)) {
@@ -203,7 +225,7 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
             uint32_t uses[2] = {0, 0}, rph[NG];
             for (int g = 0; g < NG; ++g) rph[g] = 0;
             int k = 0;
-            RoundIter<NG> it{a.ts, a.P, tb, te, -1};
+            RoundIter<NG> it(a.ts, a.P, a.clen);
             Round r;
             while (it.next(r)) {
                 if (r.first) {
@@ -263,7 +285,7 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
         uint32_t fph = 0;
         int sp = 0;
         int k = 0;
-        RoundIter<NG> it{a.ts, a.P, tb, te, -1};
+        RoundIter<NG> it(a.ts, a.P, a.clen);
         Round rd;
         // atom j's dictionary row: chunk cc of k-block kb at (dpre(j) ^ (cc << 4)) + kb * KPAD * 128
         auto dpre = [&](int j) -> uint32_t { return (ds_u32 + ((uint32_t)j << 7)) ^ (((uint32_t)j & 7u) << 4); };
@@ -777,6 +799,23 @@ int omp_tc_f32(int64_t N, int m, int K, int P, const int64_t* off, const float* 
     if (e != cudaSuccess) return (int)e;
     const int64_t max_tiles = (N + OT_M - 1) / OT_M + P;
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(n_sm, max_tiles));
+    // chunk length of the round-robin tile assignment. Gram matrices that fit
+    // in L2 together: one contiguous range per CTA (fewest dictionary loads).
+    // Otherwise a few rounds per chunk, so the grid stays on a handful of
+    // shards: the longest of 1..4 rounds within 2% of the best balance
+    static const int clen_env = getenv("SDB_OMP_TC_CLEN") ? atoi(getenv("SDB_OMP_TC_CLEN")) : 0;
+    const int64_t per = (max_tiles + grid - 1) / grid;
+    int64_t clen = per;
+    if ((int64_t)P * K * K * 4 > (int64_t)16 << 20) {
+        auto worst = [&](int64_t c) { return ((max_tiles + c - 1) / c + grid - 1) / grid * c; };
+        int64_t best = INT64_MAX;
+        for (int r = 1; r <= 4; ++r) best = std::min(best, worst((int64_t)r * ng));
+        for (int r = 4; r >= 1; --r) {
+            clen = (int64_t)r * ng;
+            if (worst(clen) * 100 <= best * 102) break;
+        }
+    }
+    a.clen = clen_env > 0 ? clen_env : (int)std::min<int64_t>(clen, 1 << 30);
     fn<<<grid, (2 + 4 * ng) * 32, smem, st>>>(mD, a);
     return (int)cudaGetLastError();
 }

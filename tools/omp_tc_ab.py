@@ -74,6 +74,9 @@ def main():
             d = (a[key] != b[key])
             d = d.reshape(d.shape[0], -1).any(axis=1) if d.ndim > 1 else d
             print(f"DIFF {key}: {int(d.sum())} of {d.shape[0]} rows differ")
+            rows = np.nonzero(d)[0][:12]
+            print("   rows", rows.tolist(), "a", a[key][rows].reshape(len(rows), -1)[:, :4].tolist(),
+                  "b", b[key][rows].reshape(len(rows), -1)[:, :4].tolist())
     print("bitwise equal" if ok else "NOT bitwise equal")
 
 
