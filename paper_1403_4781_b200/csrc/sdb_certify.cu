@@ -26,6 +26,7 @@
 // entries; writes the FP64 code row.
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "sdb_common.cuh"
 #include "sdb_internal.h"
@@ -58,6 +59,96 @@ __device__ __forceinline__ double gsum(double v) {
 #pragma unroll
     for (int o = LPS / 2; o > 0; o >>= 1) v += __shfl_xor_sync(SDB_FULL, v, o, LPS);
     return v;
+}
+
+// 1 / sqrt(g) of a pivot: FP32 seed and two Newton steps in FP64 (to ~1 ulp;
+// a dozen instructions on the factorisation's critical path instead of the
+// library routine, which still serves pivots outside the FP32 range)
+__device__ __forceinline__ double pivot_rsqrt(double g) {
+    const float gf = (float)g;
+    if (!(gf > 1e-30f && gf < 1e30f)) return rsqrt(g);
+    double r = (double)rsqrtf(gf);
+    const double h = 0.5 * g;
+    r = fma(r, fma(-h * r, r, 0.5), r);
+    r = fma(r, fma(-h * r, r, 0.5), r);
+    return r;
+}
+
+// Sum of part[t] over the 8 lanes of a group, lane t receiving sum t: three
+// halving exchanges (4 + 2 + 1 values) instead of eight 3-stage butterflies
+__device__ __forceinline__ double gsum8_scatter(const double (&part)[8], int l) {
+    double q[4], r[2];
+    const bool b2 = l & 4, b1 = l & 2, b0 = l & 1;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const double send = b2 ? part[j] : part[j + 4];
+        const double keep = b2 ? part[j + 4] : part[j];
+        q[j] = keep + __shfl_xor_sync(SDB_FULL, send, 4, 8);
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const double send = b1 ? q[j] : q[j + 2];
+        const double keep = b1 ? q[j + 2] : q[j];
+        r[j] = keep + __shfl_xor_sync(SDB_FULL, send, 2, 8);
+    }
+    const double send = b0 ? r[0] : r[1];
+    const double keep = b0 ? r[1] : r[0];
+    return keep + __shfl_xor_sync(SDB_FULL, send, 1, 8);
+}
+
+// The n x n normal equations of one lane group: lane r holds row r of G_SS
+// (columns u <= r) in gr and b_r; returns x_r. Right-looking Cholesky (lane r
+// keeps row r: gr[k] -> L[r][k] for k < r; lane k keeps 1 / L[k][k], computed
+// once per pivot), forward substitution by broadcasts, back substitution
+// through the factor rows staged in shared memory (Ls, per lane group).
+template <int LPS>
+__device__ __forceinline__ double refit_solve(int n, int nmax, int l, int gbase, double b, double (&gr)[LPS],
+                                              double (*Ls)[LPS + 1]) {
+    double ik = 1.0;
+#pragma unroll
+    for (int k = 0; k < LPS; ++k) {
+        if (k < nmax) {                                // warp-uniform
+            const double gk = __shfl_sync(SDB_FULL, gr[k], gbase + k);   // lane k's pivot
+            const double rk = (k < n && gk > 0.0) ? pivot_rsqrt(gk) : 0.0;
+            if (l == k) ik = rk;
+            if (l > k) gr[k] *= rk;
+#pragma unroll
+            for (int c = k + 1; c < LPS; ++c) {
+                if (c < nmax) {
+                    const double lck = __shfl_sync(SDB_FULL, gr[k], gbase + c);   // L[c][k]
+                    if (l >= c && l < n) gr[c] = fma(-gr[k], lck, gr[c]);
+                }
+            }
+        }
+    }
+    // ---- forward L z = b (broadcasts), stage L rows for the back pass
+    double z = b;
+#pragma unroll
+    for (int k = 0; k < LPS; ++k) {
+        if (k < nmax) {
+            const double zk = __shfl_sync(SDB_FULL, z * ik, gbase + k);   // evaluated on lane k
+            if (l == k) z = zk;
+            if (l > k) z = fma(-gr[k], zk, z);
+        }
+    }
+    if (l < n) {
+#pragma unroll
+        for (int u = 0; u < LPS; ++u)
+            if (u < nmax) Ls[l][u] = gr[u];
+    }
+    __syncwarp();
+    // ---- back L^T x = z: lane k solves x_k once every x_j, j > k, is in
+    double acc = z;
+    double x = 0.0;
+#pragma unroll
+    for (int k = LPS - 1; k >= 0; --k) {
+        if (k < nmax) {
+            const double xk = __shfl_sync(SDB_FULL, acc * ik, gbase + k);
+            if (l == k) x = xk;
+            if (l < k && k < n) acc = fma(-Ls[k][l], xk, acc);
+        }
+    }
+    return x;
 }
 
 // One lane group of LPS lanes per signal; LPS is also the largest support
@@ -170,52 +261,7 @@ k_certify(CertArgs a) {
 #pragma unroll
         for (int u = 0; u < LPS; ++u)
             gr[u] = (u <= l && l < n) ? __ldg(Gp + (int64_t)my_atom * K + at[u]) : 0.0;
-        // ---- Cholesky (right-looking; lane r keeps row r: gr[k] -> L[r][k] for
-        // k < r; lane k keeps 1 / L[k][k] in ik, computed once per pivot)
-        double ik = 1.0;
-#pragma unroll
-        for (int k = 0; k < LPS; ++k) {
-            if (k < nmax) {                                // warp-uniform
-                const double gk = __shfl_sync(SDB_FULL, gr[k], gbase + k);   // lane k's pivot
-                const double rk = (k < n && gk > 0.0) ? rsqrt(gk) : 0.0;
-                if (l == k) ik = rk;
-                if (l > k) gr[k] *= rk;
-#pragma unroll
-                for (int c = k + 1; c < LPS; ++c) {
-                    if (c < nmax) {
-                        const double lck = __shfl_sync(SDB_FULL, gr[k], gbase + c);   // L[c][k]
-                        if (l >= c && l < n) gr[c] = fma(-gr[k], lck, gr[c]);
-                    }
-                }
-            }
-        }
-        // ---- forward L z = b (broadcasts), stage L rows for the back pass
-        double z = b;
-#pragma unroll
-        for (int k = 0; k < LPS; ++k) {
-            if (k < nmax) {
-                const double zk = __shfl_sync(SDB_FULL, z * ik, gbase + k);   // evaluated on lane k
-                if (l == k) z = zk;
-                if (l > k) z = fma(-gr[k], zk, z);
-            }
-        }
-        if (l < n) {
-#pragma unroll
-            for (int u = 0; u < LPS; ++u)
-                if (u < nmax) Ls[l][u] = gr[u];
-        }
-        __syncwarp();
-        // ---- back L^T x = z: lane k solves x_k once every x_j, j > k, is in
-        double acc = z;
-        double x = 0.0;
-#pragma unroll
-        for (int k = LPS - 1; k >= 0; --k) {
-            if (k < nmax) {
-                const double xk = __shfl_sync(SDB_FULL, acc * ik, gbase + k);
-                if (l == k) x = xk;
-                if (l < k && k < n) acc = fma(-Ls[k][l], xk, acc);
-            }
-        }
+        const double x = refit_solve<LPS>(n, nmax, l, gbase, b, gr, Ls);
         __syncwarp();
         // lane t holds x_t (n <= LPS here); slots past n, including those past
         // LPS when cap > LPS, are zeroed like the reference's
@@ -242,6 +288,154 @@ k_certify(CertArgs a) {
     }
 }
 
+// The same refit with the shard's FP64 dictionary resident in shared memory
+// (supports of at most 8 atoms, m <= 64): the gathers of the support rows --
+// 8 m n bytes per signal, the bulk of k_certify's L2 traffic -- become
+// shared-memory reads. A dictionary larger than the budget is taken in two
+// column halves (H = 2): pass 0 leaves the partial D_S^T y of every signal in
+// its (not yet written) output row, pass 1 adds the other half and solves.
+// Work: chunks of CS consecutive signals dealt round-robin to the CTAs (the
+// grid stays on a few shards, so the Gram entries come from L2); a chunk is
+// cut at shard boundaries and each piece loads its shard's dictionary.
+template <int WPB>
+__global__ void __launch_bounds__(WPB * 32, 1)
+k_certify_sm(CertArgs a, int H, int mh, int CS) {
+    constexpr int LPS = 8, GPW = 4;
+    extern __shared__ __align__(16) unsigned char cs_raw[];
+    double* dsm = reinterpret_cast<double*>(cs_raw);                       // K x mh
+    double (*sL)[LPS][LPS + 1] =
+        reinterpret_cast<double (*)[LPS][LPS + 1]>(dsm + (size_t)a.K * mh);   // per lane group
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int l = lane & (LPS - 1), g = lane / LPS;
+    const int gbase = g * LPS;
+    double (*Ls)[LPS + 1] = sL[wib * GPW + g];
+    const int m = a.m, K = a.K, cap = a.cap, P = a.P;
+    const int64_t nchunks = (a.N + CS - 1) / CS;
+    const int hp = mh >> 1;                       // double2 per dictionary row half
+    for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+        const int64_t lo = ch * CS, hi = min(a.N, lo + (int64_t)CS);
+        int p;
+        {
+            int blo = 0, bhi = P - 1;
+            while (blo < bhi) {
+                const int mid = (blo + bhi + 1) >> 1;
+                if (__ldg(a.off + mid) <= lo) blo = mid; else bhi = mid - 1;
+            }
+            p = blo;
+        }
+        for (int64_t s0 = lo; s0 < hi;) {
+            while (__ldg(a.off + p + 1) <= s0) ++p;       // empty shards own no signals
+            const int64_t s1 = min(hi, __ldg(a.off + p + 1));
+            const double* Dp = a.D + (int64_t)p * K * m;
+            const double* Gp = a.G + (int64_t)p * K * K;
+            for (int h = 0; h < H; ++h) {
+                const int c0 = h * mh;
+                __syncthreads();                          // the previous rows are no longer read
+                for (int e = threadIdx.x; e < K * hp; e += WPB * 32) {
+                    const int j = e / hp, c = c0 + 2 * (e - j * hp);
+                    double2 v = make_double2(0.0, 0.0);
+                    if (c < m) v = __ldg(reinterpret_cast<const double2*>(Dp + (int64_t)j * m + c));
+                    reinterpret_cast<double2*>(dsm)[e] = v;
+                }
+                __syncthreads();
+                const bool last = h == H - 1;
+                // header (count, status, margin, lane l's atom), signal values of
+                // this column range and (pass 1) the partial sum are requested one
+                // iteration ahead of their use
+                struct Pre {
+                    int n, atom;
+                    bool frag;
+                    double2 y[4];
+                    double bp;
+                };
+                auto fetch = [&](int64_t i) {
+                    Pre f;
+                    f.n = 0; f.atom = 0; f.frag = false; f.bp = 0.0;
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) f.y[v] = make_double2(0.0, 0.0);
+                    if (i < s1) {
+                        f.n = __ldg(a.counts + i);
+                        f.frag = __ldg(a.status + i) != 0 || f.n > LPS ||
+                                 (a.gap != nullptr && !(__ldg(a.gap + i) >= a.tau));
+                        if (l < cap) f.atom = __ldg(a.idx + i * cap + l);
+                        if (!f.frag) {
+#pragma unroll
+                            for (int v = 0; v < 4; ++v) {
+                                const int cl = 2 * l + 2 * LPS * v, c = c0 + cl;
+                                if (cl < mh && c < m) {
+                                    if (a.Y64) {
+                                        f.y[v] = __ldg(reinterpret_cast<const double2*>(a.Y64 + i * a.ldy + c));
+                                    } else {
+                                        const float2 t = __ldg(reinterpret_cast<const float2*>(a.Y + i * a.ldy + c));
+                                        f.y[v] = make_double2((double)t.x, (double)t.y);
+                                    }
+                                }
+                            }
+                            if (last && H > 1 && l < cap) f.bp = a.val[i * cap + l];
+                        }
+                    }
+                    return f;
+                };
+                Pre nxt = fetch(s0 + wib * GPW + g);
+                for (int64_t base = s0; base < s1; base += WPB * GPW) {
+                    const int64_t i = base + wib * GPW + g;
+                    const bool valid = i < s1;
+                    const Pre cur = nxt;
+                    nxt = fetch(i + WPB * GPW);
+                    int n = cur.n;
+                    if (cur.frag) {
+                        if (last && l == 0) {
+                            const int pos = atomicAdd(a.nlist, 1);
+                            a.list[pos] = (int32_t)i;
+                        }
+                        n = 0;
+                    }
+                    const bool work = valid && !cur.frag;
+                    const int my_atom = (l < n) ? cur.atom : 0;
+                    const int nmax = __reduce_max_sync(SDB_FULL, n);
+                    int at[LPS];
+#pragma unroll
+                    for (int t = 0; t < LPS; ++t) at[t] = __shfl_sync(SDB_FULL, my_atom, gbase + t);
+                    // ---- this column range's share of b = D_S^T y (lane l: pairs 2l + 16v)
+                    double part[LPS];
+#pragma unroll
+                    for (int t = 0; t < LPS; ++t) part[t] = 0.0;
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        const int cl = 2 * l + 2 * LPS * v;       // column within the range
+                        if (cl < mh) {                            // uniform in v
+#pragma unroll
+                            for (int t = 0; t < LPS; ++t) {
+                                if (t < nmax && t < n) {
+                                    const double2 d = *reinterpret_cast<const double2*>(dsm + (size_t)at[t] * mh + cl);
+                                    part[t] = fma(d.y, cur.y[v].y, fma(d.x, cur.y[v].x, part[t]));
+                                }
+                            }
+                        }
+                    }
+                    double b = gsum8_scatter(part, l);          // lane t: b_t
+                    if (!last) {
+                        // partial sums wait in the signal's output row
+                        if (work && l < cap) a.val[i * cap + l] = b;
+                        continue;
+                    }
+                    b += cur.bp;
+                    double gr[LPS];
+#pragma unroll
+                    for (int u = 0; u < LPS; ++u)
+                        gr[u] = (u <= l && l < n) ? __ldg(Gp + (int64_t)my_atom * K + at[u]) : 0.0;
+                    const double x = refit_solve<LPS>(n, nmax, l, gbase, b, gr, Ls);
+                    __syncwarp();
+                    if (work)
+                        for (int t = l; t < cap; t += LPS) a.val[i * cap + t] = (t < n) ? x : 0.0;
+                    __syncwarp();
+                }
+            }
+            s0 = s1;
+        }
+    }
+}
+
 template <int LPS, int VPL, int WPB>
 int launch_cert(const CertArgs& a, cudaStream_t st) {
     constexpr int GPW = 32 / LPS;
@@ -265,7 +459,35 @@ int certify_refit(int64_t N, int m, int K, int cap, int P, const int64_t* off, c
     CertArgs a{N, m, K, cap, P, off, Y, Y64, ldy, D, G, idx, counts, status, gap, tau, val, rnorm, list, nlist};
     // 8-lane groups whenever the supports are short (cap <= 8, or error-
     // bounded coding: the few longer supports are re-coded exactly)
-    if ((cap <= 8 || short_supports) && m <= 64) return launch_cert<8, 8, 8>(a, st);
+    if ((cap <= 8 || short_supports) && m <= 64) {
+        // dictionary-resident variant: 16-byte aligned rows, shards long enough
+        // to amortise the dictionary loads, no residual norms
+        static const bool sm_off = getenv("SDB_CERT_SM") != nullptr && atoi(getenv("SDB_CERT_SM")) == 0;
+        constexpr int WPB = 24;
+        const bool vec2 = (m % 2 == 0) && (ldy % 4 == 0) && ((reinterpret_cast<uintptr_t>(D) & 15) == 0) &&
+                          ((reinterpret_cast<uintptr_t>(Y64 ? (const void*)Y64 : (const void*)Y) & 15) == 0);
+        const int64_t budget = 160 * 1024;
+        int H = 1, mh = (m + 1) / 2 * 2;
+        if ((int64_t)K * mh * 8 > budget) {
+            H = 2;
+            mh = ((m + 1) / 2 + 15) / 16 * 16;
+        }
+        const int64_t dyn = (int64_t)K * mh * 8 + (int64_t)WPB * 4 * 8 * 9 * 8;
+        if (!sm_off && vec2 && rnorm == nullptr && N >= (int64_t)P * 1024 && (int64_t)K * mh * 8 <= budget &&
+            mh <= 64) {
+            cudaError_t e = set_max_smem((const void*)k_certify_sm<WPB>, (int)dyn);
+            if (e != cudaSuccess) return (int)e;
+            int dev = 0, n_sm = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+            const int CS = 4096;
+            const int64_t nchunks = (N + CS - 1) / CS;
+            const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(n_sm, nchunks));
+            k_certify_sm<WPB><<<grid, WPB * 32, dyn, st>>>(a, H, mh, CS);
+            return (int)cudaGetLastError();
+        }
+        return launch_cert<8, 8, 8>(a, st);
+    }
     if ((cap <= 8 || short_supports) && m <= 256) return launch_cert<8, 32, 8>(a, st);
     if (cap <= 16 && m <= 64) return launch_cert<16, 4, 8>(a, st);
     if (cap <= 16 && m <= 256) return launch_cert<16, 16, 4>(a, st);
