@@ -297,14 +297,17 @@ k_certify(CertArgs a) {
 // Work: chunks of CS consecutive signals dealt round-robin to the CTAs (the
 // grid stays on a few shards, so the Gram entries come from L2); a chunk is
 // cut at shard boundaries and each piece loads its shard's dictionary.
-template <int WPB>
+template <int WPB, int CS>
 __global__ void __launch_bounds__(WPB * 32, 1)
-k_certify_sm(CertArgs a, int H, int mh, int CS) {
-    constexpr int LPS = 8, GPW = 4;
+k_certify_sm(CertArgs a, int H, int mh) {
+    constexpr int LPS = 8, GPW = 4, NT = WPB * 32, KPT = (CS + NT - 1) / NT;
+    static_assert(CS <= 4096, "order entries: 12-bit local index + 3-bit count");
     extern __shared__ __align__(16) unsigned char cs_raw[];
     double* dsm = reinterpret_cast<double*>(cs_raw);                       // K x mh
     double (*sL)[LPS][LPS + 1] =
         reinterpret_cast<double (*)[LPS][LPS + 1]>(dsm + (size_t)a.K * mh);   // per lane group
+    __shared__ uint16_t order[CS];      // the segment's signals by support size: local index | (n - 1) << 12
+    __shared__ int hist[LPS + 2];       // signals per support size, then bin offsets; [LPS + 1]: total
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int l = lane & (LPS - 1), g = lane / LPS;
     const int gbase = g * LPS;
@@ -328,10 +331,57 @@ k_certify_sm(CertArgs a, int H, int mh, int CS) {
             const int64_t s1 = min(hi, __ldg(a.off + p + 1));
             const double* Dp = a.D + (int64_t)p * K * m;
             const double* Gp = a.G + (int64_t)p * K * K;
+            // ---- order the segment's signals by support size, so the four
+            // signals of a warp share their loop bounds (error-bounded coding
+            // mixes supports of 1 and of 8 atoms). Fragile signals go to the
+            // list, empty supports are zero-filled here; the order within a size
+            // is arbitrary (every signal's result is independent of it)
+            __syncthreads();                              // the previous segment's order is no longer read
+            if (threadIdx.x < LPS + 2) hist[threadIdx.x] = 0;
+            __syncthreads();
+            int keys[KPT];
+#pragma unroll
+            for (int q = 0; q < KPT; ++q) {
+                const int li = threadIdx.x + q * NT;
+                keys[q] = -1;
+                if (li < CS && s0 + li < s1) {
+                    const int64_t i = s0 + li;
+                    const int n = __ldg(a.counts + i);
+                    const bool frag = __ldg(a.status + i) != 0 || n > LPS ||
+                                      (a.gap != nullptr && !(__ldg(a.gap + i) >= a.tau));
+                    if (frag) {
+                        const int pos = atomicAdd(a.nlist, 1);
+                        a.list[pos] = (int32_t)i;
+                    } else if (n == 0) {
+                        for (int t = 0; t < cap; ++t) a.val[i * cap + t] = 0.0;
+                    } else {
+                        keys[q] = (n << 16) | atomicAdd(&hist[n], 1);
+                    }
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int run = 0;
+                for (int n = 1; n <= LPS; ++n) {
+                    const int c = hist[n];
+                    hist[n] = run;
+                    run += c;
+                }
+                hist[LPS + 1] = run;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < KPT; ++q) {
+                if (keys[q] >= 0) {
+                    const int n = keys[q] >> 16;
+                    order[hist[n] + (keys[q] & 0xffff)] = (uint16_t)((threadIdx.x + q * NT) | ((n - 1) << 12));
+                }
+            }
+            const int total = hist[LPS + 1];
             for (int h = 0; h < H; ++h) {
                 const int c0 = h * mh;
-                __syncthreads();                          // the previous rows are no longer read
-                for (int e = threadIdx.x; e < K * hp; e += WPB * 32) {
+                __syncthreads();                          // the previous rows are no longer read; order[] is complete
+                for (int e = threadIdx.x; e < K * hp; e += NT) {
                     const int j = e / hp, c = c0 + 2 * (e - j * hp);
                     double2 v = make_double2(0.0, 0.0);
                     if (c < m) v = __ldg(reinterpret_cast<const double2*>(Dp + (int64_t)j * m + c));
@@ -339,58 +389,49 @@ k_certify_sm(CertArgs a, int H, int mh, int CS) {
                 }
                 __syncthreads();
                 const bool last = h == H - 1;
-                // header (count, status, margin, lane l's atom), signal values of
-                // this column range and (pass 1) the partial sum are requested one
-                // iteration ahead of their use
+                // lane l's atom, the signal values of this column range and (pass 1)
+                // the partial sum are requested one iteration ahead of their use
                 struct Pre {
+                    int64_t i;
                     int n, atom;
-                    bool frag;
                     double2 y[4];
                     double bp;
                 };
-                auto fetch = [&](int64_t i) {
+                auto fetch = [&](int w) {
                     Pre f;
-                    f.n = 0; f.atom = 0; f.frag = false; f.bp = 0.0;
+                    f.i = 0; f.n = 0; f.atom = 0; f.bp = 0.0;
 #pragma unroll
                     for (int v = 0; v < 4; ++v) f.y[v] = make_double2(0.0, 0.0);
-                    if (i < s1) {
-                        f.n = __ldg(a.counts + i);
-                        f.frag = __ldg(a.status + i) != 0 || f.n > LPS ||
-                                 (a.gap != nullptr && !(__ldg(a.gap + i) >= a.tau));
+                    if (w < total) {
+                        const int o = order[w];
+                        const int64_t i = s0 + (o & 0xfff);
+                        f.i = i;
+                        f.n = (o >> 12) + 1;
                         if (l < cap) f.atom = __ldg(a.idx + i * cap + l);
-                        if (!f.frag) {
 #pragma unroll
-                            for (int v = 0; v < 4; ++v) {
-                                const int cl = 2 * l + 2 * LPS * v, c = c0 + cl;
-                                if (cl < mh && c < m) {
-                                    if (a.Y64) {
-                                        f.y[v] = __ldg(reinterpret_cast<const double2*>(a.Y64 + i * a.ldy + c));
-                                    } else {
-                                        const float2 t = __ldg(reinterpret_cast<const float2*>(a.Y + i * a.ldy + c));
-                                        f.y[v] = make_double2((double)t.x, (double)t.y);
-                                    }
+                        for (int v = 0; v < 4; ++v) {
+                            const int cl = 2 * l + 2 * LPS * v, c = c0 + cl;
+                            if (cl < mh && c < m) {
+                                if (a.Y64) {
+                                    f.y[v] = __ldg(reinterpret_cast<const double2*>(a.Y64 + i * a.ldy + c));
+                                } else {
+                                    const float2 t = __ldg(reinterpret_cast<const float2*>(a.Y + i * a.ldy + c));
+                                    f.y[v] = make_double2((double)t.x, (double)t.y);
                                 }
                             }
-                            if (last && H > 1 && l < cap) f.bp = a.val[i * cap + l];
                         }
+                        if (last && H > 1 && l < cap) f.bp = a.val[i * cap + l];
                     }
                     return f;
                 };
-                Pre nxt = fetch(s0 + wib * GPW + g);
-                for (int64_t base = s0; base < s1; base += WPB * GPW) {
-                    const int64_t i = base + wib * GPW + g;
-                    const bool valid = i < s1;
+                Pre nxt = fetch(wib * GPW + g);
+                for (int base = 0; base < total; base += WPB * GPW) {
+                    const int w = base + wib * GPW + g;
+                    const bool work = w < total;
                     const Pre cur = nxt;
-                    nxt = fetch(i + WPB * GPW);
-                    int n = cur.n;
-                    if (cur.frag) {
-                        if (last && l == 0) {
-                            const int pos = atomicAdd(a.nlist, 1);
-                            a.list[pos] = (int32_t)i;
-                        }
-                        n = 0;
-                    }
-                    const bool work = valid && !cur.frag;
+                    nxt = fetch(w + WPB * GPW);
+                    const int64_t i = cur.i;
+                    const int n = cur.n;
                     const int my_atom = (l < n) ? cur.atom : 0;
                     const int nmax = __reduce_max_sync(SDB_FULL, n);
                     int at[LPS];
@@ -412,6 +453,19 @@ k_certify_sm(CertArgs a, int H, int mh, int CS) {
                                 }
                             }
                         }
+                    }
+                    if (nmax <= 1) {
+                        // single-atom supports (warp-uniform): x = d.y / G_aa
+                        double b = gsum<LPS>(part[0]);
+                        if (!last) {
+                            if (work && l < cap) a.val[i * cap + l] = (l == 0) ? b : 0.0;
+                            continue;
+                        }
+                        if (l == 0) b += cur.bp;
+                        const double x = (work && l == 0) ? b / __ldg(Gp + (int64_t)my_atom * K + my_atom) : 0.0;
+                        if (work)
+                            for (int t = l; t < cap; t += LPS) a.val[i * cap + t] = (t == 0) ? x : 0.0;
+                        continue;
                     }
                     double b = gsum8_scatter(part, l);          // lane t: b_t
                     if (!last) {
@@ -475,15 +529,15 @@ int certify_refit(int64_t N, int m, int K, int cap, int P, const int64_t* off, c
         const int64_t dyn = (int64_t)K * mh * 8 + (int64_t)WPB * 4 * 8 * 9 * 8;
         if (!sm_off && vec2 && rnorm == nullptr && N >= (int64_t)P * 1024 && (int64_t)K * mh * 8 <= budget &&
             mh <= 64) {
-            cudaError_t e = set_max_smem((const void*)k_certify_sm<WPB>, (int)dyn);
+            constexpr int CS = 4096;
+            cudaError_t e = set_max_smem((const void*)k_certify_sm<WPB, CS>, (int)dyn);
             if (e != cudaSuccess) return (int)e;
             int dev = 0, n_sm = 148;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-            const int CS = 4096;
             const int64_t nchunks = (N + CS - 1) / CS;
             const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(n_sm, nchunks));
-            k_certify_sm<WPB><<<grid, WPB * 32, dyn, st>>>(a, H, mh, CS);
+            k_certify_sm<WPB, CS><<<grid, WPB * 32, dyn, st>>>(a, H, mh);
             return (int)cudaGetLastError();
         }
         return launch_cert<8, 8, 8>(a, st);
