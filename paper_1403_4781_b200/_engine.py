@@ -205,10 +205,36 @@ class DeviceCodes:
         return self.counts.shape[0]
 
 
-_pinned_perm: torch.Tensor | None = None
+class _PinnedRing:
+    """Two pinned staging buffers used in turn. The H2D copy out of a buffer
+    is asynchronous, so before the host overwrites a buffer it waits for the
+    copy issued from it two calls ago (an event); back-to-back trainings
+    without a device sync keep their host/device overlap and never race."""
+
+    def __init__(self, dtype):
+        self.dtype = dtype
+        self.buf = [None, None]
+        self.ev = [None, None]
+        self.k = 0
+
+    def take(self, n: int) -> torch.Tensor:
+        k = self.k = self.k ^ 1
+        if self.ev[k] is not None:
+            self.ev[k].synchronize()
+        if self.buf[k] is None or self.buf[k].numel() < n:
+            self.buf[k] = torch.empty((max(n, 1),), dtype=self.dtype, pin_memory=True)
+        return self.buf[k][:n]
+
+    def to_device(self, host: torch.Tensor) -> torch.Tensor:
+        out = host.to(device(), non_blocking=True)
+        if self.ev[self.k] is None:
+            self.ev[self.k] = torch.cuda.Event()
+        self.ev[self.k].record()
+        return out
 
 
-_pinned_js: torch.Tensor | None = None
+_pinned_perm = _PinnedRing(torch.int64)
+_pinned_js = _PinnedRing(torch.int32)
 
 
 def split_permutation(N: int, seed) -> torch.Tensor:
@@ -218,23 +244,18 @@ def split_permutation(N: int, seed) -> torch.Tensor:
     (native, multi-threaded, streamed into a pinned buffer); the device
     resolves the swaps in parallel (sdb_permutation_from_targets). Falls back
     to the all-host routine when the 32-bit draw path does not apply."""
-    global _pinned_perm, _pinned_js
     if 2 <= N <= 0x7fffffff:
-        if _pinned_js is None or _pinned_js.numel() < N - 1:
-            _pinned_js = torch.empty((N - 1,), dtype=torch.int32, pin_memory=True)
-        host = _pinned_js[:N - 1]
+        host = _pinned_js.take(N - 1)
         if _lib.swap_targets(N, seed, host.numpy()):
-            js = host.to(device(), non_blocking=True)
+            js = _pinned_js.to_device(host)
             wsb = _lib.load().sdb_permutation_workspace_bytes(N)
             ws = empty((wsb,), torch.uint8)
             perm = empty((N,), torch.int64)
             _lib.call("sdb_permutation_from_targets", N, ptr(js), ptr(perm), ptr(ws), wsb, stream())
             return perm
-    if _pinned_perm is None or _pinned_perm.numel() < N:
-        _pinned_perm = torch.empty((max(N, 1),), dtype=torch.int64, pin_memory=True)
-    host = _pinned_perm[:N]
+    host = _pinned_perm.take(N)
     _lib.permutation(N, seed, out=host.numpy())
-    return host.to(device(), non_blocking=True)
+    return _pinned_perm.to_device(host)
 
 
 def shard_offsets(sizes) -> tuple[torch.Tensor, int]:

@@ -297,16 +297,16 @@ k_certify(CertArgs a) {
 // Work: chunks of CS consecutive signals dealt round-robin to the CTAs (the
 // grid stays on a few shards, so the Gram entries come from L2); a chunk is
 // cut at shard boundaries and each piece loads its shard's dictionary.
-template <int WPB, int CS>
+template <int WPB, int CSMAX>
 __global__ void __launch_bounds__(WPB * 32, 1)
-k_certify_sm(CertArgs a, int H, int mh) {
-    constexpr int LPS = 8, GPW = 4, NT = WPB * 32, KPT = (CS + NT - 1) / NT;
-    static_assert(CS <= 4096, "order entries: 12-bit local index + 3-bit count");
+k_certify_sm(CertArgs a, int H, int mh, int CS) {
+    constexpr int LPS = 8, GPW = 4, NT = WPB * 32, KPT = (CSMAX + NT - 1) / NT;
+    static_assert(CSMAX <= 4096, "order entries: 12-bit local index + 3-bit count");
     extern __shared__ __align__(16) unsigned char cs_raw[];
     double* dsm = reinterpret_cast<double*>(cs_raw);                       // K x mh
     double (*sL)[LPS][LPS + 1] =
         reinterpret_cast<double (*)[LPS][LPS + 1]>(dsm + (size_t)a.K * mh);   // per lane group
-    __shared__ uint16_t order[CS];      // the segment's signals by support size: local index | (n - 1) << 12
+    __shared__ uint16_t order[CSMAX];   // the segment's signals by support size: local index | (n - 1) << 12
     __shared__ int hist[LPS + 2];       // signals per support size, then bin offsets; [LPS + 1]: total
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int l = lane & (LPS - 1), g = lane / LPS;
@@ -529,15 +529,22 @@ int certify_refit(int64_t N, int m, int K, int cap, int P, const int64_t* off, c
         const int64_t dyn = (int64_t)K * mh * 8 + (int64_t)WPB * 4 * 8 * 9 * 8;
         if (!sm_off && vec2 && rnorm == nullptr && N >= (int64_t)P * 1024 && (int64_t)K * mh * 8 <= budget &&
             mh <= 64) {
-            constexpr int CS = 4096;
-            cudaError_t e = set_max_smem((const void*)k_certify_sm<WPB, CS>, (int)dyn);
-            if (e != cudaSuccess) return (int)e;
+            constexpr int CSMAX = 4096;
             int dev = 0, n_sm = 148;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+            // chunks: the same number per CTA, whole lane-group rounds, at most
+            // CSMAX signals; short chunks would not amortise the dictionary
+            // loads -> the gather kernel
+            const int64_t rounds = ((N + n_sm - 1) / n_sm + CSMAX - 1) / CSMAX;     // chunks per CTA
+            const int64_t per = (N + n_sm * rounds - 1) / (n_sm * rounds);
+            const int CS = (int)std::min<int64_t>(CSMAX, (per + WPB * 4 - 1) / (WPB * 4) * (WPB * 4));
+            if (CS < 480) return launch_cert<8, 8, 8>(a, st);
+            cudaError_t e = set_max_smem((const void*)k_certify_sm<WPB, CSMAX>, (int)dyn);
+            if (e != cudaSuccess) return (int)e;
             const int64_t nchunks = (N + CS - 1) / CS;
             const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(n_sm, nchunks));
-            k_certify_sm<WPB, CS><<<grid, WPB * 32, dyn, st>>>(a, H, mh);
+            k_certify_sm<WPB, CSMAX><<<grid, WPB * 32, dyn, st>>>(a, H, mh, CS);
             return (int)cudaGetLastError();
         }
         return launch_cert<8, 8, 8>(a, st);
