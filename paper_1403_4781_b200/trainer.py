@@ -686,15 +686,17 @@ def split_merge_device(Ydev: torch.Tensor, L: int, K1: int, local_cap: int, loca
                             t_local - t_split, t_end - t_local, t_end - t_start, codings)
 
 
-HOST_GROUPS = int(os.environ.get("SDB_HOST_GROUPS", "4"))  # shard groups streamed from pinned host memory
+HOST_GROUPS = int(os.environ.get("SDB_HOST_GROUPS", "2"))  # shard groups streamed from pinned host memory (C4 e2e: 253 ms with 2, 258 with 3, 262 with 4)
 
 
 def auto_groups(L: int) -> int:
-    """Concurrent shard groups for device-resident split phases: with many
-    shards (C4: 256) four groups on their own streams overlap one group's
-    latency-bound MOD phases with another's coding (301.6 vs 316.0 ms per C4
-    job; 2 and 8 groups measured slower); few shards keep one batch."""
-    return 4 if L >= 128 else 1
+    """Concurrent shard groups for device-resident split phases. One batch:
+    every phase kernel now fills the SMs by itself (the fused OMP and the
+    dictionary-resident refit take a whole SM's shared memory), so groups on
+    their own streams no longer overlap anything (C4 job: 227.7 ms with one
+    batch, 225 ms +- outliers with two, 236 ms with four, 242 ms with eight;
+    four was best, 301.6 vs 316.0 ms, before those kernels)."""
+    return 1
 # 1/HEAD_DIV of a host batch is copied ahead (during the host permutation)
 HEAD_DIV = int(os.environ.get("SDB_HEAD_DIV", "8"))
 
