@@ -455,14 +455,22 @@ k_certify_sm(CertArgs a, int H, int mh, int CS) {
                         }
                     }
                     if (nmax <= 1) {
-                        // single-atom supports (warp-uniform): x = d.y / G_aa
+                        // single-atom supports (warp-uniform): x = (b / l) / l with
+                        // l = sqrt(G_aa), in the general path's operation order (which
+                        // path a one-atom signal takes depends on its warp mates, i.e. on
+                        // the arbitrary order within a size; the result must not)
                         double b = gsum<LPS>(part[0]);
                         if (!last) {
                             if (work && l < cap) a.val[i * cap + l] = (l == 0) ? b : 0.0;
                             continue;
                         }
                         if (l == 0) b += cur.bp;
-                        const double x = (work && l == 0) ? b / __ldg(Gp + (int64_t)my_atom * K + my_atom) : 0.0;
+                        double x = 0.0;
+                        if (work && l == 0) {
+                            const double gaa = __ldg(Gp + (int64_t)my_atom * K + my_atom);
+                            const double rk = gaa > 0.0 ? pivot_rsqrt(gaa) : 0.0;
+                            x = (b * rk) * rk;
+                        }
                         if (work)
                             for (int t = l; t < cap; t += LPS) a.val[i * cap + t] = (t == 0) ? x : 0.0;
                         continue;

@@ -128,3 +128,39 @@ def test_certified_fp32_on_fp64_inputs_is_the_reference():
     Ds, _, _ = sdb.train_standard(Y, cs)
     Dsr, _, _ = O.train_standard(Y, 48, 4, 4, "first-columns", 2, threads=8)
     assert np.linalg.norm(Ds - Dsr) / np.linalg.norm(Dsr) <= 1e-12
+
+
+@pytest.mark.parametrize("m,K,cap,eps", [(64, 256, 16, 0.35), (64, 512, 8, 0.0), (64, 512, 8, 0.3)])
+def test_dictionary_resident_refit_matches_fp64_and_is_reproducible(m, K, cap, eps):
+    """Launches large enough for the dictionary-resident refit (k_certify_sm:
+    signals ordered by support size within a chunk, single-atom fast path, two
+    column halves at K = 512): the reference's FP64 codes on mixed support
+    sizes, and bitwise the same values from run to run (the order within a
+    size is arbitrary; no result may depend on it)."""
+    from oracle import oracle as O
+    from paper_1403_4781_b200 import _engine as E
+    D = _dict(m, K, 3 * K + cap)
+    rng = np.random.default_rng(cap)
+    N = 90000
+    # supports of 0..6 atoms: error-bounded coding stops at different sizes
+    X = np.zeros((K, N))
+    sizes = rng.integers(0, 7, N)
+    for i in range(N):
+        X[rng.choice(K, sizes[i], replace=False), i] = rng.standard_normal(sizes[i])
+    Y = (D @ X + 0.01 * rng.standard_normal((m, N))).astype(np.float32).astype(np.float64)
+    Yd = torch.from_numpy(Y.T.astype(np.float32).copy()).to(E.device())
+    Dd = E.dict_to_device(D)
+    runs = []
+    for _ in range(3):
+        c = E.code_single_dict(Yd, Dd, cap, eps, "fp32")
+        assert c.vprec == "fp64"
+        runs.append((E.d2h(c.idx), E.d2h(c.val), E.d2h(c.counts)))
+    for idx, val, cnt in runs[1:]:
+        assert np.array_equal(idx, runs[0][0]) and np.array_equal(cnt, runs[0][2])
+        assert np.array_equal(val.view(np.uint64), runs[0][1].view(np.uint64)), "refit must be reproducible"
+    idx, val, cnt = runs[0]
+    ridx, rval, rcnt, rst, _ = O.omp_raw(Y, D, cap, eps, threads=8)
+    assert np.array_equal(cnt, rcnt)
+    assert np.array_equal(idx, ridx)
+    err = np.abs(val - rval).max() / np.abs(rval).max()
+    assert err <= 1e-10, err
