@@ -284,8 +284,31 @@ k_normal_eq(int P, int K, int m, const TY* __restrict__ Y, int64_t ldy, const in
 // registers and its X X^T row in a private shared-memory row, so there is no
 // cross-warp combine and no block barrier; the summation order is fixed by
 // the bucket order (deterministic).
-template <typename TY, typename T, int MPL>
-__global__ void __launch_bounds__(256)
+// a signal's 8 code slots with 16-byte loads (cap == 8: rows are 32 / 64 bytes)
+__device__ __forceinline__ void load_row8(const int32_t* __restrict__ p, int (&v)[8]) {
+    const int4 a = __ldg(reinterpret_cast<const int4*>(p)), b = __ldg(reinterpret_cast<const int4*>(p) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void load_row8(const double* __restrict__ p, double (&v)[8]) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const double2 a = __ldg(reinterpret_cast<const double2*>(p) + q);
+        v[2 * q] = a.x;
+        v[2 * q + 1] = a.y;
+    }
+}
+__device__ __forceinline__ void load_row8(const float* __restrict__ p, float (&v)[8]) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(p)), b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+
+// CAP8 (cap == 8): every entry's index row (the other atoms of its signal) is
+// requested with two 16-byte loads before the Y rows are walked, instead of
+// one dependent scalar load per (entry, slot) in front of each match.
+template <typename TY, typename T, int MPL, bool CAP8>
+__global__ void __launch_bounds__(256, (CAP8 && MPL <= 2) ? 4 : 1)
 k_normal_eq_w(int64_t PK, int K, int m, const TY* __restrict__ Y, int64_t ldy,
               const int64_t* __restrict__ bucket_off, int cap, const int32_t* __restrict__ idx,
               const T* __restrict__ val, const int32_t* __restrict__ counts, const int32_t* __restrict__ bent,
@@ -309,6 +332,15 @@ k_normal_eq_w(int64_t PK, int K, int m, const TY* __restrict__ Y, int64_t ldy,
         const int my_sig = my_e / cap;
         const double my_val = lane < nbat ? (double)val[my_e] : 0.0;
         const int my_n = lane < nbat ? counts[my_sig] : 0;
+        int bs[8];
+        if constexpr (CAP8) {
+            if (lane < nbat) {
+                load_row8(idx + (int64_t)my_sig * 8, bs);
+            } else {
+#pragma unroll
+                for (int t = 0; t < 8; ++t) bs[t] = -1;
+            }
+        }
         for (int j = 0; j < nbat; j += 4) {
             double yv[4][MPL];
             double vv[4];
@@ -331,14 +363,8 @@ k_normal_eq_w(int64_t PK, int K, int m, const TY* __restrict__ Y, int64_t ldy,
         diag += warp_sum(my_val * my_val);
         const int my_no = my_n > 1 ? my_n : 0;
         const int nmax = (int)__reduce_max_sync(SDB_FULL, (unsigned)my_no);
-        for (int t = 0; t < nmax; ++t) {
-            int b = -1;
-            double c = 0.0;
-            if (t < my_no) {
-                b = idx[(int64_t)my_sig * cap + t];
-                c = my_val * (double)val[(int64_t)my_sig * cap + t];
-                if (b == self) b = -1;
-            }
+        auto slot = [&](int b, double c) {
+            if (b == self) b = -1;
             const bool act = b >= 0;
             const unsigned peers = __match_any_sync(SDB_FULL, act ? b : K + lane);
             const int rank = __popc(peers & ((1u << lane) - 1u));
@@ -346,6 +372,25 @@ k_normal_eq_w(int64_t PK, int K, int m, const TY* __restrict__ Y, int64_t ldy,
             for (int r = 0; r < gmax; ++r) {
                 if (act && rank == r) row[b] += c;
                 __syncwarp();
+            }
+        };
+        if constexpr (CAP8) {
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                if (t < nmax) {                                  // warp-uniform
+                    const bool in = t < my_no;
+                    slot(in ? bs[t] : -1, in ? my_val * (double)val[(int64_t)my_sig * 8 + t] : 0.0);
+                }
+            }
+        } else {
+            for (int t = 0; t < nmax; ++t) {
+                int b = -1;
+                double c = 0.0;
+                if (t < my_no) {
+                    b = idx[(int64_t)my_sig * cap + t];
+                    c = my_val * (double)val[(int64_t)my_sig * cap + t];
+                }
+                slot(b, c);
             }
         }
         __syncwarp();
@@ -845,13 +890,18 @@ static int mod_update_impl(const ModArgs<T>& a, const TY* Ysrc, cudaStream_t st)
         if (PK >= (int64_t)148 * 32) {
             // enough buckets for a warp each
             const int smem = 8 * K * (int)sizeof(double);
-            if (smem > 48 * 1024) {
-                cudaError_t e = set_max_smem((const void*)k_normal_eq_w<TY, T, MPL>, smem);
-                if (e != cudaSuccess) return (int)e;
-            }
-            k_normal_eq_w<TY, T, MPL><<<(unsigned)((PK + 7) / 8), 256, smem, st>>>(
-                PK, K, m, Ysrc, a.ldy, w.bucket_off, cap, a.idx, a.val, a.counts, w.bent, w.B, w.A);
-            return (int)cudaGetLastError();
+            const bool cap8 = cap == 8 && (reinterpret_cast<uintptr_t>(a.idx) & 15) == 0 &&
+                              (reinterpret_cast<uintptr_t>(a.val) & 15) == 0;
+            auto go = [&](auto kern) -> int {
+                if (smem > 48 * 1024) {
+                    cudaError_t e = set_max_smem((const void*)kern, smem);
+                    if (e != cudaSuccess) return (int)e;
+                }
+                kern<<<(unsigned)((PK + 7) / 8), 256, smem, st>>>(PK, K, m, Ysrc, a.ldy, w.bucket_off, cap, a.idx,
+                                                                 a.val, a.counts, w.bent, w.B, w.A);
+                return (int)cudaGetLastError();
+            };
+            return cap8 ? go(k_normal_eq_w<TY, T, MPL, true>) : go(k_normal_eq_w<TY, T, MPL, false>);
         }
         const int smem = 8 * (K + 32 * MPL) * (int)sizeof(double);
         if (smem > 48 * 1024) {
