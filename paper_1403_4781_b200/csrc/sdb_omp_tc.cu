@@ -340,6 +340,16 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
                 float ysq = 0.0f;
                 {
                     const float* yr = a.Y + i * a.ldy;
+                    // the group's next tile (normally NG tiles on) is pulled into L2
+                    // while this one is coded
+                    {
+                        const int64_t inext = i + (int64_t)NG * OT_M;
+                        if (inext < a.N) {
+                            const float* yn = a.Y + inext * a.ldy;
+                            for (int c = 0; c < a.m; c += 32)
+                                asm volatile("prefetch.global.L2 [%0];" ::"l"(yn + c));
+                        }
+                    }
                     const bool vec = ((a.ldy & 3) == 0) && ((((uintptr_t)a.Y) & 15) == 0);
 #pragma unroll
                     for (int kb = 0; kb < NKB; ++kb) {

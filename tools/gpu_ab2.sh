@@ -1,4 +1,3 @@
-# A/B vs base of the fused OMP + its tests + bench check
+# A/B vs base of the fused OMP + its tests
 timeout 600 python tools/omp_tc_ab.py tools/_ab/libsdb200_base.so paper_1403_4781_b200/libsdb200.so > gpurun_out/ab.log 2>&1; echo ab rc=$?
-timeout 600 python -m pytest tests/test_gpu_omp_tc.py tests/test_gpu_certify.py -q --timeout 600 > gpurun_out/t_omp_tc.log 2>&1; echo tests rc=$?
-timeout 900 python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-extra > gpurun_out/bench_check.json 2> gpurun_out/bench_check.err; echo bench rc=$?
+timeout 600 python -m pytest tests/test_gpu_omp_tc.py -q --timeout 600 > gpurun_out/t_omp_tc.log 2>&1; echo tests rc=$?
