@@ -8,6 +8,7 @@ computes on the host.
 from __future__ import annotations
 
 import os
+import threading
 from dataclasses import dataclass
 
 import ctypes
@@ -135,6 +136,7 @@ UPLOAD_CHUNK = 8 << 20      # f64 elements per staged chunk (64 MB)
 UPLOAD_THREADS = int(os.environ.get("SDB_UPLOAD_THREADS", "8"))
 _upload_ring: list | None = None
 _upload_pool = None
+_upload_lock = threading.Lock()      # one staged upload at a time (the ring is shared)
 
 
 def upload_pageable(Yh: np.ndarray) -> torch.Tensor:
@@ -149,7 +151,8 @@ def upload_pageable(Yh: np.ndarray) -> torch.Tensor:
     out = empty((max(n, 1),), torch.float64)[:n]
     if n < 2 * UPLOAD_CHUNK or not flat.flags.c_contiguous:
         out.copy_(torch.from_numpy(np.ascontiguousarray(flat)))
-    else:
+        return torch.as_strided(out, Yh.shape, tuple(st // 8 for st in Yh.strides))
+    with _upload_lock:
         if _upload_ring is None:
             from concurrent.futures import ThreadPoolExecutor
             _upload_ring = [[torch.empty((UPLOAD_CHUNK,), dtype=torch.float64, pin_memory=True), None]
