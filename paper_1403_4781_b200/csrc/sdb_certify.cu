@@ -28,6 +28,8 @@
 #include <cstdint>
 #include <cstdlib>
 
+#include <type_traits>
+
 #include "sdb_common.cuh"
 #include "sdb_internal.h"
 
@@ -288,6 +290,67 @@ k_certify(CertArgs a) {
     }
 }
 
+__device__ __forceinline__ void load_row8i(const int32_t* __restrict__ p, int (&v)[8]) {
+    const int4 a = __ldg(reinterpret_cast<const int4*>(p)), b = __ldg(reinterpret_cast<const int4*>(p) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+
+// The n x n normal equations of ONE signal in one thread (n <= 8): G_SS from
+// L2 into a packed lower triangle, right-looking Cholesky, forward and back
+// substitution, all in registers, no shuffles. The arithmetic is refit_solve's
+// operation for operation (same fma operands, same pivot reciprocals), so the
+// coefficients are bitwise those of the lane-parallel solve; the diagonal
+// slots hold 1 / L[k][k].
+__device__ __forceinline__ void refit_solve_own(const double* __restrict__ Gp, int K, const int (&at)[8], int n,
+                                                double (&x)[8]) {
+    double L[36];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int u = 0; u <= r; ++u)
+            L[r * (r + 1) / 2 + u] = (r < n) ? __ldg(Gp + (int64_t)at[r] * K + at[u]) : 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        if (k < n) {
+            const double gk = L[k * (k + 1) / 2 + k];
+            const double rk = gk > 0.0 ? pivot_rsqrt(gk) : 0.0;
+            L[k * (k + 1) / 2 + k] = rk;
+#pragma unroll
+            for (int r = k + 1; r < 8; ++r)
+                if (r < n) L[r * (r + 1) / 2 + k] *= rk;
+#pragma unroll
+            for (int c = k + 1; c < 8; ++c) {
+                if (c < n) {
+                    const double lck = L[c * (c + 1) / 2 + k];
+#pragma unroll
+                    for (int r = c; r < 8; ++r)
+                        if (r < n) L[r * (r + 1) / 2 + c] = fma(-L[r * (r + 1) / 2 + k], lck, L[r * (r + 1) / 2 + c]);
+                }
+            }
+        }
+    }
+    // forward L z = b (x holds b on entry)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        if (k < n) {
+            x[k] *= L[k * (k + 1) / 2 + k];
+#pragma unroll
+            for (int r = k + 1; r < 8; ++r)
+                if (r < n) x[r] = fma(-L[r * (r + 1) / 2 + k], x[k], x[r]);
+        }
+    }
+    // back L^T x = z
+#pragma unroll
+    for (int k = 7; k >= 0; --k) {
+        if (k < n) {
+            x[k] *= L[k * (k + 1) / 2 + k];
+#pragma unroll
+            for (int r = 0; r < k; ++r) x[r] = fma(-L[k * (k + 1) / 2 + r], x[k], x[r]);
+        }
+    }
+}
+
 // The same refit with the shard's FP64 dictionary resident in shared memory
 // (supports of at most 8 atoms, m <= 64): the gathers of the support rows --
 // 8 m n bytes per signal, the bulk of k_certify's L2 traffic -- become
@@ -297,21 +360,22 @@ k_certify(CertArgs a) {
 // Work: chunks of CS consecutive signals dealt round-robin to the CTAs (the
 // grid stays on a few shards, so the Gram entries come from L2); a chunk is
 // cut at shard boundaries and each piece loads its shard's dictionary.
-template <int WPB, int CSMAX>
+template <int WPB, int CSMAX, bool F64IN>
 __global__ void __launch_bounds__(WPB * 32, 1)
 k_certify_sm(CertArgs a, int H, int mh, int CS) {
     constexpr int LPS = 8, GPW = 4, NT = WPB * 32, KPT = (CSMAX + NT - 1) / NT;
     static_assert(CSMAX <= 4096, "order entries: 12-bit local index + 3-bit count");
     extern __shared__ __align__(16) unsigned char cs_raw[];
     double* dsm = reinterpret_cast<double*>(cs_raw);                       // K x mh
-    double (*sL)[LPS][LPS + 1] =
-        reinterpret_cast<double (*)[LPS][LPS + 1]>(dsm + (size_t)a.K * mh);   // per lane group
+    // per warp: b = D_S^T y of the 32 signals of eight rounds (9 doubles apart: the
+    // owner threads' 8-byte reads are conflict-free)
+    double* stage_all = dsm + (size_t)a.K * mh;
     __shared__ uint16_t order[CSMAX];   // the segment's signals by support size: local index | (n - 1) << 12
     __shared__ int hist[LPS + 2];       // signals per support size, then bin offsets; [LPS + 1]: total
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int l = lane & (LPS - 1), g = lane / LPS;
     const int gbase = g * LPS;
-    double (*Ls)[LPS + 1] = sL[wib * GPW + g];
+    double* stg = stage_all + (size_t)wib * 32 * (LPS + 1);
     const int m = a.m, K = a.K, cap = a.cap, P = a.P;
     const int64_t nchunks = (a.N + CS - 1) / CS;
     const int hp = mh >> 1;                       // double2 per dictionary row half
@@ -394,14 +458,16 @@ k_certify_sm(CertArgs a, int H, int mh, int CS) {
                 struct Pre {
                     int64_t i;
                     int n, atom;
-                    double2 y[4];
+                    // FP32 rows stay raw until their use (a conversion here would wait
+                    // for the load one round early)
+                    typename std::conditional<F64IN, double2, float2>::type y[4];
                     double bp;
                 };
                 auto fetch = [&](int w) {
                     Pre f;
                     f.i = 0; f.n = 0; f.atom = 0; f.bp = 0.0;
 #pragma unroll
-                    for (int v = 0; v < 4; ++v) f.y[v] = make_double2(0.0, 0.0);
+                    for (int v = 0; v < 4; ++v) { f.y[v].x = 0; f.y[v].y = 0; }
                     if (w < total) {
                         const int o = order[w];
                         const int64_t i = s0 + (o & 0xfff);
@@ -412,11 +478,10 @@ k_certify_sm(CertArgs a, int H, int mh, int CS) {
                         for (int v = 0; v < 4; ++v) {
                             const int cl = 2 * l + 2 * LPS * v, c = c0 + cl;
                             if (cl < mh && c < m) {
-                                if (a.Y64) {
+                                if constexpr (F64IN) {
                                     f.y[v] = __ldg(reinterpret_cast<const double2*>(a.Y64 + i * a.ldy + c));
                                 } else {
-                                    const float2 t = __ldg(reinterpret_cast<const float2*>(a.Y + i * a.ldy + c));
-                                    f.y[v] = make_double2((double)t.x, (double)t.y);
+                                    f.y[v] = __ldg(reinterpret_cast<const float2*>(a.Y + i * a.ldy + c));
                                 }
                             }
                         }
@@ -445,52 +510,73 @@ k_certify_sm(CertArgs a, int H, int mh, int CS) {
                     for (int v = 0; v < 4; ++v) {
                         const int cl = 2 * l + 2 * LPS * v;       // column within the range
                         if (cl < mh) {                            // uniform in v
+                            const double yx = (double)cur.y[v].x, yy = (double)cur.y[v].y;
 #pragma unroll
                             for (int t = 0; t < LPS; ++t) {
                                 if (t < nmax && t < n) {
                                     const double2 d = *reinterpret_cast<const double2*>(dsm + (size_t)at[t] * mh + cl);
-                                    part[t] = fma(d.y, cur.y[v].y, fma(d.x, cur.y[v].x, part[t]));
+                                    part[t] = fma(d.y, yy, fma(d.x, yx, part[t]));
                                 }
                             }
                         }
                     }
+                    // lane t of the group: b_t (single-atom rounds, warp-uniform: one
+                    // butterfly, the same additions)
+                    double b;
                     if (nmax <= 1) {
-                        // single-atom supports (warp-uniform): x = (b / l) / l with
-                        // l = sqrt(G_aa), in the general path's operation order (which
-                        // path a one-atom signal takes depends on its warp mates, i.e. on
-                        // the arbitrary order within a size; the result must not)
-                        double b = gsum<LPS>(part[0]);
-                        if (!last) {
-                            if (work && l < cap) a.val[i * cap + l] = (l == 0) ? b : 0.0;
-                            continue;
-                        }
-                        if (l == 0) b += cur.bp;
-                        double x = 0.0;
-                        if (work && l == 0) {
-                            const double gaa = __ldg(Gp + (int64_t)my_atom * K + my_atom);
-                            const double rk = gaa > 0.0 ? pivot_rsqrt(gaa) : 0.0;
-                            x = (b * rk) * rk;
-                        }
-                        if (work)
-                            for (int t = l; t < cap; t += LPS) a.val[i * cap + t] = (t == 0) ? x : 0.0;
-                        continue;
+                        b = gsum<LPS>(part[0]);
+                        if (l != 0) b = 0.0;
+                    } else {
+                        b = gsum8_scatter(part, l);
                     }
-                    double b = gsum8_scatter(part, l);          // lane t: b_t
                     if (!last) {
                         // partial sums wait in the signal's output row
                         if (work && l < cap) a.val[i * cap + l] = b;
                         continue;
                     }
                     b += cur.bp;
-                    double gr[LPS];
+                    // ---- eight rounds fill the warp's stage (round k, group g ->
+                    // slot 4k + g); then thread 4k + g solves that signal's normal
+                    // equations on its own
+                    const int rnd = (base / (WPB * GPW)) & 7;
+                    if (work) stg[(rnd * GPW + g) * (LPS + 1) + l] = b;
+                    if (rnd == 7 || base + WPB * GPW >= total) {
+                        __syncwarp();
+                        const int w_own = base - rnd * (WPB * GPW) + (lane >> 2) * (WPB * GPW) + wib * GPW + (lane & 3);
+                        if ((lane >> 2) <= rnd && w_own < total) {
+                            const int o = order[w_own];
+                            const int64_t io = s0 + (o & 0xfff);
+                            const int no = (o >> 12) + 1;
+                            int at[8];
 #pragma unroll
-                    for (int u = 0; u < LPS; ++u)
-                        gr[u] = (u <= l && l < n) ? __ldg(Gp + (int64_t)my_atom * K + at[u]) : 0.0;
-                    const double x = refit_solve<LPS>(n, nmax, l, gbase, b, gr, Ls);
-                    __syncwarp();
-                    if (work)
-                        for (int t = l; t < cap; t += LPS) a.val[i * cap + t] = (t < n) ? x : 0.0;
-                    __syncwarp();
+                            for (int t = 0; t < 8; ++t) at[t] = 0;
+                            if (cap == 8) {
+                                load_row8i(a.idx + io * 8, at);
+                            } else {
+#pragma unroll
+                                for (int t = 0; t < 8; ++t)
+                                    if (t < cap) at[t] = __ldg(a.idx + io * cap + t);
+                            }
+#pragma unroll
+                            for (int t = 0; t < 8; ++t)
+                                if (t >= no) at[t] = 0;
+                            double x[8];
+#pragma unroll
+                            for (int t = 0; t < 8; ++t) x[t] = stg[lane * (LPS + 1) + t];
+                            refit_solve_own(Gp, K, at, no, x);
+                            if (cap == 8) {
+                                double2* o2 = reinterpret_cast<double2*>(a.val + io * 8);
+#pragma unroll
+                                for (int t = 0; t < 8; t += 2)
+                                    o2[t >> 1] = make_double2(t < no ? x[t] : 0.0, t + 1 < no ? x[t + 1] : 0.0);
+                            } else {
+#pragma unroll
+                                for (int t = 0; t < 8; ++t)
+                                    if (t < cap) a.val[io * cap + t] = (t < no) ? x[t] : 0.0;
+                            }
+                        }
+                        __syncwarp();
+                    }
                 }
             }
             s0 = s1;
@@ -525,7 +611,7 @@ int certify_refit(int64_t N, int m, int K, int cap, int P, const int64_t* off, c
         // dictionary-resident variant: 16-byte aligned rows, shards long enough
         // to amortise the dictionary loads, no residual norms
         static const bool sm_off = getenv("SDB_CERT_SM") != nullptr && atoi(getenv("SDB_CERT_SM")) == 0;
-        constexpr int WPB = 24;
+        constexpr int WPB = 16;
         const bool vec2 = (m % 2 == 0) && (ldy % 4 == 0) && ((reinterpret_cast<uintptr_t>(D) & 15) == 0) &&
                           ((reinterpret_cast<uintptr_t>(Y64 ? (const void*)Y64 : (const void*)Y) & 15) == 0);
         const int64_t budget = 160 * 1024;
@@ -548,11 +634,17 @@ int certify_refit(int64_t N, int m, int K, int cap, int P, const int64_t* off, c
             const int64_t per = (N + n_sm * rounds - 1) / (n_sm * rounds);
             const int CS = (int)std::min<int64_t>(CSMAX, (per + WPB * 4 - 1) / (WPB * 4) * (WPB * 4));
             if (CS < 480) return launch_cert<8, 8, 8>(a, st);
-            cudaError_t e = set_max_smem((const void*)k_certify_sm<WPB, CSMAX>, (int)dyn);
-            if (e != cudaSuccess) return (int)e;
             const int64_t nchunks = (N + CS - 1) / CS;
             const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(n_sm, nchunks));
-            k_certify_sm<WPB, CSMAX><<<grid, WPB * 32, dyn, st>>>(a, H, mh, CS);
+            if (Y64 != nullptr) {
+                cudaError_t e = set_max_smem((const void*)k_certify_sm<WPB, CSMAX, true>, (int)dyn);
+                if (e != cudaSuccess) return (int)e;
+                k_certify_sm<WPB, CSMAX, true><<<grid, WPB * 32, dyn, st>>>(a, H, mh, CS);
+            } else {
+                cudaError_t e = set_max_smem((const void*)k_certify_sm<WPB, CSMAX, false>, (int)dyn);
+                if (e != cudaSuccess) return (int)e;
+                k_certify_sm<WPB, CSMAX, false><<<grid, WPB * 32, dyn, st>>>(a, H, mh, CS);
+            }
             return (int)cudaGetLastError();
         }
         return launch_cert<8, 8, 8>(a, st);
