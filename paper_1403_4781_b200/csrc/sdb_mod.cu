@@ -307,8 +307,11 @@ __device__ __forceinline__ void load_row8(const float* __restrict__ p, float (&v
 // CAP8 (cap == 8): every entry's index row (the other atoms of its signal) is
 // requested with two 16-byte loads before the Y rows are walked, instead of
 // one dependent scalar load per (entry, slot) in front of each match.
-template <typename TY, typename T, int MPL, bool CAP8>
-__global__ void __launch_bounds__(256, (CAP8 && MPL <= 2) ? 4 : 1)
+// Y2 (float rows of exactly 64 values, 8-byte aligned): lane l walks columns
+// 2l, 2l + 1 with one 8-byte load per entry (half the load and
+// conversion instructions of the lane, lane + 32 walk).
+template <typename TY, typename T, int MPL, bool CAP8, bool Y2 = false>
+__global__ void __launch_bounds__(256, Y2 ? 4 : (CAP8 && MPL <= 2) ? 4 : 1)
 k_normal_eq_w(int64_t PK, int K, int m, const TY* __restrict__ Y, int64_t ldy,
               const int64_t* __restrict__ bucket_off, int cap, const int32_t* __restrict__ idx,
               const T* __restrict__ val, const int32_t* __restrict__ counts, const int32_t* __restrict__ bent,
@@ -341,6 +344,25 @@ k_normal_eq_w(int64_t PK, int K, int m, const TY* __restrict__ Y, int64_t ldy,
                 for (int t = 0; t < 8; ++t) bs[t] = -1;
             }
         }
+        if constexpr (Y2) {
+            for (int j = 0; j < nbat; j += 4) {
+                float2 yv[4];
+                const bool full = j + 4 <= nbat;   // warp-uniform
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int i = __shfl_sync(SDB_FULL, my_sig, (j + u) & 31);
+                    yv[u] = make_float2(0.f, 0.f);
+                    if (full || j + u < nbat)
+                        yv[u] = __ldg(reinterpret_cast<const float2*>(Y + (int64_t)i * ldy) + lane);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const double v = __shfl_sync(SDB_FULL, my_val, (j + u) & 31);
+                    acc[0] = fma((double)yv[u].x, v, acc[0]);
+                    acc[1] = fma((double)yv[u].y, v, acc[1]);
+                }
+            }
+        } else
         for (int j = 0; j < nbat; j += 4) {
             double yv[4][MPL];
             double vv[4];
@@ -398,10 +420,14 @@ k_normal_eq_w(int64_t PK, int K, int m, const TY* __restrict__ Y, int64_t ldy,
     if (lane == 0) row[self] += diag;
     __syncwarp();
     double* outB = B + e * m;
+    if constexpr (Y2) {
+        reinterpret_cast<double2*>(outB)[lane] = make_double2(acc[0], acc[1]);
+    } else {
 #pragma unroll
-    for (int q = 0; q < MPL; ++q) {
-        const int r = lane + 32 * q;
-        if (r < m) outB[r] = acc[q];
+        for (int q = 0; q < MPL; ++q) {
+            const int r = lane + 32 * q;
+            if (r < m) outB[r] = acc[q];
+        }
     }
     double* outA = A + e * K;
     for (int b = lane; b < K; b += 32) outA[b] = row[b];
@@ -901,6 +927,11 @@ static int mod_update_impl(const ModArgs<T>& a, const TY* Ysrc, cudaStream_t st)
                                                                  a.val, a.counts, w.bent, w.B, w.A);
                 return (int)cudaGetLastError();
             };
+            if constexpr (std::is_same<TY, float>::value && MPL == 2) {
+                if (cap8 && m == 64 && (a.ldy & 1) == 0 && (reinterpret_cast<uintptr_t>(Ysrc) & 7) == 0 &&
+                    (reinterpret_cast<uintptr_t>(w.B) & 15) == 0)
+                    return go(k_normal_eq_w<TY, T, MPL, true, true>);
+            }
             return cap8 ? go(k_normal_eq_w<TY, T, MPL, true>) : go(k_normal_eq_w<TY, T, MPL, false>);
         }
         const int smem = 8 * (K + 32 * MPL) * (int)sizeof(double);
