@@ -67,6 +67,11 @@ int sdb_cast(int dtype, int64_t n, const double *src, void *dst, void *stream);
  * F64: bitwise identical to the reference. */
 int sdb_gram(int dtype, int64_t P, int64_t m, int64_t K, const double *D64, void *G, void *stream);
 
+/* The same Gram matrix in both precisions from one pass (certified FP32 mode:
+ * the coding kernels read G32, the certification G64): G32 = (float)G64, bitwise
+ * what sdb_gram(SDB_F32) returns. */
+int sdb_gram_pair(int64_t P, int64_t m, int64_t K, const double *D64, double *G64, float *G32, void *stream);
+
 /* alpha0[i, j] = <d_j, y_i> with d from the shard of i: the c0 = D^T y loop of
  * omp_single (_kernels.py:54-59) for every signal at once. F64: bitwise
  * identical sequential sums. F32: tcgen05 3xTF32 GEMM when use_tc != 0 and the

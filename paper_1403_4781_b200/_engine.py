@@ -230,6 +230,16 @@ def gram(D64: torch.Tensor, prec: str) -> torch.Tensor:
     return G
 
 
+def gram_pair(D64: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+    """(G32, G64) of one pass over the dictionaries (certified FP32 mode); G32 is
+    bitwise gram(D64, "fp32")."""
+    P, K, m = D64.shape
+    G64 = empty((P, K, K), torch.float64)
+    G32 = empty((P, K, K), torch.float32)
+    _lib.call("sdb_gram_pair", P, m, K, ptr(D64), ptr(G64), ptr(G32), stream())
+    return G32, G64
+
+
 # ---------------------------------------------------------------- coding
 @dataclass
 class DeviceCodes:
@@ -435,12 +445,16 @@ def code_shards(S: "ShardSet", D64: torch.Tensor, cap: int, eps: float, use_tc: 
     """The training loop's coding pass over every shard: FP32 kernels plus the
     FP64 certification in certified mode, the plain kernels otherwise."""
     prec = S.prec
-    codes = code(S.Y, S.off, S.max_rows, working_dict(D64, prec), gram(D64, prec), cap, eps, prec, use_tc,
+    if certifies(prec):
+        G, G64 = gram_pair(D64)
+    else:
+        G, G64 = gram(D64, prec), None
+    codes = code(S.Y, S.off, S.max_rows, working_dict(D64, prec), G, cap, eps, prec, use_tc,
                  ysq=S.signal_sq(), want_rnorm=want_rnorm and not certifies(prec),
                  want_gap=certifies(prec))
     if not certifies(prec):
         return codes
-    return certify(S.Y, S.off, D64, gram(D64, "fp64"), codes, eps, want_rnorm,
+    return certify(S.Y, S.off, D64, G64, codes, eps, want_rnorm,
                    Y64=S._exact.Y if (S._exact is not None and S._exact_auth) else None)
 
 
@@ -460,15 +474,16 @@ def code_single_dict(Ydev, D64, cap, eps, prec, use_tc=True, want_rnorm=True, Y6
     authoritative FP64 rows when Ydev rounds them (certified mode)."""
     N = Ydev.shape[0]
     DT = working_dict(D64, prec)
-    G = gram(D64, prec)
+    cert = certifies(prec)
+    if cert:
+        G, G64 = gram_pair(D64)
+    else:
+        G = gram(D64, prec)
     K = D64.shape[1]
     rows = alpha_chunk_rows(K, prec)
     ysq = None
     if not want_rnorm and prec == "fp32" and eps > 0.0:
         ysq = signal_sq(Ydev)
-    cert = certifies(prec)
-    if cert:
-        G64 = gram(D64, "fp64")
     if N <= rows:
         off, mx = shard_offsets([N])
         c = code(Ydev, off, mx, DT, G, cap, eps, prec, use_tc, ysq=ysq, want_rnorm=want_rnorm and not cert,

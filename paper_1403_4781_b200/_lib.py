@@ -30,6 +30,7 @@ SIGNATURES = {
     "sdb_ingest": (c_int, [c_int, c_i64, c_i64, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp]),
     "sdb_cast": (c_int, [c_int, c_i64, c_vp, c_vp, c_vp]),
     "sdb_gram": (c_int, [c_int, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
+    "sdb_gram_pair": (c_int, [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "sdb_correlate_workspace_bytes": (c_i64, [c_int, c_i64, c_i64, c_i64]),
     "sdb_correlate": (c_int, [c_int, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp,
                               c_vp, c_i64, c_int, c_vp, c_i64, c_vp]),
@@ -102,7 +103,7 @@ class NativeError(RuntimeError):
 
 _lib = None
 # must equal sdb_abi_version() in csrc/sdb_capi.cu (bumped whenever exports change)
-ABI_VERSION = 11
+ABI_VERSION = 12
 
 
 def load():

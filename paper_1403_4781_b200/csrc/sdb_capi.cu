@@ -55,7 +55,7 @@ __global__ void k_cast(int64_t n, const double* __restrict__ src, T* __restrict_
 
 extern "C" {
 
-int sdb_abi_version(void) { return 11; }
+int sdb_abi_version(void) { return 12; }
 const char* sdb_last_error(void) { return g_err.c_str(); }
 
 int sdb_device_cc(void) {
@@ -95,6 +95,12 @@ int sdb_gram(int dtype, int64_t P, int64_t m, int64_t K, const double* D64, void
     int rc = dtype == SDB_F64 ? sdb::gram_f64(D64, (int)P, m, K, (double*)G, S(stream))
                               : sdb::gram_f32(D64, (int)P, m, K, (float*)G, S(stream));
     return cuda_rc(rc, "sdb_gram");
+}
+
+int sdb_gram_pair(int64_t P, int64_t m, int64_t K, const double* D64, double* G64, float* G32, void* stream) {
+    if (P < 1 || m < 1 || K < 1 || G64 == nullptr || G32 == nullptr)
+        return fail(SDB_EINVAL, "sdb_gram_pair: bad args");
+    return cuda_rc(sdb::gram_f64_f32(D64, (int)P, m, K, G64, G32, S(stream)), "sdb_gram_pair");
 }
 
 int64_t sdb_correlate_workspace_bytes(int dtype, int64_t P, int64_t m, int64_t K) {

@@ -28,7 +28,8 @@ template <typename TIn, typename TOut>
 __global__ void __launch_bounds__(256)
 k_rowdot(const TIn* __restrict__ A, int64_t lda, const int64_t* __restrict__ a_off,
          int64_t a_rows_per_shard, const TIn* __restrict__ B, int64_t ldb, int64_t b_stride,
-         int64_t nb, int64_t kdim, TOut* __restrict__ C, int64_t ldc, bool sym) {
+         int64_t nb, int64_t kdim, TOut* __restrict__ C, int64_t ldc, bool sym,
+         float* __restrict__ C32 = nullptr) {
     // sym (Gram, A == B per shard): only tiles on or above the diagonal are
     // computed; an upper tile also writes its mirror (products commute, so the
     // mirrored entry is bitwise the one its own tile would compute)
@@ -86,6 +87,10 @@ k_rowdot(const TIn* __restrict__ A, int64_t lda, const int64_t* __restrict__ a_o
             if (gb < nb) {
                 C[ga * ldc + gb] = (TOut)acc[i][j];
                 if (sym && blockIdx.y > blockIdx.x) C[(a_lo + gb) * ldc + (ga - a_lo)] = (TOut)acc[i][j];
+                if (C32 != nullptr) {   // the same sums rounded once to FP32 (the coding kernels' copy)
+                    C32[ga * ldc + gb] = (float)acc[i][j];
+                    if (sym && blockIdx.y > blockIdx.x) C32[(a_lo + gb) * ldc + (ga - a_lo)] = (float)acc[i][j];
+                }
             }
         }
     }
@@ -95,15 +100,20 @@ template <typename TIn, typename TOut>
 static int launch_rowdot(const TIn* A, int64_t lda, const int64_t* a_off, int64_t a_rows_max,
                          int64_t a_rows_per_shard, const TIn* B, int64_t ldb, int64_t b_stride,
                          int64_t nb, int64_t kdim, TOut* C, int64_t ldc, int P,
-                         cudaStream_t st, bool sym = false) {
+                         cudaStream_t st, bool sym = false, float* C32 = nullptr) {
     if (a_rows_max <= 0 || nb <= 0 || P <= 0) return 0;
     dim3 grid((unsigned)((a_rows_max + RD_BM - 1) / RD_BM), (unsigned)((nb + RD_BN - 1) / RD_BN),
               (unsigned)P);
     k_rowdot<TIn, TOut><<<grid, 256, 0, st>>>(A, lda, a_off, a_rows_per_shard, B, ldb, b_stride,
-                                              nb, kdim, C, ldc, sym);
+                                              nb, kdim, C, ldc, sym, C32);
     return (int)cudaGetLastError();
 }
 
+// G64 = D^T D in FP64 and G32 = (float)G64 from one pass (gram_f32 rounds the
+// same FP64 sums, so G32 is bitwise gram_f32's)
+int gram_f64_f32(const double* D, int P, int64_t m, int64_t K, double* G64, float* G32, cudaStream_t st) {
+    return launch_rowdot<double, double>(D, m, nullptr, K, K, D, m, K * m, K, m, G64, K, P, st, true, G32);
+}
 int gram_f64(const double* D, int P, int64_t m, int64_t K, double* G, cudaStream_t st) {
     return launch_rowdot<double, double>(D, m, nullptr, K, K, D, m, K * m, K, m, G, K, P, st, true);
 }

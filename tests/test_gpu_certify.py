@@ -164,3 +164,17 @@ def test_dictionary_resident_refit_matches_fp64_and_is_reproducible(m, K, cap, e
     assert np.array_equal(idx, ridx)
     err = np.abs(val - rval).max() / np.abs(rval).max()
     assert err <= 1e-10, err
+
+
+@pytest.mark.parametrize("P,m,K", [(3, 64, 512), (2, 36, 200), (1, 144, 576), (5, 17, 70)])
+def test_gram_pair_is_both_grams_bitwise(P, m, K):
+    """sdb_gram_pair: one pass gives the FP64 Gram (bitwise sdb_gram F64) and its
+    FP32 rounding (bitwise sdb_gram F32)."""
+    from paper_1403_4781_b200 import _engine as E
+    g = torch.Generator(device=E.device()).manual_seed(5)
+    D = torch.randn(P, K, m, device=E.device(), dtype=torch.float64, generator=g)
+    D /= D.norm(dim=2, keepdim=True)
+    G32, G64 = E.gram_pair(D)
+    assert torch.equal(G64, E.gram(D, "fp64"))
+    assert torch.equal(G32, E.gram(D, "fp32"))
+    assert torch.equal(G64, G64.transpose(1, 2))
