@@ -56,6 +56,7 @@ int perm_from_targets(int64_t n, const uint32_t* js, int64_t* perm, void* ws, in
                       cudaStream_t st);
 int signal_sq_f32(int64_t N, int m, const float* Y, int64_t ldy, float* out, cudaStream_t st);
 int gram_f32(const double* D, int P, int64_t m, int64_t K, float* G, cudaStream_t st);
+int gram_screen_f32(const float* D, int P, int64_t m, int64_t K, float* G, cudaStream_t st);
 int gram_f64_f32(const double* D, int P, int64_t m, int64_t K, double* G64, float* G32, cudaStream_t st);
 int correlate_simt_f64(const double* Y, int64_t ldy, const int64_t* off, int64_t max_rows, int P,
                        const double* D, int64_t m, int64_t K, double* alpha, int64_t lda,

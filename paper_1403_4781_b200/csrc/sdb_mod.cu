@@ -645,11 +645,26 @@ k_mod_apply(int P, int K, int m, const double* __restrict__ Z, const double* __r
 }
 
 // ---- replace_degenerate_atoms (dictionary_update.py:134-176)
+// Twin pairs (|<d_a, d_j>| > 0.999 on the normalised atoms, dictionary_update.py:146-151;
+// the reference forms the coherences with a BLAS product): a FP32 Gram of the
+// FP32-rounded normalised atoms screens the pairs (error ~1e-5, screen at
+// 0.998), and only the screened pairs are decided, by the FP64 dot product of
+// the FP64 normalised rows (the same routine in both kernels below).
+constexpr float TWIN_SCREEN = 0.998f;
+__device__ __forceinline__ bool twin_exact(const double* __restrict__ Dn, int64_t ea, int64_t ej, int m, int lane) {
+    const double* da = Dn + ea * m;
+    const double* dj = Dn + ej * m;
+    double s = 0.0;
+    for (int r = lane; r < m; r += 32) s = fma(da[r], dj[r], s);
+    return fabs(warp_sum(s)) > 0.999;
+}
+
 // (1) warp per (shard, atom): degenerate flag (unused or zero norm) and "row
-// has a twin to its right" (|C_aj| > 0.999, j > a);
+// has a twin to its right" (j > a);
 __global__ void __launch_bounds__(256)
-k_twin_flags(int P, int K, const double* __restrict__ C, const double* __restrict__ D, int m,
-             const int32_t* __restrict__ usage, int8_t* __restrict__ deg, int8_t* __restrict__ tw) {
+k_twin_flags(int P, int K, const float* __restrict__ C32, const double* __restrict__ Dn,
+             const double* __restrict__ D, int m, const int32_t* __restrict__ usage, int8_t* __restrict__ deg,
+             int8_t* __restrict__ tw) {
     const int lane = threadIdx.x & 31;
     const int64_t e = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     if (e >= (int64_t)P * K) return;
@@ -658,10 +673,17 @@ k_twin_flags(int P, int K, const double* __restrict__ C, const double* __restric
     double s = 0.0;
     for (int r = lane; r < m; r += 32) s = fma(d[r], d[r], s);
     s = warp_sum(s);
-    const double* ci = C + e * K;
+    const float* ci = C32 + e * K;
     bool any = false;
-    for (int j = a + 1 + lane; j < K; j += 32) any |= fabs(ci[j]) > 0.999;
-    any = __any_sync(SDB_FULL, any);
+    for (int j0 = a + 1; j0 < K && !any; j0 += 32) {   // warp-uniform
+        const int j = j0 + lane;
+        unsigned mk = __ballot_sync(SDB_FULL, j < K && fabsf(ci[j]) > TWIN_SCREEN);
+        while (mk && !any) {
+            const int jj = j0 + __ffs(mk) - 1;
+            mk &= mk - 1u;
+            any = twin_exact(Dn, e, e - a + jj, m, lane);
+        }
+    }
     if (lane == 0) {
         deg[e] = (usage[e] == 0 || sqrt(s) <= 1e-12) ? 1 : 0;
         tw[e] = any ? 1 : 0;
@@ -670,12 +692,12 @@ k_twin_flags(int P, int K, const double* __restrict__ C, const double* __restric
 
 // (2) one warp per shard: the order-dependent rule (the lower index of a pair
 // is kept unless itself degenerate) over the rows that have twins, ascending;
-// the columns of a row are marked lane-parallel.
+// the columns of a row are screened lane-parallel.
 __global__ void __launch_bounds__(32)
-k_twins(int K, const double* __restrict__ C, const int8_t* __restrict__ tw, int8_t* __restrict__ deg,
-        int32_t* __restrict__ ntarget) {
+k_twins(int K, int m, const float* __restrict__ C32, const double* __restrict__ Dn, const int8_t* __restrict__ tw,
+        int8_t* __restrict__ deg, int32_t* __restrict__ ntarget) {
     const int p = blockIdx.x, lane = threadIdx.x;
-    const double* Cp = C + (int64_t)p * K * K;
+    const float* Cp = C32 + (int64_t)p * K * K;
     int8_t* dg = deg + (int64_t)p * K;
     const int8_t* twp = tw + (int64_t)p * K;
     for (int i0 = 0; i0 < K; i0 += 32) {
@@ -684,9 +706,17 @@ k_twins(int K, const double* __restrict__ C, const int8_t* __restrict__ tw, int8
             const int i = i0 + __ffs(r) - 1;
             __syncwarp();
             if (dg[i]) continue;  // warp-uniform (read after the barrier)
-            const double* ci = Cp + (int64_t)i * K;
-            for (int j = i + 1 + lane; j < K; j += 32)
-                if (fabs(ci[j]) > 0.999) dg[j] = 1;
+            const float* ci = Cp + (int64_t)i * K;
+            for (int j0 = i + 1; j0 < K; j0 += 32) {
+                const int j = j0 + lane;
+                unsigned mk = __ballot_sync(SDB_FULL, j < K && fabsf(ci[j]) > TWIN_SCREEN);
+                while (mk) {
+                    const int jj = j0 + __ffs(mk) - 1;
+                    mk &= mk - 1u;
+                    const bool t = twin_exact(Dn, (int64_t)p * K + i, (int64_t)p * K + jj, m, lane);
+                    if (t && lane == 0) dg[jj] = 1;
+                }
+            }
         }
     }
     __syncwarp();
@@ -697,14 +727,20 @@ k_twins(int K, const double* __restrict__ C, const int8_t* __restrict__ tw, int8
 }
 
 // normalised copy Dn = D / ||D|| (columns with zero norm untouched)
-__global__ void k_normalize_rows(int64_t rows, int m, const double* __restrict__ D, double* __restrict__ Dn) {
+// (Dn32: optional FP32 rounding of the normalised rows, the twin screen's input)
+__global__ void k_normalize_rows(int64_t rows, int m, const double* __restrict__ D, double* __restrict__ Dn,
+                                 float* __restrict__ Dn32 = nullptr) {
     const int lane = threadIdx.x & 31;
     const int64_t a = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     if (a >= rows) return;
     double s = 0.0;
     for (int r = lane; r < m; r += 32) s = fma(D[a * m + r], D[a * m + r], s);
     const double nrm = sqrt(warp_sum(s));
-    for (int r = lane; r < m; r += 32) Dn[a * m + r] = nrm > 0.0 ? D[a * m + r] / nrm : D[a * m + r];
+    for (int r = lane; r < m; r += 32) {
+        const double v = nrm > 0.0 ? D[a * m + r] / nrm : D[a * m + r];
+        Dn[a * m + r] = v;
+        if (Dn32 != nullptr) Dn32[a * m + r] = (float)v;
+    }
 }
 
 // Candidate selection: targets (ascending atom) take data columns in order
@@ -1010,6 +1046,7 @@ int64_t replace_ws_bytes(int P, int64_t N, int m, int K) {
     add(sizeof(double) * std::max<int64_t>(N, 1));  // ||y||^2
     add(sizeof(int8_t) * std::max<int64_t>(N, 1));  // taken
     add(sizeof(int64_t) * (int64_t)P * K);     // picks
+    add(sizeof(float) * (int64_t)P * K * m);   // FP32 normalised copy (twin screen)
     return b + 256;
 }
 
@@ -1020,7 +1057,7 @@ int replace_degenerate(const ReplaceArgs<T>& a, cudaStream_t st) {
     unsigned char* p = (unsigned char*)a.ws;
     auto take = [&](int64_t bytes) { void* r = p; p += (bytes + 255) & ~int64_t(255); return r; };
     double* Dn = (double*)take(sizeof(double) * PK * m);
-    double* C = (double*)take(sizeof(double) * PK * K);
+    float* C32 = (float*)take(sizeof(double) * PK * K);   // FP32 coherence screen (half the slot)
     int8_t* deg = (int8_t*)take(PK);
     int8_t* twin = (int8_t*)take(PK);
     int32_t* ntarget = (int32_t*)take(sizeof(int32_t) * P);
@@ -1028,12 +1065,13 @@ int replace_degenerate(const ReplaceArgs<T>& a, cudaStream_t st) {
     double* ysq = (double*)take(sizeof(double) * std::max<int64_t>(N, 1));
     int8_t* taken = (int8_t*)take(std::max<int64_t>(N, 1));
     int64_t* pick = (int64_t*)take(sizeof(int64_t) * PK);
+    float* Dn32 = (float*)take(sizeof(float) * PK * m);
 
-    k_normalize_rows<<<(unsigned)((PK + 7) / 8), 256, 0, st>>>(PK, m, a.D, Dn);
-    int rc = gram_f64(Dn, P, m, K, C, st);
+    k_normalize_rows<<<(unsigned)((PK + 7) / 8), 256, 0, st>>>(PK, m, a.D, Dn, Dn32);
+    int rc = gram_screen_f32(Dn32, P, m, K, C32, st);
     if (rc) return rc;
-    k_twin_flags<<<(unsigned)((PK + 7) / 8), 256, 0, st>>>(P, K, C, a.D, m, a.usage, deg, twin);
-    k_twins<<<P, 32, 0, st>>>(K, C, twin, deg, ntarget);
+    k_twin_flags<<<(unsigned)((PK + 7) / 8), 256, 0, st>>>(P, K, C32, Dn, a.D, m, a.usage, deg, twin);
+    k_twins<<<P, 32, 0, st>>>(K, m, C32, Dn, twin, deg, ntarget);
     // residuals with the current D and the given codes (always computed; the
     // reference skips them when no atom is degenerate, which changes nothing)
     rc = with_mpl(m, [&](auto c) {

@@ -114,6 +114,10 @@ static int launch_rowdot(const TIn* A, int64_t lda, const int64_t* a_off, int64_
 int gram_f64_f32(const double* D, int P, int64_t m, int64_t K, double* G64, float* G32, cudaStream_t st) {
     return launch_rowdot<double, double>(D, m, nullptr, K, K, D, m, K * m, K, m, G64, K, P, st, true, G32);
 }
+// FP32 Gram of FP32 rows (a screening pass: atom-pair coherences to ~1e-5)
+int gram_screen_f32(const float* D, int P, int64_t m, int64_t K, float* G, cudaStream_t st) {
+    return launch_rowdot<float, float>(D, m, nullptr, K, K, D, m, K * m, K, m, G, K, P, st, true);
+}
 int gram_f64(const double* D, int P, int64_t m, int64_t K, double* G, cudaStream_t st) {
     return launch_rowdot<double, double>(D, m, nullptr, K, K, D, m, K * m, K, m, G, K, P, st, true);
 }
