@@ -136,6 +136,8 @@ k_chunk_offsets(const int64_t* __restrict__ cf, int P, int K, const int32_t* __r
     }
 }
 
+__device__ __forceinline__ void load_row8(const int32_t* __restrict__ p, int (&v)[8]);
+
 // ---- (e) stable placement: order inside a bucket = (chunk, 32-signal group,
 // slot, lane) — a fixed function of the input.
 template <typename T>
@@ -151,29 +153,62 @@ k_place(const int64_t* __restrict__ off, const int64_t* __restrict__ cf, int P, 
     for (int a = lane; a < K; a += 32) pos[a] = chunk_off[c * K + a];
     __syncwarp();
     const ChunkInfo ci = chunk_info(off, cf, P, c, CH);
+    // one (slot t) round of a 32-signal group: lanes with the same atom take
+    // consecutive positions in lane order
+    auto round = [&](int64_t i, int t, bool act, int a) {
+        const unsigned am = __ballot_sync(SDB_FULL, act);
+        unsigned peers = 0;
+        int64_t base = 0;
+        if (act) {
+            peers = __match_any_sync(am, a);
+            base = pos[a];
+        }
+        __syncwarp();
+        if (act) {
+            const int rank = __popc(peers & ((1u << lane) - 1u));
+            const int64_t q = base + rank;
+            bent[q] = (int32_t)(i * cap + t);  // flat code index: signal i, slot t
+            if (rank == 0) pos[a] = base + __popc(peers);
+        }
+        __syncwarp();
+    };
+    const bool row8 = cap == 8 && (reinterpret_cast<uintptr_t>(idx) & 15) == 0;
+    if (row8) {
+        // the whole index row of every signal of the group (and of the next
+        // group) is requested before its eight rounds, instead of one
+        // dependent load in front of every round
+        int nn = 0, an[8];
+        auto fetch = [&](int64_t i, int& n, int (&as)[8]) {
+            n = 0;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) as[t] = 0;
+            if (i < ci.hi) {
+                n = counts[i];
+                load_row8(idx + i * 8, as);
+            }
+        };
+        fetch(ci.lo + lane, nn, an);
+        for (int64_t g = ci.lo; g < ci.hi; g += 32) {
+            const int64_t i = g + lane;
+            const int n = nn;
+            int as[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) as[t] = an[t];
+            fetch(i + 32, nn, an);
+            const int nmax = __reduce_max_sync(SDB_FULL, n);
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+                if (t < nmax) round(i, t, t < n, as[t]);   // warp-uniform
+        }
+        return;
+    }
     for (int64_t g = ci.lo; g < ci.hi; g += 32) {
         const int64_t i = g + lane;
         const int n = (i < ci.hi) ? counts[i] : 0;
         const int nmax = __reduce_max_sync(SDB_FULL, n);
         for (int t = 0; t < nmax; ++t) {
             const bool act = t < n;
-            const unsigned am = __ballot_sync(SDB_FULL, act);
-            int a = 0;
-            unsigned peers = 0;
-            int64_t base = 0;
-            if (act) {
-                a = idx[i * cap + t];
-                peers = __match_any_sync(am, a);
-                base = pos[a];
-            }
-            __syncwarp();
-            if (act) {
-                const int rank = __popc(peers & ((1u << lane) - 1u));
-                const int64_t q = base + rank;
-                bent[q] = (int32_t)(i * cap + t);  // flat code index: signal i, slot t
-                if (rank == 0) pos[a] = base + __popc(peers);
-            }
-            __syncwarp();
+            round(i, t, act, act ? idx[i * cap + t] : 0);
         }
     }
 }
