@@ -418,6 +418,17 @@ k_normal_eq_w(int64_t PK, int K, int m, const TY* __restrict__ Y, int64_t ldy,
                 for (int q = 0; q < MPL; ++q) acc[q] = fma(yv[u][q], vv[u], acc[q]);
         }
         diag += warp_sum(my_val * my_val);
+        // the entry's code values: one request for the row instead of a dependent
+        // load in front of every slot round
+        T vs[8];
+        if constexpr (CAP8 && Y2) {
+            if (lane < nbat) {
+                load_row8(val + (int64_t)my_sig * 8, vs);
+            } else {
+#pragma unroll
+                for (int t = 0; t < 8; ++t) vs[t] = T(0);
+            }
+        }
         const int my_no = my_n > 1 ? my_n : 0;
         const int nmax = (int)__reduce_max_sync(SDB_FULL, (unsigned)my_no);
         auto slot = [&](int b, double c) {
@@ -436,7 +447,8 @@ k_normal_eq_w(int64_t PK, int K, int m, const TY* __restrict__ Y, int64_t ldy,
             for (int t = 0; t < 8; ++t) {
                 if (t < nmax) {                                  // warp-uniform
                     const bool in = t < my_no;
-                    slot(in ? bs[t] : -1, in ? my_val * (double)val[(int64_t)my_sig * 8 + t] : 0.0);
+                    if constexpr (Y2) slot(in ? bs[t] : -1, in ? my_val * (double)vs[t] : 0.0);
+                    else slot(in ? bs[t] : -1, in ? my_val * (double)val[(int64_t)my_sig * 8 + t] : 0.0);
                 }
             }
         } else {
