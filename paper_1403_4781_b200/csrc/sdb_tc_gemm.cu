@@ -93,6 +93,38 @@ __device__ __forceinline__ Item item_of(int64_t it, const int64_t* __restrict__ 
     return r;
 }
 
+// A role's walk over its consecutive items: one search for the first item, then
+// (tile, chunk, shard) advance in place (the search is ~5 dependent loads and a
+// 64-bit division per item otherwise)
+struct ItemWalk {
+    Item I;
+    int64_t nt;   // tiles of the current shard
+    __device__ __forceinline__ ItemWalk(int64_t it, int64_t it_end, const int64_t* __restrict__ tile_start, int P,
+                                        int nchunk) {
+        if (it < it_end) {
+            I = item_of(it, tile_start, P, nchunk);
+            nt = tile_start[I.p + 1] - tile_start[I.p];
+        } else {
+            I.p = 0; I.chunk = 0; I.tile = 0; I.seg = 0;
+            nt = 1;
+        }
+    }
+    // the next item starts another (shard, chunk) segment
+    __device__ __forceinline__ bool seg_ends() const { return I.tile + 1 >= nt; }
+    __device__ __forceinline__ void next(const int64_t* __restrict__ tile_start, int P, int nchunk) {
+        if (++I.tile < nt) return;
+        I.tile = 0;
+        if (++I.chunk >= nchunk) {
+            I.chunk = 0;
+            do {   // empty shards own no items
+                ++I.p;
+                nt = I.p < P ? tile_start[I.p + 1] - tile_start[I.p] : 1;
+            } while (I.p < P && nt == 0);
+        }
+        I.seg = (int64_t)I.p * nchunk + I.chunk;
+    }
+};
+
 // CODE: the epilogue also runs the first greedy step of the error-bounded
 // FP32 OMP (k_omp_fast, sdb_omp.cu) on each signal's TMEM row, with the same
 // arithmetic: argmax |alpha0| (lowest index among equal maxima), stall and
@@ -388,8 +420,9 @@ k_corr_tc2(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUte
         // ---------------- TMA producer
         if (lane == 0) {
             int64_t q = 0, seg_prev = -1, nseg = 0;
-            for (int64_t it = it0; it < it1; ++it) {
-                const Item I = item_of(it, tile_start, P, nchunk);
+            ItemWalk W(it0, it1, tile_start, P, nchunk);
+            for (int64_t it = it0; it < it1; ++it, W.next(tile_start, P, nchunk)) {
+                const Item I = W.I;
                 const int64_t row0 = off[I.p] + I.tile * TM;
                 const int64_t d_row0 = (int64_t)I.p * K + (int64_t)I.chunk * TN;
                 if (RES && I.seg != seg_prev) {
@@ -422,8 +455,9 @@ k_corr_tc2(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUte
         const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TN >> 3) << 17) |
                                ((uint32_t)(TM >> 4) << 24);
         int64_t q = 0, n = 0, seg_prev = -1, nseg = 0;
-        for (int64_t it = it0; it < it1; ++it, ++n) {
-            const Item I = item_of(it, tile_start, P, nchunk);
+        ItemWalk W(it0, it1, tile_start, P, nchunk);
+        for (int64_t it = it0; it < it1; ++it, ++n, W.next(tile_start, P, nchunk)) {
+            const Item I = W.I;
             const int b = (int)(n & 1);
             const int64_t buse = n >> 1;
             if (lane == 0) {
@@ -455,7 +489,7 @@ k_corr_tc2(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUte
                     if (kb == nkb - 1) mma_commit(smem_u32(&bars[B_TFULL + b]));  // accumulator ready
                 }
                 if (RES) {  // resident D no longer needed after this item?
-                    const bool last = (it + 1 >= it1) || item_of(it + 1, tile_start, P, nchunk).seg != I.seg;
+                    const bool last = (it + 1 >= it1) || W.seg_ends();
                     if (last) mma_commit(smem_u32(&bars[B_BFREE]));
                 }
             }
@@ -475,8 +509,9 @@ k_corr_tc2(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUte
         const int c_mid = ((K + 63) / 64) * 32;
         int64_t n = 0;
         int sb = 0;  // staging buffer toggle
-        for (int64_t it = it0; it < it1; ++it, ++n) {
-            const Item I = item_of(it, tile_start, P, nchunk);
+        ItemWalk W(it0, it1, tile_start, P, nchunk);
+        for (int64_t it = it0; it < it1; ++it, ++n, W.next(tile_start, P, nchunk)) {
+            const Item I = W.I;
             const int b = (int)(n & 1);
             // CODE: ||y||^2 of this warp's rows and the shard's G diagonal are
             // fetched before the accumulator is waited for (their latency then
