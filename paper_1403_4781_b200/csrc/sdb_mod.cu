@@ -232,6 +232,8 @@ k_normal_eq(int P, int K, int m, const TY* __restrict__ Y, int64_t ldy, const in
     extern __shared__ double sh_row[];  // 8 warps x K (X X^T row partials), then 8 x 32*MPL (Y X^T)
     double (*part)[MPL * 32] = reinterpret_cast<double (*)[MPL * 32]>(sh_row + 8 * (int64_t)K);
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const bool y2 = MPL == 2 && std::is_same<TY, float>::value && m == 64 && (ldy & 1) == 0 &&
+                    (reinterpret_cast<uintptr_t>(Y) & 7) == 0;
     const int64_t e = blockIdx.x;  // (p, a)
     const int self = (int)(e % K);
     double* row = sh_row + (int64_t)wib * K;
@@ -248,7 +250,29 @@ k_normal_eq(int P, int K, int m, const TY* __restrict__ Y, int64_t ldy, const in
         const int my_sig = my_e / cap;
         const double my_val = lane < nbat ? (double)val[my_e] : 0.0;
         const int my_n = lane < nbat ? counts[my_sig] : 0;
-        // Y X^T
+        // Y X^T (64-value float rows: lane l walks columns 2l, 2l + 1 with one
+        // 8-byte load per entry)
+        if (y2) {
+            if constexpr (MPL == 2 && std::is_same<TY, float>::value) {
+                for (int j = 0; j < nbat; j += 4) {
+                    float2 yv[4];
+                    const bool full = j + 4 <= nbat;   // warp-uniform
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int i = __shfl_sync(SDB_FULL, my_sig, (j + u) & 31);
+                        yv[u] = make_float2(0.f, 0.f);
+                        if (full || j + u < nbat)
+                            yv[u] = __ldg(reinterpret_cast<const float2*>(Y + (int64_t)i * ldy) + lane);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const double v = __shfl_sync(SDB_FULL, my_val, (j + u) & 31);
+                        acc[0] = fma((double)yv[u].x, v, acc[0]);
+                        acc[1] = fma((double)yv[u].y, v, acc[1]);
+                    }
+                }
+            }
+        } else
         for (int j = 0; j < nbat; j += 4) {
             double yv[4][MPL];
             double vv[4];
@@ -273,13 +297,24 @@ k_normal_eq(int P, int K, int m, const TY* __restrict__ Y, int64_t ldy, const in
         diag += warp_sum(my_val * my_val);
         const int my_no = my_n > 1 ? my_n : 0;
         const int nmax = (int)__reduce_max_sync(SDB_FULL, (unsigned)my_no);
+        // slot t + 1's index and value are requested before slot t's rounds
+        int bn = -1;
+        double cn = 0.0;
+        if (0 < my_no) {
+            bn = idx[(int64_t)my_sig * cap];
+            cn = (double)val[(int64_t)my_sig * cap];
+        }
         for (int t = 0; t < nmax; ++t) {
             int b = -1;
             double c = 0.0;
             if (t < my_no) {
-                b = idx[(int64_t)my_sig * cap + t];
-                c = my_val * (double)val[(int64_t)my_sig * cap + t];
+                b = bn;
+                c = my_val * cn;
                 if (b == self) b = -1;  // diagonal: summed above
+            }
+            if (t + 1 < my_no) {
+                bn = idx[(int64_t)my_sig * cap + t + 1];
+                cn = (double)val[(int64_t)my_sig * cap + t + 1];
             }
             const bool act = b >= 0;
             const unsigned peers = __match_any_sync(SDB_FULL, act ? b : K + lane);
@@ -294,7 +329,7 @@ k_normal_eq(int P, int K, int m, const TY* __restrict__ Y, int64_t ldy, const in
     }
     if (lane == 0) row[self] += diag;
 #pragma unroll
-    for (int q = 0; q < MPL; ++q) part[wib][lane + 32 * q] = acc[q];
+    for (int q = 0; q < MPL; ++q) part[wib][y2 ? 2 * lane + q : lane + 32 * q] = acc[q];
     __syncthreads();
     double* outB = B + e * m;
     for (int r = threadIdx.x; r < m; r += 256) {
