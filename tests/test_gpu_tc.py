@@ -38,6 +38,10 @@ def _alpha(Y, Ds, sizes, use_tc):
     (64, 1024, [130, 127, 260]),
     (16, 24, [50, 70]),
     (12, 20, [7]),
+    # several items per CTA, the walks cross shard and chunk boundaries and skip empty shards
+    (64, 512, [9000, 0, 7000, 130, 0, 12000]),
+    (64, 256, [0, 20000, 0, 0, 1, 15000, 0]),
+    (144, 576, [6000, 0, 5000]),
 ])
 def test_tc_correlation_matches_fp64(m, K, sizes):
     rng = np.random.default_rng(m * 1000 + K)
