@@ -484,8 +484,14 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
                             }
                         }
                         win = OT_WIN * rn + 1e-6f * ynorm;
-                        if (act) {
-                            thr = cmax - win;
+                        // a maximum below the window itself (a residual at rounding
+                        // level, e.g. a signal that is one of the dictionary's atoms):
+                        // EVERY atom is within the window, and the OT_CMAX lowest
+                        // candidates -- all that is kept -- are in block 0, so only
+                        // that block is walked instead of all K columns
+                        if (act) thr = cmax - win;
+                        const bool allin = act && thr < 0.f;
+                        if (act && (!allin || sb == 0)) {
                             float v[32];
 #pragma unroll
                             for (int cc = 0; cc < 8; ++cc) {
@@ -503,6 +509,7 @@ k_omp_tc(const __grid_constant__ CUtensorMap tmD, const OtArgs a) {
 #pragma unroll
                         for (int blk = 0; blk < 16; ++blk)
                             if ((blk >> 3) < NCH && blk * 32 < K && bm[blk] >= thr && blk != sb) need |= 1u << blk;
+                        if (allin) need &= 1u;
                         unsigned wneed = __reduce_or_sync(SDB_FULL, need);
 #pragma unroll 1
                         while (wneed) {

@@ -14,7 +14,9 @@ sys.path.insert(0, str(ROOT))
 
 # (P, n, K, s, m, eps)
 SHAPES = [(256, 15625, 512, 8, 64, 0.0), (64, 8192, 512, 4, 64, 0.0), (32, 20000, 256, 5, 64, 0.0),
-          (16, 7000, 200, 4, 36, 0.0), (32, 8000, 256, 8, 64, 0.3)]
+          (16, 7000, 200, 4, 36, 0.0), (32, 8000, 256, 8, 64, 0.3), (64, 15625, 512, 8, 64, 0.0),
+          (16, 9000, 256, 5, 64, 0.0)]
+FIRSTCOLS = {5, 6}
 
 
 def run(out):
@@ -34,6 +36,9 @@ def run(out):
         Y = torch.einsum("ns,nsm->nm", coef, D[shard[:, None], sup])
         Y = (Y + 0.02 * torch.randn(N, m, device=dev, dtype=torch.float64, generator=g)).float().contiguous()
         del sup, coef
+        if k in FIRSTCOLS:   # first-columns initial dictionaries: the first K signals of a shard are its atoms
+            D = Y.double().reshape(P, n, m)[:, :K, :].clone()
+            D /= D.norm(dim=2, keepdim=True)
         off, mx = E.shard_offsets([n] * P)
         DT, G = E.working_dict(D, "fp32"), E.gram(D, "fp32")
         assert E.omp_tc_applies(m, K, s, "fp32")
