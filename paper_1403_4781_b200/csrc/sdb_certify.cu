@@ -20,10 +20,12 @@
 //
 // Layout: LPS lanes per signal (8 for m <= 64 and cap <= 8: four signals per
 // warp; 32 otherwise), lane l holds y[l + LPS v]; the dot products are
-// reduced within the lane group; the small SPD solve is a lane-parallel
-// right-looking Cholesky in shared memory. Reads y (4m bytes), the support's
-// dictionary rows (8 m n bytes, L2-resident per shard) and n(n+1)/2 Gram
-// entries; writes the FP64 code row.
+// reduced within the lane group. The small SPD solve is a lane-parallel
+// right-looking Cholesky (k_certify, group shuffles) or, in the
+// dictionary-resident kernel k_certify_sm, one thread per signal after eight
+// rounds of dot products (refit_solve_own: the same arithmetic, no shuffles).
+// Reads y (4m bytes), the support's dictionary rows (8 m n bytes, shared
+// memory or L2) and n(n+1)/2 Gram entries; writes the FP64 code row.
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
