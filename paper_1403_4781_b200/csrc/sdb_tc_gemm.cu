@@ -154,8 +154,14 @@ struct Step1 {
 // ascending scan gives). Columns past K enter as 0, which is never selected
 // (selection needs |x| > the running maximum >= 0). alpha0 is finite here:
 // rows whose ||y||^2 is not finite are deferred before this is consulted.
-template <bool FULL>
-__device__ __forceinline__ void block_argmax(const uint32_t (&v)[32], int c, int K, float& bx, uint32_t& bk) {
+// SECOND: also the block's runner-up magnitude (certification margin). Every
+// element but the winner loses exactly one comparison of the tree and the
+// second largest loses only to the winner, so the runner-up is the largest
+// loser -- one min and one max per comparison instead of a second pass over
+// the block (a second element equal to the maximum is a loser too).
+template <bool FULL, bool SECOND>
+__device__ __forceinline__ void block_argmax(const uint32_t (&v)[32], int c, int K, float& bx, uint32_t& bk,
+                                             float& bs) {
     float a[32];
     uint32_t k[32];
 #pragma unroll
@@ -163,31 +169,22 @@ __device__ __forceinline__ void block_argmax(const uint32_t (&v)[32], int c, int
         a[t] = (FULL || c + t < K) ? __uint_as_float(v[t]) : 0.0f;
         k[t] = (uint32_t)t;
     }
+    float l0 = 0.0f, l1 = 0.0f;
 #pragma unroll
     for (int w = 1; w < 32; w <<= 1)
 #pragma unroll
         for (int t = 0; t < 32; t += 2 * w) {
             const bool r = fabsf(a[t + w]) > fabsf(a[t]);
+            if (SECOND) {
+                const float lo = fminf(fabsf(a[t + w]), fabsf(a[t]));
+                if ((t / (2 * w)) & 1) l1 = fmaxf(l1, lo); else l0 = fmaxf(l0, lo);
+            }
             a[t] = r ? a[t + w] : a[t];
             k[t] = r ? k[t + w] : k[t];
         }
     bx = a[0];
     bk = k[0] + (uint32_t)c;
-}
-
-// second-largest |x| of one 32-column block given its argmax column bk
-// (certification margin; columns past K are 0)
-template <bool FULL>
-__device__ __forceinline__ float block_second(const uint32_t (&v)[32], int c, int K, uint32_t bk) {
-    float s0 = 0.0f, s1 = 0.0f;
-#pragma unroll
-    for (int t = 0; t < 32; t += 2) {
-        const float a0 = (FULL || c + t < K) && (uint32_t)(c + t) != bk ? fabsf(__uint_as_float(v[t])) : 0.0f;
-        const float a1 = (FULL || c + t + 1 < K) && (uint32_t)(c + t + 1) != bk ? fabsf(__uint_as_float(v[t + 1])) : 0.0f;
-        s0 = fmaxf(s0, a0);
-        s1 = fmaxf(s1, a1);
-    }
-    return fmaxf(s0, s1);
+    bs = fmaxf(l0, l1);
 }
 
 __device__ __forceinline__ void pair_sync(int quad) {
@@ -216,13 +213,15 @@ __device__ __forceinline__ void code_step1(const Step1& s1, uint32_t trow, int64
     uint32_t va[32], vb[32];
     const bool margin = s1.gap != nullptr;
     auto scan = [&](const uint32_t (&v)[32], int c) {
-        float bx;
+        float bx, bs;
         uint32_t bk;
-        if (c + 32 <= K) block_argmax<true>(v, c, K, bx, bk);   // warp-uniform
-        else block_argmax<false>(v, c, K, bx, bk);
-        if (margin) {
-            const float bs = (c + 32 <= K) ? block_second<true>(v, c, K, bk) : block_second<false>(v, c, K, bk);
+        if (margin) {   // warp-uniform
+            if (c + 32 <= K) block_argmax<true, true>(v, c, K, bx, bk, bs);
+            else block_argmax<false, true>(v, c, K, bx, bk, bs);
             sec = fmaxf(fmaxf(sec, bs), fminf(cur, fabsf(bx)));
+        } else {
+            if (c + 32 <= K) block_argmax<true, false>(v, c, K, bx, bk, bs);
+            else block_argmax<false, false>(v, c, K, bx, bk, bs);
         }
         if (fabsf(bx) > cur) { cur = fabsf(bx); cx = bx; key = bk; }
     };
